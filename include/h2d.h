@@ -1,0 +1,215 @@
+/*
+ * h2d.h — C-ABI drop-in boundary of the B200 Lagrange + DirectCF step.
+ *
+ * The reference (`/root/reference/proj`, "hydro2d") exposes its solver as a
+ * C++ value API in proj/include/hydro/ (*.hpp) and has no C-ABI or device path.
+ * This header is the flat boundary a foreign caller (ctypes, cgo, JNI, the
+ * C++ `hydro::` shim in include/hydro/) binds.  Every entry point names the
+ * reference interface it replaces (file:line, relative to proj/).
+ *
+ * Layout contract (identical to the reference `Field<T>`, field.hpp:15-44):
+ *   - cell fields hold (nx + 2*H2D_GHOST) * (ny + 2*H2D_GHOST) doubles,
+ *     row-major in j, contiguous in i, element (i,j) at
+ *     (j + H2D_GHOST) * (nx + 2*H2D_GHOST) + (i + H2D_GHOST);
+ *   - node fields are the same with nx+1 / ny+1;
+ *   - Vec2 fields (normals, velocities) are interleaved {x, y} pairs, exactly
+ *     the bytes of std::vector<hydro::Vec2>.
+ * So `State::m[a].raw().data()` can be passed as-is.
+ *
+ * Three libraries implement this ABI with different symbol prefixes:
+ *   h2d_   libh2d.so            the product (CUDA sm_100a, device resident)
+ *   h2do_  oracle/libh2d_oracle.so  plain-C restatement (test checker only)
+ *   h2dr_  oracle/_ref/libh2d_ref.so reference library itself (test checker)
+ * Only the h2d_ prefix is declared here; the oracle libraries export the same
+ * signatures under their prefix.
+ *
+ * Errors: every call returns 0 on success or an H2D_ERR_* kind; details
+ * (reference exception class, located cell, step, message) are fetched with
+ * h2d_last_error.  Kinds mirror proj/include/hydro/errors.hpp:11-34.
+ */
+#ifndef H2D_H
+#define H2D_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define H2D_ABI_VERSION 1
+#define H2D_MAX_MAT 2 /* reference kMaxMat, state.hpp:13 */
+#define H2D_GHOST 2   /* reference kGhost, field.hpp:11 */
+
+/* BoundaryKind, mesh.hpp:8 */
+enum { H2D_BC_PERIODIC = 0, H2D_BC_WALL = 1 };
+/* EosModel::Kind, eos.hpp:12 */
+enum { H2D_EOS_PERFECT = 0, H2D_EOS_STIFFENED = 1 };
+/* CornerScheme, reconstruct.hpp:7 (same ordinal order) */
+enum {
+    H2D_CORNER_UPWIND = 0,
+    H2D_CORNER_AVGMIN = 1,
+    H2D_CORNER_LINEARXY = 2,
+    H2D_CORNER_LINEARDIAG = 3,
+    H2D_CORNER_MULTID = 4
+};
+/* RemapKind, remap.hpp:9 */
+enum { H2D_REMAP_AD = 0, H2D_REMAP_DIRECT = 1, H2D_REMAP_DIRECTCF = 2 };
+
+/* Error kinds: 0 = ok; 1..6 = the reference exception classes; >= 100 API. */
+enum {
+    H2D_OK = 0,
+    H2D_ERR_SIM = 1,          /* SimError (errors.hpp:11) */
+    H2D_ERR_TANGLED = 2,      /* TangledCellError (errors.hpp:30) */
+    H2D_ERR_UNPHYSICAL = 3,   /* UnphysicalStateError (errors.hpp:31) */
+    H2D_ERR_NEGMASS = 4,      /* NegativeMassError (errors.hpp:32) */
+    H2D_ERR_CFL = 5,          /* CflViolationError (errors.hpp:33) */
+    H2D_ERR_ISOLATED = 6,     /* IsolatedMixedCellError (errors.hpp:34) */
+    H2D_ERR_INVALID = 100,    /* bad argument / unsupported option */
+    H2D_ERR_DEVICE = 101,     /* CUDA runtime failure */
+    H2D_ERR_NOMEM = 102
+};
+
+/* Mesh (mesh.hpp:13-29). */
+typedef struct {
+    int nx, ny;
+    double dx, dy, x0, y0;
+    int bc_x, bc_y; /* H2D_BC_* */
+} h2d_mesh;
+
+/* EosModel (eos.hpp:11-19). */
+typedef struct {
+    int kind; /* H2D_EOS_* */
+    double gamma;
+    double pi;
+} h2d_eos;
+
+/* MaterialSet (state.hpp:29-32) + PseudoViscosityParams (lagrange.hpp:7-10)
+ * + ReconConfig (reconstruct.hpp:9-13): everything fixed for a run. */
+typedef struct {
+    h2d_mesh mesh;
+    int nmat;
+    h2d_eos eos[H2D_MAX_MAT];
+    double pv_a1, pv_a2;
+    int face_order;        /* ReconConfig::face_order */
+    int corner;            /* H2D_CORNER_* */
+    int interface_degrade; /* ReconConfig::interface_degrade */
+} h2d_config;
+
+/* Host view of a reference State (state.hpp:39-63).  Any derived pointer
+ * (vol, m_mix, e_mix, rho_mix, p_mix) may be NULL on upload, in which case
+ * the device recomputes it with sync_derived semantics (state.cpp:120-143). */
+typedef struct {
+    double* m[H2D_MAX_MAT];
+    double* e[H2D_MAX_MAT];
+    double* k[H2D_MAX_MAT];
+    double* vol;
+    double* m_mix;
+    double* e_mix;
+    double* rho_mix;
+    double* p_mix;
+    double* iface_normal; /* cell Vec2, interleaved */
+    double* u;            /* node Vec2, interleaved */
+    int step;
+    double time;
+} h2d_state;
+
+/* Host view of a LagrangeResult (lagrange.hpp:38-45). */
+typedef struct {
+    double* u_half; /* node Vec2 */
+    double* u_lag;  /* node Vec2 */
+    double* e_lag[H2D_MAX_MAT];
+    double* vol_lag;
+    double* q;
+    int floor_count;
+} h2d_lagrange;
+
+/* RemapDiag (remap.hpp:42-46). */
+typedef struct {
+    double max_k_violation;
+    int k_clip_count;
+    int mass_fix_count;
+} h2d_remap_diag;
+
+/* Located exception record (errors.hpp:11-28). `what` is the reference's
+ * formatted what() string of the innermost throw; `in_step` is 1 when the
+ * error was raised inside lagrange_step/remap_step, where run() re-throws it
+ * with " [<case> step <n>]" appended (harness.cpp:404-407). */
+typedef struct {
+    int kind;
+    int i, j, step;
+    int in_step;
+    char what[256];
+} h2d_error;
+
+/* Device-resident run loop (harness.cpp:380-412, non-kinematic branch). */
+typedef struct {
+    int max_steps;    /* 0 = until t_end (compares the state's absolute step) */
+    double t_end;
+    double cfl;
+    int remap_kind;   /* only H2D_REMAP_DIRECTCF is implemented on device */
+    double* dt_log;   /* optional host array receiving each step's dt */
+    int dt_log_cap;
+    /* outputs */
+    int steps_done;
+    int floor_count;  /* sum of LagrangeResult::floor_count */
+    h2d_remap_diag diag;
+} h2d_run_args;
+
+typedef struct h2d_ctx h2d_ctx;
+
+/* Library identity: returns H2D_ABI_VERSION. */
+int h2d_abi_version(void);
+
+/* Mesh + MaterialSet + params (state.hpp:65 make_state's inputs). device<0
+ * selects the current device. Validates like Mesh::Mesh (mesh.hpp:26-29). */
+int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out);
+void h2d_destroy(h2d_ctx* ctx);
+
+/* Replace the context's State (all ghost layers included). */
+int h2d_upload_state(h2d_ctx* ctx, const h2d_state* s);
+/* Read the State back into the reference layout; NULL pointers are skipped. */
+int h2d_download_state(h2d_ctx* ctx, h2d_state* s);
+
+/* Init helpers on the context's State, as init_case calls them
+ * (harness.cpp:286-288): void fill_ghosts(State&) (state.hpp:87,
+ * state.cpp:110-118); void sync_derived(State&, const MaterialSet&)
+ * (state.hpp:91, state.cpp:120-143); void update_interface_normals(State&)
+ * (remap.hpp:64, remap.cpp:1093-1096). */
+int h2d_fill_ghosts(h2d_ctx* ctx);
+int h2d_sync_derived(h2d_ctx* ctx);
+int h2d_update_interface_normals(h2d_ctx* ctx);
+
+/* double cfl_dt(const State&, const MaterialSet&, double cfl)
+ * (harness.hpp:64, harness.cpp:293-313). */
+int h2d_cfl_dt(h2d_ctx* ctx, double cfl, double* dt_out);
+
+/* LagrangeResult lagrange_step(State, MaterialSet, dt, PseudoViscosityParams)
+ * (lagrange.hpp:56-59). The result stays on the device for h2d_remap_step;
+ * `out` (nullable) receives a copy. */
+int h2d_lagrange_step(h2d_ctx* ctx, double dt, h2d_lagrange* out);
+
+/* Install an externally built LagrangeResult (e.g. the imposed-velocity
+ * `kinematic()` of test_remap.cpp:46-54). NULL e_lag/vol_lag/q entries are
+ * zero-filled. */
+int h2d_set_lagrange(h2d_ctx* ctx, const h2d_lagrange* lag);
+
+/* State remap_step(State, MaterialSet, LagrangeResult, dt, RemapKind,
+ * ReconConfig, x_first, remap_velocity, RemapDiag*) (remap.hpp:51-53).
+ * Replaces the device State by the remapped one (step+1, time+dt).
+ * `diag` (nullable) is accumulated like the reference's RemapDiag. */
+int h2d_remap_step(h2d_ctx* ctx, double dt, int remap_kind, int x_first,
+                   int remap_velocity, h2d_remap_diag* diag);
+
+/* RunReport run(...) hot loop without the catalogue/init (harness.cpp:390-412):
+ * cfl_dt -> min(t_end - t) -> lagrange_step -> remap_step -> nan_scan. */
+int h2d_run(h2d_ctx* ctx, h2d_run_args* args);
+
+/* Totals compute_totals(const State&) (state.hpp:100, state.cpp:145-160);
+ * out = {mass, mass_mat0, mass_mat1, momentum.x, momentum.y, internal_energy}. */
+int h2d_totals(h2d_ctx* ctx, double out[6]);
+
+/* Last error recorded on this context (kind H2D_OK if none). */
+int h2d_last_error(h2d_ctx* ctx, h2d_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2D_H */

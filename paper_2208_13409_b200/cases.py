@@ -1,0 +1,266 @@
+"""Initial data for the BASELINE.json configurations.
+
+``paint`` restates the interior painter of ``init_case``
+(proj/src/harness.cpp:165-207 coverage/contains, :226-284 painting) in
+vectorised numpy with the reference's operation order, so a painted state
+followed by ``Solver.init_from`` (fill_ghosts + sync_derived +
+update_interface_normals, harness.cpp:286-288) is bit-identical to the
+reference ``init_case`` (pinned by tests/test_oracle_vs_reference.py).
+
+Two shapes the reference painter lacks are added for configs 4 and 5 (the
+reference has no perturbed circle and no Voronoi region): a
+seeded Fourier-perturbed circle sampled 16x16 per cell like the reference
+circle (harness.cpp:179-189).  Config 5 needs three materials, which the
+reference (kMaxMat = 2, state.hpp:13) and this build do not support; it is
+not offered here (DESIGN.md §"Out of scope").
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from .abi import (BC_WALL, CORNER_LINEARDIAG, EOS_PERFECT, EOS_STIFFENED, Config, HostState, GHOST,
+                  make_config)
+
+K_PURE_TOL = 1e-10  # state.hpp:17
+
+ALL, HALFPLANE_X, RECTANGLE, CIRCLE, PERTURBED_CIRCLE = range(5)
+
+
+@dataclass
+class Region:
+    """hydro::Region (harness.hpp:17-28) plus PERTURBED_CIRCLE (radius(theta))."""
+    shape: int = ALL
+    xsplit: float = 0.0
+    rect: Tuple[float, float, float, float] = (0.0, 0.0, 0.0, 0.0)  # lo.x, lo.y, hi.x, hi.y
+    center: Tuple[float, float] = (0.0, 0.0)
+    radius: float = 0.0
+    mat: int = 0
+    rho: float = 1.0
+    p: float = 1e5
+    u: Tuple[float, float] = (0.0, 0.0)
+    radius_fn: Optional[Callable[[np.ndarray], np.ndarray]] = None  # PERTURBED_CIRCLE only
+
+    def row(self) -> List[float]:
+        """Flat row for the reference probe h2dr_init_regions."""
+        return [self.shape, self.xsplit, *self.rect, *self.center, self.radius, self.mat, self.rho, self.p,
+                *self.u]
+
+
+def energy_from_p(eos, rho, p):
+    """harness.cpp:32-35."""
+    kind, gamma, pi = eos
+    pi = pi if kind == EOS_STIFFENED else 0.0
+    return (p + pi) / ((gamma - 1.0) * rho)
+
+
+def _contains(r: Region, px: np.ndarray, py: np.ndarray) -> np.ndarray:
+    """contains(), harness.cpp:194-207."""
+    if r.shape == ALL:
+        return np.ones(np.broadcast(px, py).shape, bool)
+    if r.shape == HALFPLANE_X:
+        return np.broadcast_to(px < r.xsplit, np.broadcast(px, py).shape)
+    if r.shape == RECTANGLE:
+        return (px >= r.rect[0]) & (px <= r.rect[2]) & (py >= r.rect[1]) & (py <= r.rect[3])
+    ddx, ddy = px - r.center[0], py - r.center[1]
+    if r.shape == CIRCLE:
+        return ddx * ddx + ddy * ddy <= r.radius * r.radius
+    theta = np.arctan2(ddy, ddx)
+    rad = r.radius_fn(theta)
+    return np.sqrt(ddx * ddx + ddy * ddy) <= rad
+
+
+def _ref_max(a, b):
+    return np.where(a < b, b, a)
+
+
+def _ref_min(a, b):
+    return np.where(b < a, b, a)
+
+
+def _coverage(r: Region, lox, loy, hix, hiy, dx, dy, mask) -> np.ndarray:
+    """coverage(), harness.cpp:166-192, evaluated where ``mask`` holds."""
+    out = np.zeros(mask.shape)
+    if r.shape == ALL:
+        out[:] = 1.0
+        return out
+    if r.shape == HALFPLANE_X:
+        v = (r.xsplit - lox) / dx
+        v = np.where(v < 0.0, 0.0, np.where(1.0 < v, 1.0, v))
+        return np.broadcast_to(v, mask.shape).copy()
+    if r.shape == RECTANGLE:
+        ox = _ref_max(0.0, _ref_min(hix, r.rect[2]) - _ref_max(lox, r.rect[0]))
+        oy = _ref_max(0.0, _ref_min(hiy, r.rect[3]) - _ref_max(loy, r.rect[1]))
+        return np.broadcast_to((ox / dx) * (oy / dy), mask.shape).copy()
+    # circles: 16x16 sub-cell samples, only cells whose box meets the disc
+    # bounding box can be covered (all others are exactly 0)
+    reach = r.radius * (1.5 if r.shape == PERTURBED_CIRCLE else 1.0)
+    jj, ii = np.nonzero(mask)
+    lx, ly = np.broadcast_to(lox, mask.shape)[jj, ii], np.broadcast_to(loy, mask.shape)[jj, ii]
+    near = (lx + dx >= r.center[0] - reach) & (lx <= r.center[0] + reach) & \
+           (ly + dy >= r.center[1] - reach) & (ly <= r.center[1] + reach)
+    jj, ii, lx, ly = jj[near], ii[near], lx[near], ly[near]
+    offs = (np.arange(16) + 0.5) / 16.0
+    chunk = 1 << 16
+    for s in range(0, len(jj), chunk):
+        sx = lx[s:s + chunk, None, None] + offs[None, None, :] * dx
+        sy = ly[s:s + chunk, None, None] + offs[None, :, None] * dy
+        inside = _contains(r, sx, sy).sum(axis=(1, 2))
+        out[jj[s:s + chunk], ii[s:s + chunk]] = inside / 256.0
+    return out
+
+
+def paint(cfg: Config, regions: Sequence[Region]) -> HostState:
+    """Interior of init_case (harness.cpp:226-284); ghosts/derived/normals are
+    completed on the solver by ``Solver.init_from``."""
+    m = cfg.mesh
+    nx, ny, dx, dy, x0, y0 = m.nx, m.ny, m.dx, m.dy, m.x0, m.y0
+    nmat = cfg.nmat
+    eos = [(cfg.eos[a].kind, cfg.eos[a].gamma, cfg.eos[a].pi) for a in range(nmat)]
+    cv = dx * dy
+    i = np.arange(nx, dtype=np.float64)[None, :]
+    j = np.arange(ny, dtype=np.float64)[:, None]
+    lox, loy = x0 + i * dx, y0 + j * dy              # node_pos(i, j)
+    hix, hiy = x0 + (i + 1) * dx, y0 + (j + 1) * dy  # node_pos(i+1, j+1)
+    cenx, ceny = x0 + (i + 0.5) * dx, y0 + (j + 0.5) * dy
+    shape = (ny, nx)
+    karr = np.zeros((2,) + shape)
+    marr = np.zeros((2,) + shape)
+    mearr = np.zeros((2,) + shape)
+    for r_idx, reg in enumerate(regions):
+        if r_idx == 0:
+            f = np.ones(shape)
+        else:
+            frac = (nmat == 2) & (karr[reg.mat] < 1.0)
+            f = np.where(_contains(reg, cenx, ceny), 1.0, 0.0)
+            if frac.any():
+                cov = _coverage(reg, lox, loy, hix, hiy, dx, dy, frac)
+                f = np.where(frac, cov, f)
+        upd = f > 0.0
+        e = energy_from_p(eos[reg.mat], reg.rho, reg.p)
+        for a in range(nmat):
+            karr[a] = np.where(upd, karr[a] * (1.0 - f), karr[a])
+            marr[a] = np.where(upd, marr[a] * (1.0 - f), marr[a])
+            mearr[a] = np.where(upd, mearr[a] * (1.0 - f), mearr[a])
+        karr[reg.mat] = np.where(upd, karr[reg.mat] + f, karr[reg.mat])
+        marr[reg.mat] = np.where(upd, marr[reg.mat] + f * reg.rho * cv, marr[reg.mat])
+        mearr[reg.mat] = np.where(upd, mearr[reg.mat] + f * reg.rho * e * cv, mearr[reg.mat])
+    for a in range(nmat):  # snap trace fractions to pure (harness.cpp:260-269)
+        snap = karr[a] < K_PURE_TOL
+        b = 1 - a
+        karr[b] = np.where(snap, karr[b] + karr[a], karr[b])
+        marr[b] = np.where(snap, marr[b] + marr[a], marr[b])
+        mearr[b] = np.where(snap, mearr[b] + mearr[a], mearr[b])
+        karr[a] = np.where(snap, 0.0, karr[a])
+        marr[a] = np.where(snap, 0.0, marr[a])
+        mearr[a] = np.where(snap, 0.0, mearr[a])
+    st = HostState.empty(nx, ny, nmat, cv)
+    g = GHOST
+    for a in range(nmat):
+        st.k[a, g:g + ny, g:g + nx] = karr[a]
+        st.m[a, g:g + ny, g:g + nx] = marr[a]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            st.e[a, g:g + ny, g:g + nx] = np.where(marr[a] > 0.0, mearr[a] / marr[a], 0.0)
+    # node velocities: last region containing the node (harness.cpp:277-284)
+    ni = np.arange(nx + 1, dtype=np.float64)[None, :]
+    nj = np.arange(ny + 1, dtype=np.float64)[:, None]
+    px, py = x0 + ni * dx, y0 + nj * dy
+    ux = np.zeros((ny + 1, nx + 1))
+    uy = np.zeros((ny + 1, nx + 1))
+    for reg in regions:
+        inside = np.broadcast_to(_contains(reg, px, py), ux.shape)
+        ux = np.where(inside, reg.u[0], ux)
+        uy = np.where(inside, reg.u[1], uy)
+    st.u[g:g + ny + 1, g:g + nx + 1, 0] = ux
+    st.u[g:g + ny + 1, g:g + nx + 1, 1] = uy
+    return st
+
+
+@dataclass
+class Case:
+    name: str
+    cfg: Config
+    regions: List[Region]
+    cfl: float
+    steps: int
+    note: str = ""
+
+    @property
+    def cells(self) -> int:
+        return self.cfg.mesh.nx * self.cfg.mesh.ny
+
+    def paint(self) -> HostState:
+        return paint(self.cfg, self.regions)
+
+
+def _mesh_cfg(nx, ny, lx, ly, eos, **kw) -> Config:
+    # CaseSpec::make_mesh divides the extent (harness.cpp:9-11)
+    return make_config(nx, ny, lx / nx, ly / ny, 0.0, 0.0, BC_WALL, BC_WALL, eos=eos,
+                       corner=CORNER_LINEARDIAG, **kw)
+
+
+def riemann2d(n: int = 256) -> Case:
+    """Config 1: gamma 1.4 two-state Riemann problem on the unit square."""
+    air = (EOS_PERFECT, 1.4, 0.0)
+    return Case(f"riemann2d_{n}", _mesh_cfg(n, n, 1.0, 1.0, [air]),
+                [Region(ALL, rho=0.125, p=0.1), Region(HALFPLANE_X, xsplit=0.5, rho=1.0, p=1.0)], 0.5, 100)
+
+
+def sedov(n: int = 1024) -> Case:
+    """Config 2: point blast, E0 = 1 in the 2x2 corner cells (sum m e = 1)."""
+    gamma = 1.4
+    dx = dy = 1.0 / n
+    p0 = (gamma - 1.0) * 1.0 / (4.0 * dx * dy)
+    return Case(f"sedov_{n}", _mesh_cfg(n, n, 1.0, 1.0, [(EOS_PERFECT, gamma, 0.0)]),
+                [Region(ALL, rho=1.0, p=1e-6), Region(RECTANGLE, rect=(0.0, 0.0, 2 * dx, 2 * dy), rho=1.0, p=p0)],
+                0.5, 500)
+
+
+def triple_point(nx: int = 2048, ny: int = 1024) -> Case:
+    """Config 3: two-material three-state interface problem on [0,7]x[0,3]
+    (A: gamma 1.5 = material 0, B: gamma 1.4 = material 1).  Region order is
+    the one in BASELINE.json; the reference aborts after step 819 at full size
+    (SURVEY.md finding 6)."""
+    A, B = (EOS_PERFECT, 1.5, 0.0), (EOS_PERFECT, 1.4, 0.0)
+    return Case(f"triple_point_{nx}x{ny}", _mesh_cfg(nx, ny, 7.0, 3.0, [A, B]),
+                [Region(ALL, mat=0, rho=1.0, p=1.0),
+                 Region(RECTANGLE, rect=(1.0, 0.0, 7.0, 1.5), mat=0, rho=1.0, p=0.1),
+                 Region(RECTANGLE, rect=(1.0, 1.5, 7.0, 3.0), mat=1, rho=0.125, p=0.1)], 0.4, 1000)
+
+
+def bubble_radius_fn(seed: int = 20241001, amp: float = 0.005, r0: float = 0.1):
+    """r(theta) = r0 + delta(theta), delta a seeded sum of Fourier modes 2..32
+    rescaled so max |delta| = amp (measured on a 2^16-point theta grid)."""
+    rng = np.random.Generator(np.random.MT19937(seed))
+    modes = np.arange(2, 33)
+    a = rng.standard_normal(len(modes)) / modes
+    ph = rng.uniform(0.0, 2.0 * np.pi, len(modes))
+    th = np.linspace(0.0, 2.0 * np.pi, 1 << 16, endpoint=False)
+    raw = (a[:, None] * np.cos(modes[:, None] * th[None, :] + ph[:, None])).sum(0)
+    scale = amp / np.abs(raw).max()
+
+    def fn(theta: np.ndarray) -> np.ndarray:
+        d = np.zeros(np.shape(theta))
+        for ak, mk, pk in zip(a, modes, ph):
+            d = d + ak * np.cos(mk * theta + pk)
+        return r0 + scale * d
+
+    return fn
+
+
+def shock_bubble(n: int = 8192, seed: int = 20241001) -> Case:
+    """Config 4: shock-bubble, A gamma 1.4 (material 0), B gamma 1.67
+    (material 1) bubble of radius 0.1 +- 0.005 at (0.5, 0.5), post-shock slab
+    x < 0.3; fractions by 16x16 sub-cell sampling. CFL 0.3 (the reference
+    default, harness.hpp:39; unstated in BASELINE.json), walls."""
+    A, B = (EOS_PERFECT, 1.4, 0.0), (EOS_PERFECT, 1.67, 0.0)
+    return Case(f"shock_bubble_{n}", _mesh_cfg(n, n, 1.0, 1.0, [A, B]),
+                [Region(ALL, mat=0, rho=1.0, p=1.0),
+                 Region(HALFPLANE_X, xsplit=0.3, mat=0, rho=1.376, p=1.5, u=(0.394, 0.0)),
+                 Region(PERTURBED_CIRCLE, center=(0.5, 0.5), radius=0.1, mat=1, rho=0.138, p=1.0,
+                        radius_fn=bubble_radius_fn(seed))], 0.3, 200)
+
+
+CASES = {"c1": riemann2d, "c2": sedov, "c3": triple_point, "c4": shock_bubble}
