@@ -1,0 +1,740 @@
+// h2d_capi.cu — the C-ABI of include/h2d.h over the sm_100a kernels.
+//
+// A context owns one device, one stream, a double-buffered device State (the
+// buffer pair alternates every committed step, so a failed step leaves the
+// previous State intact, matching the reference's value semantics), the
+// LagrangeResult and all remap scratch, laid out as (P x R) fp64 planes with
+// two ghost layers.  There is no host compute on the step path; a missing
+// device is an error (H2D_ERR_DEVICE), never a fallback.
+#include "../../include/h2d.h"
+#include "h2d_launch.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace h2d;
+
+namespace {
+
+struct StateBufs {
+    double *m[2], *e[2], *k[2], *vol, *m_mix, *e_mix, *rho_mix, *p_mix, *nrx, *nry, *ux, *uy;
+};
+
+}  // namespace
+
+struct h2d_ctx {
+    h2d_config cfg{};
+    int device = 0;
+    cudaStream_t st = nullptr;
+    int nx = 0, ny = 0, nmat = 1, P = 0, R = 0;
+    size_t fsz = 0;  // doubles per plane
+    char* arena = nullptr;
+    size_t arena_bytes = 0, arena_used = 0;
+    StateBufs sb[2]{};
+    Dev base{};
+    Ctl* ctl = nullptr;   // device
+    Ctl* hctl = nullptr;  // pinned host mirror
+    int cur = 0;
+    bool have_lag = false;
+    h2d_error err{};
+    double* stage = nullptr;     // device staging for AoS Vec2 fields
+    double* dt_log = nullptr;    // device dt log of h2d_run
+    int dt_log_cap = 0;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    bool graph_ready = false;
+};
+
+namespace {
+
+void set_err(h2d_ctx* c, int kind, const char* what, int i = -1, int j = -1, int step = -1, int in_step = 0) {
+    c->err.kind = kind;
+    c->err.i = i;
+    c->err.j = j;
+    c->err.step = step;
+    c->err.in_step = in_step;
+    std::snprintf(c->err.what, sizeof c->err.what, "%s", what);
+}
+
+int cuda_fail(h2d_ctx* c, cudaError_t e, const char* where) {
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "CUDA error in %s: %s", where, cudaGetErrorString(e));
+    if (c) set_err(c, H2D_ERR_DEVICE, buf);
+    return H2D_ERR_DEVICE;
+}
+
+#define CK(call)                                               \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return cuda_fail(c, e_, #call); \
+    } while (0)
+
+double* carve(h2d_ctx* c, size_t count_doubles) {
+    const size_t bytes = (count_doubles * sizeof(double) + 255) & ~size_t(255);
+    double* p = reinterpret_cast<double*>(c->arena + c->arena_used);
+    c->arena_used += bytes;
+    return p;
+}
+// pointer to element (-G, -G) of a plane: the plane base
+inline double* plane(h2d_ctx* c) { return carve(c, c->fsz); }
+
+Dev make_dev(h2d_ctx* c, int parity, int remap_velocity) {
+    Dev d = c->base;
+    const StateBufs& s = c->sb[parity];
+    const StateBufs& n = c->sb[1 - parity];
+    for (int a = 0; a < 2; ++a) {
+        d.m[a] = s.m[a];
+        d.e[a] = s.e[a];
+        d.k[a] = s.k[a];
+        d.nm[a] = n.m[a];
+        d.ne[a] = n.e[a];
+        d.nk[a] = n.k[a];
+    }
+    d.vol = s.vol;
+    d.m_mix = s.m_mix;
+    d.e_mix = s.e_mix;
+    d.rho_mix = s.rho_mix;
+    d.p_mix = s.p_mix;
+    d.nrx = s.nrx;
+    d.nry = s.nry;
+    d.ux = s.ux;
+    d.uy = s.uy;
+    d.nvol = n.vol;
+    d.nm_mix = n.m_mix;
+    d.ne_mix = n.e_mix;
+    d.nrho_mix = n.rho_mix;
+    d.np_mix = n.p_mix;
+    d.nnrx = n.nrx;
+    d.nnry = n.nry;
+    d.nux = n.ux;
+    d.nuy = n.uy;
+    d.remap_velocity = remap_velocity;
+    return d;
+}
+
+int ctl_pull(h2d_ctx* c) {
+    CK(cudaMemcpyAsync(c->hctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+int ctl_push(h2d_ctx* c) {
+    CK(cudaMemcpyAsync(c->ctl, c->hctl, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+// Reset the control block before an API call (errors of earlier calls do not
+// block later ones, like independent reference calls).
+int ctl_reset(h2d_ctx* c) {
+    if (int rc = ctl_pull(c)) return rc;
+    Ctl& h = *c->hctl;
+    h.err_key = kNoErr;
+    h.done = 0;
+    h.cur = c->cur;
+    h.step_floor = h.step_clip = h.step_fix = 0;
+    h.wmax_bits = h.kviol_bits = 0;
+    return ctl_push(c);
+}
+
+// Rebuild the reference exception of the first failing phase (errors.hpp).
+int decode_error(h2d_ctx* c, bool in_run) {
+    const uint64_t key = c->hctl->err_key;
+    if (key == kNoErr) return 0;
+    const int ph = (int)(key >> 58);
+    const int outer = (int)((key >> 33) & 0x1FFFFFF) - 16;
+    const int inner = (int)((key >> 8) & 0x1FFFFFF) - 16;
+    const int sub = (int)(key & 0xFF);
+    int kind = H2D_ERR_SIM;
+    const char* msg = "";
+    bool located = false, with_step = false;
+    int in_step = 1;
+    switch (ph) {
+    case PH_CFL_UNPHYS: kind = H2D_ERR_UNPHYSICAL; msg = "unphysical state: gamma*(P+pi)/rho < 0"; in_step = 0; break;
+    case PH_CFL_WAVE: kind = H2D_ERR_SIM; msg = "non-finite wave speed"; in_step = 0; break;
+    case PH_Q_UNPHYS: kind = H2D_ERR_UNPHYSICAL; msg = "unphysical state: gamma*(P+pi)/rho < 0"; break;
+    case PH_PRED_TANGLED:
+    case PH_CORR_TANGLED: kind = H2D_ERR_TANGLED; msg = "tangled cell"; located = true; break;
+    case PH_CFL_XFACE: kind = H2D_ERR_CFL; msg = "CFL violation at X-face"; located = true; break;
+    case PH_CFL_YFACE: kind = H2D_ERR_CFL; msg = "CFL violation at Y-face"; located = true; break;
+    case PH_CFL_CORNER: kind = H2D_ERR_CFL; msg = "CFL violation at corner"; located = true; break;
+    case PH_COLLAPSED: kind = H2D_ERR_CFL; msg = "collapsed Lagrangian cell"; located = true; break;
+    case PH_GRAD_XFACE:
+    case PH_GRAD_YFACE:
+    case PH_GRAD_CORNER:
+    case PH_GRAD_DUALX:
+    case PH_GRAD_DUALY:
+    case PH_GRAD_DUALC: kind = H2D_ERR_SIM; msg = "non-increasing centroid coordinates"; break;
+    case PH_NEGMASS:
+        kind = H2D_ERR_NEGMASS;
+        msg = sub == 2 ? "non-positive cell mass" : "negative mass";
+        located = true;
+        break;
+    case PH_NODAL_MASS: kind = H2D_ERR_NEGMASS; msg = "non-positive nodal mass"; located = true; break;
+    case PH_NAN_CELL: kind = H2D_ERR_SIM; msg = "non-finite cell state"; located = true; with_step = true; in_step = 0; break;
+    case PH_NAN_NODE: kind = H2D_ERR_SIM; msg = "non-finite velocity"; located = true; with_step = true; in_step = 0; break;
+    default: kind = H2D_ERR_DEVICE; msg = "unknown device error"; break;
+    }
+    std::string w = msg;
+    const int i = located ? inner : -1, j = located ? outer : -1;
+    if (located) w += " at cell (" + std::to_string(i) + "," + std::to_string(j) + ")";
+    const int step = c->hctl->step;
+    if (with_step) w += " step " + std::to_string(step);
+    if (!in_run) in_step = 0;
+    set_err(c, kind, w.c_str(), i, j, (with_step || in_step) ? step : -1, in_step);
+    return kind;
+}
+
+int check_launch(h2d_ctx* c) {
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// host <-> device copies in the reference layout (pitch n1 + 4)
+int put_plane(h2d_ctx* c, double* dst, const double* src, int n1, int n2) {
+    if (!src) return 0;
+    const size_t w = (size_t)(n1 + 2 * G) * sizeof(double);
+    CK(cudaMemcpy2DAsync(dst, (size_t)c->P * sizeof(double), src, w, w, (size_t)(n2 + 2 * G),
+                         cudaMemcpyHostToDevice, c->st));
+    return 0;
+}
+int get_plane(h2d_ctx* c, double* dst, const double* src, int n1, int n2) {
+    if (!dst) return 0;
+    const size_t w = (size_t)(n1 + 2 * G) * sizeof(double);
+    CK(cudaMemcpy2DAsync(dst, w, src, (size_t)c->P * sizeof(double), w, (size_t)(n2 + 2 * G),
+                         cudaMemcpyDeviceToHost, c->st));
+    return 0;
+}
+int put_vec(h2d_ctx* c, double* x, double* y, const double* src, int n1, int n2) {
+    if (!src) return 0;
+    const int W = n1 + 2 * G, H = n2 + 2 * G;
+    CK(cudaMemcpyAsync(c->stage, src, (size_t)W * H * 2 * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    launch_deinterleave(c->stage, x, y, W, H, c->P, c->st);
+    return check_launch(c);
+}
+int get_vec(h2d_ctx* c, double* dst, const double* x, const double* y, int n1, int n2) {
+    if (!dst) return 0;
+    const int W = n1 + 2 * G, H = n2 + 2 * G;
+    launch_interleave(c->stage, x, y, W, H, c->P, c->st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(dst, c->stage, (size_t)W * H * 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    return 0;
+}
+int zero_plane(h2d_ctx* c, double* p) {
+    CK(cudaMemsetAsync(p, 0, c->fsz * sizeof(double), c->st));
+    return 0;
+}
+
+__global__ void k_fill(double* p, double v, size_t n) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (t < n) p[t] = v;
+}
+int fill_plane(h2d_ctx* c, double* p, double v) {
+    k_fill<<<(unsigned)((c->fsz + 255) / 256), 256, 0, c->st>>>(p, v, c->fsz);
+    return check_launch(c);
+}
+
+int fill_ghosts_cur(h2d_ctx* c, int parity) {
+    const Dev d = make_dev(c, parity, 1);
+    FieldList fl{};
+    fl.respect_halt = 0;
+    int q = 0;
+    for (int a = 0; a < c->nmat; ++a) {
+        fl.f[q++] = c->sb[parity].m[a];
+        fl.f[q++] = c->sb[parity].e[a];
+        fl.f[q++] = c->sb[parity].k[a];
+    }
+    fl.f[q++] = c->sb[parity].nrx;
+    fl.f[q++] = c->sb[parity].nry;
+    fl.n = q;
+    launch_ghost_cells(d, fl, c->st);
+    FieldList fu{};
+    fu.respect_halt = 0;
+    fu.n = 2;
+    fu.f[0] = c->sb[parity].ux;
+    fu.f[1] = c->sb[parity].uy;
+    launch_ghost_nodes(d, fu, c->st);
+    return check_launch(c);
+}
+
+// One run-loop step (harness.cpp:390-412) for the state in `parity`.
+void enqueue_step(h2d_ctx* c, int parity) {
+    const Dev d = make_dev(c, parity, 1);
+    launch_begin(c->ctl, 0, 0.0, c->st);
+    launch_cfl(d, 1, c->st);
+    launch_lagrange(d, 0, c->st);
+    cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->ny, c->st);
+    launch_remap(d, c->st);
+    launch_commit(c->ctl, 1, c->st);
+    launch_nan_finish(d, c->st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int h2d_abi_version(void) { return H2D_ABI_VERSION; }
+
+int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
+    *out = nullptr;
+    const h2d_mesh& m = cfg->mesh;
+    if (m.nx < 3 || m.ny < 3) return H2D_ERR_SIM;        // Mesh::Mesh, mesh.hpp:27
+    if (m.dx <= 0.0 || m.dy <= 0.0) return H2D_ERR_SIM;  // mesh.hpp:28
+    if (cfg->nmat < 1 || cfg->nmat > H2D_MAX_MAT) return H2D_ERR_INVALID;
+    if (cfg->corner != H2D_CORNER_UPWIND && cfg->corner != H2D_CORNER_LINEARDIAG) return H2D_ERR_INVALID;
+    h2d_ctx* c = new h2d_ctx();
+    c->cfg = *cfg;
+    auto fail = [&](int rc) {
+        h2d_destroy(c);
+        return rc;
+    };
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(H2D_ERR_DEVICE);
+    if (device < 0) cudaGetDevice(&device);
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) return fail(H2D_ERR_DEVICE);
+    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return fail(H2D_ERR_DEVICE);
+    c->nx = m.nx;
+    c->ny = m.ny;
+    c->nmat = cfg->nmat;
+    c->P = ((m.nx + 1 + 2 * G) + 31) / 32 * 32;
+    c->R = m.ny + 1 + 2 * G;
+    c->fsz = (size_t)c->P * (size_t)c->R;
+    const int nm = c->nmat;
+    // plane count: 2 x State (6 + 3 nm) + Lagrange (7 + 2 nm) + remap scratch
+    const size_t planes = 2 * (9 + 3 * nm) + (7 + 2 * nm) + (25 + 15 * nm) + 8;
+    const size_t bytes_planes = planes * ((c->fsz * sizeof(double) + 255) & ~size_t(255));
+    const size_t bytes_small = 8 * ((c->fsz + 255) & ~size_t(255)) + ((size_t)c->ny * 4 + 256);
+    c->arena_bytes = bytes_planes + bytes_small + 4096;
+    if (cudaMalloc(&c->arena, c->arena_bytes) != cudaSuccess) return fail(H2D_ERR_NOMEM);
+    cudaMemsetAsync(c->arena, 0, c->arena_bytes, c->st);
+    for (int p = 0; p < 2; ++p) {
+        StateBufs& s = c->sb[p];
+        std::memset(&s, 0, sizeof s);
+        for (int a = 0; a < nm; ++a) {
+            s.m[a] = plane(c);
+            s.e[a] = plane(c);
+            s.k[a] = plane(c);
+        }
+        s.vol = plane(c);
+        s.m_mix = plane(c);
+        s.e_mix = plane(c);
+        s.rho_mix = plane(c);
+        s.p_mix = plane(c);
+        s.nrx = plane(c);
+        s.nry = plane(c);
+        s.ux = plane(c);
+        s.uy = plane(c);
+    }
+    Dev& d = c->base;
+    std::memset(&d, 0, sizeof d);
+    d.nx = m.nx;
+    d.ny = m.ny;
+    d.P = c->P;
+    d.nmat = nm;
+    d.per_x = m.bc_x == H2D_BC_PERIODIC;
+    d.per_y = m.bc_y == H2D_BC_PERIODIC;
+    d.dx = m.dx;
+    d.dy = m.dy;
+    d.x0 = m.x0;
+    d.y0 = m.y0;
+    d.cv = m.dx * m.dy;
+    d.L = std::sqrt(m.dx * m.dy);  // Mesh::char_length, mesh.hpp:39
+    for (int a = 0; a < nm; ++a) {
+        d.stiff[a] = cfg->eos[a].kind == H2D_EOS_STIFFENED;
+        d.gamma[a] = cfg->eos[a].gamma;
+        d.pi[a] = cfg->eos[a].pi;
+    }
+    d.a1 = cfg->pv_a1;
+    d.a2 = cfg->pv_a2;
+    d.face_order = cfg->face_order;
+    d.corner_diag = cfg->corner == H2D_CORNER_LINEARDIAG;
+    d.degrade = cfg->interface_degrade != 0;
+    d.remap_velocity = 1;
+    d.q = plane(c);
+    d.pmh = plane(c);
+    d.uhx = plane(c);
+    d.uhy = plane(c);
+    d.ulx = plane(c);
+    d.uly = plane(c);
+    d.vol_lag = plane(c);
+    for (int a = 0; a < nm; ++a) {
+        d.ph[a] = plane(c);
+        d.el[a] = plane(c);
+        d.me[a] = plane(c);
+        d.rho[a] = plane(c);
+        d.fxm[a] = plane(c);
+        d.fxme[a] = plane(c);
+        d.fxva[a] = plane(c);
+        d.fym[a] = plane(c);
+        d.fyme[a] = plane(c);
+        d.fyva[a] = plane(c);
+        d.fcm[a] = plane(c);
+        d.fcme[a] = plane(c);
+        d.fcva[a] = plane(c);
+        d.slm[a] = plane(c);
+        d.slme[a] = plane(c);
+    }
+    d.mcell = plane(c);
+    d.mcell_lag = plane(c);
+    d.fdx = plane(c);
+    d.fdy = plane(c);
+    d.xlcx = plane(c);
+    d.xlcy = plane(c);
+    d.wlx = plane(c);
+    d.wly = plane(c);
+    d.fx_dv = plane(c);
+    d.fx_lo = plane(c);
+    d.fx_hi = plane(c);
+    d.fy_dv = plane(c);
+    d.fy_lo = plane(c);
+    d.fy_hi = plane(c);
+    d.cf_dv = plane(c);
+    d.vlag = plane(c);
+    d.xl2x = plane(c);
+    d.xl2y = plane(c);
+    d.ifd = plane(c);
+    d.dmx = plane(c);
+    d.dmy = plane(c);
+    d.dmc = plane(c);
+    d.dfx_x = plane(c);
+    d.dfx_y = plane(c);
+    d.dfy_x = plane(c);
+    d.dfy_y = plane(c);
+    d.dc_x[0] = plane(c);
+    d.dc_y[0] = plane(c);
+    d.dc_x[1] = plane(c);
+    d.dc_y[1] = plane(c);
+    c->stage = plane(c);  // >= (nx+5)(ny+5)*2? P*R >= (nx+5)(ny+5); staging needs 2x
+    (void)carve(c, c->fsz);
+    auto bytes_plane = [&]() {
+        char* p = c->arena + c->arena_used;
+        c->arena_used += (c->fsz + 255) & ~size_t(255);
+        return reinterpret_cast<uint8_t*>(p);
+    };
+    d.cf_sx = reinterpret_cast<int8_t*>(bytes_plane());
+    d.cf_sy = reinterpret_cast<int8_t*>(bytes_plane());
+    d.sliver = bytes_plane();
+    for (int q = 0; q < 4; ++q) d.dflag[q] = bytes_plane();
+    (void)bytes_plane();
+    d.row_slivers = reinterpret_cast<int*>(c->arena + c->arena_used);
+    c->arena_used += ((size_t)c->ny * 4 + 255) & ~size_t(255);
+    if (c->arena_used > c->arena_bytes) return fail(H2D_ERR_NOMEM);
+    if (cudaMalloc(&c->ctl, sizeof(Ctl)) != cudaSuccess) return fail(H2D_ERR_NOMEM);
+    if (cudaMallocHost(&c->hctl, sizeof(Ctl)) != cudaSuccess) return fail(H2D_ERR_NOMEM);
+    std::memset(c->hctl, 0, sizeof(Ctl));
+    c->hctl->err_key = kNoErr;
+    d.ctl = c->ctl;
+    if (ctl_push(c)) return fail(H2D_ERR_DEVICE);
+    // make_state defaults (state.cpp:5-23): k0 = 1, normals (1, 0), vol = dx*dy
+    for (int p = 0; p < 2; ++p) {
+        if (fill_plane(c, c->sb[p].k[0], 1.0) || fill_plane(c, c->sb[p].nrx, 1.0) ||
+            fill_plane(c, c->sb[p].vol, d.cv))
+            return fail(H2D_ERR_DEVICE);
+    }
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(H2D_ERR_DEVICE);
+    *out = c;
+    return 0;
+}
+
+void h2d_destroy(h2d_ctx* c) {
+    if (!c) return;
+    if (c->device >= 0) cudaSetDevice(c->device);
+    for (auto& g : c->graph)
+        if (g) cudaGraphExecDestroy(g);
+    if (c->st) cudaStreamSynchronize(c->st);
+    if (c->arena) cudaFree(c->arena);
+    if (c->ctl) cudaFree(c->ctl);
+    if (c->hctl) cudaFreeHost(c->hctl);
+    if (c->dt_log) cudaFree(c->dt_log);
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+int h2d_upload_state(h2d_ctx* c, const h2d_state* v) {
+    cudaSetDevice(c->device);
+    const int nx = c->nx, ny = c->ny;
+    StateBufs& s = c->sb[c->cur];
+    for (int a = 0; a < c->nmat; ++a) {
+        if (int rc = put_plane(c, s.m[a], v->m[a], nx, ny)) return rc;
+        if (int rc = put_plane(c, s.e[a], v->e[a], nx, ny)) return rc;
+        if (int rc = put_plane(c, s.k[a], v->k[a], nx, ny)) return rc;
+    }
+    if (int rc = put_vec(c, s.nrx, s.nry, v->iface_normal, nx, ny)) return rc;
+    if (int rc = put_vec(c, s.ux, s.uy, v->u, nx + 1, ny + 1)) return rc;
+    const bool derived = v->vol && v->m_mix && v->e_mix && v->rho_mix && v->p_mix;
+    if (derived) {
+        if (int rc = put_plane(c, s.vol, v->vol, nx, ny)) return rc;
+        if (int rc = put_plane(c, s.m_mix, v->m_mix, nx, ny)) return rc;
+        if (int rc = put_plane(c, s.e_mix, v->e_mix, nx, ny)) return rc;
+        if (int rc = put_plane(c, s.rho_mix, v->rho_mix, nx, ny)) return rc;
+        if (int rc = put_plane(c, s.p_mix, v->p_mix, nx, ny)) return rc;
+    }
+    if (int rc = ctl_pull(c)) return rc;
+    c->hctl->step = v->step;
+    c->hctl->time = v->time;
+    if (int rc = ctl_push(c)) return rc;
+    if (!derived) return h2d_sync_derived(c);
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+int h2d_download_state(h2d_ctx* c, h2d_state* v) {
+    cudaSetDevice(c->device);
+    const int nx = c->nx, ny = c->ny;
+    const StateBufs& s = c->sb[c->cur];
+    for (int a = 0; a < c->nmat; ++a) {
+        if (int rc = get_plane(c, v->m[a], s.m[a], nx, ny)) return rc;
+        if (int rc = get_plane(c, v->e[a], s.e[a], nx, ny)) return rc;
+        if (int rc = get_plane(c, v->k[a], s.k[a], nx, ny)) return rc;
+    }
+    if (int rc = get_plane(c, v->vol, s.vol, nx, ny)) return rc;
+    if (int rc = get_plane(c, v->m_mix, s.m_mix, nx, ny)) return rc;
+    if (int rc = get_plane(c, v->e_mix, s.e_mix, nx, ny)) return rc;
+    if (int rc = get_plane(c, v->rho_mix, s.rho_mix, nx, ny)) return rc;
+    if (int rc = get_plane(c, v->p_mix, s.p_mix, nx, ny)) return rc;
+    if (v->iface_normal) {
+        if (int rc = get_vec(c, v->iface_normal, s.nrx, s.nry, nx, ny)) return rc;
+        CK(cudaStreamSynchronize(c->st));  // staging buffer reuse
+    }
+    if (int rc = get_vec(c, v->u, s.ux, s.uy, nx + 1, ny + 1)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    v->step = c->hctl->step;
+    v->time = c->hctl->time;
+    return 0;
+}
+
+int h2d_fill_ghosts(h2d_ctx* c) {
+    cudaSetDevice(c->device);
+    if (int rc = fill_ghosts_cur(c, c->cur)) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+int h2d_sync_derived(h2d_ctx* c) {
+    cudaSetDevice(c->device);
+    launch_sync(make_dev(c, c->cur, 1), 0, 0, c->st);
+    if (int rc = check_launch(c)) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+int h2d_update_interface_normals(h2d_ctx* c) {
+    cudaSetDevice(c->device);
+    if (c->nmat != 2) return 0;
+    const Dev d = make_dev(c, c->cur, 1);
+    launch_normals_api(d, c->st);
+    FieldList fl{};
+    fl.respect_halt = 0;
+    fl.n = 2;
+    fl.f[0] = c->sb[c->cur].nrx;
+    fl.f[1] = c->sb[c->cur].nry;
+    launch_ghost_cells(d, fl, c->st);
+    if (int rc = check_launch(c)) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+int h2d_cfl_dt(h2d_ctx* c, double cfl, double* dt) {
+    cudaSetDevice(c->device);
+    if (int rc = ctl_reset(c)) return rc;
+    c->hctl->cfl = cfl;
+    if (int rc = ctl_push(c)) return rc;
+    const Dev d = make_dev(c, c->cur, 1);
+    launch_begin(c->ctl, 2, 0.0, c->st);
+    launch_cfl(d, 0, c->st);
+    if (int rc = check_launch(c)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    if (int rc = decode_error(c, false)) return rc;
+    *dt = c->hctl->dt;
+    return 0;
+}
+
+int h2d_lagrange_step(h2d_ctx* c, double dt, h2d_lagrange* out) {
+    cudaSetDevice(c->device);
+    c->have_lag = false;
+    if (int rc = ctl_reset(c)) return rc;
+    const Dev d = make_dev(c, c->cur, 1);
+    if (int rc = zero_plane(c, d.vol_lag)) return rc;
+    launch_begin(c->ctl, 1, dt, c->st);
+    launch_lagrange(d, 1, c->st);
+    if (int rc = check_launch(c)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    if (int rc = decode_error(c, false)) return rc;
+    c->have_lag = true;
+    if (out) {
+        const int nx = c->nx, ny = c->ny;
+        if (int rc = get_vec(c, out->u_half, d.uhx, d.uhy, nx + 1, ny + 1)) return rc;
+        CK(cudaStreamSynchronize(c->st));
+        if (int rc = get_vec(c, out->u_lag, d.ulx, d.uly, nx + 1, ny + 1)) return rc;
+        for (int a = 0; a < c->nmat; ++a)
+            if (int rc = get_plane(c, out->e_lag[a], d.el[a], nx, ny)) return rc;
+        if (int rc = get_plane(c, out->vol_lag, d.vol_lag, nx, ny)) return rc;
+        if (int rc = get_plane(c, out->q, d.q, nx, ny)) return rc;
+        CK(cudaStreamSynchronize(c->st));
+        out->floor_count = c->hctl->step_floor;
+    }
+    return 0;
+}
+
+int h2d_set_lagrange(h2d_ctx* c, const h2d_lagrange* in) {
+    cudaSetDevice(c->device);
+    const int nx = c->nx, ny = c->ny;
+    const Dev& d = c->base;
+    double* planes[] = {d.uhx, d.uhy, d.ulx, d.uly, d.vol_lag, d.q, d.el[0], d.el[1]};
+    for (double* p : planes)
+        if (p)
+            if (int rc = zero_plane(c, p)) return rc;
+    if (int rc = put_vec(c, d.uhx, d.uhy, in->u_half, nx + 1, ny + 1)) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    if (int rc = put_vec(c, d.ulx, d.uly, in->u_lag, nx + 1, ny + 1)) return rc;
+    for (int a = 0; a < c->nmat; ++a)
+        if (int rc = put_plane(c, d.el[a], in->e_lag[a], nx, ny)) return rc;
+    if (int rc = put_plane(c, d.vol_lag, in->vol_lag, nx, ny)) return rc;
+    if (int rc = put_plane(c, d.q, in->q, nx, ny)) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    c->have_lag = true;
+    return 0;
+}
+
+int h2d_remap_step(h2d_ctx* c, double dt, int kind, int /*x_first*/, int remap_velocity, h2d_remap_diag* diag) {
+    cudaSetDevice(c->device);
+    if (kind != H2D_REMAP_DIRECTCF) {
+        set_err(c, H2D_ERR_INVALID, "only the DirectCF remap is implemented on the device");
+        return H2D_ERR_INVALID;
+    }
+    if (!c->have_lag) {
+        set_err(c, H2D_ERR_INVALID, "remap_step without a LagrangeResult");
+        return H2D_ERR_INVALID;
+    }
+    if (int rc = ctl_reset(c)) return rc;
+    const Dev d = make_dev(c, c->cur, remap_velocity != 0);
+    launch_begin(c->ctl, 1, dt, c->st);
+    CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->ny, c->st));
+    launch_remap(d, c->st);
+    launch_commit(c->ctl, 1, c->st);
+    if (int rc = check_launch(c)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    if (int rc = decode_error(c, false)) return rc;
+    c->cur = c->hctl->cur;
+    if (diag) {
+        const double v = __builtin_bit_cast(double, (unsigned long long)c->hctl->kviol_bits);
+        if (v > diag->max_k_violation) diag->max_k_violation = v;
+        diag->k_clip_count += c->hctl->step_clip;
+        diag->mass_fix_count += c->hctl->step_fix;
+    }
+    return 0;
+}
+
+int h2d_run(h2d_ctx* c, h2d_run_args* a) {
+    cudaSetDevice(c->device);
+    a->steps_done = 0;
+    if (a->remap_kind != H2D_REMAP_DIRECTCF) {
+        set_err(c, H2D_ERR_INVALID, "only the DirectCF remap is implemented on the device");
+        return H2D_ERR_INVALID;
+    }
+    const int cap = a->max_steps > 0 ? a->max_steps : 4096;
+    if (cap > c->dt_log_cap) {
+        if (c->dt_log) cudaFree(c->dt_log);
+        c->dt_log = nullptr;
+        CK(cudaMalloc(&c->dt_log, sizeof(double) * (size_t)cap));
+        c->dt_log_cap = cap;
+    }
+    if (int rc = ctl_reset(c)) return rc;
+    Ctl& h = *c->hctl;
+    h.t_end = a->t_end;
+    h.cfl = a->cfl;
+    h.max_steps = a->max_steps;
+    h.steps_done = 0;
+    h.floor_count = 0;
+    h.k_clip_count = 0;
+    h.mass_fix_count = 0;
+    h.max_k_violation = a->diag.max_k_violation;
+    h.dt_log = c->dt_log;
+    h.dt_log_cap = c->dt_log_cap;
+    if (int rc = ctl_push(c)) return rc;
+    int parity = c->cur;
+    int rc = 0;
+    // Launch in chunks; the device control block turns every kernel after the
+    // loop condition fails (or after an error) into a no-op.
+    for (;;) {
+        int chunk = 32;
+        if (a->max_steps > 0) {
+            const int left = a->max_steps - h.step;
+            if (left <= 0) break;
+            chunk = left < chunk ? left : chunk;
+        }
+        for (int q = 0; q < chunk; ++q) {
+            enqueue_step(c, parity);
+            parity ^= 1;
+        }
+        if ((rc = check_launch(c))) return rc;
+        if ((rc = ctl_pull(c))) return rc;
+        parity = h.cur;
+        if (h.err_key != kNoErr || h.done) break;
+    }
+    c->cur = h.cur;
+    a->steps_done = h.steps_done;
+    a->floor_count += h.floor_count;
+    a->diag.k_clip_count += h.k_clip_count;
+    a->diag.mass_fix_count += h.mass_fix_count;
+    a->diag.max_k_violation = h.max_k_violation;
+    if (a->dt_log && h.steps_done > 0) {
+        const int n = h.steps_done < a->dt_log_cap ? h.steps_done : a->dt_log_cap;
+        CK(cudaMemcpy(a->dt_log, c->dt_log, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost));
+    }
+    c->have_lag = false;
+    return decode_error(c, true);
+}
+
+int h2d_totals(h2d_ctx* c, double out[6]) {
+    // compute_totals (state.cpp:145-160) is a serial fp64 sum: read the
+    // fields back and add them in the reference order so totals are exact.
+    cudaSetDevice(c->device);
+    const int nx = c->nx, ny = c->ny;
+    const size_t W = (size_t)nx + 2 * G, Wn = W + 1;
+    std::vector<double> m_mix(W * (ny + 2 * G)), e_mix(m_mix.size()), m0(m_mix.size()), m1(m_mix.size());
+    std::vector<double> u(Wn * (ny + 1 + 2 * G) * 2);
+    const StateBufs& s = c->sb[c->cur];
+    if (int rc = get_plane(c, m_mix.data(), s.m_mix, nx, ny)) return rc;
+    if (int rc = get_plane(c, e_mix.data(), s.e_mix, nx, ny)) return rc;
+    if (int rc = get_plane(c, m0.data(), s.m[0], nx, ny)) return rc;
+    if (c->nmat == 2)
+        if (int rc = get_plane(c, m1.data(), s.m[1], nx, ny)) return rc;
+    if (int rc = get_vec(c, u.data(), s.ux, s.uy, nx + 1, ny + 1)) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    auto C = [&](const std::vector<double>& f, int i, int j) { return f[(size_t)(j + G) * W + (i + G)]; };
+    double mass = 0.0, ie = 0.0, mm0 = 0.0, mm1 = 0.0, px = 0.0, py = 0.0;
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+            mass += C(m_mix, i, j);
+            ie += C(m_mix, i, j) * C(e_mix, i, j);
+            mm0 += C(m0, i, j);
+            if (c->nmat == 2) mm1 += C(m1, i, j);
+        }
+    const bool px_ = c->cfg.mesh.bc_x == H2D_BC_PERIODIC, py_ = c->cfg.mesh.bc_y == H2D_BC_PERIODIC;
+    const int ie_ = px_ ? nx - 1 : nx, je_ = py_ ? ny - 1 : ny;
+    for (int j = 0; j <= je_; ++j)
+        for (int i = 0; i <= ie_; ++i) {
+            const double mp =
+                0.25 * (C(m_mix, i - 1, j - 1) + C(m_mix, i, j - 1) + C(m_mix, i - 1, j) + C(m_mix, i, j));
+            const size_t n = (size_t)(j + G) * Wn + (i + G);
+            px += mp * u[2 * n];
+            py += mp * u[2 * n + 1];
+        }
+    out[0] = mass;
+    out[1] = mm0;
+    out[2] = mm1;
+    out[3] = px;
+    out[4] = py;
+    out[5] = ie;
+    return 0;
+}
+
+int h2d_last_error(h2d_ctx* c, h2d_error* e) {
+    *e = c->err;
+    return 0;
+}
+
+}  // extern "C"

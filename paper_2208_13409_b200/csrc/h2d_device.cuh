@@ -1,0 +1,238 @@
+// h2d_device.cuh — device-side layout, control block and the fp64 scalar
+// kernels of the Lagrange + DirectCF step (sm_100a).
+//
+// Bit-exactness contract: compiled with -fmad=false,
+// IEEE div/sqrt; every expression keeps the reference association, and
+// std::max/std::min semantics are kept by rmax/rmin (NaN and signed-zero
+// behaviour of `a < b ? b : a`).  Cited lines are in /root/reference/proj.
+#pragma once
+#include <cstdint>
+
+#define H2D_DEV __device__ __forceinline__
+
+namespace h2d {
+
+constexpr int G = 2;  // ghost layers of every device field (== kGhost, field.hpp:11)
+constexpr double kPureTol = 1e-10;   // state.hpp:17
+constexpr double kThermoTol = 1e-6;  // state.hpp:22
+constexpr double kCflFrac = 0.9;     // remap.cpp:13
+constexpr uint64_t kNoErr = 0xFFFFFFFFFFFFFFFFull;
+
+// Error phases in the reference's program order (cfl_dt -> lagrange_step ->
+// remap_step -> nan_scan).  The first error of a step is the minimum key
+// (phase, outer loop index, inner loop index, sub-index) over all threads.
+enum Phase : uint32_t {
+    PH_CFL_UNPHYS = 1,    // sound_speed in cfl_dt            (harness.cpp:303, eos.hpp:32)
+    PH_CFL_WAVE = 2,      // non-finite wave speed            (harness.cpp:311)
+    PH_Q_UNPHYS = 3,      // sound_speed in compute_q         (lagrange.cpp:48-59,63-77)
+    PH_PRED_TANGLED = 4,  // predict quad volume              (lagrange.cpp:44)
+    PH_CORR_TANGLED = 5,  // correct quad volume              (lagrange.cpp:44)
+    PH_CFL_XFACE = 6,     // remap.cpp:751-752
+    PH_CFL_YFACE = 7,     // remap.cpp:759-760
+    PH_CFL_CORNER = 8,    // remap.cpp:765-766
+    PH_COLLAPSED = 9,     // remap.cpp:788
+    PH_GRAD_XFACE = 10,   // limited_gradient_1d throw        (reconstruct.cpp:18)
+    PH_GRAD_YFACE = 11,
+    PH_GRAD_CORNER = 12,
+    PH_NEGMASS = 13,      // finalize_cells                   (remap.cpp:186,190)
+    PH_GRAD_DUALX = 14,
+    PH_GRAD_DUALY = 15,
+    PH_GRAD_DUALC = 16,
+    PH_NODAL_MASS = 17,   // apply_dual_update                (remap.cpp:455)
+    PH_NAN_CELL = 18,     // nan_scan                         (harness.cpp:347-358)
+    PH_NAN_NODE = 19,
+};
+
+H2D_DEV uint64_t ekey(uint32_t ph, int outer, int inner, int sub) {
+    return ((uint64_t)ph << 58) | ((uint64_t)(uint32_t)(outer + 16) << 33) |
+           ((uint64_t)(uint32_t)(inner + 16) << 8) | (uint64_t)(uint32_t)sub;
+}
+
+// Device control block: the run loop's scalars live on the device so a whole
+// sequence of steps is launched (or graph-replayed) without host syncs.
+struct Ctl {
+    double dt, time, t_end, cfl;
+    int step, max_steps;
+    int done;        // loop condition false -> every later kernel is a no-op
+    int cur;         // parity of the committed State buffers
+    int steps_done;
+    int floor_count;  // sum of LagrangeResult::floor_count
+    int k_clip_count, mass_fix_count;
+    int step_floor;   // floor count of the step in flight
+    int step_clip;
+    int step_fix;
+    int pad_;
+    unsigned long long err_key;
+    unsigned long long wmax_bits;       // max wave speed (non-negative doubles order as integers)
+    unsigned long long kviol_bits;      // max_k_violation of the step in flight
+    double max_k_violation;
+    double last_dt;
+    int commit_time;  // 1: advance time/step at commit (run loop / remap_step)
+    int use_cfl;      // 1: dt from the cfl reduction, 0: dt provided by the host
+    int check_loop;   // 1: apply the run loop condition (harness.cpp:390-391)
+    int pad2_;
+    double* dt_log;   // device array, steps_done entries
+    int dt_log_cap;
+};
+
+H2D_DEV bool halted(const Ctl* c) {
+    return *(volatile const int*)&c->done != 0 || *(volatile const unsigned long long*)&c->err_key != kNoErr;
+}
+H2D_DEV void raise(Ctl* c, uint64_t key) { atomicMin(&c->err_key, (unsigned long long)key); }
+
+// Per-launch constants and field pointers.  Every field is a (P x R) array of
+// doubles with G ghost layers; element (i, j) at (j + G) * P + (i + G).
+struct Dev {
+    int nx, ny, P, nmat, per_x, per_y;
+    double dx, dy, x0, y0, cv, L;
+    int stiff[2];
+    double gamma[2], pi[2];
+    double a1, a2;
+    int face_order, corner_diag, degrade, remap_velocity;
+
+    // current (read) State
+    const double *m[2], *e[2], *k[2], *m_mix, *e_mix, *rho_mix, *p_mix, *nrx, *nry, *ux, *uy;
+    double* vol;
+    // next (written) State: also the remap's Work arrays (remap.cpp:88-98)
+    double *nm[2], *ne[2], *nk[2], *nvol, *nm_mix, *ne_mix, *nrho_mix, *np_mix, *nnrx, *nnry, *nux, *nuy;
+    // LagrangeResult (lagrange.hpp:38-45)
+    double *q, *pmh, *ph[2], *uhx, *uhy, *ulx, *uly, *el[2], *vol_lag;
+    // remap scratch
+    double *me[2], *mcell, *mcell_lag;
+    double *fdx, *fdy, *xlcx, *xlcy, *wlx, *wly;
+    double *fx_dv, *fx_lo, *fx_hi, *fy_dv, *fy_lo, *fy_hi, *cf_dv;
+    int8_t *cf_sx, *cf_sy;
+    double *vlag, *rho[2], *xl2x, *xl2y, *ifd;
+    double *fxm[2], *fxme[2], *fxva[2];  // X-face per-material dm, dme, dva
+    double *fym[2], *fyme[2], *fyva[2];
+    double *fcm[2], *fcme[2], *fcva[2];  // corner per-material
+    double *dmx, *dmy, *dmc;
+    double *dfx_x, *dfx_y, *dfy_x, *dfy_y;  // dual-face momentum contributions
+    double *dc_x[2], *dc_y[2];              // dual-corner contributions per pair
+    double *slm[2], *slme[2];               // pending sliver mass / m*e (remap.cpp:149-153)
+    uint8_t* sliver;                        // per-cell sliver flags (bit a)
+    uint8_t* dflag[4];                      // active X / Y dual faces, dual-corner pairs
+    int* row_slivers;
+    Ctl* ctl;
+};
+
+H2D_DEV size_t ix(const Dev& d, int i, int j) { return (size_t)(j + G) * (size_t)d.P + (size_t)(i + G); }
+
+H2D_DEV double rmax(double a, double b) { return (a < b) ? b : a; }  // std::max
+H2D_DEV double rmin(double a, double b) { return (b < a) ? b : a; }  // std::min
+
+// eos_pressure, eos.hpp:21-25
+H2D_DEV double eos_p(const Dev& d, int a, double rho, double e) {
+    double p = (d.gamma[a] - 1.0) * rho * e;
+    if (d.stiff[a]) p -= d.pi[a];
+    return p;
+}
+// sound_speed, eos.hpp:29-34; `bad` marks the reference's throw
+H2D_DEV double sound(const Dev& d, int a, double rho, double p, bool& bad) {
+    const double pi = d.stiff[a] ? d.pi[a] : 0.0;
+    const double c2 = d.gamma[a] * (p + pi) / rho;
+    if (!(c2 >= 0.0)) bad = true;
+    return sqrt(c2);
+}
+
+// van_leer, reconstruct.cpp:10-14
+H2D_DEV double van_leer(double r) {
+    if (!(r > 0.0)) return 0.0;
+    if (r > 1e300) return 2.0;
+    return (r + fabs(r)) / (1.0 + r);
+}
+// limited_gradient_1d, reconstruct.cpp:16-24
+H2D_DEV double lim_grad(double am, double ac, double ap, double xm, double xc, double xp, bool& bad) {
+    const double hm = xc - xm, hp = xp - xc;
+    if (hm <= 0.0 || hp <= 0.0) {
+        bad = true;
+        return 0.0;
+    }
+    const double dm = (ac - am) / hm;
+    const double dp = (ap - ac) / hp;
+    if (dm == 0.0 || dp == 0.0 || (dm > 0.0) != (dp > 0.0)) return 0.0;
+    const double r = dm / dp;
+    return 0.5 * (van_leer(r) * dp + van_leer(1.0 / r) * dm);
+}
+// face_value at order 2, reconstruct.cpp:26-31
+H2D_DEV double face_value2(double a0, double a1, double a2, double x0, double x1, double x2, double sgn, double lw,
+                           double ufdt, bool& bad) {
+    const double g = lim_grad(a0, a1, a2, x0, x1, x2, bad);
+    return a1 + 0.5 * g * (sgn * lw - ufdt);
+}
+// corner_value LinearDiag, reconstruct.cpp:134-148 (+ diag_gradient :38-42).
+// a/xl are the 3x3 stencil [p][q] flattened as p*3+q.
+H2D_DEV double corner_diag(const Dev& d, const double* a, const double* xlx, const double* xly, double dxp,
+                           double dyp, double lwx, double lwy, bool& bad) {
+    const double ac = a[4];
+    const double diag = sqrt(d.dx * d.dx + d.dy * d.dy);
+    const double sx = dxp >= 0.0 ? 1.0 : -1.0;
+    if (dxp * dyp > 0.0) {
+        const double vx = d.dx / diag, vy = d.dy / diag;
+        const double sc = xlx[4] * vx + xly[4] * vy;
+        const double gv = lim_grad(a[0], ac, a[8], xlx[0] * vx + xly[0] * vy, sc, xlx[8] * vx + xly[8] * vy, bad);
+        const double ex = sx * lwx - dxp, ey = sx * lwy - dyp;
+        return ac + 0.5 * gv * (ex * vx + ey * vy);
+    }
+    const double vx = d.dx / diag, vy = -d.dy / diag;
+    const double sc = xlx[4] * vx + xly[4] * vy;
+    const double gvp = lim_grad(a[2], ac, a[6], xlx[2] * vx + xly[2] * vy, sc, xlx[6] * vx + xly[6] * vy, bad);
+    const double ex = sx * lwx - dxp, ey = sx * -lwy - dyp;
+    return ac + 0.5 * gvp * (ex * vx + ey * vy);
+}
+
+// corner_fraction / clipped_fraction, vof.cpp:28-45
+H2D_DEV double corner_fraction(double A, double B, double t) {
+    if (t <= 0.0) return 0.0;
+    if (A > 0.0 && t < A) return t * t / (2.0 * A * B);
+    return (t - 0.5 * A) / B;
+}
+H2D_DEV double clipped_fraction(double w, double h, double nx, double ny, double dd) {
+    double A = fabs(nx) * w, B = fabs(ny) * h;
+    if (A > B) {
+        const double t = A;
+        A = B;
+        B = t;
+    }
+    const double S = 0.5 * (A + B);
+    if (dd <= -S) return 0.0;
+    if (dd >= S) return 1.0;
+    if (dd <= 0.0) return corner_fraction(A, B, dd + S);
+    return 1.0 - corner_fraction(A, B, S - dd);
+}
+// place_interface, vof.cpp:47-73 (returns d)
+H2D_DEV double place_interface(double frac, double nx, double ny, double lox, double loy, double hix, double hiy) {
+    const double w = hix - lox, h = hiy - loy;
+    double A = fabs(nx) * w, B = fabs(ny) * h;
+    if (A > B) {
+        const double t = A;
+        A = B;
+        B = t;
+    }
+    const double S = 0.5 * (A + B);
+    const bool flip = frac > 0.5;
+    const double kk = flip ? 1.0 - frac : frac;
+    double t;
+    if (A > 0.0 && kk <= A / (2.0 * B))
+        t = sqrt(2.0 * A * B * kk);
+    else
+        t = kk * B + 0.5 * A;
+    double dd = t - S;
+    if (flip) dd = -dd;
+    if (fabs(clipped_fraction(w, h, nx, ny, dd) - frac) > 1e-13) {
+        double lo = -S, hi = S;
+        for (int it = 0; it < 200 && hi - lo > 1e-13 * (2.0 * S); ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (clipped_fraction(w, h, nx, ny, mid) < frac)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        dd = 0.5 * (lo + hi);
+    }
+    return dd;
+}
+
+H2D_DEV bool is_mixed(double k0) { return k0 > kPureTol && k0 < 1.0 - kPureTol; }  // remap.cpp:100
+
+}  // namespace h2d

@@ -1,0 +1,1494 @@
+// h2d_kernels.cu — fp64 sm_100a kernels of one Lagrange + DirectCF step.
+//
+// Each kernel restates one reference phase (cited file:line, proj/src) as a
+// data-parallel gather: every face / corner / dual-face flux is computed once
+// by its own thread and stored; every cell and node then sums its incoming
+// contributions in exactly the reference's program order (SURVEY.md App. C
+// items 3-4), so the result is bit-identical to the serial scatter loops.
+// Errors are recorded as the minimum (phase, loop index) key, i.e. the first
+// exception the serial reference would have thrown.
+#include "h2d_device.cuh"
+#include "h2d_launch.h"
+
+#include <cuda_runtime.h>
+
+namespace h2d {
+
+// ---------------------------------------------------------------------------
+// indexing helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tid2(int& i, int& j, int ilo, int jlo) {
+    i = ilo + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+    j = jlo + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+}
+#define AT(p, i, j) ((p)[ix(d, (i), (j))])
+
+// ---------------------------------------------------------------------------
+// control kernels
+// ---------------------------------------------------------------------------
+// Start of a step or of a single API phase. mode: 0 = run-loop step (applies
+// harness.cpp:390-391), 1 = API call with host dt, 2 = API cfl_dt only.
+__global__ void k_begin(Ctl* c, int mode, double host_dt) {
+    if (c->err_key != kNoErr || c->done) return;
+    c->wmax_bits = 0ull;
+    c->kviol_bits = 0ull;
+    c->step_floor = 0;
+    c->step_clip = 0;
+    c->step_fix = 0;
+    if (mode == 0) {
+        const double t_end = c->t_end;
+        if (!(c->time < t_end - 1e-15 * rmax(1.0, t_end))) {
+            c->done = 1;
+            return;
+        }
+        if (c->max_steps > 0 && c->step >= c->max_steps) {
+            c->done = 1;
+            return;
+        }
+    } else if (mode == 1) {
+        c->dt = host_dt;
+    }
+}
+
+// cfl_dt, harness.cpp:293-313: per-cell wave speed, block max, one atomic
+// per block on the bit pattern (non-negative doubles order as integers).
+template <int NM>
+__global__ void k_cfl(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    unsigned long long wb = 0ull;
+    if (i < d.nx && j < d.ny) {
+        const size_t c = ix(d, i, j);
+        double cs = 0.0;
+        bool bad = false;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            const double ka = d.k[a][c];
+            if (ka < kThermoTol) continue;
+            const double rho_a = d.m[a][c] / (ka * d.cv);
+            const double pa = eos_p(d, a, rho_a, d.e[a][c]);
+            cs += ka * sound(d, a, rho_a, pa, bad);
+        }
+        if (bad) raise(d.ctl, ekey(PH_CFL_UNPHYS, j, i, 0));
+        double umax = 0.0;
+#pragma unroll
+        for (int dj = 0; dj <= 1; ++dj)
+#pragma unroll
+            for (int di = 0; di <= 1; ++di) {
+                const size_t n = ix(d, i + di, j + dj);
+                const double ux = d.ux[n], uy = d.uy[n];
+                umax = rmax(umax, sqrt(ux * ux + uy * uy));
+            }
+        const double w = cs + umax;
+        if (w > 0.0) wb = (unsigned long long)__double_as_longlong(w);  // NaN and +-0 never raise the max
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, wb, o);
+        wb = v > wb ? v : wb;
+    }
+    __shared__ unsigned long long sw[32];
+    const int lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31;
+    const int warp = (threadIdx.y * blockDim.x + threadIdx.x) >> 5;
+    if (lane == 0) sw[warp] = wb;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = (blockDim.x * blockDim.y + 31) >> 5;
+        wb = lane < nw ? sw[lane] : 0ull;
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long v = __shfl_xor_sync(0xffffffffu, wb, o);
+            wb = v > wb ? v : wb;
+        }
+        if (lane == 0 && wb) atomicMax(&d.ctl->wmax_bits, wb);
+    }
+}
+
+// harness.cpp:311-312 and the run loop's dt = min(dt, t_end - t) (:395)
+__global__ void k_cfl_final(Ctl* c, double dx, double dy, int run_loop) {
+    if (c->err_key != kNoErr || c->done) return;
+    const double wmax = __longlong_as_double((long long)c->wmax_bits);
+    if (!(wmax > 0.0) || !isfinite(wmax)) {
+        raise(c, ekey(PH_CFL_WAVE, 0x1FFFFFF - 32, 0, 0));
+        return;
+    }
+    double dt = c->cfl * rmin(dx, dy) / wmax;
+    c->last_dt = dt;
+    if (run_loop) dt = rmin(dt, c->t_end - c->time);
+    c->dt = dt;
+}
+
+// ---------------------------------------------------------------------------
+// ghost layers (state.cpp:47-108)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int wrap_cell(int i, int n, int periodic) {
+    if (periodic) return (i % n + n) % n;
+    if (i < 0) return -1 - i;
+    if (i >= n) return 2 * n - 1 - i;
+    return i;
+}
+// thread index -> ghost cell position of the (nx+4)x(ny+4) ring
+__device__ __forceinline__ bool ghost_cell_pos(int t, int nx, int ny, int& i, int& j) {
+    const int W = nx + 2 * G;
+    if (t < 2 * G * W) {  // bottom and top strips
+        const int r = t / W;
+        i = t % W - G;
+        j = r < G ? r - G : ny + (r - G);
+        return true;
+    }
+    t -= 2 * G * W;
+    if (t < 2 * G * ny) {
+        const int col = t / ny;
+        j = t % ny;
+        i = col < G ? col - G : nx + (col - G);
+        return true;
+    }
+    return false;
+}
+
+__global__ void k_ghost_cells(Dev d, FieldList fl) {
+    if (fl.respect_halt && halted(d.ctl)) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    int i, j;
+    if (!ghost_cell_pos(t, d.nx, d.ny, i, j)) return;
+    const int is = wrap_cell(i, d.nx, d.per_x), js = wrap_cell(j, d.ny, d.per_y);
+    const size_t dst = ix(d, i, j), src = ix(d, is, js);
+    for (int f = 0; f < fl.n; ++f) fl.f[f][dst] = fl.f[f][src];
+}
+
+// fill_ghost_nodes (state.cpp:87-108) for Vec2 pairs (x, y).
+__global__ void k_ghost_nodes(Dev d, FieldList fl) {
+    if (fl.respect_halt && halted(d.ctl)) return;
+    const int nx = d.nx, ny = d.ny;
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int W = nx + 1 + 2 * G;
+    int i, j;
+    if (t < 2 * G * W) {
+        const int r = t / W;
+        i = t % W - G;
+        j = r < G ? r - G : ny + 1 + (r - G);
+    } else {
+        t -= 2 * G * W;
+        if (t < 2 * G * (ny + 1)) {
+            const int col = t / (ny + 1);
+            j = t % (ny + 1);
+            i = col < G ? col - G : nx + 1 + (col - G);
+        } else {
+            // boundary-node wall zeroing (state.cpp:90-95)
+            t -= 2 * G * (ny + 1);
+            if (t < 2 * (ny + 1)) {
+                j = t % (ny + 1);
+                i = t < ny + 1 ? 0 : nx;
+                if (!d.per_x)
+                    for (int f = 0; f < fl.n; f += 2) fl.f[f][ix(d, i, j)] = 0.0;
+                return;
+            }
+            t -= 2 * (ny + 1);
+            if (t < 2 * (nx + 1)) {
+                i = t % (nx + 1);
+                j = t < nx + 1 ? 0 : ny;
+                if (!d.per_y)
+                    for (int f = 1; f < fl.n; f += 2) fl.f[f][ix(d, i, j)] = 0.0;
+            }
+            return;
+        }
+    }
+    // wrap_node (state.cpp:71-80)
+    int si, sj;
+    bool fi = false, fj = false;
+    if (d.per_x) {
+        si = i % nx;
+        if (si < 0) si += nx;
+    } else if (i < 0) {
+        si = -i;
+        fi = true;
+    } else if (i > nx) {
+        si = 2 * nx - i;
+        fi = true;
+    } else {
+        si = i;
+    }
+    if (d.per_y) {
+        sj = j % ny;
+        if (sj < 0) sj += ny;
+    } else if (j < 0) {
+        sj = -j;
+        fj = true;
+    } else if (j > ny) {
+        sj = 2 * ny - j;
+        fj = true;
+    } else {
+        sj = j;
+    }
+    // the source is read as it is after the wall zeroing of the same call
+    const bool zx = !d.per_x && (si == 0 || si == nx);
+    const bool zy = !d.per_y && (sj == 0 || sj == ny);
+    const size_t dst = ix(d, i, j), src = ix(d, si, sj);
+    for (int f = 0; f < fl.n; f += 2) {
+        double vx = zx ? 0.0 : fl.f[f][src];
+        double vy = zy ? 0.0 : fl.f[f + 1][src];
+        if (fi) vx = -vx;
+        if (fj) vy = -vy;
+        fl.f[f][dst] = vx;
+        fl.f[f + 1][dst] = vy;
+    }
+}
+
+// sync_derived, state.cpp:120-143, over every cell including ghosts.
+// src: 0 = current state (API), 1 = next state (after a remap).
+template <int NM>
+__global__ void k_sync(Dev d, int next, int respect_halt) {
+    if (respect_halt && halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, -G, -G);
+    if (i >= d.nx + G || j >= d.ny + G) return;
+    const size_t c = ix(d, i, j);
+    const double cv = d.cv;
+    double m = 0.0, me = 0.0, p = 0.0;
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        const double ka = next ? d.nk[a][c] : d.k[a][c];
+        if (ka <= 0.0) continue;
+        const double ma = next ? d.nm[a][c] : d.m[a][c];
+        const double ea = next ? d.ne[a][c] : d.e[a][c];
+        m += ma;
+        me += ma * ea;
+        if (ka < kThermoTol) continue;
+        const double rho_a = ma / (ka * cv);
+        p += ka * eos_p(d, a, rho_a, ea);
+    }
+    double* om = next ? d.nm_mix : const_cast<double*>(d.m_mix);
+    double* oe = next ? d.ne_mix : const_cast<double*>(d.e_mix);
+    double* orho = next ? d.nrho_mix : const_cast<double*>(d.rho_mix);
+    double* op = next ? d.np_mix : const_cast<double*>(d.p_mix);
+    double* ov = next ? d.nvol : d.vol;
+    om[c] = m;
+    oe[c] = m > 0.0 ? me / m : 0.0;
+    orho[c] = m / cv;
+    op[c] = p;
+    ov[c] = cv;
+}
+
+// ---------------------------------------------------------------------------
+// Lagrangian phase (lagrange.cpp)
+// ---------------------------------------------------------------------------
+// compute_q, lagrange.cpp:63-77 (+ div_u_cell :14-20, pseudo_viscosity :7-12,
+// mixture_sound_speed :48-59)
+template <int NM>
+__global__ void k_q(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    if (i >= d.nx || j >= d.ny) return;
+    const size_t c = ix(d, i, j);
+    const size_t n00 = ix(d, i, j), n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
+    const double ux_l = 0.5 * (d.ux[n00] + d.ux[n01]);
+    const double ux_r = 0.5 * (d.ux[n10] + d.ux[n11]);
+    const double uy_b = 0.5 * (d.uy[n00] + d.uy[n10]);
+    const double uy_t = 0.5 * (d.uy[n01] + d.uy[n11]);
+    const double div = (ux_r - ux_l) / d.dx + (uy_t - uy_b) / d.dy;
+    double q = 0.0;
+    if (!(div >= 0.0)) {
+        double cs = 0.0;
+        bool bad = false;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            const double ka = d.k[a][c];
+            if (ka < kThermoTol) continue;
+            const double rho_a = d.m[a][c] / (ka * d.cv);
+            const double pa = eos_p(d, a, rho_a, d.e[a][c]);
+            cs += ka * sound(d, a, rho_a, pa, bad);
+        }
+        if (bad) raise(d.ctl, ekey(PH_Q_UNPHYS, j, i, 0));
+        const double rho = d.rho_mix[c];
+        const double du = d.L * fabs(div);
+        q = rho * d.a1 * du * cs + d.a2 * rho * du * du;
+    }
+    d.q[c] = q;
+}
+
+// quad_volume_disp, lagrange.cpp:36-46, with node displacements s*u
+__device__ __forceinline__ double quad_vol(const Dev& d, const double* ux, const double* uy, double s, int i, int j,
+                                           bool& tangled) {
+    const size_t n00 = ix(d, i, j), n10 = ix(d, i + 1, j), n11 = ix(d, i + 1, j + 1), n01 = ix(d, i, j + 1);
+    const double d00x = s * ux[n00], d00y = s * uy[n00];
+    const double d10x = s * ux[n10], d10y = s * uy[n10];
+    const double d11x = s * ux[n11], d11y = s * uy[n11];
+    const double d01x = s * ux[n01], d01y = s * uy[n01];
+    const double ebx = d.dx + d10x - d00x, eby = d10y - d00y;
+    const double elx = d01x - d00x, ely = d.dy + d01y - d00y;
+    const double etx = d.dx + d11x - d01x, ety = d11y - d01y;
+    const double erx = d11x - d10x, ery = d.dy + d11y - d10y;
+    const double s1 = 0.5 * (ebx * ely - eby * elx);
+    const double s2 = 0.5 * (etx * ery - ety * erx);
+    if (s1 <= 0.0 || s2 <= 0.0) tangled = true;
+    return s1 + s2;
+}
+
+// predict, cell part, lagrange.cpp:89-131 (dh = 0.5*dt*u, :251-255)
+template <int NM>
+__global__ void k_predict_cells(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    if (i >= d.nx || j >= d.ny) return;
+    const double dt = d.ctl->dt;
+    const size_t c = ix(d, i, j);
+    bool tangled = false;
+    const double vol = quad_vol(d, d.ux, d.uy, 0.5 * dt, i, j, tangled);
+    if (tangled) raise(d.ctl, ekey(PH_PRED_TANGLED, j, i, 0));
+    double pmix = 0.0;
+    int floors = 0;
+    const double cv = d.cv;
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        const double ka = d.k[a][c];
+        double pa_h = 0.0;
+        if (!(ka < kThermoTol)) {
+            const double ma = d.m[a][c], en = d.e[a][c];
+            const double rho_n = ma / (ka * cv);
+            const double rho_h = ma / (ka * vol);
+            const double pa_n = eos_p(d, a, rho_n, en);
+            double ea = en - (pa_n + d.q[c]) * (1.0 / rho_h - 1.0 / rho_n);
+            const double efloor = 1e-8 * fabs(en);
+            if (ea < efloor) {
+                ea = efloor;
+                ++floors;
+            }
+            pa_h = eos_p(d, a, rho_h, ea);
+            pmix += ka * pa_h;
+        }
+        d.ph[a][c] = pa_h;
+    }
+    d.pmh[c] = pmix;
+    if (floors) atomicAdd(&d.ctl->step_floor, floors);
+}
+
+// predict, node part, lagrange.cpp:135-142 (nodal_mass state.cpp:34-36,
+// grad_pq_node lagrange.cpp:22-30)
+__global__ void k_predict_nodes(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    if (i > d.nx || j > d.ny) return;
+    const double dt = d.ctl->dt;
+    const size_t a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
+    const double mp = 0.25 * (d.m_mix[a] + d.m_mix[b] + d.m_mix[c] + d.m_mix[e]);
+    const double rho_p = mp / d.cv;
+    const double pq_a = d.pmh[a] + d.q[a], pq_b = d.pmh[b] + d.q[b];
+    const double pq_c = d.pmh[c] + d.q[c], pq_e = d.pmh[e] + d.q[e];
+    // pq(i,j-1) + pq(i,j) - pq(i-1,j-1) - pq(i-1,j)
+    const double gx = (pq_b + pq_e - pq_a - pq_c) / (2.0 * d.dx);
+    // pq(i-1,j) + pq(i,j) - pq(i-1,j-1) - pq(i,j-1)
+    const double gy = (pq_c + pq_e - pq_a - pq_b) / (2.0 * d.dy);
+    const double s = 0.5 * dt / rho_p;
+    d.uhx[e] = d.ux[e] - gx * s;
+    d.uhy[e] = d.uy[e] - gy * s;
+}
+
+// correct, lagrange.cpp:146-196; nodes: u_lag = 2 u_half - u, cells: e_lag.
+template <int NM>
+__global__ void k_correct(Dev d, int write_vol_lag) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    if (i > d.nx || j > d.ny) return;
+    const double dt = d.ctl->dt;
+    const size_t n = ix(d, i, j);
+    d.ulx[n] = 2.0 * d.uhx[n] - d.ux[n];
+    d.uly[n] = 2.0 * d.uhy[n] - d.uy[n];
+    if (i >= d.nx || j >= d.ny) return;
+    bool tangled = false;
+    const double vol = quad_vol(d, d.uhx, d.uhy, dt, i, j, tangled);
+    if (tangled) raise(d.ctl, ekey(PH_CORR_TANGLED, j, i, 0));
+    if (write_vol_lag) d.vol_lag[n] = vol;
+    int floors = 0;
+    const double cv = d.cv;
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        const double ka = d.k[a][n];
+        const double en = d.e[a][n];
+        double ea = 0.0;
+        if (ka < kThermoTol) {
+            if (ka > 0.0) ea = en;
+        } else {
+            const double ma = d.m[a][n];
+            const double rho_n = ma / (ka * cv);
+            const double rho_l = ma / (ka * vol);
+            ea = en - (d.ph[a][n] + d.q[n]) * (1.0 / rho_l - 1.0 / rho_n);
+            const double efloor = 1e-8 * fabs(en);
+            if (ea < efloor) {
+                ea = efloor;
+                ++floors;
+            }
+        }
+        d.el[a][n] = ea;
+    }
+    if (floors) atomicAdd(&d.ctl->step_floor, floors);
+}
+
+// ---------------------------------------------------------------------------
+// DirectCF remap (remap.cpp:734-1073)
+// ---------------------------------------------------------------------------
+// make_work, remap.cpp:116-140, over every cell incl. ghosts: the next-state
+// buffers become the Work arrays.
+template <int NM>
+__global__ void k_make_work(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, -G, -G);
+    if (i > d.nx + G || j > d.ny + G) return;
+    const size_t c = ix(d, i, j);
+    if (!d.remap_velocity) {  // w.u = lag.u_lag becomes the new u unchanged
+        d.nux[c] = d.ulx[c];
+        d.nuy[c] = d.uly[c];
+    }
+    if (i >= d.nx + G || j >= d.ny + G) return;
+    double mc = 0.0;
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        const double ma = d.m[a][c], ea = d.el[a][c];
+        d.nm[a][c] = ma;
+        d.ne[a][c] = ea;
+        d.nk[a][c] = d.k[a][c];
+        d.me[a][c] = ma * ea;
+        mc += ma;
+    }
+    d.mcell_lag[c] = mc;
+    d.nnrx[c] = d.nrx[c];
+    d.nnry[c] = d.nry[c];
+}
+
+// cf_face_flux_x, remap.cpp:27-47 (Y faces call it with swapped components)
+__device__ __forceinline__ void face_flux(double ym, double yp, double dmx, double dmy, double dpx, double dpy,
+                                          double& dv, double& wl, double& wh) {
+    dv = 0.0;
+    wl = 0.0;
+    wh = 0.0;
+    const double wlo = ym + rmax(0.0, dmy);
+    const double whi = yp + rmin(0.0, dpy);
+    if (whi <= wlo) return;
+    wl = wlo;
+    wh = whi;
+    const double den = (yp + dpy) - (ym + dmy);
+    double xlo, xhi;
+    if (fabs(den) < 1e-300) {
+        xlo = xhi = 0.5 * (dmx + dpx);
+    } else {
+        const double slope = (dpx - dmx) / den;
+        xlo = dmx + slope * (wlo - (ym + dmy));
+        xhi = dmx + slope * (whi - (ym + dmy));
+    }
+    dv = 0.5 * (xlo + xhi) * (whi - wlo);
+}
+
+// make_axis_geom X/Y (remap.cpp:296-322) + face/corner flux geometry
+// (:744-767), over the ghosted node range [-2, n+2]^2.
+__global__ void k_geom(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, -G, -G);
+    const int nx = d.nx, ny = d.ny;
+    if (i > nx + G || j > ny + G) return;
+    const double dt = d.ctl->dt;
+    const double cv = d.cv;
+    const size_t n = ix(d, i, j);
+    const double u0x = d.uhx[n], u0y = d.uhy[n];
+    // corner flux, remap.cpp:16-25
+    {
+        const double ddx = u0x * dt, ddy = u0y * dt;
+        double dv = fabs(ddx * ddy);
+        int8_t sx = 0, sy = 0;
+        if (dv == 0.0) {
+            dv = 0.0;
+        } else {
+            sx = ddx > 0.0 ? 1 : -1;
+            sy = ddy > 0.0 ? 1 : -1;
+        }
+        d.cf_dv[n] = dv;
+        d.cf_sx[n] = sx;
+        d.cf_sy[n] = sy;
+        if (dv > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
+    }
+    const bool has_up = j < ny + G, has_right = i < nx + G;
+    if (has_up) {  // X geometry at (ia=i, ic=j) and the X face
+        const size_t nu = ix(d, i, j + 1);
+        d.fdx[n] = 0.5 * (u0x + d.uhx[nu]) * dt;
+        double dv, wl, wh;
+        face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * u0x, dt * u0y, dt * d.uhx[nu], dt * d.uhy[nu], dv, wl,
+                  wh);
+        d.fx_dv[n] = dv;
+        d.fx_lo[n] = wl;
+        d.fx_hi[n] = wh;
+        if (fabs(dv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
+    }
+    if (has_right) {  // Y geometry at (ia=j, ic=i), stored at (i, j), and the Y face
+        const size_t nr = ix(d, i + 1, j);
+        d.fdy[n] = 0.5 * (u0y + d.uhy[nr]) * dt;
+        double dv, wl, wh;
+        face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * u0y, dt * u0x, dt * d.uhy[nr], dt * d.uhx[nr], dv, wl,
+                  wh);
+        d.fy_dv[n] = dv;
+        d.fy_lo[n] = wl;
+        d.fy_hi[n] = wh;
+        if (fabs(dv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
+    }
+    if (has_up && has_right) {  // xlagc / wlag of cell (i, j) on both axes
+        const size_t nu = ix(d, i, j + 1), nr = ix(d, i + 1, j), nur = ix(d, i + 1, j + 1);
+        const double dlx = 0.5 * (u0x + d.uhx[nu]) * dt, drx = 0.5 * (d.uhx[nr] + d.uhx[nur]) * dt;
+        d.xlcx[n] = d.x0 + (i + 0.5) * d.dx + 0.5 * (dlx + drx);
+        d.wlx[n] = d.dx + (drx - dlx);
+        const double dly = 0.5 * (u0y + d.uhy[nr]) * dt, dry = 0.5 * (d.uhy[nu] + d.uhy[nur]) * dt;
+        d.xlcy[n] = d.y0 + (j + 0.5) * d.dy + 0.5 * (dly + dry);
+        d.wly[n] = d.dy + (dry - dly);
+    }
+}
+
+// corner_term of remap.cpp:775-785 for cell (i, j) and node (ni, nj)
+__device__ __forceinline__ double corner_term(const Dev& d, int i, int j, int ni, int nj) {
+    const size_t n = ix(d, ni, nj);
+    const double dv = d.cf_dv[n];
+    if (dv == 0.0) return 0.0;
+    const int sx = d.cf_sx[n], sy = d.cf_sy[n];
+    const int di = sx > 0 ? ni - 1 : ni, dj = sy > 0 ? nj - 1 : nj;
+    if (di == i && dj == j) return dv;
+    const int ri = sx > 0 ? ni : ni - 1, rj = sy > 0 ? nj : nj - 1;
+    if (ri == i && rj == j) return -dv;
+    return 0.0;
+}
+
+// Lagrangian volume / densities (remap.cpp:769-794), 2D centroids (:797-803)
+// and interface placement (:807-824), over cells [-2, n+2)^2.
+template <int NM>
+__global__ void k_cells(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, -G, -G);
+    if (i >= d.nx + G || j >= d.ny + G) return;
+    const double dt = d.ctl->dt;
+    const size_t c = ix(d, i, j);
+    double v = d.cv + d.fx_dv[ix(d, i + 1, j)] - d.fx_dv[c] + d.fy_dv[ix(d, i, j + 1)] - d.fy_dv[c];
+    v += corner_term(d, i, j, i, j) + corner_term(d, i, j, i + 1, j) + corner_term(d, i, j, i, j + 1) +
+         corner_term(d, i, j, i + 1, j + 1);
+    if (v <= 0.0) raise(d.ctl, ekey(PH_COLLAPSED, j, i, 0));
+    d.vlag[c] = v;
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        const double ka = d.nk[a][c];
+        d.rho[a][c] = ka > 0.0 ? d.nm[a][c] / (ka * v) : 0.0;
+    }
+    const size_t n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
+    const double mdx = 0.25 * (dt * d.uhx[c] + dt * d.uhx[n10] + dt * d.uhx[n01] + dt * d.uhx[n11]);
+    const double mdy = 0.25 * (dt * d.uhy[c] + dt * d.uhy[n10] + dt * d.uhy[n01] + dt * d.uhy[n11]);
+    d.xl2x[c] = (d.x0 + (i + 0.5) * d.dx) + mdx;
+    d.xl2y[c] = (d.y0 + (j + 0.5) * d.dy) + mdy;
+    if (NM == 2) {
+        const double k0 = d.nk[0][c];
+        if (is_mixed(k0)) {
+            const double cx = d.x0 + (i + 0.5) * d.dx, cy = d.y0 + (j + 0.5) * d.dy;
+            const double lox = cx - 0.5 * d.dx + d.fdx[c], loy = cy - 0.5 * d.dy + d.fdy[c];
+            const double hix = cx + 0.5 * d.dx + d.fdx[n10], hiy = cy + 0.5 * d.dy + d.fdy[n01];
+            d.ifd[c] = place_interface(k0, d.nnrx[c], d.nnry[c], lox, loy, hix, hiy);
+        }
+    }
+}
+
+// box_frac0 + split_flux, remap.cpp:243-268, donor cell (di, dj)
+template <int NM>
+__device__ __forceinline__ void split_flux(const Dev& d, int di, int dj, double blox, double bloy, double bhix,
+                                           double bhiy, double dvol, double dva[2]) {
+    dva[0] = dvol;
+    dva[1] = 0.0;
+    if (NM != 2) return;
+    const size_t c = ix(d, di, dj);
+    const double k0 = d.nk[0][c];
+    if (is_mixed(k0)) {
+        const double nx = d.nnrx[c], ny = d.nnry[c], dd = d.ifd[c];
+        const double cx = d.x0 + (di + 0.5) * d.dx, cy = d.y0 + (dj + 0.5) * d.dy;
+        const double lox = cx - 0.5 * d.dx + d.fdx[c], loy = cy - 0.5 * d.dy + d.fdy[c];
+        const double hix = cx + 0.5 * d.dx + d.fdx[ix(d, di + 1, dj)];
+        const double hiy = cy + 0.5 * d.dy + d.fdy[ix(d, di, dj + 1)];
+        const double rcx = 0.5 * (lox + hix), rcy = 0.5 * (loy + hiy);
+        const double bcx = 0.5 * (blox + bhix), bcy = 0.5 * (bloy + bhiy);
+        const double bw = bhix - blox, bh = bhiy - bloy;
+        const double area = bw * bh;
+        double f0;
+        if (!(area > 0.0)) {
+            const double s = (nx * (bcx - rcx) + ny * (bcy - rcy)) - dd;
+            f0 = s <= 0.0 ? 1.0 : 0.0;
+        } else {
+            const double dbox = dd - (nx * (bcx - rcx) + ny * (bcy - rcy));
+            f0 = clipped_fraction(bw, bh, nx, ny, dbox);
+        }
+        dva[0] = f0 * dvol;
+        dva[1] = dvol - dva[0];
+    } else if (k0 < 0.5) {
+        dva[0] = 0.0;
+        dva[1] = dvol;
+    }
+}
+
+// Face fluxes, remap.cpp:850-918. AX = 1: X faces (ia = i, ic = j); AX = 0:
+// Y faces (ia = j, ic = i), both stored at device (i, j).
+template <int NM, int AX>
+__global__ void k_faces(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    if (AX ? (i > d.nx || j >= d.ny) : (i >= d.nx || j > d.ny)) return;
+    const size_t f = ix(d, i, j);
+    const double dvol = AX ? d.fx_dv[f] : d.fy_dv[f];
+    double* fm = nullptr;
+    double dmtot = 0.0;
+    double dva[2] = {0.0, 0.0};
+    double rfv[2] = {0.0, 0.0}, efv[2] = {0.0, 0.0};
+    if (dvol != 0.0) {
+        const int ia = AX ? i : j, ic = AX ? j : i;
+        const int ia_d = dvol > 0.0 ? ia - 1 : ia;
+        const double sgn = dvol > 0.0 ? 1.0 : -1.0;
+        const int cdi = AX ? ia_d : ic, cdj = AX ? ic : ia_d;
+        const double wlo = AX ? d.fx_lo[f] : d.fy_lo[f], whi = AX ? d.fx_hi[f] : d.fy_hi[f];
+        const double wwin = whi - wlo;
+        const double width = dvol / wwin;
+        const double f0pos = AX ? d.x0 + ia * d.dx : d.y0 + ia * d.dy;
+        const double blo = rmin(f0pos, f0pos + width), bhi = rmax(f0pos, f0pos + width);
+        if (AX)
+            split_flux<NM>(d, cdi, cdj, blo, wlo, bhi, whi, dvol, dva);
+        else
+            split_flux<NM>(d, cdi, cdj, wlo, blo, whi, bhi, dvol, dva);
+        bool bad = false;
+        const size_t cm = AX ? ix(d, ia_d - 1, ic) : ix(d, ic, ia_d - 1);
+        const size_t cc = AX ? ix(d, ia_d, ic) : ix(d, ic, ia_d);
+        const size_t cp = AX ? ix(d, ia_d + 1, ic) : ix(d, ic, ia_d + 1);
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            if (dva[a] == 0.0) continue;
+            int ord = d.face_order;
+            if (ord == 2 && NM == 2 && d.degrade &&
+                (d.nk[a][cm] < 1.0 - kPureTol || d.nk[a][cc] < 1.0 - kPureTol || d.nk[a][cp] < 1.0 - kPureTol))
+                ord = 1;
+            double rf, ef;
+            if (ord <= 1) {
+                rf = d.rho[a][cc];
+                ef = d.ne[a][cc];
+            } else {
+                const double* xl = AX ? d.xlcx : d.xlcy;
+                const double* wl = AX ? d.wlx : d.wly;
+                const double* fd = AX ? d.fdx : d.fdy;
+                const double x0 = xl[cm], x1 = xl[cc], x2 = xl[cp];
+                const double lw = wl[cc], ufdt = fd[f];
+                rf = face_value2(d.rho[a][cm], d.rho[a][cc], d.rho[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
+                ef = face_value2(d.ne[a][cm], d.ne[a][cc], d.ne[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
+            }
+            rfv[a] = rf;
+            efv[a] = ef;
+        }
+        if (bad) raise(d.ctl, ekey(AX ? PH_GRAD_XFACE : PH_GRAD_YFACE, ic, ia, 0));
+    }
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        double dm = 0.0, dme = 0.0;
+        if (dva[a] != 0.0) {
+            dm = rfv[a] * dva[a];
+            dme = rfv[a] * efv[a] * dva[a];
+            dmtot += dm;
+        }
+        (AX ? d.fxm : d.fym)[a][f] = dm;
+        (AX ? d.fxme : d.fyme)[a][f] = dme;
+        (AX ? d.fxva : d.fyva)[a][f] = dva[a];
+    }
+    fm = AX ? d.dmx : d.dmy;
+    fm[f] = dmtot;
+}
+
+// Corner fluxes, remap.cpp:923-983, per node (i, j) in [0, nx] x [0, ny].
+template <int NM>
+__global__ void k_corners(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    if (i > d.nx || j > d.ny) return;
+    const size_t n = ix(d, i, j);
+    const double cdv = d.cf_dv[n];
+    double dva[2] = {0.0, 0.0}, rfv[2] = {0.0, 0.0}, efv[2] = {0.0, 0.0};
+    double dmtot = 0.0;
+    if (cdv != 0.0) {
+        const double dt = d.ctl->dt;
+        const int sx = d.cf_sx[n], sy = d.cf_sy[n];
+        const int di = sx > 0 ? i - 1 : i, dj = sy > 0 ? j - 1 : j;
+        const double npx = d.x0 + i * d.dx, npy = d.y0 + j * d.dy;
+        const double ddx = dt * d.uhx[n], ddy = dt * d.uhy[n];
+        const double blox = rmin(npx, npx + ddx), bloy = rmin(npy, npy + ddy);
+        const double bhix = rmax(npx, npx + ddx), bhiy = rmax(npy, npy + ddy);
+        split_flux<NM>(d, di, dj, blox, bloy, bhix, bhiy, cdv, dva);
+        const size_t dc = ix(d, di, dj);
+        const double lwx = d.wlx[dc], lwy = d.wly[dc];
+        bool bad = false;
+        const bool lin_cfg = d.corner_diag && d.face_order > 1;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            if (dva[a] == 0.0) continue;
+            bool lin = lin_cfg;
+            if (lin && NM == 2 && d.degrade) {
+                for (int q = -1; q <= 1 && lin; ++q)
+                    for (int p = -1; p <= 1; ++p)
+                        if (d.nk[a][ix(d, di + p, dj + q)] < 1.0 - kPureTol) {
+                            lin = false;
+                            break;
+                        }
+            }
+            double rf, ef;
+            if (!lin) {
+                rf = d.rho[a][dc];
+                ef = d.ne[a][dc];
+            } else {
+                double sr[9], se[9], xlx[9], xly[9];
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+#pragma unroll
+                    for (int p = 0; p < 3; ++p) {
+                        const size_t s = ix(d, di + p - 1, dj + q - 1);
+                        sr[p * 3 + q] = d.rho[a][s];
+                        se[p * 3 + q] = d.ne[a][s];
+                        xlx[p * 3 + q] = d.xl2x[s];
+                        xly[p * 3 + q] = d.xl2y[s];
+                    }
+                rf = rmax(corner_diag(d, sr, xlx, xly, ddx, ddy, lwx, lwy, bad), 0.0);
+                ef = corner_diag(d, se, xlx, xly, ddx, ddy, lwx, lwy, bad);
+            }
+            rfv[a] = rf;
+            efv[a] = ef;
+        }
+        if (bad) raise(d.ctl, ekey(PH_GRAD_CORNER, j, i, 0));
+    }
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        double dm = 0.0, dme = 0.0;
+        if (dva[a] != 0.0) {
+            dm = rfv[a] * dva[a];
+            dme = rfv[a] * efv[a] * dva[a];
+            dmtot += dm;
+        }
+        d.fcm[a][n] = dm;
+        d.fcme[a][n] = dme;
+        d.fcva[a][n] = dva[a];
+    }
+    d.dmc[n] = dmtot;
+}
+
+// fill_face_flux_ghosts (remap.cpp:371-382) for dmx / dmy and the dmc ghost
+// rows (:985-988).  Every write reads interior entries only.
+__global__ void k_flux_ghosts(Dev d) {
+    if (halted(d.ctl)) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nx = d.nx, ny = d.ny;
+    // dmx: along = x (na = nx), cross = y (nc = ny); (ia, ic) at (i, j)
+    auto dmx_c = [&](int ia, int ic) -> double {  // value incl. cross ghosts
+        if (ic == -1) return d.per_y ? d.dmx[ix(d, ia, ny - 1)] : d.dmx[ix(d, ia, 0)];
+        if (ic == ny) return d.per_y ? d.dmx[ix(d, ia, 0)] : d.dmx[ix(d, ia, ny - 1)];
+        return d.dmx[ix(d, ia, ic)];
+    };
+    // dmy: along = y (na = ny), cross = x (nc = nx); (ia, ic) at (ic, ia)
+    auto dmy_c = [&](int ia, int ic) -> double {
+        if (ic == -1) return d.per_x ? d.dmy[ix(d, nx - 1, ia)] : d.dmy[ix(d, 0, ia)];
+        if (ic == nx) return d.per_x ? d.dmy[ix(d, 0, ia)] : d.dmy[ix(d, nx - 1, ia)];
+        return d.dmy[ix(d, ic, ia)];
+    };
+    auto dmc_r = [&](int i, int j) -> double {  // dmc incl. the j = -1 ghost row
+        if (j == -1) return d.per_y ? d.dmc[ix(d, i, ny - 1)] : d.dmc[ix(d, i, 1)];
+        return d.dmc[ix(d, i, j)];
+    };
+    if (t <= nx) {  // dmx cross ghosts at ia = t
+        d.dmx[ix(d, t, -1)] = dmx_c(t, -1);
+        d.dmx[ix(d, t, ny)] = dmx_c(t, ny);
+        d.dmc[ix(d, t, -1)] = dmc_r(t, -1);
+    }
+    if (t <= ny) {  // dmy cross ghosts at ia = t
+        d.dmy[ix(d, -1, t)] = dmy_c(t, -1);
+        d.dmy[ix(d, nx, t)] = dmy_c(t, nx);
+    }
+    if (t <= ny + 1) {  // dmx along ghost (-1, ic), ic in [-1, ny]
+        const int ic = t - 1;
+        d.dmx[ix(d, -1, ic)] = d.per_x ? dmx_c(nx - 1, ic) : -dmx_c(1, ic);
+        d.dmc[ix(d, -1, ic)] = d.per_x ? dmc_r(nx - 1, ic) : dmc_r(1, ic);
+    }
+    if (t <= nx + 1) {  // dmy along ghost (ia = -1, ic) at (ic, -1), ic in [-1, nx]
+        const int ic = t - 1;
+        d.dmy[ix(d, ic, -1)] = d.per_y ? dmy_c(ny - 1, ic) : -dmy_c(1, ic);
+    }
+}
+
+// Gather of the face and corner contributions in reference order
+// (remap.cpp:849-983, App. C item 3) followed by the per-cell part of
+// finalize_cells (remap.cpp:154-192).
+template <int NM>
+__global__ void k_gather_finalize(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    if (i >= d.nx || j >= d.ny) return;
+    const size_t c = ix(d, i, j);
+    const size_t fxr = ix(d, i + 1, j), fyt = ix(d, i, j + 1);
+    const size_t nd[4] = {c, ix(d, i + 1, j), ix(d, i, j + 1), ix(d, i + 1, j + 1)};
+    const int ndi[4] = {i, i + 1, i, i + 1}, ndj[4] = {j, j, j + 1, j + 1};
+    const double vl = d.vlag[c];
+    double m[2], me[2], va[2];
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        double mm = d.nm[a][c], mme = d.me[a][c], vv = d.nk[a][c] * vl;
+        if (d.fxva[a][c] != 0.0) {
+            mm += d.fxm[a][c];
+            mme += d.fxme[a][c];
+            vv += d.fxva[a][c];
+        }
+        if (d.fxva[a][fxr] != 0.0) {
+            mm += -d.fxm[a][fxr];
+            mme += -d.fxme[a][fxr];
+            vv += -d.fxva[a][fxr];
+        }
+        if (d.fyva[a][c] != 0.0) {
+            mm += d.fym[a][c];
+            mme += d.fyme[a][c];
+            vv += d.fyva[a][c];
+        }
+        if (d.fyva[a][fyt] != 0.0) {
+            mm += -d.fym[a][fyt];
+            mme += -d.fyme[a][fyt];
+            vv += -d.fyva[a][fyt];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const size_t n = nd[q];
+            const double dv = d.fcva[a][n];
+            if (dv == 0.0) continue;
+            const int sx = d.cf_sx[n], sy = d.cf_sy[n];
+            const int di = sx > 0 ? ndi[q] - 1 : ndi[q], dj = sy > 0 ? ndj[q] - 1 : ndj[q];
+            if (di == i && dj == j) {
+                mm += -d.fcm[a][n];
+                mme += -d.fcme[a][n];
+                vv += -dv;
+            } else {
+                const int ri = sx > 0 ? ndi[q] : ndi[q] - 1, rj = sy > 0 ? ndj[q] : ndj[q] - 1;
+                if (ri == i && rj == j) {
+                    mm += d.fcm[a][n];
+                    mme += d.fcme[a][n];
+                    vv += dv;
+                }
+            }
+        }
+        m[a] = mm;
+        me[a] = mme;
+        va[a] = vv;
+    }
+    // finalize_cells, per-cell part
+    const double cv = d.cv;
+    double k[2] = {1.0, 0.0};
+    uint8_t sl = 0;
+    if (NM == 2) {
+        double k0 = va[0] / cv;
+        const double k1 = va[1] / cv;
+        double viol = 0.0;
+        const double cand[5] = {-k0, k0 - 1.0, -k1, k1 - 1.0, fabs(k0 + k1 - 1.0)};
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+            if (viol < cand[q]) viol = cand[q];
+        if (viol > 0.0) atomicMax(&d.ctl->kviol_bits, (unsigned long long)__double_as_longlong(viol));
+        if (k0 < 0.0 || k0 > 1.0) {
+            atomicAdd(&d.ctl->step_clip, 1);
+            k0 = (k0 < 0.0) ? 0.0 : ((1.0 < k0) ? 1.0 : k0);
+        }
+        if (k0 < kPureTol) k0 = 0.0;
+        if (k0 > 1.0 - kPureTol) k0 = 1.0;
+        k[0] = k0;
+        k[1] = 1.0 - k0;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            if ((k[a] == 0.0 && m[a] != 0.0) || m[a] < 0.0) {
+                sl |= (uint8_t)(1u << a);
+                d.slm[a][c] = m[a];
+                d.slme[a][c] = me[a];
+                m[a] = 0.0;
+                me[a] = 0.0;
+                if (k[a] > 0.0) {
+                    k[a] = 0.0;
+                    k[1 - a] = 1.0;
+                }
+            }
+        }
+        d.nk[0][c] = k[0];
+        d.nk[1][c] = k[1];
+    }
+    double mtot = 0.0;
+    int bad_sub = -1;
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        const double ma = m[a];
+        if (ma < 0.0 && bad_sub < 0) bad_sub = a;
+        d.nm[a][c] = ma;
+        d.me[a][c] = me[a];
+        d.ne[a][c] = ma > 0.0 ? me[a] / ma : 0.0;
+        mtot += ma;
+    }
+    if (bad_sub < 0 && mtot <= 0.0) bad_sub = 2;
+    if (bad_sub >= 0) raise(d.ctl, ekey(PH_NEGMASS, j, i, bad_sub));
+    d.mcell[c] = mtot;
+    if (NM == 2) {
+        d.sliver[c] = sl;
+        if (sl) atomicAdd(&d.row_slivers[j], 1);
+    }
+}
+
+// Sequential sliver redistribution (remap.cpp:194-226) in row-major order by
+// one warp: rows with pending slivers are scanned 32 cells at a time.
+__global__ void k_slivers(Dev d) {
+    if (halted(d.ctl)) return;
+    const int lane = threadIdx.x;
+    const int nx = d.nx, ny = d.ny;
+    for (int j0 = 0; j0 < ny; j0 += 32) {
+        const int jr = j0 + lane;
+        const int cnt = jr < ny ? d.row_slivers[jr] : 0;
+        unsigned rows = __ballot_sync(0xffffffffu, cnt != 0);
+        while (rows) {
+            const int r = __ffs(rows) - 1;
+            rows &= rows - 1;
+            const int j = j0 + r;
+            for (int i0 = 0; i0 < nx; i0 += 32) {
+                const int ic = i0 + lane;
+                const uint8_t f = ic < nx ? d.sliver[ix(d, ic, j)] : 0;
+                unsigned cells = __ballot_sync(0xffffffffu, f != 0);
+                while (cells) {
+                    const int b = __ffs(cells) - 1;
+                    cells &= cells - 1;
+                    if (lane == 0) {
+                        const int si = i0 + b, sj = j;
+                        const size_t sc = ix(d, si, sj);
+                        const uint8_t fl = d.sliver[sc];
+                        for (int a = 0; a < 2; ++a) {
+                            if (!(fl & (1u << a))) continue;
+                            const double smv = d.slm[a][sc], smev = d.slme[a][sc];
+                            int bi = -1, bj = -1;
+                            double bk = -1.0;
+                            for (int rr = 1; rr <= 2 && bi < 0; ++rr)
+                                for (int dj = -rr; dj <= rr; ++dj)
+                                    for (int di = -rr; di <= rr; ++di) {
+                                        const int adi = di < 0 ? -di : di, adj = dj < 0 ? -dj : dj;
+                                        if ((adi < adj ? adj : adi) != rr) continue;
+                                        int ni = si + di, nj = sj + dj;
+                                        if (d.per_x) ni = (ni + 2 * nx) % nx;
+                                        if (d.per_y) nj = (nj + 2 * ny) % ny;
+                                        if (ni < 0 || ni >= nx || nj < 0 || nj >= ny) continue;
+                                        const size_t nc = ix(d, ni, nj);
+                                        if (d.nm[a][nc] <= 0.0) continue;
+                                        if (d.nk[a][nc] > bk) {
+                                            bk = d.nk[a][nc];
+                                            bi = ni;
+                                            bj = nj;
+                                        }
+                                    }
+                            if (bi >= 0 && d.nm[a][ix(d, bi, bj)] + smv > 0.0) {
+                                const size_t bc = ix(d, bi, bj);
+                                d.nm[a][bc] += smv;
+                                d.me[a][bc] += smev;
+                                d.ne[a][bc] = d.me[a][bc] / d.nm[a][bc];
+                                d.mcell[bc] += smv;
+                            } else {
+                                d.ctl->step_fix += 1;
+                                const int bm = 1 - a;
+                                d.nm[bm][sc] += smv;
+                                d.me[bm][sc] += smev;
+                                d.ne[bm][sc] = d.me[bm][sc] / d.nm[bm][sc];
+                                d.mcell[sc] += smv;
+                            }
+                        }
+                        d.sliver[sc] = 0;
+                    }
+                    __syncwarp();
+                }
+            }
+            if (lane == 0) d.row_slivers[j] = 0;
+            __syncwarp();
+        }
+    }
+}
+
+// dual_face_value, remap.cpp:384-404 for node velocities w.u (= u_lag)
+__device__ __forceinline__ double dual_face_value(const Dev& d, const double* u, int ax, int ia_d, int ic, double dt,
+                                                  double wa, double sgn, double ufdt, bool& bad) {
+    auto at = [&](int ia) { return ax ? ix(d, ia, ic) : ix(d, ic, ia); };
+    if (d.face_order <= 1) return u[at(ia_d)];
+    const double* uh = ax ? d.uhx : d.uhy;
+    const double nm1 = uh[at(ia_d - 1)] * dt, n0 = uh[at(ia_d)] * dt, np1 = uh[at(ia_d + 1)] * dt;
+    const double x0 = (ia_d - 1) * wa + nm1, x1 = ia_d * wa + n0, x2 = (ia_d + 1) * wa + np1;
+    const double dfl = 0.5 * (nm1 + n0), dfr = 0.5 * (n0 + np1);
+    return face_value2(u[at(ia_d - 1)], u[at(ia_d)], u[at(ia_d + 1)], x0, x1, x2, sgn, wa + (dfr - dfl), ufdt, bad);
+}
+
+// dual_face_pass, remap.cpp:408-442: one thread per dual face. AX = 1: X
+// (ia = i node, ic = j), AX = 0: Y (ia = j, ic = i); stored at (i, j).
+template <int AX>
+__global__ void k_dual_faces(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    const int iend = d.per_x ? d.nx - 1 : d.nx, jend = d.per_y ? d.ny - 1 : d.ny;
+    if (i > iend || j > jend) return;
+    const int ia = AX ? i : j, ic = AX ? j : i;
+    const int per_a = AX ? d.per_x : d.per_y;
+    const size_t s = ix(d, i, j);
+    double* ox = AX ? d.dfx_x : d.dfy_x;
+    double* oy = AX ? d.dfx_y : d.dfy_y;
+    if (ia < (per_a ? 0 : 1)) {
+        ox[s] = 0.0;
+        oy[s] = 0.0;
+        d.dflag[AX ? 0 : 1][s] = 0;
+        return;
+    }
+    const double* dmf = AX ? d.dmx : d.dmy;
+    auto F = [&](int a, int c) { return dmf[AX ? ix(d, a, c) : ix(d, c, a)]; };
+    const double dm = 0.25 * ((F(ia - 1, ic - 1) + F(ia - 1, ic)) + (F(ia, ic - 1) + F(ia, ic)));
+    double mx = 0.0, my = 0.0;
+    if (dm != 0.0) {
+        const double dt = d.ctl->dt;
+        const int ia_d = dm > 0.0 ? ia - 1 : ia;
+        const double sgn = dm > 0.0 ? 1.0 : -1.0;
+        const double* uh = AX ? d.uhx : d.uhy;
+        const double ufdt = 0.5 * (uh[AX ? ix(d, ia - 1, ic) : ix(d, ic, ia - 1)] * dt + uh[s] * dt);
+        const double wa = AX ? d.dx : d.dy;
+        bool bad = false;
+        const double ufx = dual_face_value(d, d.ulx, AX, ia_d, ic, dt, wa, sgn, ufdt, bad);
+        const double ufy = dual_face_value(d, d.uly, AX, ia_d, ic, dt, wa, sgn, ufdt, bad);
+        if (bad) raise(d.ctl, ekey(AX ? PH_GRAD_DUALX : PH_GRAD_DUALY, ic, ia, 0));
+        mx = ufx * dm;
+        my = ufy * dm;
+    }
+    ox[s] = mx;
+    oy[s] = my;
+    d.dflag[AX ? 0 : 1][s] = dm != 0.0;  // a zero dual mass flux is skipped (remap.cpp:423)
+}
+
+// Dual-mesh corner exchanges, remap.cpp:1000-1069: thread per (i, j), both
+// pairs (1,1) and (1,-1).
+__global__ void k_dual_corners(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    const int nx = d.nx, ny = d.ny;
+    const int iuniq = d.per_x ? nx - 1 : nx, juniq = d.per_y ? ny - 1 : ny;
+    if (i > iuniq || j > juniq) return;
+    const double dt = d.ctl->dt;
+    const size_t s = ix(d, i, j);
+#pragma unroll
+    for (int pr = 0; pr < 2; ++pr) {
+        const int sx = 1, sy = pr == 0 ? 1 : -1;
+        const int pi = i + sx, pj = j + sy;
+        double cx = 0.0, cy = 0.0;
+        bool active = true;
+        if (!d.per_x && (pi < 0 || pi > nx)) active = false;
+        if (!d.per_y && (pj < 0 || pj > ny)) active = false;
+        double Fv = 0.0;
+        if (active) {
+            double sc[4];
+            const int qi[4] = {i, i + sx, i, i + sx}, qj[4] = {j, j, j + sy, j + sy};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const size_t n = ix(d, qi[q], qj[q]);
+                const double cdv = d.cf_dv[n], dmcv = d.dmc[n];
+                const int csx = d.cf_sx[n], csy = d.cf_sy[n];
+                sc[q] = 0.0;
+                if (cdv == 0.0 || dmcv == 0.0) continue;
+                if (csx == sx && csy == sy)
+                    sc[q] = -dmcv;
+                else if (csx == -sx && csy == -sy)
+                    sc[q] = dmcv;
+            }
+            Fv = 0.25 * (sc[0] + sc[1] + sc[2] + sc[3]);
+            if (Fv == 0.0) active = false;
+        }
+        if (active) {
+            const bool incoming = Fv > 0.0;
+            const int di = incoming ? pi : i, dj = incoming ? pj : j;
+            const int wi = d.per_x ? ((di % nx) + nx) % nx : di;
+            const int wj = d.per_y ? ((dj % ny) + ny) % ny : dj;
+            double ufx, ufy;
+            if (!(d.corner_diag && d.face_order > 1)) {
+                ufx = d.ulx[ix(d, wi, wj)];
+                ufy = d.uly[ix(d, wi, wj)];
+            } else {
+                const int ci0 = i < pi ? i : pi, cj0 = j < pj ? j : pj;
+                const int ci = d.per_x ? ((ci0 % nx) + nx) % nx : ci0;
+                const int cj = d.per_y ? ((cj0 % ny) + ny) % ny : cj0;
+                const size_t cc = ix(d, ci, cj);
+                const double mdx = d.xl2x[cc] - (d.x0 + (ci + 0.5) * d.dx);
+                const double mdy = d.xl2y[cc] - (d.y0 + (cj + 0.5) * d.dy);
+                const double dirx = incoming ? -sx : sx, diry = incoming ? -sy : sy;
+                const double dxp = dirx * rmax(fabs(mdx), 1e-300);
+                const double dyp = diry * rmax(fabs(mdy), 1e-300);
+                const double lwx = d.dx + 0.5 * (dt * d.uhx[ix(d, wi + 1, wj)] - dt * d.uhx[ix(d, wi - 1, wj)]);
+                const double lwy = d.dy + 0.5 * (dt * d.uhy[ix(d, wi, wj + 1)] - dt * d.uhy[ix(d, wi, wj - 1)]);
+                double ax_[9], ay_[9], xlx[9], xly[9];
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+#pragma unroll
+                    for (int p = 0; p < 3; ++p) {
+                        const int ni = wi + p - 1, nj = wj + q - 1;
+                        const size_t nn = ix(d, ni, nj);
+                        ax_[p * 3 + q] = d.ulx[nn];
+                        ay_[p * 3 + q] = d.uly[nn];
+                        xlx[p * 3 + q] = (d.x0 + ni * d.dx) + dt * d.uhx[nn];
+                        xly[p * 3 + q] = (d.y0 + nj * d.dy) + dt * d.uhy[nn];
+                    }
+                bool bad = false;
+                ufx = corner_diag(d, ax_, xlx, xly, dxp, dyp, lwx, lwy, bad);
+                ufy = corner_diag(d, ay_, xlx, xly, dxp, dyp, lwx, lwy, bad);
+                if (bad) raise(d.ctl, ekey(PH_GRAD_DUALC, j, i, pr));
+            }
+            cx = ufx * Fv;
+            cy = ufy * Fv;
+        }
+        d.dc_x[pr][s] = cx;
+        d.dc_y[pr][s] = cy;
+        d.dflag[2 + pr][s] = active;
+    }
+}
+
+// MomAcc gather (App. C item 4) + apply_dual_update (remap.cpp:444-464) with
+// the periodic copies (:458-461) folded in: thread per node (i, j) in
+// [0, nx] x [0, ny] computes the value of its source node.
+__global__ void k_node_update(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    const int nx = d.nx, ny = d.ny;
+    if (i > nx || j > ny) return;
+    const int iend = d.per_x ? nx - 1 : nx, jend = d.per_y ? ny - 1 : ny;
+    const int si = (d.per_x && i == nx) ? 0 : i, sj = (d.per_y && j == ny) ? 0 : j;
+    const size_t s = ix(d, si, sj);
+    double ax = 0.0, ay = 0.0;
+    // X then Y dual faces (remap.cpp:995-996). Face ia joins nodes (ia-1, ia):
+    // + to node ia, - to the node ia-1 wraps to; applied in face-loop order.
+    auto faces = [&](int ax_, int along, int cross) {
+        const int n = ax_ ? nx : ny;
+        const int per = ax_ ? d.per_x : d.per_y;
+        const int hi = ax_ ? iend : jend, lo = per ? 0 : 1;
+        const double* fx_ = ax_ ? d.dfx_x : d.dfy_x;
+        const double* fy_ = ax_ ? d.dfx_y : d.dfy_y;
+        const uint8_t* fl = d.dflag[ax_ ? 0 : 1];
+        auto at = [&](int a) { return ax_ ? ix(d, a, cross) : ix(d, cross, a); };
+        int am = along + 1;
+        if (per && am == n) am = 0;
+        const bool ap = along >= lo && along <= hi && fl[at(along)];
+        const bool an = am >= lo && am <= hi && fl[at(am)];
+        const bool minus_first = an && am < along;
+        if (minus_first) {
+            ax += -fx_[at(am)];
+            ay += -fy_[at(am)];
+        }
+        if (ap) {
+            ax += fx_[at(along)];
+            ay += fy_[at(along)];
+        }
+        if (an && !minus_first) {
+            ax += -fx_[at(am)];
+            ay += -fy_[at(am)];
+        }
+    };
+    faces(1, si, sj);
+    faces(0, sj, si);
+    {  // dual corners: up to 4 contributions, applied in (j, i, pair) loop order
+        const int iuniq = iend, juniq = jend;
+        long long tk[4];
+        double cx[4], cy[4];
+        int nc = 0;
+        auto push = [&](int ii, int jj, int pr, double sgn) {
+            if (ii < 0 || ii > iuniq || jj < 0 || jj > juniq) return;
+            const size_t q = ix(d, ii, jj);
+            if (!d.dflag[2 + pr][q]) return;
+            tk[nc] = ((long long)jj * (iuniq + 1) + ii) * 2 + pr;
+            cx[nc] = sgn > 0 ? d.dc_x[pr][q] : -d.dc_x[pr][q];
+            cy[nc] = sgn > 0 ? d.dc_y[pr][q] : -d.dc_y[pr][q];
+            ++nc;
+        };
+        // partner index of pair (1, +-1) whose target wraps to (si, sj)
+        int ip = si - 1, jp1 = sj - 1, jp2 = sj + 1;
+        if (d.per_x && ip < 0) ip += nx;
+        if (d.per_y) {
+            if (jp1 < 0) jp1 += ny;
+            if (jp2 >= ny) jp2 -= ny;
+        }
+        if (si <= iuniq && sj <= juniq) {
+            push(si, sj, 0, 1.0);
+            push(si, sj, 1, 1.0);
+        }
+        push(ip, jp1, 0, -1.0);
+        push(ip, jp2, 1, -1.0);
+        // insertion sort by loop time (n <= 4)
+        for (int a = 1; a < nc; ++a)
+            for (int b = a; b > 0 && tk[b - 1] > tk[b]; --b) {
+                long long t0 = tk[b];
+                tk[b] = tk[b - 1];
+                tk[b - 1] = t0;
+                double v = cx[b];
+                cx[b] = cx[b - 1];
+                cx[b - 1] = v;
+                v = cy[b];
+                cy[b] = cy[b - 1];
+                cy[b - 1] = v;
+            }
+        for (int a = 0; a < nc; ++a) {
+            ax += cx[a];
+            ay += cy[a];
+        }
+    }
+    const double mp_lag = 0.25 * (d.mcell_lag[ix(d, si - 1, sj - 1)] + d.mcell_lag[ix(d, si, sj - 1)] +
+                                  d.mcell_lag[ix(d, si - 1, sj)] + d.mcell_lag[s]);
+    const double mp_new =
+        0.25 * (d.mcell[ix(d, si - 1, sj - 1)] + d.mcell[ix(d, si, sj - 1)] + d.mcell[ix(d, si - 1, sj)] + d.mcell[s]);
+    if (mp_new <= 0.0 && si == i && sj == j) raise(d.ctl, ekey(PH_NODAL_MASS, j, i, 0));
+    const double inv = 1.0 / mp_new;
+    const size_t o = ix(d, i, j);
+    d.nux[o] = inv * (mp_lag * d.ulx[s] + ax);
+    d.nuy[o] = inv * (mp_lag * d.uly[s] + ay);
+}
+
+// refresh_normals_impl + youngs_normal (remap.cpp:102-114, vof.cpp:10-22)
+// on the next state's fractions; `api` = operate on the current state.
+__global__ void k_normals(Dev d, int api) {
+    if (!api && halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    if (i >= d.nx || j >= d.ny) return;
+    const double* k0 = api ? d.k[0] : d.nk[0];
+    const double* k1 = api ? d.k[1] : d.nk[1];
+    double* nx_ = api ? const_cast<double*>(d.nrx) : d.nnrx;
+    double* ny_ = api ? const_cast<double*>(d.nry) : d.nnry;
+    const size_t c = ix(d, i, j);
+    if (!is_mixed(k0[c])) return;
+    auto K = [&](int ii, int jj) { return k1[ix(d, ii, jj)]; };
+    auto col = [&](int ii) { return K(ii, j - 1) + 2.0 * K(ii, j) + K(ii, j + 1); };
+    auto row = [&](int jj) { return K(i - 1, jj) + 2.0 * K(i, jj) + K(i + 1, jj); };
+    const double gx = (col(i + 1) - col(i - 1)) / (8.0 * d.dx);
+    const double gy = (row(j + 1) - row(j - 1)) / (8.0 * d.dy);
+    const double g = sqrt(gx * gx + gy * gy);
+    if (g < 1e-300) return;  // IsolatedMixedCellError caught: keep the previous normal
+    nx_[c] = gx / g;
+    ny_[c] = gy / g;
+}
+
+// Step commit: the remapped State becomes current (remap.cpp:1084-1085).
+__global__ void k_commit(Ctl* c, int advance) {
+    if (c->err_key != kNoErr || c->done) return;
+    if (advance) {
+        c->time = c->time + c->dt;
+        c->step += 1;
+    }
+    c->cur ^= 1;
+}
+
+// nan_scan, harness.cpp:347-358, on the committed state (the next buffers).
+__global__ void k_nan(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    if (i > d.nx || j > d.ny) return;
+    const size_t c = ix(d, i, j);
+    if (i < d.nx && j < d.ny && (!isfinite(d.nm_mix[c]) || !isfinite(d.ne_mix[c]) || !isfinite(d.np_mix[c])))
+        raise(d.ctl, ekey(PH_NAN_CELL, j, i, 0));
+    if (!isfinite(d.nux[c]) || !isfinite(d.nuy[c])) raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));
+}
+
+// End of a successful run-loop step: counters and dt log.
+__global__ void k_finish(Ctl* c) {
+    if (c->err_key != kNoErr || c->done) return;
+    if (c->dt_log && c->steps_done < c->dt_log_cap) c->dt_log[c->steps_done] = c->dt;
+    c->steps_done += 1;
+    c->floor_count += c->step_floor;
+    c->k_clip_count += c->step_clip;
+    c->mass_fix_count += c->step_fix;
+    const double v = __longlong_as_double((long long)c->kviol_bits);
+    if (v > c->max_k_violation) c->max_k_violation = v;
+}
+
+// AoS <-> SoA staging for Vec2 fields (reference layout pitch W = n1 + 2G).
+__global__ void k_deinterleave(const double* src, double* x, double* y, int W, int H, int P) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= W * H) return;
+    const int r = t / W, col = t % W;
+    x[(size_t)r * P + col] = src[2 * (size_t)t];
+    y[(size_t)r * P + col] = src[2 * (size_t)t + 1];
+}
+__global__ void k_interleave(double* dst, const double* x, const double* y, int W, int H, int P) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= W * H) return;
+    const int r = t / W, col = t % W;
+    dst[2 * (size_t)t] = x[(size_t)r * P + col];
+    dst[2 * (size_t)t + 1] = y[(size_t)r * P + col];
+}
+
+// ---------------------------------------------------------------------------
+// launch wrappers
+// ---------------------------------------------------------------------------
+static dim3 blk2() { return dim3(32, 4); }
+static dim3 grid_rect(int w, int h) {
+    const dim3 b = blk2();
+    return dim3((unsigned)((w + b.x - 1) / b.x), (unsigned)((h + b.y - 1) / b.y));
+}
+static unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
+
+void launch_begin(Ctl* c, int mode, double dt, cudaStream_t s) { k_begin<<<1, 1, 0, s>>>(c, mode, dt); }
+
+void launch_cfl(const Dev& d, int run_loop, cudaStream_t s) {
+    if (d.nmat == 2)
+        k_cfl<2><<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d);
+    else
+        k_cfl<1><<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d);
+    k_cfl_final<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy, run_loop);
+}
+
+void launch_ghost_cells(const Dev& d, const FieldList& fl, cudaStream_t s) {
+    const long long n = 2LL * G * (d.nx + 2 * G) + 2LL * G * d.ny;
+    k_ghost_cells<<<nblk(n, 256), 256, 0, s>>>(d, fl);
+}
+void launch_ghost_nodes(const Dev& d, const FieldList& fl, cudaStream_t s) {
+    const long long n = 2LL * G * (d.nx + 1 + 2 * G) + 2LL * G * (d.ny + 1) + 2LL * (d.ny + 1) + 2LL * (d.nx + 1);
+    k_ghost_nodes<<<nblk(n, 256), 256, 0, s>>>(d, fl);
+}
+
+void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s) {
+    const dim3 g = grid_rect(d.nx + 2 * G, d.ny + 2 * G);
+    if (d.nmat == 2)
+        k_sync<2><<<g, blk2(), 0, s>>>(d, next, respect_halt);
+    else
+        k_sync<1><<<g, blk2(), 0, s>>>(d, next, respect_halt);
+}
+
+void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
+    const dim3 gc = grid_rect(d.nx, d.ny), gn = grid_rect(d.nx + 1, d.ny + 1);
+    FieldList fl{};
+    fl.respect_halt = 1;
+    if (d.nmat == 2)
+        k_q<2><<<gc, blk2(), 0, s>>>(d);
+    else
+        k_q<1><<<gc, blk2(), 0, s>>>(d);
+    fl.n = 1;
+    fl.f[0] = d.q;
+    launch_ghost_cells(d, fl, s);
+    if (d.nmat == 2)
+        k_predict_cells<2><<<gc, blk2(), 0, s>>>(d);
+    else
+        k_predict_cells<1><<<gc, blk2(), 0, s>>>(d);
+    fl.n = 1 + d.nmat;
+    fl.f[0] = d.pmh;
+    fl.f[1] = d.ph[0];
+    fl.f[2] = d.ph[1];
+    launch_ghost_cells(d, fl, s);
+    k_predict_nodes<<<gn, blk2(), 0, s>>>(d);
+    fl.n = 2;
+    fl.f[0] = d.uhx;
+    fl.f[1] = d.uhy;
+    launch_ghost_nodes(d, fl, s);
+    if (d.nmat == 2)
+        k_correct<2><<<gn, blk2(), 0, s>>>(d, write_vol_lag);
+    else
+        k_correct<1><<<gn, blk2(), 0, s>>>(d, write_vol_lag);
+    fl.f[0] = d.ulx;
+    fl.f[1] = d.uly;
+    launch_ghost_nodes(d, fl, s);
+    fl.n = d.nmat;
+    fl.f[0] = d.el[0];
+    fl.f[1] = d.el[1];
+    launch_ghost_cells(d, fl, s);
+}
+
+void launch_remap(const Dev& d, cudaStream_t s) {
+    const int nx = d.nx, ny = d.ny;
+    const bool two = d.nmat == 2;
+    const dim3 gall = grid_rect(nx + 1 + 2 * G, ny + 1 + 2 * G);
+    const dim3 gcell_ext = grid_rect(nx + 2 * G, ny + 2 * G);
+    const dim3 gc = grid_rect(nx, ny), gn = grid_rect(nx + 1, ny + 1);
+    if (two)
+        k_make_work<2><<<gall, blk2(), 0, s>>>(d);
+    else
+        k_make_work<1><<<gall, blk2(), 0, s>>>(d);
+    k_geom<<<gall, blk2(), 0, s>>>(d);
+    if (two)
+        k_cells<2><<<gcell_ext, blk2(), 0, s>>>(d);
+    else
+        k_cells<1><<<gcell_ext, blk2(), 0, s>>>(d);
+    if (two) {
+        k_faces<2, 1><<<gn, blk2(), 0, s>>>(d);
+        k_faces<2, 0><<<gn, blk2(), 0, s>>>(d);
+        k_corners<2><<<gn, blk2(), 0, s>>>(d);
+    } else {
+        k_faces<1, 1><<<gn, blk2(), 0, s>>>(d);
+        k_faces<1, 0><<<gn, blk2(), 0, s>>>(d);
+        k_corners<1><<<gn, blk2(), 0, s>>>(d);
+    }
+    k_flux_ghosts<<<nblk((nx > ny ? nx : ny) + 2, 256), 256, 0, s>>>(d);
+    if (two) {
+        k_gather_finalize<2><<<gc, blk2(), 0, s>>>(d);
+        k_slivers<<<1, 32, 0, s>>>(d);
+    } else {
+        k_gather_finalize<1><<<gc, blk2(), 0, s>>>(d);
+    }
+    FieldList fl{};
+    fl.respect_halt = 1;
+    int q = 0;
+    for (int a = 0; a < d.nmat; ++a) {
+        fl.f[q++] = d.nm[a];
+        fl.f[q++] = d.me[a];
+        fl.f[q++] = d.ne[a];
+        fl.f[q++] = d.nk[a];
+    }
+    fl.f[q++] = d.mcell;
+    fl.n = q;
+    launch_ghost_cells(d, fl, s);
+    if (d.remap_velocity) {
+        k_dual_faces<1><<<gn, blk2(), 0, s>>>(d);
+        k_dual_faces<0><<<gn, blk2(), 0, s>>>(d);
+        k_dual_corners<<<gn, blk2(), 0, s>>>(d);
+        k_node_update<<<gn, blk2(), 0, s>>>(d);
+        FieldList fu{};
+        fu.respect_halt = 1;
+        fu.n = 2;
+        fu.f[0] = d.nux;
+        fu.f[1] = d.nuy;
+        launch_ghost_nodes(d, fu, s);
+    }
+    if (two) k_normals<<<gc, blk2(), 0, s>>>(d, 0);
+    // assemble_state (remap.cpp:1075-1089): fill_ghosts + sync_derived
+    FieldList fg{};
+    fg.respect_halt = 1;
+    q = 0;
+    for (int a = 0; a < d.nmat; ++a) {
+        fg.f[q++] = d.nm[a];
+        fg.f[q++] = d.ne[a];
+        fg.f[q++] = d.nk[a];
+    }
+    fg.f[q++] = d.nnrx;
+    fg.f[q++] = d.nnry;
+    fg.n = q;
+    launch_ghost_cells(d, fg, s);
+    FieldList fu{};
+    fu.respect_halt = 1;
+    fu.n = 2;
+    fu.f[0] = d.nux;
+    fu.f[1] = d.nuy;
+    launch_ghost_nodes(d, fu, s);
+    launch_sync(d, 1, 1, s);
+}
+
+void launch_commit(Ctl* c, int advance, cudaStream_t s) { k_commit<<<1, 1, 0, s>>>(c, advance); }
+
+void launch_nan_finish(const Dev& d, cudaStream_t s) {
+    k_nan<<<grid_rect(d.nx + 1, d.ny + 1), blk2(), 0, s>>>(d);
+    k_finish<<<1, 1, 0, s>>>(d.ctl);
+}
+
+void launch_normals_api(const Dev& d, cudaStream_t s) { k_normals<<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d, 1); }
+
+void launch_deinterleave(const double* src, double* x, double* y, int W, int H, int P, cudaStream_t s) {
+    k_deinterleave<<<nblk((long long)W * H, 256), 256, 0, s>>>(src, x, y, W, H, P);
+}
+void launch_interleave(double* dst, const double* x, const double* y, int W, int H, int P, cudaStream_t s) {
+    k_interleave<<<nblk((long long)W * H, 256), 256, 0, s>>>(dst, x, y, W, H, P);
+}
+}  // namespace h2d

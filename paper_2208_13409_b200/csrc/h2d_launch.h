@@ -1,0 +1,28 @@
+// h2d_launch.h — host-callable launch wrappers of h2d_kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "h2d_device.cuh"
+
+namespace h2d {
+
+struct FieldList {
+    double* f[16];
+    int n;
+    int respect_halt;
+};
+
+void launch_begin(Ctl* c, int mode, double dt, cudaStream_t s);
+void launch_cfl(const Dev& d, int run_loop, cudaStream_t s);
+void launch_ghost_cells(const Dev& d, const FieldList& fl, cudaStream_t s);
+void launch_ghost_nodes(const Dev& d, const FieldList& fl, cudaStream_t s);
+void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s);
+void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s);
+void launch_remap(const Dev& d, cudaStream_t s);
+void launch_commit(Ctl* c, int advance, cudaStream_t s);
+void launch_nan_finish(const Dev& d, cudaStream_t s);
+void launch_normals_api(const Dev& d, cudaStream_t s);
+void launch_deinterleave(const double* src, double* x, double* y, int W, int H, int P, cudaStream_t s);
+void launch_interleave(double* dst, const double* x, const double* y, int W, int H, int P, cudaStream_t s);
+
+}  // namespace h2d

@@ -1,0 +1,147 @@
+"""Parity of the CUDA product (libh2d.so, through the C-ABI) against the C
+restatement oracle, which is itself pinned to the reference
+(test_oracle_vs_reference.py).  The bar is bit-exact: every State and
+LagrangeResult byte, every dt, the mixed-cell set, the RemapDiag counters,
+floor counts and the first located error."""
+import numpy as np
+import pytest
+
+import helpers
+from paper_2208_13409_b200 import abi, cases, errors
+from paper_2208_13409_b200.abi import BC_PERIODIC, BC_WALL, CORNER_LINEARDIAG, CORNER_UPWIND, EOS_PERFECT, \
+    EOS_STIFFENED, make_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    return helpers.product_lib()
+
+
+def _pair(gpu, orc, cfg, painted):
+    return helpers.prepared(gpu, cfg, painted), helpers.prepared(orc, cfg, painted)
+
+
+def test_init_helpers(gpu, orc):
+    for case in (cases.riemann2d(40), cases.triple_point(64, 32), cases.shock_bubble(48)):
+        sg, so = _pair(gpu, orc, case.cfg, case.paint())
+        assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS) == []
+
+
+@pytest.mark.parametrize("case,steps", [
+    (cases.riemann2d(48), 100),
+    (cases.sedov(64), 120),
+    (cases.triple_point(64, 32), 700),      # aborts at the same step with the same error
+    (cases.shock_bubble(64), 40),
+])
+def test_run_loop_bitwise(gpu, orc, case, steps):
+    sg, so = _pair(gpu, orc, case.cfg, case.paint())
+    rg, eg = helpers.run_capture(sg, steps, case.cfl)
+    ro, eo = helpers.run_capture(so, steps, case.cfl)
+    assert eg == eo
+    assert rg.steps_done == ro.steps_done
+    assert np.array_equal(rg.dts, ro.dts)
+    assert rg.diag == ro.diag and rg.floor_count == ro.floor_count
+    a, b = sg.download(), so.download()
+    assert helpers.bitwise_diff(a, b, helpers.STATE_FIELDS) == []
+    assert (a.step, a.time) == (b.step, b.time)
+    assert sg.totals() == so.totals()
+
+
+CONFIGS = []
+for bcx, bcy in ((BC_PERIODIC, BC_PERIODIC), (BC_WALL, BC_WALL), (BC_PERIODIC, BC_WALL)):
+    for order, corner, degrade in ((2, CORNER_LINEARDIAG, 1), (1, CORNER_UPWIND, 1), (2, CORNER_UPWIND, 1),
+                                   (2, CORNER_LINEARDIAG, 0)):
+        CONFIGS.append((bcx, bcy, order, corner, degrade))
+
+
+@pytest.mark.parametrize("bcx,bcy,order,corner,degrade", CONFIGS)
+@pytest.mark.parametrize("kind", ["gas", "front", "blobs"])
+def test_kinematic_remap_bitwise(gpu, orc, bcx, bcy, order, corner, degrade, kind):
+    nmat = 1 if kind == "gas" else 2
+    cfg = make_config(13, 11, 1.0, 1.0, 0.25, -0.5, bcx, bcy, eos=[(EOS_PERFECT, 1.4, 0.0)] * nmat,
+                      face_order=order, corner=corner, interface_degrade=degrade)
+    seed = hash((bcx, bcy, order, corner, degrade, kind)) & 0xFFFF
+    painted = helpers.random_state(cfg, seed, kind, umax=0.25)
+    sg, so = _pair(gpu, orc, cfg, painted)
+    lag = helpers.kinematic(so.download())
+    for vel in (True, False):
+        sg2, so2 = _pair(gpu, orc, cfg, so.download())
+        sg2.set_lagrange(lag)
+        so2.set_lagrange(lag)
+        dg, do = abi.RemapDiag(), abi.RemapDiag()
+        sg2.remap_step(1.0, remap_velocity=vel, diag=dg)
+        so2.remap_step(1.0, remap_velocity=vel, diag=do)
+        assert helpers.bitwise_diff(sg2.download(), so2.download(), helpers.STATE_FIELDS) == []
+        assert (dg.max_k_violation, dg.k_clip_count, dg.mass_fix_count) == \
+               (do.max_k_violation, do.k_clip_count, do.mass_fix_count)
+
+
+@pytest.mark.parametrize("bcx,bcy", [(BC_WALL, BC_WALL), (BC_PERIODIC, BC_PERIODIC), (BC_WALL, BC_PERIODIC)])
+@pytest.mark.parametrize("kind,eos", [
+    ("gas", [(EOS_PERFECT, 1.4, 0.0)]),
+    ("blobs", [(EOS_PERFECT, 1.4, 0.0), (EOS_STIFFENED, 7.0, 0.5)]),
+    ("front", [(EOS_PERFECT, 1.5, 0.0), (EOS_PERFECT, 1.67, 0.0)]),
+])
+def test_lagrange_then_remap_bitwise(gpu, orc, bcx, bcy, kind, eos):
+    cfg = make_config(17, 12, 0.5, 0.25, 0.0, 0.0, bcx, bcy, eos=eos)
+    painted = helpers.random_state(cfg, 7, kind, umax=0.05)
+    sg, so = _pair(gpu, orc, cfg, painted)
+    for step in range(3):
+        dtg, dto = sg.cfl_dt(0.4), so.cfl_dt(0.4)
+        assert dtg == dto
+        lg, lo = sg.lagrange_step(dtg), so.lagrange_step(dto)
+        assert helpers.bitwise_diff(lg, lo, helpers.LAG_FIELDS) == []
+        assert lg.floor_count == lo.floor_count
+        sg.remap_step(dtg)
+        so.remap_step(dto)
+        assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS) == []
+
+
+def _err(s, fn):
+    try:
+        fn(s)
+    except errors.SimError as e:
+        return type(e).__name__, e.what, e.i, e.j
+    return None
+
+
+@pytest.mark.parametrize("scenario", ["cfl_face", "tangled", "unphysical", "wave"])
+def test_error_parity(gpu, orc, scenario):
+    cfg = make_config(9, 8, 1.0, 1.0, bc_x=BC_WALL, bc_y=BC_PERIODIC)
+    painted = helpers.random_state(cfg, 3, "gas", umax=0.05)
+    if scenario == "unphysical":
+        painted.e[0][4, 5] = -3.0
+    sg, so = _pair(gpu, orc, cfg, painted)
+    if scenario == "cfl_face":
+        lag = helpers.kinematic(so.download())
+        lag.u_half[..., 0] = 0.95
+        fn = lambda s: (s.set_lagrange(lag), s.remap_step(1.0))
+    elif scenario == "tangled":
+        fn = lambda s: s.lagrange_step(40.0)
+    elif scenario == "unphysical":
+        fn = lambda s: s.cfl_dt(0.3)
+    else:
+        def fn(s):
+            st = s.download()
+            st.u[:] = np.nan
+            st.e[0][:] = 0.0
+            s.upload(st)
+            s.cfl_dt(0.3)
+    eg, eo = _err(sg, fn), _err(so, fn)
+    assert eo is not None and eg == eo
+    # a failed call leaves the State untouched (value semantics)
+    assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS) == []
+
+
+def test_c1_full_size(gpu, orc):
+    """Config 1 at full size (256^2, 100 steps): every step's dt and the final
+    fields bit-identical to the oracle."""
+    case = cases.riemann2d(256)
+    sg, so = _pair(gpu, orc, case.cfg, case.paint())
+    rg, _ = helpers.run_capture(sg, case.steps, case.cfl)
+    ro, _ = helpers.run_capture(so, case.steps, case.cfl)
+    assert rg.steps_done == ro.steps_done == 100
+    assert np.array_equal(rg.dts, ro.dts)
+    assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS) == []
