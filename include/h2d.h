@@ -206,6 +206,16 @@ int h2d_run(h2d_ctx* ctx, h2d_run_args* args);
  * out = {mass, mass_mat0, mass_mat1, momentum.x, momentum.y, internal_energy}. */
 int h2d_totals(h2d_ctx* ctx, double out[6]);
 
+/* ---- benchmark support (no reference counterpart) ---------------------- */
+/* Kernels launched by this library in the calling process so far. */
+long long h2d_launch_count(void);
+/* One run-loop step (as h2d_run with max_steps = state step + 1) bracketed by
+ * CUDA events on the context's stream: ms = {cfl_dt, lagrange, remap, total}. */
+int h2d_step_timed(h2d_ctx* ctx, double cfl, double t_end, float ms[4]);
+/* Write `bytes` of scratch on the context's stream (evicts L2 between timed
+ * steps) and wait for it. */
+int h2d_flush_l2(h2d_ctx* ctx, long long bytes);
+
 /* Last error recorded on this context (kind H2D_OK if none). */
 int h2d_last_error(h2d_ctx* ctx, h2d_error* err);
 

@@ -209,6 +209,12 @@ _SIGS = {
     "totals": ([C.c_void_p, _dp], C.c_int),
     "last_error": ([C.c_void_p, C.POINTER(ErrorRec)], C.c_int),
 }
+# product-only extras (benchmark support)
+_EXTRA = {
+    "launch_count": ([], C.c_longlong),
+    "step_timed": ([C.c_void_p, C.c_double, C.c_double, C.POINTER(C.c_float)], C.c_int),
+    "flush_l2": ([C.c_void_p, C.c_longlong], C.c_int),
+}
 
 ABI_SYMBOLS = tuple(_SIGS)
 
@@ -224,6 +230,11 @@ class Library:
             f = getattr(self.dll, prefix + name)
             f.argtypes, f.restype = args, res
             self.fn[name] = f
+        for name, (args, res) in _EXTRA.items():
+            f = getattr(self.dll, prefix + name, None)
+            if f is not None:
+                f.argtypes, f.restype = args, res
+                self.fn[name] = f
         if self.fn["abi_version"]() != 1:
             raise RuntimeError(f"{path}: unexpected ABI version")
 
@@ -329,6 +340,16 @@ class Solver:
             err.partial = res
             raise err
         return res
+
+    def step_timed(self, cfl: float, t_end: float = 1e30):
+        """One run-loop step timed with CUDA events (product only): returns
+        (cfl_ms, lagrange_ms, remap_ms, total_ms)."""
+        ms = (C.c_float * 4)()
+        self._check(self.lib.fn["step_timed"](self._h, cfl, t_end, ms))
+        return tuple(ms)
+
+    def flush_l2(self, nbytes: int = 512 << 20):
+        self._check(self.lib.fn["flush_l2"](self._h, nbytes))
 
     def totals(self) -> dict:
         out = (C.c_double * 6)()

@@ -46,6 +46,9 @@ struct h2d_ctx {
     int dt_log_cap = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     bool graph_ready = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    void* flush = nullptr;
+    size_t flush_bytes = 0;
 };
 
 namespace {
@@ -178,7 +181,8 @@ int decode_error(h2d_ctx* c, bool in_run) {
     }
     std::string w = msg;
     const int i = located ? inner : -1, j = located ? outer : -1;
-    if (located) w += " at cell (" + std::to_string(i) + "," + std::to_string(j) + ")";
+    // SimError::format appends the location only for i >= 0 || j >= 0 (errors.hpp:23)
+    if (located && (i >= 0 || j >= 0)) w += " at cell (" + std::to_string(i) + "," + std::to_string(j) + ")";
     const int step = c->hctl->step;
     if (with_step) w += " step " + std::to_string(step);
     if (!in_run) in_step = 0;
@@ -226,7 +230,7 @@ int zero_plane(h2d_ctx* c, double* p) {
     return 0;
 }
 
-__global__ void k_fill(double* p, double v, size_t n) {
+__global__ void k_fill(double* p, double v, size_t n) {  // setup only
     const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (t < n) p[t] = v;
 }
@@ -275,6 +279,8 @@ void enqueue_step(h2d_ctx* c, int parity) {
 extern "C" {
 
 int h2d_abi_version(void) { return H2D_ABI_VERSION; }
+
+long long h2d_launch_count(void) { return launch_count(); }
 
 int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
     *out = nullptr;
@@ -441,6 +447,9 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
 void h2d_destroy(h2d_ctx* c) {
     if (!c) return;
     if (c->device >= 0) cudaSetDevice(c->device);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->flush) cudaFree(c->flush);
     for (auto& g : c->graph)
         if (g) cudaGraphExecDestroy(g);
     if (c->st) cudaStreamSynchronize(c->st);
@@ -729,6 +738,55 @@ int h2d_totals(h2d_ctx* c, double out[6]) {
     out[3] = px;
     out[4] = py;
     out[5] = ie;
+    return 0;
+}
+
+int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, float ms[4]) {
+    cudaSetDevice(c->device);
+    if (!c->ev[0])
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    if (int rc = ctl_reset(c)) return rc;
+    Ctl& h = *c->hctl;
+    h.t_end = t_end;
+    h.cfl = cfl;
+    h.max_steps = 0;
+    h.steps_done = 0;
+    h.dt_log = nullptr;
+    h.dt_log_cap = 0;
+    if (int rc = ctl_push(c)) return rc;
+    const Dev d = make_dev(c, c->cur, 1);
+    CK(cudaEventRecord(c->ev[0], c->st));
+    launch_begin(c->ctl, 0, 0.0, c->st);
+    launch_cfl(d, 1, c->st);
+    CK(cudaEventRecord(c->ev[1], c->st));
+    launch_lagrange(d, 0, c->st);
+    CK(cudaEventRecord(c->ev[2], c->st));
+    CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->ny, c->st));
+    launch_remap(d, c->st);
+    launch_commit(c->ctl, 1, c->st);
+    launch_nan_finish(d, c->st);
+    CK(cudaEventRecord(c->ev[3], c->st));
+    if (int rc = check_launch(c)) return rc;
+    CK(cudaEventSynchronize(c->ev[3]));
+    CK(cudaEventElapsedTime(&ms[0], c->ev[0], c->ev[1]));
+    CK(cudaEventElapsedTime(&ms[1], c->ev[1], c->ev[2]));
+    CK(cudaEventElapsedTime(&ms[2], c->ev[2], c->ev[3]));
+    CK(cudaEventElapsedTime(&ms[3], c->ev[0], c->ev[3]));
+    if (int rc = ctl_pull(c)) return rc;
+    c->cur = h.cur;
+    return decode_error(c, true);
+}
+
+int h2d_flush_l2(h2d_ctx* c, long long bytes) {
+    cudaSetDevice(c->device);
+    if ((size_t)bytes > c->flush_bytes) {
+        if (c->flush) cudaFree(c->flush);
+        c->flush = nullptr;
+        CK(cudaMalloc(&c->flush, (size_t)bytes));
+        c->flush_bytes = (size_t)bytes;
+    }
+    CK(cudaMemsetAsync(c->flush, c->flush_bytes & 0xFF, c->flush_bytes, c->st));
+    CK(cudaStreamSynchronize(c->st));
     return 0;
 }
 

@@ -12,6 +12,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 namespace h2d {
 
 // ---------------------------------------------------------------------------
@@ -1326,6 +1328,8 @@ __global__ void k_interleave(double* dst, const double* x, const double* y, int 
 // ---------------------------------------------------------------------------
 // launch wrappers
 // ---------------------------------------------------------------------------
+static std::atomic<long long> g_launches{0};
+long long launch_count() { return g_launches.load(); }
 static dim3 blk2() { return dim3(32, 4); }
 static dim3 grid_rect(int w, int h) {
     const dim3 b = blk2();
@@ -1337,27 +1341,27 @@ void launch_begin(Ctl* c, int mode, double dt, cudaStream_t s) { k_begin<<<1, 1,
 
 void launch_cfl(const Dev& d, int run_loop, cudaStream_t s) {
     if (d.nmat == 2)
-        k_cfl<2><<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d);
+        { k_cfl<2><<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d); ++g_launches; }
     else
-        k_cfl<1><<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d);
-    k_cfl_final<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy, run_loop);
+        { k_cfl<1><<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d); ++g_launches; }
+    { k_cfl_final<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy, run_loop); ++g_launches; }
 }
 
 void launch_ghost_cells(const Dev& d, const FieldList& fl, cudaStream_t s) {
     const long long n = 2LL * G * (d.nx + 2 * G) + 2LL * G * d.ny;
-    k_ghost_cells<<<nblk(n, 256), 256, 0, s>>>(d, fl);
+    { k_ghost_cells<<<nblk(n, 256), 256, 0, s>>>(d, fl); ++g_launches; }
 }
 void launch_ghost_nodes(const Dev& d, const FieldList& fl, cudaStream_t s) {
     const long long n = 2LL * G * (d.nx + 1 + 2 * G) + 2LL * G * (d.ny + 1) + 2LL * (d.ny + 1) + 2LL * (d.nx + 1);
-    k_ghost_nodes<<<nblk(n, 256), 256, 0, s>>>(d, fl);
+    { k_ghost_nodes<<<nblk(n, 256), 256, 0, s>>>(d, fl); ++g_launches; }
 }
 
 void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s) {
     const dim3 g = grid_rect(d.nx + 2 * G, d.ny + 2 * G);
     if (d.nmat == 2)
-        k_sync<2><<<g, blk2(), 0, s>>>(d, next, respect_halt);
+        { k_sync<2><<<g, blk2(), 0, s>>>(d, next, respect_halt); ++g_launches; }
     else
-        k_sync<1><<<g, blk2(), 0, s>>>(d, next, respect_halt);
+        { k_sync<1><<<g, blk2(), 0, s>>>(d, next, respect_halt); ++g_launches; }
 }
 
 void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
@@ -1365,30 +1369,30 @@ void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
     FieldList fl{};
     fl.respect_halt = 1;
     if (d.nmat == 2)
-        k_q<2><<<gc, blk2(), 0, s>>>(d);
+        { k_q<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
     else
-        k_q<1><<<gc, blk2(), 0, s>>>(d);
+        { k_q<1><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
     fl.n = 1;
     fl.f[0] = d.q;
     launch_ghost_cells(d, fl, s);
     if (d.nmat == 2)
-        k_predict_cells<2><<<gc, blk2(), 0, s>>>(d);
+        { k_predict_cells<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
     else
-        k_predict_cells<1><<<gc, blk2(), 0, s>>>(d);
+        { k_predict_cells<1><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
     fl.n = 1 + d.nmat;
     fl.f[0] = d.pmh;
     fl.f[1] = d.ph[0];
     fl.f[2] = d.ph[1];
     launch_ghost_cells(d, fl, s);
-    k_predict_nodes<<<gn, blk2(), 0, s>>>(d);
+    { k_predict_nodes<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
     fl.n = 2;
     fl.f[0] = d.uhx;
     fl.f[1] = d.uhy;
     launch_ghost_nodes(d, fl, s);
     if (d.nmat == 2)
-        k_correct<2><<<gn, blk2(), 0, s>>>(d, write_vol_lag);
+        { k_correct<2><<<gn, blk2(), 0, s>>>(d, write_vol_lag); ++g_launches; }
     else
-        k_correct<1><<<gn, blk2(), 0, s>>>(d, write_vol_lag);
+        { k_correct<1><<<gn, blk2(), 0, s>>>(d, write_vol_lag); ++g_launches; }
     fl.f[0] = d.ulx;
     fl.f[1] = d.uly;
     launch_ghost_nodes(d, fl, s);
@@ -1405,29 +1409,29 @@ void launch_remap(const Dev& d, cudaStream_t s) {
     const dim3 gcell_ext = grid_rect(nx + 2 * G, ny + 2 * G);
     const dim3 gc = grid_rect(nx, ny), gn = grid_rect(nx + 1, ny + 1);
     if (two)
-        k_make_work<2><<<gall, blk2(), 0, s>>>(d);
+        { k_make_work<2><<<gall, blk2(), 0, s>>>(d); ++g_launches; }
     else
-        k_make_work<1><<<gall, blk2(), 0, s>>>(d);
-    k_geom<<<gall, blk2(), 0, s>>>(d);
+        { k_make_work<1><<<gall, blk2(), 0, s>>>(d); ++g_launches; }
+    { k_geom<<<gall, blk2(), 0, s>>>(d); ++g_launches; }
     if (two)
-        k_cells<2><<<gcell_ext, blk2(), 0, s>>>(d);
+        { k_cells<2><<<gcell_ext, blk2(), 0, s>>>(d); ++g_launches; }
     else
-        k_cells<1><<<gcell_ext, blk2(), 0, s>>>(d);
+        { k_cells<1><<<gcell_ext, blk2(), 0, s>>>(d); ++g_launches; }
     if (two) {
-        k_faces<2, 1><<<gn, blk2(), 0, s>>>(d);
-        k_faces<2, 0><<<gn, blk2(), 0, s>>>(d);
-        k_corners<2><<<gn, blk2(), 0, s>>>(d);
+        { k_faces<2, 1><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_faces<2, 0><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_corners<2><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
     } else {
-        k_faces<1, 1><<<gn, blk2(), 0, s>>>(d);
-        k_faces<1, 0><<<gn, blk2(), 0, s>>>(d);
-        k_corners<1><<<gn, blk2(), 0, s>>>(d);
+        { k_faces<1, 1><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_faces<1, 0><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_corners<1><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
     }
-    k_flux_ghosts<<<nblk((nx > ny ? nx : ny) + 2, 256), 256, 0, s>>>(d);
+    { k_flux_ghosts<<<nblk((nx > ny ? nx : ny) + 2, 256), 256, 0, s>>>(d); ++g_launches; }
     if (two) {
-        k_gather_finalize<2><<<gc, blk2(), 0, s>>>(d);
-        k_slivers<<<1, 32, 0, s>>>(d);
+        { k_gather_finalize<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_slivers<<<1, 32, 0, s>>>(d); ++g_launches; }
     } else {
-        k_gather_finalize<1><<<gc, blk2(), 0, s>>>(d);
+        { k_gather_finalize<1><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
     }
     FieldList fl{};
     fl.respect_halt = 1;
@@ -1442,10 +1446,10 @@ void launch_remap(const Dev& d, cudaStream_t s) {
     fl.n = q;
     launch_ghost_cells(d, fl, s);
     if (d.remap_velocity) {
-        k_dual_faces<1><<<gn, blk2(), 0, s>>>(d);
-        k_dual_faces<0><<<gn, blk2(), 0, s>>>(d);
-        k_dual_corners<<<gn, blk2(), 0, s>>>(d);
-        k_node_update<<<gn, blk2(), 0, s>>>(d);
+        { k_dual_faces<1><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_dual_faces<0><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_dual_corners<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_node_update<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
         FieldList fu{};
         fu.respect_halt = 1;
         fu.n = 2;
@@ -1453,7 +1457,7 @@ void launch_remap(const Dev& d, cudaStream_t s) {
         fu.f[1] = d.nuy;
         launch_ghost_nodes(d, fu, s);
     }
-    if (two) k_normals<<<gc, blk2(), 0, s>>>(d, 0);
+    { if (two) k_normals<<<gc, blk2(), 0, s>>>(d, 0); ++g_launches; }
     // assemble_state (remap.cpp:1075-1089): fill_ghosts + sync_derived
     FieldList fg{};
     fg.respect_halt = 1;
@@ -1479,16 +1483,16 @@ void launch_remap(const Dev& d, cudaStream_t s) {
 void launch_commit(Ctl* c, int advance, cudaStream_t s) { k_commit<<<1, 1, 0, s>>>(c, advance); }
 
 void launch_nan_finish(const Dev& d, cudaStream_t s) {
-    k_nan<<<grid_rect(d.nx + 1, d.ny + 1), blk2(), 0, s>>>(d);
-    k_finish<<<1, 1, 0, s>>>(d.ctl);
+    { k_nan<<<grid_rect(d.nx + 1, d.ny + 1), blk2(), 0, s>>>(d); ++g_launches; }
+    { k_finish<<<1, 1, 0, s>>>(d.ctl); ++g_launches; }
 }
 
 void launch_normals_api(const Dev& d, cudaStream_t s) { k_normals<<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d, 1); }
 
 void launch_deinterleave(const double* src, double* x, double* y, int W, int H, int P, cudaStream_t s) {
-    k_deinterleave<<<nblk((long long)W * H, 256), 256, 0, s>>>(src, x, y, W, H, P);
+    { k_deinterleave<<<nblk((long long)W * H, 256), 256, 0, s>>>(src, x, y, W, H, P); ++g_launches; }
 }
 void launch_interleave(double* dst, const double* x, const double* y, int W, int H, int P, cudaStream_t s) {
-    k_interleave<<<nblk((long long)W * H, 256), 256, 0, s>>>(dst, x, y, W, H, P);
+    { k_interleave<<<nblk((long long)W * H, 256), 256, 0, s>>>(dst, x, y, W, H, P); ++g_launches; }
 }
 }  // namespace h2d

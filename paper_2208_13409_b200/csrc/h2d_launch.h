@@ -12,6 +12,7 @@ struct FieldList {
     int respect_halt;
 };
 
+long long launch_count();
 void launch_begin(Ctl* c, int mode, double dt, cudaStream_t s);
 void launch_cfl(const Dev& d, int run_loop, cudaStream_t s);
 void launch_ghost_cells(const Dev& d, const FieldList& fl, cudaStream_t s);
