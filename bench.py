@@ -1,0 +1,303 @@
+#!/usr/bin/env python
+"""Benchmark of one full Lagrange + DirectCF step (fp64) on B200.
+
+Product arm (default): the CUDA library through its C-ABI.  A "step" is one
+pass of the hot path over the whole mesh: cfl_dt -> lagrange_step ->
+remap_step(DirectCF) -> nan_scan (harness.cpp:390-412).  The workload is
+BASELINE.json configs[1] (Sedov point blast, 1024^2, 1 material, walls,
+CFL 0.5) with synthetic initial data painted exactly like the reference's
+init_case.  W warm-up steps, then K timed steps, each bracketed by CUDA events
+on the library's stream with an L2 flush (512 MiB write) between steps.
+
+Reference arm (--impl reference): the reference's own CPU implementation
+(oracle/_ref, compiled from /root/reference/proj) on the host, same workload,
+single thread (the reference has no threading).
+
+Prints ONE JSON line (rank 0).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "cell-updates/s per full Lagrange+remap step (fp64)"
+UNIT = "cell-updates/s"
+B_MIN = {1: 64, 2: 160}  # algorithmic bytes per cell-step
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def workload(name):
+    from paper_2208_13409_b200 import cases
+    if name == "c1":
+        return cases.riemann2d(256)
+    if name == "c2":
+        return cases.sedov(1024)
+    if name == "c3":
+        return cases.triple_point(2048, 1024)
+    if name == "c4":
+        return cases.shock_bubble(8192)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class Clocks:
+    """SM clock / throttle-reason sampler (NVML, every 5 ms) running during
+    the timed region."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index):
+        self.index, self.samples, self.reasons, self.smax = index, [], set(), None
+        self._stop = threading.Event()
+        self.t = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.nv = pynvml
+        except Exception:
+            self.nv = None
+            return
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
+
+    def _poll(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for nm, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def stop(self):
+        if self.t is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self._stop.set()
+        self.t.join()
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        pg = dist
+    return world, rank, local, pg
+
+
+def max_over_ranks(pg, value):
+    if pg is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def cpu_lib():
+    """Reference library (oracle/_ref) if built, else the C restatement."""
+    from paper_2208_13409_b200 import abi
+    ref = os.path.join(ROOT, "oracle", "_ref", "libh2d_ref.so")
+    if os.path.exists(ref):
+        return abi.Library(ref, "h2dr_"), "reference"
+    port = os.path.join(ROOT, "oracle", "libh2d_oracle.so")
+    if not os.path.exists(port):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "oracle"], check=True)
+    return abi.Library(port, "h2do_"), "port"
+
+
+def time_cpu(case, warm, steps):
+    """Wall-clock the CPU implementation on `steps` steps after `warm`."""
+    from paper_2208_13409_b200 import abi
+    lib, kind = cpu_lib()
+    s = abi.Solver(lib, case.cfg)
+    s.init_from(case.paint())
+    if warm:
+        s.run(warm, cfl=case.cfl, log_dt=False)
+    t0 = time.perf_counter()
+    r = s.run(warm + steps, cfl=case.cfl, log_dt=False)
+    dt = time.perf_counter() - t0
+    return case.cells * r.steps_done / dt, kind, r.steps_done, dt
+
+
+def pinned_state(nx, ny, nmat, cv):
+    """HostState whose arrays live in page-locked memory (torch is plumbing)."""
+    import torch
+    from paper_2208_13409_b200.abi import HostState
+    st = HostState.empty(nx, ny, nmat, cv)
+    for f in ("m", "e", "k", "vol", "m_mix", "e_mix", "rho_mix", "p_mix", "iface_normal", "u"):
+        a = getattr(st, f)
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        setattr(st, f, t.numpy())
+    st._pins = True
+    return st
+
+
+def run_product(args, world, rank, local, pg):
+    import paper_2208_13409_b200 as pkg
+    from paper_2208_13409_b200 import abi
+
+    case = workload(args.workload)
+    nmat = case.cfg.nmat
+    lib = pkg.product_library()
+    s = abi.Solver(lib, case.cfg, local)
+    painted = case.paint()
+    s.init_from(painted)
+    for _ in range(args.warmup):
+        s.step_timed(case.cfl)
+    clocks = Clocks(local)
+    barrier(pg)
+    clocks.start()
+    launches0 = lib.fn["launch_count"]()
+    tot = np.zeros(4)
+    for _ in range(args.steps):
+        s.flush_l2(512 << 20)
+        tot += np.array(s.step_timed(case.cfl))
+    launches = lib.fn["launch_count"]() - launches0
+    clk = clocks.stop()
+    barrier(pg)
+    total_s = max_over_ranks(pg, tot[3] / 1e3)
+    cells = case.cells
+    value = cells * args.steps * world / total_s
+    ms_step = total_s * 1e3 / args.steps
+    peak, peak_kind = hbm_peak()
+    achieved = B_MIN[nmat] * cells / (ms_step / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic_per_step.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                traffic = json.load(f).get(args.workload)
+        except Exception:
+            traffic = None
+
+    # end to end through the public per-step API with host (pinned) buffers:
+    # upload State -> one run-loop step -> download State, every step
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    se = abi.Solver(lib, case.cfg, local)
+    se.init_from(painted)
+    host = pinned_state(case.cfg.mesh.nx, case.cfg.mesh.ny, nmat, case.cfg.mesh.dx * case.cfg.mesh.dy)
+    st0 = se.download()
+    for f in ("m", "e", "k", "vol", "m_mix", "e_mix", "rho_mix", "p_mix", "iface_normal", "u"):
+        getattr(host, f)[...] = getattr(st0, f)
+    h2d = sum(getattr(host, f)[:nmat].nbytes if f in ("m", "e", "k") else getattr(host, f).nbytes
+              for f in ("m", "e", "k", "vol", "m_mix", "e_mix", "rho_mix", "p_mix", "iface_normal", "u"))
+    view_up = host.view(derived=True)
+    barrier(pg)
+    t0 = time.perf_counter()
+    for q in range(e2e_steps):
+        se._check(lib.fn["upload_state"](se._h, abi.C.byref(view_up)))
+        se.run(host.step + 1, cfl=case.cfl, log_dt=False)
+        v = host.view(derived=True)
+        se._check(lib.fn["download_state"](se._h, abi.C.byref(v)))
+        host.step, host.time = v.step, v.time
+        view_up = host.view(derived=True)
+    e2e_s = max_over_ranks(pg, time.perf_counter() - t0)
+    e2e_value = cells * e2e_steps * world / e2e_s
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (init_case-equivalent painter, seeded)",
+        "config": {"workload": case.name, "cells": cells, "materials": nmat, "steps_from": "t=0 after warmup",
+                   "scheme": "DirectCF face_order=2 LinearDiag interface_degrade", "cfl": case.cfl,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "512 MiB write between timed steps; working set per step >> 126 MB L2"},
+        "phases_ms": {"cfl_dt": tot[0] / args.steps, "lagrange": tot[1] / args.steps,
+                      "remap": tot[2] / args.steps},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_kind,
+                     "basis": f"whole step: {B_MIN[nmat]} B/cell-step (state read+write once) x {cells} cells"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d,
+                "steps": e2e_steps, "path": "h2d_upload_state + h2d_run(1 step) + h2d_download_state, pinned host"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, kind, n, secs = time_cpu(case, 0, args.cpu_steps)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": kind,
+                                "sample": f"{case.name}: first {n} steps from t=0, single thread, {secs:.1f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_reference(args, world, rank, pg):
+    if rank != 0:
+        return
+    case = workload(args.workload)
+    steps = args.steps
+    v, kind, n, secs = time_cpu(case, args.warmup, steps)
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": args.warmup,
+        "ms_per_step": secs * 1e3 / max(n, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (init_case-equivalent painter, seeded)", "impl": "reference",
+        "config": {"workload": case.name, "cells": case.cells, "materials": case.cfg.nmat, "cfl": case.cfl,
+                   "parallelism": "single"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": f"{case.name}: steps {args.warmup + 1}..{args.warmup + n}, single thread "
+                                   f"(the reference has no threading), {secs:.1f} s"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, pg = dist_setup(args.gpus)
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank, pg)
+        else:
+            run_product(args, world, rank, local, pg)
+    finally:
+        if pg is not None:
+            pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -57,10 +57,11 @@ __global__ void k_begin(Ctl* c, int mode, double host_dt) {
 template <int NM>
 __global__ void k_cfl(Dev d) {
     if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, 0, 0);
     unsigned long long wb = 0ull;
-    if (i < d.nx && j < d.ny) {
+    const long long ncell = (long long)d.nx * d.ny;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ncell;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(t / d.nx), i = (int)(t - (long long)j * d.nx);
         const size_t c = ix(d, i, j);
         double cs = 0.0;
         bool bad = false;
@@ -83,19 +84,22 @@ __global__ void k_cfl(Dev d) {
                 umax = rmax(umax, sqrt(ux * ux + uy * uy));
             }
         const double w = cs + umax;
-        if (w > 0.0) wb = (unsigned long long)__double_as_longlong(w);  // NaN and +-0 never raise the max
+        // NaN and +-0 never raise the max (std::max keeps its first argument)
+        if (w > 0.0) {
+            const unsigned long long b = (unsigned long long)__double_as_longlong(w);
+            wb = b > wb ? b : wb;
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long v = __shfl_xor_sync(0xffffffffu, wb, o);
         wb = v > wb ? v : wb;
     }
     __shared__ unsigned long long sw[32];
-    const int lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31;
-    const int warp = (threadIdx.y * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) sw[warp] = wb;
     __syncthreads();
     if (warp == 0) {
-        const int nw = (blockDim.x * blockDim.y + 31) >> 5;
+        const int nw = (blockDim.x + 31) >> 5;
         wb = lane < nw ? sw[lane] : 0ull;
         for (int o = 16; o > 0; o >>= 1) {
             const unsigned long long v = __shfl_xor_sync(0xffffffffu, wb, o);
@@ -1340,10 +1344,14 @@ static unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 void launch_begin(Ctl* c, int mode, double dt, cudaStream_t s) { k_begin<<<1, 1, 0, s>>>(c, mode, dt); }
 
 void launch_cfl(const Dev& d, int run_loop, cudaStream_t s) {
+    // grid-stride: a few blocks per SM, one atomic per block
+    const long long ncell = (long long)d.nx * d.ny;
+    unsigned nb = nblk(ncell, 256);
+    if (nb > 148u * 8u) nb = 148u * 8u;
     if (d.nmat == 2)
-        { k_cfl<2><<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d); ++g_launches; }
+        { k_cfl<2><<<nb, 256, 0, s>>>(d); ++g_launches; }
     else
-        { k_cfl<1><<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d); ++g_launches; }
+        { k_cfl<1><<<nb, 256, 0, s>>>(d); ++g_launches; }
     { k_cfl_final<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy, run_loop); ++g_launches; }
 }
 
