@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libh2d.so")
-SOURCES = ["h2d_kernels.cu", "h2d_capi.cu"]
+SOURCES = ["h2d_kernels.cu", "h2d_capi.cu", "hydro_api.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"]
@@ -21,9 +21,11 @@ def build(verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h"))]
     deps.append(os.path.join(HERE, "..", "include", "h2d.h"))
+    deps.append(os.path.join(HERE, "..", "include", "hydro", "b200.hpp"))
     if os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(d) for d in deps):
         return OUT
-    cmd = [NVCC, *FLAGS, "-shared", "-o", OUT + ".tmp", *srcs, "-lcudart"]
+    cmd = [NVCC, *FLAGS, "-I" + os.path.join(HERE, "..", "include"), "-shared", "-o", OUT + ".tmp", *srcs,
+           "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
