@@ -370,15 +370,6 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
         d.el[a] = plane(c);
         d.me[a] = plane(c);
         d.rho[a] = plane(c);
-        d.fxm[a] = plane(c);
-        d.fxme[a] = plane(c);
-        d.fxva[a] = plane(c);
-        d.fym[a] = plane(c);
-        d.fyme[a] = plane(c);
-        d.fyva[a] = plane(c);
-        d.fcm[a] = plane(c);
-        d.fcme[a] = plane(c);
-        d.fcva[a] = plane(c);
         d.slm[a] = plane(c);
         d.slme[a] = plane(c);
     }

@@ -75,9 +75,14 @@ struct Ctl {
     int dt_log_cap;
 };
 
+// Every thread of a kernel reads the control block: go through the read-only
+// (L1-cached) path so the broadcast costs one L2 request per SM rather than
+// one per warp on a single L2 line.  A value that is stale within a kernel is
+// harmless (errors only need to stop later kernels).
 H2D_DEV bool halted(const Ctl* c) {
-    return *(volatile const int*)&c->done != 0 || *(volatile const unsigned long long*)&c->err_key != kNoErr;
+    return __ldg(&c->done) != 0 || __ldg(&c->err_key) != kNoErr;
 }
+H2D_DEV double step_dt(const Ctl* c) { return __ldg(&c->dt); }
 H2D_DEV void raise(Ctl* c, uint64_t key) { atomicMin(&c->err_key, (unsigned long long)key); }
 
 // Per-launch constants and field pointers.  Every field is a (P x R) array of
@@ -103,9 +108,6 @@ struct Dev {
     double *fx_dv, *fx_lo, *fx_hi, *fy_dv, *fy_lo, *fy_hi, *cf_dv;
     int8_t *cf_sx, *cf_sy;
     double *vlag, *rho[2], *xl2x, *xl2y, *ifd;
-    double *fxm[2], *fxme[2], *fxva[2];  // X-face per-material dm, dme, dva
-    double *fym[2], *fyme[2], *fyva[2];
-    double *fcm[2], *fcme[2], *fcva[2];  // corner per-material
     double *dmx, *dmy, *dmc;
     double *dfx_x, *dfx_y, *dfy_x, *dfy_y;  // dual-face momentum contributions
     double *dc_x[2], *dc_y[2];              // dual-corner contributions per pair

@@ -277,49 +277,14 @@ __global__ void k_sync(Dev d, int next, int respect_halt) {
 // ---------------------------------------------------------------------------
 // Lagrangian phase (lagrange.cpp)
 // ---------------------------------------------------------------------------
-// compute_q, lagrange.cpp:63-77 (+ div_u_cell :14-20, pseudo_viscosity :7-12,
-// mixture_sound_speed :48-59)
-template <int NM>
-__global__ void k_q(Dev d) {
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, 0, 0);
-    if (i >= d.nx || j >= d.ny) return;
-    const size_t c = ix(d, i, j);
-    const size_t n00 = ix(d, i, j), n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
-    const double ux_l = 0.5 * (d.ux[n00] + d.ux[n01]);
-    const double ux_r = 0.5 * (d.ux[n10] + d.ux[n11]);
-    const double uy_b = 0.5 * (d.uy[n00] + d.uy[n10]);
-    const double uy_t = 0.5 * (d.uy[n01] + d.uy[n11]);
-    const double div = (ux_r - ux_l) / d.dx + (uy_t - uy_b) / d.dy;
-    double q = 0.0;
-    if (!(div >= 0.0)) {
-        double cs = 0.0;
-        bool bad = false;
-#pragma unroll
-        for (int a = 0; a < NM; ++a) {
-            const double ka = d.k[a][c];
-            if (ka < kThermoTol) continue;
-            const double rho_a = d.m[a][c] / (ka * d.cv);
-            const double pa = eos_p(d, a, rho_a, d.e[a][c]);
-            cs += ka * sound(d, a, rho_a, pa, bad);
-        }
-        if (bad) raise(d.ctl, ekey(PH_Q_UNPHYS, j, i, 0));
-        const double rho = d.rho_mix[c];
-        const double du = d.L * fabs(div);
-        q = rho * d.a1 * du * cs + d.a2 * rho * du * du;
-    }
-    d.q[c] = q;
-}
-
 // quad_volume_disp, lagrange.cpp:36-46, with node displacements s*u
-__device__ __forceinline__ double quad_vol(const Dev& d, const double* ux, const double* uy, double s, int i, int j,
-                                           bool& tangled) {
-    const size_t n00 = ix(d, i, j), n10 = ix(d, i + 1, j), n11 = ix(d, i + 1, j + 1), n01 = ix(d, i, j + 1);
-    const double d00x = s * ux[n00], d00y = s * uy[n00];
-    const double d10x = s * ux[n10], d10y = s * uy[n10];
-    const double d11x = s * ux[n11], d11y = s * uy[n11];
-    const double d01x = s * ux[n01], d01y = s * uy[n01];
+__device__ __forceinline__ double quad_vol4(const Dev& d, double u00x, double u00y, double u10x, double u10y,
+                                            double u11x, double u11y, double u01x, double u01y, double s,
+                                            bool& tangled) {
+    const double d00x = s * u00x, d00y = s * u00y;
+    const double d10x = s * u10x, d10y = s * u10y;
+    const double d11x = s * u11x, d11y = s * u11y;
+    const double d01x = s * u01x, d01y = s * u01y;
     const double ebx = d.dx + d10x - d00x, eby = d10y - d00y;
     const double elx = d01x - d00x, ely = d.dy + d01y - d00y;
     const double etx = d.dx + d11x - d01x, ety = d11y - d01y;
@@ -330,38 +295,72 @@ __device__ __forceinline__ double quad_vol(const Dev& d, const double* ux, const
     return s1 + s2;
 }
 
-// predict, cell part, lagrange.cpp:89-131 (dh = 0.5*dt*u, :251-255)
+// compute_q (lagrange.cpp:63-77: div_u_cell :14-20, pseudo_viscosity :7-12,
+// mixture_sound_speed :48-59) fused with the cell part of predict
+// (lagrange.cpp:89-131, dh = 0.5*dt*u :251-255): one thread per cell.
 template <int NM>
-__global__ void k_predict_cells(Dev d) {
+__global__ void k_lag_cells(Dev d) {
     if (halted(d.ctl)) return;
     int i, j;
     tid2(i, j, 0, 0);
     if (i >= d.nx || j >= d.ny) return;
-    const double dt = d.ctl->dt;
+    const double dt = step_dt(d.ctl);
     const size_t c = ix(d, i, j);
+    const size_t n00 = c, n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
+    const double u00x = d.ux[n00], u00y = d.uy[n00], u10x = d.ux[n10], u10y = d.uy[n10];
+    const double u01x = d.ux[n01], u01y = d.uy[n01], u11x = d.ux[n11], u11y = d.uy[n11];
+    double ka[2], ma[2], en[2];
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        ka[a] = d.k[a][c];
+        ma[a] = d.m[a][c];
+        en[a] = d.e[a][c];
+    }
+    // Q^n
+    const double ux_l = 0.5 * (u00x + u01x);
+    const double ux_r = 0.5 * (u10x + u11x);
+    const double uy_b = 0.5 * (u00y + u10y);
+    const double uy_t = 0.5 * (u01y + u11y);
+    const double div = (ux_r - ux_l) / d.dx + (uy_t - uy_b) / d.dy;
+    double q = 0.0;
+    if (!(div >= 0.0)) {
+        double cs = 0.0;
+        bool bad = false;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            if (ka[a] < kThermoTol) continue;
+            const double rho_a = ma[a] / (ka[a] * d.cv);
+            const double pa = eos_p(d, a, rho_a, en[a]);
+            cs += ka[a] * sound(d, a, rho_a, pa, bad);
+        }
+        if (bad) raise(d.ctl, ekey(PH_Q_UNPHYS, j, i, 0));
+        const double rho = d.rho_mix[c];
+        const double du = d.L * fabs(div);
+        q = rho * d.a1 * du * cs + d.a2 * rho * du * du;
+    }
+    d.q[c] = q;
+    // predict
     bool tangled = false;
-    const double vol = quad_vol(d, d.ux, d.uy, 0.5 * dt, i, j, tangled);
+    const double vol = quad_vol4(d, u00x, u00y, u10x, u10y, u11x, u11y, u01x, u01y, 0.5 * dt, tangled);
     if (tangled) raise(d.ctl, ekey(PH_PRED_TANGLED, j, i, 0));
     double pmix = 0.0;
     int floors = 0;
     const double cv = d.cv;
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
-        const double ka = d.k[a][c];
         double pa_h = 0.0;
-        if (!(ka < kThermoTol)) {
-            const double ma = d.m[a][c], en = d.e[a][c];
-            const double rho_n = ma / (ka * cv);
-            const double rho_h = ma / (ka * vol);
-            const double pa_n = eos_p(d, a, rho_n, en);
-            double ea = en - (pa_n + d.q[c]) * (1.0 / rho_h - 1.0 / rho_n);
-            const double efloor = 1e-8 * fabs(en);
+        if (!(ka[a] < kThermoTol)) {
+            const double rho_n = ma[a] / (ka[a] * cv);
+            const double rho_h = ma[a] / (ka[a] * vol);
+            const double pa_n = eos_p(d, a, rho_n, en[a]);
+            double ea = en[a] - (pa_n + q) * (1.0 / rho_h - 1.0 / rho_n);
+            const double efloor = 1e-8 * fabs(en[a]);
             if (ea < efloor) {
                 ea = efloor;
                 ++floors;
             }
             pa_h = eos_p(d, a, rho_h, ea);
-            pmix += ka * pa_h;
+            pmix += ka[a] * pa_h;
         }
         d.ph[a][c] = pa_h;
     }
@@ -369,46 +368,62 @@ __global__ void k_predict_cells(Dev d) {
     if (floors) atomicAdd(&d.ctl->step_floor, floors);
 }
 
-// predict, node part, lagrange.cpp:135-142 (nodal_mass state.cpp:34-36,
-// grad_pq_node lagrange.cpp:22-30)
-__global__ void k_predict_nodes(Dev d) {
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, 0, 0);
-    if (i > d.nx || j > d.ny) return;
-    const double dt = d.ctl->dt;
-    const size_t a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
-    const double mp = 0.25 * (d.m_mix[a] + d.m_mix[b] + d.m_mix[c] + d.m_mix[e]);
-    const double rho_p = mp / d.cv;
-    const double pq_a = d.pmh[a] + d.q[a], pq_b = d.pmh[b] + d.q[b];
-    const double pq_c = d.pmh[c] + d.q[c], pq_e = d.pmh[e] + d.q[e];
-    // pq(i,j-1) + pq(i,j) - pq(i-1,j-1) - pq(i-1,j)
-    const double gx = (pq_b + pq_e - pq_a - pq_c) / (2.0 * d.dx);
-    // pq(i-1,j) + pq(i,j) - pq(i-1,j-1) - pq(i,j-1)
-    const double gy = (pq_c + pq_e - pq_a - pq_b) / (2.0 * d.dy);
-    const double s = 0.5 * dt / rho_p;
-    d.uhx[e] = d.ux[e] - gx * s;
-    d.uhy[e] = d.uy[e] - gy * s;
-}
-
-// correct, lagrange.cpp:146-196; nodes: u_lag = 2 u_half - u, cells: e_lag.
+// Node part of predict (lagrange.cpp:135-142: nodal_mass state.cpp:34-36,
+// grad_pq_node lagrange.cpp:22-30) and correct (lagrange.cpp:146-196), fused
+// per 32x8 tile: u_half of the tile's (33 x 9) nodes goes to shared memory,
+// u_lag is written per node and e_lag per cell from the four u_half.
+constexpr int LTX = 32, LTY = 8;
 template <int NM>
-__global__ void k_correct(Dev d, int write_vol_lag) {
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, 0, 0);
-    if (i > d.nx || j > d.ny) return;
-    const double dt = d.ctl->dt;
-    const size_t n = ix(d, i, j);
-    d.ulx[n] = 2.0 * d.uhx[n] - d.ux[n];
-    d.uly[n] = 2.0 * d.uhy[n] - d.uy[n];
-    if (i >= d.nx || j >= d.ny) return;
+__global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_lag) {
+    constexpr int NN = (LTX + 1) * (LTY + 1);
+    __shared__ double shx[NN], shy[NN];
+    __shared__ int s_halt;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
+    const int nx = d.nx, ny = d.ny;
+    const int i0 = blockIdx.x * LTX, j0 = blockIdx.y * LTY;
+    const double dt = step_dt(d.ctl);
+    for (int t = tid; t < NN; t += LTX * LTY) {
+        const int i = i0 + t % (LTX + 1), j = j0 + t / (LTX + 1);
+        double hx = 0.0, hy = 0.0;
+        if (i <= nx && j <= ny) {
+            const size_t a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
+            const double mp = 0.25 * (d.m_mix[a] + d.m_mix[b] + d.m_mix[c] + d.m_mix[e]);
+            const double rho_p = mp / d.cv;
+            const double pq_a = d.pmh[a] + d.q[a], pq_b = d.pmh[b] + d.q[b];
+            const double pq_c = d.pmh[c] + d.q[c], pq_e = d.pmh[e] + d.q[e];
+            const double gx = (pq_b + pq_e - pq_a - pq_c) / (2.0 * d.dx);  // pq(i,j-1)+pq(i,j)-pq(i-1,j-1)-pq(i-1,j)
+            const double gy = (pq_c + pq_e - pq_a - pq_b) / (2.0 * d.dy);  // pq(i-1,j)+pq(i,j)-pq(i-1,j-1)-pq(i,j-1)
+            const double sc = 0.5 * dt / rho_p;
+            const double ux = d.ux[e], uy = d.uy[e];
+            hx = ux - gx * sc;
+            hy = uy - gy * sc;
+            if ((i < i0 + LTX || i == nx) && (j < j0 + LTY || j == ny)) {
+                d.uhx[e] = hx;
+                d.uhy[e] = hy;
+                d.ulx[e] = 2.0 * hx - ux;
+                d.uly[e] = 2.0 * hy - uy;
+            }
+        }
+        shx[t] = hx;
+        shy[t] = hy;
+    }
+    __syncthreads();
+    const int tx = tid % LTX, ty = tid / LTX;
+    const int i = i0 + tx, j = j0 + ty;
+    if (i >= nx || j >= ny) return;
+    const int q00 = tx + ty * (LTX + 1), q10 = q00 + 1, q01 = q00 + LTX + 1, q11 = q01 + 1;
     bool tangled = false;
-    const double vol = quad_vol(d, d.uhx, d.uhy, dt, i, j, tangled);
+    const double vol =
+        quad_vol4(d, shx[q00], shy[q00], shx[q10], shy[q10], shx[q11], shy[q11], shx[q01], shy[q01], dt, tangled);
     if (tangled) raise(d.ctl, ekey(PH_CORR_TANGLED, j, i, 0));
+    const size_t n = ix(d, i, j);
     if (write_vol_lag) d.vol_lag[n] = vol;
     int floors = 0;
     const double cv = d.cv;
+    const double qn = d.q[n];
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
         const double ka = d.k[a][n];
@@ -420,7 +435,7 @@ __global__ void k_correct(Dev d, int write_vol_lag) {
             const double ma = d.m[a][n];
             const double rho_n = ma / (ka * cv);
             const double rho_l = ma / (ka * vol);
-            ea = en - (d.ph[a][n] + d.q[n]) * (1.0 / rho_l - 1.0 / rho_n);
+            ea = en - (d.ph[a][n] + qn) * (1.0 / rho_l - 1.0 / rho_n);
             const double efloor = 1e-8 * fabs(en);
             if (ea < efloor) {
                 ea = efloor;
@@ -439,6 +454,11 @@ __global__ void k_correct(Dev d, int write_vol_lag) {
 // buffers become the Work arrays.
 template <int NM>
 __global__ void k_make_work(Dev d) {
+    // The Work arrays of make_work (remap.cpp:116-140) are read in place:
+    // w.m = state m, w.e = e_lag, w.k = state k, w.me = m * e_lag (recomputed
+    // where read), so flux threads never race with finalize writing the next
+    // State.  Only the lagged cell mass, the carried normals and (without the
+    // velocity remap) u are materialised here.
     if (halted(d.ctl)) return;
     int i, j;
     tid2(i, j, -G, -G);
@@ -451,14 +471,7 @@ __global__ void k_make_work(Dev d) {
     if (i >= d.nx + G || j >= d.ny + G) return;
     double mc = 0.0;
 #pragma unroll
-    for (int a = 0; a < NM; ++a) {
-        const double ma = d.m[a][c], ea = d.el[a][c];
-        d.nm[a][c] = ma;
-        d.ne[a][c] = ea;
-        d.nk[a][c] = d.k[a][c];
-        d.me[a][c] = ma * ea;
-        mc += ma;
-    }
+    for (int a = 0; a < NM; ++a) mc += d.m[a][c];
     d.mcell_lag[c] = mc;
     d.nnrx[c] = d.nrx[c];
     d.nnry[c] = d.nry[c];
@@ -495,7 +508,7 @@ __global__ void k_geom(Dev d) {
     tid2(i, j, -G, -G);
     const int nx = d.nx, ny = d.ny;
     if (i > nx + G || j > ny + G) return;
-    const double dt = d.ctl->dt;
+    const double dt = step_dt(d.ctl);
     const double cv = d.cv;
     const size_t n = ix(d, i, j);
     const double u0x = d.uhx[n], u0y = d.uhy[n];
@@ -570,7 +583,7 @@ __global__ void k_cells(Dev d) {
     int i, j;
     tid2(i, j, -G, -G);
     if (i >= d.nx + G || j >= d.ny + G) return;
-    const double dt = d.ctl->dt;
+    const double dt = step_dt(d.ctl);
     const size_t c = ix(d, i, j);
     double v = d.cv + d.fx_dv[ix(d, i + 1, j)] - d.fx_dv[c] + d.fy_dv[ix(d, i, j + 1)] - d.fy_dv[c];
     v += corner_term(d, i, j, i, j) + corner_term(d, i, j, i + 1, j) + corner_term(d, i, j, i, j + 1) +
@@ -579,8 +592,8 @@ __global__ void k_cells(Dev d) {
     d.vlag[c] = v;
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
-        const double ka = d.nk[a][c];
-        d.rho[a][c] = ka > 0.0 ? d.nm[a][c] / (ka * v) : 0.0;
+        const double ka = d.k[a][c];
+        d.rho[a][c] = ka > 0.0 ? d.m[a][c] / (ka * v) : 0.0;
     }
     const size_t n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
     const double mdx = 0.25 * (dt * d.uhx[c] + dt * d.uhx[n10] + dt * d.uhx[n01] + dt * d.uhx[n11]);
@@ -588,12 +601,12 @@ __global__ void k_cells(Dev d) {
     d.xl2x[c] = (d.x0 + (i + 0.5) * d.dx) + mdx;
     d.xl2y[c] = (d.y0 + (j + 0.5) * d.dy) + mdy;
     if (NM == 2) {
-        const double k0 = d.nk[0][c];
+        const double k0 = d.k[0][c];
         if (is_mixed(k0)) {
             const double cx = d.x0 + (i + 0.5) * d.dx, cy = d.y0 + (j + 0.5) * d.dy;
             const double lox = cx - 0.5 * d.dx + d.fdx[c], loy = cy - 0.5 * d.dy + d.fdy[c];
             const double hix = cx + 0.5 * d.dx + d.fdx[n10], hiy = cy + 0.5 * d.dy + d.fdy[n01];
-            d.ifd[c] = place_interface(k0, d.nnrx[c], d.nnry[c], lox, loy, hix, hiy);
+            d.ifd[c] = place_interface(k0, d.nrx[c], d.nry[c], lox, loy, hix, hiy);
         }
     }
 }
@@ -606,9 +619,9 @@ __device__ __forceinline__ void split_flux(const Dev& d, int di, int dj, double 
     dva[1] = 0.0;
     if (NM != 2) return;
     const size_t c = ix(d, di, dj);
-    const double k0 = d.nk[0][c];
+    const double k0 = d.k[0][c];
     if (is_mixed(k0)) {
-        const double nx = d.nnrx[c], ny = d.nnry[c], dd = d.ifd[c];
+        const double nx = d.nrx[c], ny = d.nry[c], dd = d.ifd[c];
         const double cx = d.x0 + (di + 0.5) * d.dx, cy = d.y0 + (dj + 0.5) * d.dy;
         const double lox = cx - 0.5 * d.dx + d.fdx[c], loy = cy - 0.5 * d.dy + d.fdy[c];
         const double hix = cx + 0.5 * d.dx + d.fdx[ix(d, di + 1, dj)];
@@ -635,15 +648,12 @@ __device__ __forceinline__ void split_flux(const Dev& d, int di, int dj, double 
 
 // Face fluxes, remap.cpp:850-918. AX = 1: X faces (ia = i, ic = j); AX = 0:
 // Y faces (ia = j, ic = i), both stored at device (i, j).
+// Returns the face's total mass flux (dmx / dmy entry); dm, dme, dva get the
+// per-material contributions (dva = 0 marks a skipped material).
 template <int NM, int AX>
-__global__ void k_faces(Dev d) {
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, 0, 0);
-    if (AX ? (i > d.nx || j >= d.ny) : (i >= d.nx || j > d.ny)) return;
+__device__ __forceinline__ double face_item(const Dev& d, int i, int j, double* odm, double* odme, double* odva) {
     const size_t f = ix(d, i, j);
     const double dvol = AX ? d.fx_dv[f] : d.fy_dv[f];
-    double* fm = nullptr;
     double dmtot = 0.0;
     double dva[2] = {0.0, 0.0};
     double rfv[2] = {0.0, 0.0}, efv[2] = {0.0, 0.0};
@@ -670,12 +680,12 @@ __global__ void k_faces(Dev d) {
             if (dva[a] == 0.0) continue;
             int ord = d.face_order;
             if (ord == 2 && NM == 2 && d.degrade &&
-                (d.nk[a][cm] < 1.0 - kPureTol || d.nk[a][cc] < 1.0 - kPureTol || d.nk[a][cp] < 1.0 - kPureTol))
+                (d.k[a][cm] < 1.0 - kPureTol || d.k[a][cc] < 1.0 - kPureTol || d.k[a][cp] < 1.0 - kPureTol))
                 ord = 1;
             double rf, ef;
             if (ord <= 1) {
                 rf = d.rho[a][cc];
-                ef = d.ne[a][cc];
+                ef = d.el[a][cc];
             } else {
                 const double* xl = AX ? d.xlcx : d.xlcy;
                 const double* wl = AX ? d.wlx : d.wly;
@@ -683,7 +693,7 @@ __global__ void k_faces(Dev d) {
                 const double x0 = xl[cm], x1 = xl[cc], x2 = xl[cp];
                 const double lw = wl[cc], ufdt = fd[f];
                 rf = face_value2(d.rho[a][cm], d.rho[a][cc], d.rho[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
-                ef = face_value2(d.ne[a][cm], d.ne[a][cc], d.ne[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
+                ef = face_value2(d.el[a][cm], d.el[a][cc], d.el[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
             }
             rfv[a] = rf;
             efv[a] = ef;
@@ -698,27 +708,22 @@ __global__ void k_faces(Dev d) {
             dme = rfv[a] * efv[a] * dva[a];
             dmtot += dm;
         }
-        (AX ? d.fxm : d.fym)[a][f] = dm;
-        (AX ? d.fxme : d.fyme)[a][f] = dme;
-        (AX ? d.fxva : d.fyva)[a][f] = dva[a];
+        odm[a] = dm;
+        odme[a] = dme;
+        odva[a] = dva[a];
     }
-    fm = AX ? d.dmx : d.dmy;
-    fm[f] = dmtot;
+    return dmtot;
 }
 
 // Corner fluxes, remap.cpp:923-983, per node (i, j) in [0, nx] x [0, ny].
 template <int NM>
-__global__ void k_corners(Dev d) {
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, 0, 0);
-    if (i > d.nx || j > d.ny) return;
+__device__ __forceinline__ double corner_item(const Dev& d, int i, int j, double* odm, double* odme, double* odva) {
     const size_t n = ix(d, i, j);
     const double cdv = d.cf_dv[n];
     double dva[2] = {0.0, 0.0}, rfv[2] = {0.0, 0.0}, efv[2] = {0.0, 0.0};
     double dmtot = 0.0;
     if (cdv != 0.0) {
-        const double dt = d.ctl->dt;
+        const double dt = step_dt(d.ctl);
         const int sx = d.cf_sx[n], sy = d.cf_sy[n];
         const int di = sx > 0 ? i - 1 : i, dj = sy > 0 ? j - 1 : j;
         const double npx = d.x0 + i * d.dx, npy = d.y0 + j * d.dy;
@@ -737,7 +742,7 @@ __global__ void k_corners(Dev d) {
             if (lin && NM == 2 && d.degrade) {
                 for (int q = -1; q <= 1 && lin; ++q)
                     for (int p = -1; p <= 1; ++p)
-                        if (d.nk[a][ix(d, di + p, dj + q)] < 1.0 - kPureTol) {
+                        if (d.k[a][ix(d, di + p, dj + q)] < 1.0 - kPureTol) {
                             lin = false;
                             break;
                         }
@@ -745,7 +750,7 @@ __global__ void k_corners(Dev d) {
             double rf, ef;
             if (!lin) {
                 rf = d.rho[a][dc];
-                ef = d.ne[a][dc];
+                ef = d.el[a][dc];
             } else {
                 double sr[9], se[9], xlx[9], xly[9];
 #pragma unroll
@@ -754,7 +759,7 @@ __global__ void k_corners(Dev d) {
                     for (int p = 0; p < 3; ++p) {
                         const size_t s = ix(d, di + p - 1, dj + q - 1);
                         sr[p * 3 + q] = d.rho[a][s];
-                        se[p * 3 + q] = d.ne[a][s];
+                        se[p * 3 + q] = d.el[a][s];
                         xlx[p * 3 + q] = d.xl2x[s];
                         xly[p * 3 + q] = d.xl2y[s];
                     }
@@ -774,11 +779,11 @@ __global__ void k_corners(Dev d) {
             dme = rfv[a] * efv[a] * dva[a];
             dmtot += dm;
         }
-        d.fcm[a][n] = dm;
-        d.fcme[a][n] = dme;
-        d.fcva[a][n] = dva[a];
+        odm[a] = dm;
+        odme[a] = dme;
+        odva[a] = dva[a];
     }
-    d.dmc[n] = dmtot;
+    return dmtot;
 }
 
 // fill_face_flux_ghosts (remap.cpp:371-382) for dmx / dmy and the dmc ghost
@@ -823,60 +828,123 @@ __global__ void k_flux_ghosts(Dev d) {
     }
 }
 
-// Gather of the face and corner contributions in reference order
-// (remap.cpp:849-983, App. C item 3) followed by the per-cell part of
-// finalize_cells (remap.cpp:154-192).
+// Face + corner fluxes (remap.cpp:849-983) and their gather in reference
+// order (App. C item 3), fused per 32x8 cell tile: every face / corner flux of
+// the tile (one extra column / row of faces and corners) is computed once into
+// shared memory, then each cell adds its contributions in program order and
+// runs the per-cell part of finalize_cells (remap.cpp:154-192).
+constexpr int FTX = 32, FTY = 8;
 template <int NM>
-__global__ void k_gather_finalize(Dev d) {
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, 0, 0);
-    if (i >= d.nx || j >= d.ny) return;
+__global__ void __launch_bounds__(FTX * FTY) k_flux_gather(Dev d) {
+    constexpr int NXF = (FTX + 1) * FTY, NYF = FTX * (FTY + 1), NCF = (FTX + 1) * (FTY + 1);
+    __shared__ double sxf[3][NM][NXF];
+    __shared__ double syf[3][NM][NYF];
+    __shared__ double scf[3][NM][NCF];
+    __shared__ int s_halt;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
+    const int nx = d.nx, ny = d.ny;
+    const int i0 = blockIdx.x * FTX, j0 = blockIdx.y * FTY;
+    double dm[2], dme[2], dva[2];
+    for (int t = tid; t < NXF; t += FTX * FTY) {  // X faces ia in [i0, i0+FTX], rows [j0, j0+FTY)
+        const int ia = i0 + t % (FTX + 1), ic = j0 + t / (FTX + 1);
+        dva[0] = dva[1] = 0.0;
+        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
+        if (ia <= nx && ic < ny) {
+            const double tot = face_item<NM, 1>(d, ia, ic, dm, dme, dva);
+            if (ia < i0 + FTX || ia == nx) d.dmx[ix(d, ia, ic)] = tot;
+        }
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            sxf[0][a][t] = dm[a];
+            sxf[1][a][t] = dme[a];
+            sxf[2][a][t] = dva[a];
+        }
+    }
+    for (int t = tid; t < NYF; t += FTX * FTY) {  // Y faces: columns [i0, i0+FTX), ja in [j0, j0+FTY]
+        const int ic = i0 + t % FTX, ja = j0 + t / FTX;
+        dva[0] = dva[1] = 0.0;
+        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
+        if (ic < nx && ja <= ny) {
+            const double tot = face_item<NM, 0>(d, ic, ja, dm, dme, dva);
+            if (ja < j0 + FTY || ja == ny) d.dmy[ix(d, ic, ja)] = tot;
+        }
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            syf[0][a][t] = dm[a];
+            syf[1][a][t] = dme[a];
+            syf[2][a][t] = dva[a];
+        }
+    }
+    for (int t = tid; t < NCF; t += FTX * FTY) {  // corner nodes [i0, i0+FTX] x [j0, j0+FTY]
+        const int ni = i0 + t % (FTX + 1), nj = j0 + t / (FTX + 1);
+        dva[0] = dva[1] = 0.0;
+        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
+        if (ni <= nx && nj <= ny) {
+            const double tot = corner_item<NM>(d, ni, nj, dm, dme, dva);
+            if ((ni < i0 + FTX || ni == nx) && (nj < j0 + FTY || nj == ny)) d.dmc[ix(d, ni, nj)] = tot;
+        }
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            scf[0][a][t] = dm[a];
+            scf[1][a][t] = dme[a];
+            scf[2][a][t] = dva[a];
+        }
+    }
+    __syncthreads();
+    const int tx = tid % FTX, ty = tid / FTX;
+    const int i = i0 + tx, j = j0 + ty;
+    if (i >= nx || j >= ny) return;
     const size_t c = ix(d, i, j);
-    const size_t fxr = ix(d, i + 1, j), fyt = ix(d, i, j + 1);
-    const size_t nd[4] = {c, ix(d, i + 1, j), ix(d, i, j + 1), ix(d, i + 1, j + 1)};
+    const int xl = tx + ty * (FTX + 1), xr = xl + 1;       // X faces i, i+1
+    const int yb = tx + ty * FTX, yt = yb + FTX;            // Y faces j, j+1
+    const int cq[4] = {tx + ty * (FTX + 1), tx + 1 + ty * (FTX + 1), tx + (ty + 1) * (FTX + 1),
+                       tx + 1 + (ty + 1) * (FTX + 1)};
     const int ndi[4] = {i, i + 1, i, i + 1}, ndj[4] = {j, j, j + 1, j + 1};
     const double vl = d.vlag[c];
     double m[2], me[2], va[2];
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
-        double mm = d.nm[a][c], mme = d.me[a][c], vv = d.nk[a][c] * vl;
-        if (d.fxva[a][c] != 0.0) {
-            mm += d.fxm[a][c];
-            mme += d.fxme[a][c];
-            vv += d.fxva[a][c];
+        const double m0 = d.m[a][c];
+        double mm = m0, mme = m0 * d.el[a][c], vv = d.k[a][c] * vl;
+        if (sxf[2][a][xl] != 0.0) {
+            mm += sxf[0][a][xl];
+            mme += sxf[1][a][xl];
+            vv += sxf[2][a][xl];
         }
-        if (d.fxva[a][fxr] != 0.0) {
-            mm += -d.fxm[a][fxr];
-            mme += -d.fxme[a][fxr];
-            vv += -d.fxva[a][fxr];
+        if (sxf[2][a][xr] != 0.0) {
+            mm += -sxf[0][a][xr];
+            mme += -sxf[1][a][xr];
+            vv += -sxf[2][a][xr];
         }
-        if (d.fyva[a][c] != 0.0) {
-            mm += d.fym[a][c];
-            mme += d.fyme[a][c];
-            vv += d.fyva[a][c];
+        if (syf[2][a][yb] != 0.0) {
+            mm += syf[0][a][yb];
+            mme += syf[1][a][yb];
+            vv += syf[2][a][yb];
         }
-        if (d.fyva[a][fyt] != 0.0) {
-            mm += -d.fym[a][fyt];
-            mme += -d.fyme[a][fyt];
-            vv += -d.fyva[a][fyt];
+        if (syf[2][a][yt] != 0.0) {
+            mm += -syf[0][a][yt];
+            mme += -syf[1][a][yt];
+            vv += -syf[2][a][yt];
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const size_t n = nd[q];
-            const double dv = d.fcva[a][n];
+            const double dv = scf[2][a][cq[q]];
             if (dv == 0.0) continue;
+            const size_t n = ix(d, ndi[q], ndj[q]);
             const int sx = d.cf_sx[n], sy = d.cf_sy[n];
             const int di = sx > 0 ? ndi[q] - 1 : ndi[q], dj = sy > 0 ? ndj[q] - 1 : ndj[q];
             if (di == i && dj == j) {
-                mm += -d.fcm[a][n];
-                mme += -d.fcme[a][n];
+                mm += -scf[0][a][cq[q]];
+                mme += -scf[1][a][cq[q]];
                 vv += -dv;
             } else {
                 const int ri = sx > 0 ? ndi[q] : ndi[q] - 1, rj = sy > 0 ? ndj[q] : ndj[q] - 1;
                 if (ri == i && rj == j) {
-                    mm += d.fcm[a][n];
-                    mme += d.fcme[a][n];
+                    mm += scf[0][a][cq[q]];
+                    mme += scf[1][a][cq[q]];
                     vv += dv;
                 }
             }
@@ -922,6 +990,8 @@ __global__ void k_gather_finalize(Dev d) {
         }
         d.nk[0][c] = k[0];
         d.nk[1][c] = k[1];
+    } else {
+        d.nk[0][c] = d.k[0][c];  // one material: w.k = s.k carried unchanged
     }
     double mtot = 0.0;
     int bad_sub = -1;
@@ -1053,7 +1123,7 @@ __global__ void k_dual_faces(Dev d) {
     const double dm = 0.25 * ((F(ia - 1, ic - 1) + F(ia - 1, ic)) + (F(ia, ic - 1) + F(ia, ic)));
     double mx = 0.0, my = 0.0;
     if (dm != 0.0) {
-        const double dt = d.ctl->dt;
+        const double dt = step_dt(d.ctl);
         const int ia_d = dm > 0.0 ? ia - 1 : ia;
         const double sgn = dm > 0.0 ? 1.0 : -1.0;
         const double* uh = AX ? d.uhx : d.uhy;
@@ -1080,7 +1150,7 @@ __global__ void k_dual_corners(Dev d) {
     const int nx = d.nx, ny = d.ny;
     const int iuniq = d.per_x ? nx - 1 : nx, juniq = d.per_y ? ny - 1 : ny;
     if (i > iuniq || j > juniq) return;
-    const double dt = d.ctl->dt;
+    const double dt = step_dt(d.ctl);
     const size_t s = ix(d, i, j);
 #pragma unroll
     for (int pr = 0; pr < 2; ++pr) {
@@ -1373,37 +1443,30 @@ void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s) {
 }
 
 void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
-    const dim3 gc = grid_rect(d.nx, d.ny), gn = grid_rect(d.nx + 1, d.ny + 1);
+    const dim3 gc = grid_rect(d.nx, d.ny);
+    const dim3 gl((unsigned)((d.nx + 1 + LTX - 1) / LTX), (unsigned)((d.ny + 1 + LTY - 1) / LTY));
+    if (d.nmat == 2)
+        { k_lag_cells<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
+    else
+        { k_lag_cells<1><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
     FieldList fl{};
     fl.respect_halt = 1;
-    if (d.nmat == 2)
-        { k_q<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
-    else
-        { k_q<1><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
-    fl.n = 1;
+    fl.n = 2;  // Q (lagrange.cpp:75) and p_mix_half (:132) ghosts; p_half ghosts are never read
     fl.f[0] = d.q;
+    fl.f[1] = d.pmh;
     launch_ghost_cells(d, fl, s);
     if (d.nmat == 2)
-        { k_predict_cells<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_lag_nodes<2><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag); ++g_launches; }
     else
-        { k_predict_cells<1><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
-    fl.n = 1 + d.nmat;
-    fl.f[0] = d.pmh;
-    fl.f[1] = d.ph[0];
-    fl.f[2] = d.ph[1];
-    launch_ghost_cells(d, fl, s);
-    { k_predict_nodes<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-    fl.n = 2;
-    fl.f[0] = d.uhx;
-    fl.f[1] = d.uhy;
-    launch_ghost_nodes(d, fl, s);
-    if (d.nmat == 2)
-        { k_correct<2><<<gn, blk2(), 0, s>>>(d, write_vol_lag); ++g_launches; }
-    else
-        { k_correct<1><<<gn, blk2(), 0, s>>>(d, write_vol_lag); ++g_launches; }
-    fl.f[0] = d.ulx;
-    fl.f[1] = d.uly;
-    launch_ghost_nodes(d, fl, s);
+        { k_lag_nodes<1><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag); ++g_launches; }
+    FieldList fn{};
+    fn.respect_halt = 1;
+    fn.n = 4;
+    fn.f[0] = d.uhx;
+    fn.f[1] = d.uhy;
+    fn.f[2] = d.ulx;
+    fn.f[3] = d.uly;
+    launch_ghost_nodes(d, fn, s);
     fl.n = d.nmat;
     fl.f[0] = d.el[0];
     fl.f[1] = d.el[1];
@@ -1425,22 +1488,14 @@ void launch_remap(const Dev& d, cudaStream_t s) {
         { k_cells<2><<<gcell_ext, blk2(), 0, s>>>(d); ++g_launches; }
     else
         { k_cells<1><<<gcell_ext, blk2(), 0, s>>>(d); ++g_launches; }
+    const dim3 gft((unsigned)((nx + FTX - 1) / FTX), (unsigned)((ny + FTY - 1) / FTY));
     if (two) {
-        { k_faces<2, 1><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-        { k_faces<2, 0><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-        { k_corners<2><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-    } else {
-        { k_faces<1, 1><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-        { k_faces<1, 0><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-        { k_corners<1><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-    }
-    { k_flux_ghosts<<<nblk((nx > ny ? nx : ny) + 2, 256), 256, 0, s>>>(d); ++g_launches; }
-    if (two) {
-        { k_gather_finalize<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_flux_gather<2><<<gft, FTX * FTY, 0, s>>>(d); ++g_launches; }
         { k_slivers<<<1, 32, 0, s>>>(d); ++g_launches; }
     } else {
-        { k_gather_finalize<1><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_flux_gather<1><<<gft, FTX * FTY, 0, s>>>(d); ++g_launches; }
     }
+    { k_flux_ghosts<<<nblk((nx > ny ? nx : ny) + 2, 256), 256, 0, s>>>(d); ++g_launches; }
     FieldList fl{};
     fl.respect_halt = 1;
     int q = 0;
