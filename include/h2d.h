@@ -210,8 +210,10 @@ int h2d_totals(h2d_ctx* ctx, double out[6]);
 /* Kernels launched by this library in the calling process so far. */
 long long h2d_launch_count(void);
 /* One run-loop step (as h2d_run with max_steps = state step + 1) bracketed by
- * CUDA events on the context's stream: ms = {cfl_dt, lagrange, remap, total}. */
-int h2d_step_timed(h2d_ctx* ctx, double cfl, double t_end, float ms[4]);
+ * CUDA events on the context's stream: ms = {cfl_dt, lagrange, remap, total}.
+ * phases = 0: the production CUDA-graph replay (only ms[3] is set);
+ * phases = 1: plain launches with events between the three phases. */
+int h2d_step_timed(h2d_ctx* ctx, double cfl, double t_end, int phases, float ms[4]);
 /* Write `bytes` of scratch on the context's stream (evicts L2 between timed
  * steps) and wait for it. */
 int h2d_flush_l2(h2d_ctx* ctx, long long bytes);

@@ -212,7 +212,7 @@ _SIGS = {
 # product-only extras (benchmark support)
 _EXTRA = {
     "launch_count": ([], C.c_longlong),
-    "step_timed": ([C.c_void_p, C.c_double, C.c_double, C.POINTER(C.c_float)], C.c_int),
+    "step_timed": ([C.c_void_p, C.c_double, C.c_double, C.c_int, C.POINTER(C.c_float)], C.c_int),
     "flush_l2": ([C.c_void_p, C.c_longlong], C.c_int),
 }
 
@@ -341,11 +341,12 @@ class Solver:
             raise err
         return res
 
-    def step_timed(self, cfl: float, t_end: float = 1e30):
+    def step_timed(self, cfl: float, t_end: float = 1e30, phases: bool = False):
         """One run-loop step timed with CUDA events (product only): returns
-        (cfl_ms, lagrange_ms, remap_ms, total_ms)."""
+        (cfl_ms, lagrange_ms, remap_ms, total_ms); phases=False replays the
+        production CUDA graph (only total is set)."""
         ms = (C.c_float * 4)()
-        self._check(self.lib.fn["step_timed"](self._h, cfl, t_end, ms))
+        self._check(self.lib.fn["step_timed"](self._h, cfl, t_end, int(phases), ms))
         return tuple(ms)
 
     def flush_l2(self, nbytes: int = 512 << 20):

@@ -44,8 +44,8 @@ struct h2d_ctx {
     double* stage = nullptr;     // device staging for AoS Vec2 fields
     double* dt_log = nullptr;    // device dt log of h2d_run
     int dt_log_cap = 0;
-    cudaGraphExec_t graph[2] = {nullptr, nullptr};
-    bool graph_ready = false;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one run-loop step per State parity
+    long long graph_kernels = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     void* flush = nullptr;
     size_t flush_bytes = 0;
@@ -274,6 +274,32 @@ void enqueue_step(h2d_ctx* c, int parity) {
     launch_nan_finish(d, c->st);
 }
 
+// The run-loop step is a fixed sequence of ~20 kernels whose arguments only
+// depend on the State parity: capture it once per parity as a CUDA graph and
+// replay it, so the per-kernel launch cost is paid once.
+int ensure_graphs(h2d_ctx* c) {
+    if (c->graph[0] && c->graph[1]) return 0;
+    for (int p = 0; p < 2; ++p) {
+        cudaGraph_t g = nullptr;
+        const long long before = launch_count();
+        CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+        enqueue_step(c, p);
+        CK(cudaStreamEndCapture(c->st, &g));
+        c->graph_kernels = launch_count() - before;
+        add_launches(-c->graph_kernels);  // captured, not executed
+        const cudaError_t e = cudaGraphInstantiate(&c->graph[p], g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+    }
+    return 0;
+}
+
+int launch_step_graph(h2d_ctx* c, int parity) {
+    CK(cudaGraphLaunch(c->graph[parity], c->st));
+    add_launches(c->graph_kernels);
+    return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -328,8 +354,13 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
         s.e_mix = plane(c);
         s.rho_mix = plane(c);
         s.p_mix = plane(c);
-        s.nrx = plane(c);
-        s.nry = plane(c);
+        if (p == 0 || nm == 2) {
+            s.nrx = plane(c);
+            s.nry = plane(c);
+        } else {  // one material: the normals are carried unchanged, so both parities share them
+            s.nrx = c->sb[0].nrx;
+            s.nry = c->sb[0].nry;
+        }
         s.ux = plane(c);
         s.uy = plane(c);
     }
@@ -426,7 +457,7 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
     if (ctl_push(c)) return fail(H2D_ERR_DEVICE);
     // make_state defaults (state.cpp:5-23): k0 = 1, normals (1, 0), vol = dx*dy
     for (int p = 0; p < 2; ++p) {
-        if (fill_plane(c, c->sb[p].k[0], 1.0) || fill_plane(c, c->sb[p].nrx, 1.0) ||
+        if (fill_plane(c, c->sb[p].k[0], 1.0) || (p == 0 || nm == 2 ? fill_plane(c, c->sb[p].nrx, 1.0) : 0) ||
             fill_plane(c, c->sb[p].vol, d.cv))
             return fail(H2D_ERR_DEVICE);
     }
@@ -656,6 +687,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
     if (int rc = ctl_push(c)) return rc;
     int parity = c->cur;
     int rc = 0;
+    if ((rc = ensure_graphs(c))) return rc;
     // Launch in chunks; the device control block turns every kernel after the
     // loop condition fails (or after an error) into a no-op.
     for (;;) {
@@ -666,7 +698,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
             chunk = left < chunk ? left : chunk;
         }
         for (int q = 0; q < chunk; ++q) {
-            enqueue_step(c, parity);
+            if ((rc = launch_step_graph(c, parity))) return rc;
             parity ^= 1;
         }
         if ((rc = check_launch(c))) return rc;
@@ -732,7 +764,7 @@ int h2d_totals(h2d_ctx* c, double out[6]) {
     return 0;
 }
 
-int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, float ms[4]) {
+int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[4]) {
     cudaSetDevice(c->device);
     if (!c->ev[0])
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
@@ -745,24 +777,34 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, float ms[4]) {
     h.dt_log = nullptr;
     h.dt_log_cap = 0;
     if (int rc = ctl_push(c)) return rc;
-    const Dev d = make_dev(c, c->cur, 1);
-    CK(cudaEventRecord(c->ev[0], c->st));
-    launch_begin(c->ctl, 0, 0.0, c->st);
-    launch_cfl(d, 1, c->st);
-    CK(cudaEventRecord(c->ev[1], c->st));
-    launch_lagrange(d, 0, c->st);
-    CK(cudaEventRecord(c->ev[2], c->st));
-    CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->ny, c->st));
-    launch_remap(d, c->st);
-    launch_commit(c->ctl, 1, c->st);
-    launch_nan_finish(d, c->st);
-    CK(cudaEventRecord(c->ev[3], c->st));
-    if (int rc = check_launch(c)) return rc;
-    CK(cudaEventSynchronize(c->ev[3]));
-    CK(cudaEventElapsedTime(&ms[0], c->ev[0], c->ev[1]));
-    CK(cudaEventElapsedTime(&ms[1], c->ev[1], c->ev[2]));
-    CK(cudaEventElapsedTime(&ms[2], c->ev[2], c->ev[3]));
-    CK(cudaEventElapsedTime(&ms[3], c->ev[0], c->ev[3]));
+    if (phases) {  // un-graphed launch with events between the phases
+        const Dev d = make_dev(c, c->cur, 1);
+        CK(cudaEventRecord(c->ev[0], c->st));
+        launch_begin(c->ctl, 0, 0.0, c->st);
+        launch_cfl(d, 1, c->st);
+        CK(cudaEventRecord(c->ev[1], c->st));
+        launch_lagrange(d, 0, c->st);
+        CK(cudaEventRecord(c->ev[2], c->st));
+        CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->ny, c->st));
+        launch_remap(d, c->st);
+        launch_commit(c->ctl, 1, c->st);
+        launch_nan_finish(d, c->st);
+        CK(cudaEventRecord(c->ev[3], c->st));
+        if (int rc = check_launch(c)) return rc;
+        CK(cudaEventSynchronize(c->ev[3]));
+        CK(cudaEventElapsedTime(&ms[0], c->ev[0], c->ev[1]));
+        CK(cudaEventElapsedTime(&ms[1], c->ev[1], c->ev[2]));
+        CK(cudaEventElapsedTime(&ms[2], c->ev[2], c->ev[3]));
+        CK(cudaEventElapsedTime(&ms[3], c->ev[0], c->ev[3]));
+    } else {  // the production path: one graph launch
+        if (int rc = ensure_graphs(c)) return rc;
+        CK(cudaEventRecord(c->ev[0], c->st));
+        if (int rc = launch_step_graph(c, c->cur)) return rc;
+        CK(cudaEventRecord(c->ev[3], c->st));
+        CK(cudaEventSynchronize(c->ev[3]));
+        ms[0] = ms[1] = ms[2] = 0.0f;
+        CK(cudaEventElapsedTime(&ms[3], c->ev[0], c->ev[3]));
+    }
     if (int rc = ctl_pull(c)) return rc;
     c->cur = h.cur;
     return decode_error(c, true);

@@ -151,9 +151,7 @@ __device__ __forceinline__ bool ghost_cell_pos(int t, int nx, int ny, int& i, in
     return false;
 }
 
-__global__ void k_ghost_cells(Dev d, FieldList fl) {
-    if (fl.respect_halt && halted(d.ctl)) return;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void ghost_cells_at(const Dev& d, const FieldList& fl, int t) {
     int i, j;
     if (!ghost_cell_pos(t, d.nx, d.ny, i, j)) return;
     const int is = wrap_cell(i, d.nx, d.per_x), js = wrap_cell(j, d.ny, d.per_y);
@@ -162,10 +160,8 @@ __global__ void k_ghost_cells(Dev d, FieldList fl) {
 }
 
 // fill_ghost_nodes (state.cpp:87-108) for Vec2 pairs (x, y).
-__global__ void k_ghost_nodes(Dev d, FieldList fl) {
-    if (fl.respect_halt && halted(d.ctl)) return;
+__device__ __forceinline__ void ghost_nodes_at(const Dev& d, const FieldList& fl, int t) {
     const int nx = d.nx, ny = d.ny;
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int W = nx + 1 + 2 * G;
     int i, j;
     if (t < 2 * G * W) {
@@ -452,29 +448,18 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
 // ---------------------------------------------------------------------------
 // make_work, remap.cpp:116-140, over every cell incl. ghosts: the next-state
 // buffers become the Work arrays.
-template <int NM>
-__global__ void k_make_work(Dev d) {
-    // The Work arrays of make_work (remap.cpp:116-140) are read in place:
-    // w.m = state m, w.e = e_lag, w.k = state k, w.me = m * e_lag (recomputed
-    // where read), so flux threads never race with finalize writing the next
-    // State.  Only the lagged cell mass, the carried normals and (without the
-    // velocity remap) u are materialised here.
+// remap_velocity == false: the new u is lag.u_lag unchanged (remap.cpp:130,
+// 993); the Work arrays of make_work (remap.cpp:116-140) are otherwise read in
+// place (w.m = state m, w.e = e_lag, w.k = state k, w.me = m * e_lag), so the
+// flux threads never race with finalize writing the next State.
+__global__ void k_copy_u(Dev d) {
     if (halted(d.ctl)) return;
     int i, j;
     tid2(i, j, -G, -G);
     if (i > d.nx + G || j > d.ny + G) return;
     const size_t c = ix(d, i, j);
-    if (!d.remap_velocity) {  // w.u = lag.u_lag becomes the new u unchanged
-        d.nux[c] = d.ulx[c];
-        d.nuy[c] = d.uly[c];
-    }
-    if (i >= d.nx + G || j >= d.ny + G) return;
-    double mc = 0.0;
-#pragma unroll
-    for (int a = 0; a < NM; ++a) mc += d.m[a][c];
-    d.mcell_lag[c] = mc;
-    d.nnrx[c] = d.nrx[c];
-    d.nnry[c] = d.nry[c];
+    d.nux[c] = d.ulx[c];
+    d.nuy[c] = d.uly[c];
 }
 
 // cf_face_flux_x, remap.cpp:27-47 (Y faces call it with swapped components)
@@ -500,94 +485,116 @@ __device__ __forceinline__ void face_flux(double ym, double yp, double dmx, doub
     dv = 0.5 * (xlo + xhi) * (whi - wlo);
 }
 
-// make_axis_geom X/Y (remap.cpp:296-322) + face/corner flux geometry
-// (:744-767), over the ghosted node range [-2, n+2]^2.
-__global__ void k_geom(Dev d) {
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, -G, -G);
+// make_axis_geom X/Y (remap.cpp:296-322), face / corner flux geometry
+// (:744-767), Lagrangian volumes and densities (:769-794), 2D centroids
+// (:797-803) and interfaces (:807-824), fused per 32x8 cell tile over the
+// ghosted range: the (33 x 9) node items of a tile go to shared memory (and
+// the owned ones to HBM for the flux pass), then each cell reads its four
+// faces and corners from shared memory.
+constexpr int GTX = 32, GTY = 8;
+template <int NM>
+__global__ void __launch_bounds__(GTX * GTY) k_geom_cells(Dev d) {
+    constexpr int W = GTX + 1, NN = W * (GTY + 1);
+    __shared__ double s_hx[NN], s_hy[NN], s_cf[NN], s_fdx[NN], s_fdy[NN], s_fx[NN], s_fy[NN];
+    __shared__ int8_t s_sx[NN], s_sy[NN];
+    __shared__ int s_halt;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
     const int nx = d.nx, ny = d.ny;
-    if (i > nx + G || j > ny + G) return;
+    const int imax = nx + G, jmax = ny + G;  // node range [-G, n+G]
+    const int i0 = -G + (int)blockIdx.x * GTX, j0 = -G + (int)blockIdx.y * GTY;
     const double dt = step_dt(d.ctl);
     const double cv = d.cv;
-    const size_t n = ix(d, i, j);
-    const double u0x = d.uhx[n], u0y = d.uhy[n];
-    // corner flux, remap.cpp:16-25
-    {
-        const double ddx = u0x * dt, ddy = u0y * dt;
-        double dv = fabs(ddx * ddy);
-        int8_t sx = 0, sy = 0;
-        if (dv == 0.0) {
-            dv = 0.0;
-        } else {
-            sx = ddx > 0.0 ? 1 : -1;
-            sy = ddy > 0.0 ? 1 : -1;
+    for (int t = tid; t < NN; t += GTX * GTY) {
+        const int i = i0 + t % W, j = j0 + t / W;
+        if (i > imax || j > jmax) continue;
+        const bool own = (i < i0 + GTX || i == imax) && (j < j0 + GTY || j == jmax);
+        const size_t n = ix(d, i, j);
+        const double u0x = d.uhx[n], u0y = d.uhy[n];
+        s_hx[t] = u0x;
+        s_hy[t] = u0y;
+        {  // cf_corner_flux, remap.cpp:16-25
+            const double ddx = u0x * dt, ddy = u0y * dt;
+            double dv = fabs(ddx * ddy);
+            int8_t sx = 0, sy = 0;
+            if (dv == 0.0) {
+                dv = 0.0;
+            } else {
+                sx = ddx > 0.0 ? 1 : -1;
+                sy = ddy > 0.0 ? 1 : -1;
+            }
+            s_cf[t] = dv;
+            s_sx[t] = sx;
+            s_sy[t] = sy;
+            if (own) {
+                d.cf_dv[n] = dv;
+                d.cf_sx[n] = sx;
+                d.cf_sy[n] = sy;
+            }
+            if (dv > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
         }
-        d.cf_dv[n] = dv;
-        d.cf_sx[n] = sx;
-        d.cf_sy[n] = sy;
-        if (dv > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
+        if (j < jmax) {  // X geometry at (ia=i, ic=j) and the X face
+            const size_t nu = ix(d, i, j + 1);
+            const double ux1 = d.uhx[nu], uy1 = d.uhy[nu];
+            const double fd = 0.5 * (u0x + ux1) * dt;
+            double dv, wl, wh;
+            face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * u0x, dt * u0y, dt * ux1, dt * uy1, dv, wl, wh);
+            s_fdx[t] = fd;
+            s_fx[t] = dv;
+            if (own) {
+                d.fdx[n] = fd;
+                d.fx_dv[n] = dv;
+                d.fx_lo[n] = wl;
+                d.fx_hi[n] = wh;
+            }
+            if (fabs(dv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
+        }
+        if (i < imax) {  // Y geometry at (ia=j, ic=i), stored at (i, j), and the Y face
+            const size_t nr = ix(d, i + 1, j);
+            const double ux1 = d.uhx[nr], uy1 = d.uhy[nr];
+            const double fd = 0.5 * (u0y + uy1) * dt;
+            double dv, wl, wh;
+            face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * u0y, dt * u0x, dt * uy1, dt * ux1, dv, wl, wh);
+            s_fdy[t] = fd;
+            s_fy[t] = dv;
+            if (own) {
+                d.fdy[n] = fd;
+                d.fy_dv[n] = dv;
+                d.fy_lo[n] = wl;
+                d.fy_hi[n] = wh;
+            }
+            if (fabs(dv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
+        }
     }
-    const bool has_up = j < ny + G, has_right = i < nx + G;
-    if (has_up) {  // X geometry at (ia=i, ic=j) and the X face
-        const size_t nu = ix(d, i, j + 1);
-        d.fdx[n] = 0.5 * (u0x + d.uhx[nu]) * dt;
-        double dv, wl, wh;
-        face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * u0x, dt * u0y, dt * d.uhx[nu], dt * d.uhy[nu], dv, wl,
-                  wh);
-        d.fx_dv[n] = dv;
-        d.fx_lo[n] = wl;
-        d.fx_hi[n] = wh;
-        if (fabs(dv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
-    }
-    if (has_right) {  // Y geometry at (ia=j, ic=i), stored at (i, j), and the Y face
-        const size_t nr = ix(d, i + 1, j);
-        d.fdy[n] = 0.5 * (u0y + d.uhy[nr]) * dt;
-        double dv, wl, wh;
-        face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * u0y, dt * u0x, dt * d.uhy[nr], dt * d.uhx[nr], dv, wl,
-                  wh);
-        d.fy_dv[n] = dv;
-        d.fy_lo[n] = wl;
-        d.fy_hi[n] = wh;
-        if (fabs(dv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
-    }
-    if (has_up && has_right) {  // xlagc / wlag of cell (i, j) on both axes
-        const size_t nu = ix(d, i, j + 1), nr = ix(d, i + 1, j), nur = ix(d, i + 1, j + 1);
-        const double dlx = 0.5 * (u0x + d.uhx[nu]) * dt, drx = 0.5 * (d.uhx[nr] + d.uhx[nur]) * dt;
-        d.xlcx[n] = d.x0 + (i + 0.5) * d.dx + 0.5 * (dlx + drx);
-        d.wlx[n] = d.dx + (drx - dlx);
-        const double dly = 0.5 * (u0y + d.uhy[nr]) * dt, dry = 0.5 * (d.uhy[nu] + d.uhy[nur]) * dt;
-        d.xlcy[n] = d.y0 + (j + 0.5) * d.dy + 0.5 * (dly + dry);
-        d.wly[n] = d.dy + (dry - dly);
-    }
-}
-
-// corner_term of remap.cpp:775-785 for cell (i, j) and node (ni, nj)
-__device__ __forceinline__ double corner_term(const Dev& d, int i, int j, int ni, int nj) {
-    const size_t n = ix(d, ni, nj);
-    const double dv = d.cf_dv[n];
-    if (dv == 0.0) return 0.0;
-    const int sx = d.cf_sx[n], sy = d.cf_sy[n];
-    const int di = sx > 0 ? ni - 1 : ni, dj = sy > 0 ? nj - 1 : nj;
-    if (di == i && dj == j) return dv;
-    const int ri = sx > 0 ? ni : ni - 1, rj = sy > 0 ? nj : nj - 1;
-    if (ri == i && rj == j) return -dv;
-    return 0.0;
-}
-
-// Lagrangian volume / densities (remap.cpp:769-794), 2D centroids (:797-803)
-// and interface placement (:807-824), over cells [-2, n+2)^2.
-template <int NM>
-__global__ void k_cells(Dev d) {
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, -G, -G);
-    if (i >= d.nx + G || j >= d.ny + G) return;
-    const double dt = step_dt(d.ctl);
+    __syncthreads();
+    const int tx = tid % GTX, ty = tid / GTX;
+    const int i = i0 + tx, j = j0 + ty;
+    if (i >= nx + G || j >= ny + G) return;
+    const int q00 = tx + ty * W, q10 = q00 + 1, q01 = q00 + W, q11 = q01 + 1;
     const size_t c = ix(d, i, j);
-    double v = d.cv + d.fx_dv[ix(d, i + 1, j)] - d.fx_dv[c] + d.fy_dv[ix(d, i, j + 1)] - d.fy_dv[c];
-    v += corner_term(d, i, j, i, j) + corner_term(d, i, j, i + 1, j) + corner_term(d, i, j, i, j + 1) +
-         corner_term(d, i, j, i + 1, j + 1);
+    {  // xlagc / wlag of cell (i, j) on both axes
+        const double dlx = s_fdx[q00], drx = s_fdx[q10];
+        d.xlcx[c] = d.x0 + (i + 0.5) * d.dx + 0.5 * (dlx + drx);
+        d.wlx[c] = d.dx + (drx - dlx);
+        const double dly = s_fdy[q00], dry = s_fdy[q01];
+        d.xlcy[c] = d.y0 + (j + 0.5) * d.dy + 0.5 * (dly + dry);
+        d.wly[c] = d.dy + (dry - dly);
+    }
+    // corner_term of remap.cpp:775-785
+    auto cterm = [&](int q, int ni, int nj) -> double {
+        const double dv = s_cf[q];
+        if (dv == 0.0) return 0.0;
+        const int sx = s_sx[q], sy = s_sy[q];
+        const int di = sx > 0 ? ni - 1 : ni, dj = sy > 0 ? nj - 1 : nj;
+        if (di == i && dj == j) return dv;
+        const int ri = sx > 0 ? ni : ni - 1, rj = sy > 0 ? nj : nj - 1;
+        if (ri == i && rj == j) return -dv;
+        return 0.0;
+    };
+    double v = cv + s_fx[q10] - s_fx[q00] + s_fy[q01] - s_fy[q00];
+    v += cterm(q00, i, j) + cterm(q10, i + 1, j) + cterm(q01, i, j + 1) + cterm(q11, i + 1, j + 1);
     if (v <= 0.0) raise(d.ctl, ekey(PH_COLLAPSED, j, i, 0));
     d.vlag[c] = v;
 #pragma unroll
@@ -595,17 +602,16 @@ __global__ void k_cells(Dev d) {
         const double ka = d.k[a][c];
         d.rho[a][c] = ka > 0.0 ? d.m[a][c] / (ka * v) : 0.0;
     }
-    const size_t n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
-    const double mdx = 0.25 * (dt * d.uhx[c] + dt * d.uhx[n10] + dt * d.uhx[n01] + dt * d.uhx[n11]);
-    const double mdy = 0.25 * (dt * d.uhy[c] + dt * d.uhy[n10] + dt * d.uhy[n01] + dt * d.uhy[n11]);
+    const double mdx = 0.25 * (dt * s_hx[q00] + dt * s_hx[q10] + dt * s_hx[q01] + dt * s_hx[q11]);
+    const double mdy = 0.25 * (dt * s_hy[q00] + dt * s_hy[q10] + dt * s_hy[q01] + dt * s_hy[q11]);
     d.xl2x[c] = (d.x0 + (i + 0.5) * d.dx) + mdx;
     d.xl2y[c] = (d.y0 + (j + 0.5) * d.dy) + mdy;
     if (NM == 2) {
         const double k0 = d.k[0][c];
         if (is_mixed(k0)) {
             const double cx = d.x0 + (i + 0.5) * d.dx, cy = d.y0 + (j + 0.5) * d.dy;
-            const double lox = cx - 0.5 * d.dx + d.fdx[c], loy = cy - 0.5 * d.dy + d.fdy[c];
-            const double hix = cx + 0.5 * d.dx + d.fdx[n10], hiy = cy + 0.5 * d.dy + d.fdy[n01];
+            const double lox = cx - 0.5 * d.dx + s_fdx[q00], loy = cy - 0.5 * d.dy + s_fdy[q00];
+            const double hix = cx + 0.5 * d.dx + s_fdx[q10], hiy = cy + 0.5 * d.dy + s_fdy[q01];
             d.ifd[c] = place_interface(k0, d.nrx[c], d.nry[c], lox, loy, hix, hiy);
         }
     }
@@ -788,9 +794,7 @@ __device__ __forceinline__ double corner_item(const Dev& d, int i, int j, double
 
 // fill_face_flux_ghosts (remap.cpp:371-382) for dmx / dmy and the dmc ghost
 // rows (:985-988).  Every write reads interior entries only.
-__global__ void k_flux_ghosts(Dev d) {
-    if (halted(d.ctl)) return;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void flux_ghosts_at(const Dev& d, int t) {
     const int nx = d.nx, ny = d.ny;
     // dmx: along = x (na = nx), cross = y (nc = ny); (ia, ic) at (i, j)
     auto dmx_c = [&](int ia, int ic) -> double {  // value incl. cross ghosts
@@ -825,6 +829,21 @@ __global__ void k_flux_ghosts(Dev d) {
     if (t <= nx + 1) {  // dmy along ghost (ia = -1, ic) at (ic, -1), ic in [-1, nx]
         const int ic = t - 1;
         d.dmy[ix(d, ic, -1)] = d.per_y ? dmy_c(ny - 1, ic) : -dmy_c(1, ic);
+    }
+}
+
+// Ghost layers of several cell fields (blockIdx.y = 0), node Vec2 fields
+// (blockIdx.y = 1) and the face / corner mass-flux ghosts (blockIdx.y = 2) in
+// one launch; every write reads interior entries only.
+__global__ void k_ghost_multi(Dev d, FieldList cells, FieldList nodes, int flux, int respect_halt) {
+    if (respect_halt && halted(d.ctl)) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (blockIdx.y == 0) {
+        if (cells.n) ghost_cells_at(d, cells, t);
+    } else if (blockIdx.y == 1) {
+        if (nodes.n) ghost_nodes_at(d, nodes, t);
+    } else if (flux) {
+        flux_ghosts_at(d, t);
     }
 }
 
@@ -1101,12 +1120,7 @@ __device__ __forceinline__ double dual_face_value(const Dev& d, const double* u,
 // dual_face_pass, remap.cpp:408-442: one thread per dual face. AX = 1: X
 // (ia = i node, ic = j), AX = 0: Y (ia = j, ic = i); stored at (i, j).
 template <int AX>
-__global__ void k_dual_faces(Dev d) {
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, 0, 0);
-    const int iend = d.per_x ? d.nx - 1 : d.nx, jend = d.per_y ? d.ny - 1 : d.ny;
-    if (i > iend || j > jend) return;
+__device__ __forceinline__ void dual_face_item(const Dev& d, int i, int j) {
     const int ia = AX ? i : j, ic = AX ? j : i;
     const int per_a = AX ? d.per_x : d.per_y;
     const size_t s = ix(d, i, j);
@@ -1141,15 +1155,10 @@ __global__ void k_dual_faces(Dev d) {
     d.dflag[AX ? 0 : 1][s] = dm != 0.0;  // a zero dual mass flux is skipped (remap.cpp:423)
 }
 
-// Dual-mesh corner exchanges, remap.cpp:1000-1069: thread per (i, j), both
+// Dual-mesh corner exchanges, remap.cpp:1000-1069: iteration (i, j), both
 // pairs (1,1) and (1,-1).
-__global__ void k_dual_corners(Dev d) {
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, 0, 0);
+__device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
     const int nx = d.nx, ny = d.ny;
-    const int iuniq = d.per_x ? nx - 1 : nx, juniq = d.per_y ? ny - 1 : ny;
-    if (i > iuniq || j > juniq) return;
     const double dt = step_dt(d.ctl);
     const size_t s = ix(d, i, j);
 #pragma unroll
@@ -1224,6 +1233,19 @@ __global__ void k_dual_corners(Dev d) {
         d.dc_y[pr][s] = cy;
         d.dflag[2 + pr][s] = active;
     }
+}
+
+// All dual-mesh items of one unique node (i, j): its X and Y dual faces and
+// its two diagonal corner exchanges (remap.cpp:995-1069).
+__global__ void k_dual_items(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    const int iend = d.per_x ? d.nx - 1 : d.nx, jend = d.per_y ? d.ny - 1 : d.ny;
+    if (i > iend || j > jend) return;
+    dual_face_item<1>(d, i, j);
+    dual_face_item<0>(d, i, j);
+    dual_corner_items(d, i, j);
 }
 
 // MomAcc gather (App. C item 4) + apply_dual_update (remap.cpp:444-464) with
@@ -1314,15 +1336,25 @@ __global__ void k_node_update(Dev d) {
             ay += cy[a];
         }
     }
-    const double mp_lag = 0.25 * (d.mcell_lag[ix(d, si - 1, sj - 1)] + d.mcell_lag[ix(d, si, sj - 1)] +
-                                  d.mcell_lag[ix(d, si - 1, sj)] + d.mcell_lag[s]);
+    // mcell before finalize = make_work's sum of the state's partial masses
+    // (remap.cpp:133-138), incl. ghost cells
+    auto ml = [&](size_t c) {
+        double mc = 0.0;
+        for (int a = 0; a < d.nmat; ++a) mc += d.m[a][c];
+        return mc;
+    };
+    const double mp_lag = 0.25 * (ml(ix(d, si - 1, sj - 1)) + ml(ix(d, si, sj - 1)) + ml(ix(d, si - 1, sj)) + ml(s));
     const double mp_new =
         0.25 * (d.mcell[ix(d, si - 1, sj - 1)] + d.mcell[ix(d, si, sj - 1)] + d.mcell[ix(d, si - 1, sj)] + d.mcell[s]);
     if (mp_new <= 0.0 && si == i && sj == j) raise(d.ctl, ekey(PH_NODAL_MASS, j, i, 0));
     const double inv = 1.0 / mp_new;
     const size_t o = ix(d, i, j);
-    d.nux[o] = inv * (mp_lag * d.ulx[s] + ax);
-    d.nuy[o] = inv * (mp_lag * d.uly[s] + ay);
+    double ux = inv * (mp_lag * d.ulx[s] + ax), uy = inv * (mp_lag * d.uly[s] + ay);
+    // fill_ghost_nodes (remap.cpp:462) zeroes the normal component on walls
+    if (!d.per_x && (i == 0 || i == nx)) ux = 0.0;
+    if (!d.per_y && (j == 0 || j == ny)) uy = 0.0;
+    d.nux[o] = ux;
+    d.nuy[o] = uy;
 }
 
 // refresh_normals_impl + youngs_normal (remap.cpp:102-114, vof.cpp:10-22)
@@ -1337,6 +1369,10 @@ __global__ void k_normals(Dev d, int api) {
     double* nx_ = api ? const_cast<double*>(d.nrx) : d.nnrx;
     double* ny_ = api ? const_cast<double*>(d.nry) : d.nnry;
     const size_t c = ix(d, i, j);
+    if (!api) {  // the Work normals start as the State's (remap.cpp:130)
+        nx_[c] = d.nrx[c];
+        ny_[c] = d.nry[c];
+    }
     if (!is_mixed(k0[c])) return;
     auto K = [&](int ii, int jj) { return k1[ix(d, ii, jj)]; };
     auto col = [&](int ii) { return K(ii, j - 1) + 2.0 * K(ii, j) + K(ii, j + 1); };
@@ -1366,9 +1402,12 @@ __global__ void k_nan(Dev d) {
     tid2(i, j, 0, 0);
     if (i > d.nx || j > d.ny) return;
     const size_t c = ix(d, i, j);
-    if (i < d.nx && j < d.ny && (!isfinite(d.nm_mix[c]) || !isfinite(d.ne_mix[c]) || !isfinite(d.np_mix[c])))
-        raise(d.ctl, ekey(PH_NAN_CELL, j, i, 0));
-    if (!isfinite(d.nux[c]) || !isfinite(d.nuy[c])) raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));
+    const bool cell = i < d.nx && j < d.ny;
+    // issue every load before testing any of them (no short-circuit chains)
+    const double a = cell ? d.nm_mix[c] : 0.0, b = cell ? d.ne_mix[c] : 0.0, p = cell ? d.np_mix[c] : 0.0;
+    const double ux = d.nux[c], uy = d.nuy[c];
+    if (!isfinite(a) | !isfinite(b) | !isfinite(p)) raise(d.ctl, ekey(PH_NAN_CELL, j, i, 0));
+    if (!isfinite(ux) | !isfinite(uy)) raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));
 }
 
 // End of a successful run-loop step: counters and dt log.
@@ -1404,6 +1443,7 @@ __global__ void k_interleave(double* dst, const double* x, const double* y, int 
 // ---------------------------------------------------------------------------
 static std::atomic<long long> g_launches{0};
 long long launch_count() { return g_launches.load(); }
+void add_launches(long long n) { g_launches += n; }
 static dim3 blk2() { return dim3(32, 4); }
 static dim3 grid_rect(int w, int h) {
     const dim3 b = blk2();
@@ -1425,13 +1465,25 @@ void launch_cfl(const Dev& d, int run_loop, cudaStream_t s) {
     { k_cfl_final<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy, run_loop); ++g_launches; }
 }
 
+static long long ghost_threads(const Dev& d) {
+    const long long nc = 2LL * G * (d.nx + 2 * G) + 2LL * G * d.ny;
+    const long long nn = 2LL * G * (d.nx + 1 + 2 * G) + 2LL * G * (d.ny + 1) + 2LL * (d.ny + 1) + 2LL * (d.nx + 1);
+    const long long nf = (d.nx > d.ny ? d.nx : d.ny) + 2;
+    long long m = nc > nn ? nc : nn;
+    return m > nf ? m : nf;
+}
+void launch_ghost_multi(const Dev& d, const FieldList& cells, const FieldList& nodes, int flux, int respect_halt,
+                        cudaStream_t s) {
+    const dim3 g(nblk(ghost_threads(d), 256), 3);
+    { k_ghost_multi<<<g, 256, 0, s>>>(d, cells, nodes, flux, respect_halt); ++g_launches; }
+}
 void launch_ghost_cells(const Dev& d, const FieldList& fl, cudaStream_t s) {
-    const long long n = 2LL * G * (d.nx + 2 * G) + 2LL * G * d.ny;
-    { k_ghost_cells<<<nblk(n, 256), 256, 0, s>>>(d, fl); ++g_launches; }
+    FieldList none{};
+    launch_ghost_multi(d, fl, none, 0, fl.respect_halt, s);
 }
 void launch_ghost_nodes(const Dev& d, const FieldList& fl, cudaStream_t s) {
-    const long long n = 2LL * G * (d.nx + 1 + 2 * G) + 2LL * G * (d.ny + 1) + 2LL * (d.ny + 1) + 2LL * (d.nx + 1);
-    { k_ghost_nodes<<<nblk(n, 256), 256, 0, s>>>(d, fl); ++g_launches; }
+    FieldList none{};
+    launch_ghost_multi(d, none, fl, 0, fl.respect_halt, s);
 }
 
 void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s) {
@@ -1460,34 +1512,28 @@ void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
     else
         { k_lag_nodes<1><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag); ++g_launches; }
     FieldList fn{};
-    fn.respect_halt = 1;
     fn.n = 4;
     fn.f[0] = d.uhx;
     fn.f[1] = d.uhy;
     fn.f[2] = d.ulx;
     fn.f[3] = d.uly;
-    launch_ghost_nodes(d, fn, s);
     fl.n = d.nmat;
     fl.f[0] = d.el[0];
     fl.f[1] = d.el[1];
-    launch_ghost_cells(d, fl, s);
+    launch_ghost_multi(d, fl, fn, 0, 1, s);
 }
 
 void launch_remap(const Dev& d, cudaStream_t s) {
     const int nx = d.nx, ny = d.ny;
     const bool two = d.nmat == 2;
     const dim3 gall = grid_rect(nx + 1 + 2 * G, ny + 1 + 2 * G);
-    const dim3 gcell_ext = grid_rect(nx + 2 * G, ny + 2 * G);
     const dim3 gc = grid_rect(nx, ny), gn = grid_rect(nx + 1, ny + 1);
+    if (!d.remap_velocity) { k_copy_u<<<gall, blk2(), 0, s>>>(d); ++g_launches; }
+    const dim3 ggc((unsigned)((nx + 2 * G + GTX - 1) / GTX), (unsigned)((ny + 2 * G + GTY - 1) / GTY));
     if (two)
-        { k_make_work<2><<<gall, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_geom_cells<2><<<ggc, GTX * GTY, 0, s>>>(d); ++g_launches; }
     else
-        { k_make_work<1><<<gall, blk2(), 0, s>>>(d); ++g_launches; }
-    { k_geom<<<gall, blk2(), 0, s>>>(d); ++g_launches; }
-    if (two)
-        { k_cells<2><<<gcell_ext, blk2(), 0, s>>>(d); ++g_launches; }
-    else
-        { k_cells<1><<<gcell_ext, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_geom_cells<1><<<ggc, GTX * GTY, 0, s>>>(d); ++g_launches; }
     const dim3 gft((unsigned)((nx + FTX - 1) / FTX), (unsigned)((ny + FTY - 1) / FTY));
     if (two) {
         { k_flux_gather<2><<<gft, FTX * FTY, 0, s>>>(d); ++g_launches; }
@@ -1495,9 +1541,8 @@ void launch_remap(const Dev& d, cudaStream_t s) {
     } else {
         { k_flux_gather<1><<<gft, FTX * FTY, 0, s>>>(d); ++g_launches; }
     }
-    { k_flux_ghosts<<<nblk((nx > ny ? nx : ny) + 2, 256), 256, 0, s>>>(d); ++g_launches; }
+    // finalize_cells ghost fill (remap.cpp:227-233) + face / corner flux ghosts
     FieldList fl{};
-    fl.respect_halt = 1;
     int q = 0;
     for (int a = 0; a < d.nmat; ++a) {
         fl.f[q++] = d.nm[a];
@@ -1507,39 +1552,25 @@ void launch_remap(const Dev& d, cudaStream_t s) {
     }
     fl.f[q++] = d.mcell;
     fl.n = q;
-    launch_ghost_cells(d, fl, s);
+    FieldList none{};
+    launch_ghost_multi(d, fl, none, 1, 1, s);
     if (d.remap_velocity) {
-        { k_dual_faces<1><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-        { k_dual_faces<0><<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-        { k_dual_corners<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_dual_items<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
         { k_node_update<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-        FieldList fu{};
-        fu.respect_halt = 1;
-        fu.n = 2;
-        fu.f[0] = d.nux;
-        fu.f[1] = d.nuy;
-        launch_ghost_nodes(d, fu, s);
     }
-    { if (two) k_normals<<<gc, blk2(), 0, s>>>(d, 0); ++g_launches; }
-    // assemble_state (remap.cpp:1075-1089): fill_ghosts + sync_derived
+    if (two) { k_normals<<<gc, blk2(), 0, s>>>(d, 0); ++g_launches; }
+    // assemble_state (remap.cpp:1075-1089): fill_ghosts + sync_derived.  The
+    // m, e, k ghosts were filled by finalize (identical values); the new u and
+    // the normals still need theirs.
     FieldList fg{};
-    fg.respect_halt = 1;
-    q = 0;
-    for (int a = 0; a < d.nmat; ++a) {
-        fg.f[q++] = d.nm[a];
-        fg.f[q++] = d.ne[a];
-        fg.f[q++] = d.nk[a];
-    }
-    fg.f[q++] = d.nnrx;
-    fg.f[q++] = d.nnry;
-    fg.n = q;
-    launch_ghost_cells(d, fg, s);
+    fg.n = 2;
+    fg.f[0] = d.nnrx;
+    fg.f[1] = d.nnry;
     FieldList fu{};
-    fu.respect_halt = 1;
     fu.n = 2;
     fu.f[0] = d.nux;
     fu.f[1] = d.nuy;
-    launch_ghost_nodes(d, fu, s);
+    launch_ghost_multi(d, fg, fu, 0, 1, s);
     launch_sync(d, 1, 1, s);
 }
 

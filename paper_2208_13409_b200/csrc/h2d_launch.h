@@ -13,6 +13,7 @@ struct FieldList {
 };
 
 long long launch_count();
+void add_launches(long long n);  // kernels replayed by a CUDA graph launch
 void launch_begin(Ctl* c, int mode, double dt, cudaStream_t s);
 void launch_cfl(const Dev& d, int run_loop, cudaStream_t s);
 void launch_ghost_cells(const Dev& d, const FieldList& fl, cudaStream_t s);
