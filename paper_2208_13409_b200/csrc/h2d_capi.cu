@@ -400,29 +400,10 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
         d.ph[a] = plane(c);
         d.el[a] = plane(c);
         d.me[a] = plane(c);
-        d.rho[a] = plane(c);
         d.slm[a] = plane(c);
         d.slme[a] = plane(c);
     }
     d.mcell = plane(c);
-    d.mcell_lag = plane(c);
-    d.fdx = plane(c);
-    d.fdy = plane(c);
-    d.xlcx = plane(c);
-    d.xlcy = plane(c);
-    d.wlx = plane(c);
-    d.wly = plane(c);
-    d.fx_dv = plane(c);
-    d.fx_lo = plane(c);
-    d.fx_hi = plane(c);
-    d.fy_dv = plane(c);
-    d.fy_lo = plane(c);
-    d.fy_hi = plane(c);
-    d.cf_dv = plane(c);
-    d.vlag = plane(c);
-    d.xl2x = plane(c);
-    d.xl2y = plane(c);
-    d.ifd = plane(c);
     d.dmx = plane(c);
     d.dmy = plane(c);
     d.dmc = plane(c);
@@ -441,8 +422,6 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
         c->arena_used += (c->fsz + 255) & ~size_t(255);
         return reinterpret_cast<uint8_t*>(p);
     };
-    d.cf_sx = reinterpret_cast<int8_t*>(bytes_plane());
-    d.cf_sy = reinterpret_cast<int8_t*>(bytes_plane());
     d.sliver = bytes_plane();
     for (int q = 0; q < 4; ++q) d.dflag[q] = bytes_plane();
     (void)bytes_plane();

@@ -102,12 +102,8 @@ struct Dev {
     double *nm[2], *ne[2], *nk[2], *nvol, *nm_mix, *ne_mix, *nrho_mix, *np_mix, *nnrx, *nnry, *nux, *nuy;
     // LagrangeResult (lagrange.hpp:38-45)
     double *q, *pmh, *ph[2], *uhx, *uhy, *ulx, *uly, *el[2], *vol_lag;
-    // remap scratch
-    double *me[2], *mcell, *mcell_lag;
-    double *fdx, *fdy, *xlcx, *xlcy, *wlx, *wly;
-    double *fx_dv, *fx_lo, *fx_hi, *fy_dv, *fy_lo, *fy_hi, *cf_dv;
-    int8_t *cf_sx, *cf_sy;
-    double *vlag, *rho[2], *xl2x, *xl2y, *ifd;
+    // remap scratch (the tile kernel keeps its geometry in shared memory)
+    double *me[2], *mcell;
     double *dmx, *dmy, *dmc;
     double *dfx_x, *dfx_y, *dfy_x, *dfy_y;  // dual-face momentum contributions
     double *dc_x[2], *dc_y[2];              // dual-corner contributions per pair

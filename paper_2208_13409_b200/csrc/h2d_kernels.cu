@@ -485,161 +485,111 @@ __device__ __forceinline__ void face_flux(double ym, double yp, double dmx, doub
     dv = 0.5 * (xlo + xhi) * (whi - wlo);
 }
 
-// make_axis_geom X/Y (remap.cpp:296-322), face / corner flux geometry
-// (:744-767), Lagrangian volumes and densities (:769-794), 2D centroids
-// (:797-803) and interfaces (:807-824), fused per 32x8 cell tile over the
-// ghosted range: the (33 x 9) node items of a tile go to shared memory (and
-// the owned ones to HBM for the flux pass), then each cell reads its four
-// faces and corners from shared memory.
-constexpr int GTX = 32, GTY = 8;
+// ---------------------------------------------------------------------------
+// The fused remap tile kernel (remap.cpp:739-991): for a 32x8 tile of cells it
+// computes, in shared memory, the axis geometry, face / corner flux geometry,
+// Lagrangian volumes, densities, centroids and interfaces of the tile plus a
+// two-cell halo (the reference's ghosted ranges at the mesh edge), then every
+// face and corner flux of the tile once, then gathers them per cell in the
+// reference's order and runs the per-cell part of finalize_cells.  Only the
+// State inputs (u_half, e_lag, m, k, normals) are read from HBM and only the
+// Work outputs (m, me, e, k, mcell, sliver flags) and the mass fluxes the dual
+// pass needs (dmx, dmy, dmc) are written back.
+// ---------------------------------------------------------------------------
+constexpr int RTX = 32, RTY = 8;
+constexpr int RCW = RTX + 4, RCH = RTY + 4;  // cell region [i0-2, i0+RTX+2)
+constexpr int RNW = RTX + 5, RNH = RTY + 5;  // node region [i0-2, i0+RTX+2]
+constexpr int RNN = RNW * RNH, RNC = RCW * RCH;
+constexpr int NXF = (RTX + 1) * RTY, NYF = RTX * (RTY + 1), NCF = (RTX + 1) * (RTY + 1);
+constexpr int RCELL1 = 9, RCELL2 = 16;  // cell arrays per material count
+
 template <int NM>
-__global__ void __launch_bounds__(GTX * GTY) k_geom_cells(Dev d) {
-    constexpr int W = GTX + 1, NN = W * (GTY + 1);
-    __shared__ double s_hx[NN], s_hy[NN], s_cf[NN], s_fdx[NN], s_fdy[NN], s_fx[NN], s_fy[NN];
-    __shared__ int8_t s_sx[NN], s_sy[NN];
-    __shared__ int s_halt;
-    const int tid = threadIdx.x;
-    if (tid == 0) s_halt = halted(d.ctl);
-    __syncthreads();
-    if (s_halt) return;
-    const int nx = d.nx, ny = d.ny;
-    const int imax = nx + G, jmax = ny + G;  // node range [-G, n+G]
-    const int i0 = -G + (int)blockIdx.x * GTX, j0 = -G + (int)blockIdx.y * GTY;
-    const double dt = step_dt(d.ctl);
-    const double cv = d.cv;
-    for (int t = tid; t < NN; t += GTX * GTY) {
-        const int i = i0 + t % W, j = j0 + t / W;
-        if (i > imax || j > jmax) continue;
-        const bool own = (i < i0 + GTX || i == imax) && (j < j0 + GTY || j == jmax);
-        const size_t n = ix(d, i, j);
-        const double u0x = d.uhx[n], u0y = d.uhy[n];
-        s_hx[t] = u0x;
-        s_hy[t] = u0y;
-        {  // cf_corner_flux, remap.cpp:16-25
-            const double ddx = u0x * dt, ddy = u0y * dt;
-            double dv = fabs(ddx * ddy);
-            int8_t sx = 0, sy = 0;
-            if (dv == 0.0) {
-                dv = 0.0;
-            } else {
-                sx = ddx > 0.0 ? 1 : -1;
-                sy = ddy > 0.0 ? 1 : -1;
-            }
-            s_cf[t] = dv;
-            s_sx[t] = sx;
-            s_sy[t] = sy;
-            if (own) {
-                d.cf_dv[n] = dv;
-                d.cf_sx[n] = sx;
-                d.cf_sy[n] = sy;
-            }
-            if (dv > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
-        }
-        if (j < jmax) {  // X geometry at (ia=i, ic=j) and the X face
-            const size_t nu = ix(d, i, j + 1);
-            const double ux1 = d.uhx[nu], uy1 = d.uhy[nu];
-            const double fd = 0.5 * (u0x + ux1) * dt;
-            double dv, wl, wh;
-            face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * u0x, dt * u0y, dt * ux1, dt * uy1, dv, wl, wh);
-            s_fdx[t] = fd;
-            s_fx[t] = dv;
-            if (own) {
-                d.fdx[n] = fd;
-                d.fx_dv[n] = dv;
-                d.fx_lo[n] = wl;
-                d.fx_hi[n] = wh;
-            }
-            if (fabs(dv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
-        }
-        if (i < imax) {  // Y geometry at (ia=j, ic=i), stored at (i, j), and the Y face
-            const size_t nr = ix(d, i + 1, j);
-            const double ux1 = d.uhx[nr], uy1 = d.uhy[nr];
-            const double fd = 0.5 * (u0y + uy1) * dt;
-            double dv, wl, wh;
-            face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * u0y, dt * u0x, dt * uy1, dt * ux1, dv, wl, wh);
-            s_fdy[t] = fd;
-            s_fy[t] = dv;
-            if (own) {
-                d.fdy[n] = fd;
-                d.fy_dv[n] = dv;
-                d.fy_lo[n] = wl;
-                d.fy_hi[n] = wh;
-            }
-            if (fabs(dv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
-        }
-    }
-    __syncthreads();
-    const int tx = tid % GTX, ty = tid / GTX;
-    const int i = i0 + tx, j = j0 + ty;
-    if (i >= nx + G || j >= ny + G) return;
-    const int q00 = tx + ty * W, q10 = q00 + 1, q01 = q00 + W, q11 = q01 + 1;
-    const size_t c = ix(d, i, j);
-    {  // xlagc / wlag of cell (i, j) on both axes
-        const double dlx = s_fdx[q00], drx = s_fdx[q10];
-        d.xlcx[c] = d.x0 + (i + 0.5) * d.dx + 0.5 * (dlx + drx);
-        d.wlx[c] = d.dx + (drx - dlx);
-        const double dly = s_fdy[q00], dry = s_fdy[q01];
-        d.xlcy[c] = d.y0 + (j + 0.5) * d.dy + 0.5 * (dly + dry);
-        d.wly[c] = d.dy + (dry - dly);
-    }
-    // corner_term of remap.cpp:775-785
-    auto cterm = [&](int q, int ni, int nj) -> double {
-        const double dv = s_cf[q];
-        if (dv == 0.0) return 0.0;
-        const int sx = s_sx[q], sy = s_sy[q];
-        const int di = sx > 0 ? ni - 1 : ni, dj = sy > 0 ? nj - 1 : nj;
-        if (di == i && dj == j) return dv;
-        const int ri = sx > 0 ? ni : ni - 1, rj = sy > 0 ? nj : nj - 1;
-        if (ri == i && rj == j) return -dv;
-        return 0.0;
-    };
-    double v = cv + s_fx[q10] - s_fx[q00] + s_fy[q01] - s_fy[q00];
-    v += cterm(q00, i, j) + cterm(q10, i + 1, j) + cterm(q01, i, j + 1) + cterm(q11, i + 1, j + 1);
-    if (v <= 0.0) raise(d.ctl, ekey(PH_COLLAPSED, j, i, 0));
-    d.vlag[c] = v;
-#pragma unroll
-    for (int a = 0; a < NM; ++a) {
-        const double ka = d.k[a][c];
-        d.rho[a][c] = ka > 0.0 ? d.m[a][c] / (ka * v) : 0.0;
-    }
-    const double mdx = 0.25 * (dt * s_hx[q00] + dt * s_hx[q10] + dt * s_hx[q01] + dt * s_hx[q11]);
-    const double mdy = 0.25 * (dt * s_hy[q00] + dt * s_hy[q10] + dt * s_hy[q01] + dt * s_hy[q11]);
-    d.xl2x[c] = (d.x0 + (i + 0.5) * d.dx) + mdx;
-    d.xl2y[c] = (d.y0 + (j + 0.5) * d.dy) + mdy;
-    if (NM == 2) {
-        const double k0 = d.k[0][c];
-        if (is_mixed(k0)) {
-            const double cx = d.x0 + (i + 0.5) * d.dx, cy = d.y0 + (j + 0.5) * d.dy;
-            const double lox = cx - 0.5 * d.dx + s_fdx[q00], loy = cy - 0.5 * d.dy + s_fdy[q00];
-            const double hix = cx + 0.5 * d.dx + s_fdx[q10], hiy = cy + 0.5 * d.dy + s_fdy[q01];
-            d.ifd[c] = place_interface(k0, d.nrx[c], d.nry[c], lox, loy, hix, hiy);
-        }
-    }
+struct Tile {
+    int ci0, cj0;  // origin of both regions: (i0 - 2, j0 - 2)
+    double *hx, *hy, *cf, *fdx, *fdy, *fxdv, *fydv;  // nodes
+    int8_t *sx, *sy;
+    double *vl, *rho[2], *el[2], *kk[2], *xl2x, *xl2y, *xlcx, *wlx, *xlcy, *wly, *ifd, *nrx, *nry;  // cells
+    double *fx[3][2], *fy[3][2], *fc[3][2];  // flux items: dm, dme, dva per material
+    __device__ __forceinline__ int c(int i, int j) const { return (i - ci0) + (j - cj0) * RCW; }
+    __device__ __forceinline__ int n(int i, int j) const { return (i - ci0) + (j - cj0) * RNW; }
+};
+
+template <int NM>
+constexpr size_t remap_smem_bytes() {
+    return sizeof(double) * (7 * RNN + (NM == 2 ? RCELL2 : RCELL1) * RNC + 3 * NM * (NXF + NYF + NCF)) + 2 * RNN + 64;
 }
 
-// box_frac0 + split_flux, remap.cpp:243-268, donor cell (di, dj)
 template <int NM>
-__device__ __forceinline__ void split_flux(const Dev& d, int di, int dj, double blox, double bloy, double bhix,
-                                           double bhiy, double dvol, double dva[2]) {
+__device__ __forceinline__ Tile<NM> carve_tile(char* base, int ci0, int cj0) {
+    Tile<NM> T;
+    T.ci0 = ci0;
+    T.cj0 = cj0;
+    double* p = reinterpret_cast<double*>(base);
+    auto take = [&](int n) {
+        double* r = p;
+        p += n;
+        return r;
+    };
+    T.hx = take(RNN);
+    T.hy = take(RNN);
+    T.cf = take(RNN);
+    T.fdx = take(RNN);
+    T.fdy = take(RNN);
+    T.fxdv = take(RNN);
+    T.fydv = take(RNN);
+    T.vl = take(RNC);
+    T.xl2x = take(RNC);
+    T.xl2y = take(RNC);
+    T.xlcx = take(RNC);
+    T.wlx = take(RNC);
+    T.xlcy = take(RNC);
+    T.wly = take(RNC);
+    for (int a = 0; a < NM; ++a) {
+        T.rho[a] = take(RNC);
+        T.el[a] = take(RNC);
+    }
+    if (NM == 2) {
+        T.kk[0] = take(RNC);
+        T.kk[1] = take(RNC);
+        T.ifd = take(RNC);
+        T.nrx = take(RNC);
+        T.nry = take(RNC);
+    }
+    for (int k = 0; k < 3; ++k)
+        for (int a = 0; a < NM; ++a) {
+            T.fx[k][a] = take(NXF);
+            T.fy[k][a] = take(NYF);
+            T.fc[k][a] = take(NCF);
+        }
+    int8_t* b = reinterpret_cast<int8_t*>(p);
+    T.sx = b;
+    T.sy = b + RNN;
+    return T;
+}
+
+// box_frac0 + split_flux, remap.cpp:243-268, donor cell (di, dj) of the tile
+template <int NM>
+__device__ __forceinline__ void split_flux_t(const Dev& d, const Tile<NM>& T, int di, int dj, double blox,
+                                             double bloy, double bhix, double bhiy, double dvol, double dva[2]) {
     dva[0] = dvol;
     dva[1] = 0.0;
     if (NM != 2) return;
-    const size_t c = ix(d, di, dj);
-    const double k0 = d.k[0][c];
+    const int c = T.c(di, dj);
+    const double k0 = T.kk[0][c];
     if (is_mixed(k0)) {
-        const double nx = d.nrx[c], ny = d.nry[c], dd = d.ifd[c];
+        const double nx = T.nrx[c], ny = T.nry[c], dd = T.ifd[c];
         const double cx = d.x0 + (di + 0.5) * d.dx, cy = d.y0 + (dj + 0.5) * d.dy;
-        const double lox = cx - 0.5 * d.dx + d.fdx[c], loy = cy - 0.5 * d.dy + d.fdy[c];
-        const double hix = cx + 0.5 * d.dx + d.fdx[ix(d, di + 1, dj)];
-        const double hiy = cy + 0.5 * d.dy + d.fdy[ix(d, di, dj + 1)];
+        const double lox = cx - 0.5 * d.dx + T.fdx[T.n(di, dj)], loy = cy - 0.5 * d.dy + T.fdy[T.n(di, dj)];
+        const double hix = cx + 0.5 * d.dx + T.fdx[T.n(di + 1, dj)];
+        const double hiy = cy + 0.5 * d.dy + T.fdy[T.n(di, dj + 1)];
         const double rcx = 0.5 * (lox + hix), rcy = 0.5 * (loy + hiy);
         const double bcx = 0.5 * (blox + bhix), bcy = 0.5 * (bloy + bhiy);
         const double bw = bhix - blox, bh = bhiy - bloy;
         const double area = bw * bh;
         double f0;
         if (!(area > 0.0)) {
-            const double s = (nx * (bcx - rcx) + ny * (bcy - rcy)) - dd;
-            f0 = s <= 0.0 ? 1.0 : 0.0;
+            const double sdist = (nx * (bcx - rcx) + ny * (bcy - rcy)) - dd;
+            f0 = sdist <= 0.0 ? 1.0 : 0.0;
         } else {
             const double dbox = dd - (nx * (bcx - rcx) + ny * (bcy - rcy));
             f0 = clipped_fraction(bw, bh, nx, ny, dbox);
@@ -652,54 +602,59 @@ __device__ __forceinline__ void split_flux(const Dev& d, int di, int dj, double 
     }
 }
 
-// Face fluxes, remap.cpp:850-918. AX = 1: X faces (ia = i, ic = j); AX = 0:
-// Y faces (ia = j, ic = i), both stored at device (i, j).
-// Returns the face's total mass flux (dmx / dmy entry); dm, dme, dva get the
-// per-material contributions (dva = 0 marks a skipped material).
+// Face flux (remap.cpp:850-918) of the X (AX = 1, at node i, row j) or Y
+// (AX = 0, at column i, node row j) face; returns the face's dmx / dmy entry.
 template <int NM, int AX>
-__device__ __forceinline__ double face_item(const Dev& d, int i, int j, double* odm, double* odme, double* odva) {
-    const size_t f = ix(d, i, j);
-    const double dvol = AX ? d.fx_dv[f] : d.fy_dv[f];
+__device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, int i, int j, double dt,
+                                              double* odm, double* odme, double* odva) {
+    const int qn = T.n(i, j);
+    const double dvol = AX ? T.fxdv[qn] : T.fydv[qn];
     double dmtot = 0.0;
-    double dva[2] = {0.0, 0.0};
-    double rfv[2] = {0.0, 0.0}, efv[2] = {0.0, 0.0};
+    double dva[2] = {0.0, 0.0}, rfv[2] = {0.0, 0.0}, efv[2] = {0.0, 0.0};
     if (dvol != 0.0) {
         const int ia = AX ? i : j, ic = AX ? j : i;
         const int ia_d = dvol > 0.0 ? ia - 1 : ia;
         const double sgn = dvol > 0.0 ? 1.0 : -1.0;
         const int cdi = AX ? ia_d : ic, cdj = AX ? ic : ia_d;
-        const double wlo = AX ? d.fx_lo[f] : d.fy_lo[f], whi = AX ? d.fx_hi[f] : d.fy_hi[f];
+        // the flux window [wlo, whi] of cf_face_flux (recomputed, same bits)
+        double dv2, wlo, whi;
+        const int q1 = AX ? T.n(i, j + 1) : T.n(i + 1, j);
+        if (AX)
+            face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * T.hx[qn], dt * T.hy[qn], dt * T.hx[q1],
+                      dt * T.hy[q1], dv2, wlo, whi);
+        else
+            face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * T.hy[qn], dt * T.hx[qn], dt * T.hy[q1],
+                      dt * T.hx[q1], dv2, wlo, whi);
         const double wwin = whi - wlo;
         const double width = dvol / wwin;
         const double f0pos = AX ? d.x0 + ia * d.dx : d.y0 + ia * d.dy;
         const double blo = rmin(f0pos, f0pos + width), bhi = rmax(f0pos, f0pos + width);
         if (AX)
-            split_flux<NM>(d, cdi, cdj, blo, wlo, bhi, whi, dvol, dva);
+            split_flux_t<NM>(d, T, cdi, cdj, blo, wlo, bhi, whi, dvol, dva);
         else
-            split_flux<NM>(d, cdi, cdj, wlo, blo, whi, bhi, dvol, dva);
+            split_flux_t<NM>(d, T, cdi, cdj, wlo, blo, whi, bhi, dvol, dva);
         bool bad = false;
-        const size_t cm = AX ? ix(d, ia_d - 1, ic) : ix(d, ic, ia_d - 1);
-        const size_t cc = AX ? ix(d, ia_d, ic) : ix(d, ic, ia_d);
-        const size_t cp = AX ? ix(d, ia_d + 1, ic) : ix(d, ic, ia_d + 1);
+        const int cm = AX ? T.c(ia_d - 1, ic) : T.c(ic, ia_d - 1);
+        const int cc = AX ? T.c(ia_d, ic) : T.c(ic, ia_d);
+        const int cp = AX ? T.c(ia_d + 1, ic) : T.c(ic, ia_d + 1);
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
             if (dva[a] == 0.0) continue;
             int ord = d.face_order;
             if (ord == 2 && NM == 2 && d.degrade &&
-                (d.k[a][cm] < 1.0 - kPureTol || d.k[a][cc] < 1.0 - kPureTol || d.k[a][cp] < 1.0 - kPureTol))
+                (T.kk[a][cm] < 1.0 - kPureTol || T.kk[a][cc] < 1.0 - kPureTol || T.kk[a][cp] < 1.0 - kPureTol))
                 ord = 1;
             double rf, ef;
             if (ord <= 1) {
-                rf = d.rho[a][cc];
-                ef = d.el[a][cc];
+                rf = T.rho[a][cc];
+                ef = T.el[a][cc];
             } else {
-                const double* xl = AX ? d.xlcx : d.xlcy;
-                const double* wl = AX ? d.wlx : d.wly;
-                const double* fd = AX ? d.fdx : d.fdy;
+                const double* xl = AX ? T.xlcx : T.xlcy;
+                const double* wl = AX ? T.wlx : T.wly;
                 const double x0 = xl[cm], x1 = xl[cc], x2 = xl[cp];
-                const double lw = wl[cc], ufdt = fd[f];
-                rf = face_value2(d.rho[a][cm], d.rho[a][cc], d.rho[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
-                ef = face_value2(d.el[a][cm], d.el[a][cc], d.el[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
+                const double lw = wl[cc], ufdt = AX ? T.fdx[qn] : T.fdy[qn];
+                rf = face_value2(T.rho[a][cm], T.rho[a][cc], T.rho[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
+                ef = face_value2(T.el[a][cm], T.el[a][cc], T.el[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
             }
             rfv[a] = rf;
             efv[a] = ef;
@@ -721,24 +676,24 @@ __device__ __forceinline__ double face_item(const Dev& d, int i, int j, double* 
     return dmtot;
 }
 
-// Corner fluxes, remap.cpp:923-983, per node (i, j) in [0, nx] x [0, ny].
+// Corner flux (remap.cpp:923-983) at node (i, j); returns the dmc entry.
 template <int NM>
-__device__ __forceinline__ double corner_item(const Dev& d, int i, int j, double* odm, double* odme, double* odva) {
-    const size_t n = ix(d, i, j);
-    const double cdv = d.cf_dv[n];
+__device__ __forceinline__ double corner_item_t(const Dev& d, const Tile<NM>& T, int i, int j, double dt,
+                                                double* odm, double* odme, double* odva) {
+    const int qn = T.n(i, j);
+    const double cdv = T.cf[qn];
     double dva[2] = {0.0, 0.0}, rfv[2] = {0.0, 0.0}, efv[2] = {0.0, 0.0};
     double dmtot = 0.0;
     if (cdv != 0.0) {
-        const double dt = step_dt(d.ctl);
-        const int sx = d.cf_sx[n], sy = d.cf_sy[n];
+        const int sx = T.sx[qn], sy = T.sy[qn];
         const int di = sx > 0 ? i - 1 : i, dj = sy > 0 ? j - 1 : j;
         const double npx = d.x0 + i * d.dx, npy = d.y0 + j * d.dy;
-        const double ddx = dt * d.uhx[n], ddy = dt * d.uhy[n];
+        const double ddx = dt * T.hx[qn], ddy = dt * T.hy[qn];
         const double blox = rmin(npx, npx + ddx), bloy = rmin(npy, npy + ddy);
         const double bhix = rmax(npx, npx + ddx), bhiy = rmax(npy, npy + ddy);
-        split_flux<NM>(d, di, dj, blox, bloy, bhix, bhiy, cdv, dva);
-        const size_t dc = ix(d, di, dj);
-        const double lwx = d.wlx[dc], lwy = d.wly[dc];
+        split_flux_t<NM>(d, T, di, dj, blox, bloy, bhix, bhiy, cdv, dva);
+        const int dc = T.c(di, dj);
+        const double lwx = T.wlx[dc], lwy = T.wly[dc];
         bool bad = false;
         const bool lin_cfg = d.corner_diag && d.face_order > 1;
 #pragma unroll
@@ -748,26 +703,26 @@ __device__ __forceinline__ double corner_item(const Dev& d, int i, int j, double
             if (lin && NM == 2 && d.degrade) {
                 for (int q = -1; q <= 1 && lin; ++q)
                     for (int p = -1; p <= 1; ++p)
-                        if (d.k[a][ix(d, di + p, dj + q)] < 1.0 - kPureTol) {
+                        if (T.kk[a][T.c(di + p, dj + q)] < 1.0 - kPureTol) {
                             lin = false;
                             break;
                         }
             }
             double rf, ef;
             if (!lin) {
-                rf = d.rho[a][dc];
-                ef = d.el[a][dc];
+                rf = T.rho[a][dc];
+                ef = T.el[a][dc];
             } else {
                 double sr[9], se[9], xlx[9], xly[9];
 #pragma unroll
                 for (int q = 0; q < 3; ++q)
 #pragma unroll
                     for (int p = 0; p < 3; ++p) {
-                        const size_t s = ix(d, di + p - 1, dj + q - 1);
-                        sr[p * 3 + q] = d.rho[a][s];
-                        se[p * 3 + q] = d.el[a][s];
-                        xlx[p * 3 + q] = d.xl2x[s];
-                        xly[p * 3 + q] = d.xl2y[s];
+                        const int sidx = T.c(di + p - 1, dj + q - 1);
+                        sr[p * 3 + q] = T.rho[a][sidx];
+                        se[p * 3 + q] = T.el[a][sidx];
+                        xlx[p * 3 + q] = T.xl2x[sidx];
+                        xly[p * 3 + q] = T.xl2y[sidx];
                     }
                 rf = rmax(corner_diag(d, sr, xlx, xly, ddx, ddy, lwx, lwy, bad), 0.0);
                 ef = corner_diag(d, se, xlx, xly, ddx, ddy, lwx, lwy, bad);
@@ -847,123 +802,220 @@ __global__ void k_ghost_multi(Dev d, FieldList cells, FieldList nodes, int flux,
     }
 }
 
-// Face + corner fluxes (remap.cpp:849-983) and their gather in reference
-// order (App. C item 3), fused per 32x8 cell tile: every face / corner flux of
-// the tile (one extra column / row of faces and corners) is computed once into
-// shared memory, then each cell adds its contributions in program order and
-// runs the per-cell part of finalize_cells (remap.cpp:154-192).
-constexpr int FTX = 32, FTY = 8;
 template <int NM>
-__global__ void __launch_bounds__(FTX * FTY) k_flux_gather(Dev d) {
-    constexpr int NXF = (FTX + 1) * FTY, NYF = FTX * (FTY + 1), NCF = (FTX + 1) * (FTY + 1);
-    __shared__ double sxf[3][NM][NXF];
-    __shared__ double syf[3][NM][NYF];
-    __shared__ double scf[3][NM][NCF];
+__global__ void __launch_bounds__(RTX * RTY) k_remap_tile(Dev d) {
+    extern __shared__ __align__(16) char smem[];
     __shared__ int s_halt;
     const int tid = threadIdx.x;
     if (tid == 0) s_halt = halted(d.ctl);
     __syncthreads();
     if (s_halt) return;
     const int nx = d.nx, ny = d.ny;
-    const int i0 = blockIdx.x * FTX, j0 = blockIdx.y * FTY;
-    double dm[2], dme[2], dva[2];
-    for (int t = tid; t < NXF; t += FTX * FTY) {  // X faces ia in [i0, i0+FTX], rows [j0, j0+FTY)
-        const int ia = i0 + t % (FTX + 1), ic = j0 + t / (FTX + 1);
-        dva[0] = dva[1] = 0.0;
-        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
-        if (ia <= nx && ic < ny) {
-            const double tot = face_item<NM, 1>(d, ia, ic, dm, dme, dva);
-            if (ia < i0 + FTX || ia == nx) d.dmx[ix(d, ia, ic)] = tot;
+    const int i0 = blockIdx.x * RTX, j0 = blockIdx.y * RTY;
+    const Tile<NM> T = carve_tile<NM>(smem, i0 - G, j0 - G);
+    const double dt = step_dt(d.ctl);
+    const double cv = d.cv;
+    // ---- node items: u_half, corner flux, axis geometry, face flux volumes
+    // (make_axis_geom remap.cpp:296-322, flux geometry :744-767)
+    for (int t = tid; t < RNN; t += RTX * RTY) {
+        const int i = T.ci0 + t % RNW, j = T.cj0 + t / RNW;
+        double hx = 0.0, hy = 0.0, cfv = 0.0, fdx = 0.0, fdy = 0.0, fxv = 0.0, fyv = 0.0;
+        int8_t sx = 0, sy = 0;
+        if (i <= nx + G && j <= ny + G) {
+            const size_t n = ix(d, i, j);
+            hx = d.uhx[n];
+            hy = d.uhy[n];
+            const double ddx = hx * dt, ddy = hy * dt;  // cf_corner_flux, remap.cpp:16-25
+            cfv = fabs(ddx * ddy);
+            if (cfv == 0.0) {
+                cfv = 0.0;
+            } else {
+                sx = ddx > 0.0 ? 1 : -1;
+                sy = ddy > 0.0 ? 1 : -1;
+            }
+            if (cfv > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
+            if (j < ny + G) {
+                const size_t nu = ix(d, i, j + 1);
+                const double ux1 = d.uhx[nu], uy1 = d.uhy[nu];
+                fdx = 0.5 * (hx + ux1) * dt;
+                double wl, wh;
+                face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * hx, dt * hy, dt * ux1, dt * uy1, fxv, wl, wh);
+                if (fabs(fxv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
+            }
+            if (i < nx + G) {
+                const size_t nr = ix(d, i + 1, j);
+                const double ux1 = d.uhx[nr], uy1 = d.uhy[nr];
+                fdy = 0.5 * (hy + uy1) * dt;
+                double wl, wh;
+                face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * hy, dt * hx, dt * uy1, dt * ux1, fyv, wl, wh);
+                if (fabs(fyv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
+            }
         }
-#pragma unroll
-        for (int a = 0; a < NM; ++a) {
-            sxf[0][a][t] = dm[a];
-            sxf[1][a][t] = dme[a];
-            sxf[2][a][t] = dva[a];
-        }
+        T.hx[t] = hx;
+        T.hy[t] = hy;
+        T.cf[t] = cfv;
+        T.sx[t] = sx;
+        T.sy[t] = sy;
+        T.fdx[t] = fdx;
+        T.fdy[t] = fdy;
+        T.fxdv[t] = fxv;
+        T.fydv[t] = fyv;
     }
-    for (int t = tid; t < NYF; t += FTX * FTY) {  // Y faces: columns [i0, i0+FTX), ja in [j0, j0+FTY]
-        const int ic = i0 + t % FTX, ja = j0 + t / FTX;
-        dva[0] = dva[1] = 0.0;
-        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
-        if (ic < nx && ja <= ny) {
-            const double tot = face_item<NM, 0>(d, ic, ja, dm, dme, dva);
-            if (ja < j0 + FTY || ja == ny) d.dmy[ix(d, ic, ja)] = tot;
-        }
+    __syncthreads();
+    // ---- cell items: xlagc/wlag, Lagrangian volume, densities, centroids,
+    // interfaces (remap.cpp:769-824)
+    for (int t = tid; t < RNC; t += RTX * RTY) {
+        const int i = T.ci0 + t % RCW, j = T.cj0 + t / RCW;
+        if (i >= nx + G || j >= ny + G) continue;
+        const int q00 = T.n(i, j), q10 = q00 + 1, q01 = q00 + RNW, q11 = q01 + 1;
+        const double dlx = T.fdx[q00], drx = T.fdx[q10];
+        T.xlcx[t] = d.x0 + (i + 0.5) * d.dx + 0.5 * (dlx + drx);
+        T.wlx[t] = d.dx + (drx - dlx);
+        const double dly = T.fdy[q00], dry = T.fdy[q01];
+        T.xlcy[t] = d.y0 + (j + 0.5) * d.dy + 0.5 * (dly + dry);
+        T.wly[t] = d.dy + (dry - dly);
+        auto cterm = [&](int q, int ni, int nj) -> double {  // remap.cpp:775-785
+            const double dv = T.cf[q];
+            if (dv == 0.0) return 0.0;
+            const int csx = T.sx[q], csy = T.sy[q];
+            const int di = csx > 0 ? ni - 1 : ni, dj = csy > 0 ? nj - 1 : nj;
+            if (di == i && dj == j) return dv;
+            const int ri = csx > 0 ? ni : ni - 1, rj = csy > 0 ? nj : nj - 1;
+            if (ri == i && rj == j) return -dv;
+            return 0.0;
+        };
+        double v = cv + T.fxdv[q10] - T.fxdv[q00] + T.fydv[q01] - T.fydv[q00];
+        v += cterm(q00, i, j) + cterm(q10, i + 1, j) + cterm(q01, i, j + 1) + cterm(q11, i + 1, j + 1);
+        if (v <= 0.0) raise(d.ctl, ekey(PH_COLLAPSED, j, i, 0));
+        T.vl[t] = v;
+        const size_t c = ix(d, i, j);
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
-            syf[0][a][t] = dm[a];
-            syf[1][a][t] = dme[a];
-            syf[2][a][t] = dva[a];
+            const double ka = d.k[a][c];
+            T.rho[a][t] = ka > 0.0 ? d.m[a][c] / (ka * v) : 0.0;
+            T.el[a][t] = d.el[a][c];
+            if (NM == 2) T.kk[a][t] = ka;
         }
-    }
-    for (int t = tid; t < NCF; t += FTX * FTY) {  // corner nodes [i0, i0+FTX] x [j0, j0+FTY]
-        const int ni = i0 + t % (FTX + 1), nj = j0 + t / (FTX + 1);
-        dva[0] = dva[1] = 0.0;
-        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
-        if (ni <= nx && nj <= ny) {
-            const double tot = corner_item<NM>(d, ni, nj, dm, dme, dva);
-            if ((ni < i0 + FTX || ni == nx) && (nj < j0 + FTY || nj == ny)) d.dmc[ix(d, ni, nj)] = tot;
-        }
-#pragma unroll
-        for (int a = 0; a < NM; ++a) {
-            scf[0][a][t] = dm[a];
-            scf[1][a][t] = dme[a];
-            scf[2][a][t] = dva[a];
+        const double mdx = 0.25 * (dt * T.hx[q00] + dt * T.hx[q10] + dt * T.hx[q01] + dt * T.hx[q11]);
+        const double mdy = 0.25 * (dt * T.hy[q00] + dt * T.hy[q10] + dt * T.hy[q01] + dt * T.hy[q11]);
+        T.xl2x[t] = (d.x0 + (i + 0.5) * d.dx) + mdx;
+        T.xl2y[t] = (d.y0 + (j + 0.5) * d.dy) + mdy;
+        if (NM == 2) {
+            const double k0 = T.kk[0][t];
+            const double nrx = d.nrx[c], nry = d.nry[c];
+            T.nrx[t] = nrx;
+            T.nry[t] = nry;
+            double dd = 0.0;
+            if (is_mixed(k0)) {
+                const double cx = d.x0 + (i + 0.5) * d.dx, cy = d.y0 + (j + 0.5) * d.dy;
+                dd = place_interface(k0, nrx, nry, cx - 0.5 * d.dx + dlx, cy - 0.5 * d.dy + dly,
+                                     cx + 0.5 * d.dx + drx, cy + 0.5 * d.dy + dry);
+            }
+            T.ifd[t] = dd;
         }
     }
     __syncthreads();
-    const int tx = tid % FTX, ty = tid / FTX;
+    // ---- face and corner fluxes of the tile, once each
+    double dm[2], dme[2], dva[2];
+    for (int t = tid; t < NXF; t += RTX * RTY) {  // X faces ia in [i0, i0+RTX], rows [j0, j0+RTY)
+        const int ia = i0 + t % (RTX + 1), ic = j0 + t / (RTX + 1);
+        dva[0] = dva[1] = 0.0;
+        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
+        if (ia <= nx && ic < ny) {
+            const double tot = face_item_t<NM, 1>(d, T, ia, ic, dt, dm, dme, dva);
+            if (ia < i0 + RTX || ia == nx) d.dmx[ix(d, ia, ic)] = tot;
+        }
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            T.fx[0][a][t] = dm[a];
+            T.fx[1][a][t] = dme[a];
+            T.fx[2][a][t] = dva[a];
+        }
+    }
+    for (int t = tid; t < NYF; t += RTX * RTY) {  // Y faces: columns [i0, i0+RTX), ja in [j0, j0+RTY]
+        const int ic = i0 + t % RTX, ja = j0 + t / RTX;
+        dva[0] = dva[1] = 0.0;
+        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
+        if (ic < nx && ja <= ny) {
+            const double tot = face_item_t<NM, 0>(d, T, ic, ja, dt, dm, dme, dva);
+            if (ja < j0 + RTY || ja == ny) d.dmy[ix(d, ic, ja)] = tot;
+        }
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            T.fy[0][a][t] = dm[a];
+            T.fy[1][a][t] = dme[a];
+            T.fy[2][a][t] = dva[a];
+        }
+    }
+    for (int t = tid; t < NCF; t += RTX * RTY) {  // corner nodes [i0, i0+RTX] x [j0, j0+RTY]
+        const int ni = i0 + t % (RTX + 1), nj = j0 + t / (RTX + 1);
+        dva[0] = dva[1] = 0.0;
+        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
+        if (ni <= nx && nj <= ny) {
+            const double tot = corner_item_t<NM>(d, T, ni, nj, dt, dm, dme, dva);
+            if ((ni < i0 + RTX || ni == nx) && (nj < j0 + RTY || nj == ny)) d.dmc[ix(d, ni, nj)] = tot;
+        }
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            T.fc[0][a][t] = dm[a];
+            T.fc[1][a][t] = dme[a];
+            T.fc[2][a][t] = dva[a];
+        }
+    }
+    __syncthreads();
+    // ---- gather in reference order (App. C item 3)
+    const int tx = tid % RTX, ty = tid / RTX;
     const int i = i0 + tx, j = j0 + ty;
     if (i >= nx || j >= ny) return;
     const size_t c = ix(d, i, j);
-    const int xl = tx + ty * (FTX + 1), xr = xl + 1;       // X faces i, i+1
-    const int yb = tx + ty * FTX, yt = yb + FTX;            // Y faces j, j+1
-    const int cq[4] = {tx + ty * (FTX + 1), tx + 1 + ty * (FTX + 1), tx + (ty + 1) * (FTX + 1),
-                       tx + 1 + (ty + 1) * (FTX + 1)};
+    const int tc = T.c(i, j);
+    const int xl = tx + ty * (RTX + 1), xr = xl + 1;
+    const int yb = tx + ty * RTX, yt = yb + RTX;
+    const int cq[4] = {tx + ty * (RTX + 1), tx + 1 + ty * (RTX + 1), tx + (ty + 1) * (RTX + 1),
+                       tx + 1 + (ty + 1) * (RTX + 1)};
     const int ndi[4] = {i, i + 1, i, i + 1}, ndj[4] = {j, j, j + 1, j + 1};
-    const double vl = d.vlag[c];
+    const double vl = T.vl[tc];
     double m[2], me[2], va[2];
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
         const double m0 = d.m[a][c];
-        double mm = m0, mme = m0 * d.el[a][c], vv = d.k[a][c] * vl;
-        if (sxf[2][a][xl] != 0.0) {
-            mm += sxf[0][a][xl];
-            mme += sxf[1][a][xl];
-            vv += sxf[2][a][xl];
+        double mm = m0, mme = m0 * T.el[a][tc], vv = d.k[a][c] * vl;
+        if (T.fx[2][a][xl] != 0.0) {
+            mm += T.fx[0][a][xl];
+            mme += T.fx[1][a][xl];
+            vv += T.fx[2][a][xl];
         }
-        if (sxf[2][a][xr] != 0.0) {
-            mm += -sxf[0][a][xr];
-            mme += -sxf[1][a][xr];
-            vv += -sxf[2][a][xr];
+        if (T.fx[2][a][xr] != 0.0) {
+            mm += -T.fx[0][a][xr];
+            mme += -T.fx[1][a][xr];
+            vv += -T.fx[2][a][xr];
         }
-        if (syf[2][a][yb] != 0.0) {
-            mm += syf[0][a][yb];
-            mme += syf[1][a][yb];
-            vv += syf[2][a][yb];
+        if (T.fy[2][a][yb] != 0.0) {
+            mm += T.fy[0][a][yb];
+            mme += T.fy[1][a][yb];
+            vv += T.fy[2][a][yb];
         }
-        if (syf[2][a][yt] != 0.0) {
-            mm += -syf[0][a][yt];
-            mme += -syf[1][a][yt];
-            vv += -syf[2][a][yt];
+        if (T.fy[2][a][yt] != 0.0) {
+            mm += -T.fy[0][a][yt];
+            mme += -T.fy[1][a][yt];
+            vv += -T.fy[2][a][yt];
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const double dv = scf[2][a][cq[q]];
+            const double dv = T.fc[2][a][cq[q]];
             if (dv == 0.0) continue;
-            const size_t n = ix(d, ndi[q], ndj[q]);
-            const int sx = d.cf_sx[n], sy = d.cf_sy[n];
-            const int di = sx > 0 ? ndi[q] - 1 : ndi[q], dj = sy > 0 ? ndj[q] - 1 : ndj[q];
+            const int qn = T.n(ndi[q], ndj[q]);
+            const int csx = T.sx[qn], csy = T.sy[qn];
+            const int di = csx > 0 ? ndi[q] - 1 : ndi[q], dj = csy > 0 ? ndj[q] - 1 : ndj[q];
             if (di == i && dj == j) {
-                mm += -scf[0][a][cq[q]];
-                mme += -scf[1][a][cq[q]];
+                mm += -T.fc[0][a][cq[q]];
+                mme += -T.fc[1][a][cq[q]];
                 vv += -dv;
             } else {
-                const int ri = sx > 0 ? ndi[q] : ndi[q] - 1, rj = sy > 0 ? ndj[q] : ndj[q] - 1;
+                const int ri = csx > 0 ? ndi[q] : ndi[q] - 1, rj = csy > 0 ? ndj[q] : ndj[q] - 1;
                 if (ri == i && rj == j) {
-                    mm += scf[0][a][cq[q]];
-                    mme += scf[1][a][cq[q]];
+                    mm += T.fc[0][a][cq[q]];
+                    mme += T.fc[1][a][cq[q]];
                     vv += dv;
                 }
             }
@@ -973,7 +1025,6 @@ __global__ void __launch_bounds__(FTX * FTY) k_flux_gather(Dev d) {
         va[a] = vv;
     }
     // finalize_cells, per-cell part
-    const double cv = d.cv;
     double k[2] = {1.0, 0.0};
     uint8_t sl = 0;
     if (NM == 2) {
@@ -1031,6 +1082,7 @@ __global__ void __launch_bounds__(FTX * FTY) k_flux_gather(Dev d) {
         if (sl) atomicAdd(&d.row_slivers[j], 1);
     }
 }
+
 
 // Sequential sliver redistribution (remap.cpp:194-226) in row-major order by
 // one warp: rows with pending slivers are scanned 32 cells at a time.
@@ -1176,10 +1228,12 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const size_t n = ix(d, qi[q], qj[q]);
-                const double cdv = d.cf_dv[n], dmcv = d.dmc[n];
-                const int csx = d.cf_sx[n], csy = d.cf_sy[n];
+                // cf_corner_flux (remap.cpp:16-25) recomputed from u_half
+                const double ddx = d.uhx[n] * dt, ddy = d.uhy[n] * dt;
+                const double cdv = fabs(ddx * ddy), dmcv = d.dmc[n];
                 sc[q] = 0.0;
                 if (cdv == 0.0 || dmcv == 0.0) continue;
+                const int csx = ddx > 0.0 ? 1 : -1, csy = ddy > 0.0 ? 1 : -1;
                 if (csx == sx && csy == sy)
                     sc[q] = -dmcv;
                 else if (csx == -sx && csy == -sy)
@@ -1201,9 +1255,14 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
                 const int ci0 = i < pi ? i : pi, cj0 = j < pj ? j : pj;
                 const int ci = d.per_x ? ((ci0 % nx) + nx) % nx : ci0;
                 const int cj = d.per_y ? ((cj0 % ny) + ny) % ny : cj0;
-                const size_t cc = ix(d, ci, cj);
-                const double mdx = d.xl2x[cc] - (d.x0 + (ci + 0.5) * d.dx);
-                const double mdy = d.xl2y[cc] - (d.y0 + (cj + 0.5) * d.dy);
+                // xlag2 of cell (ci, cj) (remap.cpp:797-803) recomputed from u_half
+                const size_t n00 = ix(d, ci, cj), n10 = ix(d, ci + 1, cj), n01 = ix(d, ci, cj + 1),
+                             n11 = ix(d, ci + 1, cj + 1);
+                const double xmd = 0.25 * (dt * d.uhx[n00] + dt * d.uhx[n10] + dt * d.uhx[n01] + dt * d.uhx[n11]);
+                const double ymd = 0.25 * (dt * d.uhy[n00] + dt * d.uhy[n10] + dt * d.uhy[n01] + dt * d.uhy[n11]);
+                const double cxc = d.x0 + (ci + 0.5) * d.dx, cyc = d.y0 + (cj + 0.5) * d.dy;
+                const double mdx = (cxc + xmd) - cxc;
+                const double mdy = (cyc + ymd) - cyc;
                 const double dirx = incoming ? -sx : sx, diry = incoming ? -sy : sy;
                 const double dxp = dirx * rmax(fabs(mdx), 1e-300);
                 const double dyp = diry * rmax(fabs(mdy), 1e-300);
@@ -1523,23 +1582,27 @@ void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
     launch_ghost_multi(d, fl, fn, 0, 1, s);
 }
 
+void remap_init() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(k_remap_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<1>());
+    cudaFuncSetAttribute(k_remap_tile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<2>());
+    done = true;
+}
+
 void launch_remap(const Dev& d, cudaStream_t s) {
+    remap_init();
     const int nx = d.nx, ny = d.ny;
     const bool two = d.nmat == 2;
     const dim3 gall = grid_rect(nx + 1 + 2 * G, ny + 1 + 2 * G);
     const dim3 gc = grid_rect(nx, ny), gn = grid_rect(nx + 1, ny + 1);
     if (!d.remap_velocity) { k_copy_u<<<gall, blk2(), 0, s>>>(d); ++g_launches; }
-    const dim3 ggc((unsigned)((nx + 2 * G + GTX - 1) / GTX), (unsigned)((ny + 2 * G + GTY - 1) / GTY));
-    if (two)
-        { k_geom_cells<2><<<ggc, GTX * GTY, 0, s>>>(d); ++g_launches; }
-    else
-        { k_geom_cells<1><<<ggc, GTX * GTY, 0, s>>>(d); ++g_launches; }
-    const dim3 gft((unsigned)((nx + FTX - 1) / FTX), (unsigned)((ny + FTY - 1) / FTY));
+    const dim3 gft((unsigned)((nx + RTX - 1) / RTX), (unsigned)((ny + RTY - 1) / RTY));
     if (two) {
-        { k_flux_gather<2><<<gft, FTX * FTY, 0, s>>>(d); ++g_launches; }
+        { k_remap_tile<2><<<gft, RTX * RTY, remap_smem_bytes<2>(), s>>>(d); ++g_launches; }
         { k_slivers<<<1, 32, 0, s>>>(d); ++g_launches; }
     } else {
-        { k_flux_gather<1><<<gft, FTX * FTY, 0, s>>>(d); ++g_launches; }
+        { k_remap_tile<1><<<gft, RTX * RTY, remap_smem_bytes<1>(), s>>>(d); ++g_launches; }
     }
     // finalize_cells ghost fill (remap.cpp:227-233) + face / corner flux ghosts
     FieldList fl{};
