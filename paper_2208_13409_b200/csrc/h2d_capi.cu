@@ -138,6 +138,8 @@ int ctl_reset(h2d_ctx* c) {
     h.cur = c->cur;
     h.step_floor = h.step_clip = h.step_fix = 0;
     h.wmax_bits = h.kviol_bits = 0;
+    h.next_wmax_bits = 0;
+    h.next_err_key = kNoErr;
     return ctl_push(c);
 }
 
@@ -263,16 +265,11 @@ int fill_ghosts_cur(h2d_ctx* c, int parity) {
 }
 
 // One run-loop step (harness.cpp:390-412) for the state in `parity`.
-void enqueue_step(h2d_ctx* c, int parity) {
-    const Dev d = make_dev(c, parity, 1);
-    launch_begin(c->ctl, 0, 0.0, c->st);
-    launch_cfl(d, 1, c->st);
-    launch_lagrange(d, 0, c->st);
-    cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->ny, c->st);
-    launch_remap(d, c->st);
-    launch_commit(c->ctl, 1, c->st);
-    launch_nan_finish(d, c->st);
-}
+void enqueue_step(h2d_ctx* c, int parity) { launch_step(make_dev(c, parity, 1), c->st, c->base.row_slivers); }
+
+// cfl_dt of the current State into the control block's "next" slots, which
+// the first k_step_start of a run consumes (later steps get them from k_post)
+void enqueue_cfl_next(h2d_ctx* c) { launch_cfl_next(make_dev(c, c->cur, 1), c->st); }
 
 // The run-loop step is a fixed sequence of ~20 kernels whose arguments only
 // depend on the State parity: capture it once per parity as a CUDA graph and
@@ -333,6 +330,10 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
     c->P = ((m.nx + 1 + 2 * G) + 31) / 32 * 32;
     c->R = m.ny + 1 + 2 * G;
     c->fsz = (size_t)c->P * (size_t)c->R;
+    if (c->fsz >= (size_t)1 << 31) {  // device plane offsets are 32-bit
+        h2d_destroy(c);
+        return H2D_ERR_INVALID;
+    }
     const int nm = c->nmat;
     // plane count: 2 x State (6 + 3 nm) + Lagrange (7 + 2 nm) + remap scratch
     const size_t planes = 2 * (9 + 3 * nm) + (7 + 2 * nm) + (25 + 15 * nm) + 8;
@@ -667,6 +668,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
     int parity = c->cur;
     int rc = 0;
     if ((rc = ensure_graphs(c))) return rc;
+    enqueue_cfl_next(c);
     // Launch in chunks; the device control block turns every kernel after the
     // loop condition fails (or after an error) into a no-op.
     for (;;) {
@@ -756,18 +758,20 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[4]
     h.dt_log = nullptr;
     h.dt_log_cap = 0;
     if (int rc = ctl_push(c)) return rc;
+    // the wave speed of the current State (normally left by the previous
+    // step's k_post) is recomputed outside the timed region
+    enqueue_cfl_next(c);
     if (phases) {  // un-graphed launch with events between the phases
         const Dev d = make_dev(c, c->cur, 1);
         CK(cudaEventRecord(c->ev[0], c->st));
-        launch_begin(c->ctl, 0, 0.0, c->st);
-        launch_cfl(d, 1, c->st);
+        launch_step_start(d, c->st);
         CK(cudaEventRecord(c->ev[1], c->st));
         launch_lagrange(d, 0, c->st);
         CK(cudaEventRecord(c->ev[2], c->st));
         CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->ny, c->st));
-        launch_remap(d, c->st);
-        launch_commit(c->ctl, 1, c->st);
-        launch_nan_finish(d, c->st);
+        launch_remap_core(d, c->st);
+        post_and_ghosts(d, 1, c->st);
+        launch_commit_finish(d, c->st);
         CK(cudaEventRecord(c->ev[3], c->st));
         if (int rc = check_launch(c)) return rc;
         CK(cudaEventSynchronize(c->ev[3]));

@@ -65,6 +65,8 @@ struct Ctl {
     unsigned long long err_key;
     unsigned long long wmax_bits;       // max wave speed (non-negative doubles order as integers)
     unsigned long long kviol_bits;      // max_k_violation of the step in flight
+    unsigned long long next_wmax_bits;  // wave-speed max of the state just produced (next step's cfl_dt)
+    unsigned long long next_err_key;    // first cfl_dt error of that state
     double max_k_violation;
     double last_dt;
     int commit_time;  // 1: advance time/step at commit (run loop / remap_step)
@@ -114,7 +116,9 @@ struct Dev {
     Ctl* ctl;
 };
 
-H2D_DEV size_t ix(const Dev& d, int i, int j) { return (size_t)(j + G) * (size_t)d.P + (size_t)(i + G); }
+// 32-bit plane offsets: P * R < 2^31 for every mesh up to 16384^2 (checked at
+// context creation), which halves the index arithmetic of the stencils.
+H2D_DEV int ix(const Dev& d, int i, int j) { return (j + G) * d.P + (i + G); }
 
 H2D_DEV double rmax(double a, double b) { return (a < b) ? b : a; }  // std::max
 H2D_DEV double rmin(double a, double b) { return (b < a) ? b : a; }  // std::min

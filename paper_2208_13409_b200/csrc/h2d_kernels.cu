@@ -55,14 +55,14 @@ __global__ void k_begin(Ctl* c, int mode, double host_dt) {
 // cfl_dt, harness.cpp:293-313: per-cell wave speed, block max, one atomic
 // per block on the bit pattern (non-negative doubles order as integers).
 template <int NM>
-__global__ void k_cfl(Dev d) {
+__global__ void k_cfl(Dev d, int into_next) {
     if (halted(d.ctl)) return;
     unsigned long long wb = 0ull;
     const long long ncell = (long long)d.nx * d.ny;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ncell;
          t += (long long)gridDim.x * blockDim.x) {
         const int j = (int)(t / d.nx), i = (int)(t - (long long)j * d.nx);
-        const size_t c = ix(d, i, j);
+        const int c = ix(d, i, j);
         double cs = 0.0;
         bool bad = false;
 #pragma unroll
@@ -73,13 +73,13 @@ __global__ void k_cfl(Dev d) {
             const double pa = eos_p(d, a, rho_a, d.e[a][c]);
             cs += ka * sound(d, a, rho_a, pa, bad);
         }
-        if (bad) raise(d.ctl, ekey(PH_CFL_UNPHYS, j, i, 0));
+        if (bad) atomicMin(into_next ? &d.ctl->next_err_key : &d.ctl->err_key, ekey(PH_CFL_UNPHYS, j, i, 0));
         double umax = 0.0;
 #pragma unroll
         for (int dj = 0; dj <= 1; ++dj)
 #pragma unroll
             for (int di = 0; di <= 1; ++di) {
-                const size_t n = ix(d, i + di, j + dj);
+                const int n = ix(d, i + di, j + dj);
                 const double ux = d.ux[n], uy = d.uy[n];
                 umax = rmax(umax, sqrt(ux * ux + uy * uy));
             }
@@ -105,7 +105,7 @@ __global__ void k_cfl(Dev d) {
             const unsigned long long v = __shfl_xor_sync(0xffffffffu, wb, o);
             wb = v > wb ? v : wb;
         }
-        if (lane == 0 && wb) atomicMax(&d.ctl->wmax_bits, wb);
+        if (lane == 0 && wb) atomicMax(into_next ? &d.ctl->next_wmax_bits : &d.ctl->wmax_bits, wb);
     }
 }
 
@@ -155,7 +155,7 @@ __device__ __forceinline__ void ghost_cells_at(const Dev& d, const FieldList& fl
     int i, j;
     if (!ghost_cell_pos(t, d.nx, d.ny, i, j)) return;
     const int is = wrap_cell(i, d.nx, d.per_x), js = wrap_cell(j, d.ny, d.per_y);
-    const size_t dst = ix(d, i, j), src = ix(d, is, js);
+    const int dst = ix(d, i, j), src = ix(d, is, js);
     for (int f = 0; f < fl.n; ++f) fl.f[f][dst] = fl.f[f][src];
 }
 
@@ -224,7 +224,7 @@ __device__ __forceinline__ void ghost_nodes_at(const Dev& d, const FieldList& fl
     // the source is read as it is after the wall zeroing of the same call
     const bool zx = !d.per_x && (si == 0 || si == nx);
     const bool zy = !d.per_y && (sj == 0 || sj == ny);
-    const size_t dst = ix(d, i, j), src = ix(d, si, sj);
+    const int dst = ix(d, i, j), src = ix(d, si, sj);
     for (int f = 0; f < fl.n; f += 2) {
         double vx = zx ? 0.0 : fl.f[f][src];
         double vy = zy ? 0.0 : fl.f[f + 1][src];
@@ -243,7 +243,7 @@ __global__ void k_sync(Dev d, int next, int respect_halt) {
     int i, j;
     tid2(i, j, -G, -G);
     if (i >= d.nx + G || j >= d.ny + G) return;
-    const size_t c = ix(d, i, j);
+    const int c = ix(d, i, j);
     const double cv = d.cv;
     double m = 0.0, me = 0.0, p = 0.0;
 #pragma unroll
@@ -301,8 +301,8 @@ __global__ void k_lag_cells(Dev d) {
     tid2(i, j, 0, 0);
     if (i >= d.nx || j >= d.ny) return;
     const double dt = step_dt(d.ctl);
-    const size_t c = ix(d, i, j);
-    const size_t n00 = c, n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
+    const int c = ix(d, i, j);
+    const int n00 = c, n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
     const double u00x = d.ux[n00], u00y = d.uy[n00], u10x = d.ux[n10], u10y = d.uy[n10];
     const double u01x = d.ux[n01], u01y = d.uy[n01], u11x = d.ux[n11], u11y = d.uy[n11];
     double ka[2], ma[2], en[2];
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
         const int i = i0 + t % (LTX + 1), j = j0 + t / (LTX + 1);
         double hx = 0.0, hy = 0.0;
         if (i <= nx && j <= ny) {
-            const size_t a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
+            const int a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
             const double mp = 0.25 * (d.m_mix[a] + d.m_mix[b] + d.m_mix[c] + d.m_mix[e]);
             const double rho_p = mp / d.cv;
             const double pq_a = d.pmh[a] + d.q[a], pq_b = d.pmh[b] + d.q[b];
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
     const double vol =
         quad_vol4(d, shx[q00], shy[q00], shx[q10], shy[q10], shx[q11], shy[q11], shx[q01], shy[q01], dt, tangled);
     if (tangled) raise(d.ctl, ekey(PH_CORR_TANGLED, j, i, 0));
-    const size_t n = ix(d, i, j);
+    const int n = ix(d, i, j);
     if (write_vol_lag) d.vol_lag[n] = vol;
     int floors = 0;
     const double cv = d.cv;
@@ -457,7 +457,7 @@ __global__ void k_copy_u(Dev d) {
     int i, j;
     tid2(i, j, -G, -G);
     if (i > d.nx + G || j > d.ny + G) return;
-    const size_t c = ix(d, i, j);
+    const int c = ix(d, i, j);
     d.nux[c] = d.ulx[c];
     d.nuy[c] = d.uly[c];
 }
@@ -473,6 +473,10 @@ __device__ __forceinline__ void face_flux(double ym, double yp, double dmx, doub
     if (whi <= wlo) return;
     wl = wlo;
     wh = whi;
+    // static face line (both offsets zero): the trapezoid volume is a signed
+    // zero, and no output depends on the sign of a zero face volume (it is
+    // skipped by `dvol == 0.0` and adds nothing to vlag), so skip the divide
+    if (dmx == 0.0 && dpx == 0.0) return;
     const double den = (yp + dpy) - (ym + dmy);
     double xlo, xhi;
     if (fabs(den) < 1e-300) {
@@ -501,17 +505,34 @@ constexpr int RCW = RTX + 4, RCH = RTY + 4;  // cell region [i0-2, i0+RTX+2)
 constexpr int RNW = RTX + 5, RNH = RTY + 5;  // node region [i0-2, i0+RTX+2]
 constexpr int RNN = RNW * RNH, RNC = RCW * RCH;
 constexpr int NXF = (RTX + 1) * RTY, NYF = RTX * (RTY + 1), NCF = (RTX + 1) * (RTY + 1);
-constexpr int RCELL1 = 9, RCELL2 = 16;  // cell arrays per material count
+constexpr int RCELL1 = 5, RCELL2 = 12;  // cell arrays per material count
 
 template <int NM>
 struct Tile {
     int ci0, cj0;  // origin of both regions: (i0 - 2, j0 - 2)
     double *hx, *hy, *cf, *fdx, *fdy, *fxdv, *fydv;  // nodes
     int8_t *sx, *sy;
-    double *vl, *rho[2], *el[2], *kk[2], *xl2x, *xl2y, *xlcx, *wlx, *xlcy, *wly, *ifd, *nrx, *nry;  // cells
+    double *vl, *rho[2], *el[2], *kk[2], *xl2x, *xl2y, *ifd, *nrx, *nry;  // cells
     double *fx[3][2], *fy[3][2], *fc[3][2];  // flux items: dm, dme, dva per material
     __device__ __forceinline__ int c(int i, int j) const { return (i - ci0) + (j - cj0) * RCW; }
     __device__ __forceinline__ int n(int i, int j) const { return (i - ci0) + (j - cj0) * RNW; }
+    // make_axis_geom (remap.cpp:315-320) from the face-mean displacements
+    __device__ __forceinline__ double xlcx(const Dev& d, int i, int j) const {
+        const int q = n(i, j);
+        return d.x0 + (i + 0.5) * d.dx + 0.5 * (fdx[q] + fdx[q + 1]);
+    }
+    __device__ __forceinline__ double wlx(const Dev& d, int i, int j) const {
+        const int q = n(i, j);
+        return d.dx + (fdx[q + 1] - fdx[q]);
+    }
+    __device__ __forceinline__ double xlcy(const Dev& d, int i, int j) const {
+        const int q = n(i, j);
+        return d.y0 + (j + 0.5) * d.dy + 0.5 * (fdy[q] + fdy[q + RNW]);
+    }
+    __device__ __forceinline__ double wly(const Dev& d, int i, int j) const {
+        const int q = n(i, j);
+        return d.dy + (fdy[q + RNW] - fdy[q]);
+    }
 };
 
 template <int NM>
@@ -540,10 +561,6 @@ __device__ __forceinline__ Tile<NM> carve_tile(char* base, int ci0, int cj0) {
     T.vl = take(RNC);
     T.xl2x = take(RNC);
     T.xl2y = take(RNC);
-    T.xlcx = take(RNC);
-    T.wlx = take(RNC);
-    T.xlcy = take(RNC);
-    T.wly = take(RNC);
     for (int a = 0; a < NM; ++a) {
         T.rho[a] = take(RNC);
         T.el[a] = take(RNC);
@@ -649,10 +666,13 @@ __device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, i
                 rf = T.rho[a][cc];
                 ef = T.el[a][cc];
             } else {
-                const double* xl = AX ? T.xlcx : T.xlcy;
-                const double* wl = AX ? T.wlx : T.wly;
-                const double x0 = xl[cm], x1 = xl[cc], x2 = xl[cp];
-                const double lw = wl[cc], ufdt = AX ? T.fdx[qn] : T.fdy[qn];
+                const int im = AX ? ia_d - 1 : ic, jm = AX ? ic : ia_d - 1;
+                const int ic_ = AX ? ia_d : ic, jc = AX ? ic : ia_d;
+                const int ip = AX ? ia_d + 1 : ic, jp = AX ? ic : ia_d + 1;
+                const double x0 = AX ? T.xlcx(d, im, jm) : T.xlcy(d, im, jm);
+                const double x1 = AX ? T.xlcx(d, ic_, jc) : T.xlcy(d, ic_, jc);
+                const double x2 = AX ? T.xlcx(d, ip, jp) : T.xlcy(d, ip, jp);
+                const double lw = AX ? T.wlx(d, ic_, jc) : T.wly(d, ic_, jc), ufdt = AX ? T.fdx[qn] : T.fdy[qn];
                 rf = face_value2(T.rho[a][cm], T.rho[a][cc], T.rho[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
                 ef = face_value2(T.el[a][cm], T.el[a][cc], T.el[a][cp], x0, x1, x2, sgn, lw, ufdt, bad);
             }
@@ -693,7 +713,7 @@ __device__ __forceinline__ double corner_item_t(const Dev& d, const Tile<NM>& T,
         const double bhix = rmax(npx, npx + ddx), bhiy = rmax(npy, npy + ddy);
         split_flux_t<NM>(d, T, di, dj, blox, bloy, bhix, bhiy, cdv, dva);
         const int dc = T.c(di, dj);
-        const double lwx = T.wlx[dc], lwy = T.wly[dc];
+        const double lwx = T.wlx(d, di, dj), lwy = T.wly(d, di, dj);
         bool bad = false;
         const bool lin_cfg = d.corner_diag && d.face_order > 1;
 #pragma unroll
@@ -803,7 +823,7 @@ __global__ void k_ghost_multi(Dev d, FieldList cells, FieldList nodes, int flux,
 }
 
 template <int NM>
-__global__ void __launch_bounds__(RTX * RTY) k_remap_tile(Dev d) {
+__global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     extern __shared__ __align__(16) char smem[];
     __shared__ int s_halt;
     const int tid = threadIdx.x;
@@ -815,17 +835,47 @@ __global__ void __launch_bounds__(RTX * RTY) k_remap_tile(Dev d) {
     const Tile<NM> T = carve_tile<NM>(smem, i0 - G, j0 - G);
     const double dt = step_dt(d.ctl);
     const double cv = d.cv;
-    // ---- node items: u_half, corner flux, axis geometry, face flux volumes
-    // (make_axis_geom remap.cpp:296-322, flux geometry :744-767)
+    // ---- phase 0: stage the HBM inputs of the tile + halo (all loads
+    // independent, coalesced rows): u_half on the node region, e_lag, m, k
+    // (and normals) on the cell region.  T.rho holds m and T.vl holds k0
+    // until phase 2 turns them into densities and volumes.
     for (int t = tid; t < RNN; t += RTX * RTY) {
         const int i = T.ci0 + t % RNW, j = T.cj0 + t / RNW;
-        double hx = 0.0, hy = 0.0, cfv = 0.0, fdx = 0.0, fdy = 0.0, fxv = 0.0, fyv = 0.0;
-        int8_t sx = 0, sy = 0;
+        double hx = 0.0, hy = 0.0;
         if (i <= nx + G && j <= ny + G) {
-            const size_t n = ix(d, i, j);
+            const int n = ix(d, i, j);
             hx = d.uhx[n];
             hy = d.uhy[n];
-            const double ddx = hx * dt, ddy = hy * dt;  // cf_corner_flux, remap.cpp:16-25
+        }
+        T.hx[t] = hx;
+        T.hy[t] = hy;
+    }
+    for (int t = tid; t < RNC; t += RTX * RTY) {
+        const int i = T.ci0 + t % RCW, j = T.cj0 + t / RCW;
+        if (i >= nx + G || j >= ny + G) continue;
+        const int c = ix(d, i, j);
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            T.el[a][t] = d.el[a][c];
+            T.rho[a][t] = d.m[a][c];
+            if (NM == 2) T.kk[a][t] = d.k[a][c];
+        }
+        if (NM == 1) T.vl[t] = d.k[0][c];
+        if (NM == 2) {
+            T.nrx[t] = d.nrx[c];
+            T.nry[t] = d.nry[c];
+        }
+    }
+    __syncthreads();
+    // ---- phase 1, node items: corner flux, axis geometry, face flux volumes
+    // (cf_corner_flux remap.cpp:16-25, make_axis_geom :296-322, :744-767)
+    for (int t = tid; t < RNN; t += RTX * RTY) {
+        const int i = T.ci0 + t % RNW, j = T.cj0 + t / RNW;
+        double cfv = 0.0, fdx = 0.0, fdy = 0.0, fxv = 0.0, fyv = 0.0;
+        int8_t sx = 0, sy = 0;
+        if (i <= nx + G && j <= ny + G) {
+            const double hx = T.hx[t], hy = T.hy[t];
+            const double ddx = hx * dt, ddy = hy * dt;
             cfv = fabs(ddx * ddy);
             if (cfv == 0.0) {
                 cfv = 0.0;
@@ -834,25 +884,22 @@ __global__ void __launch_bounds__(RTX * RTY) k_remap_tile(Dev d) {
                 sy = ddy > 0.0 ? 1 : -1;
             }
             if (cfv > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
-            if (j < ny + G) {
-                const size_t nu = ix(d, i, j + 1);
-                const double ux1 = d.uhx[nu], uy1 = d.uhy[nu];
+            // faces on the region's last node row / column feed no region cell
+            if (j < ny + G && j < T.cj0 + RNH - 1) {
+                const double ux1 = T.hx[t + RNW], uy1 = T.hy[t + RNW];
                 fdx = 0.5 * (hx + ux1) * dt;
                 double wl, wh;
                 face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * hx, dt * hy, dt * ux1, dt * uy1, fxv, wl, wh);
                 if (fabs(fxv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
             }
-            if (i < nx + G) {
-                const size_t nr = ix(d, i + 1, j);
-                const double ux1 = d.uhx[nr], uy1 = d.uhy[nr];
+            if (i < nx + G && i < T.ci0 + RNW - 1) {
+                const double ux1 = T.hx[t + 1], uy1 = T.hy[t + 1];
                 fdy = 0.5 * (hy + uy1) * dt;
                 double wl, wh;
                 face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * hy, dt * hx, dt * uy1, dt * ux1, fyv, wl, wh);
                 if (fabs(fyv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
             }
         }
-        T.hx[t] = hx;
-        T.hy[t] = hy;
         T.cf[t] = cfv;
         T.sx[t] = sx;
         T.sy[t] = sy;
@@ -862,18 +909,12 @@ __global__ void __launch_bounds__(RTX * RTY) k_remap_tile(Dev d) {
         T.fydv[t] = fyv;
     }
     __syncthreads();
-    // ---- cell items: xlagc/wlag, Lagrangian volume, densities, centroids,
+    // ---- phase 2, cell items: Lagrangian volume, densities, centroids,
     // interfaces (remap.cpp:769-824)
     for (int t = tid; t < RNC; t += RTX * RTY) {
         const int i = T.ci0 + t % RCW, j = T.cj0 + t / RCW;
         if (i >= nx + G || j >= ny + G) continue;
         const int q00 = T.n(i, j), q10 = q00 + 1, q01 = q00 + RNW, q11 = q01 + 1;
-        const double dlx = T.fdx[q00], drx = T.fdx[q10];
-        T.xlcx[t] = d.x0 + (i + 0.5) * d.dx + 0.5 * (dlx + drx);
-        T.wlx[t] = d.dx + (drx - dlx);
-        const double dly = T.fdy[q00], dry = T.fdy[q01];
-        T.xlcy[t] = d.y0 + (j + 0.5) * d.dy + 0.5 * (dly + dry);
-        T.wly[t] = d.dy + (dry - dly);
         auto cterm = [&](int q, int ni, int nj) -> double {  // remap.cpp:775-785
             const double dv = T.cf[q];
             if (dv == 0.0) return 0.0;
@@ -887,29 +928,25 @@ __global__ void __launch_bounds__(RTX * RTY) k_remap_tile(Dev d) {
         double v = cv + T.fxdv[q10] - T.fxdv[q00] + T.fydv[q01] - T.fydv[q00];
         v += cterm(q00, i, j) + cterm(q10, i + 1, j) + cterm(q01, i, j + 1) + cterm(q11, i + 1, j + 1);
         if (v <= 0.0) raise(d.ctl, ekey(PH_COLLAPSED, j, i, 0));
-        T.vl[t] = v;
-        const size_t c = ix(d, i, j);
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
-            const double ka = d.k[a][c];
-            T.rho[a][t] = ka > 0.0 ? d.m[a][c] / (ka * v) : 0.0;
-            T.el[a][t] = d.el[a][c];
-            if (NM == 2) T.kk[a][t] = ka;
+            const double ka = NM == 2 ? T.kk[a][t] : T.vl[t];
+            const double ma = T.rho[a][t];
+            T.rho[a][t] = ka > 0.0 ? ma / (ka * v) : 0.0;
         }
+        T.vl[t] = v;
         const double mdx = 0.25 * (dt * T.hx[q00] + dt * T.hx[q10] + dt * T.hx[q01] + dt * T.hx[q11]);
         const double mdy = 0.25 * (dt * T.hy[q00] + dt * T.hy[q10] + dt * T.hy[q01] + dt * T.hy[q11]);
         T.xl2x[t] = (d.x0 + (i + 0.5) * d.dx) + mdx;
         T.xl2y[t] = (d.y0 + (j + 0.5) * d.dy) + mdy;
         if (NM == 2) {
             const double k0 = T.kk[0][t];
-            const double nrx = d.nrx[c], nry = d.nry[c];
-            T.nrx[t] = nrx;
-            T.nry[t] = nry;
             double dd = 0.0;
             if (is_mixed(k0)) {
                 const double cx = d.x0 + (i + 0.5) * d.dx, cy = d.y0 + (j + 0.5) * d.dy;
-                dd = place_interface(k0, nrx, nry, cx - 0.5 * d.dx + dlx, cy - 0.5 * d.dy + dly,
-                                     cx + 0.5 * d.dx + drx, cy + 0.5 * d.dy + dry);
+                dd = place_interface(k0, T.nrx[t], T.nry[t], cx - 0.5 * d.dx + T.fdx[q00],
+                                     cy - 0.5 * d.dy + T.fdy[q00], cx + 0.5 * d.dx + T.fdx[q10],
+                                     cy + 0.5 * d.dy + T.fdy[q01]);
             }
             T.ifd[t] = dd;
         }
@@ -967,7 +1004,7 @@ __global__ void __launch_bounds__(RTX * RTY) k_remap_tile(Dev d) {
     const int tx = tid % RTX, ty = tid / RTX;
     const int i = i0 + tx, j = j0 + ty;
     if (i >= nx || j >= ny) return;
-    const size_t c = ix(d, i, j);
+    const int c = ix(d, i, j);
     const int tc = T.c(i, j);
     const int xl = tx + ty * (RTX + 1), xr = xl + 1;
     const int yb = tx + ty * RTX, yt = yb + RTX;
@@ -1107,7 +1144,7 @@ __global__ void k_slivers(Dev d) {
                     cells &= cells - 1;
                     if (lane == 0) {
                         const int si = i0 + b, sj = j;
-                        const size_t sc = ix(d, si, sj);
+                        const int sc = ix(d, si, sj);
                         const uint8_t fl = d.sliver[sc];
                         for (int a = 0; a < 2; ++a) {
                             if (!(fl & (1u << a))) continue;
@@ -1123,7 +1160,7 @@ __global__ void k_slivers(Dev d) {
                                         if (d.per_x) ni = (ni + 2 * nx) % nx;
                                         if (d.per_y) nj = (nj + 2 * ny) % ny;
                                         if (ni < 0 || ni >= nx || nj < 0 || nj >= ny) continue;
-                                        const size_t nc = ix(d, ni, nj);
+                                        const int nc = ix(d, ni, nj);
                                         if (d.nm[a][nc] <= 0.0) continue;
                                         if (d.nk[a][nc] > bk) {
                                             bk = d.nk[a][nc];
@@ -1132,7 +1169,7 @@ __global__ void k_slivers(Dev d) {
                                         }
                                     }
                             if (bi >= 0 && d.nm[a][ix(d, bi, bj)] + smv > 0.0) {
-                                const size_t bc = ix(d, bi, bj);
+                                const int bc = ix(d, bi, bj);
                                 d.nm[a][bc] += smv;
                                 d.me[a][bc] += smev;
                                 d.ne[a][bc] = d.me[a][bc] / d.nm[a][bc];
@@ -1175,7 +1212,7 @@ template <int AX>
 __device__ __forceinline__ void dual_face_item(const Dev& d, int i, int j) {
     const int ia = AX ? i : j, ic = AX ? j : i;
     const int per_a = AX ? d.per_x : d.per_y;
-    const size_t s = ix(d, i, j);
+    const int s = ix(d, i, j);
     double* ox = AX ? d.dfx_x : d.dfy_x;
     double* oy = AX ? d.dfx_y : d.dfy_y;
     if (ia < (per_a ? 0 : 1)) {
@@ -1212,7 +1249,7 @@ __device__ __forceinline__ void dual_face_item(const Dev& d, int i, int j) {
 __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
     const int nx = d.nx, ny = d.ny;
     const double dt = step_dt(d.ctl);
-    const size_t s = ix(d, i, j);
+    const int s = ix(d, i, j);
 #pragma unroll
     for (int pr = 0; pr < 2; ++pr) {
         const int sx = 1, sy = pr == 0 ? 1 : -1;
@@ -1227,7 +1264,7 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
             const int qi[4] = {i, i + sx, i, i + sx}, qj[4] = {j, j, j + sy, j + sy};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const size_t n = ix(d, qi[q], qj[q]);
+                const int n = ix(d, qi[q], qj[q]);
                 // cf_corner_flux (remap.cpp:16-25) recomputed from u_half
                 const double ddx = d.uhx[n] * dt, ddy = d.uhy[n] * dt;
                 const double cdv = fabs(ddx * ddy), dmcv = d.dmc[n];
@@ -1256,7 +1293,7 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
                 const int ci = d.per_x ? ((ci0 % nx) + nx) % nx : ci0;
                 const int cj = d.per_y ? ((cj0 % ny) + ny) % ny : cj0;
                 // xlag2 of cell (ci, cj) (remap.cpp:797-803) recomputed from u_half
-                const size_t n00 = ix(d, ci, cj), n10 = ix(d, ci + 1, cj), n01 = ix(d, ci, cj + 1),
+                const int n00 = ix(d, ci, cj), n10 = ix(d, ci + 1, cj), n01 = ix(d, ci, cj + 1),
                              n11 = ix(d, ci + 1, cj + 1);
                 const double xmd = 0.25 * (dt * d.uhx[n00] + dt * d.uhx[n10] + dt * d.uhx[n01] + dt * d.uhx[n11]);
                 const double ymd = 0.25 * (dt * d.uhy[n00] + dt * d.uhy[n10] + dt * d.uhy[n01] + dt * d.uhy[n11]);
@@ -1274,7 +1311,7 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
 #pragma unroll
                     for (int p = 0; p < 3; ++p) {
                         const int ni = wi + p - 1, nj = wj + q - 1;
-                        const size_t nn = ix(d, ni, nj);
+                        const int nn = ix(d, ni, nj);
                         ax_[p * 3 + q] = d.ulx[nn];
                         ay_[p * 3 + q] = d.uly[nn];
                         xlx[p * 3 + q] = (d.x0 + ni * d.dx) + dt * d.uhx[nn];
@@ -1318,7 +1355,7 @@ __global__ void k_node_update(Dev d) {
     if (i > nx || j > ny) return;
     const int iend = d.per_x ? nx - 1 : nx, jend = d.per_y ? ny - 1 : ny;
     const int si = (d.per_x && i == nx) ? 0 : i, sj = (d.per_y && j == ny) ? 0 : j;
-    const size_t s = ix(d, si, sj);
+    const int s = ix(d, si, sj);
     double ax = 0.0, ay = 0.0;
     // X then Y dual faces (remap.cpp:995-996). Face ia joins nodes (ia-1, ia):
     // + to node ia, - to the node ia-1 wraps to; applied in face-loop order.
@@ -1357,7 +1394,7 @@ __global__ void k_node_update(Dev d) {
         int nc = 0;
         auto push = [&](int ii, int jj, int pr, double sgn) {
             if (ii < 0 || ii > iuniq || jj < 0 || jj > juniq) return;
-            const size_t q = ix(d, ii, jj);
+            const int q = ix(d, ii, jj);
             if (!d.dflag[2 + pr][q]) return;
             tk[nc] = ((long long)jj * (iuniq + 1) + ii) * 2 + pr;
             cx[nc] = sgn > 0 ? d.dc_x[pr][q] : -d.dc_x[pr][q];
@@ -1407,7 +1444,7 @@ __global__ void k_node_update(Dev d) {
         0.25 * (d.mcell[ix(d, si - 1, sj - 1)] + d.mcell[ix(d, si, sj - 1)] + d.mcell[ix(d, si - 1, sj)] + d.mcell[s]);
     if (mp_new <= 0.0 && si == i && sj == j) raise(d.ctl, ekey(PH_NODAL_MASS, j, i, 0));
     const double inv = 1.0 / mp_new;
-    const size_t o = ix(d, i, j);
+    const int o = ix(d, i, j);
     double ux = inv * (mp_lag * d.ulx[s] + ax), uy = inv * (mp_lag * d.uly[s] + ay);
     // fill_ghost_nodes (remap.cpp:462) zeroes the normal component on walls
     if (!d.per_x && (i == 0 || i == nx)) ux = 0.0;
@@ -1427,7 +1464,7 @@ __global__ void k_normals(Dev d, int api) {
     const double* k1 = api ? d.k[1] : d.nk[1];
     double* nx_ = api ? const_cast<double*>(d.nrx) : d.nnrx;
     double* ny_ = api ? const_cast<double*>(d.nry) : d.nnry;
-    const size_t c = ix(d, i, j);
+    const int c = ix(d, i, j);
     if (!api) {  // the Work normals start as the State's (remap.cpp:130)
         nx_[c] = d.nrx[c];
         ny_[c] = d.nry[c];
@@ -1460,7 +1497,7 @@ __global__ void k_nan(Dev d) {
     int i, j;
     tid2(i, j, 0, 0);
     if (i > d.nx || j > d.ny) return;
-    const size_t c = ix(d, i, j);
+    const int c = ix(d, i, j);
     const bool cell = i < d.nx && j < d.ny;
     // issue every load before testing any of them (no short-circuit chains)
     const double a = cell ? d.nm_mix[c] : 0.0, b = cell ? d.ne_mix[c] : 0.0, p = cell ? d.np_mix[c] : 0.0;
@@ -1479,6 +1516,165 @@ __global__ void k_finish(Ctl* c) {
     c->mass_fix_count += c->step_fix;
     const double v = __longlong_as_double((long long)c->kviol_bits);
     if (v > c->max_k_violation) c->max_k_violation = v;
+}
+
+// Start of a run-loop step (harness.cpp:390-395): loop condition, then the
+// cfl_dt of the current State, whose wave-speed maximum and first error were
+// produced by the previous step's k_post (or k_cfl before the first step).
+__global__ void k_step_start(Ctl* c, double dx, double dy) {
+    if (c->err_key != kNoErr || c->done) return;
+    c->kviol_bits = 0ull;
+    c->step_floor = 0;
+    c->step_clip = 0;
+    c->step_fix = 0;
+    const double t_end = c->t_end;
+    if (!(c->time < t_end - 1e-15 * rmax(1.0, t_end)) || (c->max_steps > 0 && c->step >= c->max_steps)) {
+        c->done = 1;
+        return;
+    }
+    if (c->next_err_key != kNoErr) {
+        c->err_key = c->next_err_key;
+        return;
+    }
+    const double wmax = __longlong_as_double((long long)c->next_wmax_bits);
+    if (!(wmax > 0.0) || !isfinite(wmax)) {
+        c->err_key = ekey(PH_CFL_WAVE, 0x1FFFFFF - 32, 0, 0);
+        return;
+    }
+    double dt = c->cfl * rmin(dx, dy) / wmax;
+    c->last_dt = dt;
+    c->dt = rmin(dt, t_end - c->time);
+    c->next_wmax_bits = 0ull;
+    c->next_err_key = kNoErr;
+}
+
+// End of a run-loop step: the remapped State becomes current
+// (remap.cpp:1084-1085) unless an earlier phase failed; nan_scan errors come
+// after the commit (harness.cpp:402-409), so they still commit.
+__global__ void k_commit_finish(Ctl* c) {
+    if (c->done) return;
+    const unsigned long long e = c->err_key;
+    const bool ok = e == kNoErr;
+    if (!ok && (int)(e >> 58) < PH_NAN_CELL) return;
+    c->time = c->time + c->dt;
+    c->step += 1;
+    c->cur ^= 1;
+    if (!ok) return;
+    if (c->dt_log && c->steps_done < c->dt_log_cap) c->dt_log[c->steps_done] = c->dt;
+    c->steps_done += 1;
+    c->floor_count += c->step_floor;
+    c->k_clip_count += c->step_clip;
+    c->mass_fix_count += c->step_fix;
+    const double v = __longlong_as_double((long long)c->kviol_bits);
+    if (v > c->max_k_violation) c->max_k_violation = v;
+}
+
+// The end of the remap on the new State, one thread per position of the
+// ghosted node range: sync_derived over every cell (state.cpp:120-143, from
+// assemble_state remap.cpp:1087), refresh_normals_impl on interior cells
+// (remap.cpp:102-114, vof.cpp:10-22), and in the run loop nan_scan
+// (harness.cpp:347-358) plus the wave speed of the next step's cfl_dt
+// (harness.cpp:293-310), so the State is read once.
+template <int NM>
+__global__ void __launch_bounds__(256) k_post(Dev d, int run_loop) {
+    __shared__ unsigned long long sw[8];
+    __shared__ int s_halt;
+    if (threadIdx.x == 0 && threadIdx.y == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
+    int i, j;
+    tid2(i, j, -G, -G);
+    const int nx = d.nx, ny = d.ny;
+    unsigned long long wb = 0ull;
+    if (i < nx + G && j < ny + G) {
+        const int c = ix(d, i, j);
+        const double cv = d.cv;
+        double ka[2], ma[2], ea[2];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            ka[a] = d.nk[a][c];
+            ma[a] = d.nm[a][c];
+            ea[a] = d.ne[a][c];
+        }
+        double m = 0.0, me = 0.0, p = 0.0;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            if (ka[a] <= 0.0) continue;
+            m += ma[a];
+            me += ma[a] * ea[a];
+            if (ka[a] < kThermoTol) continue;
+            const double rho_a = ma[a] / (ka[a] * cv);
+            p += ka[a] * eos_p(d, a, rho_a, ea[a]);
+        }
+        const double emix = m > 0.0 ? me / m : 0.0;
+        d.nm_mix[c] = m;
+        d.ne_mix[c] = emix;
+        d.nrho_mix[c] = m / cv;
+        d.np_mix[c] = p;
+        d.nvol[c] = cv;
+        const bool interior = i >= 0 && j >= 0 && i < nx && j < ny;
+        if (interior) {
+            if (NM == 2) {  // normals of the new fractions
+                double nrx = d.nrx[c], nry = d.nry[c];
+                if (is_mixed(ka[0])) {
+                    auto K = [&](int ii, int jj) { return d.nk[1][ix(d, ii, jj)]; };
+                    auto col = [&](int ii) { return K(ii, j - 1) + 2.0 * K(ii, j) + K(ii, j + 1); };
+                    auto row = [&](int jj) { return K(i - 1, jj) + 2.0 * K(i, jj) + K(i + 1, jj); };
+                    const double gx = (col(i + 1) - col(i - 1)) / (8.0 * d.dx);
+                    const double gy = (row(j + 1) - row(j - 1)) / (8.0 * d.dy);
+                    const double g = sqrt(gx * gx + gy * gy);
+                    if (!(g < 1e-300)) {  // an isolated mixed cell keeps its normal
+                        nrx = gx / g;
+                        nry = gy / g;
+                    }
+                }
+                d.nnrx[c] = nrx;
+                d.nnry[c] = nry;
+            }
+            if (run_loop) {
+                if (!isfinite(m) | !isfinite(emix) | !isfinite(p)) raise(d.ctl, ekey(PH_NAN_CELL, j, i, 0));
+                // next step's wave speed on the new State
+                double cs = 0.0;
+                bool bad = false;
+#pragma unroll
+                for (int a = 0; a < NM; ++a) {
+                    if (ka[a] < kThermoTol) continue;
+                    const double rho_a = ma[a] / (ka[a] * cv);
+                    const double pa = eos_p(d, a, rho_a, ea[a]);
+                    cs += ka[a] * sound(d, a, rho_a, pa, bad);
+                }
+                if (bad) atomicMin(&d.ctl->next_err_key, ekey(PH_CFL_UNPHYS, j, i, 0));
+                double umax = 0.0;
+#pragma unroll
+                for (int dj = 0; dj <= 1; ++dj)
+#pragma unroll
+                    for (int di = 0; di <= 1; ++di) {
+                        const int n = ix(d, i + di, j + dj);
+                        const double ux = d.nux[n], uy = d.nuy[n];
+                        umax = rmax(umax, sqrt(ux * ux + uy * uy));
+                    }
+                const double w = cs + umax;
+                if (w > 0.0) wb = (unsigned long long)__double_as_longlong(w);
+            }
+        }
+    }
+    if (run_loop && i >= 0 && j >= 0 && i <= nx && j <= ny) {
+        const int n = ix(d, i, j);
+        if (!isfinite(d.nux[n]) | !isfinite(d.nuy[n])) raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));
+    }
+    if (run_loop) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long v = __shfl_xor_sync(0xffffffffu, wb, o);
+            wb = v > wb ? v : wb;
+        }
+        const int t = threadIdx.y * blockDim.x + threadIdx.x;
+        if ((t & 31) == 0) sw[t >> 5] = wb;
+        __syncthreads();
+        if (t == 0) {
+            for (int w = 1; w < (int)(blockDim.x * blockDim.y) / 32; ++w) wb = sw[w] > wb ? sw[w] : wb;
+            if (wb) atomicMax(&d.ctl->next_wmax_bits, wb);
+        }
+    }
 }
 
 // AoS <-> SoA staging for Vec2 fields (reference layout pitch W = n1 + 2G).
@@ -1518,9 +1714,9 @@ void launch_cfl(const Dev& d, int run_loop, cudaStream_t s) {
     unsigned nb = nblk(ncell, 256);
     if (nb > 148u * 8u) nb = 148u * 8u;
     if (d.nmat == 2)
-        { k_cfl<2><<<nb, 256, 0, s>>>(d); ++g_launches; }
+        { k_cfl<2><<<nb, 256, 0, s>>>(d, 0); ++g_launches; }
     else
-        { k_cfl<1><<<nb, 256, 0, s>>>(d); ++g_launches; }
+        { k_cfl<1><<<nb, 256, 0, s>>>(d, 0); ++g_launches; }
     { k_cfl_final<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy, run_loop); ++g_launches; }
 }
 
@@ -1590,7 +1786,28 @@ void remap_init() {
     done = true;
 }
 
-void launch_remap(const Dev& d, cudaStream_t s) {
+// k_post (sync_derived, normals, and in the run loop nan_scan + next cfl) and
+// the ghost layers of the new u and normals (assemble_state's fill_ghosts).
+void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s) {
+    const dim3 gp((unsigned)((d.nx + 1 + 2 * G + 31) / 32), (unsigned)((d.ny + 1 + 2 * G + 7) / 8));
+    if (d.nmat == 2)
+        { k_post<2><<<gp, dim3(32, 8), 0, s>>>(d, run_loop); ++g_launches; }
+    else
+        { k_post<1><<<gp, dim3(32, 8), 0, s>>>(d, run_loop); ++g_launches; }
+    FieldList fg{};
+    fg.n = 2;
+    fg.f[0] = d.nnrx;
+    fg.f[1] = d.nnry;
+    FieldList fu{};
+    fu.n = 2;
+    fu.f[0] = d.nux;
+    fu.f[1] = d.nuy;
+    launch_ghost_multi(d, fg, fu, 0, 1, s);
+}
+
+void launch_remap(const Dev& d, cudaStream_t s) { launch_remap_core(d, s); post_and_ghosts(d, 0, s); }
+
+void launch_remap_core(const Dev& d, cudaStream_t s) {
     remap_init();
     const int nx = d.nx, ny = d.ny;
     const bool two = d.nmat == 2;
@@ -1621,20 +1838,28 @@ void launch_remap(const Dev& d, cudaStream_t s) {
         { k_dual_items<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
         { k_node_update<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
     }
-    if (two) { k_normals<<<gc, blk2(), 0, s>>>(d, 0); ++g_launches; }
-    // assemble_state (remap.cpp:1075-1089): fill_ghosts + sync_derived.  The
-    // m, e, k ghosts were filled by finalize (identical values); the new u and
-    // the normals still need theirs.
-    FieldList fg{};
-    fg.n = 2;
-    fg.f[0] = d.nnrx;
-    fg.f[1] = d.nnry;
-    FieldList fu{};
-    fu.n = 2;
-    fu.f[0] = d.nux;
-    fu.f[1] = d.nuy;
-    launch_ghost_multi(d, fg, fu, 0, 1, s);
-    launch_sync(d, 1, 1, s);
+}
+
+void launch_step(const Dev& d, cudaStream_t s, int* row_slivers) {
+    { k_step_start<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy); ++g_launches; }
+    launch_lagrange(d, 0, s);
+    cudaMemsetAsync(row_slivers, 0, sizeof(int) * (size_t)d.ny, s);
+    launch_remap_core(d, s);
+    post_and_ghosts(d, 1, s);
+    { k_commit_finish<<<1, 1, 0, s>>>(d.ctl); ++g_launches; }
+}
+
+void launch_step_start(const Dev& d, cudaStream_t s) { k_step_start<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy); ++g_launches; }
+void launch_commit_finish(const Dev& d, cudaStream_t s) { k_commit_finish<<<1, 1, 0, s>>>(d.ctl); ++g_launches; }
+
+void launch_cfl_next(const Dev& d, cudaStream_t s) {
+    const long long ncell = (long long)d.nx * d.ny;
+    unsigned nb = nblk(ncell, 256);
+    if (nb > 148u * 8u) nb = 148u * 8u;
+    if (d.nmat == 2)
+        { k_cfl<2><<<nb, 256, 0, s>>>(d, 1); ++g_launches; }
+    else
+        { k_cfl<1><<<nb, 256, 0, s>>>(d, 1); ++g_launches; }
 }
 
 void launch_commit(Ctl* c, int advance, cudaStream_t s) { k_commit<<<1, 1, 0, s>>>(c, advance); }

@@ -21,6 +21,12 @@ void launch_ghost_nodes(const Dev& d, const FieldList& fl, cudaStream_t s);
 void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s);
 void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s);
 void launch_remap(const Dev& d, cudaStream_t s);
+void launch_remap_core(const Dev& d, cudaStream_t s);
+void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s);
+void launch_step(const Dev& d, cudaStream_t s, int* row_slivers);  // one run-loop step
+void launch_cfl_next(const Dev& d, cudaStream_t s);
+void launch_step_start(const Dev& d, cudaStream_t s);
+void launch_commit_finish(const Dev& d, cudaStream_t s);               // wave speed of the current State
 void launch_commit(Ctl* c, int advance, cudaStream_t s);
 void launch_nan_finish(const Dev& d, cudaStream_t s);
 void launch_normals_api(const Dev& d, cudaStream_t s);
