@@ -153,6 +153,13 @@ typedef struct {
     h2d_remap_diag diag;
 } h2d_run_args;
 
+/* One block of a 2D domain decomposition (no reference counterpart: the
+ * reference is serial): owned cells [oi, oi+bnx) x [oj, oj+bny)
+ * of the global mesh plus a halo of `halo` (>= 8) cells stored around them. */
+typedef struct {
+    int oi, oj, bnx, bny, halo;
+} h2d_block;
+
 typedef struct h2d_ctx h2d_ctx;
 
 /* Library identity: returns H2D_ABI_VERSION. */

@@ -47,6 +47,10 @@ struct h2d_ctx {
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one run-loop step per State parity
     long long graph_kernels = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    h2d_block blk{};   // the block of the 2D decomposition (the whole mesh for h2d_create)
+    bool is_block = false;
+    double* xbuf = nullptr;  // device staging for window uploads / owned downloads
+    size_t xbuf_bytes = 0;
     void* flush = nullptr;
     size_t flush_bytes = 0;
 };
@@ -297,6 +301,40 @@ int launch_step_graph(h2d_ctx* c, int parity) {
     return 0;
 }
 
+// Compute ranges of every phase: the reference's ranges, and
+// on block sides facing a neighbour block the storage window shrunk by the
+// stencil reach accumulated up to that phase, so that after one step the
+// owned cells and nodes are exact and only the halo needs the exchange.
+void block_ranges(h2d_ctx* c) {
+    Dev& d = c->base;
+    const h2d_block& b = c->blk;
+    const int NX = d.nx, NY = d.ny, H = b.halo;
+    const bool li = b.oi > 0, ri = b.oi + b.bnx < NX, bi = b.oj > 0, ti = b.oj + b.bny < NY;
+    const int wl = b.oi - H, wr = b.oi + b.bnx + H, wb = b.oj - H, wt = b.oj + b.bny + H;
+    auto R = [&](int rlo, int rhi, int slo, int shi, int rjlo, int rjhi) {
+        Rng r;
+        r.i0 = li ? std::max(rlo, wl + slo) : rlo;
+        r.i1 = ri ? std::min(rhi, wr - shi) : rhi;
+        r.j0 = bi ? std::max(rjlo, wb + slo) : rjlo;
+        r.j1 = ti ? std::min(rjhi, wt - shi) : rjhi;
+        return r;
+    };
+    d.r_lagc = R(0, NX, 0, 0, 0, NY);
+    d.r_lagn = R(0, NX + 1, 1, 0, 0, NY + 1);
+    d.r_lage = R(0, NX, 1, 1, 0, NY);
+    d.r_gath = R(0, NX, 3, 3, 0, NY);
+    d.r_dual = R(0, NX + 1, 4, 3, 0, NY + 1);
+    d.r_node = R(0, NX + 1, 6, 5, 0, NY + 1);
+    d.r_sync = R(-G, NX + G, 5, 5, -G, NY + G);
+    d.r_nrm = R(0, NX, 6, 6, 0, NY);
+    d.own_c = {li ? b.oi : -G, ri ? b.oi + b.bnx : NX + G, bi ? b.oj : -G, ti ? b.oj + b.bny : NY + G};
+    d.own_n = {li ? b.oi : -G, ri ? b.oi + b.bnx : NX + G + 1, bi ? b.oj : -G, ti ? b.oj + b.bny : NY + G + 1};
+    d.win_c = {std::max(wl, -G), std::min(wr, NX + G), std::max(wb, -G), std::min(wt, NY + G)};
+    d.win_n = {std::max(wl, -G), std::min(wr + 1, NX + G + 1), std::max(wb, -G), std::min(wt + 1, NY + G + 1)};
+}
+
+int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx** out);
+
 }  // namespace
 
 extern "C" {
@@ -306,6 +344,31 @@ int h2d_abi_version(void) { return H2D_ABI_VERSION; }
 long long h2d_launch_count(void) { return launch_count(); }
 
 int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
+    h2d_block whole;
+    whole.oi = 0;
+    whole.oj = 0;
+    whole.bnx = cfg->mesh.nx;
+    whole.bny = cfg->mesh.ny;
+    whole.halo = G;
+    return create_ctx(cfg, &whole, device, out);
+}
+
+int h2d_create_block(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx** out) {
+    *out = nullptr;
+    const h2d_mesh& m = cfg->mesh;
+    if (m.bc_x == H2D_BC_PERIODIC || m.bc_y == H2D_BC_PERIODIC) return H2D_ERR_INVALID;  // walls only
+    if (blk->halo < 8 || blk->oi < 0 || blk->oj < 0 || blk->bnx < blk->halo || blk->bny < blk->halo ||
+        blk->oi + blk->bnx > m.nx || blk->oj + blk->bny > m.ny)
+        return H2D_ERR_INVALID;
+    const int rc = create_ctx(cfg, blk, device, out);
+    if (!rc) (*out)->is_block = true;
+    return rc;
+}
+
+}  // extern "C"
+
+namespace {
+int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx** out) {
     *out = nullptr;
     const h2d_mesh& m = cfg->mesh;
     if (m.nx < 3 || m.ny < 3) return H2D_ERR_SIM;        // Mesh::Mesh, mesh.hpp:27
@@ -327,8 +390,10 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
     c->nx = m.nx;
     c->ny = m.ny;
     c->nmat = cfg->nmat;
-    c->P = ((m.nx + 1 + 2 * G) + 31) / 32 * 32;
-    c->R = m.ny + 1 + 2 * G;
+    c->blk = *blk;
+    const int H = blk->halo;
+    c->P = ((blk->bnx + 1 + 2 * H) + 31) / 32 * 32;
+    c->R = blk->bny + 1 + 2 * H;
     c->fsz = (size_t)c->P * (size_t)c->R;
     if (c->fsz >= (size_t)1 << 31) {  // device plane offsets are 32-bit
         h2d_destroy(c);
@@ -338,7 +403,7 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
     // plane count: 2 x State (6 + 3 nm) + Lagrange (7 + 2 nm) + remap scratch
     const size_t planes = 2 * (9 + 3 * nm) + (7 + 2 * nm) + (25 + 15 * nm) + 8;
     const size_t bytes_planes = planes * ((c->fsz * sizeof(double) + 255) & ~size_t(255));
-    const size_t bytes_small = 8 * ((c->fsz + 255) & ~size_t(255)) + ((size_t)c->ny * 4 + 256);
+    const size_t bytes_small = 8 * ((c->fsz + 255) & ~size_t(255)) + ((size_t)c->R * 4 + 256);
     c->arena_bytes = bytes_planes + bytes_small + 4096;
     if (cudaMalloc(&c->arena, c->arena_bytes) != cudaSuccess) return fail(H2D_ERR_NOMEM);
     cudaMemsetAsync(c->arena, 0, c->arena_bytes, c->st);
@@ -370,6 +435,11 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
     d.nx = m.nx;
     d.ny = m.ny;
     d.P = c->P;
+    d.oi = blk->oi;
+    d.oj = blk->oj;
+    d.H = H;
+    d.off = (H - blk->oj) * c->P + (H - blk->oi);
+    block_ranges(c);
     d.nmat = nm;
     d.per_x = m.bc_x == H2D_BC_PERIODIC;
     d.per_y = m.bc_y == H2D_BC_PERIODIC;
@@ -427,7 +497,7 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
     for (int q = 0; q < 4; ++q) d.dflag[q] = bytes_plane();
     (void)bytes_plane();
     d.row_slivers = reinterpret_cast<int*>(c->arena + c->arena_used);
-    c->arena_used += ((size_t)c->ny * 4 + 255) & ~size_t(255);
+    c->arena_used += ((size_t)c->R * 4 + 255) & ~size_t(255);
     if (c->arena_used > c->arena_bytes) return fail(H2D_ERR_NOMEM);
     if (cudaMalloc(&c->ctl, sizeof(Ctl)) != cudaSuccess) return fail(H2D_ERR_NOMEM);
     if (cudaMallocHost(&c->hctl, sizeof(Ctl)) != cudaSuccess) return fail(H2D_ERR_NOMEM);
@@ -445,6 +515,9 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
     *out = c;
     return 0;
 }
+}  // namespace
+
+extern "C" {
 
 void h2d_destroy(h2d_ctx* c) {
     if (!c) return;
@@ -622,7 +695,7 @@ int h2d_remap_step(h2d_ctx* c, double dt, int kind, int /*x_first*/, int remap_v
     if (int rc = ctl_reset(c)) return rc;
     const Dev d = make_dev(c, c->cur, remap_velocity != 0);
     launch_begin(c->ctl, 1, dt, c->st);
-    CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->ny, c->st));
+    CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->R, c->st));
     launch_remap(d, c->st);
     launch_commit(c->ctl, 1, c->st);
     if (int rc = check_launch(c)) return rc;
@@ -768,7 +841,7 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[4]
         CK(cudaEventRecord(c->ev[1], c->st));
         launch_lagrange(d, 0, c->st);
         CK(cudaEventRecord(c->ev[2], c->st));
-        CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->ny, c->st));
+        CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->R, c->st));
         launch_remap_core(d, c->st);
         post_and_ghosts(d, 1, c->st);
         launch_commit_finish(d, c->st);

@@ -87,10 +87,25 @@ H2D_DEV bool halted(const Ctl* c) {
 H2D_DEV double step_dt(const Ctl* c) { return __ldg(&c->dt); }
 H2D_DEV void raise(Ctl* c, uint64_t key) { atomicMin(&c->err_key, (unsigned long long)key); }
 
-// Per-launch constants and field pointers.  Every field is a (P x R) array of
-// doubles with G ghost layers; element (i, j) at (j + G) * P + (i + G).
+// Half-open range of GLOBAL indices [i0, i1) x [j0, j1).
+struct Rng {
+    int i0, i1, j0, j1;
+};
+
+// Per-launch constants and field pointers.  Kernels work in GLOBAL mesh
+// indices (the reference's i, j); a context stores the window of one block of
+// the 2D decomposition: global (i, j) lives at j * P + i + off, where off maps
+// the block origin (oi, oj) minus the halo H to the start of every plane.  A
+// single-domain context is the block (0, 0, nx, ny) with H = G = 2, i.e. the
+// reference Field layout.
 struct Dev {
-    int nx, ny, P, nmat, per_x, per_y;
+    int nx, ny, P, nmat, per_x, per_y;  // nx, ny: GLOBAL mesh size
+    int oi, oj, H, off;                 // block origin, storage halo, index offset
+    // compute ranges per phase (reference ranges, extended into the halo on
+    // block sides that face a neighbour block; see capi.cu block_ranges)
+    Rng r_lagc, r_lagn, r_lage, r_gath, r_dual, r_node, r_sync, r_nrm;
+    Rng own_c, own_n;  // cells / nodes this block answers for (errors, counters, nan, cfl)
+    Rng win_c, win_n;  // cells / nodes present in storage
     double dx, dy, x0, y0, cv, L;
     int stiff[2];
     double gamma[2], pi[2];
@@ -118,7 +133,8 @@ struct Dev {
 
 // 32-bit plane offsets: P * R < 2^31 for every mesh up to 16384^2 (checked at
 // context creation), which halves the index arithmetic of the stencils.
-H2D_DEV int ix(const Dev& d, int i, int j) { return (j + G) * d.P + (i + G); }
+H2D_DEV int ix(const Dev& d, int i, int j) { return j * d.P + i + d.off; }
+H2D_DEV bool in(const Rng& r, int i, int j) { return i >= r.i0 && i < r.i1 && j >= r.j0 && j < r.j1; }
 
 H2D_DEV double rmax(double a, double b) { return (a < b) ? b : a; }  // std::max
 H2D_DEV double rmin(double a, double b) { return (b < a) ? b : a; }  // std::min

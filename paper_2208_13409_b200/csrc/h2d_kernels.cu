@@ -23,7 +23,16 @@ __device__ __forceinline__ void tid2(int& i, int& j, int ilo, int jlo) {
     i = ilo + (int)(blockIdx.x * blockDim.x + threadIdx.x);
     j = jlo + (int)(blockIdx.y * blockDim.y + threadIdx.y);
 }
-#define AT(p, i, j) ((p)[ix(d, (i), (j))])
+// ownership: every global cell / node / face is answered for (errors,
+// counters, nan_scan, cfl) by exactly one block
+__device__ __forceinline__ bool own_cell(const Dev& d, int i, int j) { return in(d.own_c, i, j); }
+__device__ __forceinline__ bool own_node(const Dev& d, int i, int j) { return in(d.own_n, i, j); }
+__device__ __forceinline__ bool own_xface(const Dev& d, int i, int j) {  // node column i, cell row j
+    return i >= d.own_n.i0 && i < d.own_n.i1 && j >= d.own_c.j0 && j < d.own_c.j1;
+}
+__device__ __forceinline__ bool own_yface(const Dev& d, int i, int j) {  // cell column i, node row j
+    return i >= d.own_c.i0 && i < d.own_c.i1 && j >= d.own_n.j0 && j < d.own_n.j1;
+}
 
 // ---------------------------------------------------------------------------
 // control kernels
@@ -58,10 +67,15 @@ template <int NM>
 __global__ void k_cfl(Dev d, int into_next) {
     if (halted(d.ctl)) return;
     unsigned long long wb = 0ull;
-    const long long ncell = (long long)d.nx * d.ny;
+    // owned interior cells (cfl_dt loops over the whole mesh; the blocks of a
+    // decomposition split it and the maxima are combined across ranks)
+    const int ci0 = max(d.own_c.i0, 0), ci1 = min(d.own_c.i1, d.nx);
+    const int cj0 = max(d.own_c.j0, 0), cj1 = min(d.own_c.j1, d.ny);
+    const int w = ci1 - ci0;
+    const long long ncell = (long long)w * (cj1 - cj0);
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ncell;
          t += (long long)gridDim.x * blockDim.x) {
-        const int j = (int)(t / d.nx), i = (int)(t - (long long)j * d.nx);
+        const int j = cj0 + (int)(t / w), i = ci0 + (int)(t % w);
         const int c = ix(d, i, j);
         double cs = 0.0;
         bool bad = false;
@@ -83,10 +97,10 @@ __global__ void k_cfl(Dev d, int into_next) {
                 const double ux = d.ux[n], uy = d.uy[n];
                 umax = rmax(umax, sqrt(ux * ux + uy * uy));
             }
-        const double w = cs + umax;
+        const double ws = cs + umax;
         // NaN and +-0 never raise the max (std::max keeps its first argument)
-        if (w > 0.0) {
-            const unsigned long long b = (unsigned long long)__double_as_longlong(w);
+        if (ws > 0.0) {
+            const unsigned long long b = (unsigned long long)__double_as_longlong(ws);
             wb = b > wb ? b : wb;
         }
     }
@@ -154,6 +168,7 @@ __device__ __forceinline__ bool ghost_cell_pos(int t, int nx, int ny, int& i, in
 __device__ __forceinline__ void ghost_cells_at(const Dev& d, const FieldList& fl, int t) {
     int i, j;
     if (!ghost_cell_pos(t, d.nx, d.ny, i, j)) return;
+    if (!in(d.win_c, i, j)) return;
     const int is = wrap_cell(i, d.nx, d.per_x), js = wrap_cell(j, d.ny, d.per_y);
     const int dst = ix(d, i, j), src = ix(d, is, js);
     for (int f = 0; f < fl.n; ++f) fl.f[f][dst] = fl.f[f][src];
@@ -180,7 +195,7 @@ __device__ __forceinline__ void ghost_nodes_at(const Dev& d, const FieldList& fl
             if (t < 2 * (ny + 1)) {
                 j = t % (ny + 1);
                 i = t < ny + 1 ? 0 : nx;
-                if (!d.per_x)
+                if (!d.per_x && in(d.win_n, i, j))
                     for (int f = 0; f < fl.n; f += 2) fl.f[f][ix(d, i, j)] = 0.0;
                 return;
             }
@@ -188,12 +203,13 @@ __device__ __forceinline__ void ghost_nodes_at(const Dev& d, const FieldList& fl
             if (t < 2 * (nx + 1)) {
                 i = t % (nx + 1);
                 j = t < nx + 1 ? 0 : ny;
-                if (!d.per_y)
+                if (!d.per_y && in(d.win_n, i, j))
                     for (int f = 1; f < fl.n; f += 2) fl.f[f][ix(d, i, j)] = 0.0;
             }
             return;
         }
     }
+    if (!in(d.win_n, i, j)) return;
     // wrap_node (state.cpp:71-80)
     int si, sj;
     bool fi = false, fj = false;
@@ -241,8 +257,8 @@ template <int NM>
 __global__ void k_sync(Dev d, int next, int respect_halt) {
     if (respect_halt && halted(d.ctl)) return;
     int i, j;
-    tid2(i, j, -G, -G);
-    if (i >= d.nx + G || j >= d.ny + G) return;
+    tid2(i, j, d.win_c.i0, d.win_c.j0);
+    if (!in(d.win_c, i, j) || i < -G || j < -G || i >= d.nx + G || j >= d.ny + G) return;
     const int c = ix(d, i, j);
     const double cv = d.cv;
     double m = 0.0, me = 0.0, p = 0.0;
@@ -298,8 +314,9 @@ template <int NM>
 __global__ void k_lag_cells(Dev d) {
     if (halted(d.ctl)) return;
     int i, j;
-    tid2(i, j, 0, 0);
-    if (i >= d.nx || j >= d.ny) return;
+    tid2(i, j, d.r_lagc.i0, d.r_lagc.j0);
+    if (!in(d.r_lagc, i, j)) return;
+    const bool own = own_cell(d, i, j);
     const double dt = step_dt(d.ctl);
     const int c = ix(d, i, j);
     const int n00 = c, n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
@@ -329,7 +346,7 @@ __global__ void k_lag_cells(Dev d) {
             const double pa = eos_p(d, a, rho_a, en[a]);
             cs += ka[a] * sound(d, a, rho_a, pa, bad);
         }
-        if (bad) raise(d.ctl, ekey(PH_Q_UNPHYS, j, i, 0));
+        if (bad && own) raise(d.ctl, ekey(PH_Q_UNPHYS, j, i, 0));
         const double rho = d.rho_mix[c];
         const double du = d.L * fabs(div);
         q = rho * d.a1 * du * cs + d.a2 * rho * du * du;
@@ -338,7 +355,7 @@ __global__ void k_lag_cells(Dev d) {
     // predict
     bool tangled = false;
     const double vol = quad_vol4(d, u00x, u00y, u10x, u10y, u11x, u11y, u01x, u01y, 0.5 * dt, tangled);
-    if (tangled) raise(d.ctl, ekey(PH_PRED_TANGLED, j, i, 0));
+    if (tangled && own) raise(d.ctl, ekey(PH_PRED_TANGLED, j, i, 0));
     double pmix = 0.0;
     int floors = 0;
     const double cv = d.cv;
@@ -361,7 +378,7 @@ __global__ void k_lag_cells(Dev d) {
         d.ph[a][c] = pa_h;
     }
     d.pmh[c] = pmix;
-    if (floors) atomicAdd(&d.ctl->step_floor, floors);
+    if (floors && own) atomicAdd(&d.ctl->step_floor, floors);
 }
 
 // Node part of predict (lagrange.cpp:135-142: nodal_mass state.cpp:34-36,
@@ -378,13 +395,13 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
     if (tid == 0) s_halt = halted(d.ctl);
     __syncthreads();
     if (s_halt) return;
-    const int nx = d.nx, ny = d.ny;
-    const int i0 = blockIdx.x * LTX, j0 = blockIdx.y * LTY;
+    const Rng rn = d.r_lagn;
+    const int i0 = rn.i0 + blockIdx.x * LTX, j0 = rn.j0 + blockIdx.y * LTY;
     const double dt = step_dt(d.ctl);
     for (int t = tid; t < NN; t += LTX * LTY) {
         const int i = i0 + t % (LTX + 1), j = j0 + t / (LTX + 1);
         double hx = 0.0, hy = 0.0;
-        if (i <= nx && j <= ny) {
+        if (in(rn, i, j)) {
             const int a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
             const double mp = 0.25 * (d.m_mix[a] + d.m_mix[b] + d.m_mix[c] + d.m_mix[e]);
             const double rho_p = mp / d.cv;
@@ -396,7 +413,7 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
             const double ux = d.ux[e], uy = d.uy[e];
             hx = ux - gx * sc;
             hy = uy - gy * sc;
-            if ((i < i0 + LTX || i == nx) && (j < j0 + LTY || j == ny)) {
+            if ((i < i0 + LTX || i == rn.i1 - 1) && (j < j0 + LTY || j == rn.j1 - 1)) {
                 d.uhx[e] = hx;
                 d.uhy[e] = hy;
                 d.ulx[e] = 2.0 * hx - ux;
@@ -409,12 +426,13 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
     __syncthreads();
     const int tx = tid % LTX, ty = tid / LTX;
     const int i = i0 + tx, j = j0 + ty;
-    if (i >= nx || j >= ny) return;
+    if (!in(d.r_lage, i, j)) return;
+    const bool own = own_cell(d, i, j);
     const int q00 = tx + ty * (LTX + 1), q10 = q00 + 1, q01 = q00 + LTX + 1, q11 = q01 + 1;
     bool tangled = false;
     const double vol =
         quad_vol4(d, shx[q00], shy[q00], shx[q10], shy[q10], shx[q11], shy[q11], shx[q01], shy[q01], dt, tangled);
-    if (tangled) raise(d.ctl, ekey(PH_CORR_TANGLED, j, i, 0));
+    if (tangled && own) raise(d.ctl, ekey(PH_CORR_TANGLED, j, i, 0));
     const int n = ix(d, i, j);
     if (write_vol_lag) d.vol_lag[n] = vol;
     int floors = 0;
@@ -440,7 +458,7 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
         }
         d.el[a][n] = ea;
     }
-    if (floors) atomicAdd(&d.ctl->step_floor, floors);
+    if (floors && own) atomicAdd(&d.ctl->step_floor, floors);
 }
 
 // ---------------------------------------------------------------------------
@@ -455,8 +473,8 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
 __global__ void k_copy_u(Dev d) {
     if (halted(d.ctl)) return;
     int i, j;
-    tid2(i, j, -G, -G);
-    if (i > d.nx + G || j > d.ny + G) return;
+    tid2(i, j, d.win_n.i0, d.win_n.j0);
+    if (!in(d.win_n, i, j)) return;
     const int c = ix(d, i, j);
     d.nux[c] = d.ulx[c];
     d.nuy[c] = d.uly[c];
@@ -679,7 +697,8 @@ __device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, i
             rfv[a] = rf;
             efv[a] = ef;
         }
-        if (bad) raise(d.ctl, ekey(AX ? PH_GRAD_XFACE : PH_GRAD_YFACE, ic, ia, 0));
+        if (bad && (AX ? own_xface(d, i, j) : own_yface(d, i, j)))
+            raise(d.ctl, ekey(AX ? PH_GRAD_XFACE : PH_GRAD_YFACE, ic, ia, 0));
     }
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
@@ -750,7 +769,7 @@ __device__ __forceinline__ double corner_item_t(const Dev& d, const Tile<NM>& T,
             rfv[a] = rf;
             efv[a] = ef;
         }
-        if (bad) raise(d.ctl, ekey(PH_GRAD_CORNER, j, i, 0));
+        if (bad && own_node(d, i, j)) raise(d.ctl, ekey(PH_GRAD_CORNER, j, i, 0));
     }
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
@@ -787,23 +806,32 @@ __device__ __forceinline__ void flux_ghosts_at(const Dev& d, int t) {
         if (j == -1) return d.per_y ? d.dmc[ix(d, i, ny - 1)] : d.dmc[ix(d, i, 1)];
         return d.dmc[ix(d, i, j)];
     };
+    // only the ghost entries inside this block's window (the global mesh
+    // boundary); X-face entries live at (node column, cell row), Y-face
+    // entries at (cell column, node row)
+    auto wxf = [&](int i, int j) {
+        return i >= d.win_n.i0 && i < d.win_n.i1 && j >= d.win_c.j0 && j < d.win_c.j1;
+    };
+    auto wyf = [&](int i, int j) {
+        return i >= d.win_c.i0 && i < d.win_c.i1 && j >= d.win_n.j0 && j < d.win_n.j1;
+    };
     if (t <= nx) {  // dmx cross ghosts at ia = t
-        d.dmx[ix(d, t, -1)] = dmx_c(t, -1);
-        d.dmx[ix(d, t, ny)] = dmx_c(t, ny);
-        d.dmc[ix(d, t, -1)] = dmc_r(t, -1);
+        if (wxf(t, -1)) d.dmx[ix(d, t, -1)] = dmx_c(t, -1);
+        if (wxf(t, ny)) d.dmx[ix(d, t, ny)] = dmx_c(t, ny);
+        if (in(d.win_n, t, -1)) d.dmc[ix(d, t, -1)] = dmc_r(t, -1);
     }
     if (t <= ny) {  // dmy cross ghosts at ia = t
-        d.dmy[ix(d, -1, t)] = dmy_c(t, -1);
-        d.dmy[ix(d, nx, t)] = dmy_c(t, nx);
+        if (wyf(-1, t)) d.dmy[ix(d, -1, t)] = dmy_c(t, -1);
+        if (wyf(nx, t)) d.dmy[ix(d, nx, t)] = dmy_c(t, nx);
     }
     if (t <= ny + 1) {  // dmx along ghost (-1, ic), ic in [-1, ny]
         const int ic = t - 1;
-        d.dmx[ix(d, -1, ic)] = d.per_x ? dmx_c(nx - 1, ic) : -dmx_c(1, ic);
-        d.dmc[ix(d, -1, ic)] = d.per_x ? dmc_r(nx - 1, ic) : dmc_r(1, ic);
+        if (wxf(-1, ic)) d.dmx[ix(d, -1, ic)] = d.per_x ? dmx_c(nx - 1, ic) : -dmx_c(1, ic);
+        if (in(d.win_n, -1, ic)) d.dmc[ix(d, -1, ic)] = d.per_x ? dmc_r(nx - 1, ic) : dmc_r(1, ic);
     }
     if (t <= nx + 1) {  // dmy along ghost (ia = -1, ic) at (ic, -1), ic in [-1, nx]
         const int ic = t - 1;
-        d.dmy[ix(d, ic, -1)] = d.per_y ? dmy_c(ny - 1, ic) : -dmy_c(1, ic);
+        if (wyf(ic, -1)) d.dmy[ix(d, ic, -1)] = d.per_y ? dmy_c(ny - 1, ic) : -dmy_c(1, ic);
     }
 }
 
@@ -831,7 +859,8 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     __syncthreads();
     if (s_halt) return;
     const int nx = d.nx, ny = d.ny;
-    const int i0 = blockIdx.x * RTX, j0 = blockIdx.y * RTY;
+    const Rng rg = d.r_gath;
+    const int i0 = rg.i0 + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
     const Tile<NM> T = carve_tile<NM>(smem, i0 - G, j0 - G);
     const double dt = step_dt(d.ctl);
     const double cv = d.cv;
@@ -842,7 +871,7 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     for (int t = tid; t < RNN; t += RTX * RTY) {
         const int i = T.ci0 + t % RNW, j = T.cj0 + t / RNW;
         double hx = 0.0, hy = 0.0;
-        if (i <= nx + G && j <= ny + G) {
+        if (i >= -G && j >= -G && i <= nx + G && j <= ny + G) {
             const int n = ix(d, i, j);
             hx = d.uhx[n];
             hy = d.uhy[n];
@@ -852,7 +881,7 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     }
     for (int t = tid; t < RNC; t += RTX * RTY) {
         const int i = T.ci0 + t % RCW, j = T.cj0 + t / RCW;
-        if (i >= nx + G || j >= ny + G) continue;
+        if (i < -G || j < -G || i >= nx + G || j >= ny + G) continue;
         const int c = ix(d, i, j);
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
@@ -873,7 +902,7 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         const int i = T.ci0 + t % RNW, j = T.cj0 + t / RNW;
         double cfv = 0.0, fdx = 0.0, fdy = 0.0, fxv = 0.0, fyv = 0.0;
         int8_t sx = 0, sy = 0;
-        if (i <= nx + G && j <= ny + G) {
+        if (i >= -G && j >= -G && i <= nx + G && j <= ny + G) {
             const double hx = T.hx[t], hy = T.hy[t];
             const double ddx = hx * dt, ddy = hy * dt;
             cfv = fabs(ddx * ddy);
@@ -883,21 +912,21 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
                 sx = ddx > 0.0 ? 1 : -1;
                 sy = ddy > 0.0 ? 1 : -1;
             }
-            if (cfv > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
+            if (cfv > kCflFrac * cv && own_node(d, i, j)) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
             // faces on the region's last node row / column feed no region cell
             if (j < ny + G && j < T.cj0 + RNH - 1) {
                 const double ux1 = T.hx[t + RNW], uy1 = T.hy[t + RNW];
                 fdx = 0.5 * (hx + ux1) * dt;
                 double wl, wh;
                 face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * hx, dt * hy, dt * ux1, dt * uy1, fxv, wl, wh);
-                if (fabs(fxv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
+                if (fabs(fxv) > kCflFrac * cv && own_xface(d, i, j)) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
             }
             if (i < nx + G && i < T.ci0 + RNW - 1) {
                 const double ux1 = T.hx[t + 1], uy1 = T.hy[t + 1];
                 fdy = 0.5 * (hy + uy1) * dt;
                 double wl, wh;
                 face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * hy, dt * hx, dt * uy1, dt * ux1, fyv, wl, wh);
-                if (fabs(fyv) > kCflFrac * cv) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
+                if (fabs(fyv) > kCflFrac * cv && own_yface(d, i, j)) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
             }
         }
         T.cf[t] = cfv;
@@ -913,7 +942,7 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     // interfaces (remap.cpp:769-824)
     for (int t = tid; t < RNC; t += RTX * RTY) {
         const int i = T.ci0 + t % RCW, j = T.cj0 + t / RCW;
-        if (i >= nx + G || j >= ny + G) continue;
+        if (i < -G || j < -G || i >= nx + G || j >= ny + G) continue;
         const int q00 = T.n(i, j), q10 = q00 + 1, q01 = q00 + RNW, q11 = q01 + 1;
         auto cterm = [&](int q, int ni, int nj) -> double {  // remap.cpp:775-785
             const double dv = T.cf[q];
@@ -927,7 +956,7 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         };
         double v = cv + T.fxdv[q10] - T.fxdv[q00] + T.fydv[q01] - T.fydv[q00];
         v += cterm(q00, i, j) + cterm(q10, i + 1, j) + cterm(q01, i, j + 1) + cterm(q11, i + 1, j + 1);
-        if (v <= 0.0) raise(d.ctl, ekey(PH_COLLAPSED, j, i, 0));
+        if (v <= 0.0 && own_cell(d, i, j)) raise(d.ctl, ekey(PH_COLLAPSED, j, i, 0));
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
             const double ka = NM == 2 ? T.kk[a][t] : T.vl[t];
@@ -958,9 +987,9 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         const int ia = i0 + t % (RTX + 1), ic = j0 + t / (RTX + 1);
         dva[0] = dva[1] = 0.0;
         dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
-        if (ia <= nx && ic < ny) {
+        if (ia <= min(nx, rg.i1) && ic < min(ny, rg.j1)) {
             const double tot = face_item_t<NM, 1>(d, T, ia, ic, dt, dm, dme, dva);
-            if (ia < i0 + RTX || ia == nx) d.dmx[ix(d, ia, ic)] = tot;
+            if (ia < i0 + RTX || ia == min(nx, rg.i1)) d.dmx[ix(d, ia, ic)] = tot;
         }
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
@@ -973,9 +1002,9 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         const int ic = i0 + t % RTX, ja = j0 + t / RTX;
         dva[0] = dva[1] = 0.0;
         dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
-        if (ic < nx && ja <= ny) {
+        if (ic < min(nx, rg.i1) && ja <= min(ny, rg.j1)) {
             const double tot = face_item_t<NM, 0>(d, T, ic, ja, dt, dm, dme, dva);
-            if (ja < j0 + RTY || ja == ny) d.dmy[ix(d, ic, ja)] = tot;
+            if (ja < j0 + RTY || ja == min(ny, rg.j1)) d.dmy[ix(d, ic, ja)] = tot;
         }
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
@@ -988,9 +1017,10 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         const int ni = i0 + t % (RTX + 1), nj = j0 + t / (RTX + 1);
         dva[0] = dva[1] = 0.0;
         dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
-        if (ni <= nx && nj <= ny) {
+        const int ni1 = min(nx, rg.i1), nj1 = min(ny, rg.j1);
+        if (ni <= ni1 && nj <= nj1) {
             const double tot = corner_item_t<NM>(d, T, ni, nj, dt, dm, dme, dva);
-            if ((ni < i0 + RTX || ni == nx) && (nj < j0 + RTY || nj == ny)) d.dmc[ix(d, ni, nj)] = tot;
+            if ((ni < i0 + RTX || ni == ni1) && (nj < j0 + RTY || nj == nj1)) d.dmc[ix(d, ni, nj)] = tot;
         }
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
@@ -1003,7 +1033,8 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     // ---- gather in reference order (App. C item 3)
     const int tx = tid % RTX, ty = tid / RTX;
     const int i = i0 + tx, j = j0 + ty;
-    if (i >= nx || j >= ny) return;
+    if (!in(rg, i, j)) return;
+    const bool own = own_cell(d, i, j);
     const int c = ix(d, i, j);
     const int tc = T.c(i, j);
     const int xl = tx + ty * (RTX + 1), xr = xl + 1;
@@ -1072,9 +1103,9 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
 #pragma unroll
         for (int q = 0; q < 5; ++q)
             if (viol < cand[q]) viol = cand[q];
-        if (viol > 0.0) atomicMax(&d.ctl->kviol_bits, (unsigned long long)__double_as_longlong(viol));
+        if (viol > 0.0 && own) atomicMax(&d.ctl->kviol_bits, (unsigned long long)__double_as_longlong(viol));
         if (k0 < 0.0 || k0 > 1.0) {
-            atomicAdd(&d.ctl->step_clip, 1);
+            if (own) atomicAdd(&d.ctl->step_clip, 1);
             k0 = (k0 < 0.0) ? 0.0 : ((1.0 < k0) ? 1.0 : k0);
         }
         if (k0 < kPureTol) k0 = 0.0;
@@ -1112,11 +1143,11 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         mtot += ma;
     }
     if (bad_sub < 0 && mtot <= 0.0) bad_sub = 2;
-    if (bad_sub >= 0) raise(d.ctl, ekey(PH_NEGMASS, j, i, bad_sub));
+    if (bad_sub >= 0 && own) raise(d.ctl, ekey(PH_NEGMASS, j, i, bad_sub));
     d.mcell[c] = mtot;
     if (NM == 2) {
         d.sliver[c] = sl;
-        if (sl) atomicAdd(&d.row_slivers[j], 1);
+        if (sl) atomicAdd(&d.row_slivers[j - d.win_c.j0], 1);
     }
 }
 
@@ -1127,17 +1158,18 @@ __global__ void k_slivers(Dev d) {
     if (halted(d.ctl)) return;
     const int lane = threadIdx.x;
     const int nx = d.nx, ny = d.ny;
-    for (int j0 = 0; j0 < ny; j0 += 32) {
+    const Rng rg = d.r_gath;  // the cells finalized by this block, in row-major order
+    for (int j0 = rg.j0; j0 < rg.j1; j0 += 32) {
         const int jr = j0 + lane;
-        const int cnt = jr < ny ? d.row_slivers[jr] : 0;
+        const int cnt = jr < rg.j1 ? d.row_slivers[jr - d.win_c.j0] : 0;
         unsigned rows = __ballot_sync(0xffffffffu, cnt != 0);
         while (rows) {
             const int r = __ffs(rows) - 1;
             rows &= rows - 1;
             const int j = j0 + r;
-            for (int i0 = 0; i0 < nx; i0 += 32) {
+            for (int i0 = rg.i0; i0 < rg.i1; i0 += 32) {
                 const int ic = i0 + lane;
-                const uint8_t f = ic < nx ? d.sliver[ix(d, ic, j)] : 0;
+                const uint8_t f = ic < rg.i1 ? d.sliver[ix(d, ic, j)] : 0;
                 unsigned cells = __ballot_sync(0xffffffffu, f != 0);
                 while (cells) {
                     const int b = __ffs(cells) - 1;
@@ -1160,6 +1192,7 @@ __global__ void k_slivers(Dev d) {
                                         if (d.per_x) ni = (ni + 2 * nx) % nx;
                                         if (d.per_y) nj = (nj + 2 * ny) % ny;
                                         if (ni < 0 || ni >= nx || nj < 0 || nj >= ny) continue;
+                                        if (!in(rg, ni, nj)) continue;  // outside this block's finalized cells
                                         const int nc = ix(d, ni, nj);
                                         if (d.nm[a][nc] <= 0.0) continue;
                                         if (d.nk[a][nc] > bk) {
@@ -1175,7 +1208,7 @@ __global__ void k_slivers(Dev d) {
                                 d.ne[a][bc] = d.me[a][bc] / d.nm[a][bc];
                                 d.mcell[bc] += smv;
                             } else {
-                                d.ctl->step_fix += 1;
+                                if (own_cell(d, si, sj)) d.ctl->step_fix += 1;
                                 const int bm = 1 - a;
                                 d.nm[bm][sc] += smv;
                                 d.me[bm][sc] += smev;
@@ -1188,7 +1221,7 @@ __global__ void k_slivers(Dev d) {
                     __syncwarp();
                 }
             }
-            if (lane == 0) d.row_slivers[j] = 0;
+            if (lane == 0) d.row_slivers[j - d.win_c.j0] = 0;
             __syncwarp();
         }
     }
@@ -1235,7 +1268,7 @@ __device__ __forceinline__ void dual_face_item(const Dev& d, int i, int j) {
         bool bad = false;
         const double ufx = dual_face_value(d, d.ulx, AX, ia_d, ic, dt, wa, sgn, ufdt, bad);
         const double ufy = dual_face_value(d, d.uly, AX, ia_d, ic, dt, wa, sgn, ufdt, bad);
-        if (bad) raise(d.ctl, ekey(AX ? PH_GRAD_DUALX : PH_GRAD_DUALY, ic, ia, 0));
+        if (bad && own_node(d, i, j)) raise(d.ctl, ekey(AX ? PH_GRAD_DUALX : PH_GRAD_DUALY, ic, ia, 0));
         mx = ufx * dm;
         my = ufy * dm;
     }
@@ -1320,7 +1353,7 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
                 bool bad = false;
                 ufx = corner_diag(d, ax_, xlx, xly, dxp, dyp, lwx, lwy, bad);
                 ufy = corner_diag(d, ay_, xlx, xly, dxp, dyp, lwx, lwy, bad);
-                if (bad) raise(d.ctl, ekey(PH_GRAD_DUALC, j, i, pr));
+                if (bad && own_node(d, i, j)) raise(d.ctl, ekey(PH_GRAD_DUALC, j, i, pr));
             }
             cx = ufx * Fv;
             cy = ufy * Fv;
@@ -1336,9 +1369,9 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
 __global__ void k_dual_items(Dev d) {
     if (halted(d.ctl)) return;
     int i, j;
-    tid2(i, j, 0, 0);
+    tid2(i, j, d.r_dual.i0, d.r_dual.j0);
     const int iend = d.per_x ? d.nx - 1 : d.nx, jend = d.per_y ? d.ny - 1 : d.ny;
-    if (i > iend || j > jend) return;
+    if (!in(d.r_dual, i, j) || i < 0 || j < 0 || i > iend || j > jend) return;
     dual_face_item<1>(d, i, j);
     dual_face_item<0>(d, i, j);
     dual_corner_items(d, i, j);
@@ -1350,9 +1383,9 @@ __global__ void k_dual_items(Dev d) {
 __global__ void k_node_update(Dev d) {
     if (halted(d.ctl)) return;
     int i, j;
-    tid2(i, j, 0, 0);
+    tid2(i, j, d.r_node.i0, d.r_node.j0);
     const int nx = d.nx, ny = d.ny;
-    if (i > nx || j > ny) return;
+    if (!in(d.r_node, i, j) || i < 0 || j < 0 || i > nx || j > ny) return;
     const int iend = d.per_x ? nx - 1 : nx, jend = d.per_y ? ny - 1 : ny;
     const int si = (d.per_x && i == nx) ? 0 : i, sj = (d.per_y && j == ny) ? 0 : j;
     const int s = ix(d, si, sj);
@@ -1442,7 +1475,7 @@ __global__ void k_node_update(Dev d) {
     const double mp_lag = 0.25 * (ml(ix(d, si - 1, sj - 1)) + ml(ix(d, si, sj - 1)) + ml(ix(d, si - 1, sj)) + ml(s));
     const double mp_new =
         0.25 * (d.mcell[ix(d, si - 1, sj - 1)] + d.mcell[ix(d, si, sj - 1)] + d.mcell[ix(d, si - 1, sj)] + d.mcell[s]);
-    if (mp_new <= 0.0 && si == i && sj == j) raise(d.ctl, ekey(PH_NODAL_MASS, j, i, 0));
+    if (mp_new <= 0.0 && si == i && sj == j && own_node(d, i, j)) raise(d.ctl, ekey(PH_NODAL_MASS, j, i, 0));
     const double inv = 1.0 / mp_new;
     const int o = ix(d, i, j);
     double ux = inv * (mp_lag * d.ulx[s] + ax), uy = inv * (mp_lag * d.uly[s] + ay);
@@ -1583,10 +1616,10 @@ __global__ void __launch_bounds__(256) k_post(Dev d, int run_loop) {
     __syncthreads();
     if (s_halt) return;
     int i, j;
-    tid2(i, j, -G, -G);
+    tid2(i, j, d.r_sync.i0, d.r_sync.j0);
     const int nx = d.nx, ny = d.ny;
     unsigned long long wb = 0ull;
-    if (i < nx + G && j < ny + G) {
+    if (in(d.r_sync, i, j)) {
         const int c = ix(d, i, j);
         const double cv = d.cv;
         double ka[2], ma[2], ea[2];
@@ -1613,7 +1646,7 @@ __global__ void __launch_bounds__(256) k_post(Dev d, int run_loop) {
         d.np_mix[c] = p;
         d.nvol[c] = cv;
         const bool interior = i >= 0 && j >= 0 && i < nx && j < ny;
-        if (interior) {
+        if (interior && in(d.r_nrm, i, j)) {
             if (NM == 2) {  // normals of the new fractions
                 double nrx = d.nrx[c], nry = d.nry[c];
                 if (is_mixed(ka[0])) {
@@ -1631,7 +1664,7 @@ __global__ void __launch_bounds__(256) k_post(Dev d, int run_loop) {
                 d.nnrx[c] = nrx;
                 d.nnry[c] = nry;
             }
-            if (run_loop) {
+            if (run_loop && own_cell(d, i, j)) {
                 if (!isfinite(m) | !isfinite(emix) | !isfinite(p)) raise(d.ctl, ekey(PH_NAN_CELL, j, i, 0));
                 // next step's wave speed on the new State
                 double cs = 0.0;
@@ -1658,7 +1691,7 @@ __global__ void __launch_bounds__(256) k_post(Dev d, int run_loop) {
             }
         }
     }
-    if (run_loop && i >= 0 && j >= 0 && i <= nx && j <= ny) {
+    if (run_loop && i >= 0 && j >= 0 && i <= nx && j <= ny && own_node(d, i, j)) {
         const int n = ix(d, i, j);
         if (!isfinite(d.nux[n]) | !isfinite(d.nuy[n])) raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));
     }
@@ -1705,6 +1738,11 @@ static dim3 grid_rect(int w, int h) {
     return dim3((unsigned)((w + b.x - 1) / b.x), (unsigned)((h + b.y - 1) / b.y));
 }
 static unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
+static int ext(int a, int b) { return b > a ? b - a : 1; }
+static dim3 grid_of(const Rng& r) { return grid_rect(ext(r.i0, r.i1), ext(r.j0, r.j1)); }
+static dim3 tiles_of(const Rng& r, int tx, int ty) {
+    return dim3((unsigned)((ext(r.i0, r.i1) + tx - 1) / tx), (unsigned)((ext(r.j0, r.j1) + ty - 1) / ty));
+}
 
 void launch_begin(Ctl* c, int mode, double dt, cudaStream_t s) { k_begin<<<1, 1, 0, s>>>(c, mode, dt); }
 
@@ -1742,7 +1780,7 @@ void launch_ghost_nodes(const Dev& d, const FieldList& fl, cudaStream_t s) {
 }
 
 void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s) {
-    const dim3 g = grid_rect(d.nx + 2 * G, d.ny + 2 * G);
+    const dim3 g = grid_of(d.win_c);
     if (d.nmat == 2)
         { k_sync<2><<<g, blk2(), 0, s>>>(d, next, respect_halt); ++g_launches; }
     else
@@ -1750,8 +1788,8 @@ void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s) {
 }
 
 void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
-    const dim3 gc = grid_rect(d.nx, d.ny);
-    const dim3 gl((unsigned)((d.nx + 1 + LTX - 1) / LTX), (unsigned)((d.ny + 1 + LTY - 1) / LTY));
+    const dim3 gc = grid_of(d.r_lagc);
+    const dim3 gl = tiles_of(d.r_lagn, LTX, LTY);
     if (d.nmat == 2)
         { k_lag_cells<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
     else
@@ -1789,7 +1827,7 @@ void remap_init() {
 // k_post (sync_derived, normals, and in the run loop nan_scan + next cfl) and
 // the ghost layers of the new u and normals (assemble_state's fill_ghosts).
 void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s) {
-    const dim3 gp((unsigned)((d.nx + 1 + 2 * G + 31) / 32), (unsigned)((d.ny + 1 + 2 * G + 7) / 8));
+    const dim3 gp = tiles_of(d.r_sync, 32, 8);
     if (d.nmat == 2)
         { k_post<2><<<gp, dim3(32, 8), 0, s>>>(d, run_loop); ++g_launches; }
     else
@@ -1811,10 +1849,10 @@ void launch_remap_core(const Dev& d, cudaStream_t s) {
     remap_init();
     const int nx = d.nx, ny = d.ny;
     const bool two = d.nmat == 2;
-    const dim3 gall = grid_rect(nx + 1 + 2 * G, ny + 1 + 2 * G);
-    const dim3 gc = grid_rect(nx, ny), gn = grid_rect(nx + 1, ny + 1);
-    if (!d.remap_velocity) { k_copy_u<<<gall, blk2(), 0, s>>>(d); ++g_launches; }
-    const dim3 gft((unsigned)((nx + RTX - 1) / RTX), (unsigned)((ny + RTY - 1) / RTY));
+    (void)nx;
+    (void)ny;
+    if (!d.remap_velocity) { k_copy_u<<<grid_of(d.win_n), blk2(), 0, s>>>(d); ++g_launches; }
+    const dim3 gft = tiles_of(d.r_gath, RTX, RTY);
     if (two) {
         { k_remap_tile<2><<<gft, RTX * RTY, remap_smem_bytes<2>(), s>>>(d); ++g_launches; }
         { k_slivers<<<1, 32, 0, s>>>(d); ++g_launches; }
@@ -1835,15 +1873,15 @@ void launch_remap_core(const Dev& d, cudaStream_t s) {
     FieldList none{};
     launch_ghost_multi(d, fl, none, 1, 1, s);
     if (d.remap_velocity) {
-        { k_dual_items<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
-        { k_node_update<<<gn, blk2(), 0, s>>>(d); ++g_launches; }
+        { k_dual_items<<<grid_of(d.r_dual), blk2(), 0, s>>>(d); ++g_launches; }
+        { k_node_update<<<grid_of(d.r_node), blk2(), 0, s>>>(d); ++g_launches; }
     }
 }
 
 void launch_step(const Dev& d, cudaStream_t s, int* row_slivers) {
     { k_step_start<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy); ++g_launches; }
     launch_lagrange(d, 0, s);
-    cudaMemsetAsync(row_slivers, 0, sizeof(int) * (size_t)d.ny, s);
+    cudaMemsetAsync(row_slivers, 0, sizeof(int) * (size_t)(d.win_c.j1 - d.win_c.j0 + 1), s);
     launch_remap_core(d, s);
     post_and_ghosts(d, 1, s);
     { k_commit_finish<<<1, 1, 0, s>>>(d.ctl); ++g_launches; }
