@@ -213,6 +213,34 @@ int h2d_run(h2d_ctx* ctx, h2d_run_args* args);
  * out = {mass, mass_mat0, mass_mat1, momentum.x, momentum.y, internal_energy}. */
 int h2d_totals(h2d_ctx* ctx, double out[6]);
 
+/* ---- 2D block decomposition (no reference counterpart) ----
+ * A block context owns [oi, oi+bnx) x [oj, oj+bny) of the global mesh plus a
+ * halo (>= 8 cells). One run-loop step computes the whole step on the window
+ * with redundant halo work, so ONE halo exchange of the State (8 neighbours,
+ * corners included) and one all-reduce of the next step's wave speed per step
+ * keep every owned value bit-identical to the single-domain run. Walls only. */
+int h2d_create_block(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx** out);
+/* window upload / owned-region download in the GLOBAL reference layout */
+int h2d_block_upload(h2d_ctx* ctx, const h2d_state* global_state);
+int h2d_block_download(h2d_ctx* ctx, h2d_state* global_state);
+/* run control: begin (computes the owned wave speed of the initial State),
+ * one graph-launched step, the scalars to combine across blocks
+ * {next wave-speed max bits (MAX), next cfl error key (MIN), error key (MIN),
+ * done}, writing the combined values back, and undoing a commit when another
+ * block failed earlier in the same step */
+int h2d_block_begin(h2d_ctx* ctx, int max_steps, double t_end, double cfl);
+int h2d_block_step(h2d_ctx* ctx);
+int h2d_block_scalars(h2d_ctx* ctx, unsigned long long out[4]);
+int h2d_block_set(h2d_ctx* ctx, const unsigned long long in[3]);
+int h2d_block_rollback(h2d_ctx* ctx);
+/* halo exchange with the neighbour at (dx, dy) in {-1,0,1}^2: buffer sizes,
+ * pack of the owned data it needs, unpack of the data it sent (device ptrs) */
+long long h2d_halo_bytes(h2d_ctx* ctx, int dx, int dy, int pack);
+int h2d_halo_pack(h2d_ctx* ctx, int dx, int dy, void* dev_buf);
+int h2d_halo_unpack(h2d_ctx* ctx, int dx, int dy, const void* dev_buf);
+/* counters, dt log and first error of the block's run (like h2d_run) */
+int h2d_block_result(h2d_ctx* ctx, h2d_run_args* args);
+
 /* ---- benchmark support (no reference counterpart) ---------------------- */
 /* Kernels launched by this library in the calling process so far. */
 long long h2d_launch_count(void);

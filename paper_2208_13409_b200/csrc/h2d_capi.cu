@@ -532,6 +532,7 @@ void h2d_destroy(h2d_ctx* c) {
     if (c->ctl) cudaFree(c->ctl);
     if (c->hctl) cudaFreeHost(c->hctl);
     if (c->dt_log) cudaFree(c->dt_log);
+    if (c->xbuf) cudaFree(c->xbuf);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
 }
@@ -877,6 +878,259 @@ int h2d_flush_l2(h2d_ctx* c, long long bytes) {
     CK(cudaMemsetAsync(c->flush, c->flush_bytes & 0xFF, c->flush_bytes, c->st));
     CK(cudaStreamSynchronize(c->st));
     return 0;
+}
+
+// ---- 2D block decomposition -------------------------------------------------
+
+namespace {
+
+int ensure_xbuf(h2d_ctx* c, size_t bytes) {
+    if (bytes <= c->xbuf_bytes) return 0;
+    if (c->xbuf) cudaFree(c->xbuf);
+    c->xbuf = nullptr;
+    c->xbuf_bytes = 0;
+    CK(cudaMalloc(&c->xbuf, bytes));
+    c->xbuf_bytes = bytes;
+    return 0;
+}
+
+// global-layout host planes <-> this block's planes over rectangle r
+int global_rect(h2d_ctx* c, double* host, int vec, bool node, Rng r, double* px, double* py, bool upload) {
+    if (!host || r.i1 <= r.i0 || r.j1 <= r.j0) return 0;
+    const int W = c->nx + (node ? 1 : 0) + 2 * G, Hh = c->ny + (node ? 1 : 0) + 2 * G;
+    const size_t bytes = (size_t)W * Hh * (vec ? 2 : 1) * sizeof(double);
+    if (int rc = ensure_xbuf(c, bytes)) return rc;
+    const Dev d = make_dev(c, c->cur, 1);
+    if (upload) {
+        CK(cudaMemcpyAsync(c->xbuf, host, bytes, cudaMemcpyHostToDevice, c->st));
+        launch_global_xfer(d, c->xbuf, W, r, px, py, vec, 1, c->st);
+    } else {
+        CK(cudaMemcpyAsync(c->xbuf, host, bytes, cudaMemcpyHostToDevice, c->st));  // keep other blocks' parts
+        launch_global_xfer(d, c->xbuf, W, r, px, py, vec, 0, c->st);
+        CK(cudaMemcpyAsync(host, c->xbuf, bytes, cudaMemcpyDeviceToHost, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+// state planes exchanged with the neighbours: cells and nodes
+void state_lists(h2d_ctx* c, FieldList& cl, FieldList& nl) {
+    const StateBufs& sb = c->sb[c->cur];
+    cl = FieldList{};
+    nl = FieldList{};
+    for (int a = 0; a < c->nmat; ++a) {
+        cl.f[cl.n++] = sb.m[a];
+        cl.f[cl.n++] = sb.e[a];
+        cl.f[cl.n++] = sb.k[a];
+    }
+    cl.f[cl.n++] = sb.vol;
+    cl.f[cl.n++] = sb.m_mix;
+    cl.f[cl.n++] = sb.e_mix;
+    cl.f[cl.n++] = sb.rho_mix;
+    cl.f[cl.n++] = sb.p_mix;
+    cl.f[cl.n++] = sb.nrx;
+    cl.f[cl.n++] = sb.nry;
+    nl.f[nl.n++] = sb.ux;
+    nl.f[nl.n++] = sb.uy;
+}
+
+// halo rectangles (global indices) for the neighbour in direction (dx, dy):
+// pack = my owned data that neighbour needs, unpack = my halo it fills
+void halo_rects(h2d_ctx* c, int dx, int dy, bool pack, Rng& rc, Rng& rn) {
+    const h2d_block& b = c->blk;
+    const Dev& d = c->base;
+    const int H = b.halo;
+    auto axis = [&](int dd, int o, int n, int own_c0, int own_c1, int own_n0, int own_n1, int& c0, int& c1,
+                    int& n0, int& n1) {
+        if (dd == 0) {
+            c0 = own_c0;
+            c1 = own_c1;
+            n0 = own_n0;
+            n1 = own_n1;
+        } else if (pack) {
+            if (dd > 0) {
+                c0 = n0 = o + n - H;
+                c1 = n1 = o + n;
+            } else {
+                c0 = n0 = o;
+                c1 = o + H;
+                n1 = o + H + 1;
+            }
+        } else {
+            if (dd < 0) {
+                c0 = n0 = o - H;
+                c1 = n1 = o;
+            } else {
+                c0 = n0 = o + n;
+                c1 = o + n + H;
+                n1 = o + n + H + 1;
+            }
+        }
+    };
+    axis(dx, b.oi, b.bnx, d.own_c.i0, d.own_c.i1, d.own_n.i0, d.own_n.i1, rc.i0, rc.i1, rn.i0, rn.i1);
+    axis(dy, b.oj, b.bny, d.own_c.j0, d.own_c.j1, d.own_n.j0, d.own_n.j1, rc.j0, rc.j1, rn.j0, rn.j1);
+}
+
+long long rect_doubles(const FieldList& cl, const FieldList& nl, const Rng& rc, const Rng& rn) {
+    return (long long)(rc.i1 - rc.i0) * (rc.j1 - rc.j0) * cl.n + (long long)(rn.i1 - rn.i0) * (rn.j1 - rn.j0) * nl.n;
+}
+
+}  // namespace
+
+int h2d_block_upload(h2d_ctx* c, const h2d_state* g) {
+    cudaSetDevice(c->device);
+    const Dev& d = c->base;
+    StateBufs& s = c->sb[c->cur];
+    const Rng wc = d.win_c, wn = d.win_n;
+    for (int a = 0; a < c->nmat; ++a) {
+        if (int rc = global_rect(c, g->m[a], 0, false, wc, s.m[a], nullptr, true)) return rc;
+        if (int rc = global_rect(c, g->e[a], 0, false, wc, s.e[a], nullptr, true)) return rc;
+        if (int rc = global_rect(c, g->k[a], 0, false, wc, s.k[a], nullptr, true)) return rc;
+    }
+    double* dv[5] = {s.vol, s.m_mix, s.e_mix, s.rho_mix, s.p_mix};
+    double* hv[5] = {g->vol, g->m_mix, g->e_mix, g->rho_mix, g->p_mix};
+    for (int q = 0; q < 5; ++q)
+        if (int rc = global_rect(c, hv[q], 0, false, wc, dv[q], nullptr, true)) return rc;
+    if (int rc = global_rect(c, g->iface_normal, 1, false, wc, s.nrx, s.nry, true)) return rc;
+    if (int rc = global_rect(c, g->u, 1, true, wn, s.ux, s.uy, true)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    c->hctl->step = g->step;
+    c->hctl->time = g->time;
+    return ctl_push(c);
+}
+
+int h2d_block_download(h2d_ctx* c, h2d_state* g) {
+    cudaSetDevice(c->device);
+    const Dev& d = c->base;
+    StateBufs& s = c->sb[c->cur];
+    const Rng oc = d.own_c, on = d.own_n;
+    for (int a = 0; a < c->nmat; ++a) {
+        if (int rc = global_rect(c, g->m[a], 0, false, oc, s.m[a], nullptr, false)) return rc;
+        if (int rc = global_rect(c, g->e[a], 0, false, oc, s.e[a], nullptr, false)) return rc;
+        if (int rc = global_rect(c, g->k[a], 0, false, oc, s.k[a], nullptr, false)) return rc;
+    }
+    double* dv[5] = {s.vol, s.m_mix, s.e_mix, s.rho_mix, s.p_mix};
+    double* hv[5] = {g->vol, g->m_mix, g->e_mix, g->rho_mix, g->p_mix};
+    for (int q = 0; q < 5; ++q)
+        if (int rc = global_rect(c, hv[q], 0, false, oc, dv[q], nullptr, false)) return rc;
+    if (int rc = global_rect(c, g->iface_normal, 1, false, oc, s.nrx, s.nry, false)) return rc;
+    if (int rc = global_rect(c, g->u, 1, true, on, s.ux, s.uy, false)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    g->step = c->hctl->step;
+    g->time = c->hctl->time;
+    return 0;
+}
+
+int h2d_block_begin(h2d_ctx* c, int max_steps, double t_end, double cfl) {
+    cudaSetDevice(c->device);
+    if (int rc = ctl_reset(c)) return rc;
+    Ctl& h = *c->hctl;
+    h.t_end = t_end;
+    h.cfl = cfl;
+    h.max_steps = max_steps;
+    h.steps_done = 0;
+    h.floor_count = h.k_clip_count = h.mass_fix_count = 0;
+    h.max_k_violation = 0.0;
+    const int cap = max_steps > 0 ? max_steps : 4096;
+    if (cap > c->dt_log_cap) {
+        if (c->dt_log) cudaFree(c->dt_log);
+        c->dt_log = nullptr;
+        CK(cudaMalloc(&c->dt_log, sizeof(double) * (size_t)cap));
+        c->dt_log_cap = cap;
+    }
+    h.dt_log = c->dt_log;
+    h.dt_log_cap = c->dt_log_cap;
+    if (int rc = ctl_push(c)) return rc;
+    if (int rc = ensure_graphs(c)) return rc;
+    enqueue_cfl_next(c);  // wave speed of the owned cells of the initial State
+    if (int rc = check_launch(c)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    return 0;
+}
+
+int h2d_block_scalars(h2d_ctx* c, unsigned long long out[4]) {
+    cudaSetDevice(c->device);
+    if (int rc = ctl_pull(c)) return rc;
+    out[0] = c->hctl->next_wmax_bits;
+    out[1] = c->hctl->next_err_key;
+    out[2] = c->hctl->err_key;
+    out[3] = (unsigned long long)c->hctl->done;
+    return 0;
+}
+
+int h2d_block_set(h2d_ctx* c, const unsigned long long in[3]) {
+    cudaSetDevice(c->device);
+    if (int rc = ctl_pull(c)) return rc;
+    c->hctl->next_wmax_bits = in[0];
+    c->hctl->next_err_key = in[1];
+    c->hctl->err_key = in[2];
+    return ctl_push(c);
+}
+
+int h2d_block_step(h2d_ctx* c) {
+    cudaSetDevice(c->device);
+    if (int rc = launch_step_graph(c, c->cur)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    c->cur = c->hctl->cur;
+    return 0;
+}
+
+int h2d_block_rollback(h2d_ctx* c) {
+    cudaSetDevice(c->device);
+    launch_rollback(c->ctl, c->st);
+    if (int rc = check_launch(c)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    c->cur = c->hctl->cur;
+    return 0;
+}
+
+long long h2d_halo_bytes(h2d_ctx* c, int dx, int dy, int pack) {
+    FieldList cl, nl;
+    state_lists(c, cl, nl);
+    Rng rc, rn;
+    halo_rects(c, dx, dy, pack != 0, rc, rn);
+    return rect_doubles(cl, nl, rc, rn) * (long long)sizeof(double);
+}
+
+int h2d_halo_pack(h2d_ctx* c, int dx, int dy, void* dev_buf) {
+    cudaSetDevice(c->device);
+    FieldList cl, nl;
+    state_lists(c, cl, nl);
+    Rng rc, rn;
+    halo_rects(c, dx, dy, true, rc, rn);
+    launch_rect_xfer(make_dev(c, c->cur, 1), cl, nl, rc, rn, static_cast<double*>(dev_buf), 1, c->st);
+    if (int rc2 = check_launch(c)) return rc2;
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+int h2d_halo_unpack(h2d_ctx* c, int dx, int dy, const void* dev_buf) {
+    cudaSetDevice(c->device);
+    FieldList cl, nl;
+    state_lists(c, cl, nl);
+    Rng rc, rn;
+    halo_rects(c, dx, dy, false, rc, rn);
+    launch_rect_xfer(make_dev(c, c->cur, 1), cl, nl, rc, rn, const_cast<double*>(static_cast<const double*>(dev_buf)),
+                     0, c->st);
+    if (int rc2 = check_launch(c)) return rc2;
+    CK(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+int h2d_block_result(h2d_ctx* c, h2d_run_args* a) {
+    cudaSetDevice(c->device);
+    if (int rc = ctl_pull(c)) return rc;
+    const Ctl& h = *c->hctl;
+    a->steps_done = h.steps_done;
+    a->floor_count = h.floor_count;
+    a->diag.k_clip_count = h.k_clip_count;
+    a->diag.mass_fix_count = h.mass_fix_count;
+    a->diag.max_k_violation = h.max_k_violation;
+    if (a->dt_log && h.steps_done > 0) {
+        const int n = h.steps_done < a->dt_log_cap ? h.steps_done : a->dt_log_cap;
+        CK(cudaMemcpy(a->dt_log, c->dt_log, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost));
+    }
+    return decode_error(c, true);
 }
 
 int h2d_last_error(h2d_ctx* c, h2d_error* e) {

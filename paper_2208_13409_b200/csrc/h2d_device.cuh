@@ -75,6 +75,9 @@ struct Ctl {
     int pad2_;
     double* dt_log;   // device array, steps_done entries
     int dt_log_cap;
+    // undo record of the last commit (block mode: a peer block failed first)
+    double prev_time, prev_max_k_violation;
+    int committed, counted;
 };
 
 // Every thread of a kernel reads the control block: go through the read-only

@@ -1585,13 +1585,18 @@ __global__ void k_step_start(Ctl* c, double dx, double dy) {
 // (remap.cpp:1084-1085) unless an earlier phase failed; nan_scan errors come
 // after the commit (harness.cpp:402-409), so they still commit.
 __global__ void k_commit_finish(Ctl* c) {
+    c->committed = 0;
+    c->counted = 0;
     if (c->done) return;
     const unsigned long long e = c->err_key;
     const bool ok = e == kNoErr;
     if (!ok && (int)(e >> 58) < PH_NAN_CELL) return;
+    c->prev_time = c->time;
+    c->prev_max_k_violation = c->max_k_violation;
     c->time = c->time + c->dt;
     c->step += 1;
     c->cur ^= 1;
+    c->committed = 1;
     if (!ok) return;
     if (c->dt_log && c->steps_done < c->dt_log_cap) c->dt_log[c->steps_done] = c->dt;
     c->steps_done += 1;
@@ -1600,6 +1605,85 @@ __global__ void k_commit_finish(Ctl* c) {
     c->mass_fix_count += c->step_fix;
     const double v = __longlong_as_double((long long)c->kviol_bits);
     if (v > c->max_k_violation) c->max_k_violation = v;
+    c->counted = 1;
+}
+
+// Undo the last commit (block mode: another block failed in the same step
+// before its commit, so the decomposed State must stay at the previous step).
+__global__ void k_rollback(Ctl* c) {
+    if (!c->committed) return;
+    c->time = c->prev_time;
+    c->step -= 1;
+    c->cur ^= 1;
+    if (c->counted) {
+        c->steps_done -= 1;
+        c->floor_count -= c->step_floor;
+        c->k_clip_count -= c->step_clip;
+        c->mass_fix_count -= c->step_fix;
+        c->max_k_violation = c->prev_max_k_violation;
+    }
+    c->committed = 0;
+    c->counted = 0;
+}
+
+// Copy a rectangle (global indices, half-open) of several planes to / from a
+// contiguous buffer: cell planes use `rc`, node planes `rn` (halo exchange).
+__global__ void k_rect_xfer(Dev d, FieldList cells, FieldList nodes, Rng rc, Rng rn, double* buf, int to_buf) {
+    const int wc = rc.i1 - rc.i0, hc = rc.j1 - rc.j0, wn = rn.i1 - rn.i0, hn = rn.j1 - rn.j0;
+    const long long ac = (long long)wc * hc, an = (long long)wn * hn;
+    const long long total = ac * cells.n + an * nodes.n;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        double* pl;
+        int i, j;
+        if (t < ac * cells.n) {
+            const int f = (int)(t / ac);
+            const long long r = t - f * ac;
+            pl = cells.f[f];
+            i = rc.i0 + (int)(r % wc);
+            j = rc.j0 + (int)(r / wc);
+        } else {
+            const long long u = t - ac * cells.n;
+            const int f = (int)(u / an);
+            const long long r = u - f * an;
+            pl = nodes.f[f];
+            i = rn.i0 + (int)(r % wn);
+            j = rn.j0 + (int)(r / wn);
+        }
+        if (to_buf)
+            buf[t] = pl[ix(d, i, j)];
+        else
+            pl[ix(d, i, j)] = buf[t];
+    }
+}
+
+// Rectangle copy between a global-layout host mirror in a device buffer
+// (reference Field layout of the whole mesh: pitch W, ghost 2) and this
+// block's planes; vec != 0: interleaved Vec2 source split into x / y planes.
+__global__ void k_global_xfer(Dev d, double* gx, int W, Rng r, double* px, double* py, int vec, int to_block) {
+    const int w = r.i1 - r.i0, h = r.j1 - r.j0;
+    const long long n = (long long)w * h;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int i = r.i0 + (int)(t % w), j = r.j0 + (int)(t / w);
+        const long long gi = (long long)(j + G) * W + (i + G);
+        const int li = ix(d, i, j);
+        if (to_block) {
+            if (vec) {
+                px[li] = gx[2 * gi];
+                py[li] = gx[2 * gi + 1];
+            } else {
+                px[li] = gx[gi];
+            }
+        } else {
+            if (vec) {
+                gx[2 * gi] = px[li];
+                gx[2 * gi + 1] = py[li];
+            } else {
+                gx[gi] = px[li];
+            }
+        }
+    }
 }
 
 // The end of the remap on the new State, one thread per position of the
@@ -1898,6 +1982,23 @@ void launch_cfl_next(const Dev& d, cudaStream_t s) {
         { k_cfl<2><<<nb, 256, 0, s>>>(d, 1); ++g_launches; }
     else
         { k_cfl<1><<<nb, 256, 0, s>>>(d, 1); ++g_launches; }
+}
+
+void launch_rollback(Ctl* c, cudaStream_t s) { k_rollback<<<1, 1, 0, s>>>(c); ++g_launches; }
+void launch_rect_xfer(const Dev& d, const FieldList& cells, const FieldList& nodes, Rng rc, Rng rn, double* buf,
+                      int to_buf, cudaStream_t s) {
+    const long long n = (long long)(rc.i1 - rc.i0) * (rc.j1 - rc.j0) * cells.n +
+                        (long long)(rn.i1 - rn.i0) * (rn.j1 - rn.j0) * nodes.n;
+    unsigned nb = nblk(n > 0 ? n : 1, 256);
+    if (nb > 148u * 16u) nb = 148u * 16u;
+    { k_rect_xfer<<<nb, 256, 0, s>>>(d, cells, nodes, rc, rn, buf, to_buf); ++g_launches; }
+}
+void launch_global_xfer(const Dev& d, double* gx, int W, Rng r, double* px, double* py, int vec, int to_block,
+                        cudaStream_t s) {
+    const long long n = (long long)(r.i1 - r.i0) * (r.j1 - r.j0);
+    unsigned nb = nblk(n > 0 ? n : 1, 256);
+    if (nb > 148u * 16u) nb = 148u * 16u;
+    { k_global_xfer<<<nb, 256, 0, s>>>(d, gx, W, r, px, py, vec, to_block); ++g_launches; }
 }
 
 void launch_commit(Ctl* c, int advance, cudaStream_t s) { k_commit<<<1, 1, 0, s>>>(c, advance); }

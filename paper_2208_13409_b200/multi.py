@@ -1,0 +1,334 @@
+"""2D block decomposition of the step over several GPUs.
+
+Each block context (C-ABI ``h2d_create_block``) owns a rectangle of the global
+mesh plus an 8-cell halo and computes the whole Lagrange + DirectCF step on its
+window with redundant halo work.  Per step the blocks then need exactly:
+
+* one all-reduce of three scalars: the next step's wave-speed maximum (MAX of
+  the fp64 bit pattern), the first cfl_dt error key and the first step error
+  key (MIN; keys order errors like the reference's program order), and
+* one halo exchange of the State with the (up to) 8 neighbours, corners
+  included, which the unsplit 9-point remap needs.
+
+``Transport`` abstracts where blocks live: ``LocalTransport`` keeps several
+blocks in one process (one GPU, device-to-device copies — used by the
+bit-equality tests), ``DistTransport`` is one block per rank over
+``torch.distributed`` (NCCL on GPUs, gloo in the CPU tests of the exchange
+plumbing).  Owned values are bit-identical to the single-domain run.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import errors
+from .abi import Config, ErrorRec, HostState, Library, RunArgs, _ptr
+
+HALO = 8
+NO_ERR = (1 << 64) - 1
+DIRS = [(dx, dy) for dy in (-1, 0, 1) for dx in (-1, 0, 1) if (dx, dy) != (0, 0)]
+
+
+class Block(C.Structure):
+    _fields_ = [("oi", C.c_int), ("oj", C.c_int), ("bnx", C.c_int), ("bny", C.c_int), ("halo", C.c_int)]
+
+
+def split(n: int, parts: int) -> List[Tuple[int, int]]:
+    """Near-equal 1D split: (origin, size) per part."""
+    base, rem = divmod(n, parts)
+    out, o = [], 0
+    for p in range(parts):
+        sz = base + (1 if p < rem else 0)
+        out.append((o, sz))
+        o += sz
+    return out
+
+
+def grid_shape(nranks: int, nx: int, ny: int) -> Tuple[int, int]:
+    """px x py = nranks, splitting the longer axis first (1x1, 2x1, 2x2, 4x2)."""
+    px, py = 1, 1
+    n = nranks
+    while n > 1:
+        if nx / px >= ny / py:
+            px *= 2
+        else:
+            py *= 2
+        n //= 2
+    assert px * py == nranks, "power-of-two rank counts"
+    return px, py
+
+
+@dataclass
+class BlockSpec:
+    rank: int
+    bx: int
+    by: int
+    oi: int
+    oj: int
+    bnx: int
+    bny: int
+
+    def neighbour(self, px: int, py: int, dx: int, dy: int) -> Optional[int]:
+        x, y = self.bx + dx, self.by + dy
+        if 0 <= x < px and 0 <= y < py:
+            return y * px + x
+        return None
+
+
+def decompose(nx: int, ny: int, px: int, py: int) -> List[BlockSpec]:
+    xs, ys = split(nx, px), split(ny, py)
+    return [BlockSpec(by * px + bx, bx, by, xs[bx][0], ys[by][0], xs[bx][1], ys[by][1])
+            for by in range(py) for bx in range(px)]
+
+
+_SIGS = {
+    "create_block": ([C.POINTER(Config), C.POINTER(Block), C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "block_upload": ([C.c_void_p, C.c_void_p], C.c_int),
+    "block_download": ([C.c_void_p, C.c_void_p], C.c_int),
+    "block_begin": ([C.c_void_p, C.c_int, C.c_double, C.c_double], C.c_int),
+    "block_step": ([C.c_void_p], C.c_int),
+    "block_scalars": ([C.c_void_p, C.POINTER(C.c_ulonglong)], C.c_int),
+    "block_set": ([C.c_void_p, C.POINTER(C.c_ulonglong)], C.c_int),
+    "block_rollback": ([C.c_void_p], C.c_int),
+    "halo_bytes": ([C.c_void_p, C.c_int, C.c_int, C.c_int], C.c_longlong),
+    "halo_pack": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p], C.c_int),
+    "halo_unpack": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p], C.c_int),
+    "block_result": ([C.c_void_p, C.POINTER(RunArgs)], C.c_int),
+}
+
+
+def bind(lib: Library):
+    for name, (args, res) in _SIGS.items():
+        f = getattr(lib.dll, lib.prefix + name)
+        f.argtypes, f.restype = args, res
+        lib.fn[name] = f
+    return lib
+
+
+class BlockSolver:
+    """One block context of the decomposition (product library only)."""
+
+    def __init__(self, lib: Library, cfg: Config, spec: BlockSpec, device: int = 0, halo: int = HALO):
+        self.lib, self.cfg, self.spec = bind(lib), cfg, spec
+        self._h = C.c_void_p()
+        b = Block(spec.oi, spec.oj, spec.bnx, spec.bny, halo)
+        rc = lib.fn["create_block"](C.byref(cfg), C.byref(b), device, C.byref(self._h))
+        if rc:
+            raise errors.from_code(rc, f"h2d_create_block failed ({rc})")
+
+    def close(self):
+        if self._h:
+            self.lib.fn["destroy"](self._h)
+            self._h = C.c_void_p()
+
+    __del__ = close
+
+    def _check(self, rc):
+        if rc:
+            rec = ErrorRec()
+            self.lib.fn["last_error"](self._h, C.byref(rec))
+            raise errors.from_record(rec)
+
+    def upload(self, g: HostState):
+        self._check(self.lib.fn["block_upload"](self._h, C.byref(g.view())))
+
+    def download_into(self, g: HostState):
+        v = g.view()
+        self._check(self.lib.fn["block_download"](self._h, C.byref(v)))
+        g.step, g.time = v.step, v.time
+
+    def begin(self, max_steps: int, t_end: float, cfl: float):
+        self._check(self.lib.fn["block_begin"](self._h, max_steps, t_end, cfl))
+
+    def step(self):
+        self._check(self.lib.fn["block_step"](self._h))
+
+    def scalars(self) -> List[int]:
+        out = (C.c_ulonglong * 4)()
+        self._check(self.lib.fn["block_scalars"](self._h, out))
+        return list(out)
+
+    def set_scalars(self, wmax: int, next_err: int, err: int):
+        self._check(self.lib.fn["block_set"](self._h, (C.c_ulonglong * 3)(wmax, next_err, err)))
+
+    def rollback(self):
+        self._check(self.lib.fn["block_rollback"](self._h))
+
+    def halo_bytes(self, dx, dy, pack) -> int:
+        return int(self.lib.fn["halo_bytes"](self._h, dx, dy, int(pack)))
+
+    def pack(self, dx, dy, ptr):
+        self._check(self.lib.fn["halo_pack"](self._h, dx, dy, C.c_void_p(ptr)))
+
+    def unpack(self, dx, dy, ptr):
+        self._check(self.lib.fn["halo_unpack"](self._h, dx, dy, C.c_void_p(ptr)))
+
+    def result(self, cap: int):
+        a = RunArgs()
+        dts = np.zeros(max(cap, 1))
+        a.dt_log, a.dt_log_cap = _ptr(dts), len(dts)
+        rc = self.lib.fn["block_result"](self._h, C.byref(a))
+        err = None
+        if rc:
+            rec = ErrorRec()
+            self.lib.fn["last_error"](self._h, C.byref(rec))
+            err = errors.from_record(rec)
+        return a, dts[:a.steps_done], err
+
+
+def combine(scal: Sequence[Sequence[int]]) -> Tuple[int, int, int]:
+    """MAX of the wave-speed bits, MIN of the error keys (unsigned)."""
+    return max(s[0] for s in scal), min(s[1] for s in scal), min(s[2] for s in scal)
+
+
+def phase_of(key: int) -> int:
+    return key >> 58
+
+
+PH_NAN_CELL = 18
+
+
+class LocalTransport:
+    """All blocks in this process on one device; exchange by device copies
+    through a scratch tensor (the same pack / unpack calls a rank makes)."""
+
+    def __init__(self, blocks: Sequence[BlockSolver], px: int, py: int):
+        import torch
+        self.blocks, self.px, self.py = list(blocks), px, py
+        nbytes = max(b.halo_bytes(dx, dy, 1) for b in blocks for dx, dy in DIRS)
+        self.buf = torch.empty(max(nbytes // 8, 1), dtype=torch.float64, device="cuda")
+
+    def allreduce(self, scal: List[List[int]]):
+        return combine(scal)
+
+    def exchange(self):
+        for b in self.blocks:
+            for dx, dy in DIRS:
+                n = b.spec.neighbour(self.px, self.py, dx, dy)
+                if n is None:
+                    continue
+                src = self.blocks[n]
+                assert src.halo_bytes(-dx, -dy, 1) == b.halo_bytes(dx, dy, 0)
+                src.pack(-dx, -dy, self.buf.data_ptr())
+                b.unpack(dx, dy, self.buf.data_ptr())
+
+
+class DistTransport:
+    """One block per rank over torch.distributed (NCCL on GPUs)."""
+
+    def __init__(self, block: BlockSolver, px: int, py: int, device):
+        import torch
+        import torch.distributed as dist
+        self.block, self.px, self.py, self.dist, self.torch, self.device = block, px, py, dist, torch, device
+        self.send, self.recv = {}, {}
+        for dx, dy in DIRS:
+            if block.spec.neighbour(px, py, dx, dy) is None:
+                continue
+            self.send[(dx, dy)] = torch.empty(block.halo_bytes(dx, dy, 1) // 8, dtype=torch.float64, device=device)
+            self.recv[(dx, dy)] = torch.empty(block.halo_bytes(dx, dy, 0) // 8, dtype=torch.float64, device=device)
+
+    def allreduce(self, scal: List[List[int]]):
+        torch, dist = self.torch, self.dist
+        s = scal[0]
+        flip = 1 << 63  # unsigned order -> signed order
+        t = torch.tensor([s[0] - flip, s[1] - flip, s[2] - flip], dtype=torch.int64, device=self.device)
+        hi = t[:1].clone()
+        lo = t[1:].clone()
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        return int(hi[0]) + flip, int(lo[0]) + flip, int(lo[1]) + flip
+
+    def exchange(self):
+        dist = self.dist
+        ops = []
+        for (dx, dy), buf in self.send.items():
+            self.block.pack(dx, dy, buf.data_ptr())
+        if self.device.type == "cuda":
+            self.torch.cuda.synchronize(self.device)
+        for (dx, dy), buf in self.send.items():
+            peer = self.block.spec.neighbour(self.px, self.py, dx, dy)
+            ops.append(dist.P2POp(dist.isend, buf, peer))
+            ops.append(dist.P2POp(dist.irecv, self.recv[(dx, dy)], peer))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        if self.device.type == "cuda":
+            self.torch.cuda.synchronize(self.device)
+        for (dx, dy), buf in self.recv.items():
+            self.block.unpack(dx, dy, buf.data_ptr())
+
+
+def run_blocks(blocks: Sequence[BlockSolver], transport, max_steps: int, t_end: float, cfl: float,
+               on_step=None) -> int:
+    """The run loop (harness.cpp:390-412) over a decomposition: per step one
+    graph launch per block, one 3-scalar all-reduce and one halo exchange.
+    Returns the number of steps taken; raises the first error, with every
+    block left at the last step all blocks completed."""
+    for b in blocks:
+        b.begin(max_steps, t_end, cfl)
+    g = transport.allreduce([b.scalars() for b in blocks])
+    for b in blocks:
+        b.set_scalars(g[0], g[1], NO_ERR)
+    steps = 0
+    while True:
+        for b in blocks:
+            b.step()
+        scal = [b.scalars() for b in blocks]
+        wmax, nerr, err = transport.allreduce(scal)
+        if err != NO_ERR:
+            # blocks whose own step committed roll back when the first error
+            # precedes the commit (nan_scan errors come after it)
+            if phase_of(err) < PH_NAN_CELL:
+                for b, s in zip(blocks, scal):
+                    if s[2] == NO_ERR:
+                        b.rollback()
+            for b in blocks:
+                b.set_scalars(wmax, nerr, err)
+            break
+        if all(s[3] for s in scal):
+            break
+        steps += 1
+        transport.exchange()
+        for b in blocks:
+            b.set_scalars(wmax, nerr, NO_ERR)
+        if on_step:
+            on_step(steps)
+    return steps
+
+
+def own_ranges(spec: BlockSpec, nx: int, ny: int, g: int = 2):
+    """Owned cell / node ranges (global, half-open) — capi.cu block_ranges."""
+    li, ri = spec.oi > 0, spec.oi + spec.bnx < nx
+    bi, ti = spec.oj > 0, spec.oj + spec.bny < ny
+    oc = (spec.oi if li else -g, spec.oi + spec.bnx if ri else nx + g,
+          spec.oj if bi else -g, spec.oj + spec.bny if ti else ny + g)
+    on = (spec.oi if li else -g, spec.oi + spec.bnx if ri else nx + g + 1,
+          spec.oj if bi else -g, spec.oj + spec.bny if ti else ny + g + 1)
+    return oc, on
+
+
+def halo_rects(spec: BlockSpec, nx: int, ny: int, dx: int, dy: int, pack: bool, h: int = HALO):
+    """Cell and node rectangles of the halo exchange with neighbour (dx, dy)
+    (mirror of capi.cu halo_rects): pack = my owned data it needs, unpack =
+    my halo it fills."""
+    oc, on = own_ranges(spec, nx, ny)
+
+    def axis(dd, o, n, c0, c1, n0, n1):
+        if dd == 0:
+            return (c0, c1), (n0, n1)
+        if pack:
+            return ((o + n - h, o + n), (o + n - h, o + n)) if dd > 0 else ((o, o + h), (o, o + h + 1))
+        return ((o - h, o), (o - h, o)) if dd < 0 else ((o + n, o + n + h), (o + n, o + n + h + 1))
+
+    (cx, nxr) = axis(dx, spec.oi, spec.bnx, oc[0], oc[1], on[0], on[1])
+    (cy, nyr) = axis(dy, spec.oj, spec.bny, oc[2], oc[3], on[2], on[3])
+    return (cx[0], cx[1], cy[0], cy[1]), (nxr[0], nxr[1], nyr[0], nyr[1])
+
+
+def state_planes(nmat: int) -> Tuple[int, int]:
+    """(cell planes, node planes) exchanged per step: m, e, k per material,
+    vol, m_mix, e_mix, rho_mix, p_mix, normal x/y | u x/y."""
+    return 3 * nmat + 7, 2
