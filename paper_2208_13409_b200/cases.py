@@ -218,6 +218,17 @@ def sedov(n: int = 1024) -> Case:
                 0.5, 500)
 
 
+def sedov_weak(px: int, py: int, n: int = 1024) -> Case:
+    """Config 2 grown for weak scaling over px x py GPUs: the same 1/n cell
+    size and corner blast, on a (px*n) x (py*n) mesh over [0,px] x [0,py]."""
+    gamma = 1.4
+    dx = dy = 1.0 / n
+    p0 = (gamma - 1.0) * 1.0 / (4.0 * dx * dy)
+    return Case(f"sedov_{px * n}x{py * n}", _mesh_cfg(px * n, py * n, float(px), float(py), [(EOS_PERFECT, gamma, 0.0)]),
+                [Region(ALL, rho=1.0, p=1e-6), Region(RECTANGLE, rect=(0.0, 0.0, 2 * dx, 2 * dy), rho=1.0, p=p0)],
+                0.5, 500)
+
+
 def triple_point(nx: int = 2048, ny: int = 1024) -> Case:
     """Config 3: two-material three-state interface problem on [0,7]x[0,3]
     (A: gamma 1.5 = material 0, B: gamma 1.4 = material 1).  Region order is

@@ -894,20 +894,23 @@ int ensure_xbuf(h2d_ctx* c, size_t bytes) {
     return 0;
 }
 
-// global-layout host planes <-> this block's planes over rectangle r
+// global-layout host planes <-> this block's planes over rectangle r: only
+// the rectangle's rows are copied (strided 2D copy into a compact buffer)
 int global_rect(h2d_ctx* c, double* host, int vec, bool node, Rng r, double* px, double* py, bool upload) {
     if (!host || r.i1 <= r.i0 || r.j1 <= r.j0) return 0;
-    const int W = c->nx + (node ? 1 : 0) + 2 * G, Hh = c->ny + (node ? 1 : 0) + 2 * G;
-    const size_t bytes = (size_t)W * Hh * (vec ? 2 : 1) * sizeof(double);
+    const int W = c->nx + (node ? 1 : 0) + 2 * G;
+    const int w = r.i1 - r.i0, h = r.j1 - r.j0, e = vec ? 2 : 1;
+    const size_t bytes = (size_t)w * h * e * sizeof(double);
     if (int rc = ensure_xbuf(c, bytes)) return rc;
     const Dev d = make_dev(c, c->cur, 1);
+    double* hstart = host + ((size_t)(r.j0 + G) * W + (r.i0 + G)) * e;
+    const size_t hpitch = (size_t)W * e * sizeof(double), row = (size_t)w * e * sizeof(double);
     if (upload) {
-        CK(cudaMemcpyAsync(c->xbuf, host, bytes, cudaMemcpyHostToDevice, c->st));
-        launch_global_xfer(d, c->xbuf, W, r, px, py, vec, 1, c->st);
+        CK(cudaMemcpy2DAsync(c->xbuf, row, hstart, hpitch, row, (size_t)h, cudaMemcpyHostToDevice, c->st));
+        launch_global_xfer(d, c->xbuf, r, px, py, vec, 1, c->st);
     } else {
-        CK(cudaMemcpyAsync(c->xbuf, host, bytes, cudaMemcpyHostToDevice, c->st));  // keep other blocks' parts
-        launch_global_xfer(d, c->xbuf, W, r, px, py, vec, 0, c->st);
-        CK(cudaMemcpyAsync(host, c->xbuf, bytes, cudaMemcpyDeviceToHost, c->st));
+        launch_global_xfer(d, c->xbuf, r, px, py, vec, 0, c->st);
+        CK(cudaMemcpy2DAsync(hstart, hpitch, c->xbuf, row, row, (size_t)h, cudaMemcpyDeviceToHost, c->st));
     }
     CK(cudaStreamSynchronize(c->st));
     return 0;

@@ -1657,34 +1657,34 @@ __global__ void k_rect_xfer(Dev d, FieldList cells, FieldList nodes, Rng rc, Rng
     }
 }
 
-// Rectangle copy between a global-layout host mirror in a device buffer
-// (reference Field layout of the whole mesh: pitch W, ghost 2) and this
-// block's planes; vec != 0: interleaved Vec2 source split into x / y planes.
-__global__ void k_global_xfer(Dev d, double* gx, int W, Rng r, double* px, double* py, int vec, int to_block) {
+// Rectangle r of this block's planes <-> a compact buffer (row pitch r width;
+// vec != 0: interleaved Vec2 split into x / y planes) — window uploads and
+// owned-region downloads in the global reference layout.
+__global__ void k_global_xfer(Dev d, double* buf, Rng r, double* px, double* py, int vec, int to_block) {
     const int w = r.i1 - r.i0, h = r.j1 - r.j0;
     const long long n = (long long)w * h;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
         const int i = r.i0 + (int)(t % w), j = r.j0 + (int)(t / w);
-        const long long gi = (long long)(j + G) * W + (i + G);
         const int li = ix(d, i, j);
         if (to_block) {
             if (vec) {
-                px[li] = gx[2 * gi];
-                py[li] = gx[2 * gi + 1];
+                px[li] = buf[2 * t];
+                py[li] = buf[2 * t + 1];
             } else {
-                px[li] = gx[gi];
+                px[li] = buf[t];
             }
         } else {
             if (vec) {
-                gx[2 * gi] = px[li];
-                gx[2 * gi + 1] = py[li];
+                buf[2 * t] = px[li];
+                buf[2 * t + 1] = py[li];
             } else {
-                gx[gi] = px[li];
+                buf[t] = px[li];
             }
         }
     }
 }
+
 
 // The end of the remap on the new State, one thread per position of the
 // ghosted node range: sync_derived over every cell (state.cpp:120-143, from
@@ -1993,12 +1993,12 @@ void launch_rect_xfer(const Dev& d, const FieldList& cells, const FieldList& nod
     if (nb > 148u * 16u) nb = 148u * 16u;
     { k_rect_xfer<<<nb, 256, 0, s>>>(d, cells, nodes, rc, rn, buf, to_buf); ++g_launches; }
 }
-void launch_global_xfer(const Dev& d, double* gx, int W, Rng r, double* px, double* py, int vec, int to_block,
+void launch_global_xfer(const Dev& d, double* buf, Rng r, double* px, double* py, int vec, int to_block,
                         cudaStream_t s) {
     const long long n = (long long)(r.i1 - r.i0) * (r.j1 - r.j0);
     unsigned nb = nblk(n > 0 ? n : 1, 256);
     if (nb > 148u * 16u) nb = 148u * 16u;
-    { k_global_xfer<<<nb, 256, 0, s>>>(d, gx, W, r, px, py, vec, to_block); ++g_launches; }
+    { k_global_xfer<<<nb, 256, 0, s>>>(d, buf, r, px, py, vec, to_block); ++g_launches; }
 }
 
 void launch_commit(Ctl* c, int advance, cudaStream_t s) { k_commit<<<1, 1, 0, s>>>(c, advance); }

@@ -33,7 +33,7 @@ void launch_normals_api(const Dev& d, cudaStream_t s);
 void launch_rollback(Ctl* c, cudaStream_t s);
 void launch_rect_xfer(const Dev& d, const FieldList& cells, const FieldList& nodes, Rng rc, Rng rn, double* buf,
                       int to_buf, cudaStream_t s);
-void launch_global_xfer(const Dev& d, double* gx, int W, Rng r, double* px, double* py, int vec, int to_block,
+void launch_global_xfer(const Dev& d, double* buf, Rng r, double* px, double* py, int vec, int to_block,
                         cudaStream_t s);
 void launch_deinterleave(const double* src, double* x, double* y, int W, int H, int P, cudaStream_t s);
 void launch_interleave(double* dst, const double* x, const double* y, int W, int H, int P, cudaStream_t s);
