@@ -11,6 +11,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -449,6 +450,15 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     d.y0 = m.y0;
     d.cv = m.dx * m.dy;
     d.L = std::sqrt(m.dx * m.dy);  // Mesh::char_length, mesh.hpp:39
+    auto pow2_recip = [](double v) {  // 1/v when v is an exact power of two with a normal reciprocal
+        int e = 0;
+        const double mnt = std::frexp(v, &e);
+        const double r = 1.0 / v;
+        return (mnt == 0.5 && std::isnormal(r) && std::isnormal(v)) ? r : 0.0;
+    };
+    d.rdx = pow2_recip(m.dx);
+    d.rdy = pow2_recip(m.dy);
+    d.rcv = pow2_recip(d.cv);
     for (int a = 0; a < nm; ++a) {
         d.stiff[a] = cfg->eos[a].kind == H2D_EOS_STIFFENED;
         d.gamma[a] = cfg->eos[a].gamma;
@@ -475,6 +485,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
         d.slme[a] = plane(c);
     }
     d.mcell = plane(c);
+    d.unrm = plane(c);
     d.dmx = plane(c);
     d.dmy = plane(c);
     d.dmc = plane(c);

@@ -110,6 +110,9 @@ struct Dev {
     Rng own_c, own_n;  // cells / nodes this block answers for (errors, counters, nan, cfl)
     Rng win_c, win_n;  // cells / nodes present in storage
     double dx, dy, x0, y0, cv, L;
+    // exact reciprocals of dx, dy, dx*dy when they are powers of two (0
+    // otherwise): x / dx == x * (1/dx) bit for bit in that case
+    double rdx, rdy, rcv;
     int stiff[2];
     double gamma[2], pi[2];
     double a1, a2;
@@ -123,7 +126,7 @@ struct Dev {
     // LagrangeResult (lagrange.hpp:38-45)
     double *q, *pmh, *ph[2], *uhx, *uhy, *ulx, *uly, *el[2], *vol_lag;
     // remap scratch (the tile kernel keeps its geometry in shared memory)
-    double *me[2], *mcell;
+    double *me[2], *mcell, *unrm;
     double *dmx, *dmy, *dmc;
     double *dfx_x, *dfx_y, *dfy_x, *dfy_y;  // dual-face momentum contributions
     double *dc_x[2], *dc_y[2];              // dual-corner contributions per pair
@@ -139,6 +142,13 @@ struct Dev {
 H2D_DEV int ix(const Dev& d, int i, int j) { return j * d.P + i + d.off; }
 H2D_DEV bool in(const Rng& r, int i, int j) { return i >= r.i0 && i < r.i1 && j >= r.j0 && j < r.j1; }
 
+H2D_DEV double div_dx(const Dev& d, double x, double k) {  // x / (k * dx), k a power of two
+    return d.rdx != 0.0 ? x * (d.rdx * (1.0 / k)) : x / (k * d.dx);
+}
+H2D_DEV double div_dy(const Dev& d, double x, double k) {
+    return d.rdy != 0.0 ? x * (d.rdy * (1.0 / k)) : x / (k * d.dy);
+}
+H2D_DEV double div_cv(const Dev& d, double x) { return d.rcv != 0.0 ? x * d.rcv : x / d.cv; }
 H2D_DEV double rmax(double a, double b) { return (a < b) ? b : a; }  // std::max
 H2D_DEV double rmin(double a, double b) { return (b < a) ? b : a; }  // std::min
 

@@ -281,7 +281,7 @@ __global__ void k_sync(Dev d, int next, int respect_halt) {
     double* ov = next ? d.nvol : d.vol;
     om[c] = m;
     oe[c] = m > 0.0 ? me / m : 0.0;
-    orho[c] = m / cv;
+    orho[c] = div_cv(d, m);
     op[c] = p;
     ov[c] = cv;
 }
@@ -334,7 +334,7 @@ __global__ void k_lag_cells(Dev d) {
     const double ux_r = 0.5 * (u10x + u11x);
     const double uy_b = 0.5 * (u00y + u10y);
     const double uy_t = 0.5 * (u01y + u11y);
-    const double div = (ux_r - ux_l) / d.dx + (uy_t - uy_b) / d.dy;
+    const double div = div_dx(d, ux_r - ux_l, 1.0) + div_dy(d, uy_t - uy_b, 1.0);
     double q = 0.0;
     if (!(div >= 0.0)) {
         double cs = 0.0;
@@ -404,11 +404,11 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
         if (in(rn, i, j)) {
             const int a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
             const double mp = 0.25 * (d.m_mix[a] + d.m_mix[b] + d.m_mix[c] + d.m_mix[e]);
-            const double rho_p = mp / d.cv;
+            const double rho_p = div_cv(d, mp);
             const double pq_a = d.pmh[a] + d.q[a], pq_b = d.pmh[b] + d.q[b];
             const double pq_c = d.pmh[c] + d.q[c], pq_e = d.pmh[e] + d.q[e];
-            const double gx = (pq_b + pq_e - pq_a - pq_c) / (2.0 * d.dx);  // pq(i,j-1)+pq(i,j)-pq(i-1,j-1)-pq(i-1,j)
-            const double gy = (pq_c + pq_e - pq_a - pq_b) / (2.0 * d.dy);  // pq(i-1,j)+pq(i,j)-pq(i-1,j-1)-pq(i,j-1)
+            const double gx = div_dx(d, pq_b + pq_e - pq_a - pq_c, 2.0);  // pq(i,j-1)+pq(i,j)-pq(i-1,j-1)-pq(i-1,j)
+            const double gy = div_dy(d, pq_c + pq_e - pq_a - pq_b, 2.0);  // pq(i-1,j)+pq(i,j)-pq(i-1,j-1)-pq(i,j-1)
             const double sc = 0.5 * dt / rho_p;
             const double ux = d.ux[e], uy = d.uy[e];
             hx = ux - gx * sc;
@@ -1096,8 +1096,8 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     double k[2] = {1.0, 0.0};
     uint8_t sl = 0;
     if (NM == 2) {
-        double k0 = va[0] / cv;
-        const double k1 = va[1] / cv;
+        double k0 = div_cv(d, va[0]);
+        const double k1 = div_cv(d, va[1]);
         double viol = 0.0;
         const double cand[5] = {-k0, k0 - 1.0, -k1, k1 - 1.0, fabs(k0 + k1 - 1.0)};
 #pragma unroll
@@ -1441,14 +1441,16 @@ __global__ void k_node_update(Dev d) {
             if (jp1 < 0) jp1 += ny;
             if (jp2 >= ny) jp2 -= ny;
         }
+        push(ip, jp1, 0, -1.0);
         if (si <= iuniq && sj <= juniq) {
             push(si, sj, 0, 1.0);
             push(si, sj, 1, 1.0);
         }
-        push(ip, jp1, 0, -1.0);
         push(ip, jp2, 1, -1.0);
-        // insertion sort by loop time (n <= 4)
-        for (int a = 1; a < nc; ++a)
+        // with walls the pushes above are already in loop order; periodic
+        // wrap can reorder them: insertion sort by loop time (n <= 4)
+        if (d.per_x || d.per_y)
+            for (int a = 1; a < nc; ++a)
             for (int b = a; b > 0 && tk[b - 1] > tk[b]; --b) {
                 long long t0 = tk[b];
                 tk[b] = tk[b - 1];
@@ -1484,6 +1486,7 @@ __global__ void k_node_update(Dev d) {
     if (!d.per_y && (j == 0 || j == ny)) uy = 0.0;
     d.nux[o] = ux;
     d.nuy[o] = uy;
+    d.unrm[o] = sqrt(ux * ux + uy * uy);  // |u| for the next cfl_dt (harness.cpp:308)
 }
 
 // refresh_normals_impl + youngs_normal (remap.cpp:102-114, vof.cpp:10-22)
@@ -1506,8 +1509,8 @@ __global__ void k_normals(Dev d, int api) {
     auto K = [&](int ii, int jj) { return k1[ix(d, ii, jj)]; };
     auto col = [&](int ii) { return K(ii, j - 1) + 2.0 * K(ii, j) + K(ii, j + 1); };
     auto row = [&](int jj) { return K(i - 1, jj) + 2.0 * K(i, jj) + K(i + 1, jj); };
-    const double gx = (col(i + 1) - col(i - 1)) / (8.0 * d.dx);
-    const double gy = (row(j + 1) - row(j - 1)) / (8.0 * d.dy);
+    const double gx = div_dx(d, col(i + 1) - col(i - 1), 8.0);
+    const double gy = div_dy(d, row(j + 1) - row(j - 1), 8.0);
     const double g = sqrt(gx * gx + gy * gy);
     if (g < 1e-300) return;  // IsolatedMixedCellError caught: keep the previous normal
     nx_[c] = gx / g;
@@ -1726,7 +1729,7 @@ __global__ void __launch_bounds__(256) k_post(Dev d, int run_loop) {
         const double emix = m > 0.0 ? me / m : 0.0;
         d.nm_mix[c] = m;
         d.ne_mix[c] = emix;
-        d.nrho_mix[c] = m / cv;
+        d.nrho_mix[c] = div_cv(d, m);
         d.np_mix[c] = p;
         d.nvol[c] = cv;
         const bool interior = i >= 0 && j >= 0 && i < nx && j < ny;
@@ -1737,8 +1740,8 @@ __global__ void __launch_bounds__(256) k_post(Dev d, int run_loop) {
                     auto K = [&](int ii, int jj) { return d.nk[1][ix(d, ii, jj)]; };
                     auto col = [&](int ii) { return K(ii, j - 1) + 2.0 * K(ii, j) + K(ii, j + 1); };
                     auto row = [&](int jj) { return K(i - 1, jj) + 2.0 * K(i, jj) + K(i + 1, jj); };
-                    const double gx = (col(i + 1) - col(i - 1)) / (8.0 * d.dx);
-                    const double gy = (row(j + 1) - row(j - 1)) / (8.0 * d.dy);
+                    const double gx = div_dx(d, col(i + 1) - col(i - 1), 8.0);
+                    const double gy = div_dy(d, row(j + 1) - row(j - 1), 8.0);
                     const double g = sqrt(gx * gx + gy * gy);
                     if (!(g < 1e-300)) {  // an isolated mixed cell keeps its normal
                         nrx = gx / g;
@@ -1765,11 +1768,7 @@ __global__ void __launch_bounds__(256) k_post(Dev d, int run_loop) {
 #pragma unroll
                 for (int dj = 0; dj <= 1; ++dj)
 #pragma unroll
-                    for (int di = 0; di <= 1; ++di) {
-                        const int n = ix(d, i + di, j + dj);
-                        const double ux = d.nux[n], uy = d.nuy[n];
-                        umax = rmax(umax, sqrt(ux * ux + uy * uy));
-                    }
+                    for (int di = 0; di <= 1; ++di) umax = rmax(umax, d.unrm[ix(d, i + di, j + dj)]);
                 const double w = cs + umax;
                 if (w > 0.0) wb = (unsigned long long)__double_as_longlong(w);
             }
