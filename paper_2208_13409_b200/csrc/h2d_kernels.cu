@@ -871,7 +871,7 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     for (int t = tid; t < RNN; t += RTX * RTY) {
         const int i = T.ci0 + t % RNW, j = T.cj0 + t / RNW;
         double hx = 0.0, hy = 0.0;
-        if (i >= -G && j >= -G && i <= nx + G && j <= ny + G) {
+        if (in(d.win_n, i, j)) {  // = [-2, n+2] on a whole mesh
             const int n = ix(d, i, j);
             hx = d.uhx[n];
             hy = d.uhy[n];
@@ -881,7 +881,7 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     }
     for (int t = tid; t < RNC; t += RTX * RTY) {
         const int i = T.ci0 + t % RCW, j = T.cj0 + t / RCW;
-        if (i < -G || j < -G || i >= nx + G || j >= ny + G) continue;
+        if (!in(d.win_c, i, j)) continue;  // = [-2, n+2) on a whole mesh
         const int c = ix(d, i, j);
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
@@ -902,7 +902,7 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         const int i = T.ci0 + t % RNW, j = T.cj0 + t / RNW;
         double cfv = 0.0, fdx = 0.0, fdy = 0.0, fxv = 0.0, fyv = 0.0;
         int8_t sx = 0, sy = 0;
-        if (i >= -G && j >= -G && i <= nx + G && j <= ny + G) {
+        if (in(d.win_n, i, j)) {
             const double hx = T.hx[t], hy = T.hy[t];
             const double ddx = hx * dt, ddy = hy * dt;
             cfv = fabs(ddx * ddy);
@@ -914,14 +914,14 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
             }
             if (cfv > kCflFrac * cv && own_node(d, i, j)) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
             // faces on the region's last node row / column feed no region cell
-            if (j < ny + G && j < T.cj0 + RNH - 1) {
+            if (j < ny + G && j < T.cj0 + RNH - 1 && j + 1 < d.win_n.j1) {
                 const double ux1 = T.hx[t + RNW], uy1 = T.hy[t + RNW];
                 fdx = 0.5 * (hx + ux1) * dt;
                 double wl, wh;
                 face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * hx, dt * hy, dt * ux1, dt * uy1, fxv, wl, wh);
                 if (fabs(fxv) > kCflFrac * cv && own_xface(d, i, j)) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
             }
-            if (i < nx + G && i < T.ci0 + RNW - 1) {
+            if (i < nx + G && i < T.ci0 + RNW - 1 && i + 1 < d.win_n.i1) {
                 const double ux1 = T.hx[t + 1], uy1 = T.hy[t + 1];
                 fdy = 0.5 * (hy + uy1) * dt;
                 double wl, wh;
@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     // interfaces (remap.cpp:769-824)
     for (int t = tid; t < RNC; t += RTX * RTY) {
         const int i = T.ci0 + t % RCW, j = T.cj0 + t / RCW;
-        if (i < -G || j < -G || i >= nx + G || j >= ny + G) continue;
+        if (!in(d.win_c, i, j) || i + 1 >= d.win_n.i1 || j + 1 >= d.win_n.j1) continue;
         const int q00 = T.n(i, j), q10 = q00 + 1, q01 = q00 + RNW, q11 = q01 + 1;
         auto cterm = [&](int q, int ni, int nj) -> double {  // remap.cpp:775-785
             const double dv = T.cf[q];
@@ -1242,22 +1242,16 @@ __device__ __forceinline__ double dual_face_value(const Dev& d, const double* u,
 // dual_face_pass, remap.cpp:408-442: one thread per dual face. AX = 1: X
 // (ia = i node, ic = j), AX = 0: Y (ia = j, ic = i); stored at (i, j).
 template <int AX>
-__device__ __forceinline__ void dual_face_item(const Dev& d, int i, int j) {
+__device__ __forceinline__ bool dual_face_val(const Dev& d, int i, int j, double& mx, double& my) {
     const int ia = AX ? i : j, ic = AX ? j : i;
     const int per_a = AX ? d.per_x : d.per_y;
     const int s = ix(d, i, j);
-    double* ox = AX ? d.dfx_x : d.dfy_x;
-    double* oy = AX ? d.dfx_y : d.dfy_y;
-    if (ia < (per_a ? 0 : 1)) {
-        ox[s] = 0.0;
-        oy[s] = 0.0;
-        d.dflag[AX ? 0 : 1][s] = 0;
-        return;
-    }
+    mx = 0.0;
+    my = 0.0;
+    if (ia < (per_a ? 0 : 1)) return false;
     const double* dmf = AX ? d.dmx : d.dmy;
     auto F = [&](int a, int c) { return dmf[AX ? ix(d, a, c) : ix(d, c, a)]; };
     const double dm = 0.25 * ((F(ia - 1, ic - 1) + F(ia - 1, ic)) + (F(ia, ic - 1) + F(ia, ic)));
-    double mx = 0.0, my = 0.0;
     if (dm != 0.0) {
         const double dt = step_dt(d.ctl);
         const int ia_d = dm > 0.0 ? ia - 1 : ia;
@@ -1272,22 +1266,28 @@ __device__ __forceinline__ void dual_face_item(const Dev& d, int i, int j) {
         mx = ufx * dm;
         my = ufy * dm;
     }
-    ox[s] = mx;
-    oy[s] = my;
-    d.dflag[AX ? 0 : 1][s] = dm != 0.0;  // a zero dual mass flux is skipped (remap.cpp:423)
+    return dm != 0.0;  // a zero dual mass flux is skipped (remap.cpp:423)
+}
+template <int AX>
+__device__ __forceinline__ void dual_face_item(const Dev& d, int i, int j) {
+    double mx, my;
+    const bool on = dual_face_val<AX>(d, i, j, mx, my);
+    const int s = ix(d, i, j);
+    (AX ? d.dfx_x : d.dfy_x)[s] = mx;
+    (AX ? d.dfx_y : d.dfy_y)[s] = my;
+    d.dflag[AX ? 0 : 1][s] = on;
 }
 
 // Dual-mesh corner exchanges, remap.cpp:1000-1069: iteration (i, j), both
 // pairs (1,1) and (1,-1).
-__device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
+__device__ __forceinline__ bool dual_corner_pair(const Dev& d, int i, int j, int pr, double& cx, double& cy) {
     const int nx = d.nx, ny = d.ny;
     const double dt = step_dt(d.ctl);
-    const int s = ix(d, i, j);
-#pragma unroll
-    for (int pr = 0; pr < 2; ++pr) {
+    {
         const int sx = 1, sy = pr == 0 ? 1 : -1;
         const int pi = i + sx, pj = j + sy;
-        double cx = 0.0, cy = 0.0;
+        cx = 0.0;
+        cy = 0.0;
         bool active = true;
         if (!d.per_x && (pi < 0 || pi > nx)) active = false;
         if (!d.per_y && (pj < 0 || pj > ny)) active = false;
@@ -1358,9 +1358,18 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
             cx = ufx * Fv;
             cy = ufy * Fv;
         }
+        return active;
+    }
+}
+__device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
+    const int s = ix(d, i, j);
+#pragma unroll
+    for (int pr = 0; pr < 2; ++pr) {
+        double cx, cy;
+        const bool on = dual_corner_pair(d, i, j, pr, cx, cy);
         d.dc_x[pr][s] = cx;
         d.dc_y[pr][s] = cy;
-        d.dflag[2 + pr][s] = active;
+        d.dflag[2 + pr][s] = on;
     }
 }
 
@@ -1375,6 +1384,122 @@ __global__ void k_dual_items(Dev d) {
     dual_face_item<1>(d, i, j);
     dual_face_item<0>(d, i, j);
     dual_corner_items(d, i, j);
+}
+
+// Wall boundaries: dual faces, dual corners and the node update fused per
+// 32x8 node tile (remap.cpp:993-1069 + 444-464). The tile's items (one extra
+// column / row of faces, one ring of corner iterations) are computed once into
+// shared memory; each node then gathers them in the reference's loop order,
+// which with walls is fixed: X face i (+), X face i+1 (-), Y face j (+),
+// Y face j+1 (-), corner (i-1, j-1, pair 1,1) (-), (i, j) pairs (+, +),
+// corner (i-1, j+1, pair 1,-1) (-).
+constexpr int DTX = 32, DTY = 8;
+__global__ void __launch_bounds__(DTX * DTY) k_dual_tile(Dev d) {
+    constexpr int NXF = (DTX + 1) * DTY, NYF = DTX * (DTY + 1), NCI = (DTX + 1) * (DTY + 2);
+    __shared__ double sx_[2][NXF], sy_[2][NYF], sc_[2][2][NCI];
+    __shared__ uint8_t fx_[NXF], fy_[NYF], fc_[2][NCI];
+    __shared__ int s_halt;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
+    const int nx = d.nx, ny = d.ny;  // walls: unique nodes [0, nx] x [0, ny]
+    const Rng rn = d.r_node;
+    const int i0 = rn.i0 + blockIdx.x * DTX, j0 = rn.j0 + blockIdx.y * DTY;
+    for (int t = tid; t < NXF; t += DTX * DTY) {
+        const int ia = i0 + t % (DTX + 1), ic = j0 + t / (DTX + 1);
+        double mx = 0.0, my = 0.0;
+        bool on = false;
+        if (ia >= 1 && ia <= nx && ic >= 0 && ic <= ny && in(d.r_dual, ia, ic)) on = dual_face_val<1>(d, ia, ic, mx, my);
+        sx_[0][t] = mx;
+        sx_[1][t] = my;
+        fx_[t] = on;
+    }
+    for (int t = tid; t < NYF; t += DTX * DTY) {
+        const int ic = i0 + t % DTX, ja = j0 + t / DTX;
+        double mx = 0.0, my = 0.0;
+        bool on = false;
+        if (ja >= 1 && ja <= ny && ic >= 0 && ic <= nx && in(d.r_dual, ic, ja)) on = dual_face_val<0>(d, ic, ja, mx, my);
+        sy_[0][t] = mx;
+        sy_[1][t] = my;
+        fy_[t] = on;
+    }
+    for (int t = tid; t < 2 * NCI; t += DTX * DTY) {
+        const int pr = t / NCI, q = t % NCI;
+        const int ci = i0 - 1 + q % (DTX + 1), cj = j0 - 1 + q / (DTX + 1);
+        double cx = 0.0, cy = 0.0;
+        bool on = false;
+        if (ci >= 0 && ci <= nx && cj >= 0 && cj <= ny && in(d.r_dual, ci, cj))
+            on = dual_corner_pair(d, ci, cj, pr, cx, cy);
+        sc_[pr][0][q] = cx;
+        sc_[pr][1][q] = cy;
+        fc_[pr][q] = on;
+    }
+    __syncthreads();
+    const int tx = tid % DTX, ty = tid / DTX;
+    const int i = i0 + tx, j = j0 + ty;
+    if (!in(rn, i, j) || i < 0 || j < 0 || i > nx || j > ny) return;
+    double ax = 0.0, ay = 0.0;
+    {
+        const int p = tx + ty * (DTX + 1), m = p + 1;  // X faces i, i+1
+        if (fx_[p]) {
+            ax += sx_[0][p];
+            ay += sx_[1][p];
+        }
+        if (fx_[m]) {
+            ax += -sx_[0][m];
+            ay += -sx_[1][m];
+        }
+    }
+    {
+        const int p = tx + ty * DTX, m = p + DTX;  // Y faces j, j+1
+        if (fy_[p]) {
+            ax += sy_[0][p];
+            ay += sy_[1][p];
+        }
+        if (fy_[m]) {
+            ax += -sy_[0][m];
+            ay += -sy_[1][m];
+        }
+    }
+    {
+        const int pp = tx + ty * (DTX + 1);            // iteration (i-1, j-1)
+        const int own = (tx + 1) + (ty + 1) * (DTX + 1);  // iteration (i, j)
+        const int pm = tx + (ty + 2) * (DTX + 1);      // iteration (i-1, j+1)
+        if (fc_[0][pp]) {
+            ax += -sc_[0][0][pp];
+            ay += -sc_[0][1][pp];
+        }
+        if (fc_[0][own]) {
+            ax += sc_[0][0][own];
+            ay += sc_[0][1][own];
+        }
+        if (fc_[1][own]) {
+            ax += sc_[1][0][own];
+            ay += sc_[1][1][own];
+        }
+        if (fc_[1][pm]) {
+            ax += -sc_[1][0][pm];
+            ay += -sc_[1][1][pm];
+        }
+    }
+    const int s = ix(d, i, j);
+    auto ml = [&](int c) {  // make_work's mcell (remap.cpp:133-138)
+        double mc = 0.0;
+        for (int a = 0; a < d.nmat; ++a) mc += d.m[a][c];
+        return mc;
+    };
+    const int c00 = ix(d, i - 1, j - 1), c10 = ix(d, i, j - 1), c01 = ix(d, i - 1, j);
+    const double mp_lag = 0.25 * (ml(c00) + ml(c10) + ml(c01) + ml(s));
+    const double mp_new = 0.25 * (d.mcell[c00] + d.mcell[c10] + d.mcell[c01] + d.mcell[s]);
+    if (mp_new <= 0.0 && own_node(d, i, j)) raise(d.ctl, ekey(PH_NODAL_MASS, j, i, 0));
+    const double inv = 1.0 / mp_new;
+    double ux = inv * (mp_lag * d.ulx[s] + ax), uy = inv * (mp_lag * d.uly[s] + ay);
+    if (i == 0 || i == nx) ux = 0.0;  // fill_ghost_nodes on walls (remap.cpp:462)
+    if (j == 0 || j == ny) uy = 0.0;
+    d.nux[s] = ux;
+    d.nuy[s] = uy;
+    d.unrm[s] = sqrt(ux * ux + uy * uy);
 }
 
 // MomAcc gather (App. C item 4) + apply_dual_update (remap.cpp:444-464) with
@@ -1956,8 +2081,12 @@ void launch_remap_core(const Dev& d, cudaStream_t s) {
     FieldList none{};
     launch_ghost_multi(d, fl, none, 1, 1, s);
     if (d.remap_velocity) {
-        { k_dual_items<<<grid_of(d.r_dual), blk2(), 0, s>>>(d); ++g_launches; }
-        { k_node_update<<<grid_of(d.r_node), blk2(), 0, s>>>(d); ++g_launches; }
+        if (d.per_x || d.per_y) {  // periodic seams reorder the node sums: items to HBM, then sorted gather
+            { k_dual_items<<<grid_of(d.r_dual), blk2(), 0, s>>>(d); ++g_launches; }
+            { k_node_update<<<grid_of(d.r_node), blk2(), 0, s>>>(d); ++g_launches; }
+        } else {
+            { k_dual_tile<<<tiles_of(d.r_node, DTX, DTY), DTX * DTY, 0, s>>>(d); ++g_launches; }
+        }
     }
 }
 
