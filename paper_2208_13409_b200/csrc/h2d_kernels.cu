@@ -1386,116 +1386,47 @@ __global__ void k_dual_items(Dev d) {
     dual_corner_items(d, i, j);
 }
 
-// Wall boundaries: dual faces, dual corners and the node update fused per
-// 32x8 node tile (remap.cpp:993-1069 + 444-464). The tile's items (one extra
-// column / row of faces, one ring of corner iterations) are computed once into
-// shared memory; each node then gathers them in the reference's loop order,
-// which with walls is fixed: X face i (+), X face i+1 (-), Y face j (+),
-// Y face j+1 (-), corner (i-1, j-1, pair 1,1) (-), (i, j) pairs (+, +),
-// corner (i-1, j+1, pair 1,-1) (-).
-constexpr int DTX = 32, DTY = 8;
-__global__ void __launch_bounds__(DTX * DTY) k_dual_tile(Dev d) {
-    constexpr int NXF = (DTX + 1) * DTY, NYF = DTX * (DTY + 1), NCI = (DTX + 1) * (DTY + 2);
-    __shared__ double sx_[2][NXF], sy_[2][NYF], sc_[2][2][NCI];
-    __shared__ uint8_t fx_[NXF], fy_[NYF], fc_[2][NCI];
-    __shared__ int s_halt;
-    const int tid = threadIdx.x;
-    if (tid == 0) s_halt = halted(d.ctl);
-    __syncthreads();
-    if (s_halt) return;
-    const int nx = d.nx, ny = d.ny;  // walls: unique nodes [0, nx] x [0, ny]
-    const Rng rn = d.r_node;
-    const int i0 = rn.i0 + blockIdx.x * DTX, j0 = rn.j0 + blockIdx.y * DTY;
-    for (int t = tid; t < NXF; t += DTX * DTY) {
-        const int ia = i0 + t % (DTX + 1), ic = j0 + t / (DTX + 1);
-        double mx = 0.0, my = 0.0;
-        bool on = false;
-        if (ia >= 1 && ia <= nx && ic >= 0 && ic <= ny && in(d.r_dual, ia, ic)) on = dual_face_val<1>(d, ia, ic, mx, my);
-        sx_[0][t] = mx;
-        sx_[1][t] = my;
-        fx_[t] = on;
-    }
-    for (int t = tid; t < NYF; t += DTX * DTY) {
-        const int ic = i0 + t % DTX, ja = j0 + t / DTX;
-        double mx = 0.0, my = 0.0;
-        bool on = false;
-        if (ja >= 1 && ja <= ny && ic >= 0 && ic <= nx && in(d.r_dual, ic, ja)) on = dual_face_val<0>(d, ic, ja, mx, my);
-        sy_[0][t] = mx;
-        sy_[1][t] = my;
-        fy_[t] = on;
-    }
-    for (int t = tid; t < 2 * NCI; t += DTX * DTY) {
-        const int pr = t / NCI, q = t % NCI;
-        const int ci = i0 - 1 + q % (DTX + 1), cj = j0 - 1 + q / (DTX + 1);
-        double cx = 0.0, cy = 0.0;
-        bool on = false;
-        if (ci >= 0 && ci <= nx && cj >= 0 && cj <= ny && in(d.r_dual, ci, cj))
-            on = dual_corner_pair(d, ci, cj, pr, cx, cy);
-        sc_[pr][0][q] = cx;
-        sc_[pr][1][q] = cy;
-        fc_[pr][q] = on;
-    }
-    __syncthreads();
-    const int tx = tid % DTX, ty = tid / DTX;
-    const int i = i0 + tx, j = j0 + ty;
-    if (!in(rn, i, j) || i < 0 || j < 0 || i > nx || j > ny) return;
-    double ax = 0.0, ay = 0.0;
-    {
-        const int p = tx + ty * (DTX + 1), m = p + 1;  // X faces i, i+1
-        if (fx_[p]) {
-            ax += sx_[0][p];
-            ay += sx_[1][p];
-        }
-        if (fx_[m]) {
-            ax += -sx_[0][m];
-            ay += -sx_[1][m];
-        }
-    }
-    {
-        const int p = tx + ty * DTX, m = p + DTX;  // Y faces j, j+1
-        if (fy_[p]) {
-            ax += sy_[0][p];
-            ay += sy_[1][p];
-        }
-        if (fy_[m]) {
-            ax += -sy_[0][m];
-            ay += -sy_[1][m];
-        }
-    }
-    {
-        const int pp = tx + ty * (DTX + 1);            // iteration (i-1, j-1)
-        const int own = (tx + 1) + (ty + 1) * (DTX + 1);  // iteration (i, j)
-        const int pm = tx + (ty + 2) * (DTX + 1);      // iteration (i-1, j+1)
-        if (fc_[0][pp]) {
-            ax += -sc_[0][0][pp];
-            ay += -sc_[0][1][pp];
-        }
-        if (fc_[0][own]) {
-            ax += sc_[0][0][own];
-            ay += sc_[0][1][own];
-        }
-        if (fc_[1][own]) {
-            ax += sc_[1][0][own];
-            ay += sc_[1][1][own];
-        }
-        if (fc_[1][pm]) {
-            ax += -sc_[1][0][pm];
-            ay += -sc_[1][1][pm];
-        }
-    }
+// Wall boundaries: the MomAcc gather in its fixed loop order — X face i (+),
+// X face i+1 (-), Y face j (+), Y face j+1 (-), corner (i-1, j-1, pair (1,1))
+// (-), own pairs (+, +), corner (i-1, j+1, pair (1,-1)) (-) — then
+// apply_dual_update (remap.cpp:444-464) and the wall condition (:462).
+__global__ void k_node_update_walls(Dev d) {
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, d.r_node.i0, d.r_node.j0);
+    const int nx = d.nx, ny = d.ny;
+    if (!in(d.r_node, i, j) || i < 0 || j < 0 || i > nx || j > ny) return;
     const int s = ix(d, i, j);
-    auto ml = [&](int c) {  // make_work's mcell (remap.cpp:133-138)
-        double mc = 0.0;
-        for (int a = 0; a < d.nmat; ++a) mc += d.m[a][c];
-        return mc;
-    };
-    const int c00 = ix(d, i - 1, j - 1), c10 = ix(d, i, j - 1), c01 = ix(d, i - 1, j);
-    const double mp_lag = 0.25 * (ml(c00) + ml(c10) + ml(c01) + ml(s));
+    const int sxr = ix(d, i + 1, j), syt = ix(d, i, j + 1);
+    const int pp = ix(d, i - 1, j - 1), pm = ix(d, i - 1, j + 1);
+    // flags of items outside the unique node range were never set: guard
+    const bool fxp = i >= 1 && d.dflag[0][s], fxm = i + 1 <= nx && d.dflag[0][sxr];
+    const bool fyp = j >= 1 && d.dflag[1][s], fym = j + 1 <= ny && d.dflag[1][syt];
+    const bool fpp = i >= 1 && j >= 1 && d.dflag[2][pp], fo0 = d.dflag[2][s], fo1 = d.dflag[3][s];
+    const bool fpm = i >= 1 && j + 1 <= ny && d.dflag[3][pm];
+    double ax = 0.0, ay = 0.0;
+    if (fxp) { ax += d.dfx_x[s]; ay += d.dfx_y[s]; }
+    if (fxm) { ax += -d.dfx_x[sxr]; ay += -d.dfx_y[sxr]; }
+    if (fyp) { ax += d.dfy_x[s]; ay += d.dfy_y[s]; }
+    if (fym) { ax += -d.dfy_x[syt]; ay += -d.dfy_y[syt]; }
+    if (fpp) { ax += -d.dc_x[0][pp]; ay += -d.dc_y[0][pp]; }
+    if (fo0) { ax += d.dc_x[0][s]; ay += d.dc_y[0][s]; }
+    if (fo1) { ax += d.dc_x[1][s]; ay += d.dc_y[1][s]; }
+    if (fpm) { ax += -d.dc_x[1][pm]; ay += -d.dc_y[1][pm]; }
+    const int c00 = pp, c10 = ix(d, i, j - 1), c01 = ix(d, i - 1, j);
+    double l00 = 0.0, l10 = 0.0, l01 = 0.0, l11 = 0.0;  // make_work's mcell (remap.cpp:133-138)
+    for (int a = 0; a < d.nmat; ++a) {
+        l00 += d.m[a][c00];
+        l10 += d.m[a][c10];
+        l01 += d.m[a][c01];
+        l11 += d.m[a][s];
+    }
+    const double mp_lag = 0.25 * (l00 + l10 + l01 + l11);
     const double mp_new = 0.25 * (d.mcell[c00] + d.mcell[c10] + d.mcell[c01] + d.mcell[s]);
     if (mp_new <= 0.0 && own_node(d, i, j)) raise(d.ctl, ekey(PH_NODAL_MASS, j, i, 0));
     const double inv = 1.0 / mp_new;
     double ux = inv * (mp_lag * d.ulx[s] + ax), uy = inv * (mp_lag * d.uly[s] + ay);
-    if (i == 0 || i == nx) ux = 0.0;  // fill_ghost_nodes on walls (remap.cpp:462)
+    if (i == 0 || i == nx) ux = 0.0;
     if (j == 0 || j == ny) uy = 0.0;
     d.nux[s] = ux;
     d.nuy[s] = uy;
@@ -2081,12 +2012,11 @@ void launch_remap_core(const Dev& d, cudaStream_t s) {
     FieldList none{};
     launch_ghost_multi(d, fl, none, 1, 1, s);
     if (d.remap_velocity) {
-        if (d.per_x || d.per_y) {  // periodic seams reorder the node sums: items to HBM, then sorted gather
-            { k_dual_items<<<grid_of(d.r_dual), blk2(), 0, s>>>(d); ++g_launches; }
+        { k_dual_items<<<grid_of(d.r_dual), blk2(), 0, s>>>(d); ++g_launches; }
+        if (d.per_x || d.per_y)  // periodic seams reorder the node sums: sorted gather
             { k_node_update<<<grid_of(d.r_node), blk2(), 0, s>>>(d); ++g_launches; }
-        } else {
-            { k_dual_tile<<<tiles_of(d.r_node, DTX, DTY), DTX * DTY, 0, s>>>(d); ++g_launches; }
-        }
+        else
+            { k_node_update_walls<<<grid_of(d.r_node), blk2(), 0, s>>>(d); ++g_launches; }
     }
 }
 
