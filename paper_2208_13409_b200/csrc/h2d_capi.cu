@@ -851,7 +851,7 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[4]
         CK(cudaEventRecord(c->ev[0], c->st));
         launch_step_start(d, c->st);
         CK(cudaEventRecord(c->ev[1], c->st));
-        launch_lagrange(d, 0, c->st);
+        launch_lagrange_run(d, c->st);
         CK(cudaEventRecord(c->ev[2], c->st));
         CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->R, c->st));
         launch_remap_core(d, c->st);

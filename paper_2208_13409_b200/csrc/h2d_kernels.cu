@@ -461,6 +461,164 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
     if (floors && own) atomicAdd(&d.ctl->step_floor, floors);
 }
 
+// The run-loop Lagrangian phase in ONE kernel per 32x8 node tile: Q and the
+// cell part of predict are evaluated for the tile's (34 x 10) surrounding
+// cells into shared memory (a ghost cell is evaluated at its wrapped
+// interior source, which is exactly what fill_ghost_cells would copy,
+// lagrange.cpp:75,132), then u_half / u_lag per node and e_lag per own cell
+// (lagrange.cpp:135-142, 146-196). Q, p_half and p_mix_half never leave the
+// chip; the API path (h2d_lagrange_step) keeps the two-kernel form because
+// it returns Q.
+template <int NM>
+__global__ void __launch_bounds__(LTX * LTY) k_lag_fused(Dev d) {
+    constexpr int CW = LTX + 2, CH = LTY + 2, NC = CW * CH, NN = (LTX + 1) * (LTY + 1);
+    __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC];
+    __shared__ double shx[NN], shy[NN];
+    __shared__ int s_halt;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
+    const int nx = d.nx, ny = d.ny;
+    const Rng rn = d.r_lagn;
+    const int i0 = rn.i0 + blockIdx.x * LTX, j0 = rn.j0 + blockIdx.y * LTY;
+    const double dt = step_dt(d.ctl);
+    const double cv = d.cv;
+    // ---- cells [i0-1, i0+LTX] x [j0-1, j0+LTY]: Q^n and predict
+    for (int t = tid; t < NC; t += LTX * LTY) {
+        const int ci = i0 - 1 + t % CW, cj = j0 - 1 + t / CW;
+        double q = 0.0, pmix = 0.0, ph[2] = {0.0, 0.0};
+        if (in(d.win_c, ci, cj) && ci >= -1 && cj >= -1 && ci <= nx && cj <= ny) {
+            const int i = (ci < 0 || ci >= nx) ? wrap_cell(ci, nx, d.per_x) : ci;
+            const int j = (cj < 0 || cj >= ny) ? wrap_cell(cj, ny, d.per_y) : cj;
+            // the canonical evaluation (errors, floor counts): an own interior cell of this tile
+            const bool canon = ci == i && cj == j && ci >= i0 && ci < i0 + LTX && cj >= j0 && cj < j0 + LTY &&
+                               in(d.r_lagc, i, j) && own_cell(d, i, j);
+            const int c = ix(d, i, j);
+            const int n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
+            const double u00x = d.ux[c], u00y = d.uy[c], u10x = d.ux[n10], u10y = d.uy[n10];
+            const double u01x = d.ux[n01], u01y = d.uy[n01], u11x = d.ux[n11], u11y = d.uy[n11];
+            double ka[2], ma[2], en[2];
+#pragma unroll
+            for (int a = 0; a < NM; ++a) {
+                ka[a] = d.k[a][c];
+                ma[a] = d.m[a][c];
+                en[a] = d.e[a][c];
+            }
+            const double ux_l = 0.5 * (u00x + u01x);
+            const double ux_r = 0.5 * (u10x + u11x);
+            const double uy_b = 0.5 * (u00y + u10y);
+            const double uy_t = 0.5 * (u01y + u11y);
+            const double div = div_dx(d, ux_r - ux_l, 1.0) + div_dy(d, uy_t - uy_b, 1.0);
+            if (!(div >= 0.0)) {
+                double cs = 0.0;
+                bool bad = false;
+#pragma unroll
+                for (int a = 0; a < NM; ++a) {
+                    if (ka[a] < kThermoTol) continue;
+                    const double rho_a = ma[a] / (ka[a] * cv);
+                    const double pa = eos_p(d, a, rho_a, en[a]);
+                    cs += ka[a] * sound(d, a, rho_a, pa, bad);
+                }
+                if (bad && canon) raise(d.ctl, ekey(PH_Q_UNPHYS, j, i, 0));
+                const double rho = d.rho_mix[c];
+                const double du = d.L * fabs(div);
+                q = rho * d.a1 * du * cs + d.a2 * rho * du * du;
+            }
+            bool tangled = false;
+            const double vol = quad_vol4(d, u00x, u00y, u10x, u10y, u11x, u11y, u01x, u01y, 0.5 * dt, tangled);
+            if (tangled && canon) raise(d.ctl, ekey(PH_PRED_TANGLED, j, i, 0));
+            int floors = 0;
+#pragma unroll
+            for (int a = 0; a < NM; ++a) {
+                if (!(ka[a] < kThermoTol)) {
+                    const double rho_n = ma[a] / (ka[a] * cv);
+                    const double rho_h = ma[a] / (ka[a] * vol);
+                    const double pa_n = eos_p(d, a, rho_n, en[a]);
+                    double ea = en[a] - (pa_n + q) * (1.0 / rho_h - 1.0 / rho_n);
+                    const double efloor = 1e-8 * fabs(en[a]);
+                    if (ea < efloor) {
+                        ea = efloor;
+                        ++floors;
+                    }
+                    ph[a] = eos_p(d, a, rho_h, ea);
+                    pmix += ka[a] * ph[a];
+                }
+            }
+            if (floors && canon) atomicAdd(&d.ctl->step_floor, floors);
+        }
+        s_q[t] = q;
+        s_pmh[t] = pmix;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) s_ph[a][t] = ph[a];
+    }
+    __syncthreads();
+    // ---- nodes: u_half, u_lag
+    for (int t = tid; t < NN; t += LTX * LTY) {
+        const int i = i0 + t % (LTX + 1), j = j0 + t / (LTX + 1);
+        double hx = 0.0, hy = 0.0;
+        if (in(rn, i, j)) {
+            const int ta = (t % (LTX + 1)) + (t / (LTX + 1)) * CW;  // cell (i-1, j-1) in the cell tile
+            const int tb = ta + 1, tc = ta + CW, te = tc + 1;
+            const int a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
+            const double mp = 0.25 * (d.m_mix[a] + d.m_mix[b] + d.m_mix[c] + d.m_mix[e]);
+            const double rho_p = div_cv(d, mp);
+            const double pq_a = s_pmh[ta] + s_q[ta], pq_b = s_pmh[tb] + s_q[tb];
+            const double pq_c = s_pmh[tc] + s_q[tc], pq_e = s_pmh[te] + s_q[te];
+            const double gx = div_dx(d, pq_b + pq_e - pq_a - pq_c, 2.0);
+            const double gy = div_dy(d, pq_c + pq_e - pq_a - pq_b, 2.0);
+            const double sc = 0.5 * dt / rho_p;
+            const double ux = d.ux[e], uy = d.uy[e];
+            hx = ux - gx * sc;
+            hy = uy - gy * sc;
+            if ((i < i0 + LTX || i == rn.i1 - 1) && (j < j0 + LTY || j == rn.j1 - 1)) {
+                d.uhx[e] = hx;
+                d.uhy[e] = hy;
+                d.ulx[e] = 2.0 * hx - ux;
+                d.uly[e] = 2.0 * hy - uy;
+            }
+        }
+        shx[t] = hx;
+        shy[t] = hy;
+    }
+    __syncthreads();
+    // ---- own cells: correct
+    const int tx = tid % LTX, ty = tid / LTX;
+    const int i = i0 + tx, j = j0 + ty;
+    if (!in(d.r_lage, i, j)) return;
+    const bool own = own_cell(d, i, j);
+    const int q00 = tx + ty * (LTX + 1), q10 = q00 + 1, q01 = q00 + LTX + 1, q11 = q01 + 1;
+    bool tangled = false;
+    const double vol =
+        quad_vol4(d, shx[q00], shy[q00], shx[q10], shy[q10], shx[q11], shy[q11], shx[q01], shy[q01], dt, tangled);
+    if (tangled && own) raise(d.ctl, ekey(PH_CORR_TANGLED, j, i, 0));
+    const int n = ix(d, i, j);
+    const int tcell = (tx + 1) + (ty + 1) * CW;
+    int floors = 0;
+    const double qn = s_q[tcell];
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        const double ka = d.k[a][n];
+        const double en = d.e[a][n];
+        double ea = 0.0;
+        if (ka < kThermoTol) {
+            if (ka > 0.0) ea = en;
+        } else {
+            const double ma = d.m[a][n];
+            const double rho_n = ma / (ka * cv);
+            const double rho_l = ma / (ka * vol);
+            ea = en - (s_ph[a][tcell] + qn) * (1.0 / rho_l - 1.0 / rho_n);
+            const double efloor = 1e-8 * fabs(en);
+            if (ea < efloor) {
+                ea = efloor;
+                ++floors;
+            }
+        }
+        d.el[a][n] = ea;
+    }
+    if (floors && own) atomicAdd(&d.ctl->step_floor, floors);
+}
+
 // ---------------------------------------------------------------------------
 // DirectCF remap (remap.cpp:734-1073)
 // ---------------------------------------------------------------------------
@@ -1984,6 +2142,25 @@ void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s) {
 
 void launch_remap(const Dev& d, cudaStream_t s) { launch_remap_core(d, s); post_and_ghosts(d, 0, s); }
 
+// run-loop Lagrangian phase: the fused kernel + ghost layers of u_half, u_lag, e_lag
+void launch_lagrange_run(const Dev& d, cudaStream_t s) {
+    if (d.nmat == 2)
+        { k_lag_fused<2><<<tiles_of(d.r_lagn, LTX, LTY), LTX * LTY, 0, s>>>(d); ++g_launches; }
+    else
+        { k_lag_fused<1><<<tiles_of(d.r_lagn, LTX, LTY), LTX * LTY, 0, s>>>(d); ++g_launches; }
+    FieldList fn{};
+    fn.n = 4;
+    fn.f[0] = d.uhx;
+    fn.f[1] = d.uhy;
+    fn.f[2] = d.ulx;
+    fn.f[3] = d.uly;
+    FieldList fl{};
+    fl.n = d.nmat;
+    fl.f[0] = d.el[0];
+    fl.f[1] = d.el[1];
+    launch_ghost_multi(d, fl, fn, 0, 1, s);
+}
+
 void launch_remap_core(const Dev& d, cudaStream_t s) {
     remap_init();
     const int nx = d.nx, ny = d.ny;
@@ -2022,7 +2199,7 @@ void launch_remap_core(const Dev& d, cudaStream_t s) {
 
 void launch_step(const Dev& d, cudaStream_t s, int* row_slivers) {
     { k_step_start<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy); ++g_launches; }
-    launch_lagrange(d, 0, s);
+    launch_lagrange_run(d, s);
     cudaMemsetAsync(row_slivers, 0, sizeof(int) * (size_t)(d.win_c.j1 - d.win_c.j0 + 1), s);
     launch_remap_core(d, s);
     post_and_ghosts(d, 1, s);

@@ -20,6 +20,7 @@ void launch_ghost_cells(const Dev& d, const FieldList& fl, cudaStream_t s);
 void launch_ghost_nodes(const Dev& d, const FieldList& fl, cudaStream_t s);
 void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s);
 void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s);
+void launch_lagrange_run(const Dev& d, cudaStream_t s);
 void launch_remap(const Dev& d, cudaStream_t s);
 void launch_remap_core(const Dev& d, cudaStream_t s);
 void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s);
