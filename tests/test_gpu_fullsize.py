@@ -1,0 +1,96 @@
+"""BASELINE.json configurations at (or near) full size on the GPU.
+
+Bitwise parity with the oracle where the oracle finishes in seconds (a few
+steps at full size), and size-independent properties over the full step
+counts: conservation of mass (walls), determinism (two runs, same bits) and
+finiteness.  Config 4 runs the first steps at full size (8192^2) on the GPU;
+its oracle parity is checked at 2048^2."""
+import numpy as np
+import pytest
+
+import helpers
+from paper_2208_13409_b200 import cases
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair_steps(case, steps):
+    painted = case.paint()
+    sg = helpers.prepared(helpers.product_lib(), case.cfg, painted)
+    so = helpers.prepared(helpers.oracle_lib(), case.cfg, painted)
+    rg, eg = helpers.run_capture(sg, steps, case.cfl)
+    ro, eo = helpers.run_capture(so, steps, case.cfl)
+    assert eg == eo
+    assert np.array_equal(rg.dts, ro.dts)
+    assert rg.diag == ro.diag and rg.floor_count == ro.floor_count
+    assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS) == []
+
+
+def test_c2_sedov_1024_first_steps_bitwise():
+    _pair_steps(cases.sedov(1024), 8)
+
+
+def test_c3_triple_point_2048x1024_first_steps_bitwise():
+    _pair_steps(cases.triple_point(2048, 1024), 3)
+
+
+def test_c4_shock_bubble_2048_first_steps_bitwise():
+    _pair_steps(cases.shock_bubble(2048), 2)
+
+
+def _mass(st, nmat):
+    return [float(np.sum(st.cell(st.m)[a])) for a in range(nmat)]
+
+
+def test_c2_sedov_full_run_properties():
+    """500 steps at 1024^2: per-material mass conserved (walls), run twice
+    bit-identical, all fields finite."""
+    case = cases.sedov(1024)
+    painted = case.paint()
+    outs = []
+    for _ in range(2):
+        s = helpers.prepared(helpers.product_lib(), case.cfg, painted)
+        m0 = _mass(s.download(), 1)
+        r = s.run(case.steps, cfl=case.cfl)
+        assert r.steps_done == 500
+        st = s.download()
+        assert np.isfinite(st.cell(st.m)).all() and np.isfinite(st.node(st.u)).all()
+        m1 = _mass(st, 1)
+        assert abs(m1[0] - m0[0]) <= 1e-12 * m0[0]
+        outs.append((st, r.dts))
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert helpers.bitwise_diff(outs[0][0], outs[1][0], helpers.STATE_FIELDS) == []
+
+
+def test_c3_triple_point_full_size_abort_step():
+    """Config 3 at full size aborts in the reference after step 819
+    (UnphysicalStateError from cfl_dt, SURVEY.md finding 6): the GPU run
+    reproduces the abort at the same step, conserving each material's mass
+    up to it."""
+    case = cases.triple_point(2048, 1024)
+    s = helpers.prepared(helpers.product_lib(), case.cfg, case.paint())
+    m0 = _mass(s.download(), 2)
+    r, err = helpers.run_capture(s, case.steps, case.cfl)
+    assert err is not None and err[0] == "UnphysicalStateError"
+    assert r.steps_done == 819
+    st = s.download()
+    assert st.step == 819
+    m1 = _mass(st, 2)
+    for a in range(2):
+        assert abs(m1[a] - m0[a]) <= 1e-11 * m0[a]
+
+
+def test_c4_shock_bubble_full_size_first_steps():
+    """Config 4 at 8192^2 (67M cells, two materials): 5 steps, masses
+    conserved, finite, deterministic dt."""
+    case = cases.shock_bubble(8192)
+    painted = case.paint()
+    s = helpers.prepared(helpers.product_lib(), case.cfg, painted)
+    m0 = _mass(s.download(), 2)
+    r = s.run(5, cfl=case.cfl)
+    assert r.steps_done == 5 and np.all(np.isfinite(r.dts)) and np.all(r.dts > 0)
+    st = s.download()
+    m1 = _mass(st, 2)
+    for a in range(2):
+        assert abs(m1[a] - m0[a]) <= 1e-11 * m0[a]
+    assert np.isfinite(st.cell(st.m)).all()
