@@ -65,8 +65,9 @@ def test_c2_sedov_full_run_properties():
 def test_c3_triple_point_full_size_abort_step():
     """Config 3 at full size aborts in the reference after step 819
     (UnphysicalStateError from cfl_dt, SURVEY.md finding 6): the GPU run
-    reproduces the abort at the same step, conserving each material's mass
-    up to it."""
+    reproduces the abort at the same step, conserving the total mass up to it
+    (slivers without a carrier join the partner material, remap.cpp:217-225,
+    so per-material masses may move between materials)."""
     case = cases.triple_point(2048, 1024)
     s = helpers.prepared(helpers.product_lib(), case.cfg, case.paint())
     m0 = _mass(s.download(), 2)
@@ -76,8 +77,7 @@ def test_c3_triple_point_full_size_abort_step():
     st = s.download()
     assert st.step == 819
     m1 = _mass(st, 2)
-    for a in range(2):
-        assert abs(m1[a] - m0[a]) <= 1e-11 * m0[a]
+    assert abs(sum(m1) - sum(m0)) <= 1e-12 * sum(m0)
 
 
 def test_c4_shock_bubble_full_size_first_steps():
@@ -91,6 +91,5 @@ def test_c4_shock_bubble_full_size_first_steps():
     assert r.steps_done == 5 and np.all(np.isfinite(r.dts)) and np.all(r.dts > 0)
     st = s.download()
     m1 = _mass(st, 2)
-    for a in range(2):
-        assert abs(m1[a] - m0[a]) <= 1e-11 * m0[a]
+    assert abs(sum(m1) - sum(m0)) <= 1e-12 * sum(m0)
     assert np.isfinite(st.cell(st.m)).all()
