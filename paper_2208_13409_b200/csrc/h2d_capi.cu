@@ -270,7 +270,7 @@ int fill_ghosts_cur(h2d_ctx* c, int parity) {
 }
 
 // One run-loop step (harness.cpp:390-412) for the state in `parity`.
-void enqueue_step(h2d_ctx* c, int parity) { launch_step(make_dev(c, parity, 1), c->st, c->base.row_slivers); }
+void enqueue_step(h2d_ctx* c, int parity) { launch_step(make_dev(c, parity, 1), c->st); }
 
 // cfl_dt of the current State into the control block's "next" slots, which
 // the first k_step_start of a run consumes (later steps get them from k_post)
@@ -506,8 +506,8 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     };
     d.sliver = bytes_plane();
     for (int q = 0; q < 4; ++q) d.dflag[q] = bytes_plane();
-    (void)bytes_plane();
-    d.row_slivers = reinterpret_cast<int*>(c->arena + c->arena_used);
+    d.sl_segs = reinterpret_cast<unsigned*>(bytes_plane());  // >= R*P/8 bytes needed
+    d.sl_rows = reinterpret_cast<unsigned*>(c->arena + c->arena_used);
     c->arena_used += ((size_t)c->R * 4 + 255) & ~size_t(255);
     if (c->arena_used > c->arena_bytes) return fail(H2D_ERR_NOMEM);
     if (cudaMalloc(&c->ctl, sizeof(Ctl)) != cudaSuccess) return fail(H2D_ERR_NOMEM);
@@ -707,7 +707,6 @@ int h2d_remap_step(h2d_ctx* c, double dt, int kind, int /*x_first*/, int remap_v
     if (int rc = ctl_reset(c)) return rc;
     const Dev d = make_dev(c, c->cur, remap_velocity != 0);
     launch_begin(c->ctl, 1, dt, c->st);
-    CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->R, c->st));
     launch_remap(d, c->st);
     launch_commit(c->ctl, 1, c->st);
     if (int rc = check_launch(c)) return rc;
@@ -853,8 +852,7 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[4]
         CK(cudaEventRecord(c->ev[1], c->st));
         launch_lagrange_run(d, c->st);
         CK(cudaEventRecord(c->ev[2], c->st));
-        CK(cudaMemsetAsync(c->base.row_slivers, 0, sizeof(int) * (size_t)c->R, c->st));
-        launch_remap_core(d, c->st);
+            launch_remap_core(d, c->st);
         post_and_ghosts(d, 1, c->st);
         launch_commit_finish(d, c->st);
         CK(cudaEventRecord(c->ev[3], c->st));

@@ -133,7 +133,9 @@ struct Dev {
     double *slm[2], *slme[2];               // pending sliver mass / m*e (remap.cpp:149-153)
     uint8_t* sliver;                        // per-cell sliver flags (bit a)
     uint8_t* dflag[4];                      // active X / Y dual faces, dual-corner pairs
-    int* row_slivers;
+    // sliver index: bit (i - r_gath.i0) of word [(j - r_gath.j0) * nwx + (i - r_gath.i0) / 32]
+    // in sl_segs, bit (j - r_gath.j0) % 32 of sl_rows[(j - r_gath.j0) / 32]; cleared as consumed
+    unsigned *sl_rows, *sl_segs;
     Ctl* ctl;
 };
 

@@ -1305,82 +1305,145 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     d.mcell[c] = mtot;
     if (NM == 2) {
         d.sliver[c] = sl;
-        if (sl) atomicAdd(&d.row_slivers[j - d.win_c.j0], 1);
+        if (sl) {  // index the sliver for k_slivers (row bit + segment bit)
+            const int jr = j - rg.j0;
+            atomicOr(&d.sl_segs[(size_t)jr * ((rg.i1 - rg.i0 + 31) >> 5) + blockIdx.x], 1u << tx);
+            atomicOr(&d.sl_rows[jr >> 5], 1u << (jr & 31));
+        }
     }
 }
 
 
-// Sequential sliver redistribution (remap.cpp:194-226) in row-major order by
-// one warp: rows with pending slivers are scanned 32 cells at a time.
+// Sequential sliver redistribution (remap.cpp:194-226), one warp, in the
+// reference's row-major `pending` order. Rows and 32-cell segments holding
+// slivers are found through the bitmaps the tile kernel set (k_remap_tile
+// finalize); each sliver's carrier search (rings r = 1, 2 in the reference
+// scan order) runs one candidate per lane and is reduced to the FIRST maximum
+// of k (strict `>` scan == lowest lane among equal maxima, ring 1 before 2).
+// The update is made by one lane; __syncwarp orders it before the next
+// sliver's loads, so the chain of dependent slivers sees the same values as
+// the reference loop. The flag byte d.sliver is rewritten for every finalized
+// cell each step, so stale bitmap bits (after an aborted step) are harmless.
+__device__ __forceinline__ void sliver_offset(int lane, int& di, int& dj, int& ring) {
+    if (lane < 8) {  // ring 1: (dj, di) row-major, centre skipped
+        const int q = lane < 4 ? lane : lane + 1;
+        dj = q / 3 - 1;
+        di = q % 3 - 1;
+        ring = 1;
+    } else {  // ring 2: dj = -2 (5), dj = -1..1 (di = -2, 2), dj = 2 (5)
+        const int q = lane - 8;
+        ring = 2;
+        if (q < 5) {
+            dj = -2;
+            di = q - 2;
+        } else if (q < 11) {
+            dj = (q - 5) / 2 - 1;
+            di = ((q - 5) & 1) ? 2 : -2;
+        } else {
+            dj = 2;
+            di = q - 13;
+        }
+    }
+}
+
+__device__ __forceinline__ void sliver_one(const Dev& d, const Rng& rg, int si, int sj, int lane) {
+    const int sc = ix(d, si, sj);
+    const unsigned fl = d.sliver[sc];
+    int di = 0, dj = 0, ring = 3;
+    if (lane < 24) sliver_offset(lane, di, dj, ring);
+    int ni = si + di, nj = sj + dj;
+    if (d.per_x) ni = (ni + 2 * d.nx) % d.nx;
+    if (d.per_y) nj = (nj + 2 * d.ny) % d.ny;
+    const bool inb = lane < 24 && ni >= 0 && ni < d.nx && nj >= 0 && nj < d.ny && in(rg, ni, nj);
+    const int nc = inb ? ix(d, ni, nj) : sc;
+#pragma unroll 1
+    for (int a = 0; a < 2; ++a) {
+        if (!(fl & (1u << a))) continue;
+        const double smv = d.slm[a][sc], smev = d.slme[a][sc];
+        double mv = 0.0, kv = -1.0, mev = 0.0, mcv = 0.0;
+        bool cand = false;
+        if (inb) {  // the carrier's me and mcell are loaded with the search (one latency)
+            mv = d.nm[a][nc];
+            kv = d.nk[a][nc];
+            mev = d.me[a][nc];
+            mcv = d.mcell[nc];
+            cand = !(mv <= 0.0) && kv > -1.0;  // the reference skips m <= 0, then needs k > bk
+        }
+        // lexicographic min of (ring, -k, lane) over candidates
+        int br = cand ? ring : 4, bl = lane;
+        double bkv = kv;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+            const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+            const double ok = __shfl_xor_sync(0xffffffffu, bkv, o);
+            const bool take = orr < br || (orr == br && br < 4 && (ok > bkv || (ok == bkv && ol < bl)));
+            if (take) {
+                br = orr;
+                bl = ol;
+                bkv = ok;
+            }
+        }
+        const bool found = br < 4;
+        const double mcar = __shfl_sync(0xffffffffu, mv, found ? bl : 0);
+        if (found && mcar + smv > 0.0) {
+            if (lane == bl) {
+                const double nmv = mv + smv;
+                const double nme = mev + smev;
+                d.nm[a][nc] = nmv;
+                d.me[a][nc] = nme;
+                d.ne[a][nc] = nme / nmv;
+                d.mcell[nc] = mcv + smv;
+            }
+        } else if (lane == 0) {
+            if (own_cell(d, si, sj)) d.ctl->step_fix += 1;
+            const int b = 1 - a;
+            const double nmv = d.nm[b][sc] + smv;
+            const double nme = d.me[b][sc] + smev;
+            d.nm[b][sc] = nmv;
+            d.me[b][sc] = nme;
+            d.ne[b][sc] = nme / nmv;
+            d.mcell[sc] += smv;
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void k_slivers(Dev d) {
     if (halted(d.ctl)) return;
     const int lane = threadIdx.x;
-    const int nx = d.nx, ny = d.ny;
-    const Rng rg = d.r_gath;  // the cells finalized by this block, in row-major order
-    for (int j0 = rg.j0; j0 < rg.j1; j0 += 32) {
-        const int jr = j0 + lane;
-        const int cnt = jr < rg.j1 ? d.row_slivers[jr - d.win_c.j0] : 0;
-        unsigned rows = __ballot_sync(0xffffffffu, cnt != 0);
-        while (rows) {
-            const int r = __ffs(rows) - 1;
-            rows &= rows - 1;
-            const int j = j0 + r;
-            for (int i0 = rg.i0; i0 < rg.i1; i0 += 32) {
-                const int ic = i0 + lane;
-                const uint8_t f = ic < rg.i1 ? d.sliver[ix(d, ic, j)] : 0;
-                unsigned cells = __ballot_sync(0xffffffffu, f != 0);
-                while (cells) {
-                    const int b = __ffs(cells) - 1;
-                    cells &= cells - 1;
-                    if (lane == 0) {
-                        const int si = i0 + b, sj = j;
-                        const int sc = ix(d, si, sj);
-                        const uint8_t fl = d.sliver[sc];
-                        for (int a = 0; a < 2; ++a) {
-                            if (!(fl & (1u << a))) continue;
-                            const double smv = d.slm[a][sc], smev = d.slme[a][sc];
-                            int bi = -1, bj = -1;
-                            double bk = -1.0;
-                            for (int rr = 1; rr <= 2 && bi < 0; ++rr)
-                                for (int dj = -rr; dj <= rr; ++dj)
-                                    for (int di = -rr; di <= rr; ++di) {
-                                        const int adi = di < 0 ? -di : di, adj = dj < 0 ? -dj : dj;
-                                        if ((adi < adj ? adj : adi) != rr) continue;
-                                        int ni = si + di, nj = sj + dj;
-                                        if (d.per_x) ni = (ni + 2 * nx) % nx;
-                                        if (d.per_y) nj = (nj + 2 * ny) % ny;
-                                        if (ni < 0 || ni >= nx || nj < 0 || nj >= ny) continue;
-                                        if (!in(rg, ni, nj)) continue;  // outside this block's finalized cells
-                                        const int nc = ix(d, ni, nj);
-                                        if (d.nm[a][nc] <= 0.0) continue;
-                                        if (d.nk[a][nc] > bk) {
-                                            bk = d.nk[a][nc];
-                                            bi = ni;
-                                            bj = nj;
-                                        }
-                                    }
-                            if (bi >= 0 && d.nm[a][ix(d, bi, bj)] + smv > 0.0) {
-                                const int bc = ix(d, bi, bj);
-                                d.nm[a][bc] += smv;
-                                d.me[a][bc] += smev;
-                                d.ne[a][bc] = d.me[a][bc] / d.nm[a][bc];
-                                d.mcell[bc] += smv;
-                            } else {
-                                if (own_cell(d, si, sj)) d.ctl->step_fix += 1;
-                                const int bm = 1 - a;
-                                d.nm[bm][sc] += smv;
-                                d.me[bm][sc] += smev;
-                                d.ne[bm][sc] = d.me[bm][sc] / d.nm[bm][sc];
-                                d.mcell[sc] += smv;
-                            }
+    const Rng rg = d.r_gath;
+    const int nrow = rg.j1 - rg.j0, nwx = (rg.i1 - rg.i0 + 31) >> 5, nrw = (nrow + 31) >> 5;
+    for (int rw0 = 0; rw0 < nrw; rw0 += 32) {
+        const int rw = rw0 + lane;
+        const unsigned rb = rw < nrw ? d.sl_rows[rw] : 0u;
+        if (rb) d.sl_rows[rw] = 0u;
+        unsigned wm = __ballot_sync(0xffffffffu, rb != 0u);
+        while (wm) {
+            const int L = __ffs(wm) - 1;
+            wm &= wm - 1;
+            unsigned bits = __shfl_sync(0xffffffffu, rb, L);
+            while (bits) {
+                const int jr = ((rw0 + L) << 5) + __ffs(bits) - 1;
+                bits &= bits - 1;
+                unsigned* seg = d.sl_segs + (size_t)jr * nwx;
+                for (int w0 = 0; w0 < nwx; w0 += 32) {
+                    const int w = w0 + lane;
+                    const unsigned sb = w < nwx ? seg[w] : 0u;
+                    if (sb) seg[w] = 0u;
+                    unsigned nz = __ballot_sync(0xffffffffu, sb != 0u);
+                    while (nz) {
+                        const int L2 = __ffs(nz) - 1;
+                        nz &= nz - 1;
+                        unsigned cb = __shfl_sync(0xffffffffu, sb, L2);
+                        while (cb) {
+                            const int i = rg.i0 + ((w0 + L2) << 5) + __ffs(cb) - 1;
+                            cb &= cb - 1;
+                            sliver_one(d, rg, i, rg.j0 + jr, lane);
                         }
-                        d.sliver[sc] = 0;
                     }
-                    __syncwarp();
                 }
             }
-            if (lane == 0) d.row_slivers[j - d.win_c.j0] = 0;
-            __syncwarp();
         }
     }
 }
@@ -2197,10 +2260,9 @@ void launch_remap_core(const Dev& d, cudaStream_t s) {
     }
 }
 
-void launch_step(const Dev& d, cudaStream_t s, int* row_slivers) {
+void launch_step(const Dev& d, cudaStream_t s) {
     { k_step_start<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy); ++g_launches; }
     launch_lagrange_run(d, s);
-    cudaMemsetAsync(row_slivers, 0, sizeof(int) * (size_t)(d.win_c.j1 - d.win_c.j0 + 1), s);
     launch_remap_core(d, s);
     post_and_ghosts(d, 1, s);
     { k_commit_finish<<<1, 1, 0, s>>>(d.ctl); ++g_launches; }

@@ -24,7 +24,7 @@ void launch_lagrange_run(const Dev& d, cudaStream_t s);
 void launch_remap(const Dev& d, cudaStream_t s);
 void launch_remap_core(const Dev& d, cudaStream_t s);
 void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s);
-void launch_step(const Dev& d, cudaStream_t s, int* row_slivers);  // one run-loop step
+void launch_step(const Dev& d, cudaStream_t s);  // one run-loop step
 void launch_cfl_next(const Dev& d, cudaStream_t s);
 void launch_step_start(const Dev& d, cudaStream_t s);
 void launch_commit_finish(const Dev& d, cudaStream_t s);               // wave speed of the current State
