@@ -7,6 +7,7 @@
 // behaviour of `a < b ? b : a`).  Cited lines are in /root/reference/proj.
 #pragma once
 #include <cstdint>
+#include <math_constants.h>
 
 #define H2D_DEV __device__ __forceinline__
 
@@ -181,8 +182,13 @@ H2D_DEV double lim_grad(double am, double ac, double ap, double xm, double xc, d
         bad = true;
         return 0.0;
     }
-    const double dm = (ac - am) / hm;
-    const double dp = (ap - ac) / hp;
+    const double nm = ac - am, np = ap - ac;
+    // a zero difference over a positive (non-NaN) spacing gives dm == 0 (or
+    // dp == 0) and the result 0: return before the divides, whose fast path
+    // rejects zero operands (same result, no slow-path call)
+    if ((nm == 0.0 && hm > 0.0) || (np == 0.0 && hp > 0.0)) return 0.0;
+    const double dm = nm / hm;
+    const double dp = np / hp;
     if (dm == 0.0 || dp == 0.0 || (dm > 0.0) != (dp > 0.0)) return 0.0;
     const double r = dm / dp;
     return 0.5 * (van_leer(r) * dp + van_leer(1.0 / r) * dm);

@@ -658,7 +658,10 @@ __device__ __forceinline__ void face_flux(double ym, double yp, double dmx, doub
     if (fabs(den) < 1e-300) {
         xlo = xhi = 0.5 * (dmx + dpx);
     } else {
-        const double slope = (dpx - dmx) / den;
+        // a zero numerator over a finite divisor: the exact signed zero of the
+        // quotient (0 * den has the sign of 0 / den) without the divide's slow path
+        const double num = dpx - dmx;
+        const double slope = (num == 0.0 && fabs(den) < CUDART_INF) ? num * den : num / den;
         xlo = dmx + slope * (wlo - (ym + dmy));
         xhi = dmx + slope * (whi - (ym + dmy));
     }
@@ -809,15 +812,12 @@ __device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, i
         const int ia_d = dvol > 0.0 ? ia - 1 : ia;
         const double sgn = dvol > 0.0 ? 1.0 : -1.0;
         const int cdi = AX ? ia_d : ic, cdj = AX ? ic : ia_d;
-        // the flux window [wlo, whi] of cf_face_flux (recomputed, same bits)
-        double dv2, wlo, whi;
+        // the flux window [wlo, whi] of cf_face_flux (remap.cpp:29-31, same
+        // bits; dvol != 0 implies whi > wlo)
         const int q1 = AX ? T.n(i, j + 1) : T.n(i + 1, j);
-        if (AX)
-            face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * T.hx[qn], dt * T.hy[qn], dt * T.hx[q1],
-                      dt * T.hy[q1], dv2, wlo, whi);
-        else
-            face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * T.hy[qn], dt * T.hx[qn], dt * T.hy[q1],
-                      dt * T.hx[q1], dv2, wlo, whi);
+        const double wlo = AX ? d.y0 + j * d.dy + rmax(0.0, dt * T.hy[qn]) : d.x0 + i * d.dx + rmax(0.0, dt * T.hx[qn]);
+        const double whi = AX ? d.y0 + (j + 1) * d.dy + rmin(0.0, dt * T.hy[q1])
+                              : d.x0 + (i + 1) * d.dx + rmin(0.0, dt * T.hx[q1]);
         const double wwin = whi - wlo;
         const double width = dvol / wwin;
         const double f0pos = AX ? d.x0 + ia * d.dx : d.y0 + ia * d.dy;
