@@ -341,13 +341,15 @@ class Solver:
             raise err
         return res
 
-    def step_timed(self, cfl: float, t_end: float = 1e30, phases: bool = False):
+    STEP_GROUPS = ("start", "lagrange", "remap_tile", "slivers", "dual", "post", "total")
+
+    def step_timed(self, cfl: float, t_end: float = 1e30, phases: bool = False) -> dict:
         """One run-loop step timed with CUDA events (product only): returns
-        (cfl_ms, lagrange_ms, remap_ms, total_ms); phases=False replays the
-        production CUDA graph (only total is set)."""
-        ms = (C.c_float * 4)()
+        milliseconds per kernel group (STEP_GROUPS); phases=False replays the
+        production CUDA graph and only "total" is set."""
+        ms = (C.c_float * 8)()
         self._check(self.lib.fn["step_timed"](self._h, cfl, t_end, int(phases), ms))
-        return tuple(ms)
+        return {k: float(ms[q]) for q, k in enumerate(self.STEP_GROUPS)}
 
     def flush_l2(self, nbytes: int = 512 << 20):
         self._check(self.lib.fn["flush_l2"](self._h, nbytes))

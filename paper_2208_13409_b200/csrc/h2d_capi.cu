@@ -47,7 +47,7 @@ struct h2d_ctx {
     int dt_log_cap = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one run-loop step per State parity
     long long graph_kernels = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[7] = {};
     h2d_block blk{};   // the block of the 2D decomposition (the whole mesh for h2d_create)
     bool is_block = false;
     double* xbuf = nullptr;  // device staging for window uploads / owned downloads
@@ -459,6 +459,11 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     d.rdx = pow2_recip(m.dx);
     d.rdy = pow2_recip(m.dy);
     d.rcv = pow2_recip(d.cv);
+    {
+        const double diag = std::sqrt(m.dx * m.dx + m.dy * m.dy);  // host IEEE, no contraction
+        d.dgx = m.dx / diag;
+        d.dgy = m.dy / diag;
+    }
     for (int a = 0; a < nm; ++a) {
         d.stiff[a] = cfg->eos[a].kind == H2D_EOS_STIFFENED;
         d.gamma[a] = cfg->eos[a].gamma;
@@ -829,7 +834,7 @@ int h2d_totals(h2d_ctx* c, double out[6]) {
     return 0;
 }
 
-int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[4]) {
+int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[8]) {
     cudaSetDevice(c->device);
     if (!c->ev[0])
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
@@ -845,31 +850,34 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[4]
     // the wave speed of the current State (normally left by the previous
     // step's k_post) is recomputed outside the timed region
     enqueue_cfl_next(c);
-    if (phases) {  // un-graphed launch with events between the phases
+    for (int q = 0; q < 8; ++q) ms[q] = 0.0f;
+    if (phases) {  // un-graphed launches with events between the kernel groups
         const Dev d = make_dev(c, c->cur, 1);
         CK(cudaEventRecord(c->ev[0], c->st));
         launch_step_start(d, c->st);
         CK(cudaEventRecord(c->ev[1], c->st));
         launch_lagrange_run(d, c->st);
         CK(cudaEventRecord(c->ev[2], c->st));
-            launch_remap_core(d, c->st);
+        launch_remap_tile(d, c->st);
+        CK(cudaEventRecord(c->ev[3], c->st));
+        launch_remap_slivers(d, c->st);
+        CK(cudaEventRecord(c->ev[4], c->st));
+        launch_remap_dual(d, c->st);
+        CK(cudaEventRecord(c->ev[5], c->st));
         post_and_ghosts(d, 1, c->st);
         launch_commit_finish(d, c->st);
-        CK(cudaEventRecord(c->ev[3], c->st));
+        CK(cudaEventRecord(c->ev[6], c->st));
         if (int rc = check_launch(c)) return rc;
-        CK(cudaEventSynchronize(c->ev[3]));
-        CK(cudaEventElapsedTime(&ms[0], c->ev[0], c->ev[1]));
-        CK(cudaEventElapsedTime(&ms[1], c->ev[1], c->ev[2]));
-        CK(cudaEventElapsedTime(&ms[2], c->ev[2], c->ev[3]));
-        CK(cudaEventElapsedTime(&ms[3], c->ev[0], c->ev[3]));
+        CK(cudaEventSynchronize(c->ev[6]));
+        for (int q = 0; q < 6; ++q) CK(cudaEventElapsedTime(&ms[q], c->ev[q], c->ev[q + 1]));
+        CK(cudaEventElapsedTime(&ms[6], c->ev[0], c->ev[6]));
     } else {  // the production path: one graph launch
         if (int rc = ensure_graphs(c)) return rc;
         CK(cudaEventRecord(c->ev[0], c->st));
         if (int rc = launch_step_graph(c, c->cur)) return rc;
-        CK(cudaEventRecord(c->ev[3], c->st));
-        CK(cudaEventSynchronize(c->ev[3]));
-        ms[0] = ms[1] = ms[2] = 0.0f;
-        CK(cudaEventElapsedTime(&ms[3], c->ev[0], c->ev[3]));
+        CK(cudaEventRecord(c->ev[6], c->st));
+        CK(cudaEventSynchronize(c->ev[6]));
+        CK(cudaEventElapsedTime(&ms[6], c->ev[0], c->ev[6]));
     }
     if (int rc = ctl_pull(c)) return rc;
     c->cur = h.cur;

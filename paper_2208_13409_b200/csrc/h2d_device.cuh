@@ -114,6 +114,9 @@ struct Dev {
     // exact reciprocals of dx, dy, dx*dy when they are powers of two (0
     // otherwise): x / dx == x * (1/dx) bit for bit in that case
     double rdx, rdy, rcv;
+    // LinearDiag unit diagonal (reconstruct.cpp:135,139,144): dx/diag, dy/diag
+    // with diag = sqrt(dx*dx + dy*dy), loop invariant, computed once (same bits)
+    double dgx, dgy;
     int stiff[2];
     double gamma[2], pi[2];
     double a1, a2;
@@ -204,16 +207,15 @@ H2D_DEV double face_value2(double a0, double a1, double a2, double x0, double x1
 H2D_DEV double corner_diag(const Dev& d, const double* a, const double* xlx, const double* xly, double dxp,
                            double dyp, double lwx, double lwy, bool& bad) {
     const double ac = a[4];
-    const double diag = sqrt(d.dx * d.dx + d.dy * d.dy);
     const double sx = dxp >= 0.0 ? 1.0 : -1.0;
     if (dxp * dyp > 0.0) {
-        const double vx = d.dx / diag, vy = d.dy / diag;
+        const double vx = d.dgx, vy = d.dgy;
         const double sc = xlx[4] * vx + xly[4] * vy;
         const double gv = lim_grad(a[0], ac, a[8], xlx[0] * vx + xly[0] * vy, sc, xlx[8] * vx + xly[8] * vy, bad);
         const double ex = sx * lwx - dxp, ey = sx * lwy - dyp;
         return ac + 0.5 * gv * (ex * vx + ey * vy);
     }
-    const double vx = d.dx / diag, vy = -d.dy / diag;
+    const double vx = d.dgx, vy = -d.dgy;  // (-dy)/diag == -(dy/diag)
     const double sc = xlx[4] * vx + xly[4] * vy;
     const double gvp = lim_grad(a[2], ac, a[6], xlx[2] * vx + xly[2] * vy, sc, xlx[6] * vx + xly[6] * vy, bad);
     const double ex = sx * lwx - dxp, ey = sx * -lwy - dyp;

@@ -2225,19 +2225,25 @@ void launch_lagrange_run(const Dev& d, cudaStream_t s) {
 }
 
 void launch_remap_core(const Dev& d, cudaStream_t s) {
-    remap_init();
-    const int nx = d.nx, ny = d.ny;
-    const bool two = d.nmat == 2;
-    (void)nx;
-    (void)ny;
     if (!d.remap_velocity) { k_copy_u<<<grid_of(d.win_n), blk2(), 0, s>>>(d); ++g_launches; }
+    launch_remap_tile(d, s);
+    launch_remap_slivers(d, s);
+    launch_remap_dual(d, s);
+}
+
+// the fused flux tile kernel alone (timed separately by h2d_step_timed)
+void launch_remap_tile(const Dev& d, cudaStream_t s) {
+    remap_init();
     const dim3 gft = tiles_of(d.r_gath, RTX, RTY);
-    if (two) {
+    if (d.nmat == 2)
         { k_remap_tile<2><<<gft, RTX * RTY, remap_smem_bytes<2>(), s>>>(d); ++g_launches; }
-        { k_slivers<<<1, 32, 0, s>>>(d); ++g_launches; }
-    } else {
+    else
         { k_remap_tile<1><<<gft, RTX * RTY, remap_smem_bytes<1>(), s>>>(d); ++g_launches; }
-    }
+}
+
+// slivers + finalize_cells ghost fill + flux ghosts
+void launch_remap_slivers(const Dev& d, cudaStream_t s) {
+    if (d.nmat == 2) { k_slivers<<<1, 32, 0, s>>>(d); ++g_launches; }
     // finalize_cells ghost fill (remap.cpp:227-233) + face / corner flux ghosts
     FieldList fl{};
     int q = 0;
@@ -2251,6 +2257,10 @@ void launch_remap_core(const Dev& d, cudaStream_t s) {
     fl.n = q;
     FieldList none{};
     launch_ghost_multi(d, fl, none, 1, 1, s);
+}
+
+// dual-mesh momentum remap (remap.cpp:993-1059)
+void launch_remap_dual(const Dev& d, cudaStream_t s) {
     if (d.remap_velocity) {
         { k_dual_items<<<grid_of(d.r_dual), blk2(), 0, s>>>(d); ++g_launches; }
         if (d.per_x || d.per_y)  // periodic seams reorder the node sums: sorted gather

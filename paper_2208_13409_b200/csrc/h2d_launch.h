@@ -22,7 +22,10 @@ void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s);
 void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s);
 void launch_lagrange_run(const Dev& d, cudaStream_t s);
 void launch_remap(const Dev& d, cudaStream_t s);
-void launch_remap_core(const Dev& d, cudaStream_t s);
+void launch_remap_core(const Dev& d, cudaStream_t s);  // = tile + slivers + dual
+void launch_remap_tile(const Dev& d, cudaStream_t s);
+void launch_remap_slivers(const Dev& d, cudaStream_t s);
+void launch_remap_dual(const Dev& d, cudaStream_t s);
 void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s);
 void launch_step(const Dev& d, cudaStream_t s);  // one run-loop step
 void launch_cfl_next(const Dev& d, cudaStream_t s);

@@ -21,7 +21,7 @@ def main():
             ts = []
             for _ in range(10):
                 s.flush_l2()
-                ts.append(s.step_timed(c.cfl)[3])
+                ts.append(s.step_timed(c.cfl)["total"])
             ms = float(np.median(ts))
             out.append({"case": name, "n": n, "cells": n * n, "ms": ms, "cells_per_s": n * n / ms * 1e3})
             print(json.dumps(out[-1]), flush=True)
