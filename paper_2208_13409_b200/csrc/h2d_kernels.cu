@@ -386,6 +386,22 @@ __global__ void k_lag_cells(Dev d) {
 // per 32x8 tile: u_half of the tile's (33 x 9) nodes goes to shared memory,
 // u_lag is written per node and e_lag per cell from the four u_half.
 constexpr int LTX = 32, LTY = 8;
+
+// (row, column) of a flat tile index t = tid, tid + BS, ... over rows of W
+// entries, stepped incrementally (no per-iteration integer divide / modulo)
+template <int W, int BS>
+struct RowCol {
+    int r, c;
+    __device__ __forceinline__ explicit RowCol(int t) : r(t / W), c(t % W) {}
+    __device__ __forceinline__ void step() {
+        r += BS / W;
+        c += BS % W;
+        if (c >= W) {
+            c -= W;
+            ++r;
+        }
+    }
+};
 template <int NM>
 __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_lag) {
     constexpr int NN = (LTX + 1) * (LTY + 1);
@@ -485,8 +501,9 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_fused(Dev d) {
     const double dt = step_dt(d.ctl);
     const double cv = d.cv;
     // ---- cells [i0-1, i0+LTX] x [j0-1, j0+LTY]: Q^n and predict
-    for (int t = tid; t < NC; t += LTX * LTY) {
-        const int ci = i0 - 1 + t % CW, cj = j0 - 1 + t / CW;
+    RowCol<CW, LTX * LTY> rc0(tid);
+    for (int t = tid; t < NC; t += LTX * LTY, rc0.step()) {
+        const int ci = i0 - 1 + rc0.c, cj = j0 - 1 + rc0.r;
         double q = 0.0, pmix = 0.0, ph[2] = {0.0, 0.0};
         if (in(d.win_c, ci, cj) && ci >= -1 && cj >= -1 && ci <= nx && cj <= ny) {
             const int i = (ci < 0 || ci >= nx) ? wrap_cell(ci, nx, d.per_x) : ci;
@@ -554,11 +571,12 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_fused(Dev d) {
     }
     __syncthreads();
     // ---- nodes: u_half, u_lag
-    for (int t = tid; t < NN; t += LTX * LTY) {
-        const int i = i0 + t % (LTX + 1), j = j0 + t / (LTX + 1);
+    RowCol<LTX + 1, LTX * LTY> rc1(tid);
+    for (int t = tid; t < NN; t += LTX * LTY, rc1.step()) {
+        const int i = i0 + rc1.c, j = j0 + rc1.r;
         double hx = 0.0, hy = 0.0;
         if (in(rn, i, j)) {
-            const int ta = (t % (LTX + 1)) + (t / (LTX + 1)) * CW;  // cell (i-1, j-1) in the cell tile
+            const int ta = rc1.c + rc1.r * CW;  // cell (i-1, j-1) in the cell tile
             const int tb = ta + 1, tc = ta + CW, te = tc + 1;
             const int a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
             const double mp = 0.25 * (d.m_mix[a] + d.m_mix[b] + d.m_mix[c] + d.m_mix[e]);
@@ -1026,8 +1044,9 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     // independent, coalesced rows): u_half on the node region, e_lag, m, k
     // (and normals) on the cell region.  T.rho holds m and T.vl holds k0
     // until phase 2 turns them into densities and volumes.
-    for (int t = tid; t < RNN; t += RTX * RTY) {
-        const int i = T.ci0 + t % RNW, j = T.cj0 + t / RNW;
+    RowCol<RNW, RTX * RTY> rs0(tid);
+    for (int t = tid; t < RNN; t += RTX * RTY, rs0.step()) {
+        const int i = T.ci0 + rs0.c, j = T.cj0 + rs0.r;
         double hx = 0.0, hy = 0.0;
         if (in(d.win_n, i, j)) {  // = [-2, n+2] on a whole mesh
             const int n = ix(d, i, j);
@@ -1037,8 +1056,9 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         T.hx[t] = hx;
         T.hy[t] = hy;
     }
-    for (int t = tid; t < RNC; t += RTX * RTY) {
-        const int i = T.ci0 + t % RCW, j = T.cj0 + t / RCW;
+    RowCol<RCW, RTX * RTY> rs1(tid);
+    for (int t = tid; t < RNC; t += RTX * RTY, rs1.step()) {
+        const int i = T.ci0 + rs1.c, j = T.cj0 + rs1.r;
         if (!in(d.win_c, i, j)) continue;  // = [-2, n+2) on a whole mesh
         const int c = ix(d, i, j);
 #pragma unroll
@@ -1056,8 +1076,9 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     __syncthreads();
     // ---- phase 1, node items: corner flux, axis geometry, face flux volumes
     // (cf_corner_flux remap.cpp:16-25, make_axis_geom :296-322, :744-767)
-    for (int t = tid; t < RNN; t += RTX * RTY) {
-        const int i = T.ci0 + t % RNW, j = T.cj0 + t / RNW;
+    RowCol<RNW, RTX * RTY> rs2(tid);
+    for (int t = tid; t < RNN; t += RTX * RTY, rs2.step()) {
+        const int i = T.ci0 + rs2.c, j = T.cj0 + rs2.r;
         double cfv = 0.0, fdx = 0.0, fdy = 0.0, fxv = 0.0, fyv = 0.0;
         int8_t sx = 0, sy = 0;
         if (in(d.win_n, i, j)) {
@@ -1098,8 +1119,9 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     __syncthreads();
     // ---- phase 2, cell items: Lagrangian volume, densities, centroids,
     // interfaces (remap.cpp:769-824)
-    for (int t = tid; t < RNC; t += RTX * RTY) {
-        const int i = T.ci0 + t % RCW, j = T.cj0 + t / RCW;
+    RowCol<RCW, RTX * RTY> rs3(tid);
+    for (int t = tid; t < RNC; t += RTX * RTY, rs3.step()) {
+        const int i = T.ci0 + rs3.c, j = T.cj0 + rs3.r;
         if (!in(d.win_c, i, j) || i + 1 >= d.win_n.i1 || j + 1 >= d.win_n.j1) continue;
         const int q00 = T.n(i, j), q10 = q00 + 1, q01 = q00 + RNW, q11 = q01 + 1;
         auto cterm = [&](int q, int ni, int nj) -> double {  // remap.cpp:775-785
@@ -1141,8 +1163,9 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     __syncthreads();
     // ---- face and corner fluxes of the tile, once each
     double dm[2], dme[2], dva[2];
-    for (int t = tid; t < NXF; t += RTX * RTY) {  // X faces ia in [i0, i0+RTX], rows [j0, j0+RTY)
-        const int ia = i0 + t % (RTX + 1), ic = j0 + t / (RTX + 1);
+    RowCol<RTX + 1, RTX * RTY> rs4(tid);
+    for (int t = tid; t < NXF; t += RTX * RTY, rs4.step()) {  // X faces ia in [i0, i0+RTX], rows [j0, j0+RTY)
+        const int ia = i0 + rs4.c, ic = j0 + rs4.r;
         dva[0] = dva[1] = 0.0;
         dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
         if (ia <= min(nx, rg.i1) && ic < min(ny, rg.j1)) {
@@ -1171,8 +1194,9 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
             T.fy[2][a][t] = dva[a];
         }
     }
-    for (int t = tid; t < NCF; t += RTX * RTY) {  // corner nodes [i0, i0+RTX] x [j0, j0+RTY]
-        const int ni = i0 + t % (RTX + 1), nj = j0 + t / (RTX + 1);
+    RowCol<RTX + 1, RTX * RTY> rs5(tid);
+    for (int t = tid; t < NCF; t += RTX * RTY, rs5.step()) {  // corner nodes [i0, i0+RTX] x [j0, j0+RTY]
+        const int ni = i0 + rs5.c, nj = j0 + rs5.r;
         dva[0] = dva[1] = 0.0;
         dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
         const int ni1 = min(nx, rg.i1), nj1 = min(ny, rg.j1);
