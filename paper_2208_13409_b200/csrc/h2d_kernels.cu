@@ -1370,9 +1370,68 @@ __device__ __forceinline__ void sliver_offset(int lane, int& di, int& dj, int& r
     }
 }
 
+// candidate data of one ring lane for material a (see sliver_one)
+struct SliverCand {
+    double mv, kv, mev, mcv;
+};
+__device__ __forceinline__ SliverCand sliver_load(const Dev& d, int a, bool inb, int nc) {
+    SliverCand q{0.0, -1.0, 0.0, 0.0};
+    if (inb) {
+        q.mv = d.nm[a][nc];
+        q.kv = d.nk[a][nc];
+        q.mev = d.me[a][nc];
+        q.mcv = d.mcell[nc];
+    }
+    return q;
+}
+
+__device__ __forceinline__ void sliver_apply(const Dev& d, int a, int si, int sj, int sc, int lane, int ring, int nc,
+                                             const SliverCand& q, double smv, double smev) {
+    const bool cand = q.kv > -1.0 && !(q.mv <= 0.0);  // the reference skips m <= 0, then needs k > bk
+    // lexicographic min of (ring, -k, lane) over candidates
+    int br = cand ? ring : 4, bl = lane;
+    double bkv = q.kv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        const double ok = __shfl_xor_sync(0xffffffffu, bkv, o);
+        const bool take = orr < br || (orr == br && br < 4 && (ok > bkv || (ok == bkv && ol < bl)));
+        if (take) {
+            br = orr;
+            bl = ol;
+            bkv = ok;
+        }
+    }
+    const bool found = br < 4;
+    const double mcar = __shfl_sync(0xffffffffu, q.mv, found ? bl : 0);
+    if (found && mcar + smv > 0.0) {
+        if (lane == bl) {
+            const double nmv = q.mv + smv;
+            const double nme = q.mev + smev;
+            d.nm[a][nc] = nmv;
+            d.me[a][nc] = nme;
+            d.ne[a][nc] = nme / nmv;
+            d.mcell[nc] = q.mcv + smv;
+        }
+    } else if (lane == 0) {
+        if (own_cell(d, si, sj)) d.ctl->step_fix += 1;
+        const int b = 1 - a;
+        const double nmv = d.nm[b][sc] + smv;
+        const double nme = d.me[b][sc] + smev;
+        d.nm[b][sc] = nmv;
+        d.me[b][sc] = nme;
+        d.ne[b][sc] = nme / nmv;
+        d.mcell[sc] += smv;
+    }
+    __syncwarp();
+}
+
+// One pending cell: the flag byte, the sliver masses and the ring candidates
+// of BOTH materials are loaded in one round (independent loads); a cell with
+// two slivers reloads material 1's candidates after material 0 is applied.
 __device__ __forceinline__ void sliver_one(const Dev& d, const Rng& rg, int si, int sj, int lane) {
     const int sc = ix(d, si, sj);
-    const unsigned fl = d.sliver[sc];
     int di = 0, dj = 0, ring = 3;
     if (lane < 24) sliver_offset(lane, di, dj, ring);
     int ni = si + di, nj = sj + dj;
@@ -1380,56 +1439,14 @@ __device__ __forceinline__ void sliver_one(const Dev& d, const Rng& rg, int si, 
     if (d.per_y) nj = (nj + 2 * d.ny) % d.ny;
     const bool inb = lane < 24 && ni >= 0 && ni < d.nx && nj >= 0 && nj < d.ny && in(rg, ni, nj);
     const int nc = inb ? ix(d, ni, nj) : sc;
-#pragma unroll 1
-    for (int a = 0; a < 2; ++a) {
-        if (!(fl & (1u << a))) continue;
-        const double smv = d.slm[a][sc], smev = d.slme[a][sc];
-        double mv = 0.0, kv = -1.0, mev = 0.0, mcv = 0.0;
-        bool cand = false;
-        if (inb) {  // the carrier's me and mcell are loaded with the search (one latency)
-            mv = d.nm[a][nc];
-            kv = d.nk[a][nc];
-            mev = d.me[a][nc];
-            mcv = d.mcell[nc];
-            cand = !(mv <= 0.0) && kv > -1.0;  // the reference skips m <= 0, then needs k > bk
-        }
-        // lexicographic min of (ring, -k, lane) over candidates
-        int br = cand ? ring : 4, bl = lane;
-        double bkv = kv;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const int orr = __shfl_xor_sync(0xffffffffu, br, o);
-            const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-            const double ok = __shfl_xor_sync(0xffffffffu, bkv, o);
-            const bool take = orr < br || (orr == br && br < 4 && (ok > bkv || (ok == bkv && ol < bl)));
-            if (take) {
-                br = orr;
-                bl = ol;
-                bkv = ok;
-            }
-        }
-        const bool found = br < 4;
-        const double mcar = __shfl_sync(0xffffffffu, mv, found ? bl : 0);
-        if (found && mcar + smv > 0.0) {
-            if (lane == bl) {
-                const double nmv = mv + smv;
-                const double nme = mev + smev;
-                d.nm[a][nc] = nmv;
-                d.me[a][nc] = nme;
-                d.ne[a][nc] = nme / nmv;
-                d.mcell[nc] = mcv + smv;
-            }
-        } else if (lane == 0) {
-            if (own_cell(d, si, sj)) d.ctl->step_fix += 1;
-            const int b = 1 - a;
-            const double nmv = d.nm[b][sc] + smv;
-            const double nme = d.me[b][sc] + smev;
-            d.nm[b][sc] = nmv;
-            d.me[b][sc] = nme;
-            d.ne[b][sc] = nme / nmv;
-            d.mcell[sc] += smv;
-        }
-        __syncwarp();
+    const unsigned fl = d.sliver[sc];
+    const double sm0 = d.slm[0][sc], sme0 = d.slme[0][sc], sm1 = d.slm[1][sc], sme1 = d.slme[1][sc];
+    const SliverCand q0 = sliver_load(d, 0, inb, nc);
+    SliverCand q1 = sliver_load(d, 1, inb, nc);
+    if (fl & 1u) sliver_apply(d, 0, si, sj, sc, lane, ring, nc, q0, sm0, sme0);
+    if (fl & 2u) {
+        if (fl & 1u) q1 = sliver_load(d, 1, inb, nc);  // material 0 may have moved a carrier's mcell
+        sliver_apply(d, 1, si, sj, sc, lane, ring, nc, q1, sm1, sme1);
     }
 }
 
@@ -1451,19 +1468,34 @@ __global__ void k_slivers(Dev d) {
                 const int jr = ((rw0 + L) << 5) + __ffs(bits) - 1;
                 bits &= bits - 1;
                 unsigned* seg = d.sl_segs + (size_t)jr * nwx;
-                for (int w0 = 0; w0 < nwx; w0 += 32) {
-                    const int w = w0 + lane;
-                    const unsigned sb = w < nwx ? seg[w] : 0u;
-                    if (sb) seg[w] = 0u;
-                    unsigned nz = __ballot_sync(0xffffffffu, sb != 0u);
-                    while (nz) {
-                        const int L2 = __ffs(nz) - 1;
-                        nz &= nz - 1;
-                        unsigned cb = __shfl_sync(0xffffffffu, sb, L2);
-                        while (cb) {
-                            const int i = rg.i0 + ((w0 + L2) << 5) + __ffs(cb) - 1;
-                            cb &= cb - 1;
-                            sliver_one(d, rg, i, rg.j0 + jr, lane);
+                // 256 segment words per pass, 8 consecutive words per lane
+                // loaded together (one latency per row); lane-major = row order
+                for (int wb = 0; wb < nwx; wb += 256) {
+                    unsigned w[8];
+                    unsigned any = 0u;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int wi = wb + lane * 8 + k;
+                        w[k] = wi < nwx ? seg[wi] : 0u;
+                        any |= w[k];
+                    }
+                    if (any) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            if (w[k]) seg[wb + lane * 8 + k] = 0u;
+                    }
+                    unsigned lanes = __ballot_sync(0xffffffffu, any != 0u);
+                    while (lanes) {
+                        const int L2 = __ffs(lanes) - 1;
+                        lanes &= lanes - 1;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            unsigned cb = __shfl_sync(0xffffffffu, w[k], L2);
+                            while (cb) {
+                                const int i = rg.i0 + ((wb + L2 * 8 + k) << 5) + __ffs(cb) - 1;
+                                cb &= cb - 1;
+                                sliver_one(d, rg, i, rg.j0 + jr, lane);
+                            }
                         }
                     }
                 }
