@@ -1552,7 +1552,7 @@ __device__ __forceinline__ void dual_face_item(const Dev& d, int i, int j) {
     const int s = ix(d, i, j);
     (AX ? d.dfx_x : d.dfy_x)[s] = mx;
     (AX ? d.dfx_y : d.dfy_y)[s] = my;
-    d.dflag[AX ? 0 : 1][s] = on;
+    if (d.per_x || d.per_y) d.dflag[AX ? 0 : 1][s] = on;  // only the periodic gather reads flags
 }
 
 // Dual-mesh corner exchanges, remap.cpp:1000-1069: iteration (i, j), both
@@ -1646,13 +1646,13 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
         const bool on = dual_corner_pair(d, i, j, pr, cx, cy);
         d.dc_x[pr][s] = cx;
         d.dc_y[pr][s] = cy;
-        d.dflag[2 + pr][s] = on;
+        if (d.per_x || d.per_y) d.dflag[2 + pr][s] = on;
     }
 }
 
 // All dual-mesh items of one unique node (i, j): its X and Y dual faces and
 // its two diagonal corner exchanges (remap.cpp:995-1069).
-__global__ void k_dual_items(Dev d) {
+__global__ void __launch_bounds__(128, 8) k_dual_items(Dev d) {
     if (halted(d.ctl)) return;
     int i, j;
     tid2(i, j, d.r_dual.i0, d.r_dual.j0);
@@ -1676,19 +1676,23 @@ __global__ void k_node_update_walls(Dev d) {
     const int s = ix(d, i, j);
     const int sxr = ix(d, i + 1, j), syt = ix(d, i, j + 1);
     const int pp = ix(d, i - 1, j - 1), pm = ix(d, i - 1, j + 1);
-    // flags of items outside the unique node range were never set: guard
-    const bool fxp = i >= 1 && d.dflag[0][s], fxm = i + 1 <= nx && d.dflag[0][sxr];
-    const bool fyp = j >= 1 && d.dflag[1][s], fym = j + 1 <= ny && d.dflag[1][syt];
-    const bool fpp = i >= 1 && j >= 1 && d.dflag[2][pp], fo0 = d.dflag[2][s], fo1 = d.dflag[3][s];
-    const bool fpm = i >= 1 && j + 1 <= ny && d.dflag[3][pm];
+    // Items outside the unique node range were never written: index guards.
+    // A skipped item (zero dual mass flux, inactive corner) is stored as
+    // exactly 0.0, and adding +-0.0 leaves the accumulator unchanged (it
+    // starts at +0.0 and a sum is -0.0 only if both terms are), so the
+    // reference's skip needs no flag here.
+    const bool fxp = i >= 1, fxm = i + 1 <= nx, fyp = j >= 1, fym = j + 1 <= ny;
+    const bool fpp = i >= 1 && j >= 1, fpm = i >= 1 && j + 1 <= ny;
     double ax = 0.0, ay = 0.0;
     if (fxp) { ax += d.dfx_x[s]; ay += d.dfx_y[s]; }
     if (fxm) { ax += -d.dfx_x[sxr]; ay += -d.dfx_y[sxr]; }
     if (fyp) { ax += d.dfy_x[s]; ay += d.dfy_y[s]; }
     if (fym) { ax += -d.dfy_x[syt]; ay += -d.dfy_y[syt]; }
     if (fpp) { ax += -d.dc_x[0][pp]; ay += -d.dc_y[0][pp]; }
-    if (fo0) { ax += d.dc_x[0][s]; ay += d.dc_y[0][s]; }
-    if (fo1) { ax += d.dc_x[1][s]; ay += d.dc_y[1][s]; }
+    ax += d.dc_x[0][s];
+    ay += d.dc_y[0][s];
+    ax += d.dc_x[1][s];
+    ay += d.dc_y[1][s];
     if (fpm) { ax += -d.dc_x[1][pm]; ay += -d.dc_y[1][pm]; }
     const int c00 = pp, c10 = ix(d, i, j - 1), c01 = ix(d, i - 1, j);
     double l00 = 0.0, l10 = 0.0, l01 = 0.0, l11 = 0.0;  // make_work's mcell (remap.cpp:133-138)
