@@ -702,17 +702,28 @@ constexpr int RCW = RTX + 4, RCH = RTY + 4;  // cell region [i0-2, i0+RTX+2)
 constexpr int RNW = RTX + 5, RNH = RTY + 5;  // node region [i0-2, i0+RTX+2]
 constexpr int RNN = RNW * RNH, RNC = RCW * RCH;
 constexpr int NXF = (RTX + 1) * RTY, NYF = RTX * (RTY + 1), NCF = (RTX + 1) * (RTY + 1);
-constexpr int RCELL1 = 5, RCELL2 = 12;  // cell arrays per material count
+constexpr int NIT = NCF > NXF ? (NCF > NYF ? NCF : NYF) : (NXF > NYF ? NXF : NYF);  // item buffer
+constexpr int RCELL1 = 5, RCELL2 = 10;  // cell arrays per material count
 
 template <int NM>
 struct Tile {
     int ci0, cj0;  // origin of both regions: (i0 - 2, j0 - 2)
-    double *hx, *hy, *cf, *fdx, *fdy, *fxdv, *fydv;  // nodes
-    int8_t *sx, *sy;
-    double *vl, *rho[2], *el[2], *kk[2], *xl2x, *xl2y, *ifd, *nrx, *nry;  // cells
-    double *fx[3][2], *fy[3][2], *fc[3][2];  // flux items: dm, dme, dva per material
+    double *hx, *hy, *fdx, *fdy, *fxdv, *fydv;  // nodes
+    double *vl, *rho[2], *el[2], *kk[2], *xl2x, *xl2y, *ifd;  // cells
+    // flux items of one sub-phase (X faces, then Y faces, then corners share
+    // the buffer): dm, dme, dva per material
+    double* it[3][2];
     __device__ __forceinline__ int c(int i, int j) const { return (i - ci0) + (j - cj0) * RCW; }
     __device__ __forceinline__ int n(int i, int j) const { return (i - ci0) + (j - cj0) * RNW; }
+    // cf_corner_flux (remap.cpp:16-25) at region node q, recomputed from the
+    // staged u_half (zero outside the window); sx / sy are meaningful only
+    // when the returned volume is nonzero
+    __device__ __forceinline__ double cfv(int q, double dt, int& sx, int& sy) const {
+        const double ddx = hx[q] * dt, ddy = hy[q] * dt;
+        sx = ddx > 0.0 ? 1 : -1;
+        sy = ddy > 0.0 ? 1 : -1;
+        return fabs(ddx * ddy);
+    }
     // make_axis_geom (remap.cpp:315-320) from the face-mean displacements
     __device__ __forceinline__ double xlcx(const Dev& d, int i, int j) const {
         const int q = n(i, j);
@@ -734,7 +745,7 @@ struct Tile {
 
 template <int NM>
 constexpr size_t remap_smem_bytes() {
-    return sizeof(double) * (7 * RNN + (NM == 2 ? RCELL2 : RCELL1) * RNC + 3 * NM * (NXF + NYF + NCF)) + 2 * RNN + 64;
+    return sizeof(double) * (6 * RNN + (NM == 2 ? RCELL2 : RCELL1) * RNC + 3 * NM * NIT) + 64;
 }
 
 template <int NM>
@@ -750,7 +761,6 @@ __device__ __forceinline__ Tile<NM> carve_tile(char* base, int ci0, int cj0) {
     };
     T.hx = take(RNN);
     T.hy = take(RNN);
-    T.cf = take(RNN);
     T.fdx = take(RNN);
     T.fdy = take(RNN);
     T.fxdv = take(RNN);
@@ -766,18 +776,9 @@ __device__ __forceinline__ Tile<NM> carve_tile(char* base, int ci0, int cj0) {
         T.kk[0] = take(RNC);
         T.kk[1] = take(RNC);
         T.ifd = take(RNC);
-        T.nrx = take(RNC);
-        T.nry = take(RNC);
     }
     for (int k = 0; k < 3; ++k)
-        for (int a = 0; a < NM; ++a) {
-            T.fx[k][a] = take(NXF);
-            T.fy[k][a] = take(NYF);
-            T.fc[k][a] = take(NCF);
-        }
-    int8_t* b = reinterpret_cast<int8_t*>(p);
-    T.sx = b;
-    T.sy = b + RNN;
+        for (int a = 0; a < NM; ++a) T.it[k][a] = take(NIT);
     return T;
 }
 
@@ -791,7 +792,8 @@ __device__ __forceinline__ void split_flux_t(const Dev& d, const Tile<NM>& T, in
     const int c = T.c(di, dj);
     const double k0 = T.kk[0][c];
     if (is_mixed(k0)) {
-        const double nx = T.nrx[c], ny = T.nry[c], dd = T.ifd[c];
+        const int g = ix(d, di, dj);  // mixed donors only: the normal from HBM (L2)
+        const double nx = d.nrx[g], ny = d.nry[g], dd = T.ifd[c];
         const double cx = d.x0 + (di + 0.5) * d.dx, cy = d.y0 + (dj + 0.5) * d.dy;
         const double lox = cx - 0.5 * d.dx + T.fdx[T.n(di, dj)], loy = cy - 0.5 * d.dy + T.fdy[T.n(di, dj)];
         const double hix = cx + 0.5 * d.dx + T.fdx[T.n(di + 1, dj)];
@@ -896,11 +898,11 @@ template <int NM>
 __device__ __forceinline__ double corner_item_t(const Dev& d, const Tile<NM>& T, int i, int j, double dt,
                                                 double* odm, double* odme, double* odva) {
     const int qn = T.n(i, j);
-    const double cdv = T.cf[qn];
+    int sx, sy;
+    const double cdv = T.cfv(qn, dt, sx, sy);
     double dva[2] = {0.0, 0.0}, rfv[2] = {0.0, 0.0}, efv[2] = {0.0, 0.0};
     double dmtot = 0.0;
     if (cdv != 0.0) {
-        const int sx = T.sx[qn], sy = T.sy[qn];
         const int di = sx > 0 ? i - 1 : i, dj = sy > 0 ? j - 1 : j;
         const double npx = d.x0 + i * d.dx, npy = d.y0 + j * d.dy;
         const double ddx = dt * T.hx[qn], ddy = dt * T.hy[qn];
@@ -1027,7 +1029,7 @@ __global__ void k_ghost_multi(Dev d, FieldList cells, FieldList nodes, int flux,
 }
 
 template <int NM>
-__global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
+__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d) {
     extern __shared__ __align__(16) char smem[];
     __shared__ int s_halt;
     const int tid = threadIdx.x;
@@ -1068,10 +1070,6 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
             if (NM == 2) T.kk[a][t] = d.k[a][c];
         }
         if (NM == 1) T.vl[t] = d.k[0][c];
-        if (NM == 2) {
-            T.nrx[t] = d.nrx[c];
-            T.nry[t] = d.nry[c];
-        }
     }
     __syncthreads();
     // ---- phase 1, node items: corner flux, axis geometry, face flux volumes
@@ -1079,18 +1077,10 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
     RowCol<RNW, RTX * RTY> rs2(tid);
     for (int t = tid; t < RNN; t += RTX * RTY, rs2.step()) {
         const int i = T.ci0 + rs2.c, j = T.cj0 + rs2.r;
-        double cfv = 0.0, fdx = 0.0, fdy = 0.0, fxv = 0.0, fyv = 0.0;
-        int8_t sx = 0, sy = 0;
+        double fdx = 0.0, fdy = 0.0, fxv = 0.0, fyv = 0.0;
         if (in(d.win_n, i, j)) {
             const double hx = T.hx[t], hy = T.hy[t];
-            const double ddx = hx * dt, ddy = hy * dt;
-            cfv = fabs(ddx * ddy);
-            if (cfv == 0.0) {
-                cfv = 0.0;
-            } else {
-                sx = ddx > 0.0 ? 1 : -1;
-                sy = ddy > 0.0 ? 1 : -1;
-            }
+            const double cfv = fabs((hx * dt) * (hy * dt));
             if (cfv > kCflFrac * cv && own_node(d, i, j)) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
             // faces on the region's last node row / column feed no region cell
             if (j < ny + G && j < T.cj0 + RNH - 1 && j + 1 < d.win_n.j1) {
@@ -1108,9 +1098,6 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
                 if (fabs(fyv) > kCflFrac * cv && own_yface(d, i, j)) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
             }
         }
-        T.cf[t] = cfv;
-        T.sx[t] = sx;
-        T.sy[t] = sy;
         T.fdx[t] = fdx;
         T.fdy[t] = fdy;
         T.fxdv[t] = fxv;
@@ -1125,9 +1112,9 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         if (!in(d.win_c, i, j) || i + 1 >= d.win_n.i1 || j + 1 >= d.win_n.j1) continue;
         const int q00 = T.n(i, j), q10 = q00 + 1, q01 = q00 + RNW, q11 = q01 + 1;
         auto cterm = [&](int q, int ni, int nj) -> double {  // remap.cpp:775-785
-            const double dv = T.cf[q];
+            int csx, csy;
+            const double dv = T.cfv(q, dt, csx, csy);
             if (dv == 0.0) return 0.0;
-            const int csx = T.sx[q], csy = T.sy[q];
             const int di = csx > 0 ? ni - 1 : ni, dj = csy > 0 ? nj - 1 : nj;
             if (di == i && dj == j) return dv;
             const int ri = csx > 0 ? ni : ni - 1, rj = csy > 0 ? nj : nj - 1;
@@ -1153,7 +1140,8 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
             double dd = 0.0;
             if (is_mixed(k0)) {
                 const double cx = d.x0 + (i + 0.5) * d.dx, cy = d.y0 + (j + 0.5) * d.dy;
-                dd = place_interface(k0, T.nrx[t], T.nry[t], cx - 0.5 * d.dx + T.fdx[q00],
+                const int g = ix(d, i, j);
+                dd = place_interface(k0, d.nrx[g], d.nry[g], cx - 0.5 * d.dx + T.fdx[q00],
                                      cy - 0.5 * d.dy + T.fdy[q00], cx + 0.5 * d.dx + T.fdx[q10],
                                      cy + 0.5 * d.dy + T.fdy[q01]);
             }
@@ -1161,7 +1149,39 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         }
     }
     __syncthreads();
-    // ---- face and corner fluxes of the tile, once each
+    // ---- flux items, each computed once, in three sub-phases sharing one
+    // shared-memory buffer (X faces, Y faces, corners); after each, every
+    // cell adds that sub-phase's terms in the reference order (App. C item 3):
+    // X face i (+), i+1 (-), Y face j (+), j+1 (-), corners row-major
+    const int tx = tid % RTX, ty = tid / RTX;
+    const int i = i0 + tx, j = j0 + ty;
+    const bool act = in(rg, i, j);
+    const int c = ix(d, i, j);
+    const int tc = T.c(i, j);
+    double m[2], me[2], va[2];
+    if (act) {
+        const double vl = T.vl[tc];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            const double m0 = d.m[a][c];
+            m[a] = m0;
+            me[a] = m0 * T.el[a][tc];
+            va[a] = d.k[a][c] * vl;
+        }
+    }
+    auto add = [&](int a, int q, bool neg) {  // the skip of remap.cpp:860,929
+        const double dv = T.it[2][a][q];
+        if (dv == 0.0) return;
+        if (neg) {
+            m[a] += -T.it[0][a][q];
+            me[a] += -T.it[1][a][q];
+            va[a] += -dv;
+        } else {
+            m[a] += T.it[0][a][q];
+            me[a] += T.it[1][a][q];
+            va[a] += dv;
+        }
+    };
     double dm[2], dme[2], dva[2];
     RowCol<RTX + 1, RTX * RTY> rs4(tid);
     for (int t = tid; t < NXF; t += RTX * RTY, rs4.step()) {  // X faces ia in [i0, i0+RTX], rows [j0, j0+RTY)
@@ -1174,11 +1194,21 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         }
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
-            T.fx[0][a][t] = dm[a];
-            T.fx[1][a][t] = dme[a];
-            T.fx[2][a][t] = dva[a];
+            T.it[0][a][t] = dm[a];
+            T.it[1][a][t] = dme[a];
+            T.it[2][a][t] = dva[a];
         }
     }
+    __syncthreads();
+    if (act) {
+        const int xl = tx + ty * (RTX + 1);
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            add(a, xl, false);
+            add(a, xl + 1, true);
+        }
+    }
+    __syncthreads();
     for (int t = tid; t < NYF; t += RTX * RTY) {  // Y faces: columns [i0, i0+RTX), ja in [j0, j0+RTY]
         const int ic = i0 + t % RTX, ja = j0 + t / RTX;
         dva[0] = dva[1] = 0.0;
@@ -1189,11 +1219,21 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         }
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
-            T.fy[0][a][t] = dm[a];
-            T.fy[1][a][t] = dme[a];
-            T.fy[2][a][t] = dva[a];
+            T.it[0][a][t] = dm[a];
+            T.it[1][a][t] = dme[a];
+            T.it[2][a][t] = dva[a];
         }
     }
+    __syncthreads();
+    if (act) {
+        const int yb = tx + ty * RTX;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            add(a, yb, false);
+            add(a, yb + RTX, true);
+        }
+    }
+    __syncthreads();
     RowCol<RTX + 1, RTX * RTY> rs5(tid);
     for (int t = tid; t < NCF; t += RTX * RTY, rs5.step()) {  // corner nodes [i0, i0+RTX] x [j0, j0+RTY]
         const int ni = i0 + rs5.c, nj = j0 + rs5.r;
@@ -1206,73 +1246,30 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_remap_tile(Dev d) {
         }
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
-            T.fc[0][a][t] = dm[a];
-            T.fc[1][a][t] = dme[a];
-            T.fc[2][a][t] = dva[a];
+            T.it[0][a][t] = dm[a];
+            T.it[1][a][t] = dme[a];
+            T.it[2][a][t] = dva[a];
         }
     }
     __syncthreads();
-    // ---- gather in reference order (App. C item 3)
-    const int tx = tid % RTX, ty = tid / RTX;
-    const int i = i0 + tx, j = j0 + ty;
-    if (!in(rg, i, j)) return;
+    if (!act) return;
     const bool own = own_cell(d, i, j);
-    const int c = ix(d, i, j);
-    const int tc = T.c(i, j);
-    const int xl = tx + ty * (RTX + 1), xr = xl + 1;
-    const int yb = tx + ty * RTX, yt = yb + RTX;
-    const int cq[4] = {tx + ty * (RTX + 1), tx + 1 + ty * (RTX + 1), tx + (ty + 1) * (RTX + 1),
-                       tx + 1 + (ty + 1) * (RTX + 1)};
-    const int ndi[4] = {i, i + 1, i, i + 1}, ndj[4] = {j, j, j + 1, j + 1};
-    const double vl = T.vl[tc];
-    double m[2], me[2], va[2];
-#pragma unroll
-    for (int a = 0; a < NM; ++a) {
-        const double m0 = d.m[a][c];
-        double mm = m0, mme = m0 * T.el[a][tc], vv = d.k[a][c] * vl;
-        if (T.fx[2][a][xl] != 0.0) {
-            mm += T.fx[0][a][xl];
-            mme += T.fx[1][a][xl];
-            vv += T.fx[2][a][xl];
-        }
-        if (T.fx[2][a][xr] != 0.0) {
-            mm += -T.fx[0][a][xr];
-            mme += -T.fx[1][a][xr];
-            vv += -T.fx[2][a][xr];
-        }
-        if (T.fy[2][a][yb] != 0.0) {
-            mm += T.fy[0][a][yb];
-            mme += T.fy[1][a][yb];
-            vv += T.fy[2][a][yb];
-        }
-        if (T.fy[2][a][yt] != 0.0) {
-            mm += -T.fy[0][a][yt];
-            mme += -T.fy[1][a][yt];
-            vv += -T.fy[2][a][yt];
-        }
+    {
+        const int cq[4] = {tx + ty * (RTX + 1), tx + 1 + ty * (RTX + 1), tx + (ty + 1) * (RTX + 1),
+                           tx + 1 + (ty + 1) * (RTX + 1)};
+        const int ndi[4] = {i, i + 1, i, i + 1}, ndj[4] = {j, j, j + 1, j + 1};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const double dv = T.fc[2][a][cq[q]];
-            if (dv == 0.0) continue;
-            const int qn = T.n(ndi[q], ndj[q]);
-            const int csx = T.sx[qn], csy = T.sy[qn];
+            int csx, csy;
+            const double cd = T.cfv(T.n(ndi[q], ndj[q]), dt, csx, csy);
+            if (cd == 0.0) continue;  // no corner flux at this node (its items are all zero)
             const int di = csx > 0 ? ndi[q] - 1 : ndi[q], dj = csy > 0 ? ndj[q] - 1 : ndj[q];
-            if (di == i && dj == j) {
-                mm += -T.fc[0][a][cq[q]];
-                mme += -T.fc[1][a][cq[q]];
-                vv += -dv;
-            } else {
-                const int ri = csx > 0 ? ndi[q] : ndi[q] - 1, rj = csy > 0 ? ndj[q] : ndj[q] - 1;
-                if (ri == i && rj == j) {
-                    mm += T.fc[0][a][cq[q]];
-                    mme += T.fc[1][a][cq[q]];
-                    vv += dv;
-                }
-            }
+            const int ri = csx > 0 ? ndi[q] : ndi[q] - 1, rj = csy > 0 ? ndj[q] : ndj[q] - 1;
+            const bool donor = di == i && dj == j;
+            if (!donor && !(ri == i && rj == j)) continue;
+#pragma unroll
+            for (int a = 0; a < NM; ++a) add(a, cq[q], donor);
         }
-        m[a] = mm;
-        me[a] = mme;
-        va[a] = vv;
     }
     // finalize_cells, per-cell part
     double k[2] = {1.0, 0.0};
