@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
 // chip; the API path (h2d_lagrange_step) keeps the two-kernel form because
 // it returns Q.
 template <int NM>
-__global__ void __launch_bounds__(LTX * LTY) k_lag_fused(Dev d) {
+__global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
     constexpr int CW = LTX + 2, CH = LTY + 2, NC = CW * CH, NN = (LTX + 1) * (LTY + 1);
     __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC];
     __shared__ double shx[NN], shy[NN];
@@ -2030,7 +2030,7 @@ __global__ void k_global_xfer(Dev d, double* buf, Rng r, double* px, double* py,
 // (harness.cpp:347-358) plus the wave speed of the next step's cfl_dt
 // (harness.cpp:293-310), so the State is read once.
 template <int NM>
-__global__ void __launch_bounds__(256) k_post(Dev d, int run_loop) {
+__global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
     __shared__ unsigned long long sw[8];
     __shared__ int s_halt;
     if (threadIdx.x == 0 && threadIdx.y == 0) s_halt = halted(d.ctl);
