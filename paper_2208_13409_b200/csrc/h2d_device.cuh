@@ -172,6 +172,16 @@ H2D_DEV double sound(const Dev& d, int a, double rho, double p, bool& bad) {
     return sqrt(c2);
 }
 
+// Programmatic dependent launch: every kernel first waits for the grids it
+// depends on (a no-op when launched without the PDL attribute) and at once
+// lets its dependents launch, so a dependent grid's CTAs are resident and
+// waiting while this grid's last wave drains (hides launch gaps and tails in
+// the run-loop graph).
+H2D_DEV void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // van_leer, reconstruct.cpp:10-14
 H2D_DEV double van_leer(double r) {
     if (!(r > 0.0)) return 0.0;

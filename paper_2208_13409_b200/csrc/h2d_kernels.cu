@@ -40,6 +40,7 @@ __device__ __forceinline__ bool own_yface(const Dev& d, int i, int j) {  // cell
 // Start of a step or of a single API phase. mode: 0 = run-loop step (applies
 // harness.cpp:390-391), 1 = API call with host dt, 2 = API cfl_dt only.
 __global__ void k_begin(Ctl* c, int mode, double host_dt) {
+    pdl_enter();
     if (c->err_key != kNoErr || c->done) return;
     c->wmax_bits = 0ull;
     c->kviol_bits = 0ull;
@@ -65,6 +66,7 @@ __global__ void k_begin(Ctl* c, int mode, double host_dt) {
 // per block on the bit pattern (non-negative doubles order as integers).
 template <int NM>
 __global__ void k_cfl(Dev d, int into_next) {
+    pdl_enter();
     if (halted(d.ctl)) return;
     unsigned long long wb = 0ull;
     // owned interior cells (cfl_dt loops over the whole mesh; the blocks of a
@@ -125,6 +127,7 @@ __global__ void k_cfl(Dev d, int into_next) {
 
 // harness.cpp:311-312 and the run loop's dt = min(dt, t_end - t) (:395)
 __global__ void k_cfl_final(Ctl* c, double dx, double dy, int run_loop) {
+    pdl_enter();
     if (c->err_key != kNoErr || c->done) return;
     const double wmax = __longlong_as_double((long long)c->wmax_bits);
     if (!(wmax > 0.0) || !isfinite(wmax)) {
@@ -255,6 +258,7 @@ __device__ __forceinline__ void ghost_nodes_at(const Dev& d, const FieldList& fl
 // src: 0 = current state (API), 1 = next state (after a remap).
 template <int NM>
 __global__ void k_sync(Dev d, int next, int respect_halt) {
+    pdl_enter();
     if (respect_halt && halted(d.ctl)) return;
     int i, j;
     tid2(i, j, d.win_c.i0, d.win_c.j0);
@@ -312,6 +316,7 @@ __device__ __forceinline__ double quad_vol4(const Dev& d, double u00x, double u0
 // (lagrange.cpp:89-131, dh = 0.5*dt*u :251-255): one thread per cell.
 template <int NM>
 __global__ void k_lag_cells(Dev d) {
+    pdl_enter();
     if (halted(d.ctl)) return;
     int i, j;
     tid2(i, j, d.r_lagc.i0, d.r_lagc.j0);
@@ -404,6 +409,7 @@ struct RowCol {
 };
 template <int NM>
 __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_lag) {
+    pdl_enter();
     constexpr int NN = (LTX + 1) * (LTY + 1);
     __shared__ double shx[NN], shy[NN];
     __shared__ int s_halt;
@@ -487,6 +493,7 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
 // it returns Q.
 template <int NM>
 __global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
+    pdl_enter();
     constexpr int CW = LTX + 2, CH = LTY + 2, NC = CW * CH, NN = (LTX + 1) * (LTY + 1);
     __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC];
     __shared__ double shx[NN], shy[NN];
@@ -647,6 +654,7 @@ __global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
 // place (w.m = state m, w.e = e_lag, w.k = state k, w.me = m * e_lag), so the
 // flux threads never race with finalize writing the next State.
 __global__ void k_copy_u(Dev d) {
+    pdl_enter();
     if (halted(d.ctl)) return;
     int i, j;
     tid2(i, j, d.win_n.i0, d.win_n.j0);
@@ -1017,6 +1025,7 @@ __device__ __forceinline__ void flux_ghosts_at(const Dev& d, int t) {
 // (blockIdx.y = 1) and the face / corner mass-flux ghosts (blockIdx.y = 2) in
 // one launch; every write reads interior entries only.
 __global__ void k_ghost_multi(Dev d, FieldList cells, FieldList nodes, int flux, int respect_halt) {
+    pdl_enter();
     if (respect_halt && halted(d.ctl)) return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (blockIdx.y == 0) {
@@ -1030,6 +1039,7 @@ __global__ void k_ghost_multi(Dev d, FieldList cells, FieldList nodes, int flux,
 
 template <int NM>
 __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d) {
+    pdl_enter();
     extern __shared__ __align__(16) char smem[];
     __shared__ int s_halt;
     const int tid = threadIdx.x;
@@ -1448,6 +1458,7 @@ __device__ __forceinline__ void sliver_one(const Dev& d, const Rng& rg, int si, 
 }
 
 __global__ void k_slivers(Dev d) {
+    pdl_enter();
     if (halted(d.ctl)) return;
     const int lane = threadIdx.x;
     const Rng rg = d.r_gath;
@@ -1650,6 +1661,7 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
 // All dual-mesh items of one unique node (i, j): its X and Y dual faces and
 // its two diagonal corner exchanges (remap.cpp:995-1069).
 __global__ void __launch_bounds__(128, 8) k_dual_items(Dev d) {
+    pdl_enter();
     if (halted(d.ctl)) return;
     int i, j;
     tid2(i, j, d.r_dual.i0, d.r_dual.j0);
@@ -1665,6 +1677,7 @@ __global__ void __launch_bounds__(128, 8) k_dual_items(Dev d) {
 // (-), own pairs (+, +), corner (i-1, j+1, pair (1,-1)) (-) — then
 // apply_dual_update (remap.cpp:444-464) and the wall condition (:462).
 __global__ void k_node_update_walls(Dev d) {
+    pdl_enter();
     if (halted(d.ctl)) return;
     int i, j;
     tid2(i, j, d.r_node.i0, d.r_node.j0);
@@ -1715,6 +1728,7 @@ __global__ void k_node_update_walls(Dev d) {
 // the periodic copies (:458-461) folded in: thread per node (i, j) in
 // [0, nx] x [0, ny] computes the value of its source node.
 __global__ void k_node_update(Dev d) {
+    pdl_enter();
     if (halted(d.ctl)) return;
     int i, j;
     tid2(i, j, d.r_node.i0, d.r_node.j0);
@@ -1826,6 +1840,7 @@ __global__ void k_node_update(Dev d) {
 // refresh_normals_impl + youngs_normal (remap.cpp:102-114, vof.cpp:10-22)
 // on the next state's fractions; `api` = operate on the current state.
 __global__ void k_normals(Dev d, int api) {
+    pdl_enter();
     if (!api && halted(d.ctl)) return;
     int i, j;
     tid2(i, j, 0, 0);
@@ -1853,6 +1868,7 @@ __global__ void k_normals(Dev d, int api) {
 
 // Step commit: the remapped State becomes current (remap.cpp:1084-1085).
 __global__ void k_commit(Ctl* c, int advance) {
+    pdl_enter();
     if (c->err_key != kNoErr || c->done) return;
     if (advance) {
         c->time = c->time + c->dt;
@@ -1863,6 +1879,7 @@ __global__ void k_commit(Ctl* c, int advance) {
 
 // nan_scan, harness.cpp:347-358, on the committed state (the next buffers).
 __global__ void k_nan(Dev d) {
+    pdl_enter();
     if (halted(d.ctl)) return;
     int i, j;
     tid2(i, j, 0, 0);
@@ -1878,6 +1895,7 @@ __global__ void k_nan(Dev d) {
 
 // End of a successful run-loop step: counters and dt log.
 __global__ void k_finish(Ctl* c) {
+    pdl_enter();
     if (c->err_key != kNoErr || c->done) return;
     if (c->dt_log && c->steps_done < c->dt_log_cap) c->dt_log[c->steps_done] = c->dt;
     c->steps_done += 1;
@@ -1892,6 +1910,7 @@ __global__ void k_finish(Ctl* c) {
 // cfl_dt of the current State, whose wave-speed maximum and first error were
 // produced by the previous step's k_post (or k_cfl before the first step).
 __global__ void k_step_start(Ctl* c, double dx, double dy) {
+    pdl_enter();
     if (c->err_key != kNoErr || c->done) return;
     c->kviol_bits = 0ull;
     c->step_floor = 0;
@@ -1922,6 +1941,7 @@ __global__ void k_step_start(Ctl* c, double dx, double dy) {
 // (remap.cpp:1084-1085) unless an earlier phase failed; nan_scan errors come
 // after the commit (harness.cpp:402-409), so they still commit.
 __global__ void k_commit_finish(Ctl* c) {
+    pdl_enter();
     c->committed = 0;
     c->counted = 0;
     if (c->done) return;
@@ -1948,6 +1968,7 @@ __global__ void k_commit_finish(Ctl* c) {
 // Undo the last commit (block mode: another block failed in the same step
 // before its commit, so the decomposed State must stay at the previous step).
 __global__ void k_rollback(Ctl* c) {
+    pdl_enter();
     if (!c->committed) return;
     c->time = c->prev_time;
     c->step -= 1;
@@ -1966,6 +1987,7 @@ __global__ void k_rollback(Ctl* c) {
 // Copy a rectangle (global indices, half-open) of several planes to / from a
 // contiguous buffer: cell planes use `rc`, node planes `rn` (halo exchange).
 __global__ void k_rect_xfer(Dev d, FieldList cells, FieldList nodes, Rng rc, Rng rn, double* buf, int to_buf) {
+    pdl_enter();
     const int wc = rc.i1 - rc.i0, hc = rc.j1 - rc.j0, wn = rn.i1 - rn.i0, hn = rn.j1 - rn.j0;
     const long long ac = (long long)wc * hc, an = (long long)wn * hn;
     const long long total = ac * cells.n + an * nodes.n;
@@ -1998,6 +2020,7 @@ __global__ void k_rect_xfer(Dev d, FieldList cells, FieldList nodes, Rng rc, Rng
 // vec != 0: interleaved Vec2 split into x / y planes) — window uploads and
 // owned-region downloads in the global reference layout.
 __global__ void k_global_xfer(Dev d, double* buf, Rng r, double* px, double* py, int vec, int to_block) {
+    pdl_enter();
     const int w = r.i1 - r.i0, h = r.j1 - r.j0;
     const long long n = (long long)w * h;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
@@ -2031,6 +2054,7 @@ __global__ void k_global_xfer(Dev d, double* buf, Rng r, double* px, double* py,
 // (harness.cpp:293-310), so the State is read once.
 template <int NM>
 __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
+    pdl_enter();
     __shared__ unsigned long long sw[8];
     __shared__ int s_halt;
     if (threadIdx.x == 0 && threadIdx.y == 0) s_halt = halted(d.ctl);
@@ -2129,6 +2153,7 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
 
 // AoS <-> SoA staging for Vec2 fields (reference layout pitch W = n1 + 2G).
 __global__ void k_deinterleave(const double* src, double* x, double* y, int W, int H, int P) {
+    pdl_enter();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= W * H) return;
     const int r = t / W, col = t % W;
@@ -2136,6 +2161,7 @@ __global__ void k_deinterleave(const double* src, double* x, double* y, int W, i
     y[(size_t)r * P + col] = src[2 * (size_t)t + 1];
 }
 __global__ void k_interleave(double* dst, const double* x, const double* y, int W, int H, int P) {
+    pdl_enter();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= W * H) return;
     const int r = t / W, col = t % W;
@@ -2149,6 +2175,24 @@ __global__ void k_interleave(double* dst, const double* x, const double* y, int 
 static std::atomic<long long> g_launches{0};
 long long launch_count() { return g_launches.load(); }
 void add_launches(long long n) { g_launches += n; }
+// Launch with the programmatic-stream-serialization attribute (PDL): the
+// kernel may start while its predecessor drains and waits in pdl_enter().
+template <typename... KArgs, typename... Args>
+static void pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+    ++g_launches;
+}
+
 static dim3 blk2() { return dim3(32, 4); }
 static dim3 grid_rect(int w, int h) {
     const dim3 b = blk2();
@@ -2185,7 +2229,7 @@ static long long ghost_threads(const Dev& d) {
 void launch_ghost_multi(const Dev& d, const FieldList& cells, const FieldList& nodes, int flux, int respect_halt,
                         cudaStream_t s) {
     const dim3 g(nblk(ghost_threads(d), 256), 3);
-    { k_ghost_multi<<<g, 256, 0, s>>>(d, cells, nodes, flux, respect_halt); ++g_launches; }
+    pdl(k_ghost_multi, g, dim3(256), 0, s, d, cells, nodes, flux, respect_halt);
 }
 void launch_ghost_cells(const Dev& d, const FieldList& fl, cudaStream_t s) {
     FieldList none{};
@@ -2246,9 +2290,9 @@ void remap_init() {
 void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s) {
     const dim3 gp = tiles_of(d.r_sync, 32, 8);
     if (d.nmat == 2)
-        { k_post<2><<<gp, dim3(32, 8), 0, s>>>(d, run_loop); ++g_launches; }
+        pdl(k_post<2>, gp, dim3(32, 8), 0, s, d, run_loop);
     else
-        { k_post<1><<<gp, dim3(32, 8), 0, s>>>(d, run_loop); ++g_launches; }
+        pdl(k_post<1>, gp, dim3(32, 8), 0, s, d, run_loop);
     FieldList fg{};
     fg.n = 2;
     fg.f[0] = d.nnrx;
@@ -2265,9 +2309,9 @@ void launch_remap(const Dev& d, cudaStream_t s) { launch_remap_core(d, s); post_
 // run-loop Lagrangian phase: the fused kernel + ghost layers of u_half, u_lag, e_lag
 void launch_lagrange_run(const Dev& d, cudaStream_t s) {
     if (d.nmat == 2)
-        { k_lag_fused<2><<<tiles_of(d.r_lagn, LTX, LTY), LTX * LTY, 0, s>>>(d); ++g_launches; }
+        pdl(k_lag_fused<2>, tiles_of(d.r_lagn, LTX, LTY), dim3(LTX * LTY), 0, s, d);
     else
-        { k_lag_fused<1><<<tiles_of(d.r_lagn, LTX, LTY), LTX * LTY, 0, s>>>(d); ++g_launches; }
+        pdl(k_lag_fused<1>, tiles_of(d.r_lagn, LTX, LTY), dim3(LTX * LTY), 0, s, d);
     FieldList fn{};
     fn.n = 4;
     fn.f[0] = d.uhx;
@@ -2293,14 +2337,14 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
     remap_init();
     const dim3 gft = tiles_of(d.r_gath, RTX, RTY);
     if (d.nmat == 2)
-        { k_remap_tile<2><<<gft, RTX * RTY, remap_smem_bytes<2>(), s>>>(d); ++g_launches; }
+        pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d);
     else
-        { k_remap_tile<1><<<gft, RTX * RTY, remap_smem_bytes<1>(), s>>>(d); ++g_launches; }
+        pdl(k_remap_tile<1>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d);
 }
 
 // slivers + finalize_cells ghost fill + flux ghosts
 void launch_remap_slivers(const Dev& d, cudaStream_t s) {
-    if (d.nmat == 2) { k_slivers<<<1, 32, 0, s>>>(d); ++g_launches; }
+    if (d.nmat == 2) pdl(k_slivers, dim3(1), dim3(32), 0, s, d);
     // finalize_cells ghost fill (remap.cpp:227-233) + face / corner flux ghosts
     FieldList fl{};
     int q = 0;
@@ -2319,20 +2363,20 @@ void launch_remap_slivers(const Dev& d, cudaStream_t s) {
 // dual-mesh momentum remap (remap.cpp:993-1059)
 void launch_remap_dual(const Dev& d, cudaStream_t s) {
     if (d.remap_velocity) {
-        { k_dual_items<<<grid_of(d.r_dual), blk2(), 0, s>>>(d); ++g_launches; }
+        pdl(k_dual_items, grid_of(d.r_dual), blk2(), 0, s, d);
         if (d.per_x || d.per_y)  // periodic seams reorder the node sums: sorted gather
-            { k_node_update<<<grid_of(d.r_node), blk2(), 0, s>>>(d); ++g_launches; }
+            pdl(k_node_update, grid_of(d.r_node), blk2(), 0, s, d);
         else
-            { k_node_update_walls<<<grid_of(d.r_node), blk2(), 0, s>>>(d); ++g_launches; }
+            pdl(k_node_update_walls, grid_of(d.r_node), blk2(), 0, s, d);
     }
 }
 
 void launch_step(const Dev& d, cudaStream_t s) {
-    { k_step_start<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy); ++g_launches; }
+    pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
     launch_lagrange_run(d, s);
     launch_remap_core(d, s);
     post_and_ghosts(d, 1, s);
-    { k_commit_finish<<<1, 1, 0, s>>>(d.ctl); ++g_launches; }
+    pdl(k_commit_finish, dim3(1), dim3(1), 0, s, d.ctl);
 }
 
 void launch_step_start(const Dev& d, cudaStream_t s) { k_step_start<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy); ++g_launches; }
