@@ -1037,6 +1037,73 @@ __global__ void k_ghost_multi(Dev d, FieldList cells, FieldList nodes, int flux,
     }
 }
 
+// finalize_cells, per-cell part (remap.cpp:156-191) of cell (i, j) of a
+// remap tile: fractions, clipping, snapping, sliver capture, energies
+template <int NM>
+__device__ __forceinline__ void finalize_cell(const Dev& d, const Rng& rg, int i, int j, int c, int tx, bool own,
+                                              double* m, double* me, const double* va) {
+    double k[2] = {1.0, 0.0};
+    uint8_t sl = 0;
+    if (NM == 2) {
+        double k0 = div_cv(d, va[0]);
+        const double k1 = div_cv(d, va[1]);
+        double viol = 0.0;
+        const double cand[5] = {-k0, k0 - 1.0, -k1, k1 - 1.0, fabs(k0 + k1 - 1.0)};
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+            if (viol < cand[q]) viol = cand[q];
+        if (viol > 0.0 && own) atomicMax(&d.ctl->kviol_bits, (unsigned long long)__double_as_longlong(viol));
+        if (k0 < 0.0 || k0 > 1.0) {
+            if (own) atomicAdd(&d.ctl->step_clip, 1);
+            k0 = (k0 < 0.0) ? 0.0 : ((1.0 < k0) ? 1.0 : k0);
+        }
+        if (k0 < kPureTol) k0 = 0.0;
+        if (k0 > 1.0 - kPureTol) k0 = 1.0;
+        k[0] = k0;
+        k[1] = 1.0 - k0;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            if ((k[a] == 0.0 && m[a] != 0.0) || m[a] < 0.0) {
+                sl |= (uint8_t)(1u << a);
+                d.slm[a][c] = m[a];
+                d.slme[a][c] = me[a];
+                m[a] = 0.0;
+                me[a] = 0.0;
+                if (k[a] > 0.0) {
+                    k[a] = 0.0;
+                    k[1 - a] = 1.0;
+                }
+            }
+        }
+        d.nk[0][c] = k[0];
+        d.nk[1][c] = k[1];
+    } else {
+        d.nk[0][c] = d.k[0][c];  // one material: w.k = s.k carried unchanged
+    }
+    double mtot = 0.0;
+    int bad_sub = -1;
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        const double ma = m[a];
+        if (ma < 0.0 && bad_sub < 0) bad_sub = a;
+        d.nm[a][c] = ma;
+        d.me[a][c] = me[a];
+        d.ne[a][c] = ma > 0.0 ? me[a] / ma : 0.0;
+        mtot += ma;
+    }
+    if (bad_sub < 0 && mtot <= 0.0) bad_sub = 2;
+    if (bad_sub >= 0 && own) raise(d.ctl, ekey(PH_NEGMASS, j, i, bad_sub));
+    d.mcell[c] = mtot;
+    if (NM == 2) {
+        d.sliver[c] = sl;
+        if (sl) {  // index the sliver for k_slivers (row bit + segment bit)
+            const int jr = j - rg.j0;
+            atomicOr(&d.sl_segs[(size_t)jr * ((rg.i1 - rg.i0 + 31) >> 5) + blockIdx.x], 1u << tx);
+            atomicOr(&d.sl_rows[jr >> 5], 1u << (jr & 31));
+        }
+    }
+}
+
 template <int NM>
 __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d) {
     pdl_enter();
@@ -1052,6 +1119,48 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
     const Tile<NM> T = carve_tile<NM>(smem, i0 - G, j0 - G);
     const double dt = step_dt(d.ctl);
     const double cv = d.cv;
+    // ---- quiescent tile: u_half == 0 at every node of the tile's faces and
+    // corners makes every face / corner flux volume of the tile zero, so no
+    // flux is gathered (the reference skips zero volumes, remap.cpp:860,929),
+    // the Lagrangian volume of each own cell is exactly cv (cv + 0 - 0 ...),
+    // and the face / corner mass fluxes are +0.0: the per-cell finalize needs
+    // only the cell's own inputs (same bits as the full path below)
+    {
+        int moving = 0;
+        RowCol<RTX + 1, RTX * RTY> rq(tid);
+        for (int t = tid; t < NCF; t += RTX * RTY, rq.step()) {
+            const int ni = i0 + rq.c, nj = j0 + rq.r;
+            if (in(d.win_n, ni, nj)) {
+                const int n = ix(d, ni, nj);
+                if (d.uhx[n] != 0.0 || d.uhy[n] != 0.0) moving = 1;
+            }
+        }
+        if (!__syncthreads_or(moving)) {
+            const int ni1 = min(nx, rg.i1), nj1 = min(ny, rg.j1);
+            RowCol<RTX + 1, RTX * RTY> rz(tid);
+            for (int t = tid; t < NCF; t += RTX * RTY, rz.step()) {
+                const int ni = i0 + rz.c, nj = j0 + rz.r;
+                const bool lastx = ni < i0 + RTX || ni == ni1, lasty = nj < j0 + RTY || nj == nj1;
+                if (ni <= ni1 && nj < nj1 && nj < j0 + RTY && lastx) d.dmx[ix(d, ni, nj)] = 0.0;
+                if (ni < ni1 && ni < i0 + RTX && nj <= nj1 && lasty) d.dmy[ix(d, ni, nj)] = 0.0;
+                if (ni <= ni1 && nj <= nj1 && lastx && lasty) d.dmc[ix(d, ni, nj)] = 0.0;
+            }
+            const int tx = tid % RTX, ty = tid / RTX;
+            const int i = i0 + tx, j = j0 + ty;
+            if (!in(rg, i, j)) return;
+            const int c = ix(d, i, j);
+            double m[2], me[2], va[2];
+#pragma unroll
+            for (int a = 0; a < NM; ++a) {
+                const double m0 = d.m[a][c];
+                m[a] = m0;
+                me[a] = m0 * d.el[a][c];
+                va[a] = d.k[a][c] * cv;
+            }
+            finalize_cell<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va);
+            return;
+        }
+    }
     // ---- phase 0: stage the HBM inputs of the tile + halo (all loads
     // independent, coalesced rows): u_half on the node region, e_lag, m, k
     // (and normals) on the cell region.  T.rho holds m and T.vl holds k0
@@ -1281,67 +1390,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
             for (int a = 0; a < NM; ++a) add(a, cq[q], donor);
         }
     }
-    // finalize_cells, per-cell part
-    double k[2] = {1.0, 0.0};
-    uint8_t sl = 0;
-    if (NM == 2) {
-        double k0 = div_cv(d, va[0]);
-        const double k1 = div_cv(d, va[1]);
-        double viol = 0.0;
-        const double cand[5] = {-k0, k0 - 1.0, -k1, k1 - 1.0, fabs(k0 + k1 - 1.0)};
-#pragma unroll
-        for (int q = 0; q < 5; ++q)
-            if (viol < cand[q]) viol = cand[q];
-        if (viol > 0.0 && own) atomicMax(&d.ctl->kviol_bits, (unsigned long long)__double_as_longlong(viol));
-        if (k0 < 0.0 || k0 > 1.0) {
-            if (own) atomicAdd(&d.ctl->step_clip, 1);
-            k0 = (k0 < 0.0) ? 0.0 : ((1.0 < k0) ? 1.0 : k0);
-        }
-        if (k0 < kPureTol) k0 = 0.0;
-        if (k0 > 1.0 - kPureTol) k0 = 1.0;
-        k[0] = k0;
-        k[1] = 1.0 - k0;
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-            if ((k[a] == 0.0 && m[a] != 0.0) || m[a] < 0.0) {
-                sl |= (uint8_t)(1u << a);
-                d.slm[a][c] = m[a];
-                d.slme[a][c] = me[a];
-                m[a] = 0.0;
-                me[a] = 0.0;
-                if (k[a] > 0.0) {
-                    k[a] = 0.0;
-                    k[1 - a] = 1.0;
-                }
-            }
-        }
-        d.nk[0][c] = k[0];
-        d.nk[1][c] = k[1];
-    } else {
-        d.nk[0][c] = d.k[0][c];  // one material: w.k = s.k carried unchanged
-    }
-    double mtot = 0.0;
-    int bad_sub = -1;
-#pragma unroll
-    for (int a = 0; a < NM; ++a) {
-        const double ma = m[a];
-        if (ma < 0.0 && bad_sub < 0) bad_sub = a;
-        d.nm[a][c] = ma;
-        d.me[a][c] = me[a];
-        d.ne[a][c] = ma > 0.0 ? me[a] / ma : 0.0;
-        mtot += ma;
-    }
-    if (bad_sub < 0 && mtot <= 0.0) bad_sub = 2;
-    if (bad_sub >= 0 && own) raise(d.ctl, ekey(PH_NEGMASS, j, i, bad_sub));
-    d.mcell[c] = mtot;
-    if (NM == 2) {
-        d.sliver[c] = sl;
-        if (sl) {  // index the sliver for k_slivers (row bit + segment bit)
-            const int jr = j - rg.j0;
-            atomicOr(&d.sl_segs[(size_t)jr * ((rg.i1 - rg.i0 + 31) >> 5) + blockIdx.x], 1u << tx);
-            atomicOr(&d.sl_rows[jr >> 5], 1u << (jr & 31));
-        }
-    }
+    finalize_cell<NM>(d, rg, i, j, c, tx, own, m, me, va);
 }
 
 
