@@ -1716,6 +1716,32 @@ __global__ void __launch_bounds__(128, 8) k_dual_items(Dev d) {
     tid2(i, j, d.r_dual.i0, d.r_dual.j0);
     const int iend = d.per_x ? d.nx - 1 : d.nx, jend = d.per_y ? d.ny - 1 : d.ny;
     if (!in(d.r_dual, i, j) || i < 0 || j < 0 || i > iend || j > jend) return;
+    {  // every mass flux the node's items read is zero: all items are skipped
+       // ones (remap.cpp:423,1019), stored as exact zeros
+        const int a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
+        const int f = ix(d, i + 1, j - 1), g = ix(d, i + 1, j), h = ix(d, i, j + 1), k = ix(d, i + 1, j + 1);
+        const double* X = d.dmx;
+        const double* Y = d.dmy;
+        const double* Cn = d.dmc;
+        const bool quiet = (X[a] == 0.0) & (X[b] == 0.0) & (X[c] == 0.0) & (X[e] == 0.0) & (Y[a] == 0.0) &
+                           (Y[b] == 0.0) & (Y[c] == 0.0) & (Y[e] == 0.0) & (Cn[b] == 0.0) & (Cn[f] == 0.0) &
+                           (Cn[e] == 0.0) & (Cn[g] == 0.0) & (Cn[h] == 0.0) & (Cn[k] == 0.0);
+        if (quiet) {
+            d.dfx_x[e] = 0.0;
+            d.dfx_y[e] = 0.0;
+            d.dfy_x[e] = 0.0;
+            d.dfy_y[e] = 0.0;
+            d.dc_x[0][e] = 0.0;
+            d.dc_y[0][e] = 0.0;
+            d.dc_x[1][e] = 0.0;
+            d.dc_y[1][e] = 0.0;
+            if (d.per_x || d.per_y) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) d.dflag[q][e] = 0;
+            }
+            return;
+        }
+    }
     dual_face_item<1>(d, i, j);
     dual_face_item<0>(d, i, j);
     dual_corner_items(d, i, j);
