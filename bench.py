@@ -222,29 +222,48 @@ def run_product(args, world, rank, local, pg):
         except Exception:
             traffic = None
 
-    # end to end through the public per-step API with host (pinned) buffers:
-    # upload State -> one run-loop step -> download State, every step
-    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    # end to end through the public API with host (pinned) State buffers.
+    # (1) e2e: the reference's hot-loop call -- run(State, K steps) -- on a host
+    #     State: upload, K device steps, download, all inside the timed region;
+    # (2) e2e_per_step_api: the value API every step (upload State -> one step
+    #     -> download State), i.e. a caller that keeps its State on the host.
     se = abi.Solver(lib, case.cfg, local)
+    se.init_from(painted)
+    se.run(1, cfl=case.cfl, log_dt=False)  # one-time setup (graph capture) outside the timed region
     se.init_from(painted)
     host = pinned_state(case.cfg.mesh.nx, case.cfg.mesh.ny, nmat, case.cfg.mesh.dx * case.cfg.mesh.dy)
     st0 = se.download()
-    for f in ("m", "e", "k", "vol", "m_mix", "e_mix", "rho_mix", "p_mix", "iface_normal", "u"):
+    fields = ("m", "e", "k", "vol", "m_mix", "e_mix", "rho_mix", "p_mix", "iface_normal", "u")
+    for f in fields:
         getattr(host, f)[...] = getattr(st0, f)
-    h2d = sum(getattr(host, f)[:nmat].nbytes if f in ("m", "e", "k") else getattr(host, f).nbytes
-              for f in ("m", "e", "k", "vol", "m_mix", "e_mix", "rho_mix", "p_mix", "iface_normal", "u"))
-    view_up = host.view(derived=True)
-    barrier(pg)
-    t0 = time.perf_counter()
-    for q in range(e2e_steps):
-        se._check(lib.fn["upload_state"](se._h, abi.C.byref(view_up)))
-        se.run(host.step + 1, cfl=case.cfl, log_dt=False)
+    state_bytes = sum(getattr(host, f)[:nmat].nbytes if f in ("m", "e", "k") else getattr(host, f).nbytes
+                      for f in fields)
+
+    def upload():
+        v = host.view(derived=True)
+        se._check(lib.fn["upload_state"](se._h, abi.C.byref(v)))
+
+    def download():
         v = host.view(derived=True)
         se._check(lib.fn["download_state"](se._h, abi.C.byref(v)))
         host.step, host.time = v.step, v.time
-        view_up = host.view(derived=True)
+
+    barrier(pg)
+    t0 = time.perf_counter()
+    upload()
+    se.run(host.step + args.steps, cfl=case.cfl, log_dt=False)
+    download()
+    e2e_run_s = max_over_ranks(pg, time.perf_counter() - t0)
+    e2e_value = cells * args.steps * world / e2e_run_s
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    barrier(pg)
+    t0 = time.perf_counter()
+    for q in range(e2e_steps):
+        upload()
+        se.run(host.step + 1, cfl=case.cfl, log_dt=False)
+        download()
     e2e_s = max_over_ranks(pg, time.perf_counter() - t0)
-    e2e_value = cells * e2e_steps * world / e2e_s
+    e2e_step_value = cells * e2e_steps * world / e2e_s
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -265,8 +284,13 @@ def run_product(args, world, rank, local, pg):
                           "frac": achieved_step / peak,
                           "basis": f"whole step: {B_MIN[nmat]} B/cell-step (state read+write once, "
                                    f"SURVEY 8d) x {cells} cells"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d,
-                "steps": e2e_steps, "path": "h2d_upload_state + h2d_run(1 step) + h2d_download_state, pinned host"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": state_bytes / args.steps,
+                "d2h_bytes_per_step": state_bytes / args.steps, "steps": args.steps,
+                "path": "run(State, K steps) on a pinned host State: h2d_upload_state + h2d_run(K) + "
+                        "h2d_download_state, wall clock (the reference's hot-loop call, harness.cpp:380-424)"},
+        "e2e_per_step_api": {"value": e2e_step_value, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
+                             "d2h_bytes_per_step": state_bytes, "steps": e2e_steps,
+                             "path": "every step: h2d_upload_state + h2d_run(1 step) + h2d_download_state"},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
