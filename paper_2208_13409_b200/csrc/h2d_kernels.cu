@@ -1726,7 +1726,10 @@ __global__ void __launch_bounds__(128, 8) k_dual_items(Dev d) {
         const bool quiet = (X[a] == 0.0) & (X[b] == 0.0) & (X[c] == 0.0) & (X[e] == 0.0) & (Y[a] == 0.0) &
                            (Y[b] == 0.0) & (Y[c] == 0.0) & (Y[e] == 0.0) & (Cn[b] == 0.0) & (Cn[f] == 0.0) &
                            (Cn[e] == 0.0) & (Cn[g] == 0.0) & (Cn[h] == 0.0) & (Cn[k] == 0.0);
-        if (quiet) {
+        if (!(d.per_x || d.per_y)) {  // walls: dflag[0] marks a quiet node, its items are not stored
+            d.dflag[0][e] = quiet;
+            if (quiet) return;
+        } else if (quiet) {
             d.dfx_x[e] = 0.0;
             d.dfx_y[e] = 0.0;
             d.dfy_x[e] = 0.0;
@@ -1735,10 +1738,8 @@ __global__ void __launch_bounds__(128, 8) k_dual_items(Dev d) {
             d.dc_y[0][e] = 0.0;
             d.dc_x[1][e] = 0.0;
             d.dc_y[1][e] = 0.0;
-            if (d.per_x || d.per_y) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) d.dflag[q][e] = 0;
-            }
+            for (int q = 0; q < 4; ++q) d.dflag[q][e] = 0;
             return;
         }
     }
@@ -1766,18 +1767,25 @@ __global__ void k_node_update_walls(Dev d) {
     // exactly 0.0, and adding +-0.0 leaves the accumulator unchanged (it
     // starts at +0.0 and a sum is -0.0 only if both terms are), so the
     // reference's skip needs no flag here.
-    const bool fxp = i >= 1, fxm = i + 1 <= nx, fyp = j >= 1, fym = j + 1 <= ny;
-    const bool fpp = i >= 1 && j >= 1, fpm = i >= 1 && j + 1 <= ny;
+    // Items of a quiet node (k_dual_items, dflag[0]) are zeros that were not
+    // stored: they are skipped like the zero items above.
+    const uint8_t* qf = d.dflag[0];
+    const bool qs = qf[s];
+    const bool fxp = i >= 1 && !qs, fxm = i + 1 <= nx && !qf[sxr], fyp = j >= 1 && !qs,
+               fym = j + 1 <= ny && !qf[syt];
+    const bool fpp = i >= 1 && j >= 1 && !qf[pp], fpm = i >= 1 && j + 1 <= ny && !qf[pm];
     double ax = 0.0, ay = 0.0;
     if (fxp) { ax += d.dfx_x[s]; ay += d.dfx_y[s]; }
     if (fxm) { ax += -d.dfx_x[sxr]; ay += -d.dfx_y[sxr]; }
     if (fyp) { ax += d.dfy_x[s]; ay += d.dfy_y[s]; }
     if (fym) { ax += -d.dfy_x[syt]; ay += -d.dfy_y[syt]; }
     if (fpp) { ax += -d.dc_x[0][pp]; ay += -d.dc_y[0][pp]; }
-    ax += d.dc_x[0][s];
-    ay += d.dc_y[0][s];
-    ax += d.dc_x[1][s];
-    ay += d.dc_y[1][s];
+    if (!qs) {
+        ax += d.dc_x[0][s];
+        ay += d.dc_y[0][s];
+        ax += d.dc_x[1][s];
+        ay += d.dc_y[1][s];
+    }
     if (fpm) { ax += -d.dc_x[1][pm]; ay += -d.dc_y[1][pm]; }
     const int c00 = pp, c10 = ix(d, i, j - 1), c01 = ix(d, i - 1, j);
     double l00 = 0.0, l10 = 0.0, l01 = 0.0, l11 = 0.0;  // make_work's mcell (remap.cpp:133-138)
