@@ -31,11 +31,20 @@ import numpy as np  # noqa: E402
 METRIC = "cell-updates/s per full Lagrange+remap step (fp64)"
 UNIT = "cell-updates/s"
 B_MIN = {1: 64, 2: 160}  # algorithmic bytes per cell-step
-# k_remap_tile (the dominant kernel) compulsory HBM bytes per cell: reads
-# u_half (2 nodal doubles) + e_lag, m, k per material (+ interface normal for
-# 2 materials); writes the Work m, me, e, k per material, mcell, and the three
-# mass fluxes dmx, dmy, dmc the dual pass consumes (+ 1 sliver-flag byte).
-B_TILE = {1: 8 * (2 + 3) + 8 * (4 + 1 + 3), 2: 8 * (2 + 6 + 2) + 8 * (8 + 1 + 3) + 1}
+# Compulsory HBM bytes per cell of the three big kernels (their inputs read
+# once + outputs written once):
+#  k_lag_fused: reads m, e, k per material, u (2 nodal), m_mix, rho_mix;
+#               writes u_half, u_lag (2+2 nodal), e_lag per material;
+#  k_remap_tile: reads u_half (2), e_lag, m, k per material (+ normals for 2
+#               materials); writes Work m, me, e, k per material, mcell, the
+#               mass fluxes dmx, dmy, dmc (+ 1 sliver-flag byte for 2);
+#  k_post:      reads new m, e, k per material, |u| and u (3 nodal) (+ old
+#               normals); writes m_mix, e_mix, rho_mix, p_mix, vol (+ normals).
+KERNEL_BYTES = {
+    "lagrange": ("k_lag_fused", {1: 8 * (3 + 4) + 8 * (4 + 1), 2: 8 * (6 + 4) + 8 * (4 + 2)}),
+    "remap_tile": ("k_remap_tile", {1: 8 * (2 + 3) + 8 * (4 + 1 + 3), 2: 8 * (2 + 6 + 2) + 8 * (8 + 1 + 3) + 1}),
+    "post": ("k_post", {1: 8 * (3 + 3) + 8 * 5, 2: 8 * (6 + 3 + 2) + 8 * (5 + 2)}),
+}
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0
 
@@ -206,19 +215,25 @@ def run_product(args, world, rank, local, pg):
     clk = clocks.stop()
     barrier(pg)
     total_s = max_over_ranks(pg, tot / 1e3)
-    tile_ms = max_over_ranks(pg, ph["remap_tile"])
     cells = case.cells
     value = cells * args.steps * world / total_s
     ms_step = total_s * 1e3 / args.steps
     peak, peak_kind = hbm_peak()
     achieved_step = B_MIN[nmat] * cells / (ms_step / 1e3) / 1e9
-    achieved_tile = B_TILE[nmat] * cells / (tile_ms / 1e3) / 1e9
+    kern = {}
+    for grp, (kname, nbytes) in KERNEL_BYTES.items():
+        kms = max_over_ranks(pg, ph[grp])
+        ach = nbytes[nmat] * cells / (kms / 1e3) / 1e9
+        kern[grp] = {"kernel": f"{kname}<{nmat}>", "ms": kms, "bytes_per_cell": nbytes[nmat],
+                     "achieved": ach, "frac": ach / peak,
+                     "share_of_step": kms / ph["total"] if ph["total"] > 0 else None}
+    dom = max(kern, key=lambda g: kern[g]["ms"])
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
     if os.path.exists(tf):
         try:
             with open(tf) as f:
-                traffic = json.load(f).get(args.workload)
+                traffic = json.load(f).get(args.workload, {}).get(kern[dom]["kernel"].split("<")[0])
         except Exception:
             traffic = None
 
@@ -275,11 +290,13 @@ def run_product(args, world, rank, local, pg):
                    "l2": "512 MiB write between timed steps; working set per step >> 126 MB L2"},
         "phases_ms": dict(ph, note=f"{n_ph} un-graphed steps after the timed ones, CUDA events between "
                                     "kernel groups on the launching stream"),
-        "roofline": {"bound": "hbm", "achieved": achieved_tile, "peak": peak, "unit": "GB/s",
-                     "frac": achieved_tile / peak, "traffic": traffic, "peak_source": peak_kind,
-                     "kernel": f"k_remap_tile<{nmat}>", "kernel_ms": tile_ms,
-                     "share_of_step": tile_ms / ph["total"] if ph["total"] > 0 else None,
-                     "basis": f"{B_TILE[nmat]} B/cell compulsory I/O of the kernel x {cells} cells per launch"},
+        "roofline": {"bound": "hbm", "achieved": kern[dom]["achieved"], "peak": peak, "unit": "GB/s",
+                     "frac": kern[dom]["frac"], "traffic": traffic, "peak_source": peak_kind,
+                     "kernel": kern[dom]["kernel"], "kernel_ms": kern[dom]["ms"],
+                     "share_of_step": kern[dom]["share_of_step"],
+                     "basis": f"{kern[dom]['bytes_per_cell']} B/cell compulsory I/O of the kernel x {cells} "
+                              f"cells per launch, CUDA-event time of the launch",
+                     "kernels": kern},
         "step_roofline": {"bound": "hbm", "achieved": achieved_step, "peak": peak, "unit": "GB/s",
                           "frac": achieved_step / peak,
                           "basis": f"whole step: {B_MIN[nmat]} B/cell-step (state read+write once, "

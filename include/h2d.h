@@ -246,11 +246,11 @@ int h2d_block_result(h2d_ctx* ctx, h2d_run_args* args);
 long long h2d_launch_count(void);
 /* One run-loop step (as h2d_run with max_steps = state step + 1) bracketed by
  * CUDA events on the context's stream. ms[6] = the whole step; with
- * phases = 1 (plain launches, events between kernel groups) also
- * ms[0] step start (dt), ms[1] Lagrange (k_lag_fused + ghosts), ms[2] the
- * remap flux tile kernel alone, ms[3] slivers + Work ghosts, ms[4] dual-mesh
- * momentum, ms[5] derived fields / normals / commit; phases = 0 replays the
- * production CUDA graph (only ms[6] is set). ms[7] is reserved (0). */
+ * phases = 1 (plain launches, events between kernels) also ms[0] step start
+ * (dt), ms[1] the fused Lagrange kernel, ms[2] the remap flux tile kernel,
+ * ms[3] slivers + Work ghosts, ms[4] dual-mesh momentum, ms[5] the derived
+ * fields / normals / NaN-scan kernel, ms[7] the ghost-layer launches and the
+ * commit; phases = 0 replays the production CUDA graph (only ms[6] set). */
 int h2d_step_timed(h2d_ctx* ctx, double cfl, double t_end, int phases, float ms[8]);
 /* Write `bytes` of scratch on the context's stream (evicts L2 between timed
  * steps) and wait for it. */

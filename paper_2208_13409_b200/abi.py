@@ -341,7 +341,7 @@ class Solver:
             raise err
         return res
 
-    STEP_GROUPS = ("start", "lagrange", "remap_tile", "slivers", "dual", "post", "total")
+    STEP_GROUPS = ("start", "lagrange", "remap_tile", "slivers", "dual", "post", "total", "ghosts_commit")
 
     def step_timed(self, cfl: float, t_end: float = 1e30, phases: bool = False) -> dict:
         """One run-loop step timed with CUDA events (product only): returns

@@ -47,7 +47,7 @@ struct h2d_ctx {
     int dt_log_cap = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one run-loop step per State parity
     long long graph_kernels = 0;
-    cudaEvent_t ev[7] = {};
+    cudaEvent_t ev[9] = {};
     h2d_block blk{};   // the block of the 2D decomposition (the whole mesh for h2d_create)
     bool is_block = false;
     double* xbuf = nullptr;  // device staging for window uploads / owned downloads
@@ -851,33 +851,45 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[8]
     // step's k_post) is recomputed outside the timed region
     enqueue_cfl_next(c);
     for (int q = 0; q < 8; ++q) ms[q] = 0.0f;
-    if (phases) {  // un-graphed launches with events between the kernel groups
+    if (phases) {  // un-graphed launches with events between the kernels / groups
         const Dev d = make_dev(c, c->cur, 1);
         CK(cudaEventRecord(c->ev[0], c->st));
         launch_step_start(d, c->st);
         CK(cudaEventRecord(c->ev[1], c->st));
-        launch_lagrange_run(d, c->st);
+        launch_lag_fused(d, c->st);
         CK(cudaEventRecord(c->ev[2], c->st));
-        launch_remap_tile(d, c->st);
+        launch_lag_ghosts(d, c->st);
         CK(cudaEventRecord(c->ev[3], c->st));
-        launch_remap_slivers(d, c->st);
+        launch_remap_tile(d, c->st);
         CK(cudaEventRecord(c->ev[4], c->st));
-        launch_remap_dual(d, c->st);
+        launch_remap_slivers(d, c->st);
         CK(cudaEventRecord(c->ev[5], c->st));
-        post_and_ghosts(d, 1, c->st);
-        launch_commit_finish(d, c->st);
+        launch_remap_dual(d, c->st);
         CK(cudaEventRecord(c->ev[6], c->st));
+        launch_post(d, 1, c->st);
+        CK(cudaEventRecord(c->ev[7], c->st));
+        launch_post_ghosts(d, c->st);
+        launch_commit_finish(d, c->st);
+        CK(cudaEventRecord(c->ev[8], c->st));
         if (int rc = check_launch(c)) return rc;
-        CK(cudaEventSynchronize(c->ev[6]));
-        for (int q = 0; q < 6; ++q) CK(cudaEventElapsedTime(&ms[q], c->ev[q], c->ev[q + 1]));
-        CK(cudaEventElapsedTime(&ms[6], c->ev[0], c->ev[6]));
+        CK(cudaEventSynchronize(c->ev[8]));
+        float t[8];
+        for (int q = 0; q < 8; ++q) CK(cudaEventElapsedTime(&t[q], c->ev[q], c->ev[q + 1]));
+        ms[0] = t[0];         // step start
+        ms[1] = t[1];         // k_lag_fused
+        ms[2] = t[3];         // k_remap_tile
+        ms[3] = t[4];         // slivers + Work / flux ghosts
+        ms[4] = t[5];         // dual-mesh momentum
+        ms[5] = t[6];         // k_post
+        ms[7] = t[2] + t[7];  // Lagrange ghosts, post ghosts + commit
+        CK(cudaEventElapsedTime(&ms[6], c->ev[0], c->ev[8]));
     } else {  // the production path: one graph launch
         if (int rc = ensure_graphs(c)) return rc;
         CK(cudaEventRecord(c->ev[0], c->st));
         if (int rc = launch_step_graph(c, c->cur)) return rc;
-        CK(cudaEventRecord(c->ev[6], c->st));
-        CK(cudaEventSynchronize(c->ev[6]));
-        CK(cudaEventElapsedTime(&ms[6], c->ev[0], c->ev[6]));
+        CK(cudaEventRecord(c->ev[8], c->st));
+        CK(cudaEventSynchronize(c->ev[8]));
+        CK(cudaEventElapsedTime(&ms[6], c->ev[0], c->ev[8]));
     }
     if (int rc = ctl_pull(c)) return rc;
     c->cur = h.cur;

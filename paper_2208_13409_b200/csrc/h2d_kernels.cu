@@ -2371,11 +2371,19 @@ void remap_init() {
 // k_post (sync_derived, normals, and in the run loop nan_scan + next cfl) and
 // the ghost layers of the new u and normals (assemble_state's fill_ghosts).
 void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s) {
+    launch_post(d, run_loop, s);
+    launch_post_ghosts(d, s);
+}
+
+void launch_post(const Dev& d, int run_loop, cudaStream_t s) {
     const dim3 gp = tiles_of(d.r_sync, 32, 8);
     if (d.nmat == 2)
         pdl(k_post<2>, gp, dim3(32, 8), 0, s, d, run_loop);
     else
         pdl(k_post<1>, gp, dim3(32, 8), 0, s, d, run_loop);
+}
+
+void launch_post_ghosts(const Dev& d, cudaStream_t s) {
     FieldList fg{};
     fg.n = 2;
     fg.f[0] = d.nnrx;
@@ -2391,10 +2399,18 @@ void launch_remap(const Dev& d, cudaStream_t s) { launch_remap_core(d, s); post_
 
 // run-loop Lagrangian phase: the fused kernel + ghost layers of u_half, u_lag, e_lag
 void launch_lagrange_run(const Dev& d, cudaStream_t s) {
+    launch_lag_fused(d, s);
+    launch_lag_ghosts(d, s);
+}
+
+void launch_lag_fused(const Dev& d, cudaStream_t s) {
     if (d.nmat == 2)
         pdl(k_lag_fused<2>, tiles_of(d.r_lagn, LTX, LTY), dim3(LTX * LTY), 0, s, d);
     else
         pdl(k_lag_fused<1>, tiles_of(d.r_lagn, LTX, LTY), dim3(LTX * LTY), 0, s, d);
+}
+
+void launch_lag_ghosts(const Dev& d, cudaStream_t s) {
     FieldList fn{};
     fn.n = 4;
     fn.f[0] = d.uhx;

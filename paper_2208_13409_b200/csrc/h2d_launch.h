@@ -23,6 +23,10 @@ void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s);
 void launch_lagrange_run(const Dev& d, cudaStream_t s);
 void launch_remap(const Dev& d, cudaStream_t s);
 void launch_remap_core(const Dev& d, cudaStream_t s);  // = tile + slivers + dual
+void launch_lag_fused(const Dev& d, cudaStream_t s);
+void launch_lag_ghosts(const Dev& d, cudaStream_t s);
+void launch_post(const Dev& d, int run_loop, cudaStream_t s);
+void launch_post_ghosts(const Dev& d, cudaStream_t s);
 void launch_remap_tile(const Dev& d, cudaStream_t s);
 void launch_remap_slivers(const Dev& d, cudaStream_t s);
 void launch_remap_dual(const Dev& d, cudaStream_t s);
