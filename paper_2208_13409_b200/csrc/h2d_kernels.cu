@@ -596,6 +596,12 @@ __global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
             const double ux = d.ux[e], uy = d.uy[e];
             hx = ux - gx * sc;
             hy = uy - gy * sc;
+            // fill_ghost_nodes(u_half) zeroes the wall-normal component on the
+            // wall nodes (state.cpp:90-95) before correct reads u_half
+            // (lagrange.cpp:142,155): the wall-node gradient is a rounding
+            // residue of ((b + e) - a) - c with mirrored a = b, c = e
+            if (!d.per_x && (i == 0 || i == nx)) hx = 0.0;
+            if (!d.per_y && (j == 0 || j == ny)) hy = 0.0;
             if ((i < i0 + LTX || i == rn.i1 - 1) && (j < j0 + LTY || j == rn.j1 - 1)) {
                 d.uhx[e] = hx;
                 d.uhy[e] = hy;

@@ -3,6 +3,8 @@ restatement oracle, which is itself pinned to the reference
 (test_oracle_vs_reference.py).  The bar is bit-exact: every State and
 LagrangeResult byte, every dt, the mixed-cell set, the RemapDiag counters,
 floor counts and the first located error."""
+import zlib
+
 import numpy as np
 import pytest
 
@@ -47,6 +49,47 @@ def test_run_loop_bitwise(gpu, orc, case, steps):
     assert helpers.bitwise_diff(a, b, helpers.STATE_FIELDS) == []
     assert (a.step, a.time) == (b.step, b.time)
     assert sg.totals() == so.totals()
+
+
+@pytest.mark.parametrize("kind", ["gas", "front", "blobs"])
+@pytest.mark.parametrize("bcx,bcy,dx", [(BC_WALL, BC_WALL, 0.025), (BC_WALL, BC_WALL, 1.0 / 32),
+                                        (BC_PERIODIC, BC_WALL, 0.025), (BC_WALL, BC_PERIODIC, 1.0 / 32)])
+def test_run_loop_random_states(gpu, orc, kind, bcx, bcy, dx):
+    """The run loop (fused Lagrange kernel) on random states: rough pressure
+    next to the walls makes the wall-node gradient a rounding residue, which
+    fill_ghost_nodes zeroes before correct uses u_half (lagrange.cpp:143,155)."""
+    nmat = 1 if kind == "gas" else 2
+    cfg = make_config(40, 24, dx, dx * 1.25, 0.0, 0.0, bcx, bcy, eos=[(EOS_PERFECT, 1.4, 0.0), (EOS_PERFECT, 1.6, 0.0)][:nmat])
+    seed = zlib.crc32(repr((kind, bcx, bcy, dx)).encode()) & 0xFFFF
+    painted = helpers.random_state(cfg, seed, kind, umax=0.1, e_scale=3.0)
+    sg, so = _pair(gpu, orc, cfg, painted)
+    rg, eg = helpers.run_capture(sg, 25, 0.3)
+    ro, eo = helpers.run_capture(so, 25, 0.3)
+    assert eg == eo
+    assert rg.steps_done == ro.steps_done and np.array_equal(rg.dts, ro.dts)
+    assert rg.diag == ro.diag and rg.floor_count == ro.floor_count
+    assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS) == []
+
+
+@pytest.mark.parametrize("n,steps", [(48, 80), (64, 60)])
+def test_wall_blast_bitwise(gpu, orc, n, steps):
+    """A strong blast against the middle of the left wall: the artificial
+    viscosity dominates p + q at the wall nodes, so the rounding residue of the
+    wall-node gradient is large enough to move a cell volume unless u_half's
+    wall component is zeroed (fill_ghost_nodes) before correct uses it."""
+    from paper_2208_13409_b200.cases import Case, Region, ALL, RECTANGLE, _mesh_cfg
+    dx = 1.0 / n
+    p0 = 0.4 / (2 * dx * dx)
+    y0 = (n // 2) * dx
+    case = Case("wall_blast", _mesh_cfg(n, n, 1.0, 1.0, [(EOS_PERFECT, 1.4, 0.0)]),
+                [Region(ALL, rho=1.0, p=1e-6), Region(RECTANGLE, rect=(0.0, y0, 2 * dx, y0 + dx), rho=1.0, p=p0)],
+                0.5, steps)
+    sg, so = _pair(gpu, orc, case.cfg, case.paint())
+    rg, eg = helpers.run_capture(sg, steps, case.cfl)
+    ro, eo = helpers.run_capture(so, steps, case.cfl)
+    assert eg == eo
+    assert rg.steps_done == ro.steps_done and np.array_equal(rg.dts, ro.dts)
+    assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS) == []
 
 
 CONFIGS = []
