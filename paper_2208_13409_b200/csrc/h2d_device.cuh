@@ -8,6 +8,7 @@
 #pragma once
 #include <cstdint>
 #include <math_constants.h>
+#include <cfloat>
 
 #define H2D_DEV __device__ __forceinline__
 

@@ -557,9 +557,16 @@ __global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
             for (int a = 0; a < NM; ++a) {
                 if (!(ka[a] < kThermoTol)) {
                     const double rho_n = ma[a] / (ka[a] * cv);
-                    const double rho_h = ma[a] / (ka[a] * vol);
                     const double pa_n = eos_p(d, a, rho_n, en[a]);
-                    double ea = en[a] - (pa_n + q) * (1.0 / rho_h - 1.0 / rho_n);
+                    // vol == cv (a still or uniformly moving cell, lagrange.cpp:
+                    // 34-35) gives rho_h == rho_n bit for bit, so 1/rho_h - 1/rho_n
+                    // is +0 whenever 1/rho_n is finite: skip the three divides
+                    double rho_h = rho_n, dv = 0.0;
+                    if (!(vol == cv && fabs(rho_n) >= DBL_MIN)) {
+                        rho_h = ma[a] / (ka[a] * vol);
+                        dv = 1.0 / rho_h - 1.0 / rho_n;
+                    }
+                    double ea = en[a] - (pa_n + q) * dv;
                     const double efloor = 1e-8 * fabs(en[a]);
                     if (ea < efloor) {
                         ea = efloor;
@@ -637,8 +644,12 @@ __global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
         } else {
             const double ma = d.m[a][n];
             const double rho_n = ma / (ka * cv);
-            const double rho_l = ma / (ka * vol);
-            ea = en - (s_ph[a][tcell] + qn) * (1.0 / rho_l - 1.0 / rho_n);
+            double dv = 0.0;  // vol == cv: rho_l == rho_n, the difference of inverses is +0
+            if (!(vol == cv && fabs(rho_n) >= DBL_MIN)) {
+                const double rho_l = ma / (ka * vol);
+                dv = 1.0 / rho_l - 1.0 / rho_n;
+            }
+            ea = en - (s_ph[a][tcell] + qn) * dv;
             const double efloor = 1e-8 * fabs(en);
             if (ea < efloor) {
                 ea = efloor;
