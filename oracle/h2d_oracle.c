@@ -1154,6 +1154,156 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
 #undef DY_
 }
 
+/* directional_pass, remap.cpp:469-589: the X (axis_x = 1) or Y remap of the
+ * alternating-direction (AD) split scheme.  (along, cross) layouts as cf_pass:
+ * X: (ia, ic) = (i, j); Y: (ia, ic) = (j, i). */
+static void directional_pass(ctx_t* c, double dt, int axis_x, int remap_velocity) {
+    work_t* w = &c->w;
+    const int nx = c->nx, ny = c->ny, nmat = c->nmat;
+    const double cv = c->cv, dx = c->dx, dy = c->dy, x0 = c->x0, y0 = c->y0;
+    const int order = c->cfg.face_order;
+    const int na = axis_x ? nx : ny, nc = axis_x ? ny : nx;
+    const double wa = axis_x ? dx : dy, wc = axis_x ? dy : dx;
+    const int per_a = axis_x ? c->per_x : c->per_y, per_c = axis_x ? c->per_y : c->per_x;
+    fld gfd = axis_x ? c->fdx : c->fdy, gxl = axis_x ? c->xlcx : c->xlcy, gwl = axis_x ? c->wlx : c->wly;
+    fld dmf = axis_x ? c->dmx : c->dmy;
+    vfld uh = c->u_half;
+#define CI(ia, ic) (axis_x ? (ia) : (ic))
+#define CJ(ia, ic) (axis_x ? (ic) : (ia))
+    /* make_axis_geom, remap.cpp:296-322 */
+    for (int ic = -NG; ic < nc + NG; ++ic)
+        for (int ia = -NG; ia <= na + NG; ++ia) {
+            const double u0 = axis_x ? VX(uh, ia, ic) : VY(uh, ic, ia);
+            const double u1 = axis_x ? VX(uh, ia, ic + 1) : VY(uh, ic + 1, ia);
+            A(gfd, ia, ic) = 0.5 * (u0 + u1) * dt;
+        }
+    const double origin = axis_x ? x0 : y0;
+    for (int ic = -NG; ic < nc + NG; ++ic)
+        for (int ia = -NG; ia < na + NG; ++ia) {
+            const double dl = A(gfd, ia, ic), dr = A(gfd, ia + 1, ic);
+            A(gxl, ia, ic) = origin + (ia + 0.5) * wa + 0.5 * (dl + dr);
+            A(gwl, ia, ic) = wa + (dr - dl);
+        }
+    /* 1D Lagrangian volumes and densities, remap.cpp:478-491 */
+    for (int ic = -NG; ic < nc + NG; ++ic)
+        for (int ia = -NG; ia < na + NG; ++ia) {
+            const int i = CI(ia, ic), j = CJ(ia, ic);
+            const double v = cv + (A(gfd, ia + 1, ic) - A(gfd, ia, ic)) * wc;
+            if (v <= 0.0) raise_err(c, H2D_ERR_CFL, i, j, "collapsed Lagrangian cell");
+            A(c->vlag, i, j) = v;
+            for (int a = 0; a < nmat; ++a) {
+                const double ka = A(w->k[a], i, j);
+                A(c->rho[a], i, j) = ka > 0.0 ? A(w->m[a], i, j) / (ka * v) : 0.0;
+            }
+        }
+    /* interfaces on the 1D-displaced rectangles, remap.cpp:493-514 */
+    izero(c->if_mixed);
+    if (nmat == 2)
+        for (int ic = -NG; ic < nc + NG; ++ic)
+            for (int ia = -NG; ia < na + NG; ++ia) {
+                const int i = CI(ia, ic), j = CJ(ia, ic);
+                const double k0 = A(w->k[0], i, j);
+                if (!is_mixed(k0)) continue;
+                const double cx = x0 + (i + 0.5) * dx, cy = y0 + (j + 0.5) * dy;
+                const double dl = A(gfd, ia, ic), dr = A(gfd, ia + 1, ic);
+                double lox, loy, hix, hiy;
+                if (axis_x) {
+                    lox = cx - 0.5 * dx + dl; loy = cy - 0.5 * dy;
+                    hix = cx + 0.5 * dx + dr; hiy = cy + 0.5 * dy;
+                } else {
+                    lox = cx - 0.5 * dx; loy = cy - 0.5 * dy + dl;
+                    hix = cx + 0.5 * dx; hiy = cy + 0.5 * dy + dr;
+                }
+                const double nxv = VX(w->normals, i, j), nyv = VY(w->normals, i, j);
+                A(c->if_mixed, i, j) = 1;
+                A(c->if_lox, i, j) = lox; A(c->if_loy, i, j) = loy;
+                A(c->if_hix, i, j) = hix; A(c->if_hiy, i, j) = hiy;
+                A(c->if_nx, i, j) = nxv; A(c->if_ny, i, j) = nyv;
+                A(c->if_d, i, j) = place_interface(k0, nxv, nyv, lox, loy, hix, hiy);
+            }
+    for (int a = 0; a < nmat; ++a) {
+        fzero(c->vola[a]);
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) A(c->vola[a], i, j) = A(w->k[a], i, j) * A(c->vlag, i, j);
+    }
+    /* face fluxes, remap.cpp:526-577 */
+    fzero(dmf);
+    for (int ic = 0; ic < nc; ++ic)
+        for (int ia = 0; ia <= na; ++ia) {
+            const double dvol = A(gfd, ia, ic) * wc;
+            A(dmf, ia, ic) = 0.0;
+            if (dvol == 0.0) continue;
+            if (fabs(dvol) > CFL_FRAC * cv) raise_err(c, H2D_ERR_CFL, CI(ia, ic), CJ(ia, ic), "CFL violation at face");
+            const int ia_d = dvol > 0.0 ? ia - 1 : ia;
+            const double sgn = dvol > 0.0 ? 1.0 : -1.0;
+            const int cdi = CI(ia_d, ic), cdj = CJ(ia_d, ic);
+            /* face_flux_box, remap.cpp:325-334 */
+            const double d = A(gfd, ia, ic);
+            double blox, bloy, bhix, bhiy;
+            if (axis_x) {
+                const double xf = x0 + ia * dx;
+                blox = ref_min(xf, xf + d); bloy = y0 + ic * dy;
+                bhix = ref_max(xf, xf + d); bhiy = y0 + (ic + 1) * dy;
+            } else {
+                const double yf = y0 + ia * dy;
+                blox = x0 + ic * dx; bloy = ref_min(yf, yf + d);
+                bhix = x0 + (ic + 1) * dx; bhiy = ref_max(yf, yf + d);
+            }
+            double dva[2];
+            split_flux(c, cdi, cdj, blox, bloy, bhix, bhiy, dvol, dva);
+            double dmtot = 0.0;
+            for (int a = 0; a < nmat; ++a) {
+                if (dva[a] == 0.0) continue;
+                int ord = order;
+                if (ord == 2 && nmat == 2 && c->cfg.interface_degrade && !pure_1d(c, a, axis_x, ia_d, ic)) ord = 1;
+                double rf, ef;
+                if (ord <= 1) {
+                    rf = A(c->rho[a], cdi, cdj);
+                    ef = A(w->e[a], cdi, cdj);
+                } else {
+                    double sr[3], se[3], sxp[3];
+                    for (int q = -1; q <= 1; ++q) {
+                        const int ci = CI(ia_d + q, ic), cj = CJ(ia_d + q, ic);
+                        sr[q + 1] = A(c->rho[a], ci, cj);
+                        se[q + 1] = A(w->e[a], ci, cj);
+                        sxp[q + 1] = A(gxl, ia_d + q, ic);
+                    }
+                    rf = face_value2(c, sr, sxp, sgn, A(gwl, ia_d, ic), A(gfd, ia, ic));
+                    ef = face_value2(c, se, sxp, sgn, A(gwl, ia_d, ic), A(gfd, ia, ic));
+                }
+                const double dm = rf * dva[a];
+                const double dme = rf * ef * dva[a];
+                dmtot += dm;
+                apply_cell(c, c->vola, a, CI(ia - 1, ic), CJ(ia - 1, ic), -dm, -dme, -dva[a]);
+                apply_cell(c, c->vola, a, CI(ia, ic), CJ(ia, ic), dm, dme, dva[a]);
+            }
+            A(dmf, ia, ic) = dmtot;
+        }
+    face_flux_ghosts(dmf, na, nc, per_a, per_c);
+#undef CI
+#undef CJ
+    fcopy(c->mcell_lag, w->mcell);
+    finalize_cells(c);
+    if (remap_velocity) {
+        vzero(c->acc);
+        dual_face_pass(c, axis_x, dmf, dt);
+        apply_dual_update(c);
+    }
+    /* refresh_normals_impl, remap.cpp:102-114 */
+    if (nmat == 2) {
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) {
+                if (!is_mixed(A(w->k[0], i, j))) continue;
+                double nxv, nyv;
+                if (youngs_normal(c, w->k[1], i, j, &nxv, &nyv)) {
+                    VX(w->normals, i, j) = nxv;
+                    VY(w->normals, i, j) = nyv;
+                }
+            }
+        ghost_cells_v(c, w->normals);
+    }
+}
+
 /* assemble_state, remap.cpp:1075-1089 (make_state defaults, state.cpp:5-23) */
 static void assemble_state(ctx_t* c, double dt) {
     work_t* w = &c->w;
@@ -1357,12 +1507,11 @@ int h2do_set_lagrange(ctx_t* c, const h2d_lagrange* in) {
     return 0;
 }
 
-/* remap_step, remap.cpp:1106-1126 (DirectCF only) */
+/* remap_step, remap.cpp:1106-1126 (DirectCF and AD; not Direct) */
 int h2do_remap_step(ctx_t* c, double dt, int kind, int x_first, int remap_velocity, h2d_remap_diag* diag) {
-    (void)x_first;
-    if (kind != H2D_REMAP_DIRECTCF) {
+    if (kind != H2D_REMAP_DIRECTCF && kind != H2D_REMAP_AD) {
         c->err.kind = H2D_ERR_INVALID;
-        snprintf(c->err.what, sizeof c->err.what, "only the DirectCF remap is implemented");
+        snprintf(c->err.what, sizeof c->err.what, "only the DirectCF and AD remaps are implemented");
         return H2D_ERR_INVALID;
     }
     if (!c->have_lag) {
@@ -1375,7 +1524,12 @@ int h2do_remap_step(ctx_t* c, double dt, int kind, int x_first, int remap_veloci
     c->diag = diag ? &local : NULL;
     if (setjmp(c->jb)) { c->diag = NULL; return c->err.kind; }
     make_work(c);
-    cf_pass(c, dt, remap_velocity);
+    if (kind == H2D_REMAP_AD) {  /* remap.cpp:1110-1115 */
+        directional_pass(c, dt, x_first ? 1 : 0, remap_velocity);
+        directional_pass(c, dt, x_first ? 0 : 1, remap_velocity);
+    } else {
+        cf_pass(c, dt, remap_velocity);
+    }
     assemble_state(c, dt);
     if (diag) *diag = local;
     c->diag = NULL;

@@ -167,3 +167,65 @@ def test_scalar_kernels(ref, orc):
         k = rng.uniform(0, 1)
         lox, loy = rng.uniform(-1, 1, 2)
         assert pr(k, nx, ny, lox, loy, lox + w, loy + h) == po(k, nx, ny, lox, loy, lox + w, loy + h)
+
+
+# ---------------------------------------------------------------- AD engine
+# The alternating-direction split remap (remap.cpp:469-589, 1110-1115), the
+# first "next" row of SURVEY.md 8f.
+
+@pytest.mark.parametrize("case,steps", [
+    (cases.riemann2d(48), 60),
+    (cases.sedov(64), 80),
+    (cases.triple_point(64, 32), 700),
+    (cases.shock_bubble(64), 30),
+])
+def test_run_loop_ad_bitwise(ref, orc, case, steps):
+    sr, so = _both(ref, orc, case.cfg, case.paint())
+    rr, er = helpers.run_capture(sr, steps, case.cfl, abi.REMAP_AD)
+    ro, eo = helpers.run_capture(so, steps, case.cfl, abi.REMAP_AD)
+    assert er == eo
+    assert rr.steps_done == ro.steps_done and np.array_equal(rr.dts, ro.dts)
+    assert rr.diag == ro.diag and rr.floor_count == ro.floor_count
+    assert helpers.bitwise_diff(sr.download(), so.download(), helpers.STATE_FIELDS) == []
+
+
+@pytest.mark.parametrize("bcx,bcy,order,degrade", [(BC_PERIODIC, BC_PERIODIC, 2, 1), (BC_WALL, BC_WALL, 2, 1),
+                                                  (BC_PERIODIC, BC_WALL, 1, 1), (BC_WALL, BC_PERIODIC, 2, 0)])
+@pytest.mark.parametrize("kind", ["gas", "front", "blobs"])
+def test_kinematic_remap_ad_bitwise(ref, orc, bcx, bcy, order, degrade, kind):
+    nmat = 1 if kind == "gas" else 2
+    cfg = make_config(13, 11, 1.0, 1.0, 0.25, -0.5, bcx, bcy, eos=[(EOS_PERFECT, 1.4, 0.0)] * nmat,
+                      face_order=order, interface_degrade=degrade)
+    painted = helpers.random_state(cfg, 11 + order + 3 * degrade, kind, umax=0.25)
+    sr, so = _both(ref, orc, cfg, painted)
+    lag = helpers.kinematic(sr.download())
+    for x_first in (True, False):
+        for vel in (True, False):
+            dr, do = abi.RemapDiag(), abi.RemapDiag()
+            sr2, so2 = _both(ref, orc, cfg, sr.download())
+            sr2.set_lagrange(lag)
+            so2.set_lagrange(lag)
+            sr2.remap_step(1.0, kind=abi.REMAP_AD, x_first=x_first, remap_velocity=vel, diag=dr)
+            so2.remap_step(1.0, kind=abi.REMAP_AD, x_first=x_first, remap_velocity=vel, diag=do)
+            assert helpers.bitwise_diff(sr2.download(), so2.download(), helpers.STATE_FIELDS) == []
+            assert (dr.max_k_violation, dr.k_clip_count, dr.mass_fix_count) == \
+                   (do.max_k_violation, do.k_clip_count, do.mass_fix_count)
+
+
+@pytest.mark.parametrize("scenario", ["cfl_face", "collapsed"])
+def test_error_parity_ad(ref, orc, scenario):
+    cfg = make_config(9, 8, 1.0, 1.0, bc_x=BC_WALL, bc_y=BC_PERIODIC)
+    painted = helpers.random_state(cfg, 3, "gas", umax=0.05)
+    sr, so = _both(ref, orc, cfg, painted)
+    lag = helpers.kinematic(sr.download())
+    if scenario == "cfl_face":
+        lag.u_half[..., 0] = 0.95
+    else:  # converging X face displacements collapse a cell
+        lag.u_half[..., 0] = 0.0
+        lag.u_half[:, 5, 0] = 0.6
+        lag.u_half[:, 6, 0] = -0.6
+    out = []
+    for s in (sr, so):
+        s.set_lagrange(lag)
+        out.append(_err(s, lambda s: s.remap_step(1.0, kind=abi.REMAP_AD)))
+    assert out[0] == out[1] and out[0] is not None
