@@ -46,7 +46,10 @@ struct h2d_ctx {
     double* dt_log = nullptr;    // device dt log of h2d_run
     int dt_log_cap = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one run-loop step per State parity
-    long long graph_kernels = 0;
+    cudaGraphExec_t graph_ad[2][2] = {};            // AD steps per (State parity, x_first)
+    double* ad_mem = nullptr;                       // AD Work planes between the passes
+    AdWork adw{};
+    long long graph_kernels = 0, graph_kernels_ad = 0;
     cudaEvent_t ev[9] = {};
     h2d_block blk{};   // the block of the 2D decomposition (the whole mesh for h2d_create)
     bool is_block = false;
@@ -184,10 +187,40 @@ int decode_error(h2d_ctx* c, bool in_run) {
     case PH_NODAL_MASS: kind = H2D_ERR_NEGMASS; msg = "non-positive nodal mass"; located = true; break;
     case PH_NAN_CELL: kind = H2D_ERR_SIM; msg = "non-finite cell state"; located = true; with_step = true; in_step = 0; break;
     case PH_NAN_NODE: kind = H2D_ERR_SIM; msg = "non-finite velocity"; located = true; with_step = true; in_step = 0; break;
-    default: kind = H2D_ERR_DEVICE; msg = "unknown device error"; break;
+    default:
+        if (ph >= PH_AD_COLLAPSED && ph < PH_AD_COLLAPSED + 10) {  // AD pass 0 / 1 (remap.cpp:469-589)
+            switch ((ph - PH_AD_COLLAPSED) % 5 + PH_AD_COLLAPSED) {
+            case PH_AD_COLLAPSED: kind = H2D_ERR_CFL; msg = "collapsed Lagrangian cell"; located = true; break;
+            case PH_AD_FACE:
+                if (sub & 1) {
+                    kind = H2D_ERR_SIM;
+                    msg = "non-increasing centroid coordinates";
+                } else {
+                    kind = H2D_ERR_CFL;
+                    msg = "CFL violation at face";
+                    located = true;
+                }
+                break;
+            case PH_AD_NEGMASS:
+                kind = H2D_ERR_NEGMASS;
+                msg = sub == 2 ? "non-positive cell mass" : "negative mass";
+                located = true;
+                break;
+            case PH_AD_GRAD_DUAL: kind = H2D_ERR_SIM; msg = "non-increasing centroid coordinates"; break;
+            default: kind = H2D_ERR_NEGMASS; msg = "non-positive nodal mass"; located = true; break;
+            }
+            break;
+        }
+        kind = H2D_ERR_DEVICE;
+        msg = "unknown device error";
+        break;
     }
     std::string w = msg;
-    const int i = located ? inner : -1, j = located ? outer : -1;
+    // the AD scan and face keys are (cross, along, 2 * axis_x + ...): a Y pass
+    // stores (i, j) as (inner, outer) swapped
+    const int adp = ph >= PH_AD_COLLAPSED && ph < PH_AD_COLLAPSED + 10 ? (ph - PH_AD_COLLAPSED) % 5 : -1;
+    const bool ad_y = (adp == 0 || adp == 1) && !(sub >> 1);
+    const int i = located ? (ad_y ? outer : inner) : -1, j = located ? (ad_y ? inner : outer) : -1;
     // SimError::format appends the location only for i >= 0 || j >= 0 (errors.hpp:23)
     if (located && (i >= 0 || j >= 0)) w += " at cell (" + std::to_string(i) + "," + std::to_string(j) + ")";
     const int step = c->hctl->step;
@@ -299,6 +332,57 @@ int ensure_graphs(h2d_ctx* c) {
 int launch_step_graph(h2d_ctx* c, int parity) {
     CK(cudaGraphLaunch(c->graph[parity], c->st));
     add_launches(c->graph_kernels);
+    return 0;
+}
+
+// The AD engine's Work planes (remap.cpp:87-97 between the two directional
+// passes), allocated on first use: m, me, e, k per material, mcell, u, normals.
+int ensure_ad(h2d_ctx* c) {
+    if (c->ad_mem) return 0;
+    const int nm = c->nmat;
+    const size_t pb = (c->fsz * sizeof(double) + 255) & ~size_t(255);
+    const size_t n = 4 * (size_t)nm + 5;
+    CK(cudaMalloc(&c->ad_mem, pb * n));
+    CK(cudaMemsetAsync(c->ad_mem, 0, pb * n, c->st));
+    char* p = reinterpret_cast<char*>(c->ad_mem);
+    auto take = [&]() {
+        double* r = reinterpret_cast<double*>(p);
+        p += pb;
+        return r;
+    };
+    AdWork& W = c->adw;
+    for (int a = 0; a < nm; ++a) {
+        W.m[a] = take();
+        W.me[a] = take();
+        W.e[a] = take();
+        W.k[a] = take();
+    }
+    W.mcell = take();
+    W.ux = take();
+    W.uy = take();
+    W.nrx = take();
+    W.nry = take();
+    return 0;
+}
+
+// AD run-loop steps: the axis order alternates with the step number
+// (harness.cpp:401, x_first = step % 2 == 0), captured per (parity, x_first).
+int ensure_graphs_ad(h2d_ctx* c) {
+    if (int rc = ensure_ad(c)) return rc;
+    for (int p = 0; p < 2; ++p)
+        for (int xf = 0; xf < 2; ++xf) {
+            if (c->graph_ad[p][xf]) continue;
+            cudaGraph_t g = nullptr;
+            const long long before = launch_count();
+            CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+            launch_step_ad(make_dev(c, p, 1), c->adw, xf, c->st);
+            CK(cudaStreamEndCapture(c->st, &g));
+            c->graph_kernels_ad = launch_count() - before;
+            add_launches(-c->graph_kernels_ad);
+            const cudaError_t e = cudaGraphInstantiate(&c->graph_ad[p][xf], g, 0);
+            cudaGraphDestroy(g);
+            CK(e);
+        }
     return 0;
 }
 
@@ -543,6 +627,10 @@ void h2d_destroy(h2d_ctx* c) {
     if (c->flush) cudaFree(c->flush);
     for (auto& g : c->graph)
         if (g) cudaGraphExecDestroy(g);
+    for (auto& gp : c->graph_ad)
+        for (auto& g : gp)
+            if (g) cudaGraphExecDestroy(g);
+    if (c->ad_mem) cudaFree(c->ad_mem);
     if (c->st) cudaStreamSynchronize(c->st);
     if (c->arena) cudaFree(c->arena);
     if (c->ctl) cudaFree(c->ctl);
@@ -699,20 +787,25 @@ int h2d_set_lagrange(h2d_ctx* c, const h2d_lagrange* in) {
     return 0;
 }
 
-int h2d_remap_step(h2d_ctx* c, double dt, int kind, int /*x_first*/, int remap_velocity, h2d_remap_diag* diag) {
+int h2d_remap_step(h2d_ctx* c, double dt, int kind, int x_first, int remap_velocity, h2d_remap_diag* diag) {
     cudaSetDevice(c->device);
-    if (kind != H2D_REMAP_DIRECTCF) {
-        set_err(c, H2D_ERR_INVALID, "only the DirectCF remap is implemented on the device");
+    if (kind != H2D_REMAP_DIRECTCF && !(kind == H2D_REMAP_AD && !c->is_block)) {
+        set_err(c, H2D_ERR_INVALID, "only the DirectCF and (single-domain) AD remaps are implemented on the device");
         return H2D_ERR_INVALID;
     }
     if (!c->have_lag) {
         set_err(c, H2D_ERR_INVALID, "remap_step without a LagrangeResult");
         return H2D_ERR_INVALID;
     }
+    if (kind == H2D_REMAP_AD)
+        if (int rc = ensure_ad(c)) return rc;
     if (int rc = ctl_reset(c)) return rc;
     const Dev d = make_dev(c, c->cur, remap_velocity != 0);
     launch_begin(c->ctl, 1, dt, c->st);
-    launch_remap(d, c->st);
+    if (kind == H2D_REMAP_AD)
+        launch_remap_ad(d, c->adw, x_first != 0, remap_velocity != 0, 0, c->st);
+    else
+        launch_remap(d, c->st);
     launch_commit(c->ctl, 1, c->st);
     if (int rc = check_launch(c)) return rc;
     if (int rc = ctl_pull(c)) return rc;
@@ -730,8 +823,9 @@ int h2d_remap_step(h2d_ctx* c, double dt, int kind, int /*x_first*/, int remap_v
 int h2d_run(h2d_ctx* c, h2d_run_args* a) {
     cudaSetDevice(c->device);
     a->steps_done = 0;
-    if (a->remap_kind != H2D_REMAP_DIRECTCF) {
-        set_err(c, H2D_ERR_INVALID, "only the DirectCF remap is implemented on the device");
+    const bool ad = a->remap_kind == H2D_REMAP_AD;
+    if (a->remap_kind != H2D_REMAP_DIRECTCF && !(ad && !c->is_block)) {
+        set_err(c, H2D_ERR_INVALID, "only the DirectCF and (single-domain) AD remaps are implemented on the device");
         return H2D_ERR_INVALID;
     }
     const int cap = a->max_steps > 0 ? a->max_steps : 4096;
@@ -756,7 +850,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
     if (int rc = ctl_push(c)) return rc;
     int parity = c->cur;
     int rc = 0;
-    if ((rc = ensure_graphs(c))) return rc;
+    if ((rc = ad ? ensure_graphs_ad(c) : ensure_graphs(c))) return rc;
     enqueue_cfl_next(c);
     // Launch in chunks; the device control block turns every kernel after the
     // loop condition fails (or after an error) into a no-op.
@@ -767,8 +861,14 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
             if (left <= 0) break;
             chunk = left < chunk ? left : chunk;
         }
+        const int step0 = h.step;
         for (int q = 0; q < chunk; ++q) {
-            if ((rc = launch_step_graph(c, parity))) return rc;
+            if (ad) {  // x_first = s.step % 2 == 0 (harness.cpp:401)
+                CK(cudaGraphLaunch(c->graph_ad[parity][(step0 + q) % 2 == 0], c->st));
+                add_launches(c->graph_kernels_ad);
+            } else if ((rc = launch_step_graph(c, parity))) {
+                return rc;
+            }
             parity ^= 1;
         }
         if ((rc = check_launch(c))) return rc;

@@ -41,8 +41,17 @@ enum Phase : uint32_t {
     PH_GRAD_DUALY = 15,
     PH_GRAD_DUALC = 16,
     PH_NODAL_MASS = 17,   // apply_dual_update                (remap.cpp:455)
-    PH_NAN_CELL = 18,     // nan_scan                         (harness.cpp:347-358)
-    PH_NAN_NODE = 19,
+    // AD split remap, per directional pass p = 0, 1 (phase + 5 p): the
+    // collapsed-cell scan (remap.cpp:484), the face loop (CFL :532-535 and
+    // the limiter throw, in face order), finalize_cells, the dual faces,
+    // apply_dual_update
+    PH_AD_COLLAPSED = 20,
+    PH_AD_FACE = 21,
+    PH_AD_NEGMASS = 22,
+    PH_AD_GRAD_DUAL = 23,
+    PH_AD_NODAL = 24,
+    PH_NAN_CELL = 30,     // nan_scan                         (harness.cpp:347-358)
+    PH_NAN_NODE = 31,
 };
 
 H2D_DEV uint64_t ekey(uint32_t ph, int outer, int inner, int sub) {

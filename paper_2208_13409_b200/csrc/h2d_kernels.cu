@@ -1058,7 +1058,8 @@ __global__ void k_ghost_multi(Dev d, FieldList cells, FieldList nodes, int flux,
 // remap tile: fractions, clipping, snapping, sliver capture, energies
 template <int NM>
 __device__ __forceinline__ void finalize_cell(const Dev& d, const Rng& rg, int i, int j, int c, int tx, bool own,
-                                              double* m, double* me, const double* va) {
+                                              double* m, double* me, const double* va,
+                                              uint32_t ph_negmass = PH_NEGMASS) {
     double k[2] = {1.0, 0.0};
     uint8_t sl = 0;
     if (NM == 2) {
@@ -1109,7 +1110,7 @@ __device__ __forceinline__ void finalize_cell(const Dev& d, const Rng& rg, int i
         mtot += ma;
     }
     if (bad_sub < 0 && mtot <= 0.0) bad_sub = 2;
-    if (bad_sub >= 0 && own) raise(d.ctl, ekey(PH_NEGMASS, j, i, bad_sub));
+    if (bad_sub >= 0 && own) raise(d.ctl, ekey(ph_negmass, j, i, bad_sub));
     d.mcell[c] = mtot;
     if (NM == 2) {
         d.sliver[c] = sl;
@@ -1593,7 +1594,8 @@ __device__ __forceinline__ double dual_face_value(const Dev& d, const double* u,
 // dual_face_pass, remap.cpp:408-442: one thread per dual face. AX = 1: X
 // (ia = i node, ic = j), AX = 0: Y (ia = j, ic = i); stored at (i, j).
 template <int AX>
-__device__ __forceinline__ bool dual_face_val(const Dev& d, int i, int j, double& mx, double& my) {
+__device__ __forceinline__ bool dual_face_val(const Dev& d, int i, int j, double& mx, double& my,
+                                              uint32_t ph = AX ? PH_GRAD_DUALX : PH_GRAD_DUALY) {
     const int ia = AX ? i : j, ic = AX ? j : i;
     const int per_a = AX ? d.per_x : d.per_y;
     const int s = ix(d, i, j);
@@ -1613,7 +1615,7 @@ __device__ __forceinline__ bool dual_face_val(const Dev& d, int i, int j, double
         bool bad = false;
         const double ufx = dual_face_value(d, d.ulx, AX, ia_d, ic, dt, wa, sgn, ufdt, bad);
         const double ufy = dual_face_value(d, d.uly, AX, ia_d, ic, dt, wa, sgn, ufdt, bad);
-        if (bad && own_node(d, i, j)) raise(d.ctl, ekey(AX ? PH_GRAD_DUALX : PH_GRAD_DUALY, ic, ia, 0));
+        if (bad && own_node(d, i, j)) raise(d.ctl, ekey(ph, ic, ia, 0));
         mx = ufx * dm;
         my = ufy * dm;
     }
@@ -2251,6 +2253,352 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// AD split remap (remap.cpp:469-589), the first "next" row of SURVEY.md 8f:
+// one directional pass along AX (1 = X, 0 = Y) per kernel sequence. Work
+// inputs come from an AdIO (the State + LagrangeResult for pass 0, the AdWork
+// of pass 0 for pass 1); outputs go to the next-state / Work planes of the Dev
+// the pass is launched with, so finalize_cell, k_slivers and the ghost fills
+// are shared with DirectCF.
+// ---------------------------------------------------------------------------
+template <int NM, int AX>
+__global__ void __launch_bounds__(RTX * RTY, 3) k_ad_tile(Dev d, AdIO w) {
+    pdl_enter();
+    constexpr int CW = AX ? RTX + 4 : RTX, CH = AX ? RTY : RTY + 4;  // cells: along-axis halo of 2
+    constexpr int FW = AX ? RTX + 5 : RTX, FH = AX ? RTY : RTY + 5;  // along-axis faces of those cells
+    constexpr int NCR = CW * CH, NFR = FW * FH;
+    constexpr int NIF = AX ? (RTX + 1) * RTY : RTX * (RTY + 1);  // the tile's own faces
+    __shared__ double s_fd[NFR];
+    __shared__ double s_vl[NCR], s_xl[NCR], s_wl[NCR], s_rho[NM][NCR], s_e[NM][NCR], s_k[NM][NCR];
+    __shared__ double s_ifd[NM == 2 ? NCR : 1];
+    __shared__ double s_it[3][NM][NIF];
+    __shared__ int s_halt;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
+    const int nx = d.nx, ny = d.ny;
+    const Rng rg = d.r_gath;
+    const int i0 = rg.i0 + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
+    const double dt = step_dt(d.ctl);
+    const double cv = d.cv;
+    const int na = AX ? nx : ny, nc = AX ? ny : nx;
+    const double wa = AX ? d.dx : d.dy, wc = AX ? d.dy : d.dx, origin = AX ? d.x0 : d.y0;
+    const double* uh = AX ? d.uhx : d.uhy;
+    const uint32_t pb = 5u * (uint32_t)w.pass;
+    // (along, cross) -> region slots
+    auto F = [&](int ia, int ic) { return AX ? (ia - i0 + 2) + (ic - j0) * FW : (ic - i0) + (ia - j0 + 2) * FW; };
+    auto Cs = [&](int ia, int ic) { return AX ? (ia - i0 + 2) + (ic - j0) * CW : (ic - i0) + (ia - j0 + 2) * CW; };
+    // face-mean displacements, make_axis_geom (remap.cpp:306-313)
+    auto fd_at = [&](int ia, int ic) -> double {
+        const int n0i = AX ? ia : ic, n0j = AX ? ic : ia;
+        const int n1i = AX ? ia : ic + 1, n1j = AX ? ic + 1 : ia;
+        if (!in(d.win_n, n0i, n0j) || !in(d.win_n, n1i, n1j)) return 0.0;
+        return 0.5 * (uh[ix(d, n0i, n0j)] + uh[ix(d, n1i, n1j)]) * dt;
+    };
+    // ---- stage: face displacements and the cells' Work inputs
+    for (int t = tid; t < NFR; t += RTX * RTY) {
+        const int ia = AX ? i0 - 2 + t % FW : j0 - 2 + t / FW, ic = AX ? j0 + t / FW : i0 + t % FW;
+        s_fd[t] = fd_at(ia, ic);
+    }
+    for (int t = tid; t < NCR; t += RTX * RTY) {
+        const int i = (AX ? i0 - 2 : i0) + t % CW, j = (AX ? j0 : j0 - 2) + t / CW;
+        if (!in(d.win_c, i, j)) continue;
+        const int c = ix(d, i, j);
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            s_rho[a][t] = w.m[a][c];
+            s_e[a][t] = w.e[a][c];
+            s_k[a][t] = w.k[a][c];
+        }
+    }
+    __syncthreads();
+    // ---- cells: 1D Lagrangian volume, densities, centroid / width, interfaces
+    // (remap.cpp:478-514; the collapsed scan covers [-G, n+G) both ways)
+    for (int t = tid; t < NCR; t += RTX * RTY) {
+        const int i = (AX ? i0 - 2 : i0) + t % CW, j = (AX ? j0 : j0 - 2) + t / CW;
+        if (!in(d.win_c, i, j)) continue;
+        const int ia = AX ? i : j, ic = AX ? j : i;
+        if (ia + 1 > (AX ? d.win_n.i1 - 1 : d.win_n.j1 - 1)) continue;
+        const double dl = s_fd[F(ia, ic)], dr = s_fd[F(ia + 1, ic)];
+        const double v = cv + (dr - dl) * wc;
+        if (v <= 0.0 && ia >= -G && ia < na + G && ic >= -G && ic < nc + G)
+            raise(d.ctl, ekey(PH_AD_COLLAPSED + pb, ic, ia, 2 * AX));
+        s_vl[t] = v;
+        s_xl[t] = origin + (ia + 0.5) * wa + 0.5 * (dl + dr);
+        s_wl[t] = wa + (dr - dl);
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            const double ka = s_k[a][t];
+            s_rho[a][t] = ka > 0.0 ? s_rho[a][t] / (ka * v) : 0.0;
+        }
+        if (NM == 2) {
+            const double k0 = s_k[0][t];
+            double dd = 0.0;
+            if (is_mixed(k0)) {
+                const double cx = d.x0 + (i + 0.5) * d.dx, cy = d.y0 + (j + 0.5) * d.dy;
+                const int g = ix(d, i, j);
+                if (AX)
+                    dd = place_interface(k0, w.nrx[g], w.nry[g], cx - 0.5 * d.dx + dl, cy - 0.5 * d.dy,
+                                         cx + 0.5 * d.dx + dr, cy + 0.5 * d.dy);
+                else
+                    dd = place_interface(k0, w.nrx[g], w.nry[g], cx - 0.5 * d.dx, cy - 0.5 * d.dy + dl,
+                                         cx + 0.5 * d.dx, cy + 0.5 * d.dy + dr);
+            }
+            s_ifd[t] = dd;
+        }
+    }
+    // the scan's cross-axis ghost rows (columns) lie outside every tile: the
+    // tiles on the cross boundary check them from u_half's ghost layers
+    {
+        const int c0 = AX ? j0 : i0, c1 = AX ? min(j0 + RTY, rg.j1) : min(i0 + RTX, rg.i1);
+        const int a0 = AX ? i0 - 2 : j0 - 2, a1 = AX ? i0 + RTX + 2 : j0 + RTY + 2;
+        const bool lo = c0 == 0, hi = c1 == nc;
+        if (lo || hi) {
+            const int nrow = (lo ? 2 : 0) + (hi ? 2 : 0);
+            for (int t = tid; t < nrow * (a1 - a0); t += RTX * RTY) {
+                const int r = t / (a1 - a0), ia = a0 + t % (a1 - a0);
+                const int ic = (lo && r < 2) ? -2 + r : nc + (r - (lo ? 2 : 0));
+                if (ia < -G || ia >= na + G) continue;
+                const double v = cv + (fd_at(ia + 1, ic) - fd_at(ia, ic)) * wc;
+                if (v <= 0.0) raise(d.ctl, ekey(PH_AD_COLLAPSED + pb, ic, ia, 2 * AX));
+            }
+        }
+    }
+    __syncthreads();
+    // ---- the tile's faces along AX (remap.cpp:526-577)
+    for (int t = tid; t < NIF; t += RTX * RTY) {
+        const int ia = AX ? i0 + t % (RTX + 1) : j0 + t / RTX, ic = AX ? j0 + t / (RTX + 1) : i0 + t % RTX;
+        double dm[2] = {0.0, 0.0}, dme[2] = {0.0, 0.0}, dva[2] = {0.0, 0.0};
+        const bool valid = AX ? (ia <= min(nx, rg.i1) && ic < min(ny, rg.j1)) : (ic < min(nx, rg.i1) && ia <= min(ny, rg.j1));
+        if (valid) {
+            const double fdv = s_fd[F(ia, ic)];
+            const double dvol = fdv * wc;
+            double dmtot = 0.0;
+            if (dvol != 0.0) {
+                if (fabs(dvol) > kCflFrac * cv) raise(d.ctl, ekey(PH_AD_FACE + pb, ic, ia, 2 * AX));
+                const int ia_d = dvol > 0.0 ? ia - 1 : ia;
+                const double sgn = dvol > 0.0 ? 1.0 : -1.0;
+                const int cdi = AX ? ia_d : ic, cdj = AX ? ic : ia_d;
+                const int cd = Cs(ia_d, ic);
+                // face_flux_box (remap.cpp:325-334) and split_flux (:254-268)
+                double blox, bloy, bhix, bhiy;
+                if (AX) {
+                    const double xf = d.x0 + ia * d.dx;
+                    blox = rmin(xf, xf + fdv);
+                    bloy = d.y0 + ic * d.dy;
+                    bhix = rmax(xf, xf + fdv);
+                    bhiy = d.y0 + (ic + 1) * d.dy;
+                } else {
+                    const double yf = d.y0 + ia * d.dy;
+                    blox = d.x0 + ic * d.dx;
+                    bloy = rmin(yf, yf + fdv);
+                    bhix = d.x0 + (ic + 1) * d.dx;
+                    bhiy = rmax(yf, yf + fdv);
+                }
+                dva[0] = dvol;
+                if (NM == 2) {
+                    const double k0 = s_k[0][cd];
+                    if (is_mixed(k0)) {
+                        const int g = ix(d, cdi, cdj);
+                        const double nxv = w.nrx[g], nyv = w.nry[g], dd = s_ifd[cd];
+                        const double dl = s_fd[F(ia_d, ic)], dr = s_fd[F(ia_d + 1, ic)];
+                        const double cx = d.x0 + (cdi + 0.5) * d.dx, cy = d.y0 + (cdj + 0.5) * d.dy;
+                        const double lox = AX ? cx - 0.5 * d.dx + dl : cx - 0.5 * d.dx;
+                        const double loy = AX ? cy - 0.5 * d.dy : cy - 0.5 * d.dy + dl;
+                        const double hix = AX ? cx + 0.5 * d.dx + dr : cx + 0.5 * d.dx;
+                        const double hiy = AX ? cy + 0.5 * d.dy : cy + 0.5 * d.dy + dr;
+                        const double rcx = 0.5 * (lox + hix), rcy = 0.5 * (loy + hiy);
+                        const double bcx = 0.5 * (blox + bhix), bcy = 0.5 * (bloy + bhiy);
+                        const double bw = bhix - blox, bh = bhiy - bloy;
+                        const double area = bw * bh;
+                        double f0;
+                        if (!(area > 0.0)) {
+                            const double sd = (nxv * (bcx - rcx) + nyv * (bcy - rcy)) - dd;
+                            f0 = sd <= 0.0 ? 1.0 : 0.0;
+                        } else {
+                            const double dbox = dd - (nxv * (bcx - rcx) + nyv * (bcy - rcy));
+                            f0 = clipped_fraction(bw, bh, nxv, nyv, dbox);
+                        }
+                        dva[0] = f0 * dvol;
+                        dva[1] = dvol - dva[0];
+                    } else if (k0 < 0.5) {
+                        dva[0] = 0.0;
+                        dva[1] = dvol;
+                    }
+                }
+                bool bad = false;
+                const int cm = Cs(ia_d - 1, ic), cp = Cs(ia_d + 1, ic);
+#pragma unroll
+                for (int a = 0; a < NM; ++a) {
+                    if (dva[a] == 0.0) continue;
+                    int ord = d.face_order;
+                    if (ord == 2 && NM == 2 && d.degrade &&
+                        (s_k[a][cm] < 1.0 - kPureTol || s_k[a][cd] < 1.0 - kPureTol || s_k[a][cp] < 1.0 - kPureTol))
+                        ord = 1;
+                    double rf, ef;
+                    if (ord <= 1) {
+                        rf = s_rho[a][cd];
+                        ef = s_e[a][cd];
+                    } else {
+                        rf = face_value2(s_rho[a][cm], s_rho[a][cd], s_rho[a][cp], s_xl[cm], s_xl[cd], s_xl[cp], sgn,
+                                         s_wl[cd], fdv, bad);
+                        ef = face_value2(s_e[a][cm], s_e[a][cd], s_e[a][cp], s_xl[cm], s_xl[cd], s_xl[cp], sgn,
+                                         s_wl[cd], fdv, bad);
+                    }
+                    dm[a] = rf * dva[a];
+                    dme[a] = rf * ef * dva[a];
+                    dmtot += dm[a];
+                }
+                if (bad) raise(d.ctl, ekey(PH_AD_FACE + pb, ic, ia, 2 * AX + 1));
+            }
+            const bool ownf = AX ? (ia < i0 + RTX || ia == min(nx, rg.i1)) : (ia < j0 + RTY || ia == min(ny, rg.j1));
+            if (ownf) (AX ? d.dmx : d.dmy)[AX ? ix(d, ia, ic) : ix(d, ic, ia)] = dmtot;
+        }
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            s_it[0][a][t] = dm[a];
+            s_it[1][a][t] = dme[a];
+            s_it[2][a][t] = dva[a];
+        }
+    }
+    __syncthreads();
+    // ---- gather (left face +, right face -, remap.cpp:830-838) and finalize
+    const int tx = tid % RTX, ty = tid / RTX;
+    const int i = i0 + tx, j = j0 + ty;
+    if (!in(rg, i, j)) return;
+    const int c = ix(d, i, j);
+    const double vl = s_vl[Cs(AX ? i : j, AX ? j : i)];
+    const int ql = AX ? tx + ty * (RTX + 1) : tx + ty * RTX, qr = AX ? ql + 1 : ql + RTX;
+    double m[2], me[2], va[2];
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        const double m0 = w.m[a][c];
+        double mm = m0, mme = w.me_from_e ? m0 * w.e[a][c] : w.me[a][c], vv = w.k[a][c] * vl;
+        if (s_it[2][a][ql] != 0.0) {
+            mm += s_it[0][a][ql];
+            mme += s_it[1][a][ql];
+            vv += s_it[2][a][ql];
+        }
+        if (s_it[2][a][qr] != 0.0) {
+            mm += -s_it[0][a][qr];
+            mme += -s_it[1][a][qr];
+            vv += -s_it[2][a][qr];
+        }
+        m[a] = mm;
+        me[a] = mme;
+        va[a] = vv;
+    }
+    finalize_cell<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va, PH_AD_NEGMASS + pb);
+}
+
+// AD dual faces of one pass (dual_face_pass along AX, remap.cpp:408-442); the
+// Dev's u_lag planes are the pass's Work velocities
+template <int AX>
+__global__ void __launch_bounds__(128, 8) k_ad_dual(Dev d, int pass) {
+    pdl_enter();
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, d.r_dual.i0, d.r_dual.j0);
+    const int iend = d.per_x ? d.nx - 1 : d.nx, jend = d.per_y ? d.ny - 1 : d.ny;
+    if (!in(d.r_dual, i, j) || i < 0 || j < 0 || i > iend || j > jend) return;
+    double mx, my;
+    const bool on = dual_face_val<AX>(d, i, j, mx, my, PH_AD_GRAD_DUAL + 5u * (uint32_t)pass);
+    const int s = ix(d, i, j);
+    (AX ? d.dfx_x : d.dfy_x)[s] = mx;
+    (AX ? d.dfx_y : d.dfy_y)[s] = my;
+    d.dflag[AX ? 0 : 1][s] = on;
+}
+
+// AD MomAcc gather (one axis, face-loop order incl. the periodic seam) and
+// apply_dual_update (remap.cpp:444-464) with mcell_lag = the pass's input mcell
+template <int AX>
+__global__ void k_ad_node(Dev d, AdIO w) {
+    pdl_enter();
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, d.r_node.i0, d.r_node.j0);
+    const int nx = d.nx, ny = d.ny;
+    if (!in(d.r_node, i, j) || i < 0 || j < 0 || i > nx || j > ny) return;
+    const int iend = d.per_x ? nx - 1 : nx, jend = d.per_y ? ny - 1 : ny;
+    const int si = (d.per_x && i == nx) ? 0 : i, sj = (d.per_y && j == ny) ? 0 : j;
+    const int s = ix(d, si, sj);
+    double ax = 0.0, ay = 0.0;
+    {  // face ia joins nodes (ia-1, ia): + to node ia, - to the node ia-1 wraps to
+        const int n = AX ? nx : ny;
+        const int per = AX ? d.per_x : d.per_y;
+        const int hi = AX ? iend : jend, lo = per ? 0 : 1;
+        const int along = AX ? si : sj, cross = AX ? sj : si;
+        const double* fx_ = AX ? d.dfx_x : d.dfy_x;
+        const double* fy_ = AX ? d.dfx_y : d.dfy_y;
+        const uint8_t* fl = d.dflag[AX ? 0 : 1];
+        auto at = [&](int a) { return AX ? ix(d, a, cross) : ix(d, cross, a); };
+        int am = along + 1;
+        if (per && am == n) am = 0;
+        const bool ap = along >= lo && along <= hi && fl[at(along)];
+        const bool an = am >= lo && am <= hi && fl[at(am)];
+        const bool minus_first = an && am < along;
+        if (minus_first) {
+            ax += -fx_[at(am)];
+            ay += -fy_[at(am)];
+        }
+        if (ap) {
+            ax += fx_[at(along)];
+            ay += fy_[at(along)];
+        }
+        if (an && !minus_first) {
+            ax += -fx_[at(am)];
+            ay += -fy_[at(am)];
+        }
+    }
+    auto ml = [&](int ci, int cj) {
+        const int c = ix(d, ci, cj);
+        if (w.mcell) return w.mcell[c];
+        double mc = 0.0;  // make_work's mcell (remap.cpp:133-138)
+        for (int a = 0; a < d.nmat; ++a) mc += w.m[a][c];
+        return mc;
+    };
+    const double mp_lag = 0.25 * (ml(si - 1, sj - 1) + ml(si, sj - 1) + ml(si - 1, sj) + ml(si, sj));
+    const double mp_new =
+        0.25 * (d.mcell[ix(d, si - 1, sj - 1)] + d.mcell[ix(d, si, sj - 1)] + d.mcell[ix(d, si - 1, sj)] + d.mcell[s]);
+    if (mp_new <= 0.0 && si == i && sj == j && own_node(d, i, j))
+        raise(d.ctl, ekey(PH_AD_NODAL + 5u * (uint32_t)w.pass, j, i, 0));
+    const double inv = 1.0 / mp_new;
+    const int o = ix(d, i, j);
+    double ux = inv * (mp_lag * w.ux[s] + ax), uy = inv * (mp_lag * w.uy[s] + ay);
+    if (!d.per_x && (i == 0 || i == nx)) ux = 0.0;  // fill_ghost_nodes wall zeroing (remap.cpp:462)
+    if (!d.per_y && (j == 0 || j == ny)) uy = 0.0;
+    d.nux[o] = ux;
+    d.nuy[o] = uy;
+    d.unrm[o] = sqrt(ux * ux + uy * uy);
+}
+
+// refresh_normals_impl after AD pass 0 (remap.cpp:102-114): youngs normals of
+// the pass's new fractions where mixed, else the pass's input normals
+__global__ void k_ad_normals(Dev d, AdIO w) {
+    pdl_enter();
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, 0, 0);
+    if (i >= d.nx || j >= d.ny || !in(d.win_c, i, j)) return;
+    const int c = ix(d, i, j);
+    double nrx = w.nrx[c], nry = w.nry[c];
+    if (is_mixed(d.nk[0][c])) {
+        auto K = [&](int ii, int jj) { return d.nk[1][ix(d, ii, jj)]; };
+        auto col = [&](int ii) { return K(ii, j - 1) + 2.0 * K(ii, j) + K(ii, j + 1); };
+        auto row = [&](int jj) { return K(i - 1, jj) + 2.0 * K(i, jj) + K(i + 1, jj); };
+        const double gx = div_dx(d, col(i + 1) - col(i - 1), 8.0);
+        const double gy = div_dy(d, row(j + 1) - row(j - 1), 8.0);
+        const double g = sqrt(gx * gx + gy * gy);
+        if (!(g < 1e-300)) {
+            nrx = gx / g;
+            nry = gy / g;
+        }
+    }
+    d.nnrx[c] = nrx;
+    d.nnry[c] = nry;
+}
+
 // AoS <-> SoA staging for Vec2 fields (reference layout pitch W = n1 + 2G).
 __global__ void k_deinterleave(const double* src, double* x, double* y, int W, int H, int P) {
     pdl_enter();
@@ -2492,6 +2840,105 @@ void launch_step(const Dev& d, cudaStream_t s) {
     launch_lagrange_run(d, s);
     launch_remap_core(d, s);
     post_and_ghosts(d, 1, s);
+    pdl(k_commit_finish, dim3(1), dim3(1), 0, s, d.ctl);
+}
+
+// One AD directional pass (remap.cpp:469-589) writing into dout's planes.
+static void launch_ad_pass(const Dev& dout, const AdIO& w, int remap_velocity, cudaStream_t s) {
+    const dim3 gft = tiles_of(dout.r_gath, RTX, RTY);
+    if (dout.nmat == 2) {
+        if (w.axis_x)
+            pdl(k_ad_tile<2, 1>, gft, dim3(RTX * RTY), 0, s, dout, w);
+        else
+            pdl(k_ad_tile<2, 0>, gft, dim3(RTX * RTY), 0, s, dout, w);
+    } else {
+        if (w.axis_x)
+            pdl(k_ad_tile<1, 1>, gft, dim3(RTX * RTY), 0, s, dout, w);
+        else
+            pdl(k_ad_tile<1, 0>, gft, dim3(RTX * RTY), 0, s, dout, w);
+    }
+    launch_remap_slivers(dout, s);  // slivers + Work / face-flux ghosts (finalize_cells tail, :371-382)
+    FieldList none{};
+    if (remap_velocity) {
+        Dev dd = dout;  // the dual faces read the pass's Work velocities
+        dd.ulx = const_cast<double*>(w.ux);
+        dd.uly = const_cast<double*>(w.uy);
+        if (w.axis_x) {
+            pdl(k_ad_dual<1>, grid_of(dd.r_dual), blk2(), 0, s, dd, w.pass);
+            pdl(k_ad_node<1>, grid_of(dd.r_node), blk2(), 0, s, dd, w);
+        } else {
+            pdl(k_ad_dual<0>, grid_of(dd.r_dual), blk2(), 0, s, dd, w.pass);
+            pdl(k_ad_node<0>, grid_of(dd.r_node), blk2(), 0, s, dd, w);
+        }
+        FieldList fu{};
+        fu.n = 2;
+        fu.f[0] = dout.nux;
+        fu.f[1] = dout.nuy;
+        launch_ghost_multi(dout, none, fu, 0, 1, s);
+    }
+    if (dout.nmat == 2 && w.pass == 0) {  // pass 1's normals are k_post's
+        pdl(k_ad_normals, grid_rect(dout.nx, dout.ny), blk2(), 0, s, dout, w);
+        FieldList fc{};
+        fc.n = 2;
+        fc.f[0] = dout.nnrx;
+        fc.f[1] = dout.nnry;
+        launch_ghost_multi(dout, fc, none, 0, 1, s);
+    }
+}
+
+void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_velocity, int run_loop, cudaStream_t s) {
+    const int nm = d.nmat;
+    Dev d0 = d;  // pass 0 writes the AdWork
+    AdIO w0{}, w1{};
+    for (int a = 0; a < nm; ++a) {
+        d0.nm[a] = W.m[a];
+        d0.ne[a] = W.e[a];
+        d0.nk[a] = W.k[a];
+        d0.me[a] = W.me[a];
+        w0.m[a] = d.m[a];
+        w0.e[a] = d.el[a];
+        w0.k[a] = d.k[a];
+        w1.m[a] = W.m[a];
+        w1.me[a] = W.me[a];
+        w1.e[a] = W.e[a];
+        w1.k[a] = W.k[a];
+    }
+    d0.mcell = W.mcell;
+    d0.nux = W.ux;
+    d0.nuy = W.uy;
+    d0.nnrx = W.nrx;
+    d0.nnry = W.nry;
+    w0.nrx = d.nrx;
+    w0.nry = d.nry;
+    w0.mcell = nullptr;
+    w0.ux = d.ulx;
+    w0.uy = d.uly;
+    w0.me_from_e = 1;
+    w0.pass = 0;
+    w0.axis_x = x_first ? 1 : 0;
+    launch_ad_pass(d0, w0, remap_velocity, s);
+    w1.nrx = nm == 2 ? W.nrx : d.nrx;
+    w1.nry = nm == 2 ? W.nry : d.nry;
+    w1.mcell = W.mcell;
+    w1.ux = remap_velocity ? W.ux : d.ulx;
+    w1.uy = remap_velocity ? W.uy : d.uly;
+    w1.me_from_e = 0;
+    w1.pass = 1;
+    w1.axis_x = x_first ? 0 : 1;
+    launch_ad_pass(d, w1, remap_velocity, s);
+    if (!remap_velocity) pdl(k_copy_u, grid_of(d.win_n), blk2(), 0, s, d);  // w.u = u_lag (remap.cpp:130)
+    Dev dp = d;  // refresh_normals_impl of pass 1 starts from pass 0's normals
+    if (nm == 2) {
+        dp.nrx = W.nrx;
+        dp.nry = W.nry;
+    }
+    post_and_ghosts(dp, run_loop, s);
+}
+
+void launch_step_ad(const Dev& d, const AdWork& W, int x_first, cudaStream_t s) {
+    pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
+    launch_lagrange_run(d, s);
+    launch_remap_ad(d, W, x_first, 1, 1, s);
     pdl(k_commit_finish, dim3(1), dim3(1), 0, s, d.ctl);
 }
 

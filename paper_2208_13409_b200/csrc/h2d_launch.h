@@ -12,6 +12,21 @@ struct FieldList {
     int respect_halt;
 };
 
+// Work planes between the two passes of the AD split remap (remap.cpp:87-97):
+// pass 0 writes them, pass 1 reads them.
+struct AdWork {
+    double *m[2], *me[2], *e[2], *k[2], *nrx, *nry, *mcell, *ux, *uy;
+};
+
+// Work inputs of one AD directional pass: pass 0 reads the State and the
+// LagrangeResult (make_work, remap.cpp:116-140), pass 1 the AdWork of pass 0.
+struct AdIO {
+    const double *m[2], *me[2], *e[2], *k[2], *nrx, *nry, *mcell, *ux, *uy;
+    int me_from_e;  // pass 0: w.me = m * e_lag (remap.cpp:128); mcell == nullptr: sum of m
+    int pass;       // 0 / 1 (error phases PH_AD_* + 5 pass)
+    int axis_x;     // 1: X pass, 0: Y pass
+};
+
 long long launch_count();
 void add_launches(long long n);  // kernels replayed by a CUDA graph launch
 void launch_begin(Ctl* c, int mode, double dt, cudaStream_t s);
@@ -32,6 +47,11 @@ void launch_remap_slivers(const Dev& d, cudaStream_t s);
 void launch_remap_dual(const Dev& d, cudaStream_t s);
 void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s);
 void launch_step(const Dev& d, cudaStream_t s);  // one run-loop step
+// AD split remap: both directional passes of remap_step(AD) (remap.cpp:1110-1115)
+// leaving the next State's Work in `d`'s next-state planes, then the post
+// kernels (run_loop: also the NaN scan and the next wave speed)
+void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_velocity, int run_loop, cudaStream_t s);
+void launch_step_ad(const Dev& d, const AdWork& W, int x_first, cudaStream_t s);  // one AD run-loop step
 void launch_cfl_next(const Dev& d, cudaStream_t s);
 void launch_step_start(const Dev& d, cudaStream_t s);
 void launch_commit_finish(const Dev& d, cudaStream_t s);               // wave speed of the current State

@@ -265,8 +265,8 @@ LagrangeResult lagrange_step(const State& s, const MaterialSet& mats, double dt,
 
 State remap_step(const State& s, const MaterialSet& mats, const LagrangeResult& lag, double dt, RemapKind kind,
                  const ReconConfig& rc, bool x_first, bool remap_velocity, RemapDiag* diag) {
-    if (kind != RemapKind::DirectCF)
-        throw std::invalid_argument("hydro2d-b200 implements the DirectCF remap only (RemapKind::DirectCF)");
+    if (kind == RemapKind::Direct)
+        throw std::invalid_argument("hydro2d-b200 implements the DirectCF and AD remaps (not RemapKind::Direct)");
     h2d_ctx* h = load(s, &mats, {}, rc);
     h2d_lagrange in;
     std::memset(&in, 0, sizeof in);
@@ -283,7 +283,8 @@ State remap_step(const State& s, const MaterialSet& mats, const LagrangeResult& 
         d.k_clip_count = diag->k_clip_count;
         d.mass_fix_count = diag->mass_fix_count;
     }
-    check(h, h2d_remap_step(h, dt, H2D_REMAP_DIRECTCF, x_first ? 1 : 0, remap_velocity ? 1 : 0,
+    check(h, h2d_remap_step(h, dt, kind == RemapKind::AD ? H2D_REMAP_AD : H2D_REMAP_DIRECTCF, x_first ? 1 : 0,
+                            remap_velocity ? 1 : 0,
                             diag ? &d : nullptr));
     if (diag) {
         diag->max_k_violation = d.max_k_violation;

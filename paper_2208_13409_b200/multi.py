@@ -188,7 +188,7 @@ def phase_of(key: int) -> int:
     return key >> 58
 
 
-PH_NAN_CELL = 18
+PH_NAN_CELL = 30  # h2d_device.cuh Phase
 
 
 class LocalTransport:

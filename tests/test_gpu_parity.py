@@ -188,3 +188,71 @@ def test_c1_full_size(gpu, orc):
     assert rg.steps_done == ro.steps_done == 100
     assert np.array_equal(rg.dts, ro.dts)
     assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS) == []
+
+
+# ---------------------------------------------------------------- AD engine
+# The alternating-direction split remap on the device (remap.cpp:469-589,
+# 1110-1115) against the oracle, which tests/test_oracle_vs_reference.py pins
+# to the reference.
+
+@pytest.mark.parametrize("case,steps", [
+    (cases.riemann2d(48), 60),
+    (cases.sedov(64), 80),
+    (cases.triple_point(64, 32), 700),
+    (cases.shock_bubble(64), 30),
+    (cases.triple_point(100, 44), 120),
+])
+def test_run_loop_ad_bitwise(gpu, orc, case, steps):
+    sg, so = _pair(gpu, orc, case.cfg, case.paint())
+    rg, eg = helpers.run_capture(sg, steps, case.cfl, abi.REMAP_AD)
+    ro, eo = helpers.run_capture(so, steps, case.cfl, abi.REMAP_AD)
+    assert eg == eo
+    assert rg.steps_done == ro.steps_done and np.array_equal(rg.dts, ro.dts)
+    assert rg.diag == ro.diag and rg.floor_count == ro.floor_count
+    assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS) == []
+
+
+@pytest.mark.parametrize("bcx,bcy,order,degrade", [(BC_PERIODIC, BC_PERIODIC, 2, 1), (BC_WALL, BC_WALL, 2, 1),
+                                                  (BC_PERIODIC, BC_WALL, 1, 1), (BC_WALL, BC_PERIODIC, 2, 0)])
+@pytest.mark.parametrize("kind", ["gas", "front", "blobs"])
+def test_kinematic_remap_ad_bitwise(gpu, orc, bcx, bcy, order, degrade, kind):
+    nmat = 1 if kind == "gas" else 2
+    cfg = make_config(13, 11, 1.0, 1.0, 0.25, -0.5, bcx, bcy, eos=[(EOS_PERFECT, 1.4, 0.0)] * nmat,
+                      face_order=order, interface_degrade=degrade)
+    painted = helpers.random_state(cfg, 11 + order + 3 * degrade, kind, umax=0.25)
+    sg, so = _pair(gpu, orc, cfg, painted)
+    lag = helpers.kinematic(so.download())
+    for x_first in (True, False):
+        for vel in (True, False):
+            dg, do = abi.RemapDiag(), abi.RemapDiag()
+            sg2, so2 = _pair(gpu, orc, cfg, so.download())
+            sg2.set_lagrange(lag)
+            so2.set_lagrange(lag)
+            sg2.remap_step(1.0, kind=abi.REMAP_AD, x_first=x_first, remap_velocity=vel, diag=dg)
+            so2.remap_step(1.0, kind=abi.REMAP_AD, x_first=x_first, remap_velocity=vel, diag=do)
+            assert helpers.bitwise_diff(sg2.download(), so2.download(), helpers.STATE_FIELDS) == []
+            assert (dg.max_k_violation, dg.k_clip_count, dg.mass_fix_count) == \
+                   (do.max_k_violation, do.k_clip_count, do.mass_fix_count)
+
+
+@pytest.mark.parametrize("scenario", ["cfl_face", "collapsed"])
+def test_error_parity_ad(gpu, orc, scenario):
+    cfg = make_config(9, 8, 1.0, 1.0, bc_x=BC_WALL, bc_y=BC_PERIODIC)
+    painted = helpers.random_state(cfg, 3, "gas", umax=0.05)
+    sg, so = _pair(gpu, orc, cfg, painted)
+    lag = helpers.kinematic(so.download())
+    if scenario == "cfl_face":
+        lag.u_half[..., 0] = 0.95
+    else:
+        lag.u_half[..., 0] = 0.0
+        lag.u_half[:, 5, 0] = 0.6
+        lag.u_half[:, 6, 0] = -0.6
+    out = []
+    for s in (sg, so):
+        s.set_lagrange(lag)
+        try:
+            s.remap_step(1.0, kind=abi.REMAP_AD)
+            out.append(None)
+        except errors.SimError as e:
+            out.append((type(e).__name__, e.what, e.i, e.j))
+    assert out[0] == out[1] and out[0] is not None
