@@ -155,18 +155,19 @@ def cpu_lib():
     return abi.Library(port, "h2do_"), "port"
 
 
-def time_cpu(case, warm, steps):
+def time_cpu(case, warm, steps, remap_kind=None):
     """Wall-clock the CPU implementation on `steps` steps after `warm`."""
     from paper_2208_13409_b200 import abi
-    lib, kind = cpu_lib()
+    lib, lib_kind = cpu_lib()
+    rk = abi.REMAP_DIRECTCF if remap_kind is None else remap_kind
     s = abi.Solver(lib, case.cfg)
     s.init_from(case.paint())
     if warm:
-        s.run(warm, cfl=case.cfl, log_dt=False)
+        s.run(warm, cfl=case.cfl, log_dt=False, kind=rk)
     t0 = time.perf_counter()
-    r = s.run(warm + steps, cfl=case.cfl, log_dt=False)
+    r = s.run(warm + steps, cfl=case.cfl, log_dt=False, kind=rk)
     dt = time.perf_counter() - t0
-    return case.cells * r.steps_done / dt, kind, r.steps_done, dt
+    return case.cells * r.steps_done / dt, lib_kind, r.steps_done, dt
 
 
 def pinned_state(nx, ny, nmat, cv):
@@ -184,6 +185,8 @@ def pinned_state(nx, ny, nmat, cv):
 
 
 def run_product(args, world, rank, local, pg):
+    from paper_2208_13409_b200 import abi as _abi
+    kind = _abi.REMAP_AD if args.remap == "ad" else _abi.REMAP_DIRECTCF
     import paper_2208_13409_b200 as pkg
     from paper_2208_13409_b200 import abi
 
@@ -194,7 +197,7 @@ def run_product(args, world, rank, local, pg):
     painted = case.paint()
     s.init_from(painted)
     for _ in range(args.warmup):
-        s.step_timed(case.cfl)
+        s.step_timed(case.cfl, kind=kind)
     clocks = Clocks(local)
     barrier(pg)
     clocks.start()
@@ -202,7 +205,7 @@ def run_product(args, world, rank, local, pg):
     tot = 0.0
     for _ in range(args.steps):
         s.flush_l2(512 << 20)
-        tot += s.step_timed(case.cfl)["total"]
+        tot += s.step_timed(case.cfl, kind=kind)["total"]
     launches = lib.fn["launch_count"]() - launches0
     # kernel-group split: the same steps as plain launches with CUDA events on
     # the launching stream between the groups (k_remap_tile is timed alone)
@@ -210,7 +213,7 @@ def run_product(args, world, rank, local, pg):
     n_ph = max(3, min(args.steps, 10))
     for _ in range(n_ph):
         s.flush_l2(512 << 20)
-        for k, v in s.step_timed(case.cfl, phases=True).items():
+        for k, v in s.step_timed(case.cfl, phases=True, kind=kind).items():
             ph[k] += v / n_ph
     clk = clocks.stop()
     barrier(pg)
@@ -222,6 +225,8 @@ def run_product(args, world, rank, local, pg):
     achieved_step = B_MIN[nmat] * cells / (ms_step / 1e3) / 1e9
     kern = {}
     for grp, (kname, nbytes) in KERNEL_BYTES.items():
+        if kind == abi.REMAP_AD and grp != "lagrange":  # the AD remap + post share one timed group
+            continue
         kms = max_over_ranks(pg, ph[grp])
         ach = nbytes[nmat] * cells / (kms / 1e3) / 1e9
         kern[grp] = {"kernel": f"{kname}<{nmat}>", "ms": kms, "bytes_per_cell": nbytes[nmat],
@@ -244,7 +249,7 @@ def run_product(args, world, rank, local, pg):
     #     -> download State), i.e. a caller that keeps its State on the host.
     se = abi.Solver(lib, case.cfg, local)
     se.init_from(painted)
-    se.run(1, cfl=case.cfl, log_dt=False)  # one-time setup (graph capture) outside the timed region
+    se.run(1, cfl=case.cfl, log_dt=False, kind=kind)  # one-time setup (graph capture) outside the timed region
     se.init_from(painted)
     host = pinned_state(case.cfg.mesh.nx, case.cfg.mesh.ny, nmat, case.cfg.mesh.dx * case.cfg.mesh.dy)
     st0 = se.download()
@@ -266,7 +271,7 @@ def run_product(args, world, rank, local, pg):
     barrier(pg)
     t0 = time.perf_counter()
     upload()
-    se.run(host.step + args.steps, cfl=case.cfl, log_dt=False)
+    se.run(host.step + args.steps, cfl=case.cfl, log_dt=False, kind=kind)
     download()
     e2e_run_s = max_over_ranks(pg, time.perf_counter() - t0)
     e2e_value = cells * args.steps * world / e2e_run_s
@@ -275,7 +280,7 @@ def run_product(args, world, rank, local, pg):
     t0 = time.perf_counter()
     for q in range(e2e_steps):
         upload()
-        se.run(host.step + 1, cfl=case.cfl, log_dt=False)
+        se.run(host.step + 1, cfl=case.cfl, log_dt=False, kind=kind)
         download()
     e2e_s = max_over_ranks(pg, time.perf_counter() - t0)
     e2e_step_value = cells * e2e_steps * world / e2e_s
@@ -285,7 +290,8 @@ def run_product(args, world, rank, local, pg):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (init_case-equivalent painter, seeded)",
         "config": {"workload": case.name, "cells": cells, "materials": nmat, "steps_from": "t=0 after warmup",
-                   "scheme": "DirectCF face_order=2 LinearDiag interface_degrade", "cfl": case.cfl,
+                   "scheme": ("AD split (X/Y alternating)" if kind == abi.REMAP_AD else "DirectCF") +
+                             " face_order=2 LinearDiag interface_degrade", "cfl": case.cfl,
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "512 MiB write between timed steps; working set per step >> 126 MB L2"},
         "phases_ms": dict(ph, note=f"{n_ph} un-graphed steps after the timed ones, CUDA events between "
@@ -312,8 +318,8 @@ def run_product(args, world, rank, local, pg):
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, kind, n, secs = time_cpu(case, 0, args.cpu_steps)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": kind,
+        v, ckind, n, secs = time_cpu(case, 0, args.cpu_steps, kind)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": ckind,
                                 "sample": f"{case.name}: first {n} steps from t=0, single thread, {secs:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -387,16 +393,19 @@ def run_product_multi(args, world, rank, local, pg):
 def run_reference(args, world, rank, pg):
     if rank != 0:
         return
+    from paper_2208_13409_b200 import abi
     case = workload(args.workload)
     steps = args.steps
-    v, kind, n, secs = time_cpu(case, args.warmup, steps)
+    rk = abi.REMAP_AD if args.remap == "ad" else abi.REMAP_DIRECTCF
+    v, ckind, n, secs = time_cpu(case, args.warmup, steps, rk)
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": args.warmup,
         "ms_per_step": secs * 1e3 / max(n, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (init_case-equivalent painter, seeded)", "impl": "reference",
         "config": {"workload": case.name, "cells": case.cells, "materials": case.cfg.nmat, "cfl": case.cfl,
+                   "scheme": "AD split" if args.remap == "ad" else "DirectCF",
                    "parallelism": "single"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": kind,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": ckind,
                          "sample": f"{case.name}: steps {args.warmup + 1}..{args.warmup + n}, single thread "
                                    f"(the reference has no threading), {secs:.1f} s"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -411,6 +420,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--remap", default="directcf", choices=["directcf", "ad"],
+                    help="remap engine: DirectCF (the path) or the AD split scheme (SURVEY 8f)")
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -250,8 +250,10 @@ long long h2d_launch_count(void);
  * (dt), ms[1] the fused Lagrange kernel, ms[2] the remap flux tile kernel,
  * ms[3] slivers + Work ghosts, ms[4] dual-mesh momentum, ms[5] the derived
  * fields / normals / NaN-scan kernel, ms[7] the ghost-layer launches and the
- * commit; phases = 0 replays the production CUDA graph (only ms[6] set). */
-int h2d_step_timed(h2d_ctx* ctx, double cfl, double t_end, int phases, float ms[8]);
+ * commit; phases = 0 replays the production CUDA graph (only ms[6] set).
+ * remap_kind = H2D_REMAP_AD times the AD step (its two passes and the post
+ * kernels land in ms[2]). */
+int h2d_step_timed(h2d_ctx* ctx, double cfl, double t_end, int phases, int remap_kind, float ms[8]);
 /* Write `bytes` of scratch on the context's stream (evicts L2 between timed
  * steps) and wait for it. */
 int h2d_flush_l2(h2d_ctx* ctx, long long bytes);

@@ -212,7 +212,7 @@ _SIGS = {
 # product-only extras (benchmark support)
 _EXTRA = {
     "launch_count": ([], C.c_longlong),
-    "step_timed": ([C.c_void_p, C.c_double, C.c_double, C.c_int, C.POINTER(C.c_float)], C.c_int),
+    "step_timed": ([C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_float)], C.c_int),
     "flush_l2": ([C.c_void_p, C.c_longlong], C.c_int),
 }
 
@@ -343,12 +343,12 @@ class Solver:
 
     STEP_GROUPS = ("start", "lagrange", "remap_tile", "slivers", "dual", "post", "total", "ghosts_commit")
 
-    def step_timed(self, cfl: float, t_end: float = 1e30, phases: bool = False) -> dict:
+    def step_timed(self, cfl: float, t_end: float = 1e30, phases: bool = False, kind: int = REMAP_DIRECTCF) -> dict:
         """One run-loop step timed with CUDA events (product only): returns
         milliseconds per kernel group (STEP_GROUPS); phases=False replays the
         production CUDA graph and only "total" is set."""
         ms = (C.c_float * 8)()
-        self._check(self.lib.fn["step_timed"](self._h, cfl, t_end, int(phases), ms))
+        self._check(self.lib.fn["step_timed"](self._h, cfl, t_end, int(phases), int(kind), ms))
         return {k: float(ms[q]) for q, k in enumerate(self.STEP_GROUPS)}
 
     def flush_l2(self, nbytes: int = 512 << 20):

@@ -934,8 +934,16 @@ int h2d_totals(h2d_ctx* c, double out[6]) {
     return 0;
 }
 
-int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[8]) {
+int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_kind, float ms[8]) {
     cudaSetDevice(c->device);
+    const bool ad = remap_kind == H2D_REMAP_AD;
+    if (!(remap_kind == H2D_REMAP_DIRECTCF || (ad && !c->is_block))) {
+        set_err(c, H2D_ERR_INVALID, "h2d_step_timed: DirectCF or (single-domain) AD only");
+        return H2D_ERR_INVALID;
+    }
+    if (ad)
+        if (int rc = ensure_graphs_ad(c)) return rc;
+    const int xf = c->hctl->step % 2 == 0;  // harness.cpp:401
     if (!c->ev[0])
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
     if (int rc = ctl_reset(c)) return rc;
@@ -960,13 +968,20 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[8]
         CK(cudaEventRecord(c->ev[2], c->st));
         launch_lag_ghosts(d, c->st);
         CK(cudaEventRecord(c->ev[3], c->st));
-        launch_remap_tile(d, c->st);
-        CK(cudaEventRecord(c->ev[4], c->st));
-        launch_remap_slivers(d, c->st);
-        CK(cudaEventRecord(c->ev[5], c->st));
-        launch_remap_dual(d, c->st);
-        CK(cudaEventRecord(c->ev[6], c->st));
-        launch_post(d, 1, c->st);
+        if (ad) {  // both AD passes and the post kernels in the remap slot
+            launch_remap_ad(d, c->adw, xf, 1, 1, c->st);
+            CK(cudaEventRecord(c->ev[4], c->st));
+            CK(cudaEventRecord(c->ev[5], c->st));
+            CK(cudaEventRecord(c->ev[6], c->st));
+        } else {
+            launch_remap_tile(d, c->st);
+            CK(cudaEventRecord(c->ev[4], c->st));
+            launch_remap_slivers(d, c->st);
+            CK(cudaEventRecord(c->ev[5], c->st));
+            launch_remap_dual(d, c->st);
+            CK(cudaEventRecord(c->ev[6], c->st));
+            launch_post(d, 1, c->st);
+        }
         CK(cudaEventRecord(c->ev[7], c->st));
         launch_post_ghosts(d, c->st);
         launch_commit_finish(d, c->st);
@@ -986,7 +1001,12 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, float ms[8]
     } else {  // the production path: one graph launch
         if (int rc = ensure_graphs(c)) return rc;
         CK(cudaEventRecord(c->ev[0], c->st));
-        if (int rc = launch_step_graph(c, c->cur)) return rc;
+        if (ad) {
+            CK(cudaGraphLaunch(c->graph_ad[c->cur][xf], c->st));
+            add_launches(c->graph_kernels_ad);
+        } else if (int rc = launch_step_graph(c, c->cur)) {
+            return rc;
+        }
         CK(cudaEventRecord(c->ev[8], c->st));
         CK(cudaEventSynchronize(c->ev[8]));
         CK(cudaEventElapsedTime(&ms[6], c->ev[0], c->ev[8]));

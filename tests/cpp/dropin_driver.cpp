@@ -54,7 +54,8 @@ static void put_error(const E& e) {
 }
 
 // run loop of harness.cpp:390-412 on a caller-built State
-static void run_loop(State s, const MaterialSet& mats, double cfl, int steps, const char* tag) {
+static void run_loop(State s, const MaterialSet& mats, double cfl, int steps, const char* tag,
+                     RemapKind kind = RemapKind::DirectCF) {
     put_s(tag);
     RemapDiag diag;
     int floors = 0;
@@ -64,7 +65,7 @@ static void run_loop(State s, const MaterialSet& mats, double cfl, int steps, co
             put_d(dt);
             LagrangeResult lag = lagrange_step(s, mats, dt, PseudoViscosityParams{});
             floors += lag.floor_count;
-            s = remap_step(s, mats, lag, dt, RemapKind::DirectCF, ReconConfig{}, s.step % 2 == 0, true, &diag);
+            s = remap_step(s, mats, lag, dt, kind, ReconConfig{}, s.step % 2 == 0, true, &diag);
         }
         put_s("ok");
     } catch (const UnphysicalStateError& e) {
@@ -107,6 +108,7 @@ int main(int argc, char** argv) {
         fill_ghosts(s);
         sync_derived(s, mats);
         run_loop(s, mats, 0.5, 60, "riemann");
+        run_loop(s, mats, 0.5, 60, "riemann_ad", RemapKind::AD);
     }
     // 2. two materials: a disc of material 1 in a moving material-0 slab
     {
@@ -138,6 +140,7 @@ int main(int argc, char** argv) {
         sync_derived(s, mats);
         update_interface_normals(s);
         run_loop(s, mats, 0.3, 40, "disc");
+        run_loop(s, mats, 0.3, 40, "disc_ad", RemapKind::AD);
     }
     // 3. kinematic remaps on a periodic grid (test_remap.cpp:46-54 pattern)
     {
