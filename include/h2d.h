@@ -144,7 +144,7 @@ typedef struct {
     int max_steps;    /* 0 = until t_end (compares the state's absolute step) */
     double t_end;
     double cfl;
-    int remap_kind;   /* only H2D_REMAP_DIRECTCF is implemented on device */
+    int remap_kind;   /* H2D_REMAP_DIRECTCF or H2D_REMAP_AD (not H2D_REMAP_DIRECT) */
     double* dt_log;   /* optional host array receiving each step's dt */
     int dt_log_cap;
     /* outputs */
@@ -201,7 +201,11 @@ int h2d_set_lagrange(h2d_ctx* ctx, const h2d_lagrange* lag);
 /* State remap_step(State, MaterialSet, LagrangeResult, dt, RemapKind,
  * ReconConfig, x_first, remap_velocity, RemapDiag*) (remap.hpp:51-53).
  * Replaces the device State by the remapped one (step+1, time+dt).
- * `diag` (nullable) is accumulated like the reference's RemapDiag. */
+ * `diag` (nullable) is accumulated like the reference's RemapDiag.
+ * remap_kind: H2D_REMAP_DIRECTCF (cf_pass, remap.cpp:734-1073) or
+ * H2D_REMAP_AD (two directional passes, remap.cpp:469-589, X first when
+ * x_first != 0; block contexts: DirectCF only); H2D_REMAP_DIRECT returns
+ * H2D_ERR_INVALID. */
 int h2d_remap_step(h2d_ctx* ctx, double dt, int remap_kind, int x_first,
                    int remap_velocity, h2d_remap_diag* diag);
 
