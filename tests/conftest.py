@@ -27,3 +27,10 @@ def ref():
     if lib is None:
         pytest.skip("reference library not built (no /root/reference here)")
     return lib
+
+
+@pytest.fixture(scope="session")
+def gpu():
+    """The CUDA product library (fails loudly when it is missing)."""
+    import helpers
+    return helpers.product_lib()

@@ -16,11 +16,6 @@ from paper_2208_13409_b200.abi import BC_PERIODIC, BC_WALL, CORNER_LINEARDIAG, C
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def gpu():
-    return helpers.product_lib()
-
-
 def _pair(gpu, orc, cfg, painted):
     return helpers.prepared(gpu, cfg, painted), helpers.prepared(orc, cfg, painted)
 
