@@ -1979,35 +1979,6 @@ __global__ void k_commit(Ctl* c, int advance) {
     c->cur ^= 1;
 }
 
-// nan_scan, harness.cpp:347-358, on the committed state (the next buffers).
-__global__ void k_nan(Dev d) {
-    pdl_enter();
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, 0, 0);
-    if (i > d.nx || j > d.ny) return;
-    const int c = ix(d, i, j);
-    const bool cell = i < d.nx && j < d.ny;
-    // issue every load before testing any of them (no short-circuit chains)
-    const double a = cell ? d.nm_mix[c] : 0.0, b = cell ? d.ne_mix[c] : 0.0, p = cell ? d.np_mix[c] : 0.0;
-    const double ux = d.nux[c], uy = d.nuy[c];
-    if (!isfinite(a) | !isfinite(b) | !isfinite(p)) raise(d.ctl, ekey(PH_NAN_CELL, j, i, 0));
-    if (!isfinite(ux) | !isfinite(uy)) raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));
-}
-
-// End of a successful run-loop step: counters and dt log.
-__global__ void k_finish(Ctl* c) {
-    pdl_enter();
-    if (c->err_key != kNoErr || c->done) return;
-    if (c->dt_log && c->steps_done < c->dt_log_cap) c->dt_log[c->steps_done] = c->dt;
-    c->steps_done += 1;
-    c->floor_count += c->step_floor;
-    c->k_clip_count += c->step_clip;
-    c->mass_fix_count += c->step_fix;
-    const double v = __longlong_as_double((long long)c->kviol_bits);
-    if (v > c->max_k_violation) c->max_k_violation = v;
-}
-
 // Start of a run-loop step (harness.cpp:390-395): loop condition, then the
 // cfl_dt of the current State, whose wave-speed maximum and first error were
 // produced by the previous step's k_post (or k_cfl before the first step).
@@ -2974,10 +2945,6 @@ void launch_global_xfer(const Dev& d, double* buf, Rng r, double* px, double* py
 
 void launch_commit(Ctl* c, int advance, cudaStream_t s) { k_commit<<<1, 1, 0, s>>>(c, advance); }
 
-void launch_nan_finish(const Dev& d, cudaStream_t s) {
-    { k_nan<<<grid_rect(d.nx + 1, d.ny + 1), blk2(), 0, s>>>(d); ++g_launches; }
-    { k_finish<<<1, 1, 0, s>>>(d.ctl); ++g_launches; }
-}
 
 void launch_normals_api(const Dev& d, cudaStream_t s) { k_normals<<<grid_rect(d.nx, d.ny), blk2(), 0, s>>>(d, 1); }
 

@@ -56,7 +56,6 @@ void launch_cfl_next(const Dev& d, cudaStream_t s);
 void launch_step_start(const Dev& d, cudaStream_t s);
 void launch_commit_finish(const Dev& d, cudaStream_t s);               // wave speed of the current State
 void launch_commit(Ctl* c, int advance, cudaStream_t s);
-void launch_nan_finish(const Dev& d, cudaStream_t s);
 void launch_normals_api(const Dev& d, cudaStream_t s);
 void launch_rollback(Ctl* c, cudaStream_t s);
 void launch_rect_xfer(const Dev& d, const FieldList& cells, const FieldList& nodes, Rng rc, Rng rn, double* buf,
