@@ -48,6 +48,7 @@ struct h2d_ctx {
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one run-loop step per State parity
     cudaGraphExec_t graph_ad[2][2] = {};            // AD steps per (State parity, x_first)
     double* ad_mem = nullptr;                       // AD Work planes between the passes
+    TmaSet tma[2]{};                                // remap-tile TMA descriptors per State parity
     AdWork adw{};
     long long graph_kernels = 0, graph_kernels_ad = 0;
     cudaEvent_t ev[9] = {};
@@ -123,6 +124,7 @@ Dev make_dev(h2d_ctx* c, int parity, int remap_velocity) {
     d.nux = n.ux;
     d.nuy = n.uy;
     d.remap_velocity = remap_velocity;
+    d.tma = &c->tma[parity];
     return d;
 }
 
@@ -418,6 +420,46 @@ void block_ranges(h2d_ctx* c) {
     d.win_n = {std::max(wl, -G), std::min(wr + 1, NX + G + 1), std::max(wb, -G), std::min(wt + 1, NY + G + 1)};
 }
 
+// TMA descriptors (cuTensorMapEncodeTiled through the runtime's driver entry
+// point) of every plane the remap tile stages: 2D fp64 tensors of P x R
+// doubles (row pitch P * 8 bytes), node boxes RNW x RNH, cell boxes RCW x RCH;
+// boxes reaching past the plane are zero-filled.
+int make_tmas(h2d_ctx* c) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn enc = nullptr;
+    if (!enc) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return 1;
+        enc = reinterpret_cast<EncodeFn>(fn);
+    }
+    const Dev& d = c->base;
+    auto make = [&](CUtensorMap* m, double* base, cuuint32_t bw, cuuint32_t bh) {
+        const cuuint64_t dims[2] = {(cuuint64_t)c->P, (cuuint64_t)c->R};
+        const cuuint64_t strides[1] = {(cuuint64_t)c->P * sizeof(double)};
+        const cuuint32_t box[2] = {bw, bh};
+        const cuuint32_t es[2] = {1, 1};
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS;
+    };
+    const cuuint32_t nw = tma_node_box_w(), nh = tma_node_box_h(), cw = tma_cell_box_w(), ch = tma_cell_box_h();
+    for (int p = 0; p < 2; ++p) {
+        TmaSet& t = c->tma[p];
+        int bad = make(&t.t[TM_UHX], d.uhx, nw, nh) | make(&t.t[TM_UHY], d.uhy, nw, nh);
+        for (int a = 0; a < c->nmat; ++a) {
+            bad |= make(&t.t[TM_EL0 + a], d.el[a], cw, ch);
+            bad |= make(&t.t[TM_M0 + a], c->sb[p].m[a], cw, ch);
+            bad |= make(&t.t[TM_K0 + a], c->sb[p].k[a], cw, ch);
+        }
+        if (bad) return 1;
+    }
+    return 0;
+}
+
 int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx** out);
 
 }  // namespace
@@ -611,6 +653,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
             fill_plane(c, c->sb[p].vol, d.cv))
             return fail(H2D_ERR_DEVICE);
     }
+    if (make_tmas(c)) return fail(H2D_ERR_DEVICE);
     if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(H2D_ERR_DEVICE);
     *out = c;
     return 0;

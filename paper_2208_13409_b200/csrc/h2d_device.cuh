@@ -7,6 +7,7 @@
 // behaviour of `a < b ? b : a`).  Cited lines are in /root/reference/proj.
 #pragma once
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (the type only; maps are encoded through the runtime's driver entry point)
 #include <math_constants.h>
 #include <cfloat>
 
@@ -112,6 +113,13 @@ struct Rng {
 // the block origin (oi, oj) minus the halo H to the start of every plane.  A
 // single-domain context is the block (0, 0, nx, ny) with H = G = 2, i.e. the
 // reference Field layout.
+// TMA descriptors of the planes the remap tile stages (per State parity):
+// u_half x / y (node boxes), e_lag, m, k per material (cell boxes).
+enum { TM_UHX, TM_UHY, TM_EL0, TM_EL1, TM_M0, TM_M1, TM_K0, TM_K1, TM_N };
+struct TmaSet {
+    CUtensorMap t[TM_N];
+};
+
 struct Dev {
     int nx, ny, P, nmat, per_x, per_y;  // nx, ny: GLOBAL mesh size
     int oi, oj, H, off;                 // block origin, storage halo, index offset
@@ -151,6 +159,7 @@ struct Dev {
     // in sl_segs, bit (j - r_gath.j0) % 32 of sl_rows[(j - r_gath.j0) / 32]; cleared as consumed
     unsigned *sl_rows, *sl_segs;
     Ctl* ctl;
+    const TmaSet* tma;  // host pointer: the launch passes *tma by value (__grid_constant__)
 };
 
 // 32-bit plane offsets: P * R < 2^31 for every mesh up to 16384^2 (checked at

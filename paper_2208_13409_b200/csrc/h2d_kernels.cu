@@ -724,11 +724,12 @@ __device__ __forceinline__ void face_flux(double ym, double yp, double dmx, doub
 // ---------------------------------------------------------------------------
 constexpr int RTX = 32, RTY = 8;
 constexpr int RCW = RTX + 4, RCH = RTY + 4;  // cell region [i0-2, i0+RTX+2)
-constexpr int RNW = RTX + 5, RNH = RTY + 5;  // node region [i0-2, i0+RTX+2]
+constexpr int RNW = RTX + 6, RNH = RTY + 5;  // node region [i0-2, i0+RTX+3] (a 38-wide TMA box row = 304 B)
 constexpr int RNN = RNW * RNH, RNC = RCW * RCH;
 constexpr int NXF = (RTX + 1) * RTY, NYF = RTX * (RTY + 1), NCF = (RTX + 1) * (RTY + 1);
 constexpr int NIT = NCF > NXF ? (NCF > NYF ? NCF : NYF) : (NXF > NYF ? NXF : NYF);  // item buffer
 constexpr int RCELL1 = 5, RCELL2 = 10;  // cell arrays per material count
+__host__ __device__ constexpr int al16(int n) { return (n + 15) & ~15; }  // smem planes start 128-byte aligned (TMA destinations)
 
 template <int NM>
 struct Tile {
@@ -770,7 +771,7 @@ struct Tile {
 
 template <int NM>
 constexpr size_t remap_smem_bytes() {
-    return sizeof(double) * (6 * RNN + (NM == 2 ? RCELL2 : RCELL1) * RNC + 3 * NM * NIT) + 64;
+    return sizeof(double) * (6 * al16(RNN) + (NM == 2 ? RCELL2 : RCELL1) * al16(RNC) + 3 * NM * al16(NIT)) + 128;
 }
 
 template <int NM>
@@ -781,7 +782,7 @@ __device__ __forceinline__ Tile<NM> carve_tile(char* base, int ci0, int cj0) {
     double* p = reinterpret_cast<double*>(base);
     auto take = [&](int n) {
         double* r = p;
-        p += n;
+        p += al16(n);
         return r;
     };
     T.hx = take(RNN);
@@ -1115,28 +1116,88 @@ __device__ __forceinline__ void finalize_cell(const Dev& d, const Rng& rg, int i
     if (NM == 2) {
         d.sliver[c] = sl;
         if (sl) {  // index the sliver for k_slivers (row bit + segment bit)
-            const int jr = j - rg.j0;
-            atomicOr(&d.sl_segs[(size_t)jr * ((rg.i1 - rg.i0 + 31) >> 5) + blockIdx.x], 1u << tx);
+            const int jr = j - rg.j0, ir = i - rg.i0;
+            atomicOr(&d.sl_segs[(size_t)jr * ((rg.i1 - rg.i0 + 31) >> 5) + (ir >> 5)], 1u << (ir & 31));
             atomicOr(&d.sl_rows[jr >> 5], 1u << (jr & 31));
         }
     }
 }
 
+// plane column of the remap tiles' first region column (rg.i0 - 2) is odd
+__host__ __device__ __forceinline__ int tile_shift(const Dev& d) { return (d.r_gath.i0 - G + d.H - d.oi) & 1; }
+
+// TMA (cp.async.bulk.tensor) + mbarrier helpers for the remap tile's staging
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+
 template <int NM>
-__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d) {
+__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
     pdl_enter();
-    extern __shared__ __align__(16) char smem[];
+    extern __shared__ __align__(128) char smem_raw[];
     __shared__ int s_halt;
+    __shared__ __align__(8) uint64_t s_bar;
     const int tid = threadIdx.x;
-    if (tid == 0) s_halt = halted(d.ctl);
+    if (tid == 0) {
+        s_halt = halted(d.ctl);
+        mbar_init(&s_bar, 1);
+    }
     __syncthreads();
     if (s_halt) return;
     const int nx = d.nx, ny = d.ny;
     const Rng rg = d.r_gath;
-    const int i0 = rg.i0 + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
+    // TMA wants the box's first column 16-byte aligned (an even plane
+    // column): a block whose range starts on an odd column shifts its tile
+    // grid one column left (the extra column's items are computed, never
+    // gathered, and land outside every range a later phase reads)
+    const int sx = tile_shift(d);
+    const int i0 = rg.i0 - sx + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     const Tile<NM> T = carve_tile<NM>(smem, i0 - G, j0 - G);
+    // ---- phase 0: one thread stages the tile + halo with TMA (2D boxes of
+    // the planes, zero-filled past the plane): u_half on the node region,
+    // e_lag, m, k on the cell region.  T.rho holds m and T.vl (1 material) /
+    // T.kk hold k until phase 2 turns them into densities and volumes.
+    // Node values outside the window are never read (every use below is
+    // guarded by the window), so whatever the plane holds there is harmless.
+    if (tid == 0) {
+        constexpr uint32_t bytes = 2u * RNW * RNH * 8u + 3u * NM * RCW * RCH * 8u;
+        const int x = T.ci0 + d.H - d.oi, y = T.cj0 + d.H - d.oj;  // plane column / row of the region origin
+        mbar_expect_tx(&s_bar, bytes);
+        tma_load_2d(T.hx, &tm.t[TM_UHX], x, y, &s_bar);
+        tma_load_2d(T.hy, &tm.t[TM_UHY], x, y, &s_bar);
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            tma_load_2d(T.el[a], &tm.t[TM_EL0 + a], x, y, &s_bar);
+            tma_load_2d(T.rho[a], &tm.t[TM_M0 + a], x, y, &s_bar);
+            tma_load_2d(NM == 2 ? T.kk[a] : T.vl, &tm.t[TM_K0 + a], x, y, &s_bar);
+        }
+    }
     const double dt = step_dt(d.ctl);
     const double cv = d.cv;
+    mbar_wait(&s_bar, 0);
     // ---- quiescent tile: u_half == 0 at every node of the tile's faces and
     // corners makes every face / corner flux volume of the tile zero, so no
     // flux is gathered (the reference skips zero volumes, remap.cpp:860,929),
@@ -1149,8 +1210,8 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
         for (int t = tid; t < NCF; t += RTX * RTY, rq.step()) {
             const int ni = i0 + rq.c, nj = j0 + rq.r;
             if (in(d.win_n, ni, nj)) {
-                const int n = ix(d, ni, nj);
-                if (d.uhx[n] != 0.0 || d.uhy[n] != 0.0) moving = 1;
+                const int q = T.n(ni, nj);
+                if (T.hx[q] != 0.0 || T.hy[q] != 0.0) moving = 1;
             }
         }
         if (!__syncthreads_or(moving)) {
@@ -1169,44 +1230,16 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
             const int c = ix(d, i, j);
             double m[2], me[2], va[2];
 #pragma unroll
+            const int tc = T.c(i, j);
             for (int a = 0; a < NM; ++a) {
-                const double m0 = d.m[a][c];
+                const double m0 = T.rho[a][tc];
                 m[a] = m0;
-                me[a] = m0 * d.el[a][c];
-                va[a] = d.k[a][c] * cv;
+                me[a] = m0 * T.el[a][tc];
+                va[a] = (NM == 2 ? T.kk[a][tc] : T.vl[tc]) * cv;
             }
             finalize_cell<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va);
             return;
         }
-    }
-    // ---- phase 0: stage the HBM inputs of the tile + halo (all loads
-    // independent, coalesced rows): u_half on the node region, e_lag, m, k
-    // (and normals) on the cell region.  T.rho holds m and T.vl holds k0
-    // until phase 2 turns them into densities and volumes.
-    RowCol<RNW, RTX * RTY> rs0(tid);
-    for (int t = tid; t < RNN; t += RTX * RTY, rs0.step()) {
-        const int i = T.ci0 + rs0.c, j = T.cj0 + rs0.r;
-        double hx = 0.0, hy = 0.0;
-        if (in(d.win_n, i, j)) {  // = [-2, n+2] on a whole mesh
-            const int n = ix(d, i, j);
-            hx = d.uhx[n];
-            hy = d.uhy[n];
-        }
-        T.hx[t] = hx;
-        T.hy[t] = hy;
-    }
-    RowCol<RCW, RTX * RTY> rs1(tid);
-    for (int t = tid; t < RNC; t += RTX * RTY, rs1.step()) {
-        const int i = T.ci0 + rs1.c, j = T.cj0 + rs1.r;
-        if (!in(d.win_c, i, j)) continue;  // = [-2, n+2) on a whole mesh
-        const int c = ix(d, i, j);
-#pragma unroll
-        for (int a = 0; a < NM; ++a) {
-            T.el[a][t] = d.el[a][c];
-            T.rho[a][t] = d.m[a][c];
-            if (NM == 2) T.kk[a][t] = d.k[a][c];
-        }
-        if (NM == 1) T.vl[t] = d.k[0][c];
     }
     __syncthreads();
     // ---- phase 1, node items: corner flux, axis geometry, face flux volumes
@@ -2768,13 +2801,20 @@ void launch_remap_core(const Dev& d, cudaStream_t s) {
 }
 
 // the fused flux tile kernel alone (timed separately by h2d_step_timed)
+int tma_node_box_w() { return RNW; }
+int tma_node_box_h() { return RNH; }
+int tma_cell_box_w() { return RCW; }
+int tma_cell_box_h() { return RCH; }
+
 void launch_remap_tile(const Dev& d, cudaStream_t s) {
     remap_init();
-    const dim3 gft = tiles_of(d.r_gath, RTX, RTY);
+    Rng rt = d.r_gath;
+    rt.i0 -= tile_shift(d);
+    const dim3 gft = tiles_of(rt, RTX, RTY);
     if (d.nmat == 2)
-        pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d);
+        pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
     else
-        pdl(k_remap_tile<1>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d);
+        pdl(k_remap_tile<1>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
 }
 
 // slivers + finalize_cells ghost fill + flux ghosts

@@ -28,6 +28,10 @@ struct AdIO {
 };
 
 long long launch_count();
+int tma_node_box_w();  // remap-tile TMA box sizes (doubles)
+int tma_node_box_h();
+int tma_cell_box_w();
+int tma_cell_box_h();
 void add_launches(long long n);  // kernels replayed by a CUDA graph launch
 void launch_begin(Ctl* c, int mode, double dt, cudaStream_t s);
 void launch_cfl(const Dev& d, int run_loop, cudaStream_t s);
