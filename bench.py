@@ -38,12 +38,12 @@ B_MIN = {1: 64, 2: 160}  # algorithmic bytes per cell-step (BASELI
 #  k_remap_tile: reads u_half (2), e_lag, m, k per material (+ normals for 2
 #               materials); writes Work m, me, e, k per material, mcell, the
 #               mass fluxes dmx, dmy, dmc (+ 1 sliver-flag byte for 2);
-#  k_post:      reads new m, e, k per material, |u| and u (3 nodal) (+ old
-#               normals); writes m_mix, e_mix, rho_mix, p_mix, vol (+ normals).
+#  k_post:      reads new m, e, k per material and |u| (+ old normals);
+#               writes m_mix, e_mix, rho_mix, p_mix, vol (+ normals).
 KERNEL_BYTES = {
     "lagrange": ("k_lag_fused", {1: 8 * (3 + 4) + 8 * (4 + 1), 2: 8 * (6 + 4) + 8 * (4 + 2)}),
     "remap_tile": ("k_remap_tile", {1: 8 * (2 + 3) + 8 * (4 + 1 + 3), 2: 8 * (2 + 6 + 2) + 8 * (8 + 1 + 3) + 1}),
-    "post": ("k_post", {1: 8 * (3 + 3) + 8 * 5, 2: 8 * (6 + 3 + 2) + 8 * (5 + 2)}),
+    "post": ("k_post", {1: 8 * (3 + 1) + 8 * 5, 2: 8 * (6 + 1 + 2) + 8 * (5 + 2)}),
 }
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0

@@ -1003,7 +1003,8 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_k
     enqueue_cfl_next(c);
     for (int q = 0; q < 8; ++q) ms[q] = 0.0f;
     if (phases) {  // un-graphed launches with events between the kernels / groups
-        const Dev d = make_dev(c, c->cur, 1);
+        Dev d = make_dev(c, c->cur, 1);
+        d.scan_nodes = 1;  // as the run-loop graph
         CK(cudaEventRecord(c->ev[0], c->st));
         launch_step_start(d, c->st);
         CK(cudaEventRecord(c->ev[1], c->st));

@@ -160,6 +160,7 @@ struct Dev {
     unsigned *sl_rows, *sl_segs;
     Ctl* ctl;
     const TmaSet* tma;  // host pointer: the launch passes *tma by value (__grid_constant__)
+    int scan_nodes;     // run loop: the node update also runs nan_scan's node part (harness.cpp:353-357)
 };
 
 // 32-bit plane offsets: P * R < 2^31 for every mesh up to 16384^2 (checked at

@@ -1857,6 +1857,8 @@ __global__ void k_node_update_walls(Dev d) {
     d.nux[s] = ux;
     d.nuy[s] = uy;
     d.unrm[s] = sqrt(ux * ux + uy * uy);
+    if (d.scan_nodes && own_node(d, i, j) && (!isfinite(ux) | !isfinite(uy)))
+        raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));  // nan_scan on the new u (harness.cpp:353-357)
 }
 
 // MomAcc gather (App. C item 4) + apply_dual_update (remap.cpp:444-464) with
@@ -1970,6 +1972,8 @@ __global__ void k_node_update(Dev d) {
     d.nux[o] = ux;
     d.nuy[o] = uy;
     d.unrm[o] = sqrt(ux * ux + uy * uy);  // |u| for the next cfl_dt (harness.cpp:308)
+    if (d.scan_nodes && own_node(d, i, j) && (!isfinite(ux) | !isfinite(uy)))
+        raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));  // nan_scan on the new u (harness.cpp:353-357)
 }
 
 // refresh_normals_impl + youngs_normal (remap.cpp:102-114, vof.cpp:10-22)
@@ -2238,10 +2242,7 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
             }
         }
     }
-    if (run_loop && i >= 0 && j >= 0 && i <= nx && j <= ny && own_node(d, i, j)) {
-        const int n = ix(d, i, j);
-        if (!isfinite(d.nux[n]) | !isfinite(d.nuy[n])) raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));
-    }
+    // (nan_scan's node part runs in the node update that writes u, d.scan_nodes)
     if (run_loop) {
         for (int o = 16; o > 0; o >>= 1) {
             const unsigned long long v = __shfl_xor_sync(0xffffffffu, wb, o);
@@ -2575,6 +2576,8 @@ __global__ void k_ad_node(Dev d, AdIO w) {
     d.nux[o] = ux;
     d.nuy[o] = uy;
     d.unrm[o] = sqrt(ux * ux + uy * uy);
+    if (d.scan_nodes && w.pass == 1 && own_node(d, i, j) && (!isfinite(ux) | !isfinite(uy)))
+        raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));  // nan_scan on the final u
 }
 
 // refresh_normals_impl after AD pass 0 (remap.cpp:102-114): youngs normals of
@@ -2846,7 +2849,9 @@ void launch_remap_dual(const Dev& d, cudaStream_t s) {
     }
 }
 
-void launch_step(const Dev& d, cudaStream_t s) {
+void launch_step(const Dev& dd, cudaStream_t s) {
+    Dev d = dd;
+    d.scan_nodes = 1;
     pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
     launch_lagrange_run(d, s);
     launch_remap_core(d, s);
@@ -2946,7 +2951,9 @@ void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_veloc
     post_and_ghosts(dp, run_loop, s);
 }
 
-void launch_step_ad(const Dev& d, const AdWork& W, int x_first, cudaStream_t s) {
+void launch_step_ad(const Dev& dd, const AdWork& W, int x_first, cudaStream_t s) {
+    Dev d = dd;
+    d.scan_nodes = 1;
     pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
     launch_lagrange_run(d, s);
     launch_remap_ad(d, W, x_first, 1, 1, s);
