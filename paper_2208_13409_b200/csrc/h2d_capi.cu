@@ -530,7 +530,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     // plane count: 2 x State (6 + 3 nm) + Lagrange (7 + 2 nm) + remap scratch
     const size_t planes = 2 * (9 + 3 * nm) + (7 + 2 * nm) + (25 + 15 * nm) + 8;
     const size_t bytes_planes = planes * ((c->fsz * sizeof(double) + 255) & ~size_t(255));
-    const size_t bytes_small = 8 * ((c->fsz + 255) & ~size_t(255)) + ((size_t)c->R * 4 + 256);
+    const size_t bytes_small = 12 * ((c->fsz + 255) & ~size_t(255)) + ((size_t)c->R * 4 + 256);
     c->arena_bytes = bytes_planes + bytes_small + 4096;
     if (cudaMalloc(&c->arena, c->arena_bytes) != cudaSuccess) return fail(H2D_ERR_NOMEM);
     cudaMemsetAsync(c->arena, 0, c->arena_bytes, c->st);
@@ -638,6 +638,8 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     d.sliver = bytes_plane();
     for (int q = 0; q < 4; ++q) d.dflag[q] = bytes_plane();
     d.sl_segs = reinterpret_cast<unsigned*>(bytes_plane());  // >= R*P/8 bytes needed
+    d.sl_list = reinterpret_cast<int*>(bytes_plane());       // 4 byte planes: one int per cell
+    for (int q = 0; q < 3; ++q) (void)bytes_plane();
     d.sl_rows = reinterpret_cast<unsigned*>(c->arena + c->arena_used);
     c->arena_used += ((size_t)c->R * 4 + 255) & ~size_t(255);
     if (c->arena_used > c->arena_bytes) return fail(H2D_ERR_NOMEM);

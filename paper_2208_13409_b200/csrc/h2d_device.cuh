@@ -158,6 +158,7 @@ struct Dev {
     // sliver index: bit (i - r_gath.i0) of word [(j - r_gath.j0) * nwx + (i - r_gath.i0) / 32]
     // in sl_segs, bit (j - r_gath.j0) % 32 of sl_rows[(j - r_gath.j0) / 32]; cleared as consumed
     unsigned *sl_rows, *sl_segs;
+    int* sl_list;  // the pending slivers in the reference order (k_slivers), one int per cell of capacity
     Ctl* ctl;
     const TmaSet* tma;  // host pointer: the launch passes *tma by value (__grid_constant__)
     int scan_nodes;     // run loop: the node update also runs nan_scan's node part (harness.cpp:353-357)

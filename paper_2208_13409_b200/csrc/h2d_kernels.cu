@@ -1445,16 +1445,6 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
 }
 
 
-// Sequential sliver redistribution (remap.cpp:194-226), one warp, in the
-// reference's row-major `pending` order. Rows and 32-cell segments holding
-// slivers are found through the bitmaps the tile kernel set (k_remap_tile
-// finalize); each sliver's carrier search (rings r = 1, 2 in the reference
-// scan order) runs one candidate per lane and is reduced to the FIRST maximum
-// of k (strict `>` scan == lowest lane among equal maxima, ring 1 before 2).
-// The update is made by one lane; __syncwarp orders it before the next
-// sliver's loads, so the chain of dependent slivers sees the same values as
-// the reference loop. The flag byte d.sliver is rewritten for every finalized
-// cell each step, so stale bitmap bits (after an aborted step) are harmless.
 __device__ __forceinline__ void sliver_offset(int lane, int& di, int& dj, int& ring) {
     if (lane < 8) {  // ring 1: (dj, di) row-major, centre skipped
         const int q = lane < 4 ? lane : lane + 1;
@@ -1477,138 +1467,271 @@ __device__ __forceinline__ void sliver_offset(int lane, int& di, int& dj, int& r
     }
 }
 
-// candidate data of one ring lane for material a (see sliver_one)
-struct SliverCand {
-    double mv, kv, mev, mcv;
+// Sequential sliver redistribution (remap.cpp:194-226) in the reference's
+// row-major `pending` order. The tile kernel marks each sliver in a row bitmap
+// and a 32-cell segment bitmap (finalize_cell); this kernel (one block of
+// SLB threads) first lists the slivers of a chunk of rows in order, all warps
+// in parallel (rows compacted, per-row counts scanned, positions written),
+// then one warp applies them one after another:
+//  * each sliver's 24 ring candidates are loaded by 24 lanes and reduced to
+//    the FIRST maximum of k (the strict `>` scan = lowest lane among equal
+//    maxima, ring 1 before ring 2);
+//  * the candidates of the next SLD slivers are loaded ahead; every applied
+//    sliver broadcasts the cell and values it wrote and the pending records
+//    patch the copies they hold, so each record always sees the values the
+//    reference's loop would (exact), and the chain of dependent slivers runs
+//    at shuffle speed instead of one memory round trip per sliver.
+constexpr int SLB = 256, SLROWS = 4096, SLD = 4;
+
+struct SliverRec {
+    int sc, fl, nc, own;       // cell, flags, this lane's candidate cell, own-cell flag
+    double sm[2], sme[2];      // sliver masses (remap.cpp:172)
+    double mv[2], kv[2], mev[2], mcv;  // candidate m, k, me per material, mcell
 };
-__device__ __forceinline__ SliverCand sliver_load(const Dev& d, int a, bool inb, int nc) {
-    SliverCand q{0.0, -1.0, 0.0, 0.0};
-    if (inb) {
-        q.mv = d.nm[a][nc];
-        q.kv = d.nk[a][nc];
-        q.mev = d.me[a][nc];
-        q.mcv = d.mcell[nc];
-    }
-    return q;
-}
 
-__device__ __forceinline__ void sliver_apply(const Dev& d, int a, int si, int sj, int sc, int lane, int ring, int nc,
-                                             const SliverCand& q, double smv, double smev) {
-    const bool cand = q.kv > -1.0 && !(q.mv <= 0.0);  // the reference skips m <= 0, then needs k > bk
-    // lexicographic min of (ring, -k, lane) over candidates
-    int br = cand ? ring : 4, bl = lane;
-    double bkv = q.kv;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const int orr = __shfl_xor_sync(0xffffffffu, br, o);
-        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-        const double ok = __shfl_xor_sync(0xffffffffu, bkv, o);
-        const bool take = orr < br || (orr == br && br < 4 && (ok > bkv || (ok == bkv && ol < bl)));
-        if (take) {
-            br = orr;
-            bl = ol;
-            bkv = ok;
-        }
-    }
-    const bool found = br < 4;
-    const double mcar = __shfl_sync(0xffffffffu, q.mv, found ? bl : 0);
-    if (found && mcar + smv > 0.0) {
-        if (lane == bl) {
-            const double nmv = q.mv + smv;
-            const double nme = q.mev + smev;
-            d.nm[a][nc] = nmv;
-            d.me[a][nc] = nme;
-            d.ne[a][nc] = nme / nmv;
-            d.mcell[nc] = q.mcv + smv;
-        }
-    } else if (lane == 0) {
-        if (own_cell(d, si, sj)) d.ctl->step_fix += 1;
-        const int b = 1 - a;
-        const double nmv = d.nm[b][sc] + smv;
-        const double nme = d.me[b][sc] + smev;
-        d.nm[b][sc] = nmv;
-        d.me[b][sc] = nme;
-        d.ne[b][sc] = nme / nmv;
-        d.mcell[sc] += smv;
-    }
-    __syncwarp();
-}
-
-// One pending cell: the flag byte, the sliver masses and the ring candidates
-// of BOTH materials are loaded in one round (independent loads); a cell with
-// two slivers reloads material 1's candidates after material 0 is applied.
-__device__ __forceinline__ void sliver_one(const Dev& d, const Rng& rg, int si, int sj, int lane) {
-    const int sc = ix(d, si, sj);
-    int di = 0, dj = 0, ring = 3;
-    if (lane < 24) sliver_offset(lane, di, dj, ring);
+__device__ __forceinline__ void sliver_load(const Dev& d, const Rng& rg, int v, int lane, int di, int dj,
+                                            SliverRec& r) {
+    const int W = rg.i1 - rg.i0;  // v = (j - rg.j0) * W + (i - rg.i0)
+    const int sj = rg.j0 + v / W, si = rg.i0 + v % W;
+    const int c = ix(d, si, sj);
+    r.sc = c;
+    r.own = own_cell(d, si, sj);
     int ni = si + di, nj = sj + dj;
     if (d.per_x) ni = (ni + 2 * d.nx) % d.nx;
     if (d.per_y) nj = (nj + 2 * d.ny) % d.ny;
     const bool inb = lane < 24 && ni >= 0 && ni < d.nx && nj >= 0 && nj < d.ny && in(rg, ni, nj);
-    const int nc = inb ? ix(d, ni, nj) : sc;
-    const unsigned fl = d.sliver[sc];
-    const double sm0 = d.slm[0][sc], sme0 = d.slme[0][sc], sm1 = d.slm[1][sc], sme1 = d.slme[1][sc];
-    const SliverCand q0 = sliver_load(d, 0, inb, nc);
-    SliverCand q1 = sliver_load(d, 1, inb, nc);
-    if (fl & 1u) sliver_apply(d, 0, si, sj, sc, lane, ring, nc, q0, sm0, sme0);
-    if (fl & 2u) {
-        if (fl & 1u) q1 = sliver_load(d, 1, inb, nc);  // material 0 may have moved a carrier's mcell
-        sliver_apply(d, 1, si, sj, sc, lane, ring, nc, q1, sm1, sme1);
+    r.nc = inb ? ix(d, ni, nj) : -1;
+    r.fl = d.sliver[c];
+    r.mcv = 0.0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        r.sm[a] = d.slm[a][c];
+        r.sme[a] = d.slme[a][c];
+        r.mv[a] = 0.0;
+        r.kv[a] = -1.0;
+        r.mev[a] = 0.0;
+        if (inb) {
+            r.mv[a] = d.nm[a][r.nc];
+            r.kv[a] = d.nk[a][r.nc];
+            r.mev[a] = d.me[a][r.nc];
+        }
+    }
+    if (inb) r.mcv = d.mcell[r.nc];
+}
+
+// a write of (m, me of material a, mcell) to cell w, seen by a pending record
+__device__ __forceinline__ void sliver_patch(SliverRec& r, int w, int a, double nm, double nme, double nmc) {
+    if (r.nc == w) {
+        if (a == 0) {
+            r.mv[0] = nm;
+            r.mev[0] = nme;
+        } else {
+            r.mv[1] = nm;
+            r.mev[1] = nme;
+        }
+        r.mcv = nmc;
     }
 }
 
-__global__ void k_slivers(Dev d) {
-    pdl_enter();
-    if (halted(d.ctl)) return;
-    const int lane = threadIdx.x;
-    const Rng rg = d.r_gath;
-    const int nrow = rg.j1 - rg.j0, nwx = (rg.i1 - rg.i0 + 31) >> 5, nrw = (nrow + 31) >> 5;
-    for (int rw0 = 0; rw0 < nrw; rw0 += 32) {
-        const int rw = rw0 + lane;
-        const unsigned rb = rw < nrw ? d.sl_rows[rw] : 0u;
-        if (rb) d.sl_rows[rw] = 0u;
-        unsigned wm = __ballot_sync(0xffffffffu, rb != 0u);
-        while (wm) {
-            const int L = __ffs(wm) - 1;
-            wm &= wm - 1;
-            unsigned bits = __shfl_sync(0xffffffffu, rb, L);
-            while (bits) {
-                const int jr = ((rw0 + L) << 5) + __ffs(bits) - 1;
-                bits &= bits - 1;
-                unsigned* seg = d.sl_segs + (size_t)jr * nwx;
-                // 256 segment words per pass, 8 consecutive words per lane
-                // loaded together (one latency per row); lane-major = row order
-                for (int wb = 0; wb < nwx; wb += 256) {
-                    unsigned w[8];
-                    unsigned any = 0u;
+// Apply one pending record (both of its materials, a = 0 first as the
+// reference pushes them, remap.cpp:170-181); returns nothing, patches `p1..p3`.
+__device__ __forceinline__ void sliver_apply_rec(const Dev& d, SliverRec& r, int lane, int ring, SliverRec& p1,
+                                                 SliverRec& p2, SliverRec& p3) {
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int wi = wb + lane * 8 + k;
-                        w[k] = wi < nwx ? seg[wi] : 0u;
-                        any |= w[k];
-                    }
-                    if (any) {
+    for (int a = 0; a < 2; ++a) {
+        if (!(r.fl & (1 << a))) continue;
+        const double mv = a ? r.mv[1] : r.mv[0], kv = a ? r.kv[1] : r.kv[0];
+        const double mev = a ? r.mev[1] : r.mev[0];
+        const double smv = a ? r.sm[1] : r.sm[0], smev = a ? r.sme[1] : r.sme[0];
+        const bool cand = kv > -1.0 && !(mv <= 0.0);  // the reference skips m <= 0, then needs k > bk
+        int br = cand ? ring : 4, bl = lane;
+        double bkv = kv;
 #pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            if (w[k]) seg[wb + lane * 8 + k] = 0u;
-                    }
-                    unsigned lanes = __ballot_sync(0xffffffffu, any != 0u);
-                    while (lanes) {
-                        const int L2 = __ffs(lanes) - 1;
-                        lanes &= lanes - 1;
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            unsigned cb = __shfl_sync(0xffffffffu, w[k], L2);
-                            while (cb) {
-                                const int i = rg.i0 + ((wb + L2 * 8 + k) << 5) + __ffs(cb) - 1;
-                                cb &= cb - 1;
-                                sliver_one(d, rg, i, rg.j0 + jr, lane);
-                            }
-                        }
-                    }
-                }
+        for (int o = 16; o > 0; o >>= 1) {
+            const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+            const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+            const double ok = __shfl_xor_sync(0xffffffffu, bkv, o);
+            const bool take = orr < br || (orr == br && br < 4 && (ok > bkv || (ok == bkv && ol < bl)));
+            if (take) {
+                br = orr;
+                bl = ol;
+                bkv = ok;
             }
         }
+        const bool found = br < 4;
+        const double mcar = __shfl_sync(0xffffffffu, mv, found ? bl : 0);
+        int w, wa, src;
+        double nm = 0.0, nme = 0.0, nmc = 0.0;
+        if (found && mcar + smv > 0.0) {  // the carrier takes the sliver (remap.cpp:212-216)
+            w = __shfl_sync(0xffffffffu, r.nc, bl);
+            wa = a;
+            src = bl;
+            if (lane == bl) {
+                nm = mv + smv;
+                nme = mev + smev;
+                nmc = r.mcv + smv;
+                d.nm[a][w] = nm;
+                d.me[a][w] = nme;
+                d.ne[a][w] = nme / nm;
+                d.mcell[w] = nmc;
+            }
+        } else {  // no carrier: the partner material at the sliver's own cell (:217-225)
+            w = r.sc;
+            wa = 1 - a;
+            src = 0;
+            if (lane == 0) {  // rare: fresh loads (memory is current after the __syncwarp)
+                if (r.own) d.ctl->step_fix += 1;
+                nm = d.nm[wa][w] + smv;
+                nme = d.me[wa][w] + smev;
+                nmc = d.mcell[w] + smv;
+                d.nm[wa][w] = nm;
+                d.me[wa][w] = nme;
+                d.ne[wa][w] = nme / nm;
+                d.mcell[w] = nmc;
+            }
+        }
+        nm = __shfl_sync(0xffffffffu, nm, src);
+        nme = __shfl_sync(0xffffffffu, nme, src);
+        nmc = __shfl_sync(0xffffffffu, nmc, src);
+        sliver_patch(r, w, wa, nm, nme, nmc);  // this cell's second material sees the first
+        sliver_patch(p1, w, wa, nm, nme, nmc);
+        sliver_patch(p2, w, wa, nm, nme, nmc);
+        sliver_patch(p3, w, wa, nm, nme, nmc);
+        __syncwarp();
+    }
+}
+
+// block-wide exclusive scan of one int per thread (SLB threads); returns the total
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int t = lane < SLB / 32 ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        s_warp[32 + lane] = t;  // inclusive warp prefixes
+    }
+    __syncthreads();
+    total = s_warp[32 + SLB / 32 - 1];
+    const int base = wid ? s_warp[32 + wid - 1] : 0;
+    const int r = base + x - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(SLB, 1) k_slivers(Dev d) {
+    pdl_enter();
+    __shared__ int s_halt, s_total;
+    __shared__ int s_rows[SLROWS], s_off[SLROWS];
+    __shared__ int s_warp[64];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
+    const Rng rg = d.r_gath;
+    const int nrow = rg.j1 - rg.j0, nwx = (rg.i1 - rg.i0 + 31) >> 5;
+    int di = 0, dj = 0, ring = 3;
+    if (lane < 24) sliver_offset(lane, di, dj, ring);
+    for (int r0 = 0; r0 < nrow; r0 += SLROWS) {
+        // (1) rows of this chunk holding slivers, in order
+        constexpr int NRW = SLROWS / 32;
+        unsigned rb = 0u;
+        const int rw = (r0 >> 5) + tid;
+        if (tid < NRW && (r0 + 32 * tid) < nrow) {
+            rb = d.sl_rows[rw];
+            if (rb) d.sl_rows[rw] = 0u;
+        }
+        int nrows;
+        const int rpos = block_excl_scan(__popc(rb), s_warp, nrows);
+        for (unsigned b = rb, q = rpos; b; b &= b - 1, ++q) s_rows[q] = r0 + 32 * tid + __ffs(b) - 1;
+        __syncthreads();
+        if (nrows == 0) continue;
+        // (2) slivers per row (one warp per row), (3) scanned into offsets
+        for (int k = wid; k < nrows; k += SLB / 32) {
+            const unsigned* seg = d.sl_segs + (size_t)s_rows[k] * nwx;
+            int cnt = 0;
+            for (int w = lane; w < nwx; w += 32) cnt += __popc(seg[w]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            if (lane == 0) s_off[k] = cnt;
+        }
+        __syncthreads();
+        {
+            int run = 0;  // SLROWS / SLB rows per thread, scanned by blocks of consecutive rows
+            constexpr int PER = SLROWS / SLB;
+            int loc[PER];
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int k = tid * PER + q;
+                loc[q] = k < nrows ? s_off[k] : 0;
+                run += loc[q];
+            }
+            int tot;
+            int base = block_excl_scan(run, s_warp, tot);
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int k = tid * PER + q;
+                if (k < nrows) s_off[k] = base;
+                base += loc[q];
+            }
+            if (tid == 0) s_total = tot;
+        }
+        __syncthreads();
+        // (4) positions, row-major (words in order, bits in order), words cleared
+        for (int k = wid; k < nrows; k += SLB / 32) {
+            const int jr = s_rows[k];
+            unsigned* seg = d.sl_segs + (size_t)jr * nwx;
+            int base = s_off[k];
+            for (int w0 = 0; w0 < nwx; w0 += 32) {
+                const int w = w0 + lane;
+                unsigned bits = w < nwx ? seg[w] : 0u;
+                if (bits) seg[w] = 0u;
+                const int c = __popc(bits);
+                int x = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                int p = base + x - c;
+                for (; bits; bits &= bits - 1, ++p) d.sl_list[p] = jr * (rg.i1 - rg.i0) + (w << 5) + __ffs(bits) - 1;
+                base += __shfl_sync(0xffffffffu, x, 31);
+            }
+        }
+        __syncthreads();
+        // (5) one warp applies them in order, SLD records in flight
+        if (wid == 0) {
+            const int n = s_total;
+            SliverRec r0v, r1v, r2v, r3v;
+            if (0 < n) sliver_load(d, rg, d.sl_list[0], lane, di, dj, r0v);
+            if (1 < n) sliver_load(d, rg, d.sl_list[1], lane, di, dj, r1v);
+            if (2 < n) sliver_load(d, rg, d.sl_list[2], lane, di, dj, r2v);
+            if (3 < n) sliver_load(d, rg, d.sl_list[3], lane, di, dj, r3v);
+            for (int k = 0; k < n; k += SLD) {
+                sliver_apply_rec(d, r0v, lane, ring, r1v, r2v, r3v);
+                if (k + 4 < n) sliver_load(d, rg, d.sl_list[k + 4], lane, di, dj, r0v);
+                if (k + 1 >= n) break;
+                sliver_apply_rec(d, r1v, lane, ring, r2v, r3v, r0v);
+                if (k + 5 < n) sliver_load(d, rg, d.sl_list[k + 5], lane, di, dj, r1v);
+                if (k + 2 >= n) break;
+                sliver_apply_rec(d, r2v, lane, ring, r3v, r0v, r1v);
+                if (k + 6 < n) sliver_load(d, rg, d.sl_list[k + 6], lane, di, dj, r2v);
+                if (k + 3 >= n) break;
+                sliver_apply_rec(d, r3v, lane, ring, r0v, r1v, r2v);
+                if (k + 7 < n) sliver_load(d, rg, d.sl_list[k + 7], lane, di, dj, r3v);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -2822,7 +2945,7 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
 
 // slivers + finalize_cells ghost fill + flux ghosts
 void launch_remap_slivers(const Dev& d, cudaStream_t s) {
-    if (d.nmat == 2) pdl(k_slivers, dim3(1), dim3(32), 0, s, d);
+    if (d.nmat == 2) pdl(k_slivers, dim3(1), dim3(SLB), 0, s, d);
     // finalize_cells ghost fill (remap.cpp:227-233) + face / corner flux ghosts
     FieldList fl{};
     int q = 0;
