@@ -10,6 +10,8 @@
 #include "h2d_device.cuh"
 #include "h2d_launch.h"
 
+#include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -39,6 +41,33 @@ __device__ __forceinline__ bool own_yface(const Dev& d, int i, int j) {  // cell
 // ---------------------------------------------------------------------------
 // Start of a step or of a single API phase. mode: 0 = run-loop step (applies
 // harness.cpp:390-391), 1 = API call with host dt, 2 = API cfl_dt only.
+// RemapDiag updates (remap.cpp:161-165). Whole regions can carry a rounding-
+// level violation at once (config 4, steps 80-117: tens of millions of cells),
+// so one same-address atomic per cell would serialise at the L2 slice: the
+// lanes that update combine first (max / count are order-free, so this is
+// exact), and a max no larger than the last value seen is not sent at all
+// (the stored maximum only grows, so a stale cached copy only lets more
+// updates through).
+__device__ __forceinline__ void bump_kviol(Ctl* ctl, double viol) {
+    namespace cg = cooperative_groups;
+    const auto g = cg::coalesced_threads();
+    const unsigned long long v = cg::reduce(g, (unsigned long long)__double_as_longlong(viol),
+                                            cg::greater<unsigned long long>());
+    if (g.thread_rank() == 0 && v > __ldca(&ctl->kviol_bits)) atomicMax(&ctl->kviol_bits, v);
+}
+__device__ __forceinline__ void bump_clip(Ctl* ctl) {
+    const auto g = cooperative_groups::coalesced_threads();
+    if (g.thread_rank() == 0) atomicAdd(&ctl->step_clip, (int)g.size());
+}
+
+// LagrangeResult::floor_count (lagrange.cpp:124,187), combined the same way
+__device__ __forceinline__ void bump_floor(Ctl* ctl, int n) {
+    namespace cg = cooperative_groups;
+    const auto g = cg::coalesced_threads();
+    const int v = cg::reduce(g, n, cg::plus<int>());
+    if (g.thread_rank() == 0) atomicAdd(&ctl->step_floor, v);
+}
+
 __global__ void k_begin(Ctl* c, int mode, double host_dt) {
     pdl_enter();
     if (c->err_key != kNoErr || c->done) return;
@@ -383,7 +412,7 @@ __global__ void k_lag_cells(Dev d) {
         d.ph[a][c] = pa_h;
     }
     d.pmh[c] = pmix;
-    if (floors && own) atomicAdd(&d.ctl->step_floor, floors);
+    if (floors && own) bump_floor(d.ctl, floors);
 }
 
 // Node part of predict (lagrange.cpp:135-142: nodal_mass state.cpp:34-36,
@@ -480,7 +509,7 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
         }
         d.el[a][n] = ea;
     }
-    if (floors && own) atomicAdd(&d.ctl->step_floor, floors);
+    if (floors && own) bump_floor(d.ctl, floors);
 }
 
 // The run-loop Lagrangian phase in ONE kernel per 32x8 node tile: Q and the
@@ -576,7 +605,7 @@ __global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
                     pmix += ka[a] * ph[a];
                 }
             }
-            if (floors && canon) atomicAdd(&d.ctl->step_floor, floors);
+            if (floors && canon) bump_floor(d.ctl, floors);
         }
         s_q[t] = q;
         s_pmh[t] = pmix;
@@ -658,7 +687,7 @@ __global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
         }
         d.el[a][n] = ea;
     }
-    if (floors && own) atomicAdd(&d.ctl->step_floor, floors);
+    if (floors && own) bump_floor(d.ctl, floors);
 }
 
 // ---------------------------------------------------------------------------
@@ -1071,9 +1100,9 @@ __device__ __forceinline__ void finalize_cell(const Dev& d, const Rng& rg, int i
 #pragma unroll
         for (int q = 0; q < 5; ++q)
             if (viol < cand[q]) viol = cand[q];
-        if (viol > 0.0 && own) atomicMax(&d.ctl->kviol_bits, (unsigned long long)__double_as_longlong(viol));
+        if (viol > 0.0 && own) bump_kviol(d.ctl, viol);
         if (k0 < 0.0 || k0 > 1.0) {
-            if (own) atomicAdd(&d.ctl->step_clip, 1);
+            if (own) bump_clip(d.ctl);
             k0 = (k0 < 0.0) ? 0.0 : ((1.0 < k0) ? 1.0 : k0);
         }
         if (k0 < kPureTol) k0 = 0.0;
