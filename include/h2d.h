@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define H2D_ABI_VERSION 1
+#define H2D_ABI_VERSION 2
 #define H2D_MAX_MAT 2 /* reference kMaxMat, state.hpp:13 */
 #define H2D_GHOST 2   /* reference kGhost, field.hpp:11 */
 
@@ -139,6 +139,16 @@ typedef struct {
     char what[256];
 } h2d_error;
 
+/* StepDiag (harness.hpp:66-72) with its Totals (state.hpp:93-98): the record
+ * run() appends to RunReport::series after every step (make_diag,
+ * harness.cpp:360-376, called at :410). */
+typedef struct {
+    int step;
+    double t, dt;
+    double mass, mass_mat[H2D_MAX_MAT], momentum_x, momentum_y, internal_energy;
+    double min_rho, max_rho, min_p, max_p;
+} h2d_step_diag;
+
 /* Device-resident run loop (harness.cpp:380-412, non-kinematic branch). */
 typedef struct {
     int max_steps;    /* 0 = until t_end (compares the state's absolute step) */
@@ -151,6 +161,13 @@ typedef struct {
     int steps_done;
     int floor_count;  /* sum of LagrangeResult::floor_count */
     h2d_remap_diag diag;
+    /* optional host array receiving one StepDiag per step done (make_diag of
+     * the new State, harness.cpp:410). The product reduces it on the device
+     * inside the step: step / t / dt and the extrema are the reference's bits;
+     * the sums are a fixed-order tree instead of the reference's serial loop,
+     * so each is within n * 2^-53 * sum|term| of it (n terms). */
+    h2d_step_diag* series;
+    int series_cap;
 } h2d_run_args;
 
 /* One block of a 2D domain decomposition (no reference counterpart: the
@@ -216,6 +233,11 @@ int h2d_run(h2d_ctx* ctx, h2d_run_args* args);
 /* Totals compute_totals(const State&) (state.hpp:100, state.cpp:145-160);
  * out = {mass, mass_mat0, mass_mat1, momentum.x, momentum.y, internal_energy}. */
 int h2d_totals(h2d_ctx* ctx, double out[6]);
+
+/* StepDiag make_diag(const State&, double dt) (harness.cpp:360-376) of the
+ * context's current State, e.g. RunReport::series[0] = make_diag(s, 0.0)
+ * (harness.cpp:385); sums in the reference's serial order. */
+int h2d_step_diag_now(h2d_ctx* ctx, double dt, h2d_step_diag* out);
 
 /* ---- 2D block decomposition (no reference counterpart) ----
  * A block context owns [oi, oi+bnx) x [oj, oj+bny) of the global mesh plus a

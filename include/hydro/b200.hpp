@@ -225,12 +225,24 @@ void update_interface_normals(State& s);
 // ---- harness -------------------------------------------------------------------------
 double cfl_dt(const State& s, const MaterialSet& mats, double cfl);
 
+// StepDiag, harness.hpp:66-72 (the record run() appends per step)
+struct StepDiag {
+    int step = 0;
+    double t = 0.0, dt = 0.0;
+    Totals totals;
+    double min_rho = 0.0, max_rho = 0.0;
+    double min_p = 0.0, max_p = 0.0;
+};
+
 namespace b200 {
 
 struct StepInfo {
     int steps_done = 0;
     int floor_count = 0;
     std::vector<double> dts;
+    // make_diag of every new State (RunReport::series[1:], harness.cpp:410),
+    // reduced on the device inside the step (see h2d.h, h2d_step_diag)
+    std::vector<StepDiag> series;
 };
 
 // Device-resident run loop: the State lives on the GPU between steps; only
@@ -248,6 +260,8 @@ public:
     // runs until s.step >= max_steps (if > 0) or time >= t_end; throws the
     // reference exception of the first failing step
     StepInfo run(int max_steps, double t_end, double cfl, RemapDiag* diag = nullptr);
+    // make_diag(s, dt) of the resident State (harness.cpp:360-376), e.g. series[0]
+    StepDiag diag_now(double dt = 0.0) const;
 
 private:
     void* ctx_ = nullptr;

@@ -1549,6 +1549,8 @@ static void nan_scan(ctx_t* c) {
                 raise_err(c, H2D_ERR_SIM, i, j, "non-finite velocity");
 }
 
+int h2do_step_diag_now(ctx_t* c, double dt, h2d_step_diag* d);
+
 /* run loop, harness.cpp:390-412 (non-kinematic) */
 int h2do_run(ctx_t* c, h2d_run_args* a) {
     a->steps_done = 0;
@@ -1579,6 +1581,7 @@ int h2do_run(ctx_t* c, h2d_run_args* a) {
         }
         nan_scan(c);
         if (a->dt_log && a->steps_done < a->dt_log_cap) a->dt_log[a->steps_done] = dt;
+        if (a->series && a->steps_done < a->series_cap) h2do_step_diag_now(c, dt, &a->series[a->steps_done]);
         a->steps_done += 1;
     }
     return 0;
@@ -1602,6 +1605,32 @@ int h2do_totals(ctx_t* c, double out[6]) {
             py += mp * VY(c->u, i, j);
         }
     out[0] = mass; out[1] = mm[0]; out[2] = mm[1]; out[3] = px; out[4] = py; out[5] = ie;
+    return 0;
+}
+
+/* make_diag, harness.cpp:360-376 */
+int h2do_step_diag_now(ctx_t* c, double dt, h2d_step_diag* d) {
+    double t[6];
+    h2do_totals(c, t);
+    memset(d, 0, sizeof *d);
+    d->step = c->step;
+    d->t = c->time;
+    d->dt = dt;
+    d->mass = t[0];
+    d->mass_mat[0] = t[1];
+    d->mass_mat[1] = t[2];
+    d->momentum_x = t[3];
+    d->momentum_y = t[4];
+    d->internal_energy = t[5];
+    d->min_rho = d->max_rho = A(c->rho_mix, 0, 0);
+    d->min_p = d->max_p = A(c->p_mix, 0, 0);
+    for (int j = 0; j < c->ny; ++j)
+        for (int i = 0; i < c->nx; ++i) {
+            d->min_rho = ref_min(d->min_rho, A(c->rho_mix, i, j));
+            d->max_rho = ref_max(d->max_rho, A(c->rho_mix, i, j));
+            d->min_p = ref_min(d->min_p, A(c->p_mix, i, j));
+            d->max_p = ref_max(d->max_p, A(c->p_mix, i, j));
+        }
     return 0;
 }
 

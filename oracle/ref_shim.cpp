@@ -260,6 +260,32 @@ int h2dr_remap_step(h2dr_ctx* c, double dt, int kind, int x_first, int remap_vel
     });
 }
 
+// make_diag (harness.cpp:360-376; file-local there, restated over the
+// reference's own compute_totals)
+static h2d_step_diag ref_make_diag(const State& s, double dt) {
+    h2d_step_diag d{};
+    d.step = s.step;
+    d.t = s.time;
+    d.dt = dt;
+    const Totals t = compute_totals(s);
+    d.mass = t.mass;
+    d.mass_mat[0] = t.mass_mat[0];
+    d.mass_mat[1] = t.mass_mat[1];
+    d.momentum_x = t.momentum.x;
+    d.momentum_y = t.momentum.y;
+    d.internal_energy = t.internal_energy;
+    d.min_rho = d.max_rho = s.rho_mix(0, 0);
+    d.min_p = d.max_p = s.p_mix(0, 0);
+    for (int j = 0; j < s.mesh.ny; ++j)
+        for (int i = 0; i < s.mesh.nx; ++i) {
+            d.min_rho = std::min(d.min_rho, s.rho_mix(i, j));
+            d.max_rho = std::max(d.max_rho, s.rho_mix(i, j));
+            d.min_p = std::min(d.min_p, s.p_mix(i, j));
+            d.max_p = std::max(d.max_p, s.p_mix(i, j));
+        }
+    return d;
+}
+
 // harness.cpp:390-412 with kinematic == false, on the context's State.
 int h2dr_run(h2dr_ctx* c, h2d_run_args* a) {
     State& s = c->s;
@@ -287,6 +313,7 @@ int h2dr_run(h2dr_ctx* c, h2d_run_args* a) {
         rc = guarded(c, -1, 0, [&] { ref_nan_scan(s, s.step); });
         if (rc) break;
         if (a->dt_log && a->steps_done < a->dt_log_cap) a->dt_log[a->steps_done] = dt;
+        if (a->series && a->steps_done < a->series_cap) a->series[a->steps_done] = ref_make_diag(s, dt);
         ++a->steps_done;
     }
     a->diag.max_k_violation = rd.max_k_violation;
@@ -294,6 +321,11 @@ int h2dr_run(h2dr_ctx* c, h2d_run_args* a) {
     a->diag.mass_fix_count = rd.mass_fix_count;
     c->have_lag = false;
     return rc;
+}
+
+int h2dr_step_diag_now(h2dr_ctx* c, double dt, h2d_step_diag* out) {
+    *out = ref_make_diag(c->s, dt);
+    return 0;
 }
 
 int h2dr_totals(h2dr_ctx* c, double out[6]) {

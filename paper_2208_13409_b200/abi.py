@@ -18,6 +18,7 @@ import numpy as np
 
 from . import errors
 
+ABI_VERSION = 2  # H2D_ABI_VERSION
 MAX_MAT = 2   # kMaxMat, state.hpp:13
 GHOST = 2     # kGhost, field.hpp:11
 
@@ -69,10 +70,27 @@ class ErrorRec(C.Structure):
                 ("in_step", C.c_int), ("what", C.c_char * 256)]
 
 
+class StepDiag(C.Structure):
+    """hydro::StepDiag + Totals (harness.hpp:66-72, state.hpp:93-98)."""
+    _fields_ = [("step", C.c_int), ("t", C.c_double), ("dt", C.c_double), ("mass", C.c_double),
+                ("mass_mat", C.c_double * MAX_MAT), ("momentum_x", C.c_double), ("momentum_y", C.c_double),
+                ("internal_energy", C.c_double), ("min_rho", C.c_double), ("max_rho", C.c_double),
+                ("min_p", C.c_double), ("max_p", C.c_double)]
+
+
+# the same record as a numpy structured dtype (C layout), for series arrays
+STEP_DIAG_DTYPE = np.dtype([("step", "<i4"), ("t", "<f8"), ("dt", "<f8"), ("mass", "<f8"),
+                            ("mass_mat", "<f8", (MAX_MAT,)), ("momentum_x", "<f8"), ("momentum_y", "<f8"),
+                            ("internal_energy", "<f8"), ("min_rho", "<f8"), ("max_rho", "<f8"),
+                            ("min_p", "<f8"), ("max_p", "<f8")], align=True)
+assert STEP_DIAG_DTYPE.itemsize == C.sizeof(StepDiag)
+
+
 class RunArgs(C.Structure):
     _fields_ = [("max_steps", C.c_int), ("t_end", C.c_double), ("cfl", C.c_double),
                 ("remap_kind", C.c_int), ("dt_log", _dp), ("dt_log_cap", C.c_int),
-                ("steps_done", C.c_int), ("floor_count", C.c_int), ("diag", RemapDiag)]
+                ("steps_done", C.c_int), ("floor_count", C.c_int), ("diag", RemapDiag),
+                ("series", C.POINTER(StepDiag)), ("series_cap", C.c_int)]
 
 
 def make_config(nx, ny, dx, dy, x0=0.0, y0=0.0, bc_x=BC_WALL, bc_y=BC_WALL, eos=((EOS_PERFECT, 1.4, 0.0),),
@@ -190,6 +208,8 @@ class RunResult:
     floor_count: int
     diag: dict
     dts: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    # one make_diag record per step done (RunReport::series[1:], harness.cpp:410)
+    series: np.ndarray = field(default_factory=lambda: np.zeros(0, STEP_DIAG_DTYPE))
 
 
 _SIGS = {
@@ -207,6 +227,7 @@ _SIGS = {
     "remap_step": ([C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(RemapDiag)], C.c_int),
     "run": ([C.c_void_p, C.POINTER(RunArgs)], C.c_int),
     "totals": ([C.c_void_p, _dp], C.c_int),
+    "step_diag_now": ([C.c_void_p, C.c_double, C.POINTER(StepDiag)], C.c_int),
     "last_error": ([C.c_void_p, C.POINTER(ErrorRec)], C.c_int),
 }
 # product-only extras (benchmark support)
@@ -235,7 +256,7 @@ class Library:
             if f is not None:
                 f.argtypes, f.restype = args, res
                 self.fn[name] = f
-        if self.fn["abi_version"]() != 1:
+        if self.fn["abi_version"]() != ABI_VERSION:
             raise RuntimeError(f"{path}: unexpected ABI version")
 
 
@@ -323,17 +344,21 @@ class Solver:
                                               C.byref(diag) if diag is not None else None))
 
     def run(self, max_steps: int, t_end: float = 1e30, cfl: float = 0.3, log_dt: bool = True,
-            kind: int = REMAP_DIRECTCF) -> RunResult:
+            kind: int = REMAP_DIRECTCF, series: bool = False) -> RunResult:
         a = RunArgs()
         a.max_steps, a.t_end, a.cfl, a.remap_kind = max_steps, t_end, cfl, kind
         dts = np.zeros(max(max_steps, 1)) if log_dt else None
         if dts is not None:
             a.dt_log, a.dt_log_cap = _ptr(dts), len(dts)
+        ser = np.zeros(max(max_steps, 1) if max_steps > 0 else 4096, STEP_DIAG_DTYPE) if series else None
+        if ser is not None:
+            a.series, a.series_cap = ser.ctypes.data_as(C.POINTER(StepDiag)), len(ser)
         rc = self.lib.fn["run"](self._h, C.byref(a))
         res = RunResult(a.steps_done, a.floor_count,
                         dict(max_k_violation=a.diag.max_k_violation, k_clip_count=a.diag.k_clip_count,
                              mass_fix_count=a.diag.mass_fix_count),
-                        dts[:a.steps_done] if dts is not None else np.zeros(0))
+                        dts[:a.steps_done] if dts is not None else np.zeros(0),
+                        ser[:a.steps_done].copy() if ser is not None else np.zeros(0, STEP_DIAG_DTYPE))
         if rc:
             rec = self.last_error()
             err = errors.from_record(rec)
@@ -353,6 +378,12 @@ class Solver:
 
     def flush_l2(self, nbytes: int = 512 << 20):
         self._check(self.lib.fn["flush_l2"](self._h, nbytes))
+
+    def step_diag(self, dt: float = 0.0) -> np.void:
+        """make_diag(s, dt) of the current State (harness.cpp:360-376)."""
+        out = np.zeros(1, STEP_DIAG_DTYPE)
+        self._check(self.lib.fn["step_diag_now"](self._h, dt, out.ctypes.data_as(C.POINTER(StepDiag))))
+        return out[0]
 
     def totals(self) -> dict:
         out = (C.c_double * 6)()

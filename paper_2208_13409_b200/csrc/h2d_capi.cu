@@ -11,6 +11,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -58,6 +59,9 @@ struct h2d_ctx {
     size_t xbuf_bytes = 0;
     void* flush = nullptr;
     size_t flush_bytes = 0;
+    void* diag_mem = nullptr;       // DiagRed scratch of k_post / the node update
+    size_t diag_tick_bytes = 0;     // the ticket words at the start of diag_mem
+    double* diag_log = nullptr;     // device StepDiag log of h2d_run (kDiagRec doubles per step)
 };
 
 namespace {
@@ -150,7 +154,51 @@ int ctl_reset(h2d_ctx* c) {
     h.wmax_bits = h.kviol_bits = 0;
     h.next_wmax_bits = 0;
     h.next_err_key = kNoErr;
+    h.diag_log = nullptr;
+    h.diag_log_cap = 0;
+    // a run that ended inside a step (error) can leave diagnostics tickets
+    // half counted: clear them for the next call
+    if (c->diag_mem) CK(cudaMemsetAsync(c->diag_mem, 0, c->diag_tick_bytes, c->st));
     return ctl_push(c);
+}
+
+// dt / StepDiag logs of a run of up to `cap` steps
+int ensure_logs(h2d_ctx* c, int cap) {
+    if (cap <= c->dt_log_cap) return 0;
+    if (c->dt_log) cudaFree(c->dt_log);
+    if (c->diag_log) cudaFree(c->diag_log);
+    c->dt_log = nullptr;
+    c->diag_log = nullptr;
+    c->dt_log_cap = 0;
+    CK(cudaMalloc(&c->dt_log, sizeof(double) * (size_t)cap));
+    CK(cudaMalloc(&c->diag_log, sizeof(double) * kDiagRec * (size_t)cap));
+    c->dt_log_cap = cap;
+    return 0;
+}
+
+// device StepDiag records -> h2d_step_diag (harness.hpp:66-72)
+int copy_series(h2d_ctx* c, h2d_step_diag* out, int n) {
+    if (!out || n <= 0) return 0;
+    std::vector<double> r((size_t)n * kDiagRec);
+    CK(cudaMemcpy(r.data(), c->diag_log, sizeof(double) * r.size(), cudaMemcpyDeviceToHost));
+    for (int q = 0; q < n; ++q) {
+        const double* x = &r[(size_t)q * kDiagRec];
+        h2d_step_diag& o = out[q];
+        o.step = (int)x[0];
+        o.t = x[1];
+        o.dt = x[2];
+        o.mass = x[3 + DG_MASS];
+        o.mass_mat[0] = x[3 + DG_MM0];
+        o.mass_mat[1] = c->nmat == 2 ? x[3 + DG_MM1] : 0.0;
+        o.momentum_x = x[3 + DG_PX];
+        o.momentum_y = x[3 + DG_PY];
+        o.internal_energy = x[3 + DG_IE];
+        o.min_rho = x[3 + DG_MINR];
+        o.max_rho = x[3 + DG_MAXR];
+        o.min_p = x[3 + DG_MINP];
+        o.max_p = x[3 + DG_MAXP];
+    }
+    return 0;
 }
 
 // Rebuild the reference exception of the first failing phase (errors.hpp).
@@ -648,6 +696,18 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     std::memset(c->hctl, 0, sizeof(Ctl));
     c->hctl->err_key = kNoErr;
     d.ctl = c->ctl;
+    {  // diagnostics scratch: the ticket, the second-level partials, the block partials
+        const size_t n0 = (size_t)diag_partials(d, 0), n1 = (size_t)diag_partials(d, 1);
+        c->diag_tick_bytes = 256;
+        const size_t bytes = 256 + sizeof(double) * ((size_t)kDiagBlocks * DG_N + n0 * DG_NCELL + n1 * 2);
+        if (cudaMalloc(&c->diag_mem, bytes) != cudaSuccess) return fail(H2D_ERR_NOMEM);
+        if (cudaMemset(c->diag_mem, 0, bytes) != cudaSuccess) return fail(H2D_ERR_DEVICE);
+        double* pp = reinterpret_cast<double*>(static_cast<char*>(c->diag_mem) + 256);
+        d.dsc.tick = static_cast<unsigned*>(c->diag_mem);
+        d.dsc.lvl2 = pp;
+        d.dsc.part[0] = pp + (size_t)kDiagBlocks * DG_N;
+        d.dsc.part[1] = d.dsc.part[0] + n0 * DG_NCELL;
+    }
     if (ctl_push(c)) return fail(H2D_ERR_DEVICE);
     // make_state defaults (state.cpp:5-23): k0 = 1, normals (1, 0), vol = dx*dy
     for (int p = 0; p < 2; ++p) {
@@ -681,6 +741,8 @@ void h2d_destroy(h2d_ctx* c) {
     if (c->ctl) cudaFree(c->ctl);
     if (c->hctl) cudaFreeHost(c->hctl);
     if (c->dt_log) cudaFree(c->dt_log);
+    if (c->diag_log) cudaFree(c->diag_log);
+    if (c->diag_mem) cudaFree(c->diag_mem);
     if (c->xbuf) cudaFree(c->xbuf);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
@@ -874,12 +936,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
         return H2D_ERR_INVALID;
     }
     const int cap = a->max_steps > 0 ? a->max_steps : 4096;
-    if (cap > c->dt_log_cap) {
-        if (c->dt_log) cudaFree(c->dt_log);
-        c->dt_log = nullptr;
-        CK(cudaMalloc(&c->dt_log, sizeof(double) * (size_t)cap));
-        c->dt_log_cap = cap;
-    }
+    if (int rc = ensure_logs(c, cap)) return rc;
     if (int rc = ctl_reset(c)) return rc;
     Ctl& h = *c->hctl;
     h.t_end = a->t_end;
@@ -892,6 +949,8 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
     h.max_k_violation = a->diag.max_k_violation;
     h.dt_log = c->dt_log;
     h.dt_log_cap = c->dt_log_cap;
+    h.diag_log = c->diag_log;
+    h.diag_log_cap = c->dt_log_cap;
     if (int rc = ctl_push(c)) return rc;
     int parity = c->cur;
     int rc = 0;
@@ -931,6 +990,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
         const int n = h.steps_done < a->dt_log_cap ? h.steps_done : a->dt_log_cap;
         CK(cudaMemcpy(a->dt_log, c->dt_log, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost));
     }
+    if (int rc = copy_series(c, a->series, h.steps_done < a->series_cap ? h.steps_done : a->series_cap)) return rc;
     c->have_lag = false;
     return decode_error(c, true);
 }
@@ -979,6 +1039,42 @@ int h2d_totals(h2d_ctx* c, double out[6]) {
     return 0;
 }
 
+int h2d_step_diag_now(h2d_ctx* c, double dt, h2d_step_diag* out) {
+    // make_diag (harness.cpp:360-376) on the host, in the reference's order
+    double t[6];
+    if (int rc = h2d_totals(c, t)) return rc;
+    const int nx = c->nx, ny = c->ny;
+    const size_t W = (size_t)nx + 2 * G;
+    std::vector<double> rho(W * (ny + 2 * G)), p(rho.size());
+    const StateBufs& s = c->sb[c->cur];
+    if (int rc = get_plane(c, rho.data(), s.rho_mix, nx, ny)) return rc;
+    if (int rc = get_plane(c, p.data(), s.p_mix, nx, ny)) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    if (int rc = ctl_pull(c)) return rc;
+    auto C = [&](const std::vector<double>& f, int i, int j) { return f[(size_t)(j + G) * W + (i + G)]; };
+    h2d_step_diag d{};
+    d.step = c->hctl->step;
+    d.t = c->hctl->time;
+    d.dt = dt;
+    d.mass = t[0];
+    d.mass_mat[0] = t[1];
+    d.mass_mat[1] = t[2];
+    d.momentum_x = t[3];
+    d.momentum_y = t[4];
+    d.internal_energy = t[5];
+    d.min_rho = d.max_rho = C(rho, 0, 0);
+    d.min_p = d.max_p = C(p, 0, 0);
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+            d.min_rho = std::min(d.min_rho, C(rho, i, j));
+            d.max_rho = std::max(d.max_rho, C(rho, i, j));
+            d.min_p = std::min(d.min_p, C(p, i, j));
+            d.max_p = std::max(d.max_p, C(p, i, j));
+        }
+    *out = d;
+    return 0;
+}
+
 int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_kind, float ms[8]) {
     cudaSetDevice(c->device);
     const bool ad = remap_kind == H2D_REMAP_AD;
@@ -1007,6 +1103,7 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_k
     if (phases) {  // un-graphed launches with events between the kernels / groups
         Dev d = make_dev(c, c->cur, 1);
         d.scan_nodes = 1;  // as the run-loop graph
+        d.diag = 1;
         CK(cudaEventRecord(c->ev[0], c->st));
         launch_step_start(d, c->st);
         CK(cudaEventRecord(c->ev[1], c->st));
@@ -1230,14 +1327,11 @@ int h2d_block_begin(h2d_ctx* c, int max_steps, double t_end, double cfl) {
     h.floor_count = h.k_clip_count = h.mass_fix_count = 0;
     h.max_k_violation = 0.0;
     const int cap = max_steps > 0 ? max_steps : 4096;
-    if (cap > c->dt_log_cap) {
-        if (c->dt_log) cudaFree(c->dt_log);
-        c->dt_log = nullptr;
-        CK(cudaMalloc(&c->dt_log, sizeof(double) * (size_t)cap));
-        c->dt_log_cap = cap;
-    }
+    if (int rc = ensure_logs(c, cap)) return rc;
     h.dt_log = c->dt_log;
     h.dt_log_cap = c->dt_log_cap;
+    h.diag_log = c->diag_log;
+    h.diag_log_cap = c->dt_log_cap;
     if (int rc = ctl_push(c)) return rc;
     if (int rc = ensure_graphs(c)) return rc;
     enqueue_cfl_next(c);  // wave speed of the owned cells of the initial State
@@ -1328,6 +1422,7 @@ int h2d_block_result(h2d_ctx* c, h2d_run_args* a) {
         const int n = h.steps_done < a->dt_log_cap ? h.steps_done : a->dt_log_cap;
         CK(cudaMemcpy(a->dt_log, c->dt_log, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost));
     }
+    if (int rc = copy_series(c, a->series, h.steps_done < a->series_cap ? h.steps_done : a->series_cap)) return rc;
     return decode_error(c, true);
 }
 

@@ -90,6 +90,28 @@ struct Ctl {
     // undo record of the last commit (block mode: a peer block failed first)
     double prev_time, prev_max_k_violation;
     int committed, counted;
+    // per-step diagnostics of the run loop (make_diag, harness.cpp:360-376):
+    // the values of the step in flight (k_post: cells, node update: momentum)
+    // and the device log the commit appends one record of kDiagRec doubles to
+    double dg[12];
+    double* diag_log;
+    int diag_log_cap;
+    int pad3_;
+};
+
+// StepDiag + Totals (harness.hpp:66-72, state.hpp:93-98) slots of Ctl::dg
+enum { DG_MASS, DG_IE, DG_MM0, DG_MM1, DG_MINR, DG_MAXR, DG_MINP, DG_MAXP, DG_NCELL, DG_PX = DG_NCELL, DG_PY, DG_N };
+// one log record: step, t, dt, then Ctl::dg[0 .. DG_N)
+constexpr int kDiagRec = 3 + DG_N;
+// Per-step diagnostics reduction: k_post and the node update store one
+// fixed-shape block partial each (no fences or tickets inside those kernels),
+// then k_diag_reduce folds them in index order (kDiagBlocks blocks, then the
+// last one to arrive), so the result does not depend on block scheduling.
+constexpr int kDiagBlocks = 148;
+struct DiagScratch {
+    double* part[2];  // [0] k_post blocks x DG_NCELL, [1] node blocks x 2
+    double* lvl2;     // kDiagBlocks x DG_N
+    unsigned* tick;
 };
 
 // Every thread of a kernel reads the control block: go through the read-only
@@ -162,6 +184,8 @@ struct Dev {
     Ctl* ctl;
     const TmaSet* tma;  // host pointer: the launch passes *tma by value (__grid_constant__)
     int scan_nodes;     // run loop: the node update also runs nan_scan's node part (harness.cpp:353-357)
+    int diag;           // run loop: reduce the step's make_diag values (k_post cells, node update momentum)
+    DiagScratch dsc;    // diagnostics block partials ([0] k_post, [1] node update) + k_diag_reduce scratch
 };
 
 // 32-bit plane offsets: P * R < 2^31 for every mesh up to 16384^2 (checked at
@@ -201,6 +225,49 @@ H2D_DEV double sound(const Dev& d, int a, double rho, double p, bool& bad) {
 H2D_DEV void pdl_enter() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---- per-step diagnostics ------------------------------------------------
+// op 0: sum, 1: min (std::min), 2: max (std::max)
+H2D_DEV double dg_comb(int op, double a, double b) { return op == 0 ? a + b : (op == 1 ? rmin(a, b) : rmax(a, b)); }
+H2D_DEV double dg_ident(int op) { return op == 0 ? 0.0 : (op == 1 ? CUDART_INF : -CUDART_INF); }
+
+// Fixed-shape block combine (every thread of the block must call it; the
+// block is a whole number of warps): a shuffle tree per warp, then warp 0's
+// thread 0 folds the warps in index order. Thread 0 holds the result.
+template <int NV>
+__device__ __forceinline__ void block_combine(double (&v)[NV], const int (&op)[NV], double* sh) {
+    const int t = threadIdx.y * blockDim.x + threadIdx.x, nw = (blockDim.x * blockDim.y) >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] = dg_comb(op[k], v[k], __shfl_down_sync(0xffffffffu, v[k], o));
+    if ((t & 31) == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) sh[(t >> 5) * NV + k] = v[k];
+    __syncthreads();
+    if (t == 0)
+        for (int w = 1; w < nw; ++w)
+#pragma unroll
+            for (int k = 0; k < NV; ++k) v[k] = dg_comb(op[k], v[k], sh[w * NV + k]);
+    __syncthreads();
+}
+
+// Warp partial of NV values, stored at part[(block * warps per block + warp) * NV]
+// by lane 0 (all 32 lanes call it; no block barrier).
+template <int NV>
+__device__ __forceinline__ void warp_partial(double (&v)[NV], const int (&op)[NV], double* part) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] = dg_comb(op[k], v[k], __shfl_down_sync(0xffffffffu, v[k], o));
+    const int t = threadIdx.y * blockDim.x + threadIdx.x;
+    if ((t & 31) == 0) {
+        const int nw = (blockDim.x * blockDim.y) >> 5;
+        const size_t w = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * nw + (t >> 5);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) part[w * NV + k] = v[k];
+    }
 }
 
 // van_leer, reconstruct.cpp:10-14

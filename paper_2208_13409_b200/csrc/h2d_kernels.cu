@@ -1956,11 +1956,7 @@ __global__ void __launch_bounds__(128, 8) k_dual_items(Dev d) {
 // X face i+1 (-), Y face j (+), Y face j+1 (-), corner (i-1, j-1, pair (1,1))
 // (-), own pairs (+, +), corner (i-1, j+1, pair (1,-1)) (-) — then
 // apply_dual_update (remap.cpp:444-464) and the wall condition (:462).
-__global__ void k_node_update_walls(Dev d) {
-    pdl_enter();
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, d.r_node.i0, d.r_node.j0);
+__device__ __forceinline__ void node_update_walls_at(const Dev& d, int i, int j, double& px, double& py) {
     const int nx = d.nx, ny = d.ny;
     if (!in(d.r_node, i, j) || i < 0 || j < 0 || i > nx || j > ny) return;
     const int s = ix(d, i, j);
@@ -2011,16 +2007,82 @@ __global__ void k_node_update_walls(Dev d) {
     d.unrm[s] = sqrt(ux * ux + uy * uy);
     if (d.scan_nodes && own_node(d, i, j) && (!isfinite(ux) | !isfinite(uy)))
         raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));  // nan_scan on the new u (harness.cpp:353-357)
+    if (d.diag && own_node(d, i, j)) {  // compute_totals' momentum term (state.cpp:154-158)
+        px = mp_new * ux;
+        py = mp_new * uy;
+    }
+}
+
+// Run-loop epilogue of the node kernels: the step's total momentum
+// (compute_totals, state.cpp:154-158) for the diagnostics record.
+__device__ __forceinline__ void node_momentum(const Dev& d, double px, double py) {
+    if (!d.diag) return;
+    double v[2] = {px, py};
+    const int op[2] = {0, 0};
+    warp_partial<2>(v, op, d.dsc.part[1]);
+}
+
+// The step's make_diag values (harness.cpp:360-376) from the block partials
+// of k_post (n0 blocks) and the node update (n1 blocks): block b folds the
+// b-th slice of each in index order, the last block to finish folds the
+// slices into Ctl::dg. Halted steps leave dg alone (no record is logged).
+__global__ void __launch_bounds__(256) k_diag_reduce(Ctl* ctl, DiagScratch r, int n0, int n1) {
+    pdl_enter();
+    __shared__ int s_last;
+    if (threadIdx.x == 0) s_last = halted(ctl);
+    __syncthreads();
+    if (s_last) return;
+    const int op[DG_N] = {0, 0, 0, 0, 1, 2, 1, 2, 0, 0};
+    double v[DG_N];
+#pragma unroll
+    for (int k = 0; k < DG_N; ++k) v[k] = dg_ident(op[k]);
+    const int t = threadIdx.x, b = blockIdx.x, G = gridDim.x;
+    const long long lo0 = (long long)n0 * b / G, hi0 = (long long)n0 * (b + 1) / G;
+    const long long lo1 = (long long)n1 * b / G, hi1 = (long long)n1 * (b + 1) / G;
+    for (long long q = lo0 + t; q < hi0; q += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < DG_NCELL; ++k) v[k] = dg_comb(op[k], v[k], r.part[0][q * DG_NCELL + k]);
+    for (long long q = lo1 + t; q < hi1; q += blockDim.x) {
+        v[DG_PX] += r.part[1][q * 2];
+        v[DG_PY] += r.part[1][q * 2 + 1];
+    }
+    __shared__ double sh[8 * DG_N];
+    block_combine<DG_N>(v, op, sh);
+    if (t == 0) {
+#pragma unroll
+        for (int k = 0; k < DG_N; ++k) r.lvl2[b * DG_N + k] = v[k];
+        __threadfence();
+        s_last = atomicAdd(r.tick, 1u) == (unsigned)G - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+#pragma unroll
+    for (int k = 0; k < DG_N; ++k) v[k] = dg_ident(op[k]);
+    for (int q = t; q < G; q += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < DG_N; ++k) v[k] = dg_comb(op[k], v[k], __ldcg(&r.lvl2[q * DG_N + k]));
+    block_combine<DG_N>(v, op, sh);
+    if (t == 0) {
+#pragma unroll
+        for (int k = 0; k < DG_N; ++k) ctl->dg[k] = v[k];
+        *r.tick = 0u;
+    }
+}
+
+__global__ void k_node_update_walls(Dev d) {
+    pdl_enter();
+    if (halted(d.ctl)) return;  // one load per warp: warp-uniform
+    int i, j;
+    tid2(i, j, d.r_node.i0, d.r_node.j0);
+    double px = 0.0, py = 0.0;
+    node_update_walls_at(d, i, j, px, py);
+    node_momentum(d, px, py);
 }
 
 // MomAcc gather (App. C item 4) + apply_dual_update (remap.cpp:444-464) with
 // the periodic copies (:458-461) folded in: thread per node (i, j) in
 // [0, nx] x [0, ny] computes the value of its source node.
-__global__ void k_node_update(Dev d) {
-    pdl_enter();
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, d.r_node.i0, d.r_node.j0);
+__device__ __forceinline__ void node_update_at(const Dev& d, int i, int j, double& px, double& py) {
     const int nx = d.nx, ny = d.ny;
     if (!in(d.r_node, i, j) || i < 0 || j < 0 || i > nx || j > ny) return;
     const int iend = d.per_x ? nx - 1 : nx, jend = d.per_y ? ny - 1 : ny;
@@ -2126,6 +2188,20 @@ __global__ void k_node_update(Dev d) {
     d.unrm[o] = sqrt(ux * ux + uy * uy);  // |u| for the next cfl_dt (harness.cpp:308)
     if (d.scan_nodes && own_node(d, i, j) && (!isfinite(ux) | !isfinite(uy)))
         raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));  // nan_scan on the new u (harness.cpp:353-357)
+    if (d.diag && i <= iend && j <= jend && own_node(d, i, j)) {  // state.cpp:154-158
+        px = mp_new * ux;
+        py = mp_new * uy;
+    }
+}
+
+__global__ void k_node_update(Dev d) {
+    pdl_enter();
+    if (halted(d.ctl)) return;  // one load per warp: warp-uniform
+    int i, j;
+    tid2(i, j, d.r_node.i0, d.r_node.j0);
+    double px = 0.0, py = 0.0;
+    node_update_at(d, i, j, px, py);
+    node_momentum(d, px, py);
 }
 
 // refresh_normals_impl + youngs_normal (remap.cpp:102-114, vof.cpp:10-22)
@@ -2218,6 +2294,13 @@ __global__ void k_commit_finish(Ctl* c) {
     c->committed = 1;
     if (!ok) return;
     if (c->dt_log && c->steps_done < c->dt_log_cap) c->dt_log[c->steps_done] = c->dt;
+    if (c->diag_log && c->steps_done < c->diag_log_cap) {  // rep.series.push_back(make_diag(s, dt))
+        double* r = c->diag_log + (size_t)c->steps_done * kDiagRec;
+        r[0] = (double)c->step;
+        r[1] = c->time;
+        r[2] = c->dt;
+        for (int k = 0; k < DG_N; ++k) r[3 + k] = c->dg[k];
+    }
     c->steps_done += 1;
     c->floor_count += c->step_floor;
     c->k_clip_count += c->step_clip;
@@ -2318,6 +2401,7 @@ template <int NM>
 __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
     pdl_enter();
     __shared__ unsigned long long sw[8];
+    __shared__ double s_dg[DG_NCELL][256];  // per-thread diagnostics terms (block of 32 x 8)
     __shared__ int s_halt;
     if (threadIdx.x == 0 && threadIdx.y == 0) s_halt = halted(d.ctl);
     __syncthreads();
@@ -2326,17 +2410,20 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
     tid2(i, j, d.r_sync.i0, d.r_sync.j0);
     const int nx = d.nx, ny = d.ny;
     unsigned long long wb = 0ull;
-    if (in(d.r_sync, i, j)) {
-        const int c = ix(d, i, j);
-        const double cv = d.cv;
-        double ka[2], ma[2], ea[2];
+    const bool act = in(d.r_sync, i, j);
+    const bool interior = i >= 0 && j >= 0 && i < nx && j < ny;
+    const int c = ix(d, i, j);
+    const double cv = d.cv;
+    double ka[2], ma[2], ea[2];
+    double m = 0.0, emix = 0.0, p = 0.0;
+    if (act) {
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
             ka[a] = d.nk[a][c];
             ma[a] = d.nm[a][c];
             ea[a] = d.ne[a][c];
         }
-        double m = 0.0, me = 0.0, p = 0.0;
+        double me = 0.0;
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
             if (ka[a] <= 0.0) continue;
@@ -2346,13 +2433,30 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
             const double rho_a = ma[a] / (ka[a] * cv);
             p += ka[a] * eos_p(d, a, rho_a, ea[a]);
         }
-        const double emix = m > 0.0 ? me / m : 0.0;
+        emix = m > 0.0 ? me / m : 0.0;
         d.nm_mix[c] = m;
         d.ne_mix[c] = emix;
         d.nrho_mix[c] = div_cv(d, m);
         d.np_mix[c] = p;
         d.nvol[c] = cv;
-        const bool interior = i >= 0 && j >= 0 && i < nx && j < ny;
+    }
+    // make_diag's cell part (harness.cpp:360-376, state.cpp:148-153): this
+    // cell's terms go to shared memory now (registers stay free for the rest)
+    // and are folded after the kernel's closing barrier
+    const int tl = threadIdx.y * blockDim.x + threadIdx.x;
+    if (run_loop && d.diag) {
+        const bool on = act && interior && own_cell(d, i, j);
+        const double rho = div_cv(d, m);
+        s_dg[DG_MASS][tl] = on ? m : 0.0;
+        s_dg[DG_IE][tl] = on ? m * emix : 0.0;
+        s_dg[DG_MM0][tl] = on ? ma[0] : 0.0;
+        s_dg[DG_MM1][tl] = on && NM == 2 ? ma[NM - 1] : 0.0;
+        s_dg[DG_MINR][tl] = on ? rho : CUDART_INF;
+        s_dg[DG_MAXR][tl] = on ? rho : -CUDART_INF;
+        s_dg[DG_MINP][tl] = on ? p : CUDART_INF;
+        s_dg[DG_MAXP][tl] = on ? p : -CUDART_INF;
+    }
+    if (act) {
         if (interior && in(d.r_nrm, i, j)) {
             if (NM == 2) {  // normals of the new fractions
                 double nrx = d.nrx[c], nry = d.nry[c];
@@ -2406,6 +2510,16 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
         if (t == 0) {
             for (int w = 1; w < (int)(blockDim.x * blockDim.y) / 32; ++w) wb = sw[w] > wb ? sw[w] : wb;
             if (wb) atomicMax(&d.ctl->next_wmax_bits, wb);
+        }
+        if (d.diag) {  // warp k folds diagnostics value k over the block's 256 cells (fixed order)
+            const int k = t >> 5, lane = t & 31;
+            const int op = (k == DG_MINR || k == DG_MINP) ? 1 : ((k == DG_MAXR || k == DG_MAXP) ? 2 : 0);
+            double v = s_dg[k][lane];
+#pragma unroll
+            for (int q = 1; q < 8; ++q) v = dg_comb(op, v, s_dg[k][lane + 32 * q]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = dg_comb(op, v, __shfl_down_sync(0xffffffffu, v, o));
+            if (lane == 0) d.dsc.part[0][((size_t)blockIdx.y * gridDim.x + blockIdx.x) * DG_NCELL + k] = v;
         }
     }
 }
@@ -2670,11 +2784,7 @@ __global__ void __launch_bounds__(128, 8) k_ad_dual(Dev d, int pass) {
 // AD MomAcc gather (one axis, face-loop order incl. the periodic seam) and
 // apply_dual_update (remap.cpp:444-464) with mcell_lag = the pass's input mcell
 template <int AX>
-__global__ void k_ad_node(Dev d, AdIO w) {
-    pdl_enter();
-    if (halted(d.ctl)) return;
-    int i, j;
-    tid2(i, j, d.r_node.i0, d.r_node.j0);
+__device__ __forceinline__ void ad_node_at(const Dev& d, const AdIO& w, int i, int j, double& px, double& py) {
     const int nx = d.nx, ny = d.ny;
     if (!in(d.r_node, i, j) || i < 0 || j < 0 || i > nx || j > ny) return;
     const int iend = d.per_x ? nx - 1 : nx, jend = d.per_y ? ny - 1 : ny;
@@ -2730,6 +2840,21 @@ __global__ void k_ad_node(Dev d, AdIO w) {
     d.unrm[o] = sqrt(ux * ux + uy * uy);
     if (d.scan_nodes && w.pass == 1 && own_node(d, i, j) && (!isfinite(ux) | !isfinite(uy)))
         raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));  // nan_scan on the final u
+    if (d.diag && w.pass == 1 && i <= iend && j <= jend && own_node(d, i, j)) {  // state.cpp:154-158
+        px = mp_new * ux;
+        py = mp_new * uy;
+    }
+}
+
+template <int AX>
+__global__ void k_ad_node(Dev d, AdIO w) {
+    pdl_enter();
+    if (halted(d.ctl)) return;  // one load per warp: warp-uniform
+    int i, j;
+    tid2(i, j, d.r_node.i0, d.r_node.j0);
+    double px = 0.0, py = 0.0;
+    ad_node_at<AX>(d, w, i, j, px, py);
+    if (w.pass == 1) node_momentum(d, px, py);
 }
 
 // refresh_normals_impl after AD pass 0 (remap.cpp:102-114): youngs normals of
@@ -2905,6 +3030,19 @@ void launch_post(const Dev& d, int run_loop, cudaStream_t s) {
         pdl(k_post<2>, gp, dim3(32, 8), 0, s, d, run_loop);
     else
         pdl(k_post<1>, gp, dim3(32, 8), 0, s, d, run_loop);
+    if (run_loop && d.diag) {
+        pdl(k_diag_reduce, dim3(kDiagBlocks), dim3(256), 0, s, d.ctl, d.dsc, (int)diag_partials(d, 0),
+            (int)diag_partials(d, 1));
+    }
+}
+
+long long diag_partials(const Dev& d, int which) {  // block counts of k_post / the node grids
+    if (which == 0) {  // one partial per k_post block
+        const dim3 g = tiles_of(d.r_sync, 32, 8);
+        return (long long)g.x * g.y;
+    }
+    const dim3 g = grid_of(d.r_node), b = blk2();  // one per node-update warp
+    return (long long)g.x * g.y * (b.x * b.y / 32);
 }
 
 void launch_post_ghosts(const Dev& d, cudaStream_t s) {
@@ -3004,6 +3142,7 @@ void launch_remap_dual(const Dev& d, cudaStream_t s) {
 void launch_step(const Dev& dd, cudaStream_t s) {
     Dev d = dd;
     d.scan_nodes = 1;
+    d.diag = 1;
     pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
     launch_lagrange_run(d, s);
     launch_remap_core(d, s);
@@ -3106,6 +3245,7 @@ void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_veloc
 void launch_step_ad(const Dev& dd, const AdWork& W, int x_first, cudaStream_t s) {
     Dev d = dd;
     d.scan_nodes = 1;
+    d.diag = 1;
     pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
     launch_lagrange_run(d, s);
     launch_remap_ad(d, W, x_first, 1, 1, s);

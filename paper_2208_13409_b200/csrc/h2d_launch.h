@@ -45,6 +45,7 @@ void launch_remap_core(const Dev& d, cudaStream_t s);  // = tile + slivers + dua
 void launch_lag_fused(const Dev& d, cudaStream_t s);
 void launch_lag_ghosts(const Dev& d, cudaStream_t s);
 void launch_post(const Dev& d, int run_loop, cudaStream_t s);
+long long diag_partials(const Dev& d, int which);
 void launch_post_ghosts(const Dev& d, cudaStream_t s);
 void launch_remap_tile(const Dev& d, cudaStream_t s);
 void launch_remap_slivers(const Dev& d, cudaStream_t s);

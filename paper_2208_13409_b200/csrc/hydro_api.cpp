@@ -299,6 +299,23 @@ State remap_step(const State& s, const MaterialSet& mats, const LagrangeResult& 
 // ---- device-resident run loop ------------------------------------------------------
 namespace b200 {
 
+static StepDiag from_c(const h2d_step_diag& c) {
+    StepDiag d;
+    d.step = c.step;
+    d.t = c.t;
+    d.dt = c.dt;
+    d.totals.mass = c.mass;
+    d.totals.mass_mat[0] = c.mass_mat[0];
+    d.totals.mass_mat[1] = c.mass_mat[1];
+    d.totals.momentum = Vec2{c.momentum_x, c.momentum_y};
+    d.totals.internal_energy = c.internal_energy;
+    d.min_rho = c.min_rho;
+    d.max_rho = c.max_rho;
+    d.min_p = c.min_p;
+    d.max_p = c.max_p;
+    return d;
+}
+
 Simulation::Simulation(const State& initial, const MaterialSet& mats, const PseudoViscosityParams& pvp,
                        const ReconConfig& rc, int device)
     : mesh_(initial.mesh), nmat_(initial.nmat) {
@@ -326,6 +343,13 @@ State Simulation::download() const {
     return s;
 }
 
+StepDiag Simulation::diag_now(double dt) const {
+    h2d_ctx* h = static_cast<h2d_ctx*>(ctx_);
+    h2d_step_diag d;
+    check(h, h2d_step_diag_now(h, dt, &d));
+    return from_c(d);
+}
+
 StepInfo Simulation::run(int max_steps, double t_end, double cfl, RemapDiag* diag) {
     h2d_ctx* h = static_cast<h2d_ctx*>(ctx_);
     StepInfo info;
@@ -338,6 +362,9 @@ StepInfo Simulation::run(int max_steps, double t_end, double cfl, RemapDiag* dia
     a.remap_kind = H2D_REMAP_DIRECTCF;
     a.dt_log = info.dts.data();
     a.dt_log_cap = static_cast<int>(info.dts.size());
+    std::vector<h2d_step_diag> ser(info.dts.size());
+    a.series = ser.data();
+    a.series_cap = static_cast<int>(ser.size());
     if (diag) {
         a.diag.max_k_violation = diag->max_k_violation;
         a.diag.k_clip_count = diag->k_clip_count;
@@ -347,6 +374,7 @@ StepInfo Simulation::run(int max_steps, double t_end, double cfl, RemapDiag* dia
     info.steps_done = a.steps_done;
     info.floor_count = a.floor_count;
     info.dts.resize(std::min<size_t>(info.dts.size(), static_cast<size_t>(a.steps_done)));
+    for (size_t q = 0; q < info.dts.size(); ++q) info.series.push_back(from_c(ser[q]));
     if (diag) {
         diag->max_k_violation = a.diag.max_k_violation;
         diag->k_clip_count = a.diag.k_clip_count;

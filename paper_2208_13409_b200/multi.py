@@ -25,7 +25,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import errors
-from .abi import Config, ErrorRec, HostState, Library, RunArgs, _ptr
+from .abi import STEP_DIAG_DTYPE, Config, ErrorRec, HostState, Library, RunArgs, StepDiag, _ptr
 
 HALO = 8
 NO_ERR = (1 << 64) - 1
@@ -166,17 +166,46 @@ class BlockSolver:
     def unpack(self, dx, dy, ptr):
         self._check(self.lib.fn["halo_unpack"](self._h, dx, dy, C.c_void_p(ptr)))
 
-    def result(self, cap: int):
+    def result(self, cap: int, series: bool = False):
+        """(RunArgs, dt log, error) of the block's run; with series=True the
+        RunArgs carries `block_series`: this block's per-step make_diag
+        partials (owned cells / nodes), merged across blocks by
+        combine_series."""
         a = RunArgs()
         dts = np.zeros(max(cap, 1))
         a.dt_log, a.dt_log_cap = _ptr(dts), len(dts)
+        ser = np.zeros(max(cap, 1), STEP_DIAG_DTYPE) if series else None
+        if ser is not None:
+            a.series, a.series_cap = ser.ctypes.data_as(C.POINTER(StepDiag)), len(ser)
         rc = self.lib.fn["block_result"](self._h, C.byref(a))
         err = None
         if rc:
             rec = ErrorRec()
             self.lib.fn["last_error"](self._h, C.byref(rec))
             err = errors.from_record(rec)
+        a.block_series = ser[:a.steps_done].copy() if ser is not None else None
         return a, dts[:a.steps_done], err
+
+
+_SUMS = ("mass", "mass_mat", "momentum_x", "momentum_y", "internal_energy")
+
+
+def combine_series(parts: Sequence[np.ndarray]) -> np.ndarray:
+    """RunReport::series of the whole mesh from the blocks' per-step partials
+    (block order fixed: sums added in that order, extrema combined; step, t
+    and dt are the same on every block). No communication inside the step:
+    the diagnostics are reduced across blocks only when they are read."""
+    n = min(len(p) for p in parts)
+    out = parts[0][:n].copy()
+    for p in parts[1:]:
+        p = p[:n]
+        for f in _SUMS:
+            out[f] = out[f] + p[f]
+        out["min_rho"] = np.where(p["min_rho"] < out["min_rho"], p["min_rho"], out["min_rho"])
+        out["min_p"] = np.where(p["min_p"] < out["min_p"], p["min_p"], out["min_p"])
+        out["max_rho"] = np.where(out["max_rho"] < p["max_rho"], p["max_rho"], out["max_rho"])
+        out["max_p"] = np.where(out["max_p"] < p["max_p"], p["max_p"], out["max_p"])
+    return out
 
 
 def combine(scal: Sequence[Sequence[int]]) -> Tuple[int, int, int]:
