@@ -239,6 +239,29 @@ int h2d_totals(h2d_ctx* ctx, double out[6]);
  * (harness.cpp:385); sums in the reference's serial order. */
 int h2d_step_diag_now(h2d_ctx* ctx, double dt, h2d_step_diag* out);
 
+/* ---- field readback formats and checkpoints ------- */
+/* DumpFormat, io.hpp:9 */
+enum { H2D_DUMP_CSV = 0, H2D_DUMP_VTK = 1 };
+
+/* void write_fields(const State&, const std::string& path, DumpFormat)
+ * (io.hpp:17, io.cpp:72-83): CSV or legacy-VTK cell dump of the context's
+ * resident State, byte-identical to the reference's; H2D_ERR_SIM when the
+ * file cannot be written (the reference's SimError). Single-domain contexts. */
+int h2d_write_fields(h2d_ctx* ctx, const char* path, int fmt);
+/* The same formatter on a host State view (no device needed). */
+int h2d_write_fields_host(const h2d_config* cfg, const h2d_state* s, const char* path, int fmt);
+/* void append_diag_line(std::ostream&, step, t, dt, Totals, extrema)
+ * (io.hpp:21-22, io.cpp:85-92) of one StepDiag into buf (NUL-terminated). */
+int h2d_diag_line(const h2d_step_diag* d, char* buf, int cap);
+/* Binary checkpoint of the persistent State (no reference counterpart):
+ * header (mesh, material count, step, time) + every Field in the reference
+ * layout; a load into a context of another mesh returns H2D_ERR_INVALID.
+ * Restarting from a checkpoint continues bit-exactly. */
+int h2d_save_state(h2d_ctx* ctx, const char* path);
+int h2d_load_state(h2d_ctx* ctx, const char* path);
+int h2d_save_state_host(const h2d_config* cfg, const h2d_state* s, const char* path);
+int h2d_load_state_host(const h2d_config* cfg, h2d_state* s, const char* path);
+
 /* ---- 2D block decomposition (no reference counterpart) ----
  * A block context owns [oi, oi+bnx) x [oj, oj+bny) of the global mesh plus a
  * halo (>= 8 cells). One run-loop step computes the whole step on the window

@@ -25,6 +25,7 @@
 
 #include <array>
 #include <cmath>
+#include <iosfwd>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -234,6 +235,14 @@ struct StepDiag {
     double min_p = 0.0, max_p = 0.0;
 };
 
+// ---- io.hpp (io.hpp:9-22): the reference's CSV / legacy-VTK cell dump and
+// the conservation-ledger line, byte-identical output
+enum class DumpFormat { Csv, VtkLegacyAscii };
+void write_fields(const State& s, const std::string& path, DumpFormat fmt);
+void write_fields(const State& s, std::ostream& out, DumpFormat fmt);
+void append_diag_line(std::ostream& out, int step, double t, double dt, const Totals& totals, double min_rho,
+                      double max_rho, double min_p, double max_p);
+
 namespace b200 {
 
 struct StepInfo {
@@ -262,6 +271,11 @@ public:
     StepInfo run(int max_steps, double t_end, double cfl, RemapDiag* diag = nullptr);
     // make_diag(s, dt) of the resident State (harness.cpp:360-376), e.g. series[0]
     StepDiag diag_now(double dt = 0.0) const;
+    // write_fields of the resident State (io.hpp:17) without a State copy in the caller
+    void write_fields(const std::string& path, DumpFormat fmt) const;
+    // binary checkpoint of the resident State; load() resumes bit-exactly
+    void save(const std::string& path) const;
+    void load(const std::string& path);
 
 private:
     void* ctx_ = nullptr;

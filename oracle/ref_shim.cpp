@@ -9,6 +9,7 @@
 #include "../include/h2d.h"
 
 #include "hydro/harness.hpp"
+#include "hydro/io.hpp"
 #include "hydro/lagrange.hpp"
 #include "hydro/remap.hpp"
 #include "hydro/state.hpp"
@@ -18,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <sstream>
 #include <string>
 
 using namespace hydro;
@@ -325,6 +327,29 @@ int h2dr_run(h2dr_ctx* c, h2d_run_args* a) {
 
 int h2dr_step_diag_now(h2dr_ctx* c, double dt, h2d_step_diag* out) {
     *out = ref_make_diag(c->s, dt);
+    return 0;
+}
+
+// write_fields (io.hpp:17) of the context's State with the reference writer
+int h2dr_write_fields(h2dr_ctx* c, const char* path, int fmt) {
+    return guarded(c, -1, 0, [&] {
+        write_fields(c->s, std::string(path), fmt == H2D_DUMP_CSV ? DumpFormat::Csv : DumpFormat::VtkLegacyAscii);
+    });
+}
+
+// append_diag_line (io.hpp:21-22) of one record
+int h2dr_diag_line(const h2d_step_diag* d, char* buf, int cap) {
+    std::ostringstream o;
+    Totals t;
+    t.mass = d->mass;
+    t.mass_mat[0] = d->mass_mat[0];
+    t.mass_mat[1] = d->mass_mat[1];
+    t.momentum = Vec2{d->momentum_x, d->momentum_y};
+    t.internal_energy = d->internal_energy;
+    append_diag_line(o, d->step, d->t, d->dt, t, d->min_rho, d->max_rho, d->min_p, d->max_p);
+    const std::string s = o.str();
+    if ((int)s.size() + 1 > cap) return H2D_ERR_INVALID;
+    std::memcpy(buf, s.c_str(), s.size() + 1);
     return 0;
 }
 

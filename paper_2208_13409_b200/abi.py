@@ -26,6 +26,7 @@ BC_PERIODIC, BC_WALL = 0, 1
 EOS_PERFECT, EOS_STIFFENED = 0, 1
 CORNER_UPWIND, CORNER_AVGMIN, CORNER_LINEARXY, CORNER_LINEARDIAG, CORNER_MULTID = range(5)
 REMAP_AD, REMAP_DIRECT, REMAP_DIRECTCF = range(3)
+DUMP_CSV, DUMP_VTK = 0, 1  # DumpFormat, io.hpp:9
 
 _dp = C.POINTER(C.c_double)
 
@@ -230,8 +231,16 @@ _SIGS = {
     "step_diag_now": ([C.c_void_p, C.c_double, C.POINTER(StepDiag)], C.c_int),
     "last_error": ([C.c_void_p, C.POINTER(ErrorRec)], C.c_int),
 }
-# product-only extras (benchmark support)
+# product-only extras (benchmark support) and the field / checkpoint I/O
+# (the reference shim exports write_fields and diag_line)
 _EXTRA = {
+    "write_fields": ([C.c_void_p, C.c_char_p, C.c_int], C.c_int),
+    "write_fields_host": ([C.POINTER(Config), C.POINTER(StateView), C.c_char_p, C.c_int], C.c_int),
+    "diag_line": ([C.POINTER(StepDiag), C.c_char_p, C.c_int], C.c_int),
+    "save_state": ([C.c_void_p, C.c_char_p], C.c_int),
+    "load_state": ([C.c_void_p, C.c_char_p], C.c_int),
+    "save_state_host": ([C.POINTER(Config), C.POINTER(StateView), C.c_char_p], C.c_int),
+    "load_state_host": ([C.POINTER(Config), C.POINTER(StateView), C.c_char_p], C.c_int),
     "launch_count": ([], C.c_longlong),
     "step_timed": ([C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_float)], C.c_int),
     "flush_l2": ([C.c_void_p, C.c_longlong], C.c_int),
@@ -379,6 +388,17 @@ class Solver:
     def flush_l2(self, nbytes: int = 512 << 20):
         self._check(self.lib.fn["flush_l2"](self._h, nbytes))
 
+    # -- I/O (io.hpp:17-22) and checkpoints -----------------------------------
+    def write_fields(self, path: str, fmt: int = DUMP_CSV):
+        """write_fields(s, path, fmt) of the resident State (io.cpp:72-83)."""
+        self._check(self.lib.fn["write_fields"](self._h, path.encode(), fmt))
+
+    def save_state(self, path: str):
+        self._check(self.lib.fn["save_state"](self._h, path.encode()))
+
+    def load_state(self, path: str):
+        self._check(self.lib.fn["load_state"](self._h, path.encode()))
+
     def step_diag(self, dt: float = 0.0) -> np.void:
         """make_diag(s, dt) of the current State (harness.cpp:360-376)."""
         out = np.zeros(1, STEP_DIAG_DTYPE)
@@ -389,3 +409,14 @@ class Solver:
         out = (C.c_double * 6)()
         self._check(self.lib.fn["totals"](self._h, out))
         return dict(mass=out[0], mass_mat=(out[1], out[2]), momentum=(out[3], out[4]), internal_energy=out[5])
+
+
+def diag_line(lib: Library, rec) -> str:
+    """append_diag_line (io.cpp:85-92) of one StepDiag record."""
+    r = np.zeros(1, STEP_DIAG_DTYPE)
+    r[0] = rec
+    buf = C.create_string_buffer(1024)
+    rc = lib.fn["diag_line"](r.ctypes.data_as(C.POINTER(StepDiag)), buf, len(buf))
+    if rc:
+        raise errors.from_code(rc, "diag_line failed")
+    return buf.value.decode()

@@ -1075,6 +1075,71 @@ int h2d_step_diag_now(h2d_ctx* c, double dt, h2d_step_diag* out) {
     return 0;
 }
 
+// host staging of the whole reference State of a single-domain context
+struct HostStage {
+    std::vector<double> buf;
+    h2d_state v{};
+    HostStage(int nx, int ny, int nmat) {
+        const size_t nc = (size_t)(nx + 2 * G) * (ny + 2 * G), nn = (size_t)(nx + 1 + 2 * G) * (ny + 1 + 2 * G);
+        buf.assign(nc * (3 * (size_t)nmat + 5 + 2) + 2 * nn, 0.0);
+        double* p = buf.data();
+        auto take = [&](size_t n) {
+            double* q = p;
+            p += n;
+            return q;
+        };
+        for (int a = 0; a < nmat; ++a) v.m[a] = take(nc);
+        for (int a = 0; a < nmat; ++a) v.e[a] = take(nc);
+        for (int a = 0; a < nmat; ++a) v.k[a] = take(nc);
+        v.vol = take(nc);
+        v.m_mix = take(nc);
+        v.e_mix = take(nc);
+        v.rho_mix = take(nc);
+        v.p_mix = take(nc);
+        v.iface_normal = take(2 * nc);
+        v.u = take(2 * nn);
+    }
+};
+
+int h2d_write_fields(h2d_ctx* c, const char* path, int fmt) {
+    if (c->is_block) {
+        set_err(c, H2D_ERR_INVALID, "write_fields: single-domain contexts only");
+        return H2D_ERR_INVALID;
+    }
+    HostStage h(c->nx, c->ny, c->nmat);
+    if (int rc = h2d_download_state(c, &h.v)) return rc;
+    const int rc = h2d_write_fields_host(&c->cfg, &h.v, path, fmt);
+    if (rc == H2D_ERR_SIM) set_err(c, rc, (std::string("cannot write: ") + (path ? path : "")).c_str());
+    if (rc == H2D_ERR_INVALID) set_err(c, rc, "write_fields: bad format or path");
+    return rc;
+}
+
+int h2d_save_state(h2d_ctx* c, const char* path) {
+    if (c->is_block) {
+        set_err(c, H2D_ERR_INVALID, "save_state: single-domain contexts only");
+        return H2D_ERR_INVALID;
+    }
+    HostStage h(c->nx, c->ny, c->nmat);
+    if (int rc = h2d_download_state(c, &h.v)) return rc;
+    const int rc = h2d_save_state_host(&c->cfg, &h.v, path);
+    if (rc) set_err(c, rc, (std::string("cannot write checkpoint: ") + (path ? path : "")).c_str());
+    return rc;
+}
+
+int h2d_load_state(h2d_ctx* c, const char* path) {
+    if (c->is_block) {
+        set_err(c, H2D_ERR_INVALID, "load_state: single-domain contexts only");
+        return H2D_ERR_INVALID;
+    }
+    HostStage h(c->nx, c->ny, c->nmat);
+    const int rc = h2d_load_state_host(&c->cfg, &h.v, path);
+    if (rc) {
+        set_err(c, rc, (std::string("cannot read a checkpoint of this mesh: ") + (path ? path : "")).c_str());
+        return rc;
+    }
+    return h2d_upload_state(c, &h.v);
+}
+
 int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_kind, float ms[8]) {
     cudaSetDevice(c->device);
     const bool ad = remap_kind == H2D_REMAP_AD;

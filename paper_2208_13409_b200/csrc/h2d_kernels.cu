@@ -197,17 +197,20 @@ __device__ __forceinline__ bool ghost_cell_pos(int t, int nx, int ny, int& i, in
     return false;
 }
 
-__device__ __forceinline__ void ghost_cells_at(const Dev& d, const FieldList& fl, int t) {
+// (one field f per call: the launch spreads the fields over blockIdx.z, so
+// every thread does one independent load / store instead of a chain)
+__device__ __forceinline__ void ghost_cells_at(const Dev& d, const FieldList& fl, int t, int f) {
     int i, j;
     if (!ghost_cell_pos(t, d.nx, d.ny, i, j)) return;
     if (!in(d.win_c, i, j)) return;
     const int is = wrap_cell(i, d.nx, d.per_x), js = wrap_cell(j, d.ny, d.per_y);
-    const int dst = ix(d, i, j), src = ix(d, is, js);
-    for (int f = 0; f < fl.n; ++f) fl.f[f][dst] = fl.f[f][src];
+    double* p = fl.f[f];
+    p[ix(d, i, j)] = p[ix(d, is, js)];
 }
 
 // fill_ghost_nodes (state.cpp:87-108) for Vec2 pairs (x, y).
-__device__ __forceinline__ void ghost_nodes_at(const Dev& d, const FieldList& fl, int t) {
+// (one Vec2 pair (fl.f[f0], fl.f[f0 + 1]) per call, f0 even)
+__device__ __forceinline__ void ghost_nodes_at(const Dev& d, const FieldList& fl, int t, int f0) {
     const int nx = d.nx, ny = d.ny;
     const int W = nx + 1 + 2 * G;
     int i, j;
@@ -227,16 +230,14 @@ __device__ __forceinline__ void ghost_nodes_at(const Dev& d, const FieldList& fl
             if (t < 2 * (ny + 1)) {
                 j = t % (ny + 1);
                 i = t < ny + 1 ? 0 : nx;
-                if (!d.per_x && in(d.win_n, i, j))
-                    for (int f = 0; f < fl.n; f += 2) fl.f[f][ix(d, i, j)] = 0.0;
+                if (!d.per_x && in(d.win_n, i, j)) fl.f[f0][ix(d, i, j)] = 0.0;
                 return;
             }
             t -= 2 * (ny + 1);
             if (t < 2 * (nx + 1)) {
                 i = t % (nx + 1);
                 j = t < nx + 1 ? 0 : ny;
-                if (!d.per_y && in(d.win_n, i, j))
-                    for (int f = 1; f < fl.n; f += 2) fl.f[f][ix(d, i, j)] = 0.0;
+                if (!d.per_y && in(d.win_n, i, j)) fl.f[f0 + 1][ix(d, i, j)] = 0.0;
             }
             return;
         }
@@ -273,14 +274,12 @@ __device__ __forceinline__ void ghost_nodes_at(const Dev& d, const FieldList& fl
     const bool zx = !d.per_x && (si == 0 || si == nx);
     const bool zy = !d.per_y && (sj == 0 || sj == ny);
     const int dst = ix(d, i, j), src = ix(d, si, sj);
-    for (int f = 0; f < fl.n; f += 2) {
-        double vx = zx ? 0.0 : fl.f[f][src];
-        double vy = zy ? 0.0 : fl.f[f + 1][src];
-        if (fi) vx = -vx;
-        if (fj) vy = -vy;
-        fl.f[f][dst] = vx;
-        fl.f[f + 1][dst] = vy;
-    }
+    double vx = zx ? 0.0 : fl.f[f0][src];
+    double vy = zy ? 0.0 : fl.f[f0 + 1][src];
+    if (fi) vx = -vx;
+    if (fj) vy = -vy;
+    fl.f[f0][dst] = vx;
+    fl.f[f0 + 1][dst] = vy;
 }
 
 // sync_derived, state.cpp:120-143, over every cell including ghosts.
@@ -1074,12 +1073,12 @@ __device__ __forceinline__ void flux_ghosts_at(const Dev& d, int t) {
 __global__ void k_ghost_multi(Dev d, FieldList cells, FieldList nodes, int flux, int respect_halt) {
     pdl_enter();
     if (respect_halt && halted(d.ctl)) return;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, f = blockIdx.z;
     if (blockIdx.y == 0) {
-        if (cells.n) ghost_cells_at(d, cells, t);
+        if (f < cells.n) ghost_cells_at(d, cells, t, f);
     } else if (blockIdx.y == 1) {
-        if (nodes.n) ghost_nodes_at(d, nodes, t);
-    } else if (flux) {
+        if (2 * f < nodes.n) ghost_nodes_at(d, nodes, t, 2 * f);
+    } else if (flux && f == 0) {
         flux_ghosts_at(d, t);
     }
 }
@@ -2960,7 +2959,9 @@ static long long ghost_threads(const Dev& d) {
 }
 void launch_ghost_multi(const Dev& d, const FieldList& cells, const FieldList& nodes, int flux, int respect_halt,
                         cudaStream_t s) {
-    const dim3 g(nblk(ghost_threads(d), 256), 3);
+    int nz = cells.n > (nodes.n + 1) / 2 ? cells.n : (nodes.n + 1) / 2;
+    if (nz < 1) nz = 1;
+    const dim3 g(nblk(ghost_threads(d), 256), flux ? 3 : 2, nz);
     pdl(k_ghost_multi, g, dim3(256), 0, s, d, cells, nodes, flux, respect_halt);
 }
 void launch_ghost_cells(const Dev& d, const FieldList& fl, cudaStream_t s) {

@@ -8,9 +8,11 @@
 // reference's pure helpers make_state / nodal_mass / compute_totals.
 #include "../../include/h2d.h"
 #include "../../include/hydro/b200.hpp"
+#include "h2d_io.h"
 
 #include <cstring>
 #include <memory>
+#include <ostream>
 
 namespace hydro {
 namespace {
@@ -296,6 +298,40 @@ State remap_step(const State& s, const MaterialSet& mats, const LagrangeResult& 
     return out;
 }
 
+// ---- io.hpp --------------------------------------------------------------------------
+void write_fields(const State& s, std::ostream& out, DumpFormat fmt) {
+    const h2d_config cfg = make_cfg(s.mesh, s.nmat, nullptr, {}, {});
+    std::string text;
+    h2d_io::format_fields(cfg, view(s), fmt == DumpFormat::Csv ? H2D_DUMP_CSV : H2D_DUMP_VTK, text);
+    out << text;
+}
+
+void write_fields(const State& s, const std::string& path, DumpFormat fmt) {
+    const h2d_config cfg = make_cfg(s.mesh, s.nmat, nullptr, {}, {});
+    const h2d_state v = view(s);
+    if (h2d_write_fields_host(&cfg, &v, path.c_str(), fmt == DumpFormat::Csv ? H2D_DUMP_CSV : H2D_DUMP_VTK))
+        throw SimError("cannot write: " + path);
+}
+
+void append_diag_line(std::ostream& out, int step, double t, double dt, const Totals& totals, double min_rho,
+                      double max_rho, double min_p, double max_p) {
+    h2d_step_diag d{};
+    d.step = step;
+    d.t = t;
+    d.dt = dt;
+    d.mass = totals.mass;
+    d.mass_mat[0] = totals.mass_mat[0];
+    d.mass_mat[1] = totals.mass_mat[1];
+    d.momentum_x = totals.momentum.x;
+    d.momentum_y = totals.momentum.y;
+    d.internal_energy = totals.internal_energy;
+    d.min_rho = min_rho;
+    d.max_rho = max_rho;
+    d.min_p = min_p;
+    d.max_p = max_p;
+    out << h2d_io::diag_line(d);
+}
+
 // ---- device-resident run loop ------------------------------------------------------
 namespace b200 {
 
@@ -348,6 +384,21 @@ StepDiag Simulation::diag_now(double dt) const {
     h2d_step_diag d;
     check(h, h2d_step_diag_now(h, dt, &d));
     return from_c(d);
+}
+
+void Simulation::write_fields(const std::string& path, DumpFormat fmt) const {
+    h2d_ctx* h = static_cast<h2d_ctx*>(ctx_);
+    check(h, h2d_write_fields(h, path.c_str(), fmt == DumpFormat::Csv ? H2D_DUMP_CSV : H2D_DUMP_VTK));
+}
+
+void Simulation::save(const std::string& path) const {
+    h2d_ctx* h = static_cast<h2d_ctx*>(ctx_);
+    check(h, h2d_save_state(h, path.c_str()));
+}
+
+void Simulation::load(const std::string& path) {
+    h2d_ctx* h = static_cast<h2d_ctx*>(ctx_);
+    check(h, h2d_load_state(h, path.c_str()));
 }
 
 StepInfo Simulation::run(int max_steps, double t_end, double cfl, RemapDiag* diag) {

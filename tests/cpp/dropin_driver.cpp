@@ -9,10 +9,12 @@
 #include "hydro/remap.hpp"
 #include "hydro/state.hpp"
 #include "hydro/harness.hpp"
+#include "hydro/io.hpp"
 
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <sstream>
 #include <string>
 #include <typeinfo>
 #include <vector>
@@ -85,6 +87,14 @@ static void run_loop(State s, const MaterialSet& mats, double cfl, int steps, co
     put_d(t.internal_energy);
     put_d(t.momentum.x);
     put_d(t.momentum.y);
+    // io.hpp: the cell dumps and the ledger line of the final State
+    std::ostringstream csv, vtk, line;
+    write_fields(s, csv, DumpFormat::Csv);
+    write_fields(s, vtk, DumpFormat::VtkLegacyAscii);
+    append_diag_line(line, s.step, s.time, 0.5, t, 0.25, 4.0, 0.1, 9.0);
+    put_s(csv.str().c_str());
+    put_s(vtk.str().c_str());
+    put_s(line.str().c_str());
 }
 
 int main(int argc, char** argv) {
