@@ -10,6 +10,7 @@
 
 #include "hydro/harness.hpp"
 #include "hydro/io.hpp"
+#include "hydro/config.hpp"
 #include "hydro/lagrange.hpp"
 #include "hydro/remap.hpp"
 #include "hydro/state.hpp"
@@ -455,3 +456,74 @@ double h2dr_corner_value(int scheme, const double* a, const double* xl, const do
 }
 
 } // extern "C"
+
+// RunReport run(configure_case(RunConfig)) (harness.cpp:380-424, config.cpp:95-106),
+// the path of the pybind11 run_case (module.cpp:50-93): the series, final
+// State and report scalars {time, l2_rho, l2_k, max_k_violation, k_clip,
+// mass_fix, energy_floor}; returns the error kind (message in err_what).
+extern "C" int h2dr_run_case(const char* name, int divisor, int scheme, int face_order, int corner, double cfl,
+                             double t_end, int max_steps, h2d_step_diag* series, int cap, int* n_series,
+                             double out[8], int* steps, h2d_state* final_state, char* err_what, int err_cap) {
+    h2dr_ctx c;
+    *n_series = 0;
+    int nser = 0;
+    const int rc = guarded(&c, -1, 0, [&] {
+        RunConfig r;
+        r.case_name = name;
+        r.divisor = divisor;
+        r.scheme = static_cast<RemapKind>(scheme);
+        r.face_order = face_order;
+        r.corner = static_cast<CornerScheme>(corner);
+        r.cfl = cfl;
+        r.t_end = t_end;
+        r.max_steps = max_steps;
+        const CaseSpec cs = configure_case(r);
+        const RunReport rep = run(cs);
+        for (const StepDiag& d : rep.series) {
+            if (nser >= cap) break;
+            h2d_step_diag& o = series[nser++];
+            o = h2d_step_diag{};
+            o.step = d.step;
+            o.t = d.t;
+            o.dt = d.dt;
+            o.mass = d.totals.mass;
+            o.mass_mat[0] = d.totals.mass_mat[0];
+            o.mass_mat[1] = d.totals.mass_mat[1];
+            o.momentum_x = d.totals.momentum.x;
+            o.momentum_y = d.totals.momentum.y;
+            o.internal_energy = d.totals.internal_energy;
+            o.min_rho = d.min_rho;
+            o.max_rho = d.max_rho;
+            o.min_p = d.min_p;
+            o.max_p = d.max_p;
+        }
+        out[0] = rep.final_state.time;
+        out[1] = rep.l2_rho_vs_initial;
+        out[2] = rep.l2_k_vs_initial;
+        out[3] = rep.max_k_violation;
+        out[4] = rep.k_clip_count;
+        out[5] = rep.mass_fix_count;
+        out[6] = rep.energy_floor_count;
+        *steps = rep.steps;
+        if (final_state) {
+            const State& s = rep.final_state;
+            for (int a = 0; a < s.nmat; ++a) {
+                get(s.m[a], final_state->m[a]);
+                get(s.e[a], final_state->e[a]);
+                get(s.k[a], final_state->k[a]);
+            }
+            get(s.vol, final_state->vol);
+            get(s.m_mix, final_state->m_mix);
+            get(s.e_mix, final_state->e_mix);
+            get(s.rho_mix, final_state->rho_mix);
+            get(s.p_mix, final_state->p_mix);
+            get(s.iface_normal, final_state->iface_normal);
+            get(s.u, final_state->u);
+            final_state->step = s.step;
+            final_state->time = s.time;
+        }
+    });
+    *n_series = nser;
+    if (rc && err_what) std::snprintf(err_what, err_cap, "%s", c.err.what);
+    return rc;
+}
