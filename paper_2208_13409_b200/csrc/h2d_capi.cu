@@ -353,7 +353,15 @@ int fill_ghosts_cur(h2d_ctx* c, int parity) {
 }
 
 // One run-loop step (harness.cpp:390-412) for the state in `parity`.
-void enqueue_step(h2d_ctx* c, int parity) { launch_step(make_dev(c, parity, 1), c->st); }
+// (single domain: the step's start is the previous step's k_tail, and the
+// first step of a call gets a standalone k_step_start, start_first below)
+void enqueue_step(h2d_ctx* c, int parity) { launch_step(make_dev(c, parity, 1), !c->is_block, c->st); }
+
+// the start of the first run-loop step of a call (later starts are fused
+// into the previous step's k_tail on a single domain)
+void start_first(h2d_ctx* c) {
+    if (!c->is_block) launch_step_start(make_dev(c, c->cur, 1), c->st);
+}
 
 // cfl_dt of the current State into the control block's "next" slots, which
 // the first k_step_start of a run consumes (later steps get them from k_post)
@@ -425,7 +433,7 @@ int ensure_graphs_ad(h2d_ctx* c) {
             cudaGraph_t g = nullptr;
             const long long before = launch_count();
             CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
-            launch_step_ad(make_dev(c, p, 1), c->adw, xf, c->st);
+            launch_step_ad(make_dev(c, p, 1), c->adw, xf, 1, c->st);
             CK(cudaStreamEndCapture(c->st, &g));
             c->graph_kernels_ad = launch_count() - before;
             add_launches(-c->graph_kernels_ad);
@@ -956,6 +964,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
     int rc = 0;
     if ((rc = ad ? ensure_graphs_ad(c) : ensure_graphs(c))) return rc;
     enqueue_cfl_next(c);
+    start_first(c);
     // Launch in chunks; the device control block turns every kernel after the
     // loop condition fails (or after an error) into a no-op.
     for (;;) {
@@ -1191,8 +1200,7 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_k
             launch_post(d, 1, c->st);
         }
         CK(cudaEventRecord(c->ev[7], c->st));
-        launch_post_ghosts(d, c->st);
-        launch_commit_finish(d, c->st);
+        launch_tail(d, 0, c->st);
         CK(cudaEventRecord(c->ev[8], c->st));
         if (int rc = check_launch(c)) return rc;
         CK(cudaEventSynchronize(c->ev[8]));
@@ -1208,6 +1216,7 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_k
         CK(cudaEventElapsedTime(&ms[6], c->ev[0], c->ev[8]));
     } else {  // the production path: one graph launch
         if (int rc = ensure_graphs(c)) return rc;
+        start_first(c);  // (the graph's own k_tail starts the step after it)
         CK(cudaEventRecord(c->ev[0], c->st));
         if (ad) {
             CK(cudaGraphLaunch(c->graph_ad[c->cur][xf], c->st));

@@ -2021,53 +2021,6 @@ __device__ __forceinline__ void node_momentum(const Dev& d, double px, double py
     warp_partial<2>(v, op, d.dsc.part[1]);
 }
 
-// The step's make_diag values (harness.cpp:360-376) from the block partials
-// of k_post (n0 blocks) and the node update (n1 blocks): block b folds the
-// b-th slice of each in index order, the last block to finish folds the
-// slices into Ctl::dg. Halted steps leave dg alone (no record is logged).
-__global__ void __launch_bounds__(256) k_diag_reduce(Ctl* ctl, DiagScratch r, int n0, int n1) {
-    pdl_enter();
-    __shared__ int s_last;
-    if (threadIdx.x == 0) s_last = halted(ctl);
-    __syncthreads();
-    if (s_last) return;
-    const int op[DG_N] = {0, 0, 0, 0, 1, 2, 1, 2, 0, 0};
-    double v[DG_N];
-#pragma unroll
-    for (int k = 0; k < DG_N; ++k) v[k] = dg_ident(op[k]);
-    const int t = threadIdx.x, b = blockIdx.x, G = gridDim.x;
-    const long long lo0 = (long long)n0 * b / G, hi0 = (long long)n0 * (b + 1) / G;
-    const long long lo1 = (long long)n1 * b / G, hi1 = (long long)n1 * (b + 1) / G;
-    for (long long q = lo0 + t; q < hi0; q += blockDim.x)
-#pragma unroll
-        for (int k = 0; k < DG_NCELL; ++k) v[k] = dg_comb(op[k], v[k], r.part[0][q * DG_NCELL + k]);
-    for (long long q = lo1 + t; q < hi1; q += blockDim.x) {
-        v[DG_PX] += r.part[1][q * 2];
-        v[DG_PY] += r.part[1][q * 2 + 1];
-    }
-    __shared__ double sh[8 * DG_N];
-    block_combine<DG_N>(v, op, sh);
-    if (t == 0) {
-#pragma unroll
-        for (int k = 0; k < DG_N; ++k) r.lvl2[b * DG_N + k] = v[k];
-        __threadfence();
-        s_last = atomicAdd(r.tick, 1u) == (unsigned)G - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-#pragma unroll
-    for (int k = 0; k < DG_N; ++k) v[k] = dg_ident(op[k]);
-    for (int q = t; q < G; q += blockDim.x)
-#pragma unroll
-        for (int k = 0; k < DG_N; ++k) v[k] = dg_comb(op[k], v[k], __ldcg(&r.lvl2[q * DG_N + k]));
-    block_combine<DG_N>(v, op, sh);
-    if (t == 0) {
-#pragma unroll
-        for (int k = 0; k < DG_N; ++k) ctl->dg[k] = v[k];
-        *r.tick = 0u;
-    }
-}
-
 __global__ void k_node_update_walls(Dev d) {
     pdl_enter();
     if (halted(d.ctl)) return;  // one load per warp: warp-uniform
@@ -2246,8 +2199,7 @@ __global__ void k_commit(Ctl* c, int advance) {
 // Start of a run-loop step (harness.cpp:390-395): loop condition, then the
 // cfl_dt of the current State, whose wave-speed maximum and first error were
 // produced by the previous step's k_post (or k_cfl before the first step).
-__global__ void k_step_start(Ctl* c, double dx, double dy) {
-    pdl_enter();
+__device__ __forceinline__ void step_start_body(Ctl* c, double dx, double dy) {
     if (c->err_key != kNoErr || c->done) return;
     c->kviol_bits = 0ull;
     c->step_floor = 0;
@@ -2273,12 +2225,15 @@ __global__ void k_step_start(Ctl* c, double dx, double dy) {
     c->next_wmax_bits = 0ull;
     c->next_err_key = kNoErr;
 }
+__global__ void k_step_start(Ctl* c, double dx, double dy) {
+    pdl_enter();
+    step_start_body(c, dx, dy);
+}
 
 // End of a run-loop step: the remapped State becomes current
 // (remap.cpp:1084-1085) unless an earlier phase failed; nan_scan errors come
 // after the commit (harness.cpp:402-409), so they still commit.
-__global__ void k_commit_finish(Ctl* c) {
-    pdl_enter();
+__device__ __forceinline__ void commit_finish_body(Ctl* c) {
     c->committed = 0;
     c->counted = 0;
     if (c->done) return;
@@ -2307,6 +2262,10 @@ __global__ void k_commit_finish(Ctl* c) {
     const double v = __longlong_as_double((long long)c->kviol_bits);
     if (v > c->max_k_violation) c->max_k_violation = v;
     c->counted = 1;
+}
+__global__ void k_commit_finish(Ctl* c) {
+    pdl_enter();
+    commit_finish_body(c);
 }
 
 // Undo the last commit (block mode: another block failed in the same step
@@ -2762,6 +2721,82 @@ __global__ void __launch_bounds__(RTX * RTY, 3) k_ad_tile(Dev d, AdIO w) {
     finalize_cell<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va, PH_AD_NEGMASS + pb);
 }
 
+// Run-loop step epilogue in ONE launch (it used to be three: the ghost
+// layers of the new normals and u, the diagnostics fold, the commit): the
+// first nghost blocks fill the ghost layers (assemble_state's fill_ghosts,
+// remap.cpp:1084-1088), the next kDiagBlocks fold slices of the diagnostics
+// partials (as k_diag_reduce), and the last block to finish folds the slices,
+// commits the step (k_commit_finish) and, for a single domain, starts the
+// next one (k_step_start: loop condition and dt from the wave speed k_post
+// produced), so the next step's graph needs no head kernel.
+__global__ void __launch_bounds__(256) k_tail(Dev d, FieldList cells, FieldList nodes, int nb1, int n0, int n1,
+                                              int start_next) {
+    pdl_enter();
+    __shared__ int s_flag;
+    __shared__ double sh[8 * DG_N];
+    const int t = threadIdx.x;
+    if (t == 0) s_flag = halted(d.ctl);
+    __syncthreads();
+    const bool halt = s_flag;
+    const int b = blockIdx.x, ncomb = cells.n + nodes.n / 2;
+    const int op[DG_N] = {0, 0, 0, 0, 1, 2, 1, 2, 0, 0};
+    const DiagScratch& r = d.dsc;
+    if (b < nb1 * ncomb) {
+        if (!halt) {
+            const int comb = b / nb1, tt = (b % nb1) * 256 + t;
+            if (comb < cells.n)
+                ghost_cells_at(d, cells, tt, comb);
+            else
+                ghost_nodes_at(d, nodes, tt, 2 * (comb - cells.n));
+        }
+    } else if (d.diag) {
+        const int q = b - nb1 * ncomb, G = kDiagBlocks;
+        double v[DG_N];
+#pragma unroll
+        for (int k = 0; k < DG_N; ++k) v[k] = dg_ident(op[k]);
+        if (!halt) {
+            const long long lo0 = (long long)n0 * q / G, hi0 = (long long)n0 * (q + 1) / G;
+            const long long lo1 = (long long)n1 * q / G, hi1 = (long long)n1 * (q + 1) / G;
+            for (long long e = lo0 + t; e < hi0; e += blockDim.x)
+#pragma unroll
+                for (int k = 0; k < DG_NCELL; ++k) v[k] = dg_comb(op[k], v[k], r.part[0][e * DG_NCELL + k]);
+            for (long long e = lo1 + t; e < hi1; e += blockDim.x) {
+                v[DG_PX] += r.part[1][e * 2];
+                v[DG_PY] += r.part[1][e * 2 + 1];
+            }
+        }
+        block_combine<DG_N>(v, op, sh);
+        if (t == 0)
+#pragma unroll
+            for (int k = 0; k < DG_N; ++k) r.lvl2[q * DG_N + k] = v[k];
+    }
+    __syncthreads();
+    if (t == 0) {
+        __threadfence();
+        s_flag = atomicAdd(r.tick, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_flag) return;
+    if (d.diag && !halted(d.ctl)) {
+        double v[DG_N];
+#pragma unroll
+        for (int k = 0; k < DG_N; ++k) v[k] = dg_ident(op[k]);
+        for (int q = t; q < kDiagBlocks; q += blockDim.x)
+#pragma unroll
+            for (int k = 0; k < DG_N; ++k) v[k] = dg_comb(op[k], v[k], __ldcg(&r.lvl2[q * DG_N + k]));
+        block_combine<DG_N>(v, op, sh);
+        if (t == 0)
+#pragma unroll
+            for (int k = 0; k < DG_N; ++k) d.ctl->dg[k] = v[k];
+    }
+    if (t == 0) {
+        __threadfence();
+        *r.tick = 0u;
+        commit_finish_body(d.ctl);
+        if (start_next) step_start_body(d.ctl, d.dx, d.dy);
+    }
+}
+
 // AD dual faces of one pass (dual_face_pass along AX, remap.cpp:408-442); the
 // Dev's u_lag planes are the pass's Work velocities
 template <int AX>
@@ -3022,7 +3057,7 @@ void remap_init() {
 // the ghost layers of the new u and normals (assemble_state's fill_ghosts).
 void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s) {
     launch_post(d, run_loop, s);
-    launch_post_ghosts(d, s);
+    if (!run_loop) launch_post_ghosts(d, s);  // the run loop's k_tail fills them
 }
 
 void launch_post(const Dev& d, int run_loop, cudaStream_t s) {
@@ -3031,10 +3066,22 @@ void launch_post(const Dev& d, int run_loop, cudaStream_t s) {
         pdl(k_post<2>, gp, dim3(32, 8), 0, s, d, run_loop);
     else
         pdl(k_post<1>, gp, dim3(32, 8), 0, s, d, run_loop);
-    if (run_loop && d.diag) {
-        pdl(k_diag_reduce, dim3(kDiagBlocks), dim3(256), 0, s, d.ctl, d.dsc, (int)diag_partials(d, 0),
-            (int)diag_partials(d, 1));
-    }
+}
+
+// run-loop epilogue (k_tail): post ghosts + diagnostics fold + commit (+ next start)
+void launch_tail(const Dev& d, int start_next, cudaStream_t s) {
+    FieldList fg{};
+    fg.n = 2;
+    fg.f[0] = d.nnrx;
+    fg.f[1] = d.nnry;
+    FieldList fu{};
+    fu.n = 2;
+    fu.f[0] = d.nux;
+    fu.f[1] = d.nuy;
+    const int nb1 = (int)nblk(ghost_threads(d), 256);
+    const int nb = nb1 * 3 + (d.diag ? kDiagBlocks : 0);
+    pdl(k_tail, dim3(nb), dim3(256), 0, s, d, fg, fu, nb1, (int)diag_partials(d, 0), (int)diag_partials(d, 1),
+        start_next);
 }
 
 long long diag_partials(const Dev& d, int which) {  // block counts of k_post / the node grids
@@ -3140,15 +3187,19 @@ void launch_remap_dual(const Dev& d, cudaStream_t s) {
     }
 }
 
-void launch_step(const Dev& dd, cudaStream_t s) {
+// One run-loop step. fused_start: the step's start (loop condition, dt) was
+// done by the previous step's k_tail (single domain), and this step's k_tail
+// starts the next one; otherwise (blocks: the wave speed is combined across
+// blocks between steps) the step begins with k_step_start.
+void launch_step(const Dev& dd, int fused_start, cudaStream_t s) {
     Dev d = dd;
     d.scan_nodes = 1;
     d.diag = 1;
-    pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
+    if (!fused_start) pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
     launch_lagrange_run(d, s);
     launch_remap_core(d, s);
-    post_and_ghosts(d, 1, s);
-    pdl(k_commit_finish, dim3(1), dim3(1), 0, s, d.ctl);
+    launch_post(d, 1, s);
+    launch_tail(d, fused_start, s);
 }
 
 // One AD directional pass (remap.cpp:469-589) writing into dout's planes.
@@ -3243,14 +3294,14 @@ void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_veloc
     post_and_ghosts(dp, run_loop, s);
 }
 
-void launch_step_ad(const Dev& dd, const AdWork& W, int x_first, cudaStream_t s) {
+void launch_step_ad(const Dev& dd, const AdWork& W, int x_first, int fused_start, cudaStream_t s) {
     Dev d = dd;
     d.scan_nodes = 1;
     d.diag = 1;
-    pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
+    if (!fused_start) pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
     launch_lagrange_run(d, s);
     launch_remap_ad(d, W, x_first, 1, 1, s);
-    pdl(k_commit_finish, dim3(1), dim3(1), 0, s, d.ctl);
+    launch_tail(d, fused_start, s);
 }
 
 void launch_step_start(const Dev& d, cudaStream_t s) { k_step_start<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy); ++g_launches; }

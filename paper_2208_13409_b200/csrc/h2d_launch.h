@@ -46,17 +46,18 @@ void launch_lag_fused(const Dev& d, cudaStream_t s);
 void launch_lag_ghosts(const Dev& d, cudaStream_t s);
 void launch_post(const Dev& d, int run_loop, cudaStream_t s);
 long long diag_partials(const Dev& d, int which);
+void launch_tail(const Dev& d, int start_next, cudaStream_t s);  // run-loop epilogue
 void launch_post_ghosts(const Dev& d, cudaStream_t s);
 void launch_remap_tile(const Dev& d, cudaStream_t s);
 void launch_remap_slivers(const Dev& d, cudaStream_t s);
 void launch_remap_dual(const Dev& d, cudaStream_t s);
 void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s);
-void launch_step(const Dev& d, cudaStream_t s);  // one run-loop step
+void launch_step(const Dev& d, int fused_start, cudaStream_t s);  // one run-loop step
 // AD split remap: both directional passes of remap_step(AD) (remap.cpp:1110-1115)
 // leaving the next State's Work in `d`'s next-state planes, then the post
 // kernels (run_loop: also the NaN scan and the next wave speed)
 void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_velocity, int run_loop, cudaStream_t s);
-void launch_step_ad(const Dev& d, const AdWork& W, int x_first, cudaStream_t s);  // one AD run-loop step
+void launch_step_ad(const Dev& d, const AdWork& W, int x_first, int fused_start, cudaStream_t s);  // one AD run-loop step
 void launch_cfl_next(const Dev& d, cudaStream_t s);
 void launch_step_start(const Dev& d, cudaStream_t s);
 void launch_commit_finish(const Dev& d, cudaStream_t s);               // wave speed of the current State
