@@ -200,6 +200,12 @@ H2D_DEV double div_dy(const Dev& d, double x, double k) {
     return d.rdy != 0.0 ? x * (d.rdy * (1.0 / k)) : x / (k * d.dy);
 }
 H2D_DEV double div_cv(const Dev& d, double x) { return d.rcv != 0.0 ? x * d.rcv : x / d.cv; }
+// phase density m / (k * cv) (lagrange.cpp:54,115,180, state.cpp:133,
+// harness.cpp:301): a pure cell has k == 1 exactly, so k * cv == cv exactly
+// and the divide is div_cv's exact power-of-two multiply
+H2D_DEV double rho_of(const Dev& d, double m, double k) {
+    return (k == 1.0 && d.rcv != 0.0) ? m * d.rcv : m / (k * d.cv);
+}
 H2D_DEV double rmax(double a, double b) { return (a < b) ? b : a; }  // std::max
 H2D_DEV double rmin(double a, double b) { return (b < a) ? b : a; }  // std::min
 

@@ -114,7 +114,7 @@ __global__ void k_cfl(Dev d, int into_next) {
         for (int a = 0; a < NM; ++a) {
             const double ka = d.k[a][c];
             if (ka < kThermoTol) continue;
-            const double rho_a = d.m[a][c] / (ka * d.cv);
+            const double rho_a = rho_of(d, d.m[a][c], ka);
             const double pa = eos_p(d, a, rho_a, d.e[a][c]);
             cs += ka * sound(d, a, rho_a, pa, bad);
         }
@@ -303,7 +303,7 @@ __global__ void k_sync(Dev d, int next, int respect_halt) {
         m += ma;
         me += ma * ea;
         if (ka < kThermoTol) continue;
-        const double rho_a = ma / (ka * cv);
+        const double rho_a = rho_of(d, ma, ka);
         p += ka * eos_p(d, a, rho_a, ea);
     }
     double* om = next ? d.nm_mix : const_cast<double*>(d.m_mix);
@@ -375,7 +375,7 @@ __global__ void k_lag_cells(Dev d) {
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
             if (ka[a] < kThermoTol) continue;
-            const double rho_a = ma[a] / (ka[a] * d.cv);
+            const double rho_a = rho_of(d, ma[a], ka[a]);
             const double pa = eos_p(d, a, rho_a, en[a]);
             cs += ka[a] * sound(d, a, rho_a, pa, bad);
         }
@@ -396,7 +396,7 @@ __global__ void k_lag_cells(Dev d) {
     for (int a = 0; a < NM; ++a) {
         double pa_h = 0.0;
         if (!(ka[a] < kThermoTol)) {
-            const double rho_n = ma[a] / (ka[a] * cv);
+            const double rho_n = rho_of(d, ma[a], ka[a]);
             const double rho_h = ma[a] / (ka[a] * vol);
             const double pa_n = eos_p(d, a, rho_n, en[a]);
             double ea = en[a] - (pa_n + q) * (1.0 / rho_h - 1.0 / rho_n);
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
             if (ka > 0.0) ea = en;
         } else {
             const double ma = d.m[a][n];
-            const double rho_n = ma / (ka * cv);
+            const double rho_n = rho_of(d, ma, ka);
             const double rho_l = ma / (ka * vol);
             ea = en - (d.ph[a][n] + qn) * (1.0 / rho_l - 1.0 / rho_n);
             const double efloor = 1e-8 * fabs(en);
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
 #pragma unroll
                 for (int a = 0; a < NM; ++a) {
                     if (ka[a] < kThermoTol) continue;
-                    const double rho_a = ma[a] / (ka[a] * cv);
+                    const double rho_a = rho_of(d, ma[a], ka[a]);
                     const double pa = eos_p(d, a, rho_a, en[a]);
                     cs += ka[a] * sound(d, a, rho_a, pa, bad);
                 }
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
 #pragma unroll
             for (int a = 0; a < NM; ++a) {
                 if (!(ka[a] < kThermoTol)) {
-                    const double rho_n = ma[a] / (ka[a] * cv);
+                    const double rho_n = rho_of(d, ma[a], ka[a]);
                     const double pa_n = eos_p(d, a, rho_n, en[a]);
                     // vol == cv (a still or uniformly moving cell, lagrange.cpp:
                     // 34-35) gives rho_h == rho_n bit for bit, so 1/rho_h - 1/rho_n
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
             if (ka > 0.0) ea = en;
         } else {
             const double ma = d.m[a][n];
-            const double rho_n = ma / (ka * cv);
+            const double rho_n = rho_of(d, ma, ka);
             double dv = 0.0;  // vol == cv: rho_l == rho_n, the difference of inverses is +0
             if (!(vol == cv && fabs(rho_n) >= DBL_MIN)) {
                 const double rho_l = ma / (ka * vol);
@@ -2388,7 +2388,7 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
             m += ma[a];
             me += ma[a] * ea[a];
             if (ka[a] < kThermoTol) continue;
-            const double rho_a = ma[a] / (ka[a] * cv);
+            const double rho_a = rho_of(d, ma[a], ka[a]);
             p += ka[a] * eos_p(d, a, rho_a, ea[a]);
         }
         emix = m > 0.0 ? me / m : 0.0;
@@ -2441,7 +2441,7 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
 #pragma unroll
                 for (int a = 0; a < NM; ++a) {
                     if (ka[a] < kThermoTol) continue;
-                    const double rho_a = ma[a] / (ka[a] * cv);
+                    const double rho_a = rho_of(d, ma[a], ka[a]);
                     const double pa = eos_p(d, a, rho_a, ea[a]);
                     cs += ka[a] * sound(d, a, rho_a, pa, bad);
                 }
