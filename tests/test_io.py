@@ -129,3 +129,22 @@ def test_checkpoint_restart_is_bit_exact(gpu, tmp_path, which):
     assert (sa.step, sa.time) == (sb.step, sb.time)
     with pytest.raises(errors.SimError):
         b.write_fields("/nonexistent/dir/x.csv")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["sedov", "triple"])
+def test_upload_primary_fields_rebuilds_derived_bitwise(gpu, orc, which):
+    """h2d_upload_state with the derived pointers NULL (the e2e bench's
+    upload) rebuilds vol, m_mix, e_mix, rho_mix, p_mix exactly as the
+    reference State carries them (sync_derived, state.cpp:120-143)."""
+    case = {"sedov": cases.sedov(64), "triple": cases.triple_point(64, 32)}[which]
+    so = helpers.prepared(orc, case.cfg, case.paint())
+    so.run(8, cfl=case.cfl)
+    st = so.download()
+    a, b = abi.Solver(gpu, case.cfg), abi.Solver(gpu, case.cfg)
+    a.upload(st, derived=True)
+    b.upload(st, derived=False)
+    assert helpers.bitwise_diff(a.download(), b.download(), helpers.STATE_FIELDS) == []
+    ra, rb = a.run(14, cfl=case.cfl), b.run(14, cfl=case.cfl)
+    assert np.array_equal(ra.dts, rb.dts)
+    assert helpers.bitwise_diff(a.download(), b.download(), helpers.STATE_FIELDS) == []
