@@ -520,8 +520,13 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
 // chip; the API path (h2d_lagrange_step) keeps the two-kernel form because
 // it returns Q.
 template <int NM>
-__global__ void __launch_bounds__(LTX * LTY, 5) k_lag_fused(Dev d) {
+#ifndef H2D_FTY
+#define H2D_FTY 8
+#define H2D_FMINB 5
+#endif
+__global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     pdl_enter();
+    constexpr int LTY = H2D_FTY;
     constexpr int CW = LTX + 2, CH = LTY + 2, NC = CW * CH, NN = (LTX + 1) * (LTY + 1);
     __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC];
     __shared__ double shx[NN], shy[NN];
@@ -3115,9 +3120,9 @@ void launch_lagrange_run(const Dev& d, cudaStream_t s) {
 
 void launch_lag_fused(const Dev& d, cudaStream_t s) {
     if (d.nmat == 2)
-        pdl(k_lag_fused<2>, tiles_of(d.r_lagn, LTX, LTY), dim3(LTX * LTY), 0, s, d);
+        pdl(k_lag_fused<2>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(LTX * H2D_FTY), 0, s, d);
     else
-        pdl(k_lag_fused<1>, tiles_of(d.r_lagn, LTX, LTY), dim3(LTX * LTY), 0, s, d);
+        pdl(k_lag_fused<1>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(LTX * H2D_FTY), 0, s, d);
 }
 
 void launch_lag_ghosts(const Dev& d, cudaStream_t s) {
