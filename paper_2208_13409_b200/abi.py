@@ -19,6 +19,7 @@ import numpy as np
 from . import errors
 
 ABI_VERSION = 2  # H2D_ABI_VERSION
+RUN_LOG_CAP = 65536  # dt / StepDiag log entries of a run until t_end (h2d_run's device log)
 MAX_MAT = 2   # kMaxMat, state.hpp:13
 GHOST = 2     # kGhost, field.hpp:11
 
@@ -356,10 +357,11 @@ class Solver:
             kind: int = REMAP_DIRECTCF, series: bool = False) -> RunResult:
         a = RunArgs()
         a.max_steps, a.t_end, a.cfl, a.remap_kind = max_steps, t_end, cfl, kind
-        dts = np.zeros(max(max_steps, 1)) if log_dt else None
+        cap = max_steps if max_steps > 0 else RUN_LOG_CAP  # (max_steps is the absolute end step)
+        dts = np.zeros(max(cap, 1)) if log_dt else None
         if dts is not None:
             a.dt_log, a.dt_log_cap = _ptr(dts), len(dts)
-        ser = np.zeros(max(max_steps, 1) if max_steps > 0 else 4096, STEP_DIAG_DTYPE) if series else None
+        ser = np.zeros(max(cap, 1), STEP_DIAG_DTYPE) if series else None
         if ser is not None:
             a.series, a.series_cap = ser.ctypes.data_as(C.POINTER(StepDiag)), len(ser)
         rc = self.lib.fn["run"](self._h, C.byref(a))

@@ -66,6 +66,8 @@ struct h2d_ctx {
 
 namespace {
 
+constexpr int kRunLogCap = 65536;  // dt / StepDiag log entries of a run until t_end
+
 void set_err(h2d_ctx* c, int kind, const char* what, int i = -1, int j = -1, int step = -1, int in_step = 0) {
     c->err.kind = kind;
     c->err.i = i;
@@ -943,7 +945,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
         set_err(c, H2D_ERR_INVALID, "only the DirectCF and (single-domain) AD remaps are implemented on the device");
         return H2D_ERR_INVALID;
     }
-    const int cap = a->max_steps > 0 ? a->max_steps : 4096;
+    const int cap = a->max_steps > 0 ? a->max_steps : kRunLogCap;
     if (int rc = ensure_logs(c, cap)) return rc;
     if (int rc = ctl_reset(c)) return rc;
     Ctl& h = *c->hctl;
@@ -1400,7 +1402,7 @@ int h2d_block_begin(h2d_ctx* c, int max_steps, double t_end, double cfl) {
     h.steps_done = 0;
     h.floor_count = h.k_clip_count = h.mass_fix_count = 0;
     h.max_k_violation = 0.0;
-    const int cap = max_steps > 0 ? max_steps : 4096;
+    const int cap = max_steps > 0 ? max_steps : kRunLogCap;
     if (int rc = ensure_logs(c, cap)) return rc;
     h.dt_log = c->dt_log;
     h.dt_log_cap = c->dt_log_cap;

@@ -404,7 +404,7 @@ void Simulation::load(const std::string& path) {
 StepInfo Simulation::run(int max_steps, double t_end, double cfl, RemapDiag* diag) {
     h2d_ctx* h = static_cast<h2d_ctx*>(ctx_);
     StepInfo info;
-    info.dts.assign(max_steps > 0 ? max_steps : 4096, 0.0);
+    info.dts.assign(max_steps > 0 ? max_steps : 65536, 0.0);
     h2d_run_args a;
     std::memset(&a, 0, sizeof a);
     a.max_steps = max_steps;

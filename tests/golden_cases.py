@@ -9,9 +9,9 @@ from paper_2208_13409_b200.abi import BC_PERIODIC, BC_WALL, CORNER_LINEARDIAG, C
     EOS_STIFFENED, make_config
 
 
-def _run(steps, cfl):
+def _run(steps, cfl, t_end=1e30):
     def act(s):
-        r, err = helpers.run_capture(s, steps, cfl)
+        r, err = helpers.run_capture(s, steps, cfl, t_end=t_end)
         return {"dts": r.dts, "counters": [r.floor_count, r.diag["k_clip_count"], r.diag["mass_fix_count"],
                                            r.diag["max_k_violation"]]}, err
     return act
@@ -46,7 +46,7 @@ def _lagrange_remap(nsteps, cfl):
 
 GOLDEN = ["riemann2d_48", "sedov_64", "triple_point_64x32", "triple_point_32x16_abort", "shock_bubble_48",
           "kinematic_gas_periodic", "kinematic_blobs_wall_upwind_error", "kinematic_blobs_wall_upwind",
-          "lagrange_blobs_stiffened"]
+          "lagrange_blobs_stiffened", "impact_full_abort"]
 
 
 def build(name):
@@ -77,4 +77,12 @@ def build(name):
         cfg = make_config(24, 20, 0.5, 0.25, 0.0, 0.0, BC_WALL, BC_PERIODIC,
                           eos=[(EOS_PERFECT, 1.4, 0.0), (EOS_STIFFENED, 7.0, 0.5)], corner=CORNER_LINEARDIAG)
         return cfg, helpers.random_state(cfg, 103, "blobs", umax=0.05), _lagrange_remap(4, 0.4)
+    if name == "impact_full_abort":
+        # the reference's own robustness case at full size (acceptance.cpp
+        # criterion 7): impact / DirectCF aborts with
+        # UnphysicalStateError after ~3000 steps
+        from paper_2208_13409_b200 import frontend
+        cs = frontend.build_case(name.split("_")[0])
+        cfg = cs.config()
+        return cfg, cases.paint(cfg, cs.regions), _run(0, cs.cfl, cs.t_end)
     raise KeyError(name)

@@ -139,11 +139,11 @@ def prepared(lib: abi.Library, cfg: abi.Config, painted: HostState) -> Solver:
     return s
 
 
-def run_capture(s: Solver, steps: int, cfl: float, kind: int = abi.REMAP_DIRECTCF):
+def run_capture(s: Solver, steps: int, cfl: float, kind: int = abi.REMAP_DIRECTCF, t_end: float = 1e30):
     """Run and return (result, error-tuple-or-None)."""
     from paper_2208_13409_b200 import errors
     try:
-        r = s.run(steps, cfl=cfl, kind=kind)
+        r = s.run(steps, t_end=t_end, cfl=cfl, kind=kind)
         return r, None
     except errors.SimError as e:
         return e.partial, (type(e).__name__, e.what, e.i, e.j, e.step, e.in_step)
