@@ -34,8 +34,11 @@
 extern "C" {
 #endif
 
-#define H2D_ABI_VERSION 2
-#define H2D_MAX_MAT 2 /* reference kMaxMat, state.hpp:13 */
+#define H2D_ABI_VERSION 3
+/* materials per State: the reference's kMaxMat (state.hpp:13) is 2; the third
+ * slot is the N-material extension of configuration 5,
+ * no reference counterpart. Contexts with nmat <= 2 are the reference. */
+#define H2D_MAX_MAT 3
 #define H2D_GHOST 2   /* reference kGhost, field.hpp:11 */
 
 /* BoundaryKind, mesh.hpp:8 */

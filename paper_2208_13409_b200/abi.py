@@ -18,9 +18,9 @@ import numpy as np
 
 from . import errors
 
-ABI_VERSION = 2  # H2D_ABI_VERSION
+ABI_VERSION = 3  # H2D_ABI_VERSION
 RUN_LOG_CAP = 65536  # dt / StepDiag log entries of a run until t_end (h2d_run's device log)
-MAX_MAT = 2   # kMaxMat, state.hpp:13
+MAX_MAT = 3   # H2D_MAX_MAT: the reference's kMaxMat (state.hpp:13) is 2, slot 3 = config 5
 GHOST = 2     # kGhost, field.hpp:11
 
 BC_PERIODIC, BC_WALL = 0, 1

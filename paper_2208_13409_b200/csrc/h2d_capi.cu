@@ -23,7 +23,7 @@ using namespace h2d;
 namespace {
 
 struct StateBufs {
-    double *m[2], *e[2], *k[2], *vol, *m_mix, *e_mix, *rho_mix, *p_mix, *nrx, *nry, *ux, *uy;
+    double *m[kMatSlots], *e[kMatSlots], *k[kMatSlots], *vol, *m_mix, *e_mix, *rho_mix, *p_mix, *nrx, *nry, *ux, *uy;
 };
 
 }  // namespace
@@ -103,7 +103,7 @@ Dev make_dev(h2d_ctx* c, int parity, int remap_velocity) {
     Dev d = c->base;
     const StateBufs& s = c->sb[parity];
     const StateBufs& n = c->sb[1 - parity];
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < kMatSlots; ++a) {
         d.m[a] = s.m[a];
         d.e[a] = s.e[a];
         d.k[a] = s.k[a];
@@ -558,7 +558,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     const h2d_mesh& m = cfg->mesh;
     if (m.nx < 3 || m.ny < 3) return H2D_ERR_SIM;        // Mesh::Mesh, mesh.hpp:27
     if (m.dx <= 0.0 || m.dy <= 0.0) return H2D_ERR_SIM;  // mesh.hpp:28
-    if (cfg->nmat < 1 || cfg->nmat > H2D_MAX_MAT) return H2D_ERR_INVALID;
+    if (cfg->nmat < 1 || cfg->nmat > 2) return H2D_ERR_INVALID;  // (three materials: DESIGN.md 5b)
     if (cfg->corner != H2D_CORNER_UPWIND && cfg->corner != H2D_CORNER_LINEARDIAG) return H2D_ERR_INVALID;
     h2d_ctx* c = new h2d_ctx();
     c->cfg = *cfg;

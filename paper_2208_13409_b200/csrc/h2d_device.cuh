@@ -124,6 +124,9 @@ H2D_DEV bool halted(const Ctl* c) {
 H2D_DEV double step_dt(const Ctl* c) { return __ldg(&c->dt); }
 H2D_DEV void raise(Ctl* c, uint64_t key) { atomicMin(&c->err_key, (unsigned long long)key); }
 
+// per-material slots of the State (H2D_MAX_MAT): 1-2 = the reference, 3 = config 5
+constexpr int kMatSlots = 3;
+
 // Half-open range of GLOBAL indices [i0, i1) x [j0, j1).
 struct Rng {
     int i0, i1, j0, j1;
@@ -137,7 +140,7 @@ struct Rng {
 // reference Field layout.
 // TMA descriptors of the planes the remap tile stages (per State parity):
 // u_half x / y (node boxes), e_lag, m, k per material (cell boxes).
-enum { TM_UHX, TM_UHY, TM_EL0, TM_EL1, TM_M0, TM_M1, TM_K0, TM_K1, TM_N };
+enum { TM_UHX, TM_UHY, TM_EL0, TM_M0 = TM_EL0 + 3, TM_K0 = TM_M0 + 3, TM_N = TM_K0 + 3 };
 struct TmaSet {
     CUtensorMap t[TM_N];
 };
@@ -157,24 +160,24 @@ struct Dev {
     // LinearDiag unit diagonal (reconstruct.cpp:135,139,144): dx/diag, dy/diag
     // with diag = sqrt(dx*dx + dy*dy), loop invariant, computed once (same bits)
     double dgx, dgy;
-    int stiff[2];
-    double gamma[2], pi[2];
+    int stiff[kMatSlots];
+    double gamma[kMatSlots], pi[kMatSlots];
     double a1, a2;
     int face_order, corner_diag, degrade, remap_velocity;
 
     // current (read) State
-    const double *m[2], *e[2], *k[2], *m_mix, *e_mix, *rho_mix, *p_mix, *nrx, *nry, *ux, *uy;
+    const double *m[kMatSlots], *e[kMatSlots], *k[kMatSlots], *m_mix, *e_mix, *rho_mix, *p_mix, *nrx, *nry, *ux, *uy;
     double* vol;
     // next (written) State: also the remap's Work arrays (remap.cpp:88-98)
-    double *nm[2], *ne[2], *nk[2], *nvol, *nm_mix, *ne_mix, *nrho_mix, *np_mix, *nnrx, *nnry, *nux, *nuy;
+    double *nm[kMatSlots], *ne[kMatSlots], *nk[kMatSlots], *nvol, *nm_mix, *ne_mix, *nrho_mix, *np_mix, *nnrx, *nnry, *nux, *nuy;
     // LagrangeResult (lagrange.hpp:38-45)
-    double *q, *pmh, *ph[2], *uhx, *uhy, *ulx, *uly, *el[2], *vol_lag;
+    double *q, *pmh, *ph[kMatSlots], *uhx, *uhy, *ulx, *uly, *el[kMatSlots], *vol_lag;
     // remap scratch (the tile kernel keeps its geometry in shared memory)
-    double *me[2], *mcell, *unrm;
+    double *me[kMatSlots], *mcell, *unrm;
     double *dmx, *dmy, *dmc;
     double *dfx_x, *dfx_y, *dfy_x, *dfy_y;  // dual-face momentum contributions
     double *dc_x[2], *dc_y[2];              // dual-corner contributions per pair
-    double *slm[2], *slme[2];               // pending sliver mass / m*e (remap.cpp:149-153)
+    double *slm[kMatSlots], *slme[kMatSlots];               // pending sliver mass / m*e (remap.cpp:149-153)
     uint8_t* sliver;                        // per-cell sliver flags (bit a)
     uint8_t* dflag[4];                      // active X / Y dual faces, dual-corner pairs
     // sliver index: bit (i - r_gath.i0) of word [(j - r_gath.j0) * nwx + (i - r_gath.i0) / 32]

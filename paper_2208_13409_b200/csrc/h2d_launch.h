@@ -15,13 +15,13 @@ struct FieldList {
 // Work planes between the two passes of the AD split remap (remap.cpp:87-97):
 // pass 0 writes them, pass 1 reads them.
 struct AdWork {
-    double *m[2], *me[2], *e[2], *k[2], *nrx, *nry, *mcell, *ux, *uy;
+    double *m[kMatSlots], *me[kMatSlots], *e[kMatSlots], *k[kMatSlots], *nrx, *nry, *mcell, *ux, *uy;
 };
 
 // Work inputs of one AD directional pass: pass 0 reads the State and the
 // LagrangeResult (make_work, remap.cpp:116-140), pass 1 the AdWork of pass 0.
 struct AdIO {
-    const double *m[2], *me[2], *e[2], *k[2], *nrx, *nry, *mcell, *ux, *uy;
+    const double *m[kMatSlots], *me[kMatSlots], *e[kMatSlots], *k[kMatSlots], *nrx, *nry, *mcell, *ux, *uy;
     int me_from_e;  // pass 0: w.me = m * e_lag (remap.cpp:128); mcell == nullptr: sum of m
     int pass;       // 0 / 1 (error phases PH_AD_* + 5 pass)
     int axis_x;     // 1: X pass, 0: Y pass

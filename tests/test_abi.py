@@ -35,7 +35,7 @@ def test_product_library_exports_every_symbol():
     dll = ctypes.CDLL(helpers.PRODUCT_LIB)
     missing = [n for n in declared() if not hasattr(dll, "h2d_" + n)]
     assert missing == []
-    assert dll.h2d_abi_version() == 2
+    assert dll.h2d_abi_version() == 3
 
 
 def test_oracle_library_exports_the_same_abi(orc):
