@@ -116,7 +116,7 @@ struct h2do_ctx {
     ifld cf_sx, cf_sy;
     fld vlag, rho[H2D_MAX_MAT];
     vfld xlag2;
-    ifld if_mixed;
+    ifld if_mixed, if_lo, if_hi; /* (if_lo, if_hi: the interface pair of a 3-material cell) */
     fld if_lox, if_loy, if_hix, if_hiy, if_nx, if_ny, if_d;
     fld vola[H2D_MAX_MAT];
     fld dmx, dmy, dmc, mcell_lag;
@@ -542,6 +542,57 @@ static int youngs_normal(ctx_t* c, fld k1, int i, int j, double* nx, double* ny)
 /* ---------------------------------------------------------------- remap */
 static int is_mixed(double k0) { return k0 > PURE_TOL && k0 < 1.0 - PURE_TOL; } /* remap.cpp:100 */
 
+/* ---- three materials (configuration 5; no reference counterpart, the
+ * reference stops at kMaxMat = 2, state.hpp:13). The N-material extension
+ * applies the reference's one-interface VOF to the two
+ * largest fractions of a cell and IS the reference wherever a cell holds at
+ * most two materials (tests/test_three_materials.py checks that a 3-material
+ * run with one material absent equals the 2-material reference run):
+ *   mixed     three materials present (k > 0), or exactly two with the
+ *             lower-index one mixed in the reference's sense (remap.cpp:100);
+ *   pair      (lo, hi): the two largest fractions, ties to the lower index;
+ *   normal    Youngs normal of the pair's k_hi (remap.cpp:102-114);
+ *   interface place_interface(frac, normal, rect) with frac = k_lo, or
+ *             k_lo / (k_lo + k_hi) when the third material is present;
+ *   split     a mixed donor: the third material takes k_r * dvol of the flux
+ *             box, the pair splits the rest at the interface (box_frac0);
+ *             a pure donor gives everything to its largest fraction
+ *             (remap.cpp:243-268);
+ *   finalize  a cell where some material's remapped volume is exactly zero is
+ *             finalised by the reference's two-material rule on the other two
+ *             (the zero one: the highest such index); otherwise k_a = vola_a /
+ *             cv, clipped and snapped each, k2 = (1 - k0) - k1 (a k2 below
+ *             kPureTol snaps and k1 = 1 - k0), and a negative-mass material
+ *             hands its fraction to the largest other (remap.cpp:146-193);
+ *   slivers   an orphan sliver joins the cell's largest other material
+ *             (remap.cpp:217-225). */
+static void pair3(const double* k, int* lo, int* hi) {
+    int p = 0;
+    for (int a = 1; a < 3; ++a)
+        if (k[a] > k[p]) p = a;
+    int q = p == 0 ? 1 : 0;
+    for (int a = 0; a < 3; ++a)
+        if (a != p && k[a] > k[q]) q = a;
+    *lo = p < q ? p : q;
+    *hi = p < q ? q : p;
+}
+static int mixed3(const double* k) {
+    const int n = (k[0] > 0.0) + (k[1] > 0.0) + (k[2] > 0.0);
+    if (n == 3) return 1;
+    if (n < 2) return 0;
+    const int lo = k[0] > 0.0 ? 0 : 1;
+    return is_mixed(k[lo]);
+}
+static int largest_other3(const double* k, int a) {
+    int b = -1;
+    for (int c = 0; c < 3; ++c)
+        if (c != a && (b < 0 || k[c] > k[b])) b = c;
+    return b;
+}
+static void kcell3(fld* kf, int i, int j, double* k) {
+    for (int a = 0; a < 3; ++a) k[a] = A(kf[a], i, j);
+}
+
 /* cf_face_flux_x, remap.cpp:27-47; (dmx,dmy),(dpx,dpy) already axis-swapped for Y */
 static void cf_face_flux(double ym, double yp, double dmx, double dmy, double dpx, double dpy,
                          double* dv, double* wl, double* wh) {
@@ -586,9 +637,40 @@ static void make_work(ctx_t* c) {
 
 /* box_frac0 + split_flux, remap.cpp:243-268 */
 static void split_flux(ctx_t* c, int di, int dj, double blox, double bloy, double bhix, double bhiy,
-                       double dvol, double dva[2]) {
+                       double dvol, double dva[H2D_MAX_MAT]) {
     dva[0] = dvol;
     dva[1] = 0.0;
+    dva[2] = 0.0;
+    if (c->nmat == 3) {  /* the N-material split (see pair3) */
+        double k[3];
+        kcell3(c->w.k, di, dj, k);
+        dva[0] = 0.0;
+        if (!A(c->if_mixed, di, dj)) {
+            int p = 0;
+            for (int a = 1; a < 3; ++a)
+                if (k[a] > k[p]) p = a;
+            dva[p] = dvol;
+            return;
+        }
+        const int lo = A(c->if_lo, di, dj), hi = A(c->if_hi, di, dj), r = 3 - lo - hi;
+        const double nx = A(c->if_nx, di, dj), ny = A(c->if_ny, di, dj), d = A(c->if_d, di, dj);
+        const double rcx = 0.5 * (A(c->if_lox, di, dj) + A(c->if_hix, di, dj));
+        const double rcy = 0.5 * (A(c->if_loy, di, dj) + A(c->if_hiy, di, dj));
+        const double bcx = 0.5 * (blox + bhix), bcy = 0.5 * (bloy + bhiy);
+        const double bw = bhix - blox, bh = bhiy - bloy;
+        double f0;
+        if (!(bw * bh > 0.0)) {
+            const double sv = (nx * (bcx - rcx) + ny * (bcy - rcy)) - d;
+            f0 = sv <= 0.0 ? 1.0 : 0.0;
+        } else {
+            f0 = clipped_fraction(bw, bh, nx, ny, d - (nx * (bcx - rcx) + ny * (bcy - rcy)));
+        }
+        dva[r] = k[r] > 0.0 ? k[r] * dvol : 0.0;
+        const double rest = dvol - dva[r];
+        dva[lo] = f0 * rest;
+        dva[hi] = rest - dva[lo];
+        return;
+    }
     if (c->nmat != 2) return;
     if (A(c->if_mixed, di, dj)) {
         const double nx = A(c->if_nx, di, dj), ny = A(c->if_ny, di, dj), d = A(c->if_d, di, dj);
@@ -634,6 +716,49 @@ static void apply_cell(ctx_t* c, fld* vola, int a, int i, int j, double dm, doub
     A(vola[a], i, j) += dva;
 }
 
+/* refresh_normals_impl, remap.cpp:102-114: Youngs normal of k1 in the mixed
+ * cells (3 materials: of the pair's k_hi, pair3); an isolated cell keeps its
+ * normal */
+static void refresh_normals(ctx_t* c, fld* kf, vfld nrm) {
+    for (int j = 0; j < c->ny; ++j)
+        for (int i = 0; i < c->nx; ++i) {
+            int hi = 1;
+            if (c->nmat == 3) {
+                double k[3];
+                kcell3(kf, i, j, k);
+                if (!mixed3(k)) continue;
+                int lo;
+                pair3(k, &lo, &hi);
+            } else if (!is_mixed(A(kf[0], i, j))) {
+                continue;
+            }
+            double nxv, nyv;
+            if (youngs_normal(c, kf[hi], i, j, &nxv, &nyv)) {
+                VX(nrm, i, j) = nxv;
+                VY(nrm, i, j) = nyv;
+            }
+        }
+    ghost_cells_v(c, nrm);
+}
+
+/* the pending-sliver record of material a at (i, j), remap.cpp:170-173 */
+static void push_sliver(ctx_t* c, size_t* npend, int i, int j, int a) {
+    if (*npend == c->sl_cap) {
+        c->sl_cap = c->sl_cap ? 2 * c->sl_cap : 1024;
+        c->sl_i = realloc(c->sl_i, c->sl_cap * sizeof(int));
+        c->sl_j = realloc(c->sl_j, c->sl_cap * sizeof(int));
+        c->sl_a = realloc(c->sl_a, c->sl_cap * sizeof(int));
+        c->sl_m = realloc(c->sl_m, c->sl_cap * sizeof(double));
+        c->sl_me = realloc(c->sl_me, c->sl_cap * sizeof(double));
+    }
+    c->sl_i[*npend] = i;
+    c->sl_j[*npend] = j;
+    c->sl_a[*npend] = a;
+    c->sl_m[*npend] = A(c->w.m[a], i, j);
+    c->sl_me[*npend] = A(c->w.me[a], i, j);
+    ++*npend;
+}
+
 /* finalize_cells, remap.cpp:146-234 */
 static void finalize_cells(ctx_t* c) {
     work_t* w = &c->w;
@@ -641,6 +766,73 @@ static void finalize_cells(ctx_t* c) {
     size_t npend = 0;
     for (int j = 0; j < c->ny; ++j)
         for (int i = 0; i < c->nx; ++i) {
+            if (c->nmat == 3) {
+                int r = -1;  /* a material with an exactly zero remapped volume: two-material rule */
+                for (int a = 2; a >= 0 && r < 0; --a)
+                    if (A(c->vola[a], i, j) == 0.0) r = a;
+                if (r >= 0) {
+                    const int lo = r == 0 ? 1 : 0, hi = r == 2 ? 1 : 2;
+                    double k0 = A(c->vola[lo], i, j) / cv;
+                    const double k1 = A(c->vola[hi], i, j) / cv;
+                    double viol = 0.0;
+                    const double cand[5] = {-k0, k0 - 1.0, -k1, k1 - 1.0, fabs(k0 + k1 - 1.0)};
+                    for (int q = 0; q < 5; ++q)
+                        if (viol < cand[q]) viol = cand[q];
+                    if (c->diag && viol > c->diag->max_k_violation) c->diag->max_k_violation = viol;
+                    if (k0 < 0.0 || k0 > 1.0) {
+                        if (c->diag) ++c->diag->k_clip_count;
+                        k0 = (k0 < 0.0) ? 0.0 : ((1.0 < k0) ? 1.0 : k0);
+                    }
+                    if (k0 < PURE_TOL) k0 = 0.0;
+                    if (k0 > 1.0 - PURE_TOL) k0 = 1.0;
+                    A(w->k[lo], i, j) = k0;
+                    A(w->k[hi], i, j) = 1.0 - k0;
+                    A(w->k[r], i, j) = 0.0;
+                } else {
+                    double k[3];
+                    for (int a = 0; a < 3; ++a) k[a] = A(c->vola[a], i, j) / cv;
+                    double viol = 0.0;
+                    const double cand[7] = {-k[0], k[0] - 1.0, -k[1], k[1] - 1.0, -k[2], k[2] - 1.0,
+                                            fabs(k[0] + k[1] + k[2] - 1.0)};
+                    for (int q = 0; q < 7; ++q)
+                        if (viol < cand[q]) viol = cand[q];
+                    if (c->diag && viol > c->diag->max_k_violation) c->diag->max_k_violation = viol;
+                    int clipped = 0;
+                    for (int a = 0; a < 3; ++a) {
+                        if (k[a] < 0.0 || k[a] > 1.0) {
+                            clipped = 1;
+                            k[a] = (k[a] < 0.0) ? 0.0 : ((1.0 < k[a]) ? 1.0 : k[a]);
+                        }
+                        if (k[a] < PURE_TOL) k[a] = 0.0;
+                        if (k[a] > 1.0 - PURE_TOL) k[a] = 1.0;
+                    }
+                    if (clipped && c->diag) ++c->diag->k_clip_count;
+                    k[2] = (1.0 - k[0]) - k[1];
+                    if (k[2] < PURE_TOL) {
+                        k[2] = 0.0;
+                        k[1] = 1.0 - k[0];
+                    }
+                    for (int a = 0; a < 3; ++a) A(w->k[a], i, j) = k[a];
+                }
+                for (int a = 0; a < 3; ++a) {
+                    if ((A(w->k[a], i, j) == 0.0 && A(w->m[a], i, j) != 0.0) || A(w->m[a], i, j) < 0.0) {
+                        push_sliver(c, &npend, i, j, a);
+                        A(w->m[a], i, j) = 0.0;
+                        A(w->me[a], i, j) = 0.0;
+                        if (A(w->k[a], i, j) > 0.0) {  /* a negative mass with volume left behind */
+                            double kk[3];
+                            kcell3(w->k, i, j, kk);
+                            const int b = largest_other3(kk, a);
+                            if (r >= 0 && a != r) {  /* the reference's partner rule on the pair */
+                                A(w->k[3 - r - a], i, j) = 1.0;
+                            } else {
+                                A(w->k[b], i, j) = kk[b] + kk[a];
+                            }
+                            A(w->k[a], i, j) = 0.0;
+                        }
+                    }
+                }
+            }
             if (c->nmat == 2) {
                 double k0 = A(c->vola[0], i, j) / cv;
                 const double k1 = A(c->vola[1], i, j) / cv;
@@ -659,20 +851,7 @@ static void finalize_cells(ctx_t* c) {
                 A(w->k[1], i, j) = 1.0 - k0;
                 for (int a = 0; a < 2; ++a) {
                     if ((A(w->k[a], i, j) == 0.0 && A(w->m[a], i, j) != 0.0) || A(w->m[a], i, j) < 0.0) {
-                        if (npend == c->sl_cap) {
-                            c->sl_cap = c->sl_cap ? 2 * c->sl_cap : 1024;
-                            c->sl_i = realloc(c->sl_i, c->sl_cap * sizeof(int));
-                            c->sl_j = realloc(c->sl_j, c->sl_cap * sizeof(int));
-                            c->sl_a = realloc(c->sl_a, c->sl_cap * sizeof(int));
-                            c->sl_m = realloc(c->sl_m, c->sl_cap * sizeof(double));
-                            c->sl_me = realloc(c->sl_me, c->sl_cap * sizeof(double));
-                        }
-                        c->sl_i[npend] = i;
-                        c->sl_j[npend] = j;
-                        c->sl_a[npend] = a;
-                        c->sl_m[npend] = A(w->m[a], i, j);
-                        c->sl_me[npend] = A(w->me[a], i, j);
-                        ++npend;
+                        push_sliver(c, &npend, i, j, a);
                         A(w->m[a], i, j) = 0.0;
                         A(w->me[a], i, j) = 0.0;
                         if (A(w->k[a], i, j) > 0.0) {
@@ -721,7 +900,12 @@ static void finalize_cells(ctx_t* c) {
             A(w->mcell, bi, bj) += sm;
         } else {
             if (c->diag) ++c->diag->mass_fix_count;
-            const int b = 1 - a;
+            int b = 1 - a;
+            if (c->nmat == 3) {
+                double kk[3];
+                kcell3(w->k, si, sj, kk);
+                b = largest_other3(kk, a);
+            }
             A(w->m[b], si, sj) += sm;
             A(w->me[b], si, sj) += sme;
             A(w->e[b], si, sj) = A(w->me[b], si, sj) / A(w->m[b], si, sj);
@@ -941,11 +1125,22 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
         }
     /* interfaces, remap.cpp:807-824 */
     izero(c->if_mixed);
-    if (nmat == 2)
+    if (nmat >= 2)
         for (int j = -NG; j < ny + NG; ++j)
             for (int i = -NG; i < nx + NG; ++i) {
-                const double k0 = A(w->k[0], i, j);
-                if (!is_mixed(k0)) continue;
+                double k0 = A(w->k[0], i, j);
+                if (nmat == 3) {  /* the pair's interface (pair3) */
+                    double k[3];
+                    kcell3(w->k, i, j, k);
+                    if (!mixed3(k)) continue;
+                    int lo, hi;
+                    pair3(k, &lo, &hi);
+                    A(c->if_lo, i, j) = lo;
+                    A(c->if_hi, i, j) = hi;
+                    k0 = k[3 - lo - hi] > 0.0 ? k[lo] / (k[lo] + k[hi]) : k[lo];
+                } else if (!is_mixed(k0)) {
+                    continue;
+                }
                 const double cx = x0 + (i + 0.5) * dx, cy = y0 + (j + 0.5) * dy;
                 const double lox = cx - 0.5 * dx + A(c->fdx, i, j), loy = cy - 0.5 * dy + A(c->fdy, j, i);
                 const double hix = cx + 0.5 * dx + A(c->fdx, i + 1, j), hiy = cy + 0.5 * dy + A(c->fdy, j + 1, i);
@@ -985,14 +1180,14 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
                 const double width = dvol / wwin;
                 const double f0pos = ax ? x0 + ia * dx : y0 + ia * dy;
                 const double blo = ref_min(f0pos, f0pos + width), bhi = ref_max(f0pos, f0pos + width);
-                double dva[2];
+                double dva[H2D_MAX_MAT];
                 if (ax) split_flux(c, cdi, cdj, blo, wlo, bhi, whi, dvol, dva);
                 else split_flux(c, cdi, cdj, wlo, blo, whi, bhi, dvol, dva);
                 double dmtot = 0.0;
                 for (int a = 0; a < nmat; ++a) {
                     if (dva[a] == 0.0) continue;
                     int ord = order;
-                    if (ord == 2 && nmat == 2 && c->cfg.interface_degrade && !pure_1d(c, a, ax, ia_d, ic)) ord = 1;
+                    if (ord == 2 && nmat >= 2 && c->cfg.interface_degrade && !pure_1d(c, a, ax, ia_d, ic)) ord = 1;
                     double rf, ef;
                     if (ord <= 1) {
                         rf = A(c->rho[a], cdi, cdj);
@@ -1039,14 +1234,14 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
             const double ddx = DX_(i, j), ddy = DY_(i, j);
             const double blox = ref_min(npx, npx + ddx), bloy = ref_min(npy, npy + ddy);
             const double bhix = ref_max(npx, npx + ddx), bhiy = ref_max(npy, npy + ddy);
-            double dva[2];
+            double dva[H2D_MAX_MAT];
             split_flux(c, di, dj, blox, bloy, bhix, bhiy, cdv, dva);
             const double lwx = A(c->wlx, di, dj), lwy = A(c->wly, dj, di);
             double dmtot = 0.0;
             for (int a = 0; a < nmat; ++a) {
                 if (dva[a] == 0.0) continue;
                 int lin = diag_scheme && order > 1;
-                if (lin && nmat == 2 && c->cfg.interface_degrade && !pure_3x3(c, a, di, dj)) lin = 0;
+                if (lin && nmat >= 2 && c->cfg.interface_degrade && !pure_3x3(c, a, di, dj)) lin = 0;
                 double rf, ef;
                 if (!lin) {
                     rf = A(c->rho[a], di, dj);
@@ -1138,18 +1333,7 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
         apply_dual_update(c);
     }
     /* refresh_normals_impl, remap.cpp:102-114 */
-    if (nmat == 2) {
-        for (int j = 0; j < ny; ++j)
-            for (int i = 0; i < nx; ++i) {
-                if (!is_mixed(A(w->k[0], i, j))) continue;
-                double nxv, nyv;
-                if (youngs_normal(c, w->k[1], i, j, &nxv, &nyv)) {
-                    VX(w->normals, i, j) = nxv;
-                    VY(w->normals, i, j) = nyv;
-                }
-            }
-        ghost_cells_v(c, w->normals);
-    }
+    if (nmat >= 2) refresh_normals(c, w->k, w->normals);
 #undef DX_
 #undef DY_
 }
@@ -1249,7 +1433,7 @@ static void directional_pass(ctx_t* c, double dt, int axis_x, int remap_velocity
                 blox = x0 + ic * dx; bloy = ref_min(yf, yf + d);
                 bhix = x0 + (ic + 1) * dx; bhiy = ref_max(yf, yf + d);
             }
-            double dva[2];
+            double dva[H2D_MAX_MAT];
             split_flux(c, cdi, cdj, blox, bloy, bhix, bhiy, dvol, dva);
             double dmtot = 0.0;
             for (int a = 0; a < nmat; ++a) {
@@ -1345,6 +1529,8 @@ static void ctx_free(ctx_t* c) {
                  &c->w.m[0], &c->w.m[1], &c->w.me[0], &c->w.me[1], &c->w.e[0], &c->w.e[1], &c->w.k[0],
                  &c->w.k[1], &c->w.mcell, &c->fdx, &c->fdy, &c->xlcx, &c->xlcy, &c->wlx, &c->wly,
                  &c->fx_dv, &c->fx_lo, &c->fx_hi, &c->fy_dv, &c->fy_lo, &c->fy_hi, &c->cf_dv, &c->vlag,
+                 &c->m[2], &c->e[2], &c->k[2], &c->e_lag[2], &c->e_half[2], &c->p_half[2], &c->w.m[2],
+                 &c->w.me[2], &c->w.e[2], &c->w.k[2], &c->rho[2], &c->vola[2],
                  &c->rho[0], &c->rho[1], &c->if_lox, &c->if_loy, &c->if_hix, &c->if_hiy, &c->if_nx,
                  &c->if_ny, &c->if_d, &c->vola[0], &c->vola[1], &c->dmx, &c->dmy, &c->dmc, &c->mcell_lag};
     for (size_t q = 0; q < sizeof fl / sizeof fl[0]; ++q) free(fl[q]->p);
@@ -1353,7 +1539,7 @@ static void ctx_free(ctx_t* c) {
     for (size_t q = 0; q < sizeof vf / sizeof vf[0]; ++q) free(vf[q]->p);
     free(c->cf_sx.p);
     free(c->cf_sy.p);
-    free(c->if_mixed.p);
+    free(c->if_mixed.p); free(c->if_lo.p); free(c->if_hi.p);
     free(c->sl_i); free(c->sl_j); free(c->sl_a); free(c->sl_m); free(c->sl_me);
     free(c);
 }
@@ -1395,7 +1581,7 @@ int h2do_create(const h2d_config* cfg, int device, ctx_t** out) {
     c->fy_dv = fnew(nx, ny + 1); c->fy_lo = fnew(nx, ny + 1); c->fy_hi = fnew(nx, ny + 1);
     c->cf_dv = fnew(nx + 1, ny + 1); c->cf_sx = inew(nx + 1, ny + 1); c->cf_sy = inew(nx + 1, ny + 1);
     c->vlag = fnew(nx, ny); c->xlag2 = vnew(nx, ny);
-    c->if_mixed = inew(nx, ny);
+    c->if_mixed = inew(nx, ny); c->if_lo = inew(nx, ny); c->if_hi = inew(nx, ny);
     c->if_lox = fnew(nx, ny); c->if_loy = fnew(nx, ny); c->if_hix = fnew(nx, ny); c->if_hiy = fnew(nx, ny);
     c->if_nx = fnew(nx, ny); c->if_ny = fnew(nx, ny); c->if_d = fnew(nx, ny);
     c->dmx = fnew(nx + 1, ny); c->dmy = fnew(ny + 1, nx); c->dmc = fnew(nx + 1, ny + 1);
@@ -1456,17 +1642,8 @@ int h2do_sync_derived(ctx_t* c) {
 }
 /* update_interface_normals -> refresh_normals_impl, remap.cpp:1093-1096,102-114 */
 int h2do_update_interface_normals(ctx_t* c) {
-    if (c->nmat != 2) return 0;
-    for (int j = 0; j < c->ny; ++j)
-        for (int i = 0; i < c->nx; ++i) {
-            if (!is_mixed(A(c->k[0], i, j))) continue;
-            double nxv, nyv;
-            if (youngs_normal(c, c->k[1], i, j, &nxv, &nyv)) {
-                VX(c->nrm, i, j) = nxv;
-                VY(c->nrm, i, j) = nyv;
-            }
-        }
-    ghost_cells_v(c, c->nrm);
+    if (c->nmat < 2) return 0;
+    refresh_normals(c, c->k, c->nrm);
     return 0;
 }
 
@@ -1517,6 +1694,11 @@ int h2do_remap_step(ctx_t* c, double dt, int kind, int x_first, int remap_veloci
     if (!c->have_lag) {
         c->err.kind = H2D_ERR_INVALID;
         snprintf(c->err.what, sizeof c->err.what, "remap_step without a LagrangeResult");
+        return H2D_ERR_INVALID;
+    }
+    if (kind == H2D_REMAP_AD && c->nmat == 3) {
+        c->err.kind = H2D_ERR_INVALID;
+        snprintf(c->err.what, sizeof c->err.what, "the AD remap has no three-material extension");
         return H2D_ERR_INVALID;
     }
     h2d_remap_diag local;
@@ -1588,8 +1770,16 @@ int h2do_run(ctx_t* c, h2d_run_args* a) {
 }
 
 /* compute_totals, state.cpp:145-160 */
+static void totals7(ctx_t* c, double out[7]);
 int h2do_totals(ctx_t* c, double out[6]) {
-    double mass = 0.0, ie = 0.0, mm[2] = {0.0, 0.0}, px = 0.0, py = 0.0;
+    double t[7];
+    totals7(c, t);
+    memcpy(out, t, 6 * sizeof(double));
+    return 0;
+}
+/* {mass, mass_mat0, mass_mat1, momentum x, momentum y, internal energy, mass_mat2} */
+static void totals7(ctx_t* c, double out[7]) {
+    double mass = 0.0, ie = 0.0, mm[3] = {0.0, 0.0, 0.0}, px = 0.0, py = 0.0;
     for (int j = 0; j < c->ny; ++j)
         for (int i = 0; i < c->nx; ++i) {
             mass += A(c->m_mix, i, j);
@@ -1604,14 +1794,13 @@ int h2do_totals(ctx_t* c, double out[6]) {
             px += mp * VX(c->u, i, j);
             py += mp * VY(c->u, i, j);
         }
-    out[0] = mass; out[1] = mm[0]; out[2] = mm[1]; out[3] = px; out[4] = py; out[5] = ie;
-    return 0;
+    out[0] = mass; out[1] = mm[0]; out[2] = mm[1]; out[3] = px; out[4] = py; out[5] = ie; out[6] = mm[2];
 }
 
 /* make_diag, harness.cpp:360-376 */
 int h2do_step_diag_now(ctx_t* c, double dt, h2d_step_diag* d) {
-    double t[6];
-    h2do_totals(c, t);
+    double t[7];
+    totals7(c, t);
     memset(d, 0, sizeof *d);
     d->step = c->step;
     d->t = c->time;
@@ -1619,6 +1808,7 @@ int h2do_step_diag_now(ctx_t* c, double dt, h2d_step_diag* d) {
     d->mass = t[0];
     d->mass_mat[0] = t[1];
     d->mass_mat[1] = t[2];
+    d->mass_mat[2] = t[6];
     d->momentum_x = t[3];
     d->momentum_y = t[4];
     d->internal_energy = t[5];

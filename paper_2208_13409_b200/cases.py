@@ -10,9 +10,9 @@ reference ``init_case`` (pinned by tests/test_oracle_vs_reference.py).
 Two shapes the reference painter lacks are added for configs 4 and 5 (the
 reference has no perturbed circle and no Voronoi region): a
 seeded Fourier-perturbed circle sampled 16x16 per cell like the reference
-circle (harness.cpp:179-189).  Config 5 needs three materials, which the
-reference (kMaxMat = 2, state.hpp:13) and this build do not support; it is
-not offered here (DESIGN.md §"Out of scope").
+circle (harness.cpp:179-189), and the seeded three-material Voronoi mesh of
+config 5 (``voronoi3``; three materials are this build's N-material
+extension, the reference stops at kMaxMat = 2, state.hpp:13).
 """
 from __future__ import annotations
 
@@ -311,4 +311,108 @@ def shock_bubble(n: int = 8192, seed: int = 20241001) -> Case:
                         radius_fn=bubble_radius_fn(seed))], 0.3, 200)
 
 
-CASES = {"c1": riemann2d, "c2": sedov, "c3": triple_point, "c4": shock_bubble}
+def voronoi_sites(nsites: int = 64, seed: int = 20241005):
+    """Config 5's seeded sites: positions U[0,1]^2, material uniform over the
+    three gammas, rho and p log-uniform on [0.1, 10], u and v U[-0.5, 0.5]."""
+    rng = np.random.Generator(np.random.MT19937(seed))
+    xy = rng.uniform(0.0, 1.0, (nsites, 2))
+    mat = rng.integers(0, 3, nsites)
+    rho = 10.0 ** rng.uniform(-1.0, 1.0, nsites)
+    p = 10.0 ** rng.uniform(-1.0, 1.0, nsites)
+    uv = rng.uniform(-0.5, 0.5, (nsites, 2))
+    return xy, mat, rho, p, uv
+
+
+def _nearest(px: np.ndarray, py: np.ndarray, xy: np.ndarray, chunk: int = 1 << 18) -> np.ndarray:
+    """Index of the nearest site of each point (squared distance, ties to the
+    lower index), in chunks."""
+    out = np.empty(px.size, np.int64)
+    fx, fy = px.ravel(), py.ravel()
+    for s0 in range(0, fx.size, chunk):
+        ddx = fx[s0:s0 + chunk, None] - xy[None, :, 0]
+        ddy = fy[s0:s0 + chunk, None] - xy[None, :, 1]
+        out[s0:s0 + chunk] = np.argmin(ddx * ddx + ddy * ddy, axis=1)
+    return out.reshape(px.shape)
+
+
+def paint_voronoi3(cfg: Config, sites, sub: int = 4) -> HostState:
+    """Config 5's initial State (three materials, gammas 1.4 / 1.5 / 1.67).
+    Node u: the nearest site's velocity.  Cells: a cell whose four corners
+    have the same nearest site lies in that site's (convex) Voronoi region and
+    is pure: k = 1, m = rho cv, e = p / ((gamma - 1) rho).  Any other cell is
+    sampled on sub x sub points: k_a = n_a / sub^2, m_a = (sum of the
+    samples' rho, in sample order) * (cv / sub^2), e_a = (sum of rho e) /
+    (sum of rho)."""
+    xy, mat, rho, p, uv = sites
+    m = cfg.mesh
+    nx, ny, dx, dy, x0, y0 = m.nx, m.ny, m.dx, m.dy, m.x0, m.y0
+    gam = np.array([cfg.eos[a].gamma for a in range(3)])
+    e_site = p / ((gam[mat] - 1.0) * rho)
+    cv = dx * dy
+    st = HostState.empty(nx, ny, 3, cv)
+    g = GHOST
+    xn = x0 + np.arange(nx + 1) * dx
+    yn = y0 + np.arange(ny + 1) * dy
+    lab = _nearest(np.broadcast_to(xn[None, :], (ny + 1, nx + 1)), np.broadcast_to(yn[:, None], (ny + 1, nx + 1)), xy)
+    st.u[g:g + ny + 1, g:g + nx + 1, 0] = uv[lab, 0]
+    st.u[g:g + ny + 1, g:g + nx + 1, 1] = uv[lab, 1]
+    c00 = lab[:-1, :-1]
+    pure = (c00 == lab[:-1, 1:]) & (c00 == lab[1:, :-1]) & (c00 == lab[1:, 1:])
+    I = (slice(g, g + ny), slice(g, g + nx))
+    kk = np.zeros((3, ny, nx))
+    mm = np.zeros((3, ny, nx))
+    ee = np.zeros((3, ny, nx))
+    pm = mat[c00]
+    for a in range(3):
+        sel = pure & (pm == a)
+        kk[a][sel] = 1.0
+        mm[a][sel] = rho[c00[sel]] * cv
+        ee[a][sel] = e_site[c00[sel]]
+    jj, ii = np.nonzero(~pure)
+    if jj.size:
+        ns = sub * sub
+        offs = (np.arange(sub) + 0.5) / sub
+        sx = x0 + (ii[:, None, None] + offs[None, None, :]) * dx  # [cell, q (row), s (col)]
+        sy = y0 + (jj[:, None, None] + offs[None, :, None]) * dy
+        sx, sy = np.broadcast_to(sx, (ii.size, sub, sub)), np.broadcast_to(sy, (ii.size, sub, sub))
+        sl = _nearest(np.ascontiguousarray(sx), np.ascontiguousarray(sy), xy).reshape(ii.size, ns)
+        smat, srho, sre = mat[sl], rho[sl], rho[sl] * e_site[sl]
+        for a in range(3):
+            inm = smat == a
+            cnt = inm.sum(axis=1)
+            rs = np.zeros(ii.size)
+            res = np.zeros(ii.size)
+            for q in range(ns):  # the samples in order
+                rs = rs + np.where(inm[:, q], srho[:, q], 0.0)
+                res = res + np.where(inm[:, q], sre[:, q], 0.0)
+            kk[a][jj, ii] = cnt / float(ns)
+            mm[a][jj, ii] = rs * (cv / float(ns))
+            ee[a][jj, ii] = np.where(cnt > 0, res / np.where(cnt > 0, rs, 1.0), 0.0)
+    for a in range(3):
+        st.k[a][I] = kk[a]
+        st.m[a][I] = mm[a]
+        st.e[a][I] = ee[a]
+    return st
+
+
+@dataclass
+class VoronoiCase(Case):
+    sites: tuple = ()
+
+    def paint(self) -> HostState:
+        return paint_voronoi3(self.cfg, self.sites)
+
+
+def voronoi3(nx: int = 16384, ny: Optional[int] = None, nsites: int = 64, seed: int = 20241005) -> Case:
+    """Config 5: three-material Voronoi mesh on [0,1]^2 (gammas 1.4, 1.5,
+    1.67 = materials 0, 1, 2), 64 seeded sites, 4x4 sampling of the cells the
+    site boundaries cross, walls, CFL 0.3 (unstated in BASELINE.json), 100
+    steps. A non-square ny paints the lower part of the same unit-spaced
+    mesh (ny / nx of the height: the block of one GPU of a decomposition)."""
+    ny = nx if ny is None else ny
+    eos = [(EOS_PERFECT, 1.4, 0.0), (EOS_PERFECT, 1.5, 0.0), (EOS_PERFECT, 1.67, 0.0)]
+    return VoronoiCase(f"voronoi3_{nx}x{ny}", _mesh_cfg(nx, ny, 1.0, ny / nx, eos), [], 0.3, 100,
+                       sites=voronoi_sites(nsites, seed))
+
+
+CASES = {"c1": riemann2d, "c2": sedov, "c3": triple_point, "c4": shock_bubble, "c5": voronoi3}
