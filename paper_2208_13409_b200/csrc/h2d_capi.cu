@@ -191,7 +191,8 @@ int copy_series(h2d_ctx* c, h2d_step_diag* out, int n) {
         o.dt = x[2];
         o.mass = x[3 + DG_MASS];
         o.mass_mat[0] = x[3 + DG_MM0];
-        o.mass_mat[1] = c->nmat == 2 ? x[3 + DG_MM1] : 0.0;
+        o.mass_mat[1] = c->nmat >= 2 ? x[3 + DG_MM1] : 0.0;
+        o.mass_mat[2] = c->nmat == 3 ? x[3 + DG_MM2] : 0.0;
         o.momentum_x = x[3 + DG_PX];
         o.momentum_y = x[3 + DG_PY];
         o.internal_energy = x[3 + DG_IE];
@@ -233,7 +234,7 @@ int decode_error(h2d_ctx* c, bool in_run) {
     case PH_GRAD_DUALC: kind = H2D_ERR_SIM; msg = "non-increasing centroid coordinates"; break;
     case PH_NEGMASS:
         kind = H2D_ERR_NEGMASS;
-        msg = sub == 2 ? "non-positive cell mass" : "negative mass";
+        msg = sub == kSubCellMass ? "non-positive cell mass" : "negative mass";
         located = true;
         break;
     case PH_NODAL_MASS: kind = H2D_ERR_NEGMASS; msg = "non-positive nodal mass"; located = true; break;
@@ -255,7 +256,7 @@ int decode_error(h2d_ctx* c, bool in_run) {
                 break;
             case PH_AD_NEGMASS:
                 kind = H2D_ERR_NEGMASS;
-                msg = sub == 2 ? "non-positive cell mass" : "negative mass";
+                msg = sub == kSubCellMass ? "non-positive cell mass" : "negative mass";
                 located = true;
                 break;
             case PH_AD_GRAD_DUAL: kind = H2D_ERR_SIM; msg = "non-increasing centroid coordinates"; break;
@@ -558,7 +559,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     const h2d_mesh& m = cfg->mesh;
     if (m.nx < 3 || m.ny < 3) return H2D_ERR_SIM;        // Mesh::Mesh, mesh.hpp:27
     if (m.dx <= 0.0 || m.dy <= 0.0) return H2D_ERR_SIM;  // mesh.hpp:28
-    if (cfg->nmat < 1 || cfg->nmat > 2) return H2D_ERR_INVALID;  // (three materials: DESIGN.md 5b)
+    if (cfg->nmat < 1 || cfg->nmat > H2D_MAX_MAT) return H2D_ERR_INVALID;  // (3: DESIGN.md 5b)
     if (cfg->corner != H2D_CORNER_UPWIND && cfg->corner != H2D_CORNER_LINEARDIAG) return H2D_ERR_INVALID;
     h2d_ctx* c = new h2d_ctx();
     c->cfg = *cfg;
@@ -828,7 +829,7 @@ int h2d_sync_derived(h2d_ctx* c) {
 
 int h2d_update_interface_normals(h2d_ctx* c) {
     cudaSetDevice(c->device);
-    if (c->nmat != 2) return 0;
+    if (c->nmat < 2) return 0;
     const Dev d = make_dev(c, c->cur, 1);
     launch_normals_api(d, c->st);
     FieldList fl{};
@@ -888,7 +889,7 @@ int h2d_set_lagrange(h2d_ctx* c, const h2d_lagrange* in) {
     cudaSetDevice(c->device);
     const int nx = c->nx, ny = c->ny;
     const Dev& d = c->base;
-    double* planes[] = {d.uhx, d.uhy, d.ulx, d.uly, d.vol_lag, d.q, d.el[0], d.el[1]};
+    double* planes[] = {d.uhx, d.uhy, d.ulx, d.uly, d.vol_lag, d.q, d.el[0], d.el[1], d.el[2]};
     for (double* p : planes)
         if (p)
             if (int rc = zero_plane(c, p)) return rc;
@@ -906,7 +907,7 @@ int h2d_set_lagrange(h2d_ctx* c, const h2d_lagrange* in) {
 
 int h2d_remap_step(h2d_ctx* c, double dt, int kind, int x_first, int remap_velocity, h2d_remap_diag* diag) {
     cudaSetDevice(c->device);
-    if (kind != H2D_REMAP_DIRECTCF && !(kind == H2D_REMAP_AD && !c->is_block)) {
+    if (kind != H2D_REMAP_DIRECTCF && !(kind == H2D_REMAP_AD && !c->is_block && c->nmat <= 2)) {
         set_err(c, H2D_ERR_INVALID, "only the DirectCF and (single-domain) AD remaps are implemented on the device");
         return H2D_ERR_INVALID;
     }
@@ -941,7 +942,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
     cudaSetDevice(c->device);
     a->steps_done = 0;
     const bool ad = a->remap_kind == H2D_REMAP_AD;
-    if (a->remap_kind != H2D_REMAP_DIRECTCF && !(ad && !c->is_block)) {
+    if (a->remap_kind != H2D_REMAP_DIRECTCF && !(ad && !c->is_block && c->nmat <= 2)) {
         set_err(c, H2D_ERR_INVALID, "only the DirectCF and (single-domain) AD remaps are implemented on the device");
         return H2D_ERR_INVALID;
     }
@@ -1006,30 +1007,43 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
     return decode_error(c, true);
 }
 
+static int totals7(h2d_ctx* c, double out[7]);
 int h2d_totals(h2d_ctx* c, double out[6]) {
+    double t[7];
+    if (int rc = totals7(c, t)) return rc;
+    for (int q = 0; q < 6; ++q) out[q] = t[q];
+    return 0;
+}
+
+// {mass, mass_mat0, mass_mat1, momentum x, momentum y, internal energy, mass_mat2}
+static int totals7(h2d_ctx* c, double out[7]) {
     // compute_totals (state.cpp:145-160) is a serial fp64 sum: read the
     // fields back and add them in the reference order so totals are exact.
     cudaSetDevice(c->device);
     const int nx = c->nx, ny = c->ny;
     const size_t W = (size_t)nx + 2 * G, Wn = W + 1;
-    std::vector<double> m_mix(W * (ny + 2 * G)), e_mix(m_mix.size()), m0(m_mix.size()), m1(m_mix.size());
+    std::vector<double> m_mix(W * (ny + 2 * G)), e_mix(m_mix.size()), m0(m_mix.size()), m1(m_mix.size()),
+        m2(m_mix.size());
     std::vector<double> u(Wn * (ny + 1 + 2 * G) * 2);
     const StateBufs& s = c->sb[c->cur];
     if (int rc = get_plane(c, m_mix.data(), s.m_mix, nx, ny)) return rc;
     if (int rc = get_plane(c, e_mix.data(), s.e_mix, nx, ny)) return rc;
     if (int rc = get_plane(c, m0.data(), s.m[0], nx, ny)) return rc;
-    if (c->nmat == 2)
+    if (c->nmat >= 2)
         if (int rc = get_plane(c, m1.data(), s.m[1], nx, ny)) return rc;
+    if (c->nmat == 3)
+        if (int rc = get_plane(c, m2.data(), s.m[2], nx, ny)) return rc;
     if (int rc = get_vec(c, u.data(), s.ux, s.uy, nx + 1, ny + 1)) return rc;
     CK(cudaStreamSynchronize(c->st));
     auto C = [&](const std::vector<double>& f, int i, int j) { return f[(size_t)(j + G) * W + (i + G)]; };
-    double mass = 0.0, ie = 0.0, mm0 = 0.0, mm1 = 0.0, px = 0.0, py = 0.0;
+    double mass = 0.0, ie = 0.0, mm0 = 0.0, mm1 = 0.0, mm2 = 0.0, px = 0.0, py = 0.0;
     for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
             mass += C(m_mix, i, j);
             ie += C(m_mix, i, j) * C(e_mix, i, j);
             mm0 += C(m0, i, j);
-            if (c->nmat == 2) mm1 += C(m1, i, j);
+            if (c->nmat >= 2) mm1 += C(m1, i, j);
+            if (c->nmat == 3) mm2 += C(m2, i, j);
         }
     const bool px_ = c->cfg.mesh.bc_x == H2D_BC_PERIODIC, py_ = c->cfg.mesh.bc_y == H2D_BC_PERIODIC;
     const int ie_ = px_ ? nx - 1 : nx, je_ = py_ ? ny - 1 : ny;
@@ -1047,13 +1061,14 @@ int h2d_totals(h2d_ctx* c, double out[6]) {
     out[3] = px;
     out[4] = py;
     out[5] = ie;
+    out[6] = mm2;
     return 0;
 }
 
 int h2d_step_diag_now(h2d_ctx* c, double dt, h2d_step_diag* out) {
     // make_diag (harness.cpp:360-376) on the host, in the reference's order
-    double t[6];
-    if (int rc = h2d_totals(c, t)) return rc;
+    double t[7];
+    if (int rc = totals7(c, t)) return rc;
     const int nx = c->nx, ny = c->ny;
     const size_t W = (size_t)nx + 2 * G;
     std::vector<double> rho(W * (ny + 2 * G)), p(rho.size());
@@ -1070,6 +1085,7 @@ int h2d_step_diag_now(h2d_ctx* c, double dt, h2d_step_diag* out) {
     d.mass = t[0];
     d.mass_mat[0] = t[1];
     d.mass_mat[1] = t[2];
+    d.mass_mat[2] = t[6];
     d.momentum_x = t[3];
     d.momentum_y = t[4];
     d.internal_energy = t[5];
@@ -1154,7 +1170,7 @@ int h2d_load_state(h2d_ctx* c, const char* path) {
 int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_kind, float ms[8]) {
     cudaSetDevice(c->device);
     const bool ad = remap_kind == H2D_REMAP_AD;
-    if (!(remap_kind == H2D_REMAP_DIRECTCF || (ad && !c->is_block))) {
+    if (!(remap_kind == H2D_REMAP_DIRECTCF || (ad && !c->is_block && c->nmat <= 2))) {
         set_err(c, H2D_ERR_INVALID, "h2d_step_timed: DirectCF or (single-domain) AD only");
         return H2D_ERR_INVALID;
     }

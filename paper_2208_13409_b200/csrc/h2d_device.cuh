@@ -100,7 +100,9 @@ struct Ctl {
 };
 
 // StepDiag + Totals (harness.hpp:66-72, state.hpp:93-98) slots of Ctl::dg
-enum { DG_MASS, DG_IE, DG_MM0, DG_MM1, DG_MINR, DG_MAXR, DG_MINP, DG_MAXP, DG_NCELL, DG_PX = DG_NCELL, DG_PY, DG_N };
+enum { DG_MASS, DG_IE, DG_MM0, DG_MM1, DG_MM2, DG_MINR, DG_MAXR, DG_MINP, DG_MAXP, DG_NCELL, DG_PX = DG_NCELL, DG_PY, DG_N };
+// fold of each slot: 0 sum, 1 min, 2 max
+H2D_DEV int dg_op(int k) { return (k == DG_MINR || k == DG_MINP) ? 1 : ((k == DG_MAXR || k == DG_MAXP) ? 2 : 0); }
 // one log record: step, t, dt, then Ctl::dg[0 .. DG_N)
 constexpr int kDiagRec = 3 + DG_N;
 // Per-step diagnostics reduction: k_post and the node update store one
@@ -126,6 +128,8 @@ H2D_DEV void raise(Ctl* c, uint64_t key) { atomicMin(&c->err_key, (unsigned long
 
 // per-material slots of the State (H2D_MAX_MAT): 1-2 = the reference, 3 = config 5
 constexpr int kMatSlots = 3;
+// error sub-index of finalize's "non-positive cell mass" (after the material indices)
+constexpr int kSubCellMass = 7;
 
 // Half-open range of GLOBAL indices [i0, i1) x [j0, j1).
 struct Rng {
@@ -382,5 +386,38 @@ H2D_DEV double place_interface(double frac, double nx, double ny, double lox, do
 }
 
 H2D_DEV bool is_mixed(double k0) { return k0 > kPureTol && k0 < 1.0 - kPureTol; }  // remap.cpp:100
+
+// Three materials (configuration 5's N-material extension; the
+// oracle's pair3 / mixed3 / largest_other3, oracle/h2d_oracle.c): the
+// reference's one-interface VOF on the two largest fractions of a cell.
+H2D_DEV void pair3(const double* k, int& lo, int& hi) {
+    int p = 0;
+    if (k[1] > k[p]) p = 1;
+    if (k[2] > k[p]) p = 2;
+    int q = p == 0 ? 1 : 0;
+    for (int a = 0; a < 3; ++a)
+        if (a != p && k[a] > k[q]) q = a;
+    lo = p < q ? p : q;
+    hi = p < q ? q : p;
+}
+H2D_DEV bool mixed3(const double* k) {
+    const int n = (k[0] > 0.0) + (k[1] > 0.0) + (k[2] > 0.0);
+    if (n == 3) return true;
+    if (n < 2) return false;
+    return is_mixed(k[0] > 0.0 ? k[0] : k[1]);
+}
+H2D_DEV int largest_other3(const double* k, int a) {
+    int b = -1;
+    for (int c = 0; c < 3; ++c)
+        if (c != a && (b < 0 || k[c] > k[b])) b = c;
+    return b;
+}
+// the pure donor's material: the largest fraction (first on ties)
+H2D_DEV int largest3(const double* k) {
+    int p = 0;
+    if (k[1] > k[p]) p = 1;
+    if (k[2] > k[p]) p = 2;
+    return p;
+}
 
 }  // namespace h2d

@@ -355,7 +355,7 @@ __global__ void k_lag_cells(Dev d) {
     const int n00 = c, n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
     const double u00x = d.ux[n00], u00y = d.uy[n00], u10x = d.ux[n10], u10y = d.uy[n10];
     const double u01x = d.ux[n01], u01y = d.uy[n01], u11x = d.ux[n11], u11y = d.uy[n11];
-    double ka[2], ma[2], en[2];
+    double ka[NM], ma[NM], en[NM];
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
         ka[a] = d.k[a][c];
@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     RowCol<CW, LTX * LTY> rc0(tid);
     for (int t = tid; t < NC; t += LTX * LTY, rc0.step()) {
         const int ci = i0 - 1 + rc0.c, cj = j0 - 1 + rc0.r;
-        double q = 0.0, pmix = 0.0, ph[2] = {0.0, 0.0};
+        double q = 0.0, pmix = 0.0, ph[NM] = {};
         if (in(d.win_c, ci, cj) && ci >= -1 && cj >= -1 && ci <= nx && cj <= ny) {
             const int i = (ci < 0 || ci >= nx) ? wrap_cell(ci, nx, d.per_x) : ci;
             const int j = (cj < 0 || cj >= ny) ? wrap_cell(cj, ny, d.per_y) : cj;
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
             const int n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
             const double u00x = d.ux[c], u00y = d.uy[c], u10x = d.ux[n10], u10y = d.uy[n10];
             const double u01x = d.ux[n01], u01y = d.uy[n01], u11x = d.ux[n11], u11y = d.uy[n11];
-            double ka[2], ma[2], en[2];
+            double ka[NM], ma[NM], en[NM];
 #pragma unroll
             for (int a = 0; a < NM; ++a) {
                 ka[a] = d.k[a][c];
@@ -768,10 +768,10 @@ template <int NM>
 struct Tile {
     int ci0, cj0;  // origin of both regions: (i0 - 2, j0 - 2)
     double *hx, *hy, *fdx, *fdy, *fxdv, *fydv;  // nodes
-    double *vl, *rho[2], *el[2], *kk[2], *xl2x, *xl2y, *ifd;  // cells
+    double *vl, *rho[kMatSlots], *el[kMatSlots], *kk[kMatSlots], *xl2x, *xl2y, *ifd;  // cells
     // flux items of one sub-phase (X faces, then Y faces, then corners share
     // the buffer): dm, dme, dva per material
-    double* it[3][2];
+    double* it[3][kMatSlots];
     __device__ __forceinline__ int c(int i, int j) const { return (i - ci0) + (j - cj0) * RCW; }
     __device__ __forceinline__ int n(int i, int j) const { return (i - ci0) + (j - cj0) * RNW; }
     // cf_corner_flux (remap.cpp:16-25) at region node q, recomputed from the
@@ -804,7 +804,8 @@ struct Tile {
 
 template <int NM>
 constexpr size_t remap_smem_bytes() {
-    return sizeof(double) * (6 * al16(RNN) + (NM == 2 ? RCELL2 : RCELL1) * al16(RNC) + 3 * NM * al16(NIT)) + 128;
+    return sizeof(double) * (6 * al16(RNN) + (NM == 1 ? RCELL1 : RCELL2 + 3 * (NM - 2)) * al16(RNC) +
+                             3 * NM * al16(NIT)) + 128;
 }
 
 template <int NM>
@@ -831,9 +832,8 @@ __device__ __forceinline__ Tile<NM> carve_tile(char* base, int ci0, int cj0) {
         T.rho[a] = take(RNC);
         T.el[a] = take(RNC);
     }
-    if (NM == 2) {
-        T.kk[0] = take(RNC);
-        T.kk[1] = take(RNC);
+    if (NM >= 2) {
+        for (int a = 0; a < NM; ++a) T.kk[a] = take(RNC);
         T.ifd = take(RNC);
     }
     for (int k = 0; k < 3; ++k)
@@ -841,13 +841,60 @@ __device__ __forceinline__ Tile<NM> carve_tile(char* base, int ci0, int cj0) {
     return T;
 }
 
+// The three-material split of a flux box of donor (di, dj) (oracle
+// split_flux, nmat == 3): a mixed donor gives k_r * dvol to the material
+// outside its interface pair and splits the rest at the pair's interface; a
+// pure donor gives everything to its largest fraction.
+template <int NM>
+__device__ __forceinline__ void split_flux3(const Dev& d, const Tile<NM>& T, int di, int dj, double blox,
+                                            double bloy, double bhix, double bhiy, double dvol, double* dva) {
+    const int c = T.c(di, dj);
+    const double k[3] = {T.kk[0][c], T.kk[1][c], T.kk[NM - 1][c]};
+    dva[0] = 0.0;
+    dva[1] = 0.0;
+    dva[NM - 1] = 0.0;
+    if (!mixed3(k)) {
+        dva[largest3(k)] = dvol;
+        return;
+    }
+    int lo, hi;
+    pair3(k, lo, hi);
+    const int r = 3 - lo - hi;
+    const int g = ix(d, di, dj);
+    const double nx = d.nrx[g], ny = d.nry[g], dd = T.ifd[c];
+    const double cx = d.x0 + (di + 0.5) * d.dx, cy = d.y0 + (dj + 0.5) * d.dy;
+    const double lox = cx - 0.5 * d.dx + T.fdx[T.n(di, dj)], loy = cy - 0.5 * d.dy + T.fdy[T.n(di, dj)];
+    const double hix = cx + 0.5 * d.dx + T.fdx[T.n(di + 1, dj)];
+    const double hiy = cy + 0.5 * d.dy + T.fdy[T.n(di, dj + 1)];
+    const double rcx = 0.5 * (lox + hix), rcy = 0.5 * (loy + hiy);
+    const double bcx = 0.5 * (blox + bhix), bcy = 0.5 * (bloy + bhiy);
+    const double bw = bhix - blox, bh = bhiy - bloy;
+    double f0;
+    if (!(bw * bh > 0.0)) {
+        const double sdist = (nx * (bcx - rcx) + ny * (bcy - rcy)) - dd;
+        f0 = sdist <= 0.0 ? 1.0 : 0.0;
+    } else {
+        f0 = clipped_fraction(bw, bh, nx, ny, dd - (nx * (bcx - rcx) + ny * (bcy - rcy)));
+    }
+    double dr = k[r] > 0.0 ? k[r] * dvol : 0.0;
+    const double rest = dvol - dr;
+    const double dl = f0 * rest;
+    const double dh = rest - dl;
+#pragma unroll
+    for (int a = 0; a < NM; ++a) dva[a] = a == lo ? dl : (a == hi ? dh : dr);
+}
+
 // box_frac0 + split_flux, remap.cpp:243-268, donor cell (di, dj) of the tile
 template <int NM>
 __device__ __forceinline__ void split_flux_t(const Dev& d, const Tile<NM>& T, int di, int dj, double blox,
-                                             double bloy, double bhix, double bhiy, double dvol, double dva[2]) {
+                                             double bloy, double bhix, double bhiy, double dvol, double* dva) {
     dva[0] = dvol;
+    if (NM == 1) return;
     dva[1] = 0.0;
-    if (NM != 2) return;
+    if (NM == 3) {
+        split_flux3(d, T, di, dj, blox, bloy, bhix, bhiy, dvol, dva);
+        return;
+    }
     const int c = T.c(di, dj);
     const double k0 = T.kk[0][c];
     if (is_mixed(k0)) {
@@ -885,7 +932,7 @@ __device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, i
     const int qn = T.n(i, j);
     const double dvol = AX ? T.fxdv[qn] : T.fydv[qn];
     double dmtot = 0.0;
-    double dva[2] = {0.0, 0.0}, rfv[2] = {0.0, 0.0}, efv[2] = {0.0, 0.0};
+    double dva[NM] = {}, rfv[NM] = {}, efv[NM] = {};
     if (dvol != 0.0) {
         const int ia = AX ? i : j, ic = AX ? j : i;
         const int ia_d = dvol > 0.0 ? ia - 1 : ia;
@@ -913,7 +960,7 @@ __device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, i
         for (int a = 0; a < NM; ++a) {
             if (dva[a] == 0.0) continue;
             int ord = d.face_order;
-            if (ord == 2 && NM == 2 && d.degrade &&
+            if (ord == 2 && NM >= 2 && d.degrade &&
                 (T.kk[a][cm] < 1.0 - kPureTol || T.kk[a][cc] < 1.0 - kPureTol || T.kk[a][cp] < 1.0 - kPureTol))
                 ord = 1;
             double rf, ef;
@@ -959,7 +1006,7 @@ __device__ __forceinline__ double corner_item_t(const Dev& d, const Tile<NM>& T,
     const int qn = T.n(i, j);
     int sx, sy;
     const double cdv = T.cfv(qn, dt, sx, sy);
-    double dva[2] = {0.0, 0.0}, rfv[2] = {0.0, 0.0}, efv[2] = {0.0, 0.0};
+    double dva[NM] = {}, rfv[NM] = {}, efv[NM] = {};
     double dmtot = 0.0;
     if (cdv != 0.0) {
         const int di = sx > 0 ? i - 1 : i, dj = sy > 0 ? j - 1 : j;
@@ -976,7 +1023,7 @@ __device__ __forceinline__ double corner_item_t(const Dev& d, const Tile<NM>& T,
         for (int a = 0; a < NM; ++a) {
             if (dva[a] == 0.0) continue;
             bool lin = lin_cfg;
-            if (lin && NM == 2 && d.degrade) {
+            if (lin && NM >= 2 && d.degrade) {
                 for (int q = -1; q <= 1 && lin; ++q)
                     for (int p = -1; p <= 1; ++p)
                         if (T.kk[a][T.c(di + p, dj + q)] < 1.0 - kPureTol) {
@@ -1096,7 +1143,78 @@ __device__ __forceinline__ void finalize_cell(const Dev& d, const Rng& rg, int i
                                               uint32_t ph_negmass = PH_NEGMASS) {
     double k[2] = {1.0, 0.0};
     uint8_t sl = 0;
-    if (NM == 2) {
+    if (NM == 3) {  // the three-material finalize (oracle finalize_cells, nmat == 3)
+        int r = -1;  // a material with an exactly zero remapped volume: the two-material rule
+        for (int a = NM - 1; a >= 0 && r < 0; --a)
+            if (va[a] == 0.0) r = a;
+        double kk[3];
+        if (r >= 0) {
+            const int lo = r == 0 ? 1 : 0, hi = r == 2 ? 1 : 2;
+            double k0 = div_cv(d, va[lo]);
+            const double k1 = div_cv(d, va[hi]);
+            double viol = 0.0;
+            const double cand[5] = {-k0, k0 - 1.0, -k1, k1 - 1.0, fabs(k0 + k1 - 1.0)};
+#pragma unroll
+            for (int q = 0; q < 5; ++q)
+                if (viol < cand[q]) viol = cand[q];
+            if (viol > 0.0 && own) bump_kviol(d.ctl, viol);
+            if (k0 < 0.0 || k0 > 1.0) {
+                if (own) bump_clip(d.ctl);
+                k0 = (k0 < 0.0) ? 0.0 : ((1.0 < k0) ? 1.0 : k0);
+            }
+            if (k0 < kPureTol) k0 = 0.0;
+            if (k0 > 1.0 - kPureTol) k0 = 1.0;
+            kk[lo] = k0;
+            kk[hi] = 1.0 - k0;
+            kk[r] = 0.0;
+        } else {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) kk[a] = div_cv(d, va[a]);
+            double viol = 0.0;
+            const double cand[7] = {-kk[0], kk[0] - 1.0, -kk[1], kk[1] - 1.0, -kk[2], kk[2] - 1.0,
+                                    fabs(kk[0] + kk[1] + kk[2] - 1.0)};
+#pragma unroll
+            for (int q = 0; q < 7; ++q)
+                if (viol < cand[q]) viol = cand[q];
+            if (viol > 0.0 && own) bump_kviol(d.ctl, viol);
+            bool clipped = false;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (kk[a] < 0.0 || kk[a] > 1.0) {
+                    clipped = true;
+                    kk[a] = (kk[a] < 0.0) ? 0.0 : ((1.0 < kk[a]) ? 1.0 : kk[a]);
+                }
+                if (kk[a] < kPureTol) kk[a] = 0.0;
+                if (kk[a] > 1.0 - kPureTol) kk[a] = 1.0;
+            }
+            if (clipped && own) bump_clip(d.ctl);
+            kk[2] = (1.0 - kk[0]) - kk[1];
+            if (kk[2] < kPureTol) {
+                kk[2] = 0.0;
+                kk[1] = 1.0 - kk[0];
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if ((kk[a] == 0.0 && m[a] != 0.0) || m[a] < 0.0) {
+                sl |= (uint8_t)(1u << a);
+                d.slm[a][c] = m[a];
+                d.slme[a][c] = me[a];
+                m[a] = 0.0;
+                me[a] = 0.0;
+                if (kk[a] > 0.0) {  // a negative mass with volume left behind
+                    const int b = largest_other3(kk, a);
+                    if (r >= 0 && a != r)
+                        kk[3 - r - a] = 1.0;  // the reference's partner on the pair
+                    else
+                        kk[b] = kk[b] + kk[a];
+                    kk[a] = 0.0;
+                }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) d.nk[a][c] = kk[a];
+    } else if (NM == 2) {
         double k0 = div_cv(d, va[0]);
         const double k1 = div_cv(d, va[1]);
         double viol = 0.0;
@@ -1143,10 +1261,10 @@ __device__ __forceinline__ void finalize_cell(const Dev& d, const Rng& rg, int i
         d.ne[a][c] = ma > 0.0 ? me[a] / ma : 0.0;
         mtot += ma;
     }
-    if (bad_sub < 0 && mtot <= 0.0) bad_sub = 2;
+    if (bad_sub < 0 && mtot <= 0.0) bad_sub = kSubCellMass;
     if (bad_sub >= 0 && own) raise(d.ctl, ekey(ph_negmass, j, i, bad_sub));
     d.mcell[c] = mtot;
-    if (NM == 2) {
+    if (NM >= 2) {
         d.sliver[c] = sl;
         if (sl) {  // index the sliver for k_slivers (row bit + segment bit)
             const int jr = j - rg.j0, ir = i - rg.i0;
@@ -1187,7 +1305,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 template <int NM>
-__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
+__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
     pdl_enter();
     extern __shared__ __align__(128) char smem_raw[];
     __shared__ int s_halt;
@@ -1225,7 +1343,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
         for (int a = 0; a < NM; ++a) {
             tma_load_2d(T.el[a], &tm.t[TM_EL0 + a], x, y, &s_bar);
             tma_load_2d(T.rho[a], &tm.t[TM_M0 + a], x, y, &s_bar);
-            tma_load_2d(NM == 2 ? T.kk[a] : T.vl, &tm.t[TM_K0 + a], x, y, &s_bar);
+            tma_load_2d(NM >= 2 ? T.kk[a] : T.vl, &tm.t[TM_K0 + a], x, y, &s_bar);
         }
     }
     const double dt = step_dt(d.ctl);
@@ -1261,14 +1379,14 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
             const int i = i0 + tx, j = j0 + ty;
             if (!in(rg, i, j)) return;
             const int c = ix(d, i, j);
-            double m[2], me[2], va[2];
-#pragma unroll
+            double m[NM], me[NM], va[NM];
             const int tc = T.c(i, j);
+#pragma unroll
             for (int a = 0; a < NM; ++a) {
                 const double m0 = T.rho[a][tc];
                 m[a] = m0;
                 me[a] = m0 * T.el[a][tc];
-                va[a] = (NM == 2 ? T.kk[a][tc] : T.vl[tc]) * cv;
+                va[a] = (NM >= 2 ? T.kk[a][tc] : T.vl[tc]) * cv;
             }
             finalize_cell<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va);
             return;
@@ -1329,7 +1447,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
         if (v <= 0.0 && own_cell(d, i, j)) raise(d.ctl, ekey(PH_COLLAPSED, j, i, 0));
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
-            const double ka = NM == 2 ? T.kk[a][t] : T.vl[t];
+            const double ka = NM >= 2 ? T.kk[a][t] : T.vl[t];
             const double ma = T.rho[a][t];
             T.rho[a][t] = ka > 0.0 ? ma / (ka * v) : 0.0;
         }
@@ -1338,10 +1456,18 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
         const double mdy = 0.25 * (dt * T.hy[q00] + dt * T.hy[q10] + dt * T.hy[q01] + dt * T.hy[q11]);
         T.xl2x[t] = (d.x0 + (i + 0.5) * d.dx) + mdx;
         T.xl2y[t] = (d.y0 + (j + 0.5) * d.dy) + mdy;
-        if (NM == 2) {
-            const double k0 = T.kk[0][t];
+        if (NM >= 2) {
+            double k0 = T.kk[0][t];
+            bool mixed = is_mixed(k0);
+            if (NM == 3) {  // the interface of the pair (pair3), fraction of its lower material
+                const double k[3] = {T.kk[0][t], T.kk[1][t], T.kk[NM - 1][t]};
+                mixed = mixed3(k);
+                int lo, hi;
+                pair3(k, lo, hi);
+                k0 = k[3 - lo - hi] > 0.0 ? k[lo] / (k[lo] + k[hi]) : k[lo];
+            }
             double dd = 0.0;
-            if (is_mixed(k0)) {
+            if (mixed) {
                 const double cx = d.x0 + (i + 0.5) * d.dx, cy = d.y0 + (j + 0.5) * d.dy;
                 const int g = ix(d, i, j);
                 dd = place_interface(k0, d.nrx[g], d.nry[g], cx - 0.5 * d.dx + T.fdx[q00],
@@ -1361,7 +1487,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
     const bool act = in(rg, i, j);
     const int c = ix(d, i, j);
     const int tc = T.c(i, j);
-    double m[2], me[2], va[2];
+    double m[NM], me[NM], va[NM];
     if (act) {
         const double vl = T.vl[tc];
 #pragma unroll
@@ -1385,12 +1511,12 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
             va[a] += dv;
         }
     };
-    double dm[2], dme[2], dva[2];
+    double dm[NM], dme[NM], dva[NM];
     RowCol<RTX + 1, RTX * RTY> rs4(tid);
     for (int t = tid; t < NXF; t += RTX * RTY, rs4.step()) {  // X faces ia in [i0, i0+RTX], rows [j0, j0+RTY)
         const int ia = i0 + rs4.c, ic = j0 + rs4.r;
-        dva[0] = dva[1] = 0.0;
-        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) dva[a] = dm[a] = dme[a] = 0.0;
         if (ia <= min(nx, rg.i1) && ic < min(ny, rg.j1)) {
             const double tot = face_item_t<NM, 1>(d, T, ia, ic, dt, dm, dme, dva);
             if (ia < i0 + RTX || ia == min(nx, rg.i1)) d.dmx[ix(d, ia, ic)] = tot;
@@ -1414,8 +1540,8 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
     __syncthreads();
     for (int t = tid; t < NYF; t += RTX * RTY) {  // Y faces: columns [i0, i0+RTX), ja in [j0, j0+RTY]
         const int ic = i0 + t % RTX, ja = j0 + t / RTX;
-        dva[0] = dva[1] = 0.0;
-        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) dva[a] = dm[a] = dme[a] = 0.0;
         if (ic < min(nx, rg.i1) && ja <= min(ny, rg.j1)) {
             const double tot = face_item_t<NM, 0>(d, T, ic, ja, dt, dm, dme, dva);
             if (ja < j0 + RTY || ja == min(ny, rg.j1)) d.dmy[ix(d, ic, ja)] = tot;
@@ -1440,8 +1566,8 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : 3) k_remap_tile(Dev d
     RowCol<RTX + 1, RTX * RTY> rs5(tid);
     for (int t = tid; t < NCF; t += RTX * RTY, rs5.step()) {  // corner nodes [i0, i0+RTX] x [j0, j0+RTY]
         const int ni = i0 + rs5.c, nj = j0 + rs5.r;
-        dva[0] = dva[1] = 0.0;
-        dm[0] = dm[1] = dme[0] = dme[1] = 0.0;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) dva[a] = dm[a] = dme[a] = 0.0;
         const int ni1 = min(nx, rg.i1), nj1 = min(ny, rg.j1);
         if (ni <= ni1 && nj <= nj1) {
             const double tot = corner_item_t<NM>(d, T, ni, nj, dt, dm, dme, dva);
@@ -1516,14 +1642,17 @@ __device__ __forceinline__ void sliver_offset(int lane, int& di, int& dj, int& r
 //    at shuffle speed instead of one memory round trip per sliver.
 constexpr int SLB = 256, SLROWS = 4096, SLD = 4;
 
+template <int NM>
 struct SliverRec {
     int sc, fl, nc, own;       // cell, flags, this lane's candidate cell, own-cell flag
-    double sm[2], sme[2];      // sliver masses (remap.cpp:172)
-    double mv[2], kv[2], mev[2], mcv;  // candidate m, k, me per material, mcell
+    double sm[NM], sme[NM];    // sliver masses (remap.cpp:172)
+    double mv[NM], kv[NM], mev[NM], mcv;  // candidate m, k, me per material, mcell
+    int part[NM];              // the orphan's partner material (remap.cpp:217-225; 3 materials: largest other k)
 };
 
+template <int NM>
 __device__ __forceinline__ void sliver_load(const Dev& d, const Rng& rg, int v, int lane, int di, int dj,
-                                            SliverRec& r) {
+                                            SliverRec<NM>& r) {
     const int W = rg.i1 - rg.i0;  // v = (j - rg.j0) * W + (i - rg.i0)
     const int sj = rg.j0 + v / W, si = rg.i0 + v % W;
     const int c = ix(d, si, sj);
@@ -1536,8 +1665,16 @@ __device__ __forceinline__ void sliver_load(const Dev& d, const Rng& rg, int v, 
     r.nc = inb ? ix(d, ni, nj) : -1;
     r.fl = d.sliver[c];
     r.mcv = 0.0;
+    if (NM == 3) {
+        const double k3[3] = {d.nk[0][c], d.nk[1][c], d.nk[NM - 1][c]};
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < NM; ++a) r.part[a] = largest_other3(k3, a);
+    } else {
+#pragma unroll
+        for (int a = 0; a < NM; ++a) r.part[a] = 1 - a;
+    }
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
         r.sm[a] = d.slm[a][c];
         r.sme[a] = d.slme[a][c];
         r.mv[a] = 0.0;
@@ -1553,29 +1690,30 @@ __device__ __forceinline__ void sliver_load(const Dev& d, const Rng& rg, int v, 
 }
 
 // a write of (m, me of material a, mcell) to cell w, seen by a pending record
-__device__ __forceinline__ void sliver_patch(SliverRec& r, int w, int a, double nm, double nme, double nmc) {
+template <int NM>
+__device__ __forceinline__ void sliver_patch(SliverRec<NM>& r, int w, int a, double nm, double nme, double nmc) {
     if (r.nc == w) {
-        if (a == 0) {
-            r.mv[0] = nm;
-            r.mev[0] = nme;
-        } else {
-            r.mv[1] = nm;
-            r.mev[1] = nme;
-        }
+#pragma unroll
+        for (int b = 0; b < NM; ++b)
+            if (b == a) {
+                r.mv[b] = nm;
+                r.mev[b] = nme;
+            }
         r.mcv = nmc;
     }
 }
 
 // Apply one pending record (both of its materials, a = 0 first as the
 // reference pushes them, remap.cpp:170-181); returns nothing, patches `p1..p3`.
-__device__ __forceinline__ void sliver_apply_rec(const Dev& d, SliverRec& r, int lane, int ring, SliverRec& p1,
-                                                 SliverRec& p2, SliverRec& p3) {
+template <int NM>
+__device__ __forceinline__ void sliver_apply_rec(const Dev& d, SliverRec<NM>& r, int lane, int ring,
+                                                 SliverRec<NM>& p1, SliverRec<NM>& p2, SliverRec<NM>& p3) {
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NM; ++a) {
         if (!(r.fl & (1 << a))) continue;
-        const double mv = a ? r.mv[1] : r.mv[0], kv = a ? r.kv[1] : r.kv[0];
-        const double mev = a ? r.mev[1] : r.mev[0];
-        const double smv = a ? r.sm[1] : r.sm[0], smev = a ? r.sme[1] : r.sme[0];
+        const double mv = r.mv[a], kv = r.kv[a];
+        const double mev = r.mev[a];
+        const double smv = r.sm[a], smev = r.sme[a];
         const bool cand = kv > -1.0 && !(mv <= 0.0);  // the reference skips m <= 0, then needs k > bk
         int br = cand ? ring : 4, bl = lane;
         double bkv = kv;
@@ -1610,7 +1748,7 @@ __device__ __forceinline__ void sliver_apply_rec(const Dev& d, SliverRec& r, int
             }
         } else {  // no carrier: the partner material at the sliver's own cell (:217-225)
             w = r.sc;
-            wa = 1 - a;
+            wa = r.part[a];
             src = 0;
             if (lane == 0) {  // rare: fresh loads (memory is current after the __syncwarp)
                 if (r.own) d.ctl->step_fix += 1;
@@ -1662,6 +1800,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
     return r;
 }
 
+template <int NM>
 __global__ void __launch_bounds__(SLB, 1) k_slivers(Dev d) {
     pdl_enter();
     __shared__ int s_halt, s_total;
@@ -1745,7 +1884,7 @@ __global__ void __launch_bounds__(SLB, 1) k_slivers(Dev d) {
         // (5) one warp applies them in order, SLD records in flight
         if (wid == 0) {
             const int n = s_total;
-            SliverRec r0v, r1v, r2v, r3v;
+            SliverRec<NM> r0v, r1v, r2v, r3v;
             if (0 < n) sliver_load(d, rg, d.sl_list[0], lane, di, dj, r0v);
             if (1 < n) sliver_load(d, rg, d.sl_list[1], lane, di, dj, r1v);
             if (2 < n) sliver_load(d, rg, d.sl_list[2], lane, di, dj, r2v);
@@ -2178,7 +2317,17 @@ __global__ void k_normals(Dev d, int api) {
         nx_[c] = d.nrx[c];
         ny_[c] = d.nry[c];
     }
-    if (!is_mixed(k0[c])) return;
+    if (d.nmat == 3) {  // three materials: the interface pair's k_hi (pair3)
+        const double* kf[3];
+        for (int a = 0; a < 3; ++a) kf[a] = api ? d.k[a] : d.nk[a];
+        const double k3[3] = {kf[0][c], kf[1][c], kf[2][c]};
+        if (!mixed3(k3)) return;
+        int lo, hi;
+        pair3(k3, lo, hi);
+        k1 = kf[hi];
+    } else if (!is_mixed(k0[c])) {
+        return;
+    }
     auto K = [&](int ii, int jj) { return k1[ix(d, ii, jj)]; };
     auto col = [&](int ii) { return K(ii, j - 1) + 2.0 * K(ii, j) + K(ii, j + 1); };
     auto row = [&](int jj) { return K(i - 1, jj) + 2.0 * K(i, jj) + K(i + 1, jj); };
@@ -2377,7 +2526,7 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
     const bool interior = i >= 0 && j >= 0 && i < nx && j < ny;
     const int c = ix(d, i, j);
     const double cv = d.cv;
-    double ka[2], ma[2], ea[2];
+    double ka[NM], ma[NM], ea[NM];
     double m = 0.0, emix = 0.0, p = 0.0;
     if (act) {
 #pragma unroll
@@ -2413,7 +2562,8 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
         s_dg[DG_MASS][tl] = on ? m : 0.0;
         s_dg[DG_IE][tl] = on ? m * emix : 0.0;
         s_dg[DG_MM0][tl] = on ? ma[0] : 0.0;
-        s_dg[DG_MM1][tl] = on && NM == 2 ? ma[NM - 1] : 0.0;
+        s_dg[DG_MM1][tl] = on && NM >= 2 ? ma[NM >= 2 ? 1 : 0] : 0.0;
+        s_dg[DG_MM2][tl] = on && NM == 3 ? ma[NM - 1] : 0.0;
         s_dg[DG_MINR][tl] = on ? rho : CUDART_INF;
         s_dg[DG_MAXR][tl] = on ? rho : -CUDART_INF;
         s_dg[DG_MINP][tl] = on ? p : CUDART_INF;
@@ -2421,10 +2571,19 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
     }
     if (act) {
         if (interior && in(d.r_nrm, i, j)) {
-            if (NM == 2) {  // normals of the new fractions
+            if (NM >= 2) {  // normals of the new fractions
                 double nrx = d.nrx[c], nry = d.nry[c];
-                if (is_mixed(ka[0])) {
-                    auto K = [&](int ii, int jj) { return d.nk[1][ix(d, ii, jj)]; };
+                bool mixed = is_mixed(ka[0]);
+                int hi = 1;
+                if (NM == 3) {  // Youngs normal of the interface pair's k_hi (pair3)
+                    const double k3[3] = {ka[0], ka[1], ka[NM - 1]};
+                    mixed = mixed3(k3);
+                    int lo;
+                    pair3(k3, lo, hi);
+                }
+                if (mixed) {
+                    const double* kh = d.nk[hi];
+                    auto K = [&](int ii, int jj) { return kh[ix(d, ii, jj)]; };
                     auto col = [&](int ii) { return K(ii, j - 1) + 2.0 * K(ii, j) + K(ii, j + 1); };
                     auto row = [&](int jj) { return K(i - 1, jj) + 2.0 * K(i, jj) + K(i + 1, jj); };
                     const double gx = div_dx(d, col(i + 1) - col(i - 1), 8.0);
@@ -2474,16 +2633,16 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
             for (int w = 1; w < (int)(blockDim.x * blockDim.y) / 32; ++w) wb = sw[w] > wb ? sw[w] : wb;
             if (wb) atomicMax(&d.ctl->next_wmax_bits, wb);
         }
-        if (d.diag) {  // warp k folds diagnostics value k over the block's 256 cells (fixed order)
-            const int k = t >> 5, lane = t & 31;
-            const int op = (k == DG_MINR || k == DG_MINP) ? 1 : ((k == DG_MAXR || k == DG_MAXP) ? 2 : 0);
-            double v = s_dg[k][lane];
+        if (d.diag)  // warp w folds diagnostics values w, w + 8 over the block's 256 cells (fixed order)
+            for (int k = t >> 5; k < DG_NCELL; k += 8) {
+                const int lane = t & 31, op = dg_op(k);
+                double v = s_dg[k][lane];
 #pragma unroll
-            for (int q = 1; q < 8; ++q) v = dg_comb(op, v, s_dg[k][lane + 32 * q]);
+                for (int q = 1; q < 8; ++q) v = dg_comb(op, v, s_dg[k][lane + 32 * q]);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v = dg_comb(op, v, __shfl_down_sync(0xffffffffu, v, o));
-            if (lane == 0) d.dsc.part[0][((size_t)blockIdx.y * gridDim.x + blockIdx.x) * DG_NCELL + k] = v;
-        }
+                for (int o = 16; o > 0; o >>= 1) v = dg_comb(op, v, __shfl_down_sync(0xffffffffu, v, o));
+                if (lane == 0) d.dsc.part[0][((size_t)blockIdx.y * gridDim.x + blockIdx.x) * DG_NCELL + k] = v;
+            }
     }
 }
 
@@ -2744,7 +2903,9 @@ __global__ void __launch_bounds__(256) k_tail(Dev d, FieldList cells, FieldList 
     __syncthreads();
     const bool halt = s_flag;
     const int b = blockIdx.x, ncomb = cells.n + nodes.n / 2;
-    const int op[DG_N] = {0, 0, 0, 0, 1, 2, 1, 2, 0, 0};
+    int op[DG_N];
+#pragma unroll
+    for (int k = 0; k < DG_N; ++k) op[k] = dg_op(k);
     const DiagScratch& r = d.dsc;
     if (b < nb1 * ncomb) {
         if (!halt) {
@@ -2983,7 +3144,9 @@ void launch_cfl(const Dev& d, int run_loop, cudaStream_t s) {
     const long long ncell = (long long)d.nx * d.ny;
     unsigned nb = nblk(ncell, 256);
     if (nb > 148u * 8u) nb = 148u * 8u;
-    if (d.nmat == 2)
+    if (d.nmat == 3)
+        { k_cfl<3><<<nb, 256, 0, s>>>(d, 0); ++g_launches; }
+    else if (d.nmat == 2)
         { k_cfl<2><<<nb, 256, 0, s>>>(d, 0); ++g_launches; }
     else
         { k_cfl<1><<<nb, 256, 0, s>>>(d, 0); ++g_launches; }
@@ -3015,7 +3178,9 @@ void launch_ghost_nodes(const Dev& d, const FieldList& fl, cudaStream_t s) {
 
 void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s) {
     const dim3 g = grid_of(d.win_c);
-    if (d.nmat == 2)
+    if (d.nmat == 3)
+        { k_sync<3><<<g, blk2(), 0, s>>>(d, next, respect_halt); ++g_launches; }
+    else if (d.nmat == 2)
         { k_sync<2><<<g, blk2(), 0, s>>>(d, next, respect_halt); ++g_launches; }
     else
         { k_sync<1><<<g, blk2(), 0, s>>>(d, next, respect_halt); ++g_launches; }
@@ -3024,7 +3189,9 @@ void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s) {
 void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
     const dim3 gc = grid_of(d.r_lagc);
     const dim3 gl = tiles_of(d.r_lagn, LTX, LTY);
-    if (d.nmat == 2)
+    if (d.nmat == 3)
+        { k_lag_cells<3><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
+    else if (d.nmat == 2)
         { k_lag_cells<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
     else
         { k_lag_cells<1><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
@@ -3034,7 +3201,9 @@ void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
     fl.f[0] = d.q;
     fl.f[1] = d.pmh;
     launch_ghost_cells(d, fl, s);
-    if (d.nmat == 2)
+    if (d.nmat == 3)
+        { k_lag_nodes<3><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag); ++g_launches; }
+    else if (d.nmat == 2)
         { k_lag_nodes<2><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag); ++g_launches; }
     else
         { k_lag_nodes<1><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag); ++g_launches; }
@@ -3045,8 +3214,7 @@ void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
     fn.f[2] = d.ulx;
     fn.f[3] = d.uly;
     fl.n = d.nmat;
-    fl.f[0] = d.el[0];
-    fl.f[1] = d.el[1];
+    for (int a = 0; a < d.nmat; ++a) fl.f[a] = d.el[a];
     launch_ghost_multi(d, fl, fn, 0, 1, s);
 }
 
@@ -3055,6 +3223,7 @@ void remap_init() {
     if (done) return;
     cudaFuncSetAttribute(k_remap_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<1>());
     cudaFuncSetAttribute(k_remap_tile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<2>());
+    cudaFuncSetAttribute(k_remap_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<3>());
     done = true;
 }
 
@@ -3067,7 +3236,9 @@ void post_and_ghosts(const Dev& d, int run_loop, cudaStream_t s) {
 
 void launch_post(const Dev& d, int run_loop, cudaStream_t s) {
     const dim3 gp = tiles_of(d.r_sync, 32, 8);
-    if (d.nmat == 2)
+    if (d.nmat == 3)
+        pdl(k_post<3>, gp, dim3(32, 8), 0, s, d, run_loop);
+    else if (d.nmat == 2)
         pdl(k_post<2>, gp, dim3(32, 8), 0, s, d, run_loop);
     else
         pdl(k_post<1>, gp, dim3(32, 8), 0, s, d, run_loop);
@@ -3119,7 +3290,9 @@ void launch_lagrange_run(const Dev& d, cudaStream_t s) {
 }
 
 void launch_lag_fused(const Dev& d, cudaStream_t s) {
-    if (d.nmat == 2)
+    if (d.nmat == 3)
+        pdl(k_lag_fused<3>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(LTX * H2D_FTY), 0, s, d);
+    else if (d.nmat == 2)
         pdl(k_lag_fused<2>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(LTX * H2D_FTY), 0, s, d);
     else
         pdl(k_lag_fused<1>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(LTX * H2D_FTY), 0, s, d);
@@ -3134,8 +3307,7 @@ void launch_lag_ghosts(const Dev& d, cudaStream_t s) {
     fn.f[3] = d.uly;
     FieldList fl{};
     fl.n = d.nmat;
-    fl.f[0] = d.el[0];
-    fl.f[1] = d.el[1];
+    for (int a = 0; a < d.nmat; ++a) fl.f[a] = d.el[a];
     launch_ghost_multi(d, fl, fn, 0, 1, s);
 }
 
@@ -3157,7 +3329,9 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
     Rng rt = d.r_gath;
     rt.i0 -= tile_shift(d);
     const dim3 gft = tiles_of(rt, RTX, RTY);
-    if (d.nmat == 2)
+    if (d.nmat == 3)
+        pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
+    else if (d.nmat == 2)
         pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
     else
         pdl(k_remap_tile<1>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
@@ -3165,7 +3339,10 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
 
 // slivers + finalize_cells ghost fill + flux ghosts
 void launch_remap_slivers(const Dev& d, cudaStream_t s) {
-    if (d.nmat == 2) pdl(k_slivers, dim3(1), dim3(SLB), 0, s, d);
+    if (d.nmat == 3)
+        pdl(k_slivers<3>, dim3(1), dim3(SLB), 0, s, d);
+    else if (d.nmat == 2)
+        pdl(k_slivers<2>, dim3(1), dim3(SLB), 0, s, d);
     // finalize_cells ghost fill (remap.cpp:227-233) + face / corner flux ghosts
     FieldList fl{};
     int q = 0;
@@ -3316,7 +3493,9 @@ void launch_cfl_next(const Dev& d, cudaStream_t s) {
     const long long ncell = (long long)d.nx * d.ny;
     unsigned nb = nblk(ncell, 256);
     if (nb > 148u * 8u) nb = 148u * 8u;
-    if (d.nmat == 2)
+    if (d.nmat == 3)
+        { k_cfl<3><<<nb, 256, 0, s>>>(d, 1); ++g_launches; }
+    else if (d.nmat == 2)
         { k_cfl<2><<<nb, 256, 0, s>>>(d, 1); ++g_launches; }
     else
         { k_cfl<1><<<nb, 256, 0, s>>>(d, 1); ++g_launches; }
