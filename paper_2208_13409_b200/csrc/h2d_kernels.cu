@@ -2513,7 +2513,10 @@ template <int NM>
 __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
     pdl_enter();
     __shared__ unsigned long long sw[8];
-    __shared__ double s_dg[DG_NCELL][256];  // per-thread diagnostics terms (block of 32 x 8)
+    // per-thread diagnostics terms (block of 32 x 8); fewer than three
+    // materials keep no DG_MM2 plane (its partial is written as 0)
+    constexpr int NDG = NM == 3 ? DG_NCELL : DG_NCELL - 1;
+    __shared__ double s_dg[NDG][256];
     __shared__ int s_halt;
     if (threadIdx.x == 0 && threadIdx.y == 0) s_halt = halted(d.ctl);
     __syncthreads();
@@ -2559,15 +2562,16 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
     if (run_loop && d.diag) {
         const bool on = act && interior && own_cell(d, i, j);
         const double rho = div_cv(d, m);
+        constexpr int sh = NM == 3 ? 0 : 1;  // plane of slot k >= DG_MINR: k - sh
         s_dg[DG_MASS][tl] = on ? m : 0.0;
         s_dg[DG_IE][tl] = on ? m * emix : 0.0;
         s_dg[DG_MM0][tl] = on ? ma[0] : 0.0;
         s_dg[DG_MM1][tl] = on && NM >= 2 ? ma[NM >= 2 ? 1 : 0] : 0.0;
-        s_dg[DG_MM2][tl] = on && NM == 3 ? ma[NM - 1] : 0.0;
-        s_dg[DG_MINR][tl] = on ? rho : CUDART_INF;
-        s_dg[DG_MAXR][tl] = on ? rho : -CUDART_INF;
-        s_dg[DG_MINP][tl] = on ? p : CUDART_INF;
-        s_dg[DG_MAXP][tl] = on ? p : -CUDART_INF;
+        if (NM == 3) s_dg[NM == 3 ? DG_MM2 : 0][tl] = on ? ma[NM - 1] : 0.0;
+        s_dg[DG_MINR - sh][tl] = on ? rho : CUDART_INF;
+        s_dg[DG_MAXR - sh][tl] = on ? rho : -CUDART_INF;
+        s_dg[DG_MINP - sh][tl] = on ? p : CUDART_INF;
+        s_dg[DG_MAXP - sh][tl] = on ? p : -CUDART_INF;
     }
     if (act) {
         if (interior && in(d.r_nrm, i, j)) {
@@ -2633,16 +2637,20 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
             for (int w = 1; w < (int)(blockDim.x * blockDim.y) / 32; ++w) wb = sw[w] > wb ? sw[w] : wb;
             if (wb) atomicMax(&d.ctl->next_wmax_bits, wb);
         }
-        if (d.diag)  // warp w folds diagnostics values w, w + 8 over the block's 256 cells (fixed order)
-            for (int k = t >> 5; k < DG_NCELL; k += 8) {
+        if (d.diag) {  // warp w folds diagnostics planes w, w + 8 over the block's 256 cells (fixed order)
+            double* part = d.dsc.part[0] + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * DG_NCELL;
+            for (int pl = t >> 5; pl < NDG; pl += 8) {
+                const int k = (NM == 3 || pl < DG_MM2) ? pl : pl + 1;  // the slot of plane pl
                 const int lane = t & 31, op = dg_op(k);
-                double v = s_dg[k][lane];
+                double v = s_dg[pl][lane];
 #pragma unroll
-                for (int q = 1; q < 8; ++q) v = dg_comb(op, v, s_dg[k][lane + 32 * q]);
+                for (int q = 1; q < 8; ++q) v = dg_comb(op, v, s_dg[pl][lane + 32 * q]);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) v = dg_comb(op, v, __shfl_down_sync(0xffffffffu, v, o));
-                if (lane == 0) d.dsc.part[0][((size_t)blockIdx.y * gridDim.x + blockIdx.x) * DG_NCELL + k] = v;
+                if (lane == 0) part[k] = v;
             }
+            if (NM < 3 && t == 0) part[DG_MM2] = 0.0;
+        }
     }
 }
 
