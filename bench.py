@@ -30,7 +30,8 @@ import numpy as np  # noqa: E402
 
 METRIC = "cell-updates/s per full Lagrange+remap step (fp64)"
 UNIT = "cell-updates/s"
-B_MIN = {1: 64, 2: 160}  # algorithmic bytes per cell-step
+B_MIN = {1: 64, 2: 160, 3: 208}  # algorithmic bytes per cell-step (3 materials:
+#   m, e, k per material + normals + u = 13 fp64 read + written once)
 # Compulsory HBM bytes per cell of the three big kernels (their inputs read
 # once + outputs written once):
 #  k_lag_fused: reads m, e, k per material, u (2 nodal), m_mix, rho_mix;
@@ -41,9 +42,11 @@ B_MIN = {1: 64, 2: 160}  # algorithmic bytes per cell-step (BASELI
 #  k_post:      reads new m, e, k per material and |u| (+ old normals);
 #               writes m_mix, e_mix, rho_mix, p_mix, vol (+ normals).
 KERNEL_BYTES = {
-    "lagrange": ("k_lag_fused", {1: 8 * (3 + 4) + 8 * (4 + 1), 2: 8 * (6 + 4) + 8 * (4 + 2)}),
-    "remap_tile": ("k_remap_tile", {1: 8 * (2 + 3) + 8 * (4 + 1 + 3), 2: 8 * (2 + 6 + 2) + 8 * (8 + 1 + 3) + 1}),
-    "post": ("k_post", {1: 8 * (3 + 1) + 8 * 5, 2: 8 * (6 + 1 + 2) + 8 * (5 + 2)}),
+    "lagrange": ("k_lag_fused", {1: 8 * (3 + 4) + 8 * (4 + 1), 2: 8 * (6 + 4) + 8 * (4 + 2),
+                                 3: 8 * (9 + 4) + 8 * (4 + 3)}),
+    "remap_tile": ("k_remap_tile", {1: 8 * (2 + 3) + 8 * (4 + 1 + 3), 2: 8 * (2 + 6 + 2) + 8 * (8 + 1 + 3) + 1,
+                                    3: 8 * (2 + 9 + 2) + 8 * (12 + 1 + 3) + 1}),
+    "post": ("k_post", {1: 8 * (3 + 1) + 8 * 5, 2: 8 * (6 + 1 + 2) + 8 * (5 + 2), 3: 8 * (9 + 1 + 2) + 8 * (5 + 2)}),
 }
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0
@@ -59,6 +62,8 @@ def workload(name):
         return cases.triple_point(2048, 1024)
     if name == "c4":
         return cases.shock_bubble(8192)
+    if name == "c5":  # one GPU's block of the 8-GPU (4 x 2) decomposition of the 16384^2 problem
+        return cases.voronoi3(4096, 8192, n_full=16384)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -143,11 +148,12 @@ def barrier(pg):
         pg.barrier()
 
 
-def cpu_lib():
-    """Reference library (oracle/_ref) if built, else the C restatement."""
+def cpu_lib(nmat=1):
+    """Reference library (oracle/_ref) if built, else the C restatement (and
+    always for three materials, which the reference cannot hold)."""
     from paper_2208_13409_b200 import abi
     ref = os.path.join(ROOT, "oracle", "_ref", "libh2d_ref.so")
-    if os.path.exists(ref):
+    if os.path.exists(ref) and nmat <= 2:
         return abi.Library(ref, "h2dr_"), "reference"
     port = os.path.join(ROOT, "oracle", "libh2d_oracle.so")
     if not os.path.exists(port):
@@ -158,7 +164,7 @@ def cpu_lib():
 def time_cpu(case, warm, steps, remap_kind=None):
     """Wall-clock the CPU implementation on `steps` steps after `warm`."""
     from paper_2208_13409_b200 import abi
-    lib, lib_kind = cpu_lib()
+    lib, lib_kind = cpu_lib(case.cfg.nmat)
     rk = abi.REMAP_DIRECTCF if remap_kind is None else remap_kind
     s = abi.Solver(lib, case.cfg)
     s.init_from(case.paint())
@@ -324,7 +330,8 @@ def run_product(args, world, rank, local, pg):
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, ckind, n, secs = time_cpu(case, 0, args.cpu_steps, kind)
+        # a bounded sample: about 3e7 cell-updates (10-30 s of one core)
+        v, ckind, n, secs = time_cpu(case, 0, min(args.cpu_steps, max(1, int(3e7 // case.cells))), kind)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": ckind,
                                 "sample": f"{case.name}: first {n} steps from t=0, single thread, {secs:.1f} s"}
     if rank == 0:
@@ -425,7 +432,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--remap", default="directcf", choices=["directcf", "ad"],
                     help="remap engine: DirectCF (the path) or the AD split scheme (SURVEY 8f)")
     ap.add_argument("--cpu-steps", type=int, default=10)

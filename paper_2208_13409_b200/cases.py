@@ -403,15 +403,20 @@ class VoronoiCase(Case):
         return paint_voronoi3(self.cfg, self.sites)
 
 
-def voronoi3(nx: int = 16384, ny: Optional[int] = None, nsites: int = 64, seed: int = 20241005) -> Case:
+def voronoi3(nx: int = 16384, ny: Optional[int] = None, n_full: Optional[int] = None, nsites: int = 64,
+             seed: int = 20241005) -> Case:
     """Config 5: three-material Voronoi mesh on [0,1]^2 (gammas 1.4, 1.5,
     1.67 = materials 0, 1, 2), 64 seeded sites, 4x4 sampling of the cells the
     site boundaries cross, walls, CFL 0.3 (unstated in BASELINE.json), 100
-    steps. A non-square ny paints the lower part of the same unit-spaced
-    mesh (ny / nx of the height: the block of one GPU of a decomposition)."""
+    steps. With n_full > nx the mesh is the lower-left nx x ny block of the
+    n_full^2 mesh (cell size 1 / n_full, walls at the block edges): the share
+    of one GPU of the 8-GPU decomposition, which fits one B200 where the whole
+    16384^2 three-material problem does not."""
     ny = nx if ny is None else ny
+    n_full = nx if n_full is None else n_full
     eos = [(EOS_PERFECT, 1.4, 0.0), (EOS_PERFECT, 1.5, 0.0), (EOS_PERFECT, 1.67, 0.0)]
-    return VoronoiCase(f"voronoi3_{nx}x{ny}", _mesh_cfg(nx, ny, 1.0, ny / nx, eos), [], 0.3, 100,
+    name = f"voronoi3_{nx}x{ny}" + (f"_of_{n_full}" if n_full != nx else "")
+    return VoronoiCase(name, _mesh_cfg(nx, ny, nx / n_full, ny / n_full, eos), [], 0.3, 100,
                        sites=voronoi_sites(nsites, seed))
 
 
