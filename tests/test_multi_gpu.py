@@ -36,10 +36,10 @@ def _blocks(case, steps, px, py):
 
 
 @pytest.mark.parametrize("px,py", [(2, 1), (1, 2), (2, 2), (4, 2)])
-@pytest.mark.parametrize("which", ["riemann", "triple", "bubble"])
+@pytest.mark.parametrize("which", ["riemann", "triple", "bubble", "voronoi3"])
 def test_blocks_bitwise_equal_single_domain(which, px, py):
     case = {"riemann": cases.riemann2d(64), "triple": cases.triple_point(96, 48),
-            "bubble": cases.shock_bubble(64)}[which]
+            "bubble": cases.shock_bubble(64), "voronoi3": cases.voronoi3(128)}[which]
     steps = 40
     ref, r, err = _single(case, steps)
     got, results = _blocks(case, steps, px, py)
