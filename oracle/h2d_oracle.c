@@ -480,6 +480,115 @@ static double corner_linear_diag(ctx_t* c, const double a[3][3], const double xl
     return ac + 0.5 * gvp * (ex * vx + ey * vy);
 }
 
+/* CornerKin, reconstruct.hpp:44-51 (er = eval_rel) */
+typedef struct {
+    double dxp, dyp, lag_wx, lag_wy, sgn_fx, u_fx_dt, sgn_fy, u_fy_dt, erx, ery;
+} kin_t;
+static int sgn_i(double v) { return v > 0.0 ? 1 : (v < 0.0 ? -1 : 0); } /* reconstruct.cpp:35 */
+/* diag_gradient, reconstruct.cpp:38-42 */
+static double diag_gradient(ctx_t* c, const double a[3][3], const double xlx[3][3], const double xly[3][3],
+                            int im, int jm, int ip, int jp, double vx, double vy) {
+    const double sc = xlx[1][1] * vx + xly[1][1] * vy;
+    return limited_gradient_1d(c, a[im][jm], a[1][1], a[ip][jp], xlx[im][jm] * vx + xly[im][jm] * vy, sc,
+                               xlx[ip][jp] * vx + xly[ip][jp] * vy);
+}
+/* qr_solve_2col, reconstruct.cpp:45-72: Householder QR of the m x 2 system */
+static void qr_solve_2col(double X[8][2], double b[8], int m, double* g1, double* g2) {
+    for (int col = 0; col < 2; ++col) {
+        double nrm = 0.0;
+        for (int r = col; r < m; ++r) nrm += X[r][col] * X[r][col];
+        nrm = sqrt(nrm);
+        if (nrm < 1e-300) { *g1 = 0.0; *g2 = 0.0; return; }
+        const double alpha = X[col][col] > 0.0 ? -nrm : nrm;
+        double v[8];
+        v[col] = X[col][col] - alpha;
+        for (int r = col + 1; r < m; ++r) v[r] = X[r][col];
+        double vtv = 0.0;
+        for (int r = col; r < m; ++r) vtv += v[r] * v[r];
+        if (vtv > 0.0) {
+            for (int cc = col; cc < 2; ++cc) {
+                double sv = 0.0;
+                for (int r = col; r < m; ++r) sv += v[r] * X[r][cc];
+                sv *= 2.0 / vtv;
+                for (int r = col; r < m; ++r) X[r][cc] -= sv * v[r];
+            }
+            double sv = 0.0;
+            for (int r = col; r < m; ++r) sv += v[r] * b[r];
+            sv *= 2.0 / vtv;
+            for (int r = col; r < m; ++r) b[r] -= sv * v[r];
+        }
+    }
+    const double y2 = b[1] / X[1][1];
+    *g2 = y2;
+    *g1 = (b[0] - X[0][1] * y2) / X[0][0];
+}
+/* multid_plane, reconstruct.cpp:76-107: pl = {a0, centre, limited gradient} */
+typedef struct { double a0, cx, cy, gx, gy; } plane_t;
+static plane_t multid_plane(ctx_t* c, const double a[3][3], const double xlx[3][3], const double xly[3][3]) {
+    plane_t pl;
+    pl.a0 = a[1][1];
+    pl.cx = xlx[1][1];
+    pl.cy = xly[1][1];
+    double X[8][2], b[8];
+    int m = 0;
+    for (int p = 0; p < 3; ++p)
+        for (int q = 0; q < 3; ++q) {
+            if (p == 1 && q == 1) continue;
+            X[m][0] = xlx[p][q] - pl.cx;
+            X[m][1] = xly[p][q] - pl.cy;
+            b[m] = a[p][q] - pl.a0;
+            ++m;
+        }
+    double grx, gry;
+    qr_solve_2col(X, b, m, &grx, &gry);
+    const double gnorm = sqrt(grx * grx + gry * gry);
+    if (gnorm < 1e-300) {
+        pl.gx = 0.0;
+        pl.gy = 0.0;
+        return pl;
+    }
+    const double dx = c->dx, dy = c->dy;
+    const double diag = sqrt(dx * dx + dy * dy);
+    const double vx = dx / diag, vy = dy / diag, vpx = dx / diag, vpy = -dy / diag;
+    const double gx = limited_gradient_1d(c, a[0][1], a[1][1], a[2][1], xlx[0][1], xlx[1][1], xlx[2][1]);
+    const double gy = limited_gradient_1d(c, a[1][0], a[1][1], a[1][2], xly[1][0], xly[1][1], xly[1][2]);
+    const double gv = diag_gradient(c, a, xlx, xly, 0, 0, 2, 2, vx, vy);
+    const double gvp = diag_gradient(c, a, xlx, xly, 0, 2, 2, 0, vpx, vpy);
+    const double phi = ref_min(ref_min(fabs(gx), fabs(gy)), ref_min(fabs(gv), fabs(gvp))) / gnorm;
+    pl.gx = phi * grx;
+    pl.gy = phi * gry;
+    return pl;
+}
+/* plane_eval, reconstruct.hpp:67-69 */
+static double plane_eval(const plane_t* pl, double x, double y) {
+    return pl->a0 + (pl->gx * (x - pl->cx) + pl->gy * (y - pl->cy));
+}
+/* corner_value, reconstruct.cpp:116-152 (every corner scheme) */
+static double corner_value(ctx_t* c, int scheme, const double a[3][3], const double xlx[3][3],
+                           const double xly[3][3], const kin_t* k) {
+    const double ac = a[1][1];
+    switch (scheme) {
+    case H2D_CORNER_AVGMIN: {
+        const int sx = sgn_i(k->dxp), sy = sgn_i(k->dyp);
+        const double pair_avg = 0.5 * (ac + a[1 + sx][1 + sy]);
+        return ref_min(ac, pair_avg);
+    }
+    case H2D_CORNER_LINEARXY: {
+        const double gx = limited_gradient_1d(c, a[0][1], ac, a[2][1], xlx[0][1], xlx[1][1], xlx[2][1]);
+        const double gy = limited_gradient_1d(c, a[1][0], ac, a[1][2], xly[1][0], xly[1][1], xly[1][2]);
+        return ac + 0.5 * gx * (k->sgn_fx * k->lag_wx - k->u_fx_dt) + 0.5 * gy * (k->sgn_fy * k->lag_wy - k->u_fy_dt);
+    }
+    case H2D_CORNER_LINEARDIAG:
+        return corner_linear_diag(c, a, xlx, xly, k->dxp, k->dyp, k->lag_wx, k->lag_wy);
+    case H2D_CORNER_MULTID: {
+        const plane_t pl = multid_plane(c, a, xlx, xly);
+        return pl.a0 + (pl.gx * k->erx + pl.gy * k->ery);
+    }
+    default:
+        return ac;
+    }
+}
+
 /* ---------------------------------------------------------------- VOF */
 /* corner_fraction, vof.cpp:28-32 */
 static double corner_fraction(double A_, double B_, double t) {
@@ -1032,7 +1141,6 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
     const int nx = c->nx, ny = c->ny, nmat = c->nmat;
     const double cv = c->cv, dx = c->dx, dy = c->dy, x0 = c->x0, y0 = c->y0;
     const int order = c->cfg.face_order;
-    const int diag_scheme = c->cfg.corner == H2D_CORNER_LINEARDIAG;
     vfld uh = c->u_half;
 #define DX_(i, j) (dt * VX(uh, i, j))
 #define DY_(i, j) (dt * VY(uh, i, j))
@@ -1192,6 +1300,20 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
                     if (ord <= 1) {
                         rf = A(c->rho[a], cdi, cdj);
                         ef = A(w->e[a], cdi, cdj);
+                    } else if (c->cfg.corner == H2D_CORNER_MULTID) { /* multid_faces, remap.cpp:840,889-894 */
+                        double sr[3][3], se[3][3], xlx[3][3], xly[3][3];
+                        for (int q = 0; q < 3; ++q)
+                            for (int p = 0; p < 3; ++p) {
+                                sr[p][q] = A(c->rho[a], cdi + p - 1, cdj + q - 1);
+                                se[p][q] = A(w->e[a], cdi + p - 1, cdj + q - 1);
+                                xlx[p][q] = VX(c->xlag2, cdi + p - 1, cdj + q - 1);
+                                xly[p][q] = VY(c->xlag2, cdi + p - 1, cdj + q - 1);
+                            }
+                        const double bcx = ax ? 0.5 * (blo + bhi) : 0.5 * (wlo + whi);
+                        const double bcy = ax ? 0.5 * (wlo + whi) : 0.5 * (blo + bhi);
+                        const plane_t pr = multid_plane(c, sr, xlx, xly), pe = multid_plane(c, se, xlx, xly);
+                        rf = plane_eval(&pr, bcx, bcy);
+                        ef = plane_eval(&pe, bcx, bcy);
                     } else {
                         double sr[3], se[3], sxp[3];
                         for (int d = -1; d <= 1; ++d) {
@@ -1237,11 +1359,28 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
             double dva[H2D_MAX_MAT];
             split_flux(c, di, dj, blox, bloy, bhix, bhiy, cdv, dva);
             const double lwx = A(c->wlx, di, dj), lwy = A(c->wly, dj, di);
+            kin_t kin; /* remap.cpp:944-956 */
+            kin.dxp = ddx;
+            kin.dyp = ddy;
+            kin.lag_wx = lwx;
+            kin.lag_wy = lwy;
+            {
+                const int fxj = sy > 0 ? j - 1 : j, fyi = sx > 0 ? i - 1 : i;
+                kin.sgn_fx = A(c->fx_dv, i, fxj) >= 0.0 ? 1.0 : -1.0;
+                kin.u_fx_dt = A(c->fdx, i, fxj);
+                kin.sgn_fy = A(c->fy_dv, fyi, j) >= 0.0 ? 1.0 : -1.0;
+                kin.u_fy_dt = A(c->fdy, j, fyi);
+                kin.erx = 0.5 * (blox + bhix) - VX(c->xlag2, di, dj);
+                kin.ery = 0.5 * (bloy + bhiy) - VY(c->xlag2, di, dj);
+            }
             double dmtot = 0.0;
             for (int a = 0; a < nmat; ++a) {
                 if (dva[a] == 0.0) continue;
-                int lin = diag_scheme && order > 1;
-                if (lin && nmat >= 2 && c->cfg.interface_degrade && !pure_3x3(c, a, di, dj)) lin = 0;
+                int scheme = c->cfg.corner; /* remap.cpp:960-963 */
+                if (order <= 1) scheme = H2D_CORNER_UPWIND;
+                if (scheme != H2D_CORNER_UPWIND && nmat >= 2 && c->cfg.interface_degrade && !pure_3x3(c, a, di, dj))
+                    scheme = H2D_CORNER_UPWIND;
+                const int lin = scheme != H2D_CORNER_UPWIND;
                 double rf, ef;
                 if (!lin) {
                     rf = A(c->rho[a], di, dj);
@@ -1255,8 +1394,8 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
                             xlx[p][q] = VX(c->xlag2, di + p - 1, dj + q - 1);
                             xly[p][q] = VY(c->xlag2, di + p - 1, dj + q - 1);
                         }
-                    rf = ref_max(corner_linear_diag(c, sr, xlx, xly, ddx, ddy, lwx, lwy), 0.0);
-                    ef = corner_linear_diag(c, se, xlx, xly, ddx, ddy, lwx, lwy);
+                    rf = ref_max(corner_value(c, scheme, sr, xlx, xly, &kin), 0.0);
+                    ef = corner_value(c, scheme, se, xlx, xly, &kin);
                 }
                 const double dm = rf * dva[a];
                 const double dme = rf * ef * dva[a];
@@ -1302,7 +1441,7 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
                     const int wi = wrapi(di, c->per_x ? nx : nx + 1, c->per_x);
                     const int wj = wrapi(dj, c->per_y ? ny : ny + 1, c->per_y);
                     double ufx, ufy;
-                    if (!(diag_scheme && order > 1)) {
+                    if (!(c->cfg.corner != H2D_CORNER_UPWIND && order > 1)) { /* remap.cpp:1025-1029 */
                         ufx = VX(w->u, wi, wj);
                         ufy = VY(w->u, wi, wj);
                     } else {
@@ -1324,8 +1463,19 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
                                 xlx[p][q] = (x0 + ni * dx) + DX_(ni, nj);
                                 xly[p][q] = (y0 + nj * dy) + DY_(ni, nj);
                             }
-                        ufx = corner_linear_diag(c, ax_, xlx, xly, dxp, dyp, lwx, lwy);
-                        ufy = corner_linear_diag(c, ay_, xlx, xly, dxp, dyp, lwx, lwy);
+                        kin_t kin; /* remap.cpp:1036-1052 */
+                        kin.dxp = dxp;
+                        kin.dyp = dyp;
+                        kin.lag_wx = lwx;
+                        kin.lag_wy = lwy;
+                        kin.sgn_fx = dirx;
+                        kin.u_fx_dt = mdx;
+                        kin.sgn_fy = diry;
+                        kin.u_fy_dt = mdy;
+                        kin.erx = ((x0 + (ci + 0.5) * dx) + 0.5 * mdx) - ((x0 + wi * dx) + DX_(wi, wj));
+                        kin.ery = ((y0 + (cj + 0.5) * dy) + 0.5 * mdy) - ((y0 + wj * dy) + DY_(wi, wj));
+                        ufx = corner_value(c, c->cfg.corner, ax_, xlx, xly, &kin);
+                        ufy = corner_value(c, c->cfg.corner, ay_, xlx, xly, &kin);
                     }
                     acc_add(c, i, j, ufx * F, ufy * F);
                     acc_add(c, pi, pj, ufx * -F, ufy * -F);
@@ -1551,7 +1701,7 @@ int h2do_create(const h2d_config* cfg, int device, ctx_t** out) {
     if (m->nx < 3 || m->ny < 3) return H2D_ERR_SIM;       /* Mesh::Mesh, mesh.hpp:27 */
     if (m->dx <= 0.0 || m->dy <= 0.0) return H2D_ERR_SIM; /* mesh.hpp:28 */
     if (cfg->nmat < 1 || cfg->nmat > H2D_MAX_MAT) return H2D_ERR_INVALID;
-    if (cfg->corner != H2D_CORNER_UPWIND && cfg->corner != H2D_CORNER_LINEARDIAG) return H2D_ERR_INVALID;
+    if (cfg->corner < H2D_CORNER_UPWIND || cfg->corner > H2D_CORNER_MULTID) return H2D_ERR_INVALID;
     ctx_t* c = (ctx_t*)calloc(1, sizeof(ctx_t));
     c->cfg = *cfg;
     const int nx = m->nx, ny = m->ny;

@@ -58,8 +58,29 @@ def test_init_case_painter_matches_reference(ref, orc):
 CONFIGS = []
 for bcx, bcy in ((BC_PERIODIC, BC_PERIODIC), (BC_WALL, BC_WALL), (BC_PERIODIC, BC_WALL)):
     for order, corner, degrade in ((2, CORNER_LINEARDIAG, 1), (1, CORNER_UPWIND, 1), (2, CORNER_UPWIND, 1),
-                                   (2, CORNER_LINEARDIAG, 0)):
+                                   (2, CORNER_LINEARDIAG, 0), (2, abi.CORNER_AVGMIN, 1), (2, abi.CORNER_LINEARXY, 1),
+                                   (2, abi.CORNER_MULTID, 1), (2, abi.CORNER_MULTID, 0), (1, abi.CORNER_MULTID, 1)):
         CONFIGS.append((bcx, bcy, order, corner, degrade))
+
+
+@pytest.mark.parametrize("corner", [abi.CORNER_AVGMIN, abi.CORNER_LINEARXY, abi.CORNER_MULTID])
+@pytest.mark.parametrize("which,steps", [("riemann", 40), ("triple", 60), ("bubble", 20)])
+def test_run_loop_corner_schemes_bitwise(ref, orc, corner, which, steps):
+    """The remaining corner schemes (reconstruct.cpp:116-152; Multid also
+    reconstructs the faces, remap.cpp:840,889-894) in the run loop."""
+    case = {"riemann": cases.riemann2d(40), "triple": cases.triple_point(48, 24),
+            "bubble": cases.shock_bubble(40)}[which]
+    m = case.cfg.mesh
+    cfg = make_config(m.nx, m.ny, m.dx, m.dy, m.x0, m.y0, m.bc_x, m.bc_y,
+                      eos=[(case.cfg.eos[a].kind, case.cfg.eos[a].gamma, case.cfg.eos[a].pi)
+                           for a in range(case.cfg.nmat)], corner=corner)
+    sr, so = _both(ref, orc, cfg, case.paint())
+    rr, er = helpers.run_capture(sr, steps, case.cfl)
+    ro, eo = helpers.run_capture(so, steps, case.cfl)
+    assert er == eo
+    assert np.array_equal(rr.dts, ro.dts)
+    assert (rr.floor_count, rr.diag) == (ro.floor_count, ro.diag)
+    assert helpers.bitwise_diff(sr.download(), so.download(), helpers.STATE_FIELDS) == []
 
 
 @pytest.mark.parametrize("bcx,bcy,order,corner,degrade", CONFIGS)
