@@ -560,7 +560,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     if (m.nx < 3 || m.ny < 3) return H2D_ERR_SIM;        // Mesh::Mesh, mesh.hpp:27
     if (m.dx <= 0.0 || m.dy <= 0.0) return H2D_ERR_SIM;  // mesh.hpp:28
     if (cfg->nmat < 1 || cfg->nmat > H2D_MAX_MAT) return H2D_ERR_INVALID;  // (3: DESIGN.md 5b)
-    if (cfg->corner != H2D_CORNER_UPWIND && cfg->corner != H2D_CORNER_LINEARDIAG) return H2D_ERR_INVALID;
+    if (cfg->corner < H2D_CORNER_UPWIND || cfg->corner > H2D_CORNER_MULTID) return H2D_ERR_INVALID;
     h2d_ctx* c = new h2d_ctx();
     c->cfg = *cfg;
     auto fail = [&](int rc) {
@@ -658,6 +658,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     d.a2 = cfg->pv_a2;
     d.face_order = cfg->face_order;
     d.corner_diag = cfg->corner == H2D_CORNER_LINEARDIAG;
+    d.corner = cfg->corner;
     d.degrade = cfg->interface_degrade != 0;
     d.remap_velocity = 1;
     d.q = plane(c);

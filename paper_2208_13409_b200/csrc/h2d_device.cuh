@@ -168,6 +168,7 @@ struct Dev {
     double gamma[kMatSlots], pi[kMatSlots];
     double a1, a2;
     int face_order, corner_diag, degrade, remap_velocity;
+    int corner;  // CornerScheme (H2D_CORNER_*): Upwind, AvgMin, LinearXY, LinearDiag, Multid
 
     // current (read) State
     const double *m[kMatSlots], *e[kMatSlots], *k[kMatSlots], *m_mix, *e_mix, *rho_mix, *p_mix, *nrx, *nry, *ux, *uy;
@@ -331,6 +332,128 @@ H2D_DEV double corner_diag(const Dev& d, const double* a, const double* xlx, con
     const double gvp = lim_grad(a[2], ac, a[6], xlx[2] * vx + xly[2] * vy, sc, xlx[6] * vx + xly[6] * vy, bad);
     const double ex = sx * lwx - dxp, ey = sx * -lwy - dyp;
     return ac + 0.5 * gvp * (ex * vx + ey * vy);
+}
+
+// CornerScheme (reconstruct.hpp:7, the H2D_CORNER_* ordinals)
+enum { CS_UPWIND = 0, CS_AVGMIN = 1, CS_LINEARXY = 2, CS_LINEARDIAG = 3, CS_MULTID = 4 };
+// CornerKin (reconstruct.hpp:44-51); er = eval_rel
+struct Kin {
+    double dxp, dyp, lwx, lwy, sfx, ufx, sfy, ufy, erx, ery;
+};
+H2D_DEV int sgn3(double v) { return v > 0.0 ? 1 : (v < 0.0 ? -1 : 0); }  // reconstruct.cpp:35
+// multid_plane (reconstruct.cpp:45-107): the least-squares plane through the
+// 3x3 stencil (Householder QR of the 8x2 system), limited by the smallest of
+// the four 1D limited slopes; returns (a0, cx, cy, gx, gy)
+static __device__ __noinline__ void multid_plane(double dgx, double dgy, const double* a, const double* xlx,
+                                          const double* xly, double& a0, double& cx, double& cy, double& gx,
+                                          double& gy, bool& bad) {
+    a0 = a[4];
+    cx = xlx[4];
+    cy = xly[4];
+    double X0[8], X1[8], b[8];
+    {
+        int m = 0;
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (p == 1 && q == 1) continue;
+                X0[m] = xlx[p * 3 + q] - cx;
+                X1[m] = xly[p * 3 + q] - cy;
+                b[m] = a[p * 3 + q] - a0;
+                ++m;
+            }
+    }
+    gx = gy = 0.0;
+    bool rank_ok = true;
+#pragma unroll
+    for (int col = 0; col < 2; ++col) {
+        if (!rank_ok) break;
+        double* Xc = col == 0 ? X0 : X1;
+        double nrm = 0.0;
+#pragma unroll
+        for (int r = col; r < 8; ++r) nrm += Xc[r] * Xc[r];
+        nrm = sqrt(nrm);
+        if (nrm < 1e-300) {  // rank-deficient geometry: zero gradient
+            rank_ok = false;
+            break;
+        }
+        const double alpha = Xc[col] > 0.0 ? -nrm : nrm;
+        double v[8];
+        v[col] = Xc[col] - alpha;
+#pragma unroll
+        for (int r = col + 1; r < 8; ++r) v[r] = Xc[r];
+        double vtv = 0.0;
+#pragma unroll
+        for (int r = col; r < 8; ++r) vtv += v[r] * v[r];
+        if (vtv > 0.0) {
+#pragma unroll
+            for (int cc = col; cc < 2; ++cc) {
+                double* Xk = cc == 0 ? X0 : X1;
+                double sv = 0.0;
+#pragma unroll
+                for (int r = col; r < 8; ++r) sv += v[r] * Xk[r];
+                sv *= 2.0 / vtv;
+#pragma unroll
+                for (int r = col; r < 8; ++r) Xk[r] -= sv * v[r];
+            }
+            double sv = 0.0;
+#pragma unroll
+            for (int r = col; r < 8; ++r) sv += v[r] * b[r];
+            sv *= 2.0 / vtv;
+#pragma unroll
+            for (int r = col; r < 8; ++r) b[r] -= sv * v[r];
+        }
+    }
+    if (!rank_ok) return;
+    const double g2 = b[1] / X1[1];
+    const double g1 = (b[0] - X1[0] * g2) / X0[0];
+    const double gnorm = sqrt(g1 * g1 + g2 * g2);
+    if (gnorm < 1e-300) return;
+    const double vx = dgx, vy = dgy;  // dx/diag, dy/diag (hoisted, same bits)
+    const double lgx = lim_grad(a[1], a[4], a[7], xlx[1], xlx[4], xlx[7], bad);
+    const double lgy = lim_grad(a[3], a[4], a[5], xly[3], xly[4], xly[5], bad);
+    const double sc = xlx[4] * vx + xly[4] * vy;
+    const double gv = lim_grad(a[0], a[4], a[8], xlx[0] * vx + xly[0] * vy, sc, xlx[8] * vx + xly[8] * vy, bad);
+    const double scp = xlx[4] * vx + xly[4] * -vy;
+    const double gvp =
+        lim_grad(a[2], a[4], a[6], xlx[2] * vx + xly[2] * -vy, scp, xlx[6] * vx + xly[6] * -vy, bad);
+    const double phi = rmin(rmin(fabs(lgx), fabs(lgy)), rmin(fabs(gv), fabs(gvp))) / gnorm;
+    gx = phi * g1;
+    gy = phi * g2;
+}
+// corner_value (reconstruct.cpp:116-152) for the AvgMin, LinearXY and Multid
+// schemes (LinearDiag, the default, stays inline as corner_diag): out of line
+// so the hot kernels keep their registers; a / xl as corner_diag
+static __device__ __noinline__ double corner_value_other(int scheme, double dgx, double dgy, const double* a,
+                                                  const double* xlx, const double* xly, Kin k, bool* bad) {
+    const double ac = a[4];
+    bool b = false;
+    double r = ac;
+    if (scheme == CS_AVGMIN) {
+        const int sx = sgn3(k.dxp), sy = sgn3(k.dyp);
+        const double pair_avg = 0.5 * (ac + a[(1 + sx) * 3 + (1 + sy)]);
+        r = rmin(ac, pair_avg);
+    } else if (scheme == CS_LINEARXY) {
+        const double gx = lim_grad(a[1], ac, a[7], xlx[1], xlx[4], xlx[7], b);
+        const double gy = lim_grad(a[3], ac, a[5], xly[3], xly[4], xly[5], b);
+        r = ac + 0.5 * gx * (k.sfx * k.lwx - k.ufx) + 0.5 * gy * (k.sfy * k.lwy - k.ufy);
+    } else if (scheme == CS_MULTID) {
+        double a0, cx, cy, gx, gy;
+        multid_plane(dgx, dgy, a, xlx, xly, a0, cx, cy, gx, gy, b);
+        r = a0 + (gx * k.erx + gy * k.ery);
+    }
+    if (b) *bad = true;
+    return r;
+}
+// plane_eval(multid_plane(stencil), (bx, by)) (reconstruct.hpp:67-69), out of line
+static __device__ __noinline__ double multid_eval(double dgx, double dgy, const double* a, const double* xlx,
+                                           const double* xly, double bx, double by, bool* bad) {
+    double a0, cx, cy, gx, gy;
+    bool b = false;
+    multid_plane(dgx, dgy, a, xlx, xly, a0, cx, cy, gx, gy, b);
+    if (b) *bad = true;
+    return a0 + (gx * (bx - cx) + gy * (by - cy));
 }
 
 // corner_fraction / clipped_fraction, vof.cpp:28-45

@@ -841,6 +841,52 @@ __device__ __forceinline__ Tile<NM> carve_tile(char* base, int ci0, int cj0) {
     return T;
 }
 
+// The non-default corner schemes and the Multid faces read their 3x3
+// stencils from the tile themselves, out of line: the default LinearDiag path
+// keeps its stencil in registers (an array whose address is taken would move
+// to local memory for every path)
+struct Pair2 {  // two results and the "non-increasing centroid" flag, returned by value
+    double a, b;
+    int bad;
+};
+__device__ __noinline__ Pair2 corner_other_tile(int scheme, double dgx, double dgy, const double* rho,
+                                                const double* el, const double* x2x, const double* x2y, int dc,
+                                                Kin k) {
+    double sr[9], se[9], xlx[9], xly[9];
+    for (int q = 0; q < 3; ++q)
+        for (int p = 0; p < 3; ++p) {
+            const int sidx = dc + (p - 1) + (q - 1) * RCW;
+            sr[p * 3 + q] = rho[sidx];
+            se[p * 3 + q] = el[sidx];
+            xlx[p * 3 + q] = x2x[sidx];
+            xly[p * 3 + q] = x2y[sidx];
+        }
+    bool bad = false;
+    Pair2 r;
+    r.a = rmax(corner_value_other(scheme, dgx, dgy, sr, xlx, xly, k, &bad), 0.0);
+    r.b = corner_value_other(scheme, dgx, dgy, se, xlx, xly, k, &bad);
+    r.bad = bad;
+    return r;
+}
+__device__ __noinline__ Pair2 multid_face_tile(double dgx, double dgy, const double* rho, const double* el,
+                                               const double* x2x, const double* x2y, int dc, double bx, double by) {
+    double sr[9], se[9], xlx[9], xly[9];
+    for (int q = 0; q < 3; ++q)
+        for (int p = 0; p < 3; ++p) {
+            const int sidx = dc + (p - 1) + (q - 1) * RCW;
+            sr[p * 3 + q] = rho[sidx];
+            se[p * 3 + q] = el[sidx];
+            xlx[p * 3 + q] = x2x[sidx];
+            xly[p * 3 + q] = x2y[sidx];
+        }
+    bool bad = false;
+    Pair2 r;
+    r.a = multid_eval(dgx, dgy, sr, xlx, xly, bx, by, &bad);
+    r.b = multid_eval(dgx, dgy, se, xlx, xly, bx, by, &bad);
+    r.bad = bad;
+    return r;
+}
+
 // The three-material split of a flux box of donor (di, dj) (oracle
 // split_flux, nmat == 3): a mixed donor gives k_r * dvol to the material
 // outside its interface pair and splits the rest at the pair's interface; a
@@ -926,7 +972,7 @@ __device__ __forceinline__ void split_flux_t(const Dev& d, const Tile<NM>& T, in
 
 // Face flux (remap.cpp:850-918) of the X (AX = 1, at node i, row j) or Y
 // (AX = 0, at column i, node row j) face; returns the face's dmx / dmy entry.
-template <int NM, int AX>
+template <int NM, int AX, bool XC = false>
 __device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, int i, int j, double dt,
                                               double* odm, double* odme, double* odva) {
     const int qn = T.n(i, j);
@@ -967,6 +1013,13 @@ __device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, i
             if (ord <= 1) {
                 rf = T.rho[a][cc];
                 ef = T.el[a][cc];
+            } else if (XC && d.corner == CS_MULTID) {  // multid_faces (remap.cpp:840,889-894)
+                const double bcx = AX ? 0.5 * (blo + bhi) : 0.5 * (wlo + whi);
+                const double bcy = AX ? 0.5 * (wlo + whi) : 0.5 * (blo + bhi);
+                const Pair2 r2 = multid_face_tile(d.dgx, d.dgy, T.rho[a], T.el[a], T.xl2x, T.xl2y, T.c(cdi, cdj), bcx, bcy);
+                rf = r2.a;
+                ef = r2.b;
+                if (r2.bad) bad = true;
             } else {
                 const int im = AX ? ia_d - 1 : ic, jm = AX ? ic : ia_d - 1;
                 const int ic_ = AX ? ia_d : ic, jc = AX ? ic : ia_d;
@@ -1000,7 +1053,7 @@ __device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, i
 }
 
 // Corner flux (remap.cpp:923-983) at node (i, j); returns the dmc entry.
-template <int NM>
+template <int NM, bool XC = false>
 __device__ __forceinline__ double corner_item_t(const Dev& d, const Tile<NM>& T, int i, int j, double dt,
                                                 double* odm, double* odme, double* odva) {
     const int qn = T.n(i, j);
@@ -1018,7 +1071,21 @@ __device__ __forceinline__ double corner_item_t(const Dev& d, const Tile<NM>& T,
         const int dc = T.c(di, dj);
         const double lwx = T.wlx(d, di, dj), lwy = T.wly(d, di, dj);
         bool bad = false;
-        const bool lin_cfg = d.corner_diag && d.face_order > 1;
+        const bool lin_cfg = d.corner != CS_UPWIND && d.face_order > 1;
+        Kin kin;  // remap.cpp:944-956
+        kin.dxp = ddx;
+        kin.dyp = ddy;
+        kin.lwx = lwx;
+        kin.lwy = lwy;
+        if (XC && lin_cfg && d.corner != CS_LINEARDIAG) {
+            const int fxj = sy > 0 ? j - 1 : j, fyi = sx > 0 ? i - 1 : i;
+            kin.sfx = T.fxdv[T.n(i, fxj)] >= 0.0 ? 1.0 : -1.0;
+            kin.ufx = T.fdx[T.n(i, fxj)];
+            kin.sfy = T.fydv[T.n(fyi, j)] >= 0.0 ? 1.0 : -1.0;
+            kin.ufy = T.fdy[T.n(fyi, j)];
+            kin.erx = 0.5 * (blox + bhix) - T.xl2x[dc];
+            kin.ery = 0.5 * (bloy + bhiy) - T.xl2y[dc];
+        }
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
             if (dva[a] == 0.0) continue;
@@ -1035,6 +1102,11 @@ __device__ __forceinline__ double corner_item_t(const Dev& d, const Tile<NM>& T,
             if (!lin) {
                 rf = T.rho[a][dc];
                 ef = T.el[a][dc];
+            } else if (XC && d.corner != CS_LINEARDIAG) {
+                const Pair2 r2 = corner_other_tile(d.corner, d.dgx, d.dgy, T.rho[a], T.el[a], T.xl2x, T.xl2y, dc, kin);
+                rf = r2.a;
+                ef = r2.b;
+                if (r2.bad) bad = true;
             } else {
                 double sr[9], se[9], xlx[9], xly[9];
 #pragma unroll
@@ -1304,7 +1376,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     } while (!done);
 }
 
-template <int NM>
+// XC: the AvgMin / LinearXY / Multid corner schemes compiled in (their
+// out-of-line calls cost the default kernels registers; see launch_remap_tile)
+template <int NM, bool XC = false>
 __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
     pdl_enter();
     extern __shared__ __align__(128) char smem_raw[];
@@ -1518,7 +1592,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
 #pragma unroll
         for (int a = 0; a < NM; ++a) dva[a] = dm[a] = dme[a] = 0.0;
         if (ia <= min(nx, rg.i1) && ic < min(ny, rg.j1)) {
-            const double tot = face_item_t<NM, 1>(d, T, ia, ic, dt, dm, dme, dva);
+            const double tot = face_item_t<NM, 1, XC>(d, T, ia, ic, dt, dm, dme, dva);
             if (ia < i0 + RTX || ia == min(nx, rg.i1)) d.dmx[ix(d, ia, ic)] = tot;
         }
 #pragma unroll
@@ -1543,7 +1617,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
 #pragma unroll
         for (int a = 0; a < NM; ++a) dva[a] = dm[a] = dme[a] = 0.0;
         if (ic < min(nx, rg.i1) && ja <= min(ny, rg.j1)) {
-            const double tot = face_item_t<NM, 0>(d, T, ic, ja, dt, dm, dme, dva);
+            const double tot = face_item_t<NM, 0, XC>(d, T, ic, ja, dt, dm, dme, dva);
             if (ja < j0 + RTY || ja == min(ny, rg.j1)) d.dmy[ix(d, ic, ja)] = tot;
         }
 #pragma unroll
@@ -1570,7 +1644,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
         for (int a = 0; a < NM; ++a) dva[a] = dm[a] = dme[a] = 0.0;
         const int ni1 = min(nx, rg.i1), nj1 = min(ny, rg.j1);
         if (ni <= ni1 && nj <= nj1) {
-            const double tot = corner_item_t<NM>(d, T, ni, nj, dt, dm, dme, dva);
+            const double tot = corner_item_t<NM, XC>(d, T, ni, nj, dt, dm, dme, dva);
             if ((ni < i0 + RTX || ni == ni1) && (nj < j0 + RTY || nj == nj1)) d.dmc[ix(d, ni, nj)] = tot;
         }
 #pragma unroll
@@ -1961,6 +2035,32 @@ __device__ __forceinline__ void dual_face_item(const Dev& d, int i, int j) {
 
 // Dual-mesh corner exchanges, remap.cpp:1000-1069: iteration (i, j), both
 // pairs (1,1) and (1,-1).
+// the dual corner velocity for the AvgMin / LinearXY / Multid schemes on
+// the 3x3 node stencil around node (wi, wj) (plane index g), out of line
+// (see corner_other_tile); stencil positions node_pos + dt u_half as inline
+__device__ __noinline__ Pair2 dual_corner_other(int scheme, double dgx, double dgy, const double* ulx,
+                                                const double* uly, const double* uhx, const double* uhy, int g, int P,
+                                                int wi, int wj, double x0, double y0, double dx, double dy, double dt,
+                                                Kin k) {
+    double ax_[9], ay_[9], xlx[9], xly[9];
+    for (int q = 0; q < 3; ++q)
+        for (int p = 0; p < 3; ++p) {
+            const int ni = wi + p - 1, nj = wj + q - 1;
+            const int nn = g + (p - 1) + (q - 1) * P;
+            ax_[p * 3 + q] = ulx[nn];
+            ay_[p * 3 + q] = uly[nn];
+            xlx[p * 3 + q] = (x0 + ni * dx) + dt * uhx[nn];
+            xly[p * 3 + q] = (y0 + nj * dy) + dt * uhy[nn];
+        }
+    bool bad = false;
+    Pair2 r;
+    r.a = corner_value_other(scheme, dgx, dgy, ax_, xlx, xly, k, &bad);
+    r.b = corner_value_other(scheme, dgx, dgy, ay_, xlx, xly, k, &bad);
+    r.bad = bad;
+    return r;
+}
+
+template <bool XC>
 __device__ __forceinline__ bool dual_corner_pair(const Dev& d, int i, int j, int pr, double& cx, double& cy) {
     const int nx = d.nx, ny = d.ny;
     const double dt = step_dt(d.ctl);
@@ -1999,7 +2099,7 @@ __device__ __forceinline__ bool dual_corner_pair(const Dev& d, int i, int j, int
             const int wi = d.per_x ? ((di % nx) + nx) % nx : di;
             const int wj = d.per_y ? ((dj % ny) + ny) % ny : dj;
             double ufx, ufy;
-            if (!(d.corner_diag && d.face_order > 1)) {
+            if (!(d.corner != CS_UPWIND && d.face_order > 1)) {
                 ufx = d.ulx[ix(d, wi, wj)];
                 ufy = d.uly[ix(d, wi, wj)];
             } else {
@@ -2019,21 +2119,40 @@ __device__ __forceinline__ bool dual_corner_pair(const Dev& d, int i, int j, int
                 const double dyp = diry * rmax(fabs(mdy), 1e-300);
                 const double lwx = d.dx + 0.5 * (dt * d.uhx[ix(d, wi + 1, wj)] - dt * d.uhx[ix(d, wi - 1, wj)]);
                 const double lwy = d.dy + 0.5 * (dt * d.uhy[ix(d, wi, wj + 1)] - dt * d.uhy[ix(d, wi, wj - 1)]);
-                double ax_[9], ay_[9], xlx[9], xly[9];
-#pragma unroll
-                for (int q = 0; q < 3; ++q)
-#pragma unroll
-                    for (int p = 0; p < 3; ++p) {
-                        const int ni = wi + p - 1, nj = wj + q - 1;
-                        const int nn = ix(d, ni, nj);
-                        ax_[p * 3 + q] = d.ulx[nn];
-                        ay_[p * 3 + q] = d.uly[nn];
-                        xlx[p * 3 + q] = (d.x0 + ni * d.dx) + dt * d.uhx[nn];
-                        xly[p * 3 + q] = (d.y0 + nj * d.dy) + dt * d.uhy[nn];
-                    }
                 bool bad = false;
-                ufx = corner_diag(d, ax_, xlx, xly, dxp, dyp, lwx, lwy, bad);
-                ufy = corner_diag(d, ay_, xlx, xly, dxp, dyp, lwx, lwy, bad);
+                if (!XC || d.corner == CS_LINEARDIAG) {
+                    double ax_[9], ay_[9], xlx[9], xly[9];
+#pragma unroll
+                    for (int q = 0; q < 3; ++q)
+#pragma unroll
+                        for (int p = 0; p < 3; ++p) {
+                            const int ni = wi + p - 1, nj = wj + q - 1;
+                            const int nn = ix(d, ni, nj);
+                            ax_[p * 3 + q] = d.ulx[nn];
+                            ay_[p * 3 + q] = d.uly[nn];
+                            xlx[p * 3 + q] = (d.x0 + ni * d.dx) + dt * d.uhx[nn];
+                            xly[p * 3 + q] = (d.y0 + nj * d.dy) + dt * d.uhy[nn];
+                        }
+                    ufx = corner_diag(d, ax_, xlx, xly, dxp, dyp, lwx, lwy, bad);
+                    ufy = corner_diag(d, ay_, xlx, xly, dxp, dyp, lwx, lwy, bad);
+                } else {
+                    Kin kin;  // the synthetic kinematics of remap.cpp:1036-1052
+                    kin.dxp = dxp;
+                    kin.dyp = dyp;
+                    kin.lwx = lwx;
+                    kin.lwy = lwy;
+                    kin.sfx = dirx;
+                    kin.ufx = mdx;
+                    kin.sfy = diry;
+                    kin.ufy = mdy;
+                    kin.erx = (cxc + 0.5 * mdx) - ((d.x0 + wi * d.dx) + dt * d.uhx[ix(d, wi, wj)]);
+                    kin.ery = (cyc + 0.5 * mdy) - ((d.y0 + wj * d.dy) + dt * d.uhy[ix(d, wi, wj)]);
+                    const Pair2 r2 = dual_corner_other(d.corner, d.dgx, d.dgy, d.ulx, d.uly, d.uhx, d.uhy, ix(d, wi, wj),
+                                                       d.P, wi, wj, d.x0, d.y0, d.dx, d.dy, dt, kin);
+                    ufx = r2.a;
+                    ufy = r2.b;
+                    if (r2.bad) bad = true;
+                }
                 if (bad && own_node(d, i, j)) raise(d.ctl, ekey(PH_GRAD_DUALC, j, i, pr));
             }
             cx = ufx * Fv;
@@ -2042,12 +2161,13 @@ __device__ __forceinline__ bool dual_corner_pair(const Dev& d, int i, int j, int
         return active;
     }
 }
+template <bool XC>
 __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
     const int s = ix(d, i, j);
 #pragma unroll
     for (int pr = 0; pr < 2; ++pr) {
         double cx, cy;
-        const bool on = dual_corner_pair(d, i, j, pr, cx, cy);
+        const bool on = dual_corner_pair<XC>(d, i, j, pr, cx, cy);
         d.dc_x[pr][s] = cx;
         d.dc_y[pr][s] = cy;
         if (d.per_x || d.per_y) d.dflag[2 + pr][s] = on;
@@ -2056,6 +2176,7 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
 
 // All dual-mesh items of one unique node (i, j): its X and Y dual faces and
 // its two diagonal corner exchanges (remap.cpp:995-1069).
+template <bool XC = false>
 __global__ void __launch_bounds__(128, 8) k_dual_items(Dev d) {
     pdl_enter();
     if (halted(d.ctl)) return;
@@ -2092,7 +2213,7 @@ __global__ void __launch_bounds__(128, 8) k_dual_items(Dev d) {
     }
     dual_face_item<1>(d, i, j);
     dual_face_item<0>(d, i, j);
-    dual_corner_items(d, i, j);
+    dual_corner_items<XC>(d, i, j);
 }
 
 // Wall boundaries: the MomAcc gather in its fixed loop order — X face i (+),
@@ -3232,6 +3353,9 @@ void remap_init() {
     cudaFuncSetAttribute(k_remap_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<1>());
     cudaFuncSetAttribute(k_remap_tile<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<2>());
     cudaFuncSetAttribute(k_remap_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<3>());
+    cudaFuncSetAttribute(k_remap_tile<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<1>());
+    cudaFuncSetAttribute(k_remap_tile<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<2>());
+    cudaFuncSetAttribute(k_remap_tile<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<3>());
     done = true;
 }
 
@@ -3337,12 +3461,16 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
     Rng rt = d.r_gath;
     rt.i0 -= tile_shift(d);
     const dim3 gft = tiles_of(rt, RTX, RTY);
+    const bool xc = d.corner != CS_UPWIND && d.corner != CS_LINEARDIAG;  // the extended corner schemes
     if (d.nmat == 3)
-        pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
+        xc ? pdl(k_remap_tile<3, true>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma)
+           : pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
     else if (d.nmat == 2)
-        pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
+        xc ? pdl(k_remap_tile<2, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma)
+           : pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
     else
-        pdl(k_remap_tile<1>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
+        xc ? pdl(k_remap_tile<1, true>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma)
+           : pdl(k_remap_tile<1>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
 }
 
 // slivers + finalize_cells ghost fill + flux ghosts
@@ -3369,7 +3497,10 @@ void launch_remap_slivers(const Dev& d, cudaStream_t s) {
 // dual-mesh momentum remap (remap.cpp:993-1059)
 void launch_remap_dual(const Dev& d, cudaStream_t s) {
     if (d.remap_velocity) {
-        pdl(k_dual_items, grid_of(d.r_dual), blk2(), 0, s, d);
+        if (d.corner != CS_UPWIND && d.corner != CS_LINEARDIAG)
+            pdl(k_dual_items<true>, grid_of(d.r_dual), blk2(), 0, s, d);
+        else
+            pdl(k_dual_items<false>, grid_of(d.r_dual), blk2(), 0, s, d);
         if (d.per_x || d.per_y)  // periodic seams reorder the node sums: sorted gather
             pdl(k_node_update, grid_of(d.r_node), blk2(), 0, s, d);
         else

@@ -90,8 +90,28 @@ def test_wall_blast_bitwise(gpu, orc, n, steps):
 CONFIGS = []
 for bcx, bcy in ((BC_PERIODIC, BC_PERIODIC), (BC_WALL, BC_WALL), (BC_PERIODIC, BC_WALL)):
     for order, corner, degrade in ((2, CORNER_LINEARDIAG, 1), (1, CORNER_UPWIND, 1), (2, CORNER_UPWIND, 1),
-                                   (2, CORNER_LINEARDIAG, 0)):
+                                   (2, CORNER_LINEARDIAG, 0), (2, abi.CORNER_AVGMIN, 1), (2, abi.CORNER_LINEARXY, 1),
+                                   (2, abi.CORNER_MULTID, 1), (2, abi.CORNER_MULTID, 0)):
         CONFIGS.append((bcx, bcy, order, corner, degrade))
+
+
+@pytest.mark.parametrize("corner", [abi.CORNER_AVGMIN, abi.CORNER_LINEARXY, abi.CORNER_MULTID])
+@pytest.mark.parametrize("which,steps", [("riemann", 60), ("triple", 80), ("bubble", 30), ("voronoi3", 30)])
+def test_run_loop_corner_schemes_bitwise(gpu, orc, corner, which, steps):
+    """AvgMin / LinearXY / Multid corners (+ Multid faces), reconstruct.cpp:116-152."""
+    case = {"riemann": cases.riemann2d(48), "triple": cases.triple_point(64, 32), "bubble": cases.shock_bubble(48),
+            "voronoi3": cases.voronoi3(64)}[which]
+    m = case.cfg.mesh
+    cfg = make_config(m.nx, m.ny, m.dx, m.dy, m.x0, m.y0, m.bc_x, m.bc_y,
+                      eos=[(case.cfg.eos[a].kind, case.cfg.eos[a].gamma, case.cfg.eos[a].pi)
+                           for a in range(case.cfg.nmat)], corner=corner)
+    sg, so = _pair(gpu, orc, cfg, case.paint())
+    rg, eg = helpers.run_capture(sg, steps, case.cfl)
+    ro, eo = helpers.run_capture(so, steps, case.cfl)
+    assert eg == eo
+    assert np.array_equal(rg.dts, ro.dts)
+    assert (rg.floor_count, rg.diag) == (ro.floor_count, ro.diag)
+    assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS, case.cfg.nmat) == []
 
 
 @pytest.mark.parametrize("bcx,bcy,order,corner,degrade", CONFIGS)
