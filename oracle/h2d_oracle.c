@@ -1488,6 +1488,165 @@ static void cf_pass(ctx_t* c, double dt, int remap_velocity) {
 #undef DY_
 }
 
+/* direct_pass, remap.cpp:593-724: the unsplit one-step remap through the
+ * faces only (no corner fluxes), each axis with its own directionally
+ * displaced interface; dual faces only on the momentum side. */
+static void direct_pass(ctx_t* c, double dt, int remap_velocity) {
+    work_t* w = &c->w;
+    const int nx = c->nx, ny = c->ny, nmat = c->nmat;
+    const double cv = c->cv, dx = c->dx, dy = c->dy, x0 = c->x0, y0 = c->y0;
+    const int order = c->cfg.face_order;
+    vfld uh = c->u_half;
+    /* make_axis_geom X and Y, remap.cpp:296-322 */
+    for (int ic = -NG; ic < ny + NG; ++ic)
+        for (int ia = -NG; ia <= nx + NG; ++ia)
+            A(c->fdx, ia, ic) = 0.5 * (VX(uh, ia, ic) + VX(uh, ia, ic + 1)) * dt;
+    for (int ic = -NG; ic < ny + NG; ++ic)
+        for (int ia = -NG; ia < nx + NG; ++ia) {
+            const double dl = A(c->fdx, ia, ic), dr = A(c->fdx, ia + 1, ic);
+            A(c->xlcx, ia, ic) = x0 + (ia + 0.5) * dx + 0.5 * (dl + dr);
+            A(c->wlx, ia, ic) = dx + (dr - dl);
+        }
+    for (int ic = -NG; ic < nx + NG; ++ic)
+        for (int ia = -NG; ia <= ny + NG; ++ia)
+            A(c->fdy, ia, ic) = 0.5 * (VY(uh, ic, ia) + VY(uh, ic + 1, ia)) * dt;
+    for (int ic = -NG; ic < nx + NG; ++ic)
+        for (int ia = -NG; ia < ny + NG; ++ia) {
+            const double dl = A(c->fdy, ia, ic), dr = A(c->fdy, ia + 1, ic);
+            A(c->xlcy, ia, ic) = y0 + (ia + 0.5) * dy + 0.5 * (dl + dr);
+            A(c->wly, ia, ic) = dy + (dr - dl);
+        }
+    /* Lagrangian volume and densities, remap.cpp:601-614 */
+    for (int j = -NG; j < ny + NG; ++j)
+        for (int i = -NG; i < nx + NG; ++i) {
+            const double v = cv + (A(c->fdx, i + 1, j) - A(c->fdx, i, j)) * dy + (A(c->fdy, j + 1, i) - A(c->fdy, j, i)) * dx;
+            if (v <= 0.0) raise_err(c, H2D_ERR_CFL, i, j, "collapsed Lagrangian cell");
+            A(c->vlag, i, j) = v;
+            for (int a = 0; a < nmat; ++a) {
+                const double ka = A(w->k[a], i, j);
+                A(c->rho[a], i, j) = ka > 0.0 ? A(w->m[a], i, j) / (ka * v) : 0.0;
+            }
+        }
+    for (int a = 0; a < nmat; ++a) {
+        fzero(c->vola[a]);
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) A(c->vola[a], i, j) = A(w->k[a], i, j) * A(c->vlag, i, j);
+    }
+    /* face fluxes per axis, remap.cpp:656-713, each with the interfaces of
+     * its own displaced rectangles (remap.cpp:616-640) */
+    fzero(c->dmx);
+    fzero(c->dmy);
+    for (int axis = 0; axis < 2; ++axis) {
+        const int ax = axis == 0;
+        izero(c->if_mixed);
+        if (nmat >= 2)
+            for (int j = -NG; j < ny + NG; ++j)
+                for (int i = -NG; i < nx + NG; ++i) {
+                    double k0 = A(w->k[0], i, j);
+                    if (nmat == 3) {
+                        double k[3];
+                        kcell3(w->k, i, j, k);
+                        if (!mixed3(k)) continue;
+                        int lo, hi;
+                        pair3(k, &lo, &hi);
+                        A(c->if_lo, i, j) = lo;
+                        A(c->if_hi, i, j) = hi;
+                        k0 = k[3 - lo - hi] > 0.0 ? k[lo] / (k[lo] + k[hi]) : k[lo];
+                    } else if (!is_mixed(k0)) {
+                        continue;
+                    }
+                    const double cx = x0 + (i + 0.5) * dx, cy = y0 + (j + 0.5) * dy;
+                    const double hx = 0.5 * dx, hy = 0.5 * dy;
+                    double lox, loy, hix, hiy;
+                    if (ax) {
+                        lox = cx - hx + A(c->fdx, i, j); loy = cy - hy;
+                        hix = cx + hx + A(c->fdx, i + 1, j); hiy = cy + hy;
+                    } else {
+                        lox = cx - hx; loy = cy - hy + A(c->fdy, j, i);
+                        hix = cx + hx; hiy = cy + hy + A(c->fdy, j + 1, i);
+                    }
+                    const double nxv = VX(w->normals, i, j), nyv = VY(w->normals, i, j);
+                    A(c->if_mixed, i, j) = 1;
+                    A(c->if_lox, i, j) = lox; A(c->if_loy, i, j) = loy;
+                    A(c->if_hix, i, j) = hix; A(c->if_hiy, i, j) = hiy;
+                    A(c->if_nx, i, j) = nxv; A(c->if_ny, i, j) = nyv;
+                    A(c->if_d, i, j) = place_interface(k0, nxv, nyv, lox, loy, hix, hiy);
+                }
+        const int na = ax ? nx : ny, nc = ax ? ny : nx;
+        fld gfd = ax ? c->fdx : c->fdy, gxl = ax ? c->xlcx : c->xlcy, gwl = ax ? c->wlx : c->wly;
+        fld dmf = ax ? c->dmx : c->dmy;
+        const double wc = ax ? dy : dx;
+        for (int ic = 0; ic < nc; ++ic)
+            for (int ia = 0; ia <= na; ++ia) {
+                const double fd = A(gfd, ia, ic);
+                const double dvol = fd * wc;
+                A(dmf, ia, ic) = 0.0;
+                if (dvol == 0.0) continue;
+                if (fabs(dvol) > CFL_FRAC * cv)
+                    raise_err(c, H2D_ERR_CFL, ax ? ia : ic, ax ? ic : ia, "CFL violation at face");
+                const int ia_d = dvol > 0.0 ? ia - 1 : ia;
+                const double sgn = dvol > 0.0 ? 1.0 : -1.0;
+                const int cdi = ax ? ia_d : ic, cdj = ax ? ic : ia_d;
+                /* face_flux_box, remap.cpp:325-334 */
+                double blox, bloy, bhix, bhiy;
+                if (ax) {
+                    const double xf = x0 + ia * dx;
+                    blox = ref_min(xf, xf + fd); bhix = ref_max(xf, xf + fd);
+                    bloy = y0 + ic * dy; bhiy = y0 + (ic + 1) * dy;
+                } else {
+                    const double yf = y0 + ia * dy;
+                    blox = x0 + ic * dx; bhix = x0 + (ic + 1) * dx;
+                    bloy = ref_min(yf, yf + fd); bhiy = ref_max(yf, yf + fd);
+                }
+                double dva[H2D_MAX_MAT];
+                split_flux(c, cdi, cdj, blox, bloy, bhix, bhiy, dvol, dva);
+                double dmtot = 0.0;
+                for (int a = 0; a < nmat; ++a) {
+                    if (dva[a] == 0.0) continue;
+                    int ord = order;
+                    if (ord == 2 && nmat >= 2 && c->cfg.interface_degrade && !pure_1d(c, a, ax, ia_d, ic)) ord = 1;
+                    double rf, ef;
+                    if (ord <= 1) {
+                        rf = A(c->rho[a], cdi, cdj);
+                        ef = A(w->e[a], cdi, cdj);
+                    } else {
+                        double sr[3], se[3], sxp[3];
+                        for (int d = -1; d <= 1; ++d) {
+                            const int ci = ax ? ia_d + d : ic, cj = ax ? ic : ia_d + d;
+                            sr[d + 1] = A(c->rho[a], ci, cj);
+                            se[d + 1] = A(w->e[a], ci, cj);
+                            sxp[d + 1] = A(gxl, ia_d + d, ic);
+                        }
+                        rf = face_value2(c, sr, sxp, sgn, A(gwl, ia_d, ic), fd);
+                        ef = face_value2(c, se, sxp, sgn, A(gwl, ia_d, ic), fd);
+                    }
+                    const double dm = rf * dva[a];
+                    const double dme = rf * ef * dva[a];
+                    dmtot += dm;
+                    if (ax) {
+                        apply_cell(c, c->vola, a, ia - 1, ic, -dm, -dme, -dva[a]);
+                        apply_cell(c, c->vola, a, ia, ic, dm, dme, dva[a]);
+                    } else {
+                        apply_cell(c, c->vola, a, ic, ia - 1, -dm, -dme, -dva[a]);
+                        apply_cell(c, c->vola, a, ic, ia, dm, dme, dva[a]);
+                    }
+                }
+                A(dmf, ia, ic) = dmtot;
+            }
+    }
+    face_flux_ghosts(c->dmx, nx, ny, c->per_x, c->per_y);
+    face_flux_ghosts(c->dmy, ny, nx, c->per_y, c->per_x);
+    fcopy(c->mcell_lag, w->mcell);
+    finalize_cells(c);
+    if (remap_velocity) {
+        vzero(c->acc);
+        dual_face_pass(c, 1, c->dmx, dt);
+        dual_face_pass(c, 0, c->dmy, dt);
+        apply_dual_update(c);
+    }
+    if (nmat >= 2) refresh_normals(c, w->k, w->normals);
+}
+
 /* directional_pass, remap.cpp:469-589: the X (axis_x = 1) or Y remap of the
  * alternating-direction (AD) split scheme.  (along, cross) layouts as cf_pass:
  * X: (ia, ic) = (i, j); Y: (ia, ic) = (j, i). */
@@ -1836,7 +1995,7 @@ int h2do_set_lagrange(ctx_t* c, const h2d_lagrange* in) {
 
 /* remap_step, remap.cpp:1106-1126 (DirectCF and AD; not Direct) */
 int h2do_remap_step(ctx_t* c, double dt, int kind, int x_first, int remap_velocity, h2d_remap_diag* diag) {
-    if (kind != H2D_REMAP_DIRECTCF && kind != H2D_REMAP_AD) {
+    if (kind != H2D_REMAP_DIRECTCF && kind != H2D_REMAP_AD && kind != H2D_REMAP_DIRECT) {
         c->err.kind = H2D_ERR_INVALID;
         snprintf(c->err.what, sizeof c->err.what, "only the DirectCF and AD remaps are implemented");
         return H2D_ERR_INVALID;
@@ -1856,7 +2015,9 @@ int h2do_remap_step(ctx_t* c, double dt, int kind, int x_first, int remap_veloci
     c->diag = diag ? &local : NULL;
     if (setjmp(c->jb)) { c->diag = NULL; return c->err.kind; }
     make_work(c);
-    if (kind == H2D_REMAP_AD) {  /* remap.cpp:1110-1115 */
+    if (kind == H2D_REMAP_DIRECT) {  /* remap.cpp:1109 */
+        direct_pass(c, dt, remap_velocity);
+    } else if (kind == H2D_REMAP_AD) {  /* remap.cpp:1110-1115 */
         directional_pass(c, dt, x_first ? 1 : 0, remap_velocity);
         directional_pass(c, dt, x_first ? 0 : 1, remap_velocity);
     } else {

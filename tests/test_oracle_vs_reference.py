@@ -250,3 +250,66 @@ def test_error_parity_ad(ref, orc, scenario):
         s.set_lagrange(lag)
         out.append(_err(s, lambda s: s.remap_step(1.0, kind=abi.REMAP_AD)))
     assert out[0] == out[1] and out[0] is not None
+
+
+@pytest.mark.parametrize("bcx,bcy,order,degrade", [(BC_PERIODIC, BC_PERIODIC, 2, 1), (BC_WALL, BC_WALL, 2, 1),
+                                                   (BC_PERIODIC, BC_WALL, 1, 1), (BC_WALL, BC_PERIODIC, 2, 0)])
+@pytest.mark.parametrize("kind", ["gas", "front", "blobs"])
+def test_kinematic_remap_direct_bitwise(ref, orc, bcx, bcy, order, degrade, kind):
+    """The Direct (faces-only) engine, remap.cpp:593-724."""
+    nmat = 1 if kind == "gas" else 2
+    cfg = make_config(13, 11, 1.0, 1.0, 0.25, -0.5, bcx, bcy, eos=[(EOS_PERFECT, 1.4, 0.0)] * nmat,
+                      face_order=order, interface_degrade=degrade)
+    painted = helpers.random_state(cfg, hash((bcx, bcy, order, degrade, kind, "direct")) & 0xFFFF, kind, umax=0.25)
+    sr, so = _both(ref, orc, cfg, painted)
+    lag = helpers.kinematic(sr.download())
+    for vel in (True, False):
+        dr, do = abi.RemapDiag(), abi.RemapDiag()
+        sr2, so2 = _both(ref, orc, cfg, sr.download())
+        sr2.set_lagrange(lag)
+        so2.set_lagrange(lag)
+        sr2.remap_step(1.0, kind=abi.REMAP_DIRECT, remap_velocity=vel, diag=dr)
+        so2.remap_step(1.0, kind=abi.REMAP_DIRECT, remap_velocity=vel, diag=do)
+        assert helpers.bitwise_diff(sr2.download(), so2.download(), helpers.STATE_FIELDS) == []
+        assert (dr.max_k_violation, dr.k_clip_count, dr.mass_fix_count) == \
+               (do.max_k_violation, do.k_clip_count, do.mass_fix_count)
+
+
+@pytest.mark.parametrize("case,steps", [(cases.riemann2d(48), 80), (cases.triple_point(64, 32), 700),
+                                        (cases.shock_bubble(48), 30)])
+def test_run_loop_direct_bitwise(ref, orc, case, steps):
+    sr, so = _both(ref, orc, case.cfg, case.paint())
+    rr, er = helpers.run_capture(sr, steps, case.cfl, kind=abi.REMAP_DIRECT)
+    ro, eo = helpers.run_capture(so, steps, case.cfl, kind=abi.REMAP_DIRECT)
+    assert er == eo
+    assert np.array_equal(rr.dts, ro.dts)
+    assert (rr.floor_count, rr.diag) == (ro.floor_count, ro.diag)
+    assert helpers.bitwise_diff(sr.download(), so.download(), helpers.STATE_FIELDS) == []
+
+
+@pytest.mark.parametrize("scenario", ["cfl_face", "collapsed"])
+def test_error_parity_direct(ref, orc, scenario):
+    cfg = make_config(12, 10, 1.0, 1.0, bc_x=BC_PERIODIC, bc_y=BC_PERIODIC)
+    painted = helpers.random_state(cfg, 77, "gas", umax=0.2)
+    sr, so = _both(ref, orc, cfg, painted)
+    st = sr.download()
+    lag = helpers.kinematic(st)
+    g = abi.GHOST
+    if scenario == "cfl_face":
+        lag.u_half[g + 3, g + 5, 0] = 1.9  # one fast node: face volume > 0.9 cv
+        lag.u_half[g + 4, g + 5, 0] = 1.9
+    else:
+        lag.u_half[g + 3, g + 5, 0] = -3.0  # the cell's faces converge past its volume
+        lag.u_half[g + 4, g + 5, 0] = -3.0
+        lag.u_half[g + 3, g + 4, 0] = 3.0
+        lag.u_half[g + 4, g + 4, 0] = 3.0
+    res = []
+    for s in (sr, so):
+        s.set_lagrange(lag)
+        try:
+            s.remap_step(0.5, kind=abi.REMAP_DIRECT)
+            res.append(None)
+        except errors.SimError as e:
+            res.append((type(e).__name__, e.what, e.i, e.j))
+    assert res[0] == res[1]
+    assert res[0] is not None
