@@ -192,7 +192,7 @@ def pinned_state(nx, ny, nmat, cv):
 
 def run_product(args, world, rank, local, pg):
     from paper_2208_13409_b200 import abi as _abi
-    kind = _abi.REMAP_AD if args.remap == "ad" else _abi.REMAP_DIRECTCF
+    kind = {"ad": _abi.REMAP_AD, "direct": _abi.REMAP_DIRECT}.get(args.remap, _abi.REMAP_DIRECTCF)
     import paper_2208_13409_b200 as pkg
     from paper_2208_13409_b200 import abi
 
@@ -301,7 +301,8 @@ def run_product(args, world, rank, local, pg):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (init_case-equivalent painter, seeded)",
         "config": {"workload": case.name, "cells": cells, "materials": nmat, "steps_from": "t=0 after warmup",
-                   "scheme": ("AD split (X/Y alternating)" if kind == abi.REMAP_AD else "DirectCF") +
+                   "scheme": {abi.REMAP_AD: "AD split (X/Y alternating)", abi.REMAP_DIRECT: "Direct (faces only)"}
+                             .get(kind, "DirectCF") +
                              " face_order=2 LinearDiag interface_degrade", "cfl": case.cfl,
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "512 MiB write between timed steps; working set per step >> 126 MB L2"},
@@ -409,14 +410,14 @@ def run_reference(args, world, rank, pg):
     from paper_2208_13409_b200 import abi
     case = workload(args.workload)
     steps = args.steps
-    rk = abi.REMAP_AD if args.remap == "ad" else abi.REMAP_DIRECTCF
+    rk = {"ad": abi.REMAP_AD, "direct": abi.REMAP_DIRECT}.get(args.remap, abi.REMAP_DIRECTCF)
     v, ckind, n, secs = time_cpu(case, args.warmup, steps, rk)
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": args.warmup,
         "ms_per_step": secs * 1e3 / max(n, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (init_case-equivalent painter, seeded)", "impl": "reference",
         "config": {"workload": case.name, "cells": case.cells, "materials": case.cfg.nmat, "cfl": case.cfl,
-                   "scheme": "AD split" if args.remap == "ad" else "DirectCF",
+                   "scheme": {"ad": "AD split", "direct": "Direct"}.get(args.remap, "DirectCF"),
                    "parallelism": "single"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": ckind,
                          "sample": f"{case.name}: steps {args.warmup + 1}..{args.warmup + n}, single thread "
@@ -433,8 +434,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--remap", default="directcf", choices=["directcf", "ad"],
-                    help="remap engine: DirectCF (the path) or the AD split scheme (SURVEY 8f)")
+    ap.add_argument("--remap", default="directcf", choices=["directcf", "ad", "direct"],
+                    help="remap engine: DirectCF (the path), the AD split scheme or the Direct faces-only "
+                         "engine (SURVEY 8f)")
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -48,6 +48,7 @@ struct h2d_ctx {
     int dt_log_cap = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};  // one run-loop step per State parity
     cudaGraphExec_t graph_ad[2][2] = {};            // AD steps per (State parity, x_first)
+    cudaGraphExec_t graph_dir[2] = {nullptr, nullptr};  // Direct-engine steps per State parity
     double* ad_mem = nullptr;                       // AD Work planes between the passes
     TmaSet tma[2]{};                                // remap-tile TMA descriptors per State parity
     AdWork adw{};
@@ -228,6 +229,15 @@ int decode_error(h2d_ctx* c, bool in_run) {
     case PH_COLLAPSED: kind = H2D_ERR_CFL; msg = "collapsed Lagrangian cell"; located = true; break;
     case PH_GRAD_XFACE:
     case PH_GRAD_YFACE:
+        if (sub == kSubDirectCfl) {  // the Direct engine's face loop (remap.cpp:668-671)
+            kind = H2D_ERR_CFL;
+            msg = "CFL violation at face";
+            located = true;
+            break;
+        }
+        kind = H2D_ERR_SIM;
+        msg = "non-increasing centroid coordinates";
+        break;
     case PH_GRAD_CORNER:
     case PH_GRAD_DUALX:
     case PH_GRAD_DUALY:
@@ -272,7 +282,7 @@ int decode_error(h2d_ctx* c, bool in_run) {
     // the AD scan and face keys are (cross, along, 2 * axis_x + ...): a Y pass
     // stores (i, j) as (inner, outer) swapped
     const int adp = ph >= PH_AD_COLLAPSED && ph < PH_AD_COLLAPSED + 10 ? (ph - PH_AD_COLLAPSED) % 5 : -1;
-    const bool ad_y = (adp == 0 || adp == 1) && !(sub >> 1);
+    const bool ad_y = ((adp == 0 || adp == 1) && !(sub >> 1)) || (ph == PH_GRAD_YFACE && sub == kSubDirectCfl);
     const int i = located ? (ad_y ? outer : inner) : -1, j = located ? (ad_y ? inner : outer) : -1;
     // SimError::format appends the location only for i >= 0 || j >= 0 (errors.hpp:23)
     if (located && (i >= 0 || j >= 0)) w += " at cell (" + std::to_string(i) + "," + std::to_string(j) + ")";
@@ -384,6 +394,26 @@ int ensure_graphs(h2d_ctx* c) {
         c->graph_kernels = launch_count() - before;
         add_launches(-c->graph_kernels);  // captured, not executed
         const cudaError_t e = cudaGraphInstantiate(&c->graph[p], g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+    }
+    return 0;
+}
+
+// Direct-engine run-loop steps (remap.cpp:593-724), captured like DirectCF's
+int ensure_graphs_dir(h2d_ctx* c) {
+    if (c->graph_dir[0] && c->graph_dir[1]) return 0;
+    for (int p = 0; p < 2; ++p) {
+        cudaGraph_t g = nullptr;
+        const long long before = launch_count();
+        CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+        Dev d = make_dev(c, p, 1);
+        d.direct = 1;
+        launch_step(d, !c->is_block, c->st);
+        CK(cudaStreamEndCapture(c->st, &g));
+        c->graph_kernels = launch_count() - before;
+        add_launches(-c->graph_kernels);
+        const cudaError_t e = cudaGraphInstantiate(&c->graph_dir[p], g, 0);
         cudaGraphDestroy(g);
         CK(e);
     }
@@ -747,6 +777,8 @@ void h2d_destroy(h2d_ctx* c) {
     for (auto& gp : c->graph_ad)
         for (auto& g : gp)
             if (g) cudaGraphExecDestroy(g);
+    for (auto& g : c->graph_dir)
+        if (g) cudaGraphExecDestroy(g);
     if (c->ad_mem) cudaFree(c->ad_mem);
     if (c->st) cudaStreamSynchronize(c->st);
     if (c->arena) cudaFree(c->arena);
@@ -908,8 +940,9 @@ int h2d_set_lagrange(h2d_ctx* c, const h2d_lagrange* in) {
 
 int h2d_remap_step(h2d_ctx* c, double dt, int kind, int x_first, int remap_velocity, h2d_remap_diag* diag) {
     cudaSetDevice(c->device);
-    if (kind != H2D_REMAP_DIRECTCF && !(kind == H2D_REMAP_AD && !c->is_block && c->nmat <= 2)) {
-        set_err(c, H2D_ERR_INVALID, "only the DirectCF and (single-domain) AD remaps are implemented on the device");
+    if (kind != H2D_REMAP_DIRECTCF && !(kind == H2D_REMAP_AD && !c->is_block && c->nmat <= 2) &&
+        !(kind == H2D_REMAP_DIRECT && !c->is_block)) {
+        set_err(c, H2D_ERR_INVALID, "the device runs DirectCF, Direct and (single-domain, <= 2 materials) AD");
         return H2D_ERR_INVALID;
     }
     if (!c->have_lag) {
@@ -919,7 +952,8 @@ int h2d_remap_step(h2d_ctx* c, double dt, int kind, int x_first, int remap_veloc
     if (kind == H2D_REMAP_AD)
         if (int rc = ensure_ad(c)) return rc;
     if (int rc = ctl_reset(c)) return rc;
-    const Dev d = make_dev(c, c->cur, remap_velocity != 0);
+    Dev d = make_dev(c, c->cur, remap_velocity != 0);
+    d.direct = kind == H2D_REMAP_DIRECT;
     launch_begin(c->ctl, 1, dt, c->st);
     if (kind == H2D_REMAP_AD)
         launch_remap_ad(d, c->adw, x_first != 0, remap_velocity != 0, 0, c->st);
@@ -942,9 +976,9 @@ int h2d_remap_step(h2d_ctx* c, double dt, int kind, int x_first, int remap_veloc
 int h2d_run(h2d_ctx* c, h2d_run_args* a) {
     cudaSetDevice(c->device);
     a->steps_done = 0;
-    const bool ad = a->remap_kind == H2D_REMAP_AD;
-    if (a->remap_kind != H2D_REMAP_DIRECTCF && !(ad && !c->is_block && c->nmat <= 2)) {
-        set_err(c, H2D_ERR_INVALID, "only the DirectCF and (single-domain) AD remaps are implemented on the device");
+    const bool ad = a->remap_kind == H2D_REMAP_AD, dir = a->remap_kind == H2D_REMAP_DIRECT;
+    if (a->remap_kind != H2D_REMAP_DIRECTCF && !(ad && !c->is_block && c->nmat <= 2) && !(dir && !c->is_block)) {
+        set_err(c, H2D_ERR_INVALID, "the device runs DirectCF, Direct and (single-domain, <= 2 materials) AD");
         return H2D_ERR_INVALID;
     }
     const int cap = a->max_steps > 0 ? a->max_steps : kRunLogCap;
@@ -966,7 +1000,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
     if (int rc = ctl_push(c)) return rc;
     int parity = c->cur;
     int rc = 0;
-    if ((rc = ad ? ensure_graphs_ad(c) : ensure_graphs(c))) return rc;
+    if ((rc = ad ? ensure_graphs_ad(c) : (dir ? ensure_graphs_dir(c) : ensure_graphs(c)))) return rc;
     enqueue_cfl_next(c);
     start_first(c);
     // Launch in chunks; the device control block turns every kernel after the
@@ -983,6 +1017,9 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
             if (ad) {  // x_first = s.step % 2 == 0 (harness.cpp:401)
                 CK(cudaGraphLaunch(c->graph_ad[parity][(step0 + q) % 2 == 0], c->st));
                 add_launches(c->graph_kernels_ad);
+            } else if (dir) {
+                CK(cudaGraphLaunch(c->graph_dir[parity], c->st));
+                add_launches(c->graph_kernels);
             } else if ((rc = launch_step_graph(c, parity))) {
                 return rc;
             }
@@ -1170,13 +1207,15 @@ int h2d_load_state(h2d_ctx* c, const char* path) {
 
 int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_kind, float ms[8]) {
     cudaSetDevice(c->device);
-    const bool ad = remap_kind == H2D_REMAP_AD;
-    if (!(remap_kind == H2D_REMAP_DIRECTCF || (ad && !c->is_block && c->nmat <= 2))) {
-        set_err(c, H2D_ERR_INVALID, "h2d_step_timed: DirectCF or (single-domain) AD only");
+    const bool ad = remap_kind == H2D_REMAP_AD, dir = remap_kind == H2D_REMAP_DIRECT;
+    if (!(remap_kind == H2D_REMAP_DIRECTCF || (ad && !c->is_block && c->nmat <= 2) || (dir && !c->is_block))) {
+        set_err(c, H2D_ERR_INVALID, "h2d_step_timed: DirectCF, Direct or (single-domain) AD only");
         return H2D_ERR_INVALID;
     }
     if (ad)
         if (int rc = ensure_graphs_ad(c)) return rc;
+    if (dir)
+        if (int rc = ensure_graphs_dir(c)) return rc;
     const int xf = c->hctl->step % 2 == 0;  // harness.cpp:401
     if (!c->ev[0])
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
@@ -1197,6 +1236,7 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_k
         Dev d = make_dev(c, c->cur, 1);
         d.scan_nodes = 1;  // as the run-loop graph
         d.diag = 1;
+        d.direct = dir;
         CK(cudaEventRecord(c->ev[0], c->st));
         launch_step_start(d, c->st);
         CK(cudaEventRecord(c->ev[1], c->st));
@@ -1240,6 +1280,9 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_k
         if (ad) {
             CK(cudaGraphLaunch(c->graph_ad[c->cur][xf], c->st));
             add_launches(c->graph_kernels_ad);
+        } else if (dir) {
+            CK(cudaGraphLaunch(c->graph_dir[c->cur], c->st));
+            add_launches(c->graph_kernels);
         } else if (int rc = launch_step_graph(c, c->cur)) {
             return rc;
         }

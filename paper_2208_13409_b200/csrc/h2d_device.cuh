@@ -130,6 +130,9 @@ H2D_DEV void raise(Ctl* c, uint64_t key) { atomicMin(&c->err_key, (unsigned long
 constexpr int kMatSlots = 3;
 // error sub-index of finalize's "non-positive cell mass" (after the material indices)
 constexpr int kSubCellMass = 7;
+// the Direct engine's face loop raises its CFL check and its gradient errors
+// in one phase (loop order), sub 1 / 2 (DirectCF's gradient errors: sub 0)
+constexpr int kSubDirectCfl = 1, kSubDirectGrad = 2;
 
 // Half-open range of GLOBAL indices [i0, i1) x [j0, j1).
 struct Rng {
@@ -169,6 +172,7 @@ struct Dev {
     double a1, a2;
     int face_order, corner_diag, degrade, remap_velocity;
     int corner;  // CornerScheme (H2D_CORNER_*): Upwind, AvgMin, LinearXY, LinearDiag, Multid
+    int direct;  // 1: the Direct engine (faces only) instead of DirectCF
 
     // current (read) State
     const double *m[kMatSlots], *e[kMatSlots], *k[kMatSlots], *m_mix, *e_mix, *rho_mix, *p_mix, *nrx, *nry, *ux, *uy;

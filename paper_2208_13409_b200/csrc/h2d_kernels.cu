@@ -768,7 +768,8 @@ template <int NM>
 struct Tile {
     int ci0, cj0;  // origin of both regions: (i0 - 2, j0 - 2)
     double *hx, *hy, *fdx, *fdy, *fxdv, *fydv;  // nodes
-    double *vl, *rho[kMatSlots], *el[kMatSlots], *kk[kMatSlots], *xl2x, *xl2y, *ifd;  // cells
+    double *vl, *rho[kMatSlots], *el[kMatSlots], *kk[kMatSlots], *xl2x, *xl2y, *ifd, *ifd2;  // cells
+    // (ifd2: the Direct engine's Y-displaced interfaces; ifd its X-displaced ones)
     // flux items of one sub-phase (X faces, then Y faces, then corners share
     // the buffer): dm, dme, dva per material
     double* it[3][kMatSlots];
@@ -802,13 +803,13 @@ struct Tile {
     }
 };
 
-template <int NM>
+template <int NM, bool DIR = false>
 constexpr size_t remap_smem_bytes() {
-    return sizeof(double) * (6 * al16(RNN) + (NM == 1 ? RCELL1 : RCELL2 + 3 * (NM - 2)) * al16(RNC) +
+    return sizeof(double) * (6 * al16(RNN) + (NM == 1 ? RCELL1 : RCELL2 + 3 * (NM - 2) + (DIR ? 1 : 0)) * al16(RNC) +
                              3 * NM * al16(NIT)) + 128;
 }
 
-template <int NM>
+template <int NM, bool DIR = false>
 __device__ __forceinline__ Tile<NM> carve_tile(char* base, int ci0, int cj0) {
     Tile<NM> T;
     T.ci0 = ci0;
@@ -835,6 +836,7 @@ __device__ __forceinline__ Tile<NM> carve_tile(char* base, int ci0, int cj0) {
     if (NM >= 2) {
         for (int a = 0; a < NM; ++a) T.kk[a] = take(RNC);
         T.ifd = take(RNC);
+        T.ifd2 = DIR ? take(RNC) : T.ifd;
     }
     for (int k = 0; k < 3; ++k)
         for (int a = 0; a < NM; ++a) T.it[k][a] = take(NIT);
@@ -887,11 +889,31 @@ __device__ __noinline__ Pair2 multid_face_tile(double dgx, double dgy, const dou
     return r;
 }
 
+// The interface rectangle of donor (di, dj) (remap.cpp:807-824): RM 0 the
+// DirectCF rectangle through the Lagrangian face midpoints; the Direct
+// engine's X- (RM 1) or Y-displaced (RM 2) rectangle (remap.cpp:616-640)
+template <int RM, int NM>
+__device__ __forceinline__ void iface_rect(const Dev& d, const Tile<NM>& T, int di, int dj, double& lox, double& loy,
+                                           double& hix, double& hiy) {
+    const double cx = d.x0 + (di + 0.5) * d.dx, cy = d.y0 + (dj + 0.5) * d.dy;
+    lox = cx - 0.5 * d.dx + (RM == 2 ? 0.0 : T.fdx[T.n(di, dj)]);
+    loy = cy - 0.5 * d.dy + (RM == 1 ? 0.0 : T.fdy[T.n(di, dj)]);
+    hix = cx + 0.5 * d.dx + (RM == 2 ? 0.0 : T.fdx[T.n(di + 1, dj)]);
+    hiy = cy + 0.5 * d.dy + (RM == 1 ? 0.0 : T.fdy[T.n(di, dj + 1)]);
+    if (RM == 1) {  // cen.y -+ hy exactly (no added displacement)
+        loy = cy - 0.5 * d.dy;
+        hiy = cy + 0.5 * d.dy;
+    } else if (RM == 2) {
+        lox = cx - 0.5 * d.dx;
+        hix = cx + 0.5 * d.dx;
+    }
+}
+
 // The three-material split of a flux box of donor (di, dj) (oracle
 // split_flux, nmat == 3): a mixed donor gives k_r * dvol to the material
 // outside its interface pair and splits the rest at the pair's interface; a
 // pure donor gives everything to its largest fraction.
-template <int NM>
+template <int NM, int RM = 0>
 __device__ __forceinline__ void split_flux3(const Dev& d, const Tile<NM>& T, int di, int dj, double blox,
                                             double bloy, double bhix, double bhiy, double dvol, double* dva) {
     const int c = T.c(di, dj);
@@ -907,11 +929,9 @@ __device__ __forceinline__ void split_flux3(const Dev& d, const Tile<NM>& T, int
     pair3(k, lo, hi);
     const int r = 3 - lo - hi;
     const int g = ix(d, di, dj);
-    const double nx = d.nrx[g], ny = d.nry[g], dd = T.ifd[c];
-    const double cx = d.x0 + (di + 0.5) * d.dx, cy = d.y0 + (dj + 0.5) * d.dy;
-    const double lox = cx - 0.5 * d.dx + T.fdx[T.n(di, dj)], loy = cy - 0.5 * d.dy + T.fdy[T.n(di, dj)];
-    const double hix = cx + 0.5 * d.dx + T.fdx[T.n(di + 1, dj)];
-    const double hiy = cy + 0.5 * d.dy + T.fdy[T.n(di, dj + 1)];
+    const double nx = d.nrx[g], ny = d.nry[g], dd = RM == 2 ? T.ifd2[c] : T.ifd[c];
+    double lox, loy, hix, hiy;
+    iface_rect<RM>(d, T, di, dj, lox, loy, hix, hiy);
     const double rcx = 0.5 * (lox + hix), rcy = 0.5 * (loy + hiy);
     const double bcx = 0.5 * (blox + bhix), bcy = 0.5 * (bloy + bhiy);
     const double bw = bhix - blox, bh = bhiy - bloy;
@@ -931,25 +951,23 @@ __device__ __forceinline__ void split_flux3(const Dev& d, const Tile<NM>& T, int
 }
 
 // box_frac0 + split_flux, remap.cpp:243-268, donor cell (di, dj) of the tile
-template <int NM>
+template <int NM, int RM = 0>
 __device__ __forceinline__ void split_flux_t(const Dev& d, const Tile<NM>& T, int di, int dj, double blox,
                                              double bloy, double bhix, double bhiy, double dvol, double* dva) {
     dva[0] = dvol;
     if (NM == 1) return;
     dva[1] = 0.0;
     if (NM == 3) {
-        split_flux3(d, T, di, dj, blox, bloy, bhix, bhiy, dvol, dva);
+        split_flux3<NM, RM>(d, T, di, dj, blox, bloy, bhix, bhiy, dvol, dva);
         return;
     }
     const int c = T.c(di, dj);
     const double k0 = T.kk[0][c];
     if (is_mixed(k0)) {
         const int g = ix(d, di, dj);  // mixed donors only: the normal from HBM (L2)
-        const double nx = d.nrx[g], ny = d.nry[g], dd = T.ifd[c];
-        const double cx = d.x0 + (di + 0.5) * d.dx, cy = d.y0 + (dj + 0.5) * d.dy;
-        const double lox = cx - 0.5 * d.dx + T.fdx[T.n(di, dj)], loy = cy - 0.5 * d.dy + T.fdy[T.n(di, dj)];
-        const double hix = cx + 0.5 * d.dx + T.fdx[T.n(di + 1, dj)];
-        const double hiy = cy + 0.5 * d.dy + T.fdy[T.n(di, dj + 1)];
+        const double nx = d.nrx[g], ny = d.nry[g], dd = RM == 2 ? T.ifd2[c] : T.ifd[c];
+        double lox, loy, hix, hiy;
+        iface_rect<RM>(d, T, di, dj, lox, loy, hix, hiy);
         const double rcx = 0.5 * (lox + hix), rcy = 0.5 * (loy + hiy);
         const double bcx = 0.5 * (blox + bhix), bcy = 0.5 * (bloy + bhiy);
         const double bw = bhix - blox, bh = bhiy - bloy;
@@ -972,32 +990,50 @@ __device__ __forceinline__ void split_flux_t(const Dev& d, const Tile<NM>& T, in
 
 // Face flux (remap.cpp:850-918) of the X (AX = 1, at node i, row j) or Y
 // (AX = 0, at column i, node row j) face; returns the face's dmx / dmy entry.
-template <int NM, int AX, bool XC = false>
+template <int NM, int AX, bool XC = false, bool DIR = false>
 __device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, int i, int j, double dt,
                                               double* odm, double* odme, double* odva) {
     const int qn = T.n(i, j);
     const double dvol = AX ? T.fxdv[qn] : T.fydv[qn];
     double dmtot = 0.0;
     double dva[NM] = {}, rfv[NM] = {}, efv[NM] = {};
-    if (dvol != 0.0) {
+    bool cfl_ok = true;
+    if (DIR && dvol != 0.0 && fabs(dvol) > kCflFrac * d.cv) {  // the Direct face loop's CFL check (remap.cpp:668-671)
+        cfl_ok = false;
+        const int ia = AX ? i : j, ic = AX ? j : i;
+        if (AX ? own_xface(d, i, j) : own_yface(d, i, j))
+            raise(d.ctl, ekey(AX ? PH_GRAD_XFACE : PH_GRAD_YFACE, ic, ia, kSubDirectCfl));
+    }
+    if (dvol != 0.0 && cfl_ok) {
         const int ia = AX ? i : j, ic = AX ? j : i;
         const int ia_d = dvol > 0.0 ? ia - 1 : ia;
         const double sgn = dvol > 0.0 ? 1.0 : -1.0;
         const int cdi = AX ? ia_d : ic, cdj = AX ? ic : ia_d;
-        // the flux window [wlo, whi] of cf_face_flux (remap.cpp:29-31, same
-        // bits; dvol != 0 implies whi > wlo)
-        const int q1 = AX ? T.n(i, j + 1) : T.n(i + 1, j);
-        const double wlo = AX ? d.y0 + j * d.dy + rmax(0.0, dt * T.hy[qn]) : d.x0 + i * d.dx + rmax(0.0, dt * T.hx[qn]);
-        const double whi = AX ? d.y0 + (j + 1) * d.dy + rmin(0.0, dt * T.hy[q1])
-                              : d.x0 + (i + 1) * d.dx + rmin(0.0, dt * T.hx[q1]);
-        const double wwin = whi - wlo;
-        const double width = dvol / wwin;
-        const double f0pos = AX ? d.x0 + ia * d.dx : d.y0 + ia * d.dy;
-        const double blo = rmin(f0pos, f0pos + width), bhi = rmax(f0pos, f0pos + width);
+        double wlo, whi, blo, bhi;
+        if (DIR) {  // face_flux_box (remap.cpp:325-334)
+            const double fd = AX ? T.fdx[qn] : T.fdy[qn];
+            const double f0pos = AX ? d.x0 + ia * d.dx : d.y0 + ia * d.dy;
+            blo = rmin(f0pos, f0pos + fd);
+            bhi = rmax(f0pos, f0pos + fd);
+            wlo = AX ? d.y0 + ic * d.dy : d.x0 + ic * d.dx;
+            whi = AX ? d.y0 + (ic + 1) * d.dy : d.x0 + (ic + 1) * d.dx;
+        } else {
+            // the flux window [wlo, whi] of cf_face_flux (remap.cpp:29-31, same
+            // bits; dvol != 0 implies whi > wlo)
+            const int q1 = AX ? T.n(i, j + 1) : T.n(i + 1, j);
+            wlo = AX ? d.y0 + j * d.dy + rmax(0.0, dt * T.hy[qn]) : d.x0 + i * d.dx + rmax(0.0, dt * T.hx[qn]);
+            whi = AX ? d.y0 + (j + 1) * d.dy + rmin(0.0, dt * T.hy[q1]) : d.x0 + (i + 1) * d.dx + rmin(0.0, dt * T.hx[q1]);
+            const double wwin = whi - wlo;
+            const double width = dvol / wwin;
+            const double f0pos = AX ? d.x0 + ia * d.dx : d.y0 + ia * d.dy;
+            blo = rmin(f0pos, f0pos + width);
+            bhi = rmax(f0pos, f0pos + width);
+        }
+        constexpr int RM = DIR ? (AX ? 1 : 2) : 0;
         if (AX)
-            split_flux_t<NM>(d, T, cdi, cdj, blo, wlo, bhi, whi, dvol, dva);
+            split_flux_t<NM, RM>(d, T, cdi, cdj, blo, wlo, bhi, whi, dvol, dva);
         else
-            split_flux_t<NM>(d, T, cdi, cdj, wlo, blo, whi, bhi, dvol, dva);
+            split_flux_t<NM, RM>(d, T, cdi, cdj, wlo, blo, whi, bhi, dvol, dva);
         bool bad = false;
         const int cm = AX ? T.c(ia_d - 1, ic) : T.c(ic, ia_d - 1);
         const int cc = AX ? T.c(ia_d, ic) : T.c(ic, ia_d);
@@ -1035,7 +1071,7 @@ __device__ __forceinline__ double face_item_t(const Dev& d, const Tile<NM>& T, i
             efv[a] = ef;
         }
         if (bad && (AX ? own_xface(d, i, j) : own_yface(d, i, j)))
-            raise(d.ctl, ekey(AX ? PH_GRAD_XFACE : PH_GRAD_YFACE, ic, ia, 0));
+            raise(d.ctl, ekey(AX ? PH_GRAD_XFACE : PH_GRAD_YFACE, ic, ia, DIR ? kSubDirectGrad : 0));
     }
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
@@ -1378,7 +1414,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 // XC: the AvgMin / LinearXY / Multid corner schemes compiled in (their
 // out-of-line calls cost the default kernels registers; see launch_remap_tile)
-template <int NM, bool XC = false>
+// DIR: the Direct engine (remap.cpp:593-724): face volumes fd * width, the
+// X / Y-displaced interfaces, no corner fluxes (items and dmc zero)
+template <int NM, bool XC = false, bool DIR = false>
 __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
     pdl_enter();
     extern __shared__ __align__(128) char smem_raw[];
@@ -1400,7 +1438,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
     const int sx = tile_shift(d);
     const int i0 = rg.i0 - sx + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-    const Tile<NM> T = carve_tile<NM>(smem, i0 - G, j0 - G);
+    const Tile<NM> T = carve_tile<NM, DIR>(smem, i0 - G, j0 - G);
     // ---- phase 0: one thread stages the tile + halo with TMA (2D boxes of
     // the planes, zero-filled past the plane): u_half on the node region,
     // e_lag, m, k on the cell region.  T.rho holds m and T.vl (1 material) /
@@ -1475,22 +1513,34 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
         double fdx = 0.0, fdy = 0.0, fxv = 0.0, fyv = 0.0;
         if (in(d.win_n, i, j)) {
             const double hx = T.hx[t], hy = T.hy[t];
-            const double cfv = fabs((hx * dt) * (hy * dt));
-            if (cfv > kCflFrac * cv && own_node(d, i, j)) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
+            if (!DIR) {
+                const double cfv = fabs((hx * dt) * (hy * dt));
+                if (cfv > kCflFrac * cv && own_node(d, i, j)) raise(d.ctl, ekey(PH_CFL_CORNER, j, i, 0));
+            }
             // faces on the region's last node row / column feed no region cell
             if (j < ny + G && j < T.cj0 + RNH - 1 && j + 1 < d.win_n.j1) {
                 const double ux1 = T.hx[t + RNW], uy1 = T.hy[t + RNW];
                 fdx = 0.5 * (hx + ux1) * dt;
-                double wl, wh;
-                face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * hx, dt * hy, dt * ux1, dt * uy1, fxv, wl, wh);
-                if (fabs(fxv) > kCflFrac * cv && own_xface(d, i, j)) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
+                if (DIR) {
+                    fxv = fdx * d.dy;  // remap.cpp:663
+                } else {
+                    double wl, wh;
+                    face_flux(d.y0 + j * d.dy, d.y0 + (j + 1) * d.dy, dt * hx, dt * hy, dt * ux1, dt * uy1, fxv, wl,
+                              wh);
+                    if (fabs(fxv) > kCflFrac * cv && own_xface(d, i, j)) raise(d.ctl, ekey(PH_CFL_XFACE, j, i, 0));
+                }
             }
             if (i < nx + G && i < T.ci0 + RNW - 1 && i + 1 < d.win_n.i1) {
                 const double ux1 = T.hx[t + 1], uy1 = T.hy[t + 1];
                 fdy = 0.5 * (hy + uy1) * dt;
-                double wl, wh;
-                face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * hy, dt * hx, dt * uy1, dt * ux1, fyv, wl, wh);
-                if (fabs(fyv) > kCflFrac * cv && own_yface(d, i, j)) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
+                if (DIR) {
+                    fyv = fdy * d.dx;
+                } else {
+                    double wl, wh;
+                    face_flux(d.x0 + i * d.dx, d.x0 + (i + 1) * d.dx, dt * hy, dt * hx, dt * uy1, dt * ux1, fyv, wl,
+                              wh);
+                    if (fabs(fyv) > kCflFrac * cv && own_yface(d, i, j)) raise(d.ctl, ekey(PH_CFL_YFACE, j, i, 0));
+                }
             }
         }
         T.fdx[t] = fdx;
@@ -1516,8 +1566,13 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
             if (ri == i && rj == j) return -dv;
             return 0.0;
         };
-        double v = cv + T.fxdv[q10] - T.fxdv[q00] + T.fydv[q01] - T.fydv[q00];
-        v += cterm(q00, i, j) + cterm(q10, i + 1, j) + cterm(q01, i, j + 1) + cterm(q11, i + 1, j + 1);
+        double v;
+        if (DIR) {  // remap.cpp:605-606
+            v = cv + (T.fdx[q10] - T.fdx[q00]) * d.dy + (T.fdy[q01] - T.fdy[q00]) * d.dx;
+        } else {
+            v = cv + T.fxdv[q10] - T.fxdv[q00] + T.fydv[q01] - T.fydv[q00];
+            v += cterm(q00, i, j) + cterm(q10, i + 1, j) + cterm(q01, i, j + 1) + cterm(q11, i + 1, j + 1);
+        }
         if (v <= 0.0 && own_cell(d, i, j)) raise(d.ctl, ekey(PH_COLLAPSED, j, i, 0));
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
@@ -1540,15 +1595,19 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
                 pair3(k, lo, hi);
                 k0 = k[3 - lo - hi] > 0.0 ? k[lo] / (k[lo] + k[hi]) : k[lo];
             }
-            double dd = 0.0;
+            double dd = 0.0, dd2 = 0.0;
             if (mixed) {
-                const double cx = d.x0 + (i + 0.5) * d.dx, cy = d.y0 + (j + 0.5) * d.dy;
                 const int g = ix(d, i, j);
-                dd = place_interface(k0, d.nrx[g], d.nry[g], cx - 0.5 * d.dx + T.fdx[q00],
-                                     cy - 0.5 * d.dy + T.fdy[q00], cx + 0.5 * d.dx + T.fdx[q10],
-                                     cy + 0.5 * d.dy + T.fdy[q01]);
+                double lox, loy, hix, hiy;
+                iface_rect<DIR ? 1 : 0>(d, T, i, j, lox, loy, hix, hiy);
+                dd = place_interface(k0, d.nrx[g], d.nry[g], lox, loy, hix, hiy);
+                if (DIR) {  // the Y-displaced interface of the Direct engine
+                    iface_rect<2>(d, T, i, j, lox, loy, hix, hiy);
+                    dd2 = place_interface(k0, d.nrx[g], d.nry[g], lox, loy, hix, hiy);
+                }
             }
             T.ifd[t] = dd;
+            if (DIR) T.ifd2[t] = dd2;
         }
     }
     __syncthreads();
@@ -1592,7 +1651,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
 #pragma unroll
         for (int a = 0; a < NM; ++a) dva[a] = dm[a] = dme[a] = 0.0;
         if (ia <= min(nx, rg.i1) && ic < min(ny, rg.j1)) {
-            const double tot = face_item_t<NM, 1, XC>(d, T, ia, ic, dt, dm, dme, dva);
+            const double tot = face_item_t<NM, 1, XC, DIR>(d, T, ia, ic, dt, dm, dme, dva);
             if (ia < i0 + RTX || ia == min(nx, rg.i1)) d.dmx[ix(d, ia, ic)] = tot;
         }
 #pragma unroll
@@ -1617,7 +1676,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
 #pragma unroll
         for (int a = 0; a < NM; ++a) dva[a] = dm[a] = dme[a] = 0.0;
         if (ic < min(nx, rg.i1) && ja <= min(ny, rg.j1)) {
-            const double tot = face_item_t<NM, 0, XC>(d, T, ic, ja, dt, dm, dme, dva);
+            const double tot = face_item_t<NM, 0, XC, DIR>(d, T, ic, ja, dt, dm, dme, dva);
             if (ja < j0 + RTY || ja == min(ny, rg.j1)) d.dmy[ix(d, ic, ja)] = tot;
         }
 #pragma unroll
@@ -1644,7 +1703,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
         for (int a = 0; a < NM; ++a) dva[a] = dm[a] = dme[a] = 0.0;
         const int ni1 = min(nx, rg.i1), nj1 = min(ny, rg.j1);
         if (ni <= ni1 && nj <= nj1) {
-            const double tot = corner_item_t<NM, XC>(d, T, ni, nj, dt, dm, dme, dva);
+            const double tot = DIR ? 0.0 : corner_item_t<NM, XC>(d, T, ni, nj, dt, dm, dme, dva);
             if ((ni < i0 + RTX || ni == ni1) && (nj < j0 + RTY || nj == nj1)) d.dmc[ix(d, ni, nj)] = tot;
         }
 #pragma unroll
@@ -1657,7 +1716,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
     __syncthreads();
     if (!act) return;
     const bool own = own_cell(d, i, j);
-    {
+    if (!DIR) {  // (the Direct engine has no corner fluxes)
         const int cq[4] = {tx + ty * (RTX + 1), tx + 1 + ty * (RTX + 1), tx + (ty + 1) * (RTX + 1),
                            tx + 1 + (ty + 1) * (RTX + 1)};
         const int ndi[4] = {i, i + 1, i, i + 1}, ndj[4] = {j, j, j + 1, j + 1};
@@ -3356,6 +3415,12 @@ void remap_init() {
     cudaFuncSetAttribute(k_remap_tile<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<1>());
     cudaFuncSetAttribute(k_remap_tile<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<2>());
     cudaFuncSetAttribute(k_remap_tile<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)remap_smem_bytes<3>());
+    cudaFuncSetAttribute(k_remap_tile<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)remap_smem_bytes<1, true>());
+    cudaFuncSetAttribute(k_remap_tile<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)remap_smem_bytes<2, true>());
+    cudaFuncSetAttribute(k_remap_tile<3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)remap_smem_bytes<3, true>());
     done = true;
 }
 
@@ -3462,6 +3527,15 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
     rt.i0 -= tile_shift(d);
     const dim3 gft = tiles_of(rt, RTX, RTY);
     const bool xc = d.corner != CS_UPWIND && d.corner != CS_LINEARDIAG;  // the extended corner schemes
+    if (d.direct) {  // the Direct engine (remap.cpp:593-724)
+        if (d.nmat == 3)
+            pdl(k_remap_tile<3, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<3, true>(), s, d, *d.tma);
+        else if (d.nmat == 2)
+            pdl(k_remap_tile<2, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2, true>(), s, d, *d.tma);
+        else
+            pdl(k_remap_tile<1, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<1, true>(), s, d, *d.tma);
+        return;
+    }
     if (d.nmat == 3)
         xc ? pdl(k_remap_tile<3, true>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma)
            : pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);

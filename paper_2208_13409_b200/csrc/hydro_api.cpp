@@ -267,8 +267,6 @@ LagrangeResult lagrange_step(const State& s, const MaterialSet& mats, double dt,
 
 State remap_step(const State& s, const MaterialSet& mats, const LagrangeResult& lag, double dt, RemapKind kind,
                  const ReconConfig& rc, bool x_first, bool remap_velocity, RemapDiag* diag) {
-    if (kind == RemapKind::Direct)
-        throw std::invalid_argument("hydro2d-b200 implements the DirectCF and AD remaps (not RemapKind::Direct)");
     h2d_ctx* h = load(s, &mats, {}, rc);
     h2d_lagrange in;
     std::memset(&in, 0, sizeof in);

@@ -15,9 +15,8 @@ Python mirror of the reference's driver layer over the CUDA product:
   same arguments and the same result keys.
 
 The CLI (``python -m paper_2208_13409_b200 run <config>``) is in
-``__main__.py``.  Schemes: DirectCF and AD run on the device; the Direct
-engine and the AvgMin / LinearXY / Multid corner schemes are not built
- and raise like the device refuses them.
+``__main__.py``.  Every scheme (DirectCF, Direct, AD) and corner scheme
+runs on the device.
 """
 from __future__ import annotations
 

@@ -151,8 +151,12 @@ def test_run_case_dict_and_hook():
     seen = []
     rep = frontend.run(frontend.build_case("haas", 8), hook=lambda st, dg: seen.append((st.step, int(dg["step"]))))
     assert [a for a, _ in seen] == [b for _, b in seen] == list(range(1, rep.steps + 1))
-    with pytest.raises(errors.DeviceError):
-        frontend.run_case("haas", divisor=8, scheme="Direct")
+    ref = helpers.ref_lib()
+    if ref is not None:  # every engine runs on the device, e.g. the Direct one, as the reference driver does
+        d2 = frontend.run_case("haas", divisor=8, scheme="Direct")
+        rc, what, want, out, steps, fin = ref_run_case(ref, "haas", 8, scheme="Direct")
+        assert rc == 0 and d2["steps"] == steps and d2["time"] == out[0]
+        assert d2["l2_rho_vs_initial"] == out[1] and d2["l2_k_vs_initial"] == out[2]
 
 
 @pytest.mark.gpu

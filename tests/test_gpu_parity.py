@@ -271,3 +271,68 @@ def test_error_parity_ad(gpu, orc, scenario):
         except errors.SimError as e:
             out.append((type(e).__name__, e.what, e.i, e.j))
     assert out[0] == out[1] and out[0] is not None
+
+
+# ---- the Direct (faces-only) engine, remap.cpp:593-724 --------------------------------
+
+@pytest.mark.parametrize("bcx,bcy,order,degrade", [(BC_PERIODIC, BC_PERIODIC, 2, 1), (BC_WALL, BC_WALL, 2, 1),
+                                                   (BC_PERIODIC, BC_WALL, 1, 1), (BC_WALL, BC_PERIODIC, 2, 0)])
+@pytest.mark.parametrize("kind", ["gas", "front", "blobs"])
+def test_kinematic_remap_direct_bitwise(gpu, orc, bcx, bcy, order, degrade, kind):
+    nmat = 1 if kind == "gas" else 2
+    cfg = make_config(13, 11, 1.0, 1.0, 0.25, -0.5, bcx, bcy, eos=[(EOS_PERFECT, 1.4, 0.0)] * nmat,
+                      face_order=order, interface_degrade=degrade)
+    painted = helpers.random_state(cfg, hash((bcx, bcy, order, degrade, kind, "direct")) & 0xFFFF, kind, umax=0.25)
+    sg, so = _pair(gpu, orc, cfg, painted)
+    lag = helpers.kinematic(so.download())
+    for vel in (True, False):
+        dg, do = abi.RemapDiag(), abi.RemapDiag()
+        sg2, so2 = _pair(gpu, orc, cfg, so.download())
+        sg2.set_lagrange(lag)
+        so2.set_lagrange(lag)
+        sg2.remap_step(1.0, kind=abi.REMAP_DIRECT, remap_velocity=vel, diag=dg)
+        so2.remap_step(1.0, kind=abi.REMAP_DIRECT, remap_velocity=vel, diag=do)
+        assert helpers.bitwise_diff(sg2.download(), so2.download(), helpers.STATE_FIELDS) == []
+        assert (dg.max_k_violation, dg.k_clip_count, dg.mass_fix_count) == \
+               (do.max_k_violation, do.k_clip_count, do.mass_fix_count)
+
+
+@pytest.mark.parametrize("which,steps", [("riemann", 80), ("triple", 700), ("bubble", 30), ("voronoi3", 30)])
+def test_run_loop_direct_bitwise(gpu, orc, which, steps):
+    case = {"riemann": cases.riemann2d(48), "triple": cases.triple_point(64, 32), "bubble": cases.shock_bubble(48),
+            "voronoi3": cases.voronoi3(64)}[which]
+    sg, so = _pair(gpu, orc, case.cfg, case.paint())
+    rg, eg = helpers.run_capture(sg, steps, case.cfl, kind=abi.REMAP_DIRECT)
+    ro, eo = helpers.run_capture(so, steps, case.cfl, kind=abi.REMAP_DIRECT)
+    assert eg == eo
+    assert np.array_equal(rg.dts, ro.dts)
+    assert (rg.floor_count, rg.diag) == (ro.floor_count, ro.diag)
+    assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS, case.cfg.nmat) == []
+
+
+@pytest.mark.parametrize("scenario", ["cfl_face", "collapsed"])
+def test_error_parity_direct(gpu, orc, scenario):
+    cfg = make_config(12, 10, 1.0, 1.0, bc_x=BC_PERIODIC, bc_y=BC_PERIODIC)
+    painted = helpers.random_state(cfg, 77, "gas", umax=0.2)
+    sg, so = _pair(gpu, orc, cfg, painted)
+    lag = helpers.kinematic(so.download())
+    g = abi.GHOST
+    if scenario == "cfl_face":
+        lag.u_half[g + 3, g + 5, 0] = 1.9
+        lag.u_half[g + 4, g + 5, 0] = 1.9
+        lag.u_half[g + 6, g + 2, 1] = 1.9  # and a fast Y face later in loop order
+        lag.u_half[g + 6, g + 3, 1] = 1.9
+    else:
+        lag.u_half[g + 3, g + 5, 0] = -3.0
+        lag.u_half[g + 4, g + 5, 0] = -3.0
+        lag.u_half[g + 3, g + 4, 0] = 3.0
+        lag.u_half[g + 4, g + 4, 0] = 3.0
+    res = []
+    for s in (sg, so):
+        s.set_lagrange(lag)
+        try:
+            s.remap_step(0.5, kind=abi.REMAP_DIRECT)
+            res.append(None)
+        except errors.SimError as e:
+            res.append((type(e).__name__, e.what, e.i, e.j))
+    assert res[0] == res[1] and res[0] is not None
