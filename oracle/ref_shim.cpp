@@ -527,3 +527,22 @@ extern "C" int h2dr_run_case(const char* name, int divisor, int scheme, int face
     if (rc && err_what) std::snprintf(err_what, err_cap, "%s", c.err.what);
     return rc;
 }
+
+// convergence_study (harness.cpp:426-461) of the reference itself: errs
+// [scheme][mesh] and one slope per scheme; returns the error kind.
+extern "C" int h2dr_convergence(const char* name, const int* meshes, int nmesh, const int* schemes, int nscheme,
+                                double* errs, double* slopes, char* err_what, int err_cap) {
+    h2dr_ctx c;
+    const int rc = guarded(&c, -1, 0, [&] {
+        std::vector<int> ms(meshes, meshes + nmesh);
+        std::vector<RemapKind> ks;
+        for (int s = 0; s < nscheme; ++s) ks.push_back(static_cast<RemapKind>(schemes[s]));
+        const auto res = convergence_study(name, ms, ks);
+        for (int s = 0; s < nscheme; ++s) {
+            for (int m = 0; m < nmesh; ++m) errs[s * nmesh + m] = res[s].rows[m].err;
+            slopes[s] = res[s].slope;
+        }
+    });
+    if (rc && err_what) std::snprintf(err_what, err_cap, "%s", c.err.what);
+    return rc;
+}

@@ -2,12 +2,14 @@
 commands (proj/tools/main.cpp:15-71) over the device path:
 
     python -m paper_2208_13409_b200 run <config>
+    python -m paper_2208_13409_b200 converge <case> <schemes>
     python -m paper_2208_13409_b200 case-list
 
 ``run`` reads the key = value config (config.cpp), runs the case on the GPU
 and writes, like cmd_run: <out_dir>/diag.log (one append_diag_line per step),
 fields_<step>.csv every ``output_every`` steps, final.csv and final.vtk, then
-the summary lines.  The device keeps the State between dumps: a dump is one
+the summary lines.  ``converge`` is cmd_converge (main.cpp:86-105): the
+mesh-refinement study on 50, 100, 200 cells per side, one table.  The device keeps the State between dumps: a dump is one
 download, the ledger comes from the step series reduced on the device.
 """
 from __future__ import annotations
@@ -23,6 +25,7 @@ from . import abi, errors, frontend, product_library
 def _usage() -> int:
     print("usage: hydro2d <command> [args]\n"
           "  run <config>               run a case from a key = value config file\n"
+          "  converge <case> <schemes>  mesh-refinement study (schemes: comma list)\n"
           "  case-list                  list the built-in cases")
     return 2
 
@@ -76,6 +79,17 @@ def cmd_run(path: str) -> int:
     return 0
 
 
+def cmd_converge(case_name: str, schemes_arg: str) -> int:
+    schemes = frontend.parse_schemes(schemes_arg)
+    meshes = [50, 100, 200]
+    results = frontend.convergence_study(case_name, meshes, schemes)
+    print("%-10s" % "mesh" + "".join("  %-12s" % frontend.SCHEME_NAMES[r.scheme] for r in results))
+    for row, n in enumerate(meshes):
+        print("%-10d" % n + "".join("  %-12.5e" % r.rows[row][1] for r in results))
+    print("%-10s" % "slope" + "".join("  %-12.3f" % r.slope for r in results))
+    return 0
+
+
 def main(argv=None) -> int:
     argv = sys.argv[1:] if argv is None else argv
     if not argv:
@@ -87,6 +101,8 @@ def main(argv=None) -> int:
             return 0
         if argv[0] == "run" and len(argv) == 2:
             return cmd_run(argv[1])
+        if argv[0] == "converge" and len(argv) == 3:
+            return cmd_converge(argv[1], argv[2])
     except errors.SimError as e:
         print(f"error: {e}", file=sys.stderr)
         return 1

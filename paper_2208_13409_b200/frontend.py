@@ -476,3 +476,54 @@ def run_case(name: str, divisor: int = 1, scheme: str = "DirectCF", face_order: 
         "max_k_violation": rep.max_k_violation, "min_p": float(t1["min_p"]), "max_p": float(t1["max_p"]),
         "wall_seconds": rep.wall_seconds,
     }
+
+
+# ---- mesh-refinement study (harness.hpp:100-113, harness.cpp:426-461) ---------------
+
+@dataclass
+class ConvergenceResult:
+    """hydro::ConvergenceResult: per mesh n the L2 error of the final density
+    (volume fraction for two-material cases) against the initial field, and
+    the least-squares slope of log(err) against log(dx)."""
+    scheme: int = REMAP_DIRECTCF
+    rows: List[Tuple[int, float]] = field(default_factory=list)
+    slope: float = 0.0
+
+
+def parse_schemes(text: str) -> List[int]:
+    """Comma list of scheme names (tools/main.cpp:72-84)."""
+    out = []
+    for item in text.split(","):
+        if item not in SCHEMES:
+            raise errors.SimError(f"unknown scheme '{item}' (valid: AD, Direct, DirectCF)")
+        out.append(SCHEMES[item])
+    if not out:
+        raise errors.SimError("no schemes given")
+    return out
+
+
+def convergence_study(case_name: str, meshes: List[int], schemes: List[int]) -> List[ConvergenceResult]:
+    """convergence_study (harness.cpp:426-461): the case on n x n meshes per
+    scheme, every run on the device; the slope's sums accumulate in the
+    reference's order so it matches to the bit."""
+    out = []
+    for scheme in schemes:
+        res = ConvergenceResult(scheme=scheme)
+        for n in meshes:
+            cs = build_case(case_name)
+            cs.nx = cs.ny = n
+            cs.scheme = scheme
+            rep = run(cs)
+            res.rows.append((n, rep.l2_k_vs_initial if cs.nmat == 2 else rep.l2_rho_vs_initial))
+        sx = sy = sxx = sxy = 0.0
+        m = len(res.rows)
+        for n, err in res.rows:
+            x = math.log(1.0 / n)
+            y = math.log(max(err, 1e-300))
+            sx += x
+            sy += y
+            sxx += x * x
+            sxy += x * y
+        res.slope = (m * sxy - sx * sy) / (m * sxx - sx * sx) if m > 1 else 0.0
+        out.append(res)
+    return out

@@ -180,3 +180,74 @@ def test_cli_run(tmp_path):
         want = tmp_path / "want.csv"
         sr._check(ref.fn["write_fields"](sr._h, str(want).encode(), abi.DUMP_CSV))
         assert (out / "final.csv").read_bytes() == want.read_bytes()
+
+
+# ---- convergence study (harness.cpp:426-461, main.cpp:72-105) ---------------------
+
+def ref_convergence(ref, name, meshes, schemes):
+    f = ref.dll.h2dr_convergence
+    f.restype = C.c_int
+    ms, ks = np.array(meshes, np.int32), np.array(schemes, np.int32)
+    errs, slopes = np.zeros(len(ms) * len(ks)), np.zeros(len(ks))
+    what = C.create_string_buffer(256)
+    rc = f(name.encode(), ms.ctypes.data_as(C.c_void_p), len(ms), ks.ctypes.data_as(C.c_void_p), len(ks),
+           errs.ctypes.data_as(C.c_void_p), slopes.ctypes.data_as(C.c_void_p), what, 256)
+    assert rc == 0, what.value
+    return errs.reshape(len(ks), len(ms)), slopes
+
+
+def test_parse_schemes():
+    assert frontend.parse_schemes("AD,Direct,DirectCF") == [abi.REMAP_AD, abi.REMAP_DIRECT, abi.REMAP_DIRECTCF]
+    with pytest.raises(errors.SimError) as e:
+        frontend.parse_schemes("AD,Foo")
+    assert str(e.value) == "unknown scheme 'Foo' (valid: AD, Direct, DirectCF)"
+
+
+def test_convergence_slope_and_error_choice(monkeypatch):
+    """The study's bookkeeping with run() stubbed: the error is L2(k) for two
+    materials, L2(rho) otherwise, and the slope is the least-squares fit."""
+    seen = []
+
+    def fake_run(cs, hook=None, device=0):
+        seen.append((cs.nx, cs.ny, cs.scheme))
+        return frontend.RunReport(spec=cs, series=None, initial_state=None, final_state=None,
+                                  l2_rho_vs_initial=1.0 / cs.nx ** 2, l2_k_vs_initial=3.0 / cs.nx)
+    monkeypatch.setattr(frontend, "run", fake_run)
+    mono, multi = (frontend.convergence_study(n, [50, 100, 200], [abi.REMAP_AD, abi.REMAP_DIRECTCF])
+                   for n in ("mono_advect", "multimat_advect"))
+    assert seen[:3] == [(50, 50, abi.REMAP_AD), (100, 100, abi.REMAP_AD), (200, 200, abi.REMAP_AD)]
+    assert [e for _, e in mono[0].rows] == [1.0 / 2500, 1.0 / 10000, 1.0 / 40000]
+    assert [e for _, e in multi[1].rows] == [3.0 / 50, 3.0 / 100, 3.0 / 200]
+    assert abs(mono[0].slope - 2.0) < 1e-12 and abs(multi[1].slope - 1.0) < 1e-12
+
+
+@pytest.mark.gpu
+def test_convergence_study_matches_reference():
+    """The refinement study on the device equals the reference's own
+    convergence_study (criterion 5's call, acceptance.cpp:239-241): every
+    error and slope to the bit, on the three engines."""
+    ref = helpers.ref_lib()
+    if ref is None:
+        pytest.skip("reference library not built")
+    meshes, schemes = [50, 100, 200], [abi.REMAP_AD, abi.REMAP_DIRECT, abi.REMAP_DIRECTCF]
+    want_e, want_s = ref_convergence(ref, "mono_advect", meshes, schemes)
+    got = frontend.convergence_study("mono_advect", meshes, schemes)
+    for s, r in enumerate(got):
+        assert r.scheme == schemes[s] and [n for n, _ in r.rows] == meshes
+        assert [e for _, e in r.rows] == list(want_e[s]), frontend.SCHEME_NAMES[r.scheme]
+        assert r.slope == want_s[s]
+    # criterion 5's ordering claims hold for the device run too
+    ad, direct, cf = ([e for _, e in r.rows] for r in got)
+    for errs in (ad, direct, cf):
+        assert all(errs[m] < errs[m - 1] for m in range(1, 3))
+    assert all(direct[m] >= ad[m] and cf[m] <= 2.0 * ad[m] for m in range(3))
+
+
+@pytest.mark.gpu
+def test_cli_converge():
+    r = subprocess.run([sys.executable, "-m", "paper_2208_13409_b200", "converge", "multimat_advect", "DirectCF"],
+                       cwd=helpers.ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    assert lines[0].split() == ["mesh", "DirectCF"] and [ln.split()[0] for ln in lines[1:]] == ["50", "100", "200",
+                                                                                              "slope"]
