@@ -128,7 +128,8 @@ def dist_setup(n_gpus):
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
         pg = dist
     return world, rank, local, pg
