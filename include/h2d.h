@@ -157,7 +157,8 @@ typedef struct {
     int max_steps;    /* 0 = until t_end (compares the state's absolute step) */
     double t_end;
     double cfl;
-    int remap_kind;   /* H2D_REMAP_DIRECTCF or H2D_REMAP_AD (not H2D_REMAP_DIRECT) */
+    int remap_kind;   /* H2D_REMAP_*: all three on single-domain contexts (AD with at
+                       * most 2 materials); block contexts run DirectCF only */
     double* dt_log;   /* optional host array receiving each step's dt */
     int dt_log_cap;
     /* outputs */
@@ -224,8 +225,9 @@ int h2d_set_lagrange(h2d_ctx* ctx, const h2d_lagrange* lag);
  * `diag` (nullable) is accumulated like the reference's RemapDiag.
  * remap_kind: H2D_REMAP_DIRECTCF (cf_pass, remap.cpp:734-1073) or
  * H2D_REMAP_AD (two directional passes, remap.cpp:469-589, X first when
- * x_first != 0; block contexts: DirectCF only); H2D_REMAP_DIRECT returns
- * H2D_ERR_INVALID. */
+ * x_first != 0; at most 2 materials) or H2D_REMAP_DIRECT (direct_pass,
+ * remap.cpp:593-724) on single-domain contexts; block contexts run DirectCF
+ * only and return H2D_ERR_INVALID for the others. */
 int h2d_remap_step(h2d_ctx* ctx, double dt, int remap_kind, int x_first,
                    int remap_velocity, h2d_remap_diag* diag);
 
@@ -309,6 +311,65 @@ int h2d_step_timed(h2d_ctx* ctx, double cfl, double t_end, int phases, int remap
 /* Write `bytes` of scratch on the context's stream (evicts L2 between timed
  * steps) and wait for it. */
 int h2d_flush_l2(h2d_ctx* ctx, long long bytes);
+
+/* ---- the reference's sub-step entry points (value API of lagrange.hpp /
+ * remap.hpp that the reference's own unit tests call) -------------------- */
+
+/* HalfStepState (lagrange.hpp:14-24). */
+typedef struct {
+    double* x_half;  /* node Vec2 (filled by the caller's layer: node_pos + 0.5 dt u) */
+    double* u_half;  /* node Vec2 */
+    double* vol_half;
+    double* e_half[H2D_MAX_MAT];
+    double* p_half[H2D_MAX_MAT];
+    double* p_mix_half;
+    double* q;
+    int floor_count;
+} h2d_half;
+
+/* HalfStepState predict(State, MaterialSet, dt, PseudoViscosityParams)
+ * (lagrange.hpp:48-49, lagrange.cpp:79-144) of the context's State. */
+int h2d_predict(h2d_ctx* ctx, double dt, h2d_half* out);
+/* LagrangeResult correct(State, MaterialSet, HalfStepState, dt)
+ * (lagrange.hpp:50-51, lagrange.cpp:146-196) from a caller's HalfStepState
+ * (u_half, p_half, q with ghosts); the result stays on the device for
+ * h2d_remap_step and `out` (nullable) receives a copy. floor_count adds the
+ * half state's count like the reference. */
+int h2d_correct(h2d_ctx* ctx, double dt, const h2d_half* in, h2d_lagrange* out);
+/* State remap_single_axis(State, MaterialSet, LagrangeResult, dt, Axis,
+ * ReconConfig, remap_velocity, RemapDiag*) (remap.hpp:55-57,
+ * remap.cpp:1098-1104): one AD directional pass; single-domain, <= 2
+ * materials. */
+int h2d_remap_single_axis(h2d_ctx* ctx, double dt, int axis_x, int remap_velocity, h2d_remap_diag* diag);
+
+/* The reference's scalar kernels on the device: n records, record r reads
+ * in[r * H2D_SC_IN ...] and writes out[r * H2D_SC_OUT ...]; flags[r]
+ * (nullable) is set where the reference call throws (the exception named per
+ * op). Runs on the current device; H2D_ERR_DEVICE without one. */
+#define H2D_SC_IN 48
+#define H2D_SC_OUT 8
+enum {
+    H2D_SC_VAN_LEER = 0,          /* r -> phi                           reconstruct.cpp:10-14 */
+    H2D_SC_LIMITED_GRADIENT = 1,  /* am ac ap xm xc xp -> g; SimError   reconstruct.cpp:16-24 */
+    H2D_SC_FACE_VALUE = 2,        /* order a0 a1 a2 x0 x1 x2 sgn lw ufdt -> v; SimError  :26-31 */
+    H2D_SC_CORNER_VALUE = 3,      /* scheme a[9] xlx[9] xly[9] (index [(di+1)*3+dj+1]) dxp dyp lag_wx lag_wy
+                                   * sgn_fx u_fx_dt sgn_fy u_fy_dt eval_rel.x eval_rel.y dx dy -> v; SimError
+                                   *                                    reconstruct.cpp:116-152 */
+    H2D_SC_MULTID_PLANE = 4,      /* a[9] xlx[9] xly[9] dx dy -> a0 cx cy grad_raw.x .y grad.x .y; SimError
+                                   *                                    reconstruct.cpp:74-107 */
+    H2D_SC_CLIPPED_FRACTION = 5,  /* w h n.x n.y d -> f                 vof.cpp:28-45 */
+    H2D_SC_PLACE_INTERFACE = 6,   /* frac n.x n.y lo.x lo.y hi.x hi.y -> d   vof.cpp:47-73 */
+    H2D_SC_YOUNGS_NORMAL = 7,     /* k1[9] ([(di+1)*3+dj+1]) dx dy -> n.x n.y; IsolatedMixedCellError vof.cpp:10-22 */
+    H2D_SC_CELL_VOLUME = 8,       /* p00 p10 p11 p01 (x, y) -> vol; TangledCellError  state.cpp:25-32 */
+    H2D_SC_CF_CORNER_FLUX = 9,    /* u.x u.y dt -> dvol sx sy           remap.cpp:16-25 */
+    H2D_SC_CF_FACE_FLUX_X = 10,   /* ym yp dm.x dm.y dp.x dp.y -> dvol wlo whi  remap.cpp:27-47 */
+    H2D_SC_CF_FACE_FLUX_Y = 11,   /* xm xp dm.x dm.y dp.x dp.y -> dvol wlo whi  remap.cpp:49-51 */
+    H2D_SC_PSEUDO_VISCOSITY = 12, /* rho c div_u a1 a2 L -> q           lagrange.cpp:7-12 */
+    H2D_SC_DIV_U_CELL = 13,       /* u00 u10 u01 u11 (x, y) dx dy -> div lagrange.cpp:14-20 */
+    H2D_SC_GRAD_PQ_NODE = 14,     /* p[4] q[4] at (i-1,j-1) (i,j-1) (i-1,j) (i,j), dx dy -> g.x g.y  lagrange.cpp:22-30 */
+    H2D_SC_AD_FACE_FLUX = 15      /* u0 u1 dt width cv -> f; CflViolationError  remap.cpp:53-73 (one face) */
+};
+int h2d_scalar_eval(int op, int n, const double* in, double* out, int* flags);
 
 /* Last error recorded on this context (kind H2D_OK if none). */
 int h2d_last_error(h2d_ctx* ctx, h2d_error* err);

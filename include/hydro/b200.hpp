@@ -19,12 +19,31 @@
 //   CornerScheme, ReconConfig           reconstruct.hpp:7-13
 //   RemapKind, RemapDiag, remap_step, update_interface_normals  remap.hpp:9-64
 //   cfl_dt                              harness.hpp:64
+//   cell_volume                         state.hpp:70
+//   pseudo_viscosity, div_u_cell, grad_pq_node, HalfStepState, compute_q,
+//   predict, correct                    lagrange.hpp:12-52
+//   van_leer, limited_gradient_1d, Stencil1D, face_value, Stencil3x3,
+//   CornerKin, corner_value, PlaneRecon, multid_plane, plane_eval
+//                                       reconstruct.hpp:15-69
+//   CornerFlux, cf_corner_flux, CfFaceFlux, cf_face_flux_x/_y,
+//   ad_face_fluxes, remap_single_axis   remap.hpp:15-57
+//   InterfaceLine, youngs_normal, clipped_fraction, place_interface
+//                                       vof.hpp:13-31
+//   ImposedVelocity, Region, CaseSpec, build_case, case_list, init_case,
+//   l2_error, StepDiag, RunReport, StepHook, run, ConvergenceRow,
+//   ConvergenceResult, convergence_study, scheme_name   harness.hpp:13-113
+//   RunConfig, parse_config, load_config, configure_case  config.hpp:9-28
+//   DumpFormat, write_fields, append_diag_line            io.hpp:9-22
 // plus hydro::b200::Simulation, the device-resident run loop
 // (harness.cpp:390-412) that keeps the State on the GPU between steps.
+// Scalar functions evaluate on the device through h2d_scalar_eval (the step
+// kernels' own device functions); run() keeps the State resident and
+// downloads it only when a StepHook is installed.
 #pragma once
 
 #include <array>
 #include <cmath>
+#include <functional>
 #include <iosfwd>
 #include <stdexcept>
 #include <string>
@@ -176,6 +195,8 @@ struct State {
 };
 
 State make_state(const Mesh& mesh, int nmat);
+// two-triangle quad area, throws TangledCellError (state.hpp:70)
+double cell_volume(const Vec2& p00, const Vec2& p10, const Vec2& p11, const Vec2& p01);
 double nodal_mass(const State& s, int i, int j);
 Field<double> nodal_masses(const State& s);
 void fill_ghost_cells(const Mesh& mesh, Field<double>& f);
@@ -203,6 +224,24 @@ struct LagrangeResult {
     Field<double> vol_lag, q;
     int floor_count = 0;
 };
+double pseudo_viscosity(double rho, double c_sound, double div_u, const PseudoViscosityParams& prm, double L);
+double div_u_cell(const Mesh& mesh, const Field<Vec2>& u, int i, int j);
+Vec2 grad_pq_node(const Mesh& mesh, const Field<double>& p, const Field<double>& q, int i, int j);
+struct HalfStepState {
+    Field<Vec2> x_half;
+    Field<Vec2> u_half;
+    Field<double> vol_half;
+    std::array<Field<double>, kMaxMat> e_half;
+    std::array<Field<double>, kMaxMat> p_half;
+    Field<double> p_mix_half;
+    Field<double> q;
+    int floor_count = 0;
+};
+Field<double> compute_q(const State& s, const MaterialSet& mats, const PseudoViscosityParams& prm);
+HalfStepState predict(const State& s, const MaterialSet& mats, double dt, const PseudoViscosityParams& prm);
+LagrangeResult correct(const State& s, const MaterialSet& mats, const HalfStepState& half, double dt);
+// the reference inlines correct(predict(...)) (lagrange.hpp:56-59); the device
+// runs the same arithmetic in two fused kernels
 LagrangeResult lagrange_step(const State& s, const MaterialSet& mats, double dt, const PseudoViscosityParams& prm);
 
 // ---- remap -------------------------------------------------------------------------
@@ -212,8 +251,60 @@ struct ReconConfig {
     CornerScheme corner = CornerScheme::LinearDiag;
     bool interface_degrade = true;
 };
+double van_leer(double r);
+double limited_gradient_1d(double am, double ac, double ap, double xm, double xc, double xp);
+struct Stencil1D {
+    double a[3];
+    double x[3];
+};
+double face_value(int order, const Stencil1D& donor, double sgn_dvol, double lag_width, double u_face_dt);
+struct Stencil3x3 {
+    double a[3][3];
+    Vec2 xl[3][3];
+};
+struct CornerKin {
+    double dxp = 0.0, dyp = 0.0;
+    double lag_wx = 0.0, lag_wy = 0.0;
+    double sgn_fx = 0.0, u_fx_dt = 0.0;
+    double sgn_fy = 0.0, u_fy_dt = 0.0;
+    Vec2 eval_rel;
+    double dx = 1.0, dy = 1.0;
+};
+double corner_value(CornerScheme scheme, const Stencil3x3& st, const CornerKin& kin);
+struct PlaneRecon {
+    double a0 = 0.0;
+    Vec2 center;
+    Vec2 grad_raw;
+    Vec2 grad;
+};
+PlaneRecon multid_plane(const Stencil3x3& st, double dx, double dy);
+inline double plane_eval(const PlaneRecon& pl, const Vec2& x) { return pl.a0 + dot(pl.grad, x - pl.center); }
+
+// ---- vof.hpp (vof.hpp:13-31) -----------------------------------------------------
+struct InterfaceLine {
+    Vec2 normal;
+    double d = 0.0;
+};
+Vec2 youngs_normal(const Field<double>& k1, int i, int j, double dx, double dy);
+double clipped_fraction(double w, double h, const Vec2& n, double d);
+InterfaceLine place_interface(double frac, const Vec2& n, const Rect& proxy);
+
 enum class RemapKind { AD, Direct, DirectCF };
 enum class Axis { X, Y };
+struct CornerFlux {
+    double dvol = 0.0;
+    int sx = 0;
+    int sy = 0;
+};
+CornerFlux cf_corner_flux(const Vec2& u_half, double dt);
+struct CfFaceFlux {
+    double dvol = 0.0;
+    double wlo = 0.0;
+    double whi = 0.0;
+};
+CfFaceFlux cf_face_flux_x(double ym, double yp, const Vec2& disp_m, const Vec2& disp_p);
+CfFaceFlux cf_face_flux_y(double xm, double xp, const Vec2& disp_m, const Vec2& disp_p);
+Field<double> ad_face_fluxes(Axis axis, const Mesh& mesh, const Field<Vec2>& u_half, double dt);
 struct RemapDiag {
     double max_k_violation = 0.0;
     int k_clip_count = 0;
@@ -221,10 +312,50 @@ struct RemapDiag {
 };
 State remap_step(const State& s, const MaterialSet& mats, const LagrangeResult& lag, double dt, RemapKind kind,
                  const ReconConfig& rc, bool x_first = true, bool remap_velocity = true, RemapDiag* diag = nullptr);
+State remap_single_axis(const State& s, const MaterialSet& mats, const LagrangeResult& lag, double dt, Axis axis,
+                        const ReconConfig& rc, bool remap_velocity = true, RemapDiag* diag = nullptr);
 void update_interface_normals(State& s);
 
 // ---- harness -------------------------------------------------------------------------
+enum class ImposedVelocity { None, Constant, Rotation };
+struct Region {
+    enum class Shape { All, HalfPlaneX, Rectangle, Circle };
+    Shape shape = Shape::All;
+    double xsplit = 0.0;
+    Rect rect;
+    Vec2 center;
+    double radius = 0.0;
+    int mat = 0;
+    double rho = 1.0;
+    double p = 1e5;
+    Vec2 u;
+};
+struct CaseSpec {
+    std::string name;
+    int nx = 0, ny = 0;
+    double x0 = 0.0, y0 = 0.0, lx = 1.0, ly = 1.0;
+    BoundaryKind bc_x = BoundaryKind::Periodic;
+    BoundaryKind bc_y = BoundaryKind::Periodic;
+    MaterialSet mats;
+    std::vector<Region> regions;
+    double t_end = 0.0;
+    double cfl = 0.3;
+    int max_steps = 0;
+    RemapKind scheme = RemapKind::DirectCF;
+    ReconConfig recon;
+    PseudoViscosityParams pv;
+    ImposedVelocity imposed = ImposedVelocity::None;
+    Vec2 u_const;
+    double flip_time = -1.0;
+    Vec2 rot_center;
+    double rot_omega = 0.0;
+    Mesh make_mesh() const;
+};
+CaseSpec build_case(const std::string& name, int divisor = 1);
+std::vector<std::string> case_list();
+State init_case(const CaseSpec& cs);
 double cfl_dt(const State& s, const MaterialSet& mats, double cfl);
+double l2_error(const Field<double>& a, const Field<double>& b, const Mesh& mesh);
 
 // StepDiag, harness.hpp:66-72 (the record run() appends per step)
 struct StepDiag {
@@ -234,6 +365,55 @@ struct StepDiag {
     double min_rho = 0.0, max_rho = 0.0;
     double min_p = 0.0, max_p = 0.0;
 };
+
+struct RunReport {
+    CaseSpec spec;
+    std::vector<StepDiag> series;
+    State initial_state;
+    State final_state;
+    int steps = 0;
+    double wall_seconds = 0.0;
+    double max_k_violation = 0.0;
+    int k_clip_count = 0;
+    int mass_fix_count = 0;
+    int energy_floor_count = 0;
+    double l2_rho_vs_initial = 0.0;
+    double l2_k_vs_initial = 0.0;
+};
+using StepHook = std::function<void(const State&, const StepDiag&)>;
+// the run loop (harness.cpp:380-424) with the State resident on the device;
+// a hook receives the downloaded State after every step
+RunReport run(const CaseSpec& cs, const StepHook& hook = {});
+struct ConvergenceRow {
+    int n = 0;
+    double err = 0.0;
+};
+struct ConvergenceResult {
+    RemapKind scheme{};
+    std::vector<ConvergenceRow> rows;
+    double slope = 0.0;
+};
+std::vector<ConvergenceResult> convergence_study(const std::string& case_name, const std::vector<int>& meshes,
+                                                 const std::vector<RemapKind>& schemes);
+const char* scheme_name(RemapKind k);
+
+// ---- config.hpp (config.hpp:9-28) ------------------------------------------------------
+struct RunConfig {
+    std::string case_name;
+    RemapKind scheme = RemapKind::DirectCF;
+    int face_order = 2;
+    CornerScheme corner = CornerScheme::LinearDiag;
+    double cfl = 0.3;
+    int divisor = 1;
+    double t_end = -1.0;
+    int max_steps = 0;
+    std::string out_dir = "out";
+    int output_every = 0;
+    unsigned long seed = 0;
+};
+RunConfig parse_config(const std::string& text);
+RunConfig load_config(const std::string& path);
+CaseSpec configure_case(const RunConfig& rc);
 
 // ---- io.hpp (io.hpp:9-22): the reference's CSV / legacy-VTK cell dump and
 // the conservation-ledger line, byte-identical output

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libh2d.so")
-SOURCES = ["h2d_kernels.cu", "h2d_capi.cu", "hydro_api.cpp", "h2d_io.cpp"]
+SOURCES = ["h2d_kernels.cu", "h2d_scalar.cu", "h2d_capi.cu", "hydro_api.cpp", "hydro_harness.cpp", "h2d_io.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"]

@@ -636,7 +636,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
         s.e_mix = plane(c);
         s.rho_mix = plane(c);
         s.p_mix = plane(c);
-        if (p == 0 || nm == 2) {
+        if (p == 0 || nm >= 2) {
             s.nrx = plane(c);
             s.nry = plane(c);
         } else {  // one material: the normals are carried unchanged, so both parities share them
@@ -753,7 +753,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     if (ctl_push(c)) return fail(H2D_ERR_DEVICE);
     // make_state defaults (state.cpp:5-23): k0 = 1, normals (1, 0), vol = dx*dy
     for (int p = 0; p < 2; ++p) {
-        if (fill_plane(c, c->sb[p].k[0], 1.0) || (p == 0 || nm == 2 ? fill_plane(c, c->sb[p].nrx, 1.0) : 0) ||
+        if (fill_plane(c, c->sb[p].k[0], 1.0) || (p == 0 || nm >= 2 ? fill_plane(c, c->sb[p].nrx, 1.0) : 0) ||
             fill_plane(c, c->sb[p].vol, d.cv))
             return fail(H2D_ERR_DEVICE);
     }
@@ -970,6 +970,166 @@ int h2d_remap_step(h2d_ctx* c, double dt, int kind, int x_first, int remap_veloc
         diag->k_clip_count += c->hctl->step_clip;
         diag->mass_fix_count += c->hctl->step_fix;
     }
+    return 0;
+}
+
+// ---- sub-step entry points (lagrange.hpp predict / correct, remap.hpp
+// remap_single_axis) and the scalar kernels ---------------------------------
+int h2d_predict(h2d_ctx* c, double dt, h2d_half* out) {
+    cudaSetDevice(c->device);
+    c->have_lag = false;
+    if (c->is_block) {
+        set_err(c, H2D_ERR_INVALID, "predict on a block context");
+        return H2D_ERR_INVALID;
+    }
+    if (int rc = ctl_reset(c)) return rc;
+    Dev d = make_dev(c, c->cur, 1);
+    // vol_half / e_half land in the vol_lag / e_lag scratch (predict writes
+    // no e_lag); interior only, zero ghosts like the reference's Field(nx, ny)
+    d.volh = d.vol_lag;
+    if (int rc = zero_plane(c, d.vol_lag)) return rc;
+    for (int a = 0; a < c->nmat; ++a) {
+        d.eh[a] = d.el[a];
+        if (int rc = zero_plane(c, d.el[a])) return rc;
+    }
+    launch_begin(c->ctl, 1, dt, c->st);
+    launch_lagrange_mode(d, 0, 1, c->st);
+    if (int rc = check_launch(c)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    if (int rc = decode_error(c, false)) return rc;
+    if (out) {
+        const int nx = c->nx, ny = c->ny;
+        if (int rc = get_vec(c, out->u_half, d.uhx, d.uhy, nx + 1, ny + 1)) return rc;
+        CK(cudaStreamSynchronize(c->st));
+        if (int rc = get_plane(c, out->vol_half, d.vol_lag, nx, ny)) return rc;
+        for (int a = 0; a < c->nmat; ++a) {
+            if (int rc = get_plane(c, out->e_half[a], d.el[a], nx, ny)) return rc;
+            if (int rc = get_plane(c, out->p_half[a], d.ph[a], nx, ny)) return rc;
+        }
+        if (int rc = get_plane(c, out->p_mix_half, d.pmh, nx, ny)) return rc;
+        if (int rc = get_plane(c, out->q, d.q, nx, ny)) return rc;
+        CK(cudaStreamSynchronize(c->st));
+        out->floor_count = c->hctl->step_floor;
+    }
+    return 0;
+}
+
+int h2d_correct(h2d_ctx* c, double dt, const h2d_half* in, h2d_lagrange* out) {
+    cudaSetDevice(c->device);
+    c->have_lag = false;
+    if (c->is_block || !in || !in->u_half || !in->q) {
+        set_err(c, H2D_ERR_INVALID, "correct needs a single-domain context and a HalfStepState");
+        return H2D_ERR_INVALID;
+    }
+    const int nx = c->nx, ny = c->ny;
+    Dev d = make_dev(c, c->cur, 1);
+    if (int rc = put_vec(c, d.uhx, d.uhy, in->u_half, nx + 1, ny + 1)) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    if (int rc = put_plane(c, d.q, in->q, nx, ny)) return rc;
+    for (int a = 0; a < c->nmat; ++a) {
+        if (in->p_half[a]) {
+            if (int rc = put_plane(c, d.ph[a], in->p_half[a], nx, ny)) return rc;
+        } else if (int rc = zero_plane(c, d.ph[a])) {
+            return rc;
+        }
+    }
+    if (int rc = zero_plane(c, d.vol_lag)) return rc;
+    if (int rc = ctl_reset(c)) return rc;
+    launch_begin(c->ctl, 1, dt, c->st);
+    launch_lagrange_mode(d, 1, 2, c->st);
+    if (int rc = check_launch(c)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    if (int rc = decode_error(c, false)) return rc;
+    c->have_lag = true;
+    if (out) {
+        if (int rc = get_vec(c, out->u_half, d.uhx, d.uhy, nx + 1, ny + 1)) return rc;
+        CK(cudaStreamSynchronize(c->st));
+        if (int rc = get_vec(c, out->u_lag, d.ulx, d.uly, nx + 1, ny + 1)) return rc;
+        for (int a = 0; a < c->nmat; ++a)
+            if (int rc = get_plane(c, out->e_lag[a], d.el[a], nx, ny)) return rc;
+        if (int rc = get_plane(c, out->vol_lag, d.vol_lag, nx, ny)) return rc;
+        if (int rc = get_plane(c, out->q, d.q, nx, ny)) return rc;
+        CK(cudaStreamSynchronize(c->st));
+        out->floor_count = c->hctl->step_floor + in->floor_count;
+    }
+    return 0;
+}
+
+int h2d_remap_single_axis(h2d_ctx* c, double dt, int axis_x, int remap_velocity, h2d_remap_diag* diag) {
+    cudaSetDevice(c->device);
+    if (c->is_block || c->nmat > 2) {
+        set_err(c, H2D_ERR_INVALID, "remap_single_axis runs on single-domain contexts with <= 2 materials");
+        return H2D_ERR_INVALID;
+    }
+    if (!c->have_lag) {
+        set_err(c, H2D_ERR_INVALID, "remap_single_axis without a LagrangeResult");
+        return H2D_ERR_INVALID;
+    }
+    if (int rc = ensure_ad(c)) return rc;
+    if (int rc = ctl_reset(c)) return rc;
+    Dev d = make_dev(c, c->cur, remap_velocity != 0);
+    launch_begin(c->ctl, 1, dt, c->st);
+    launch_remap_single_axis(d, c->adw, axis_x != 0, remap_velocity != 0, c->st);
+    launch_commit(c->ctl, 1, c->st);
+    if (int rc = check_launch(c)) return rc;
+    if (int rc = ctl_pull(c)) return rc;
+    if (int rc = decode_error(c, false)) return rc;
+    c->cur = c->hctl->cur;
+    if (diag) {
+        const double v = __builtin_bit_cast(double, (unsigned long long)c->hctl->kviol_bits);
+        if (v > diag->max_k_violation) diag->max_k_violation = v;
+        diag->k_clip_count += c->hctl->step_clip;
+        diag->mass_fix_count += c->hctl->step_fix;
+    }
+    return 0;
+}
+
+namespace {
+// device scratch of h2d_scalar_eval (per host thread, grown on demand)
+struct ScalarScratch {
+    int device = -1;
+    double *in = nullptr, *out = nullptr;
+    int* flags = nullptr;
+    int cap = 0;
+    ~ScalarScratch() {
+        if (in) cudaFree(in);
+        if (out) cudaFree(out);
+        if (flags) cudaFree(flags);
+    }
+};
+thread_local ScalarScratch g_scalar;
+}  // namespace
+
+int h2d_scalar_eval(int op, int n, const double* in, double* out, int* flags) {
+    if (n < 0 || op < H2D_SC_VAN_LEER || op > H2D_SC_AD_FACE_FLUX) return H2D_ERR_INVALID;
+    if (n == 0) return 0;
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return H2D_ERR_DEVICE;
+    ScalarScratch& s = g_scalar;
+    if (s.device != dev || s.cap < n) {
+        if (s.in) cudaFree(s.in);
+        if (s.out) cudaFree(s.out);
+        if (s.flags) cudaFree(s.flags);
+        s.in = s.out = nullptr;
+        s.flags = nullptr;
+        const int cap = n < 1024 ? 1024 : n;
+        if (cudaMalloc(&s.in, (size_t)cap * H2D_SC_IN * sizeof(double)) != cudaSuccess ||
+            cudaMalloc(&s.out, (size_t)cap * H2D_SC_OUT * sizeof(double)) != cudaSuccess ||
+            cudaMalloc(&s.flags, (size_t)cap * sizeof(int)) != cudaSuccess) {
+            s.cap = 0;
+            return H2D_ERR_DEVICE;
+        }
+        s.cap = cap;
+        s.device = dev;
+    }
+    if (cudaMemcpy(s.in, in, (size_t)n * H2D_SC_IN * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+        return H2D_ERR_DEVICE;
+    launch_scalar(op, n, s.in, s.out, s.flags, nullptr);
+    if (cudaGetLastError() != cudaSuccess) return H2D_ERR_DEVICE;
+    if (cudaMemcpy(out, s.out, (size_t)n * H2D_SC_OUT * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return H2D_ERR_DEVICE;
+    if (flags && cudaMemcpy(flags, s.flags, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return H2D_ERR_DEVICE;
     return 0;
 }
 

@@ -181,6 +181,7 @@ struct Dev {
     double *nm[kMatSlots], *ne[kMatSlots], *nk[kMatSlots], *nvol, *nm_mix, *ne_mix, *nrho_mix, *np_mix, *nnrx, *nnry, *nux, *nuy;
     // LagrangeResult (lagrange.hpp:38-45)
     double *q, *pmh, *ph[kMatSlots], *uhx, *uhy, *ulx, *uly, *el[kMatSlots], *vol_lag;
+    double *volh, *eh[kMatSlots];  // HalfStepState vol_half / e_half (h2d_predict only; null otherwise)
     // remap scratch (the tile kernel keeps its geometry in shared memory)
     double *me[kMatSlots], *mcell, *unrm;
     double *dmx, *dmy, *dmc;
@@ -350,7 +351,7 @@ H2D_DEV int sgn3(double v) { return v > 0.0 ? 1 : (v < 0.0 ? -1 : 0); }  // reco
 // the four 1D limited slopes; returns (a0, cx, cy, gx, gy)
 static __device__ __noinline__ void multid_plane(double dgx, double dgy, const double* a, const double* xlx,
                                           const double* xly, double& a0, double& cx, double& cy, double& gx,
-                                          double& gy, bool& bad) {
+                                          double& gy, bool& bad, double* graw = nullptr) {
     a0 = a[4];
     cx = xlx[4];
     cy = xly[4];
@@ -412,6 +413,10 @@ static __device__ __noinline__ void multid_plane(double dgx, double dgy, const d
     if (!rank_ok) return;
     const double g2 = b[1] / X1[1];
     const double g1 = (b[0] - X1[0] * g2) / X0[0];
+    if (graw) {  // PlaneRecon::grad_raw (h2d_scalar_eval only)
+        graw[0] = g1;
+        graw[1] = g2;
+    }
     const double gnorm = sqrt(g1 * g1 + g2 * g2);
     if (gnorm < 1e-300) return;
     const double vx = dgx, vy = dgy;  // dx/diag, dy/diag (hoisted, same bits)

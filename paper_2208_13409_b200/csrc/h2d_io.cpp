@@ -46,7 +46,9 @@ struct View {
     double e(int i, int j) const { return s.e_mix[C(i, j)]; }
     double p(int i, int j) const { return s.p_mix[C(i, j)]; }
     double k0(int i, int j) const { return s.k[0][C(i, j)]; }
-    double k1(int i, int j) const { return nmat == 2 ? s.k[1][C(i, j)] : 0.0; }
+    // the reference format has k0 and k1 columns only; a three-material State
+    // dumps its first two fractions
+    double k1(int i, int j) const { return nmat >= 2 ? s.k[1][C(i, j)] : 0.0; }
     // cell_u_mean (io.cpp:21-23): 0.25 * (((u00 + u10) + u01) + u11), per component
     double um(int i, int j, int c) const {
         const double* u = s.u;
@@ -57,7 +59,7 @@ struct View {
 
 bool check_view(const h2d_state* s, int nmat) {
     if (!s || !s->rho_mix || !s->e_mix || !s->p_mix || !s->k[0] || !s->u) return false;
-    return !(nmat == 2 && !s->k[1]);
+    return !(nmat >= 2 && !s->k[1]);
 }
 
 // write_csv, io.cpp:25-39

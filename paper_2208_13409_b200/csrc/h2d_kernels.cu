@@ -392,9 +392,13 @@ __global__ void k_lag_cells(Dev d) {
     double pmix = 0.0;
     int floors = 0;
     const double cv = d.cv;
+    // h2d_predict also returns HalfStepState::vol_half / e_half (lagrange.hpp:14-24)
+    const bool half_out = d.volh != nullptr && in(d.own_c, i, j);
+    if (half_out) d.volh[c] = vol;
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
         double pa_h = 0.0;
+        double eh = ka[a] > 0.0 ? en[a] : 0.0;  // frozen sliver (lagrange.cpp:110)
         if (!(ka[a] < kThermoTol)) {
             const double rho_n = rho_of(d, ma[a], ka[a]);
             const double rho_h = ma[a] / (ka[a] * vol);
@@ -407,8 +411,10 @@ __global__ void k_lag_cells(Dev d) {
             }
             pa_h = eos_p(d, a, rho_h, ea);
             pmix += ka[a] * pa_h;
+            eh = ea;
         }
         d.ph[a][c] = pa_h;
+        if (half_out) d.eh[a][c] = eh;
     }
     d.pmh[c] = pmix;
     if (floors && own) bump_floor(d.ctl, floors);
@@ -435,8 +441,11 @@ struct RowCol {
         }
     }
 };
+// mode 0: predict's node part + correct (lagrange_step); 1: predict's node
+// part only (h2d_predict); 2: correct only, u_half read from its planes
+// (h2d_correct on a caller's HalfStepState)
 template <int NM>
-__global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_lag) {
+__global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_lag, int mode) {
     pdl_enter();
     constexpr int NN = (LTX + 1) * (LTY + 1);
     __shared__ double shx[NN], shy[NN];
@@ -451,7 +460,17 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
     for (int t = tid; t < NN; t += LTX * LTY) {
         const int i = i0 + t % (LTX + 1), j = j0 + t / (LTX + 1);
         double hx = 0.0, hy = 0.0;
-        if (in(rn, i, j)) {
+        if (mode == 2) {
+            if (in(rn, i, j)) {
+                const int e = ix(d, i, j);
+                hx = d.uhx[e];
+                hy = d.uhy[e];
+                if ((i < i0 + LTX || i == rn.i1 - 1) && (j < j0 + LTY || j == rn.j1 - 1)) {
+                    d.ulx[e] = 2.0 * hx - d.ux[e];
+                    d.uly[e] = 2.0 * hy - d.uy[e];
+                }
+            }
+        } else if (in(rn, i, j)) {
             const int a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
             const double mp = 0.25 * (d.m_mix[a] + d.m_mix[b] + d.m_mix[c] + d.m_mix[e]);
             const double rho_p = div_cv(d, mp);
@@ -473,6 +492,7 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
         shx[t] = hx;
         shy[t] = hy;
     }
+    if (mode == 1) return;
     __syncthreads();
     const int tx = tid % LTX, ty = tid / LTX;
     const int i = i0 + tx, j = j0 + ty;
@@ -3374,34 +3394,41 @@ void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s) {
         { k_sync<1><<<g, blk2(), 0, s>>>(d, next, respect_halt); ++g_launches; }
 }
 
-void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) {
+void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s) { launch_lagrange_mode(d, write_vol_lag, 0, s); }
+
+void launch_lagrange_mode(const Dev& d, int write_vol_lag, int mode, cudaStream_t s) {
     const dim3 gc = grid_of(d.r_lagc);
     const dim3 gl = tiles_of(d.r_lagn, LTX, LTY);
-    if (d.nmat == 3)
-        { k_lag_cells<3><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
-    else if (d.nmat == 2)
-        { k_lag_cells<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
-    else
-        { k_lag_cells<1><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
     FieldList fl{};
     fl.respect_halt = 1;
-    fl.n = 2;  // Q (lagrange.cpp:75) and p_mix_half (:132) ghosts; p_half ghosts are never read
-    fl.f[0] = d.q;
-    fl.f[1] = d.pmh;
-    launch_ghost_cells(d, fl, s);
+    if (mode != 2) {
+        if (d.nmat == 3)
+            { k_lag_cells<3><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
+        else if (d.nmat == 2)
+            { k_lag_cells<2><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
+        else
+            { k_lag_cells<1><<<gc, blk2(), 0, s>>>(d); ++g_launches; }
+        fl.n = 2;  // Q (lagrange.cpp:75) and p_mix_half (:132) ghosts
+        fl.f[0] = d.q;
+        fl.f[1] = d.pmh;
+        if (mode == 1) {  // HalfStepState returns p_half with its ghosts too (:133)
+            for (int a = 0; a < d.nmat; ++a) fl.f[fl.n++] = d.ph[a];
+        }
+        launch_ghost_cells(d, fl, s);
+    }
     if (d.nmat == 3)
-        { k_lag_nodes<3><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag); ++g_launches; }
+        { k_lag_nodes<3><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag, mode); ++g_launches; }
     else if (d.nmat == 2)
-        { k_lag_nodes<2><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag); ++g_launches; }
+        { k_lag_nodes<2><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag, mode); ++g_launches; }
     else
-        { k_lag_nodes<1><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag); ++g_launches; }
+        { k_lag_nodes<1><<<gl, LTX * LTY, 0, s>>>(d, write_vol_lag, mode); ++g_launches; }
     FieldList fn{};
-    fn.n = 4;
-    fn.f[0] = d.uhx;
-    fn.f[1] = d.uhy;
+    fn.n = mode == 2 ? 2 : 4;
+    fn.f[0] = mode == 2 ? d.ulx : d.uhx;
+    fn.f[1] = mode == 2 ? d.uly : d.uhy;
     fn.f[2] = d.ulx;
     fn.f[3] = d.uly;
-    fl.n = d.nmat;
+    fl.n = mode == 1 ? 0 : d.nmat;
     for (int a = 0; a < d.nmat; ++a) fl.f[a] = d.el[a];
     launch_ghost_multi(d, fl, fn, 0, 1, s);
 }
@@ -3687,6 +3714,32 @@ void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_veloc
         dp.nry = W.nry;
     }
     post_and_ghosts(dp, run_loop, s);
+}
+
+// remap_single_axis (remap.cpp:1098-1104): make_work + ONE directional pass
+// (pass 0 semantics: Work from the State and the LagrangeResult) written
+// straight into the next State, then assemble_state (ghosts + sync_derived);
+// the pass's own refresh_normals_impl (remap.cpp:588) writes the new normals
+void launch_remap_single_axis(const Dev& d, const AdWork& W, int axis_x, int remap_velocity, cudaStream_t s) {
+    Dev d0 = d;
+    d0.mcell = W.mcell;
+    AdIO w0{};
+    for (int a = 0; a < d.nmat; ++a) {
+        w0.m[a] = d.m[a];
+        w0.e[a] = d.el[a];
+        w0.k[a] = d.k[a];
+    }
+    w0.nrx = d.nrx;
+    w0.nry = d.nry;
+    w0.mcell = nullptr;
+    w0.ux = d.ulx;
+    w0.uy = d.uly;
+    w0.me_from_e = 1;
+    w0.pass = 0;
+    w0.axis_x = axis_x;
+    launch_ad_pass(d0, w0, remap_velocity, s);
+    if (!remap_velocity) pdl(k_copy_u, grid_of(d.win_n), blk2(), 0, s, d);  // w.u = u_lag (remap.cpp:130)
+    post_and_ghosts(d, 0, s);
 }
 
 void launch_step_ad(const Dev& dd, const AdWork& W, int x_first, int fused_start, cudaStream_t s) {

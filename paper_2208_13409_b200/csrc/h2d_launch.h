@@ -39,6 +39,12 @@ void launch_ghost_cells(const Dev& d, const FieldList& fl, cudaStream_t s);
 void launch_ghost_nodes(const Dev& d, const FieldList& fl, cudaStream_t s);
 void launch_sync(const Dev& d, int next, int respect_halt, cudaStream_t s);
 void launch_lagrange(const Dev& d, int write_vol_lag, cudaStream_t s);
+// mode 0 = lagrange_step, 1 = predict only, 2 = correct from the u_half / p_half / q planes
+void launch_lagrange_mode(const Dev& d, int write_vol_lag, int mode, cudaStream_t s);
+// one AD directional pass as remap_single_axis (remap.cpp:1098-1104)
+void launch_remap_single_axis(const Dev& d, const AdWork& W, int axis_x, int remap_velocity, cudaStream_t s);
+// the reference's scalar kernels over n records (h2d.h H2D_SC_*)
+void launch_scalar(int op, int n, const double* in, double* out, int* flags, cudaStream_t s);
 void launch_lagrange_run(const Dev& d, cudaStream_t s);
 void launch_remap(const Dev& d, cudaStream_t s);
 void launch_remap_core(const Dev& d, cudaStream_t s);  // = tile + slivers + dual

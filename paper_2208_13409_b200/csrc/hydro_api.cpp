@@ -283,7 +283,8 @@ State remap_step(const State& s, const MaterialSet& mats, const LagrangeResult& 
         d.k_clip_count = diag->k_clip_count;
         d.mass_fix_count = diag->mass_fix_count;
     }
-    check(h, h2d_remap_step(h, dt, kind == RemapKind::AD ? H2D_REMAP_AD : H2D_REMAP_DIRECTCF, x_first ? 1 : 0,
+    const int hk = kind == RemapKind::AD ? H2D_REMAP_AD : kind == RemapKind::Direct ? H2D_REMAP_DIRECT : H2D_REMAP_DIRECTCF;
+    check(h, h2d_remap_step(h, dt, hk, x_first ? 1 : 0,
                             remap_velocity ? 1 : 0,
                             diag ? &d : nullptr));
     if (diag) {
@@ -294,6 +295,307 @@ State remap_step(const State& s, const MaterialSet& mats, const LagrangeResult& 
     State out = make_state(s.mesh, s.nmat);
     store(h, out);
     return out;
+}
+
+State remap_single_axis(const State& s, const MaterialSet& mats, const LagrangeResult& lag, double dt, Axis axis,
+                        const ReconConfig& rc, bool remap_velocity, RemapDiag* diag) {
+    h2d_ctx* h = load(s, &mats, {}, rc);
+    h2d_lagrange in;
+    std::memset(&in, 0, sizeof in);
+    in.u_half = pv(lag.u_half);
+    in.u_lag = pv(lag.u_lag);
+    for (int a = 0; a < s.nmat; ++a) in.e_lag[a] = p(lag.e_lag[a]);
+    in.vol_lag = p(lag.vol_lag);
+    in.q = p(lag.q);
+    check(h, h2d_set_lagrange(h, &in));
+    h2d_remap_diag d{};
+    if (diag) {
+        d.max_k_violation = diag->max_k_violation;
+        d.k_clip_count = diag->k_clip_count;
+        d.mass_fix_count = diag->mass_fix_count;
+    }
+    check(h, h2d_remap_single_axis(h, dt, axis == Axis::X ? 1 : 0, remap_velocity ? 1 : 0, diag ? &d : nullptr));
+    if (diag) {
+        diag->max_k_violation = d.max_k_violation;
+        diag->k_clip_count = d.k_clip_count;
+        diag->mass_fix_count = d.mass_fix_count;
+    }
+    State out = make_state(s.mesh, s.nmat);
+    store(h, out);
+    return out;
+}
+
+// ---- predict / correct (lagrange.hpp:46-52) ---------------------------------------
+HalfStepState predict(const State& s, const MaterialSet& mats, double dt, const PseudoViscosityParams& prm) {
+    h2d_ctx* h = load(s, &mats, prm);
+    const Mesh& m = s.mesh;
+    const int nx = m.nx, ny = m.ny;
+    HalfStepState r;
+    r.u_half = Field<Vec2>(nx + 1, ny + 1);
+    r.vol_half = Field<double>(nx, ny);
+    for (int a = 0; a < s.nmat; ++a) {
+        r.e_half[a] = Field<double>(nx, ny);
+        r.p_half[a] = Field<double>(nx, ny);
+    }
+    r.p_mix_half = Field<double>(nx, ny);
+    r.q = Field<double>(nx, ny);
+    h2d_half out;
+    std::memset(&out, 0, sizeof out);
+    out.u_half = pv(r.u_half);
+    out.vol_half = p(r.vol_half);
+    for (int a = 0; a < s.nmat; ++a) {
+        out.e_half[a] = p(r.e_half[a]);
+        out.p_half[a] = p(r.p_half[a]);
+    }
+    out.p_mix_half = p(r.p_mix_half);
+    out.q = p(r.q);
+    check(h, h2d_predict(h, dt, &out));
+    r.floor_count = out.floor_count;
+    // x_half: node positions at the half step, output only (lagrange.cpp:88-93)
+    r.x_half = Field<Vec2>(nx + 1, ny + 1);
+    for (int j = -kGhost; j <= ny + kGhost; ++j)
+        for (int i = -kGhost; i <= nx + kGhost; ++i) r.x_half(i, j) = m.node_pos(i, j) + 0.5 * dt * s.u(i, j);
+    return r;
+}
+
+LagrangeResult correct(const State& s, const MaterialSet& mats, const HalfStepState& half, double dt) {
+    h2d_ctx* h = load(s, &mats);
+    const int nx = s.mesh.nx, ny = s.mesh.ny;
+    h2d_half in;
+    std::memset(&in, 0, sizeof in);
+    in.u_half = pv(half.u_half);
+    for (int a = 0; a < s.nmat; ++a) in.p_half[a] = p(half.p_half[a]);
+    in.q = p(half.q);
+    in.floor_count = half.floor_count;
+    LagrangeResult r;
+    r.u_half = Field<Vec2>(nx + 1, ny + 1);
+    r.u_lag = Field<Vec2>(nx + 1, ny + 1);
+    for (int a = 0; a < s.nmat; ++a) r.e_lag[a] = Field<double>(nx, ny);
+    r.vol_lag = Field<double>(nx, ny);
+    r.q = Field<double>(nx, ny);
+    h2d_lagrange out;
+    std::memset(&out, 0, sizeof out);
+    out.u_half = pv(r.u_half);
+    out.u_lag = pv(r.u_lag);
+    for (int a = 0; a < s.nmat; ++a) out.e_lag[a] = p(r.e_lag[a]);
+    out.vol_lag = p(r.vol_lag);
+    out.q = p(r.q);
+    check(h, h2d_correct(h, dt, &in, &out));
+    r.floor_count = out.floor_count;
+    return r;
+}
+
+Field<double> compute_q(const State& s, const MaterialSet& mats, const PseudoViscosityParams& prm) {
+    // Q^n is predict's first product (lagrange.cpp:84); with dt = 0 the half
+    // step cannot tangle, so the only error left is Q's own sound speed
+    return predict(s, mats, 0.0, prm).q;
+}
+
+// ---- scalar kernels on the device (h2d_scalar_eval) --------------------------------
+namespace {
+
+struct Scalar {
+    double in[H2D_SC_IN] = {};
+    double out[H2D_SC_OUT] = {};
+    int flag = 0;
+    // evaluate one record; true when the reference call would throw
+    bool eval(int op) {
+        const int rc = h2d_scalar_eval(op, 1, in, out, &flag);
+        if (rc) throw std::runtime_error("hydro2d-b200: the scalar kernels need a CUDA device (error " +
+                                         std::to_string(rc) + ")");
+        return flag != 0;
+    }
+};
+
+void put_st3(double* x, const Stencil3x3& st) {
+    for (int p = 0; p < 3; ++p)
+        for (int q = 0; q < 3; ++q) {
+            x[p * 3 + q] = st.a[p][q];
+            x[9 + p * 3 + q] = st.xl[p][q].x;
+            x[18 + p * 3 + q] = st.xl[p][q].y;
+        }
+}
+
+[[noreturn]] void throw_centroids() { throw SimError("non-increasing centroid coordinates"); }
+
+}  // namespace
+
+double van_leer(double r) {
+    Scalar k;
+    k.in[0] = r;
+    k.eval(H2D_SC_VAN_LEER);
+    return k.out[0];
+}
+
+double limited_gradient_1d(double am, double ac, double ap, double xm, double xc, double xp) {
+    Scalar k;
+    const double v[] = {am, ac, ap, xm, xc, xp};
+    std::memcpy(k.in, v, sizeof v);
+    if (k.eval(H2D_SC_LIMITED_GRADIENT)) throw_centroids();
+    return k.out[0];
+}
+
+double face_value(int order, const Stencil1D& d, double sgn_dvol, double lag_width, double u_face_dt) {
+    Scalar k;
+    const double v[] = {double(order), d.a[0], d.a[1], d.a[2], d.x[0], d.x[1], d.x[2], sgn_dvol, lag_width, u_face_dt};
+    std::memcpy(k.in, v, sizeof v);
+    if (k.eval(H2D_SC_FACE_VALUE)) throw_centroids();
+    return k.out[0];
+}
+
+double corner_value(CornerScheme scheme, const Stencil3x3& st, const CornerKin& kin) {
+    Scalar k;
+    k.in[0] = double(static_cast<int>(scheme));
+    put_st3(k.in + 1, st);
+    const double v[] = {kin.dxp,     kin.dyp,    kin.lag_wx,  kin.lag_wy,     kin.sgn_fx, kin.u_fx_dt,
+                        kin.sgn_fy,  kin.u_fy_dt, kin.eval_rel.x, kin.eval_rel.y, kin.dx,     kin.dy};
+    std::memcpy(k.in + 28, v, sizeof v);
+    if (k.eval(H2D_SC_CORNER_VALUE)) throw_centroids();
+    return k.out[0];
+}
+
+PlaneRecon multid_plane(const Stencil3x3& st, double dx, double dy) {
+    Scalar k;
+    put_st3(k.in, st);
+    k.in[27] = dx;
+    k.in[28] = dy;
+    if (k.eval(H2D_SC_MULTID_PLANE)) throw_centroids();
+    PlaneRecon pl;
+    pl.a0 = k.out[0];
+    pl.center = {k.out[1], k.out[2]};
+    pl.grad_raw = {k.out[3], k.out[4]};
+    pl.grad = {k.out[5], k.out[6]};
+    return pl;
+}
+
+Vec2 youngs_normal(const Field<double>& k1, int i, int j, double dx, double dy) {
+    Scalar k;
+    for (int di = -1; di <= 1; ++di)
+        for (int dj = -1; dj <= 1; ++dj) k.in[(di + 1) * 3 + dj + 1] = k1(i + di, j + dj);
+    k.in[9] = dx;
+    k.in[10] = dy;
+    if (k.eval(H2D_SC_YOUNGS_NORMAL))
+        throw IsolatedMixedCellError("isolated mixed cell: zero fraction gradient", i, j);
+    return {k.out[0], k.out[1]};
+}
+
+double clipped_fraction(double w, double h, const Vec2& n, double d) {
+    Scalar k;
+    const double v[] = {w, h, n.x, n.y, d};
+    std::memcpy(k.in, v, sizeof v);
+    k.eval(H2D_SC_CLIPPED_FRACTION);
+    return k.out[0];
+}
+
+InterfaceLine place_interface(double frac, const Vec2& n, const Rect& proxy) {
+    Scalar k;
+    const double v[] = {frac, n.x, n.y, proxy.lo.x, proxy.lo.y, proxy.hi.x, proxy.hi.y};
+    std::memcpy(k.in, v, sizeof v);
+    k.eval(H2D_SC_PLACE_INTERFACE);
+    return {n, k.out[0]};
+}
+
+double cell_volume(const Vec2& p00, const Vec2& p10, const Vec2& p11, const Vec2& p01) {
+    Scalar k;
+    const double v[] = {p00.x, p00.y, p10.x, p10.y, p11.x, p11.y, p01.x, p01.y};
+    std::memcpy(k.in, v, sizeof v);
+    if (k.eval(H2D_SC_CELL_VOLUME)) throw TangledCellError("tangled cell");
+    return k.out[0];
+}
+
+CornerFlux cf_corner_flux(const Vec2& u_half, double dt) {
+    Scalar k;
+    k.in[0] = u_half.x;
+    k.in[1] = u_half.y;
+    k.in[2] = dt;
+    k.eval(H2D_SC_CF_CORNER_FLUX);
+    CornerFlux f;
+    f.dvol = k.out[0];
+    f.sx = static_cast<int>(k.out[1]);
+    f.sy = static_cast<int>(k.out[2]);
+    return f;
+}
+
+static CfFaceFlux face_flux(int op, double lo, double hi, const Vec2& dm, const Vec2& dp) {
+    Scalar k;
+    const double v[] = {lo, hi, dm.x, dm.y, dp.x, dp.y};
+    std::memcpy(k.in, v, sizeof v);
+    k.eval(op);
+    CfFaceFlux f;
+    f.dvol = k.out[0];
+    f.wlo = k.out[1];
+    f.whi = k.out[2];
+    return f;
+}
+CfFaceFlux cf_face_flux_x(double ym, double yp, const Vec2& dm, const Vec2& dp) {
+    return face_flux(H2D_SC_CF_FACE_FLUX_X, ym, yp, dm, dp);
+}
+CfFaceFlux cf_face_flux_y(double xm, double xp, const Vec2& dm, const Vec2& dp) {
+    return face_flux(H2D_SC_CF_FACE_FLUX_Y, xm, xp, dm, dp);
+}
+
+Field<double> ad_face_fluxes(Axis axis, const Mesh& mesh, const Field<Vec2>& u_half, double dt) {
+    // every face in one launch, records in the reference loop order (j outer,
+    // i inner) so the first flagged record is the reference's first throw
+    const bool x = axis == Axis::X;
+    const int ni = x ? mesh.nx + 1 : mesh.nx, nj = x ? mesh.ny : mesh.ny + 1;
+    const int n = ni * nj;
+    std::vector<double> in(static_cast<size_t>(n) * H2D_SC_IN, 0.0), out(static_cast<size_t>(n) * H2D_SC_OUT);
+    std::vector<int> flags(n);
+    const double cv = mesh.cell_volume();
+    for (int j = 0; j < nj; ++j)
+        for (int i = 0; i < ni; ++i) {
+            double* r = &in[static_cast<size_t>(j * ni + i) * H2D_SC_IN];
+            r[0] = x ? u_half(i, j).x : u_half(i, j).y;
+            r[1] = x ? u_half(i, j + 1).x : u_half(i + 1, j).y;
+            r[2] = dt;
+            r[3] = x ? mesh.dy : mesh.dx;
+            r[4] = cv;
+        }
+    if (int rc = h2d_scalar_eval(H2D_SC_AD_FACE_FLUX, n, in.data(), out.data(), flags.data()))
+        throw std::runtime_error("hydro2d-b200: the scalar kernels need a CUDA device (error " + std::to_string(rc) + ")");
+    Field<double> f(ni, nj);
+    for (int j = 0; j < nj; ++j)
+        for (int i = 0; i < ni; ++i) {
+            const int r = j * ni + i;
+            f(i, j) = out[static_cast<size_t>(r) * H2D_SC_OUT];
+            if (flags[r]) throw CflViolationError(x ? "CFL violation at X-face" : "CFL violation at Y-face", i, j);
+        }
+    return f;
+}
+
+double pseudo_viscosity(double rho, double c_sound, double div_u, const PseudoViscosityParams& prm, double L) {
+    Scalar k;
+    const double v[] = {rho, c_sound, div_u, prm.a1, prm.a2, L};
+    std::memcpy(k.in, v, sizeof v);
+    k.eval(H2D_SC_PSEUDO_VISCOSITY);
+    return k.out[0];
+}
+
+double div_u_cell(const Mesh& mesh, const Field<Vec2>& u, int i, int j) {
+    Scalar k;
+    const Vec2 c[4] = {u(i, j), u(i + 1, j), u(i, j + 1), u(i + 1, j + 1)};
+    for (int q = 0; q < 4; ++q) {
+        k.in[2 * q] = c[q].x;
+        k.in[2 * q + 1] = c[q].y;
+    }
+    k.in[8] = mesh.dx;
+    k.in[9] = mesh.dy;
+    k.eval(H2D_SC_DIV_U_CELL);
+    return k.out[0];
+}
+
+Vec2 grad_pq_node(const Mesh& mesh, const Field<double>& pf, const Field<double>& qf, int i, int j) {
+    Scalar k;
+    const int ci[4] = {i - 1, i, i - 1, i}, cj[4] = {j - 1, j - 1, j, j};
+    for (int q = 0; q < 4; ++q) {
+        k.in[q] = pf(ci[q], cj[q]);
+        k.in[4 + q] = qf(ci[q], cj[q]);
+    }
+    k.in[8] = mesh.dx;
+    k.in[9] = mesh.dy;
+    k.eval(H2D_SC_GRAD_PQ_NODE);
+    return {k.out[0], k.out[1]};
 }
 
 // ---- io.hpp --------------------------------------------------------------------------

@@ -308,12 +308,13 @@ def run_blocks(blocks: Sequence[BlockSolver], transport, max_steps: int, t_end: 
         scal = [b.scalars() for b in blocks]
         wmax, nerr, err = transport.allreduce(scal)
         if err != NO_ERR:
-            # blocks whose own step committed roll back when the first error
-            # precedes the commit (nan_scan errors come after it)
+            # every block whose own step committed rolls back when the first
+            # error precedes the commit (nan_scan errors come after it); that
+            # includes a block whose own error is a post-commit nan_scan error
+            # (k_rollback is a no-op on a block that did not commit)
             if phase_of(err) < PH_NAN_CELL:
-                for b, s in zip(blocks, scal):
-                    if s[2] == NO_ERR:
-                        b.rollback()
+                for b in blocks:
+                    b.rollback()
             for b in blocks:
                 b.set_scalars(wmax, nerr, err)
             break

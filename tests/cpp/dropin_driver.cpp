@@ -187,6 +187,14 @@ int main(int argc, char** argv) {
             const State o = remap_step(s, mats, lag, 1.0, RemapKind::DirectCF, rc);
             put_s("kinematic");
             put_state(o);
+            // the faces-only Direct engine (remap.cpp:593-724) and AD through
+            // the same call: each RemapKind must reach its own engine
+            const State od = remap_step(s, mats, lag, 1.0, RemapKind::Direct, rc);
+            put_s("kinematic direct");
+            put_state(od);
+            const State oa = remap_step(s, mats, lag, 1.0, RemapKind::AD, rc, order == 1);
+            put_s("kinematic ad");
+            put_state(oa);
         }
         // CFL refusal with a located error (test_remap.cpp:505-513)
         Field<Vec2> fast(13, 11, Vec2{0.95, 0.0});

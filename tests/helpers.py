@@ -3,6 +3,8 @@ generators modelled on the reference fixtures (gas_state test_remap.cpp:32-43,
 front_state :403-422, kinematic() :46-54) and bitwise comparison."""
 from __future__ import annotations
 
+import ctypes as C
+import hashlib
 import os
 import subprocess
 
@@ -147,3 +149,28 @@ def run_capture(s: Solver, steps: int, cfl: float, kind: int = abi.REMAP_DIRECTC
         return r, None
     except errors.SimError as e:
         return e.partial, (type(e).__name__, e.what, e.i, e.j, e.step, e.in_step)
+
+
+def plane_hashes(solver, nmat: int) -> dict:
+    """sha256 of every State plane, downloading one plane at a time (so the
+    8192^2 pin needs one plane of host memory, not a whole State)."""
+    nx, ny = solver.nx, solver.ny
+    cs, ns = (ny + 2 * abi.GHOST, nx + 2 * abi.GHOST), (ny + 1 + 2 * abi.GHOST, nx + 1 + 2 * abi.GHOST)
+    out = {}
+    plan = [(f"{f}{a}", f, a, cs) for f in ("m", "e", "k") for a in range(nmat)]
+    plan += [(f, f, None, cs) for f in ("vol", "m_mix", "e_mix", "rho_mix", "p_mix")]
+    plan += [("iface_normal", "iface_normal", None, cs + (2,)), ("u", "u", None, ns + (2,))]
+    step = time_ = None
+    for key, f, a, shape in plan:
+        buf = np.empty(shape)
+        v = abi.StateView()
+        p = buf.ctypes.data_as(C.POINTER(C.c_double))
+        if a is None:
+            setattr(v, f, p)
+        else:
+            getattr(v, f)[a] = p
+        solver._check(solver.lib.fn["download_state"](solver._h, C.byref(v)))
+        out[key] = hashlib.sha256(buf.tobytes()).hexdigest()
+        step, time_ = v.step, v.time
+        del buf
+    return out, step, time_
