@@ -3,15 +3,17 @@
 
 Product arm (default): the CUDA library through its C-ABI.  A "step" is one
 pass of the hot path over the whole mesh: cfl_dt -> lagrange_step ->
-remap_step(DirectCF) -> nan_scan (harness.cpp:390-412).  The workload is
-BASELINE.json configs[1] (Sedov point blast, 1024^2, 1 material, walls,
-CFL 0.5) with synthetic initial data painted exactly like the reference's
-init_case.  W warm-up steps, then K timed steps, each bracketed by CUDA events
+remap_step(DirectCF) -> nan_scan (harness.cpp:390-412).  The default workload is
+the largest BASELINE.json configuration that fits one GPU: configs[3], the
+two-material shock-bubble on 8192^2 cells (the 16384^2 three-material
+configs[4] needs two GPUs), with synthetic initial data painted exactly like
+the reference's init_case (seeded bubble perturbation).  W warm-up steps, then K timed steps, each bracketed by CUDA events
 on the library's stream with an L2 flush (512 MiB write) between steps.
 
 Reference arm (--impl reference): the reference's own CPU implementation
-(oracle/_ref, compiled from /root/reference/proj) on the host, same workload,
-single thread (the reference has no threading).
+(oracle/_ref, compiled from /root/reference/proj) on the host, same workload
+and config, single thread (the reference has no threading), each run a
+bounded sample of the workload's steps (about 1.2e8 cell-updates).
 
 Prints ONE JSON line (rank 0).
 """
@@ -162,6 +164,41 @@ def cpu_lib(nmat=1):
     return abi.Library(port, "h2do_"), "port"
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+SCHEMES = {"ad": "AD split (X/Y alternating)", "direct": "Direct (faces only)"}
+
+
+def config_of(case, remap, world, parallelism=None):
+    """The `config` object, identical for the product and the reference arm."""
+    return {"workload": case.name, "cells": case.cells, "materials": case.cfg.nmat, "cfl": case.cfl,
+            "scheme": SCHEMES.get(remap, "DirectCF") + " face_order=2 LinearDiag interface_degrade",
+            "steps_from": "t=0 (+ warm-up steps)",
+            "parallelism": parallelism or ("replicas" if world > 1 else "single"),
+            "l2": "512 MiB write between timed device steps; per-step working set >> 126 MB L2"}
+
+
+def ncu_traffic(workload, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu launch list of the workload (profiles/)."""
+    tf = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
+    try:
+        with open(tf) as f:
+            rec = json.load(f).get(workload, {})
+        return rec.get(kernel), rec.get("_source")
+    except Exception:
+        return None, None
+
+
 def time_cpu(case, warm, steps, remap_kind=None):
     """Wall-clock the CPU implementation on `steps` steps after `warm`."""
     from paper_2208_13409_b200 import abi
@@ -240,14 +277,13 @@ def run_product(args, world, rank, local, pg):
                      "achieved": ach, "frac": ach / peak,
                      "share_of_step": kms / ph["total"] if ph["total"] > 0 else None}
     dom = max(kern, key=lambda g: kern[g]["ms"])
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
-    if os.path.exists(tf):
-        try:
-            with open(tf) as f:
-                traffic = json.load(f).get(args.workload, {}).get(kern[dom]["kernel"].split("<")[0])
-        except Exception:
-            traffic = None
+    dom_name = kern[dom]["kernel"].split("<")[0]
+    traffic, traffic_src = ncu_traffic(args.workload, dom_name)
+    # the dominant kernel against the HBM roofline: algorithmic bytes =
+    # SURVEY 8d's B_min per cell-step x the cells one launch covers, over the
+    # launch's CUDA-event time; its measured DRAM traffic (ncu) beside it
+    dom_ms = kern[dom]["ms"]
+    dom_alg = B_MIN[nmat] * cells / (dom_ms / 1e3) / 1e9
 
     # end to end through the public API with host (pinned) State buffers.
     # (1) e2e: the reference's hot-loop call -- run(State, K steps) -- on a host
@@ -301,20 +337,20 @@ def run_product(args, world, rank, local, pg):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (init_case-equivalent painter, seeded)",
-        "config": {"workload": case.name, "cells": cells, "materials": nmat, "steps_from": "t=0 after warmup",
-                   "scheme": {abi.REMAP_AD: "AD split (X/Y alternating)", abi.REMAP_DIRECT: "Direct (faces only)"}
-                             .get(kind, "DirectCF") +
-                             " face_order=2 LinearDiag interface_degrade", "cfl": case.cfl,
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "512 MiB write between timed steps; working set per step >> 126 MB L2"},
+        "config": config_of(case, args.remap, world),
         "phases_ms": dict(ph, note=f"{n_ph} un-graphed steps after the timed ones, CUDA events between "
                                     "kernel groups on the launching stream"),
-        "roofline": {"bound": "hbm", "achieved": kern[dom]["achieved"], "peak": peak, "unit": "GB/s",
-                     "frac": kern[dom]["frac"], "traffic": traffic, "peak_source": peak_kind,
-                     "kernel": kern[dom]["kernel"], "kernel_ms": kern[dom]["ms"],
+        "roofline": {"bound": "hbm", "achieved": dom_alg, "peak": peak, "unit": "GB/s",
+                     "frac": dom_alg / peak, "traffic": traffic, "peak_source": peak_kind,
+                     "kernel": kern[dom]["kernel"], "kernel_ms": dom_ms,
                      "share_of_step": kern[dom]["share_of_step"],
-                     "basis": f"{kern[dom]['bytes_per_cell']} B/cell compulsory I/O of the kernel x {cells} "
-                              f"cells per launch, CUDA-event time of the launch",
+                     "basis": f"algorithmic {B_MIN[nmat]} B/cell-step (SURVEY 8d B_min) x {cells} cells per "
+                              f"launch / CUDA-event time of the launch",
+                     "dram_achieved": traffic / (dom_ms / 1e3) / 1e9 if traffic else None,
+                     "dram_frac": traffic / (dom_ms / 1e3) / 1e9 / peak if traffic else None,
+                     "traffic_source": traffic_src,
+                     "kernel_boundary": {"bytes_per_cell": kern[dom]["bytes_per_cell"],
+                                         "achieved": kern[dom]["achieved"], "frac": kern[dom]["frac"]},
                      "kernels": kern},
         "step_roofline": {"bound": "hbm", "achieved": achieved_step, "peak": peak, "unit": "GB/s",
                           "frac": achieved_step / peak,
@@ -334,7 +370,8 @@ def run_product(args, world, rank, local, pg):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # a bounded sample: about 3e7 cell-updates (10-30 s of one core)
         v, ckind, n, secs = time_cpu(case, 0, min(args.cpu_steps, max(1, int(3e7 // case.cells))), kind)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": ckind,
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": ckind, "cpu": cpu_model(),
+                                "nproc": os.cpu_count(),
                                 "sample": f"{case.name}: first {n} steps from t=0, single thread, {secs:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -410,18 +447,21 @@ def run_reference(args, world, rank, pg):
         return
     from paper_2208_13409_b200 import abi
     case = workload(args.workload)
-    steps = args.steps
+    # a bounded sample: about 1.2e8 cell-updates (~1 min of one core), at
+    # least one step; warm-up steps only where they fit the same budget
+    budget = max(1, int(1.2e8 // case.cells))
+    steps = max(1, min(args.steps, budget))
+    warm = min(args.warmup, budget - steps)
     rk = {"ad": abi.REMAP_AD, "direct": abi.REMAP_DIRECT}.get(args.remap, abi.REMAP_DIRECTCF)
-    v, ckind, n, secs = time_cpu(case, args.warmup, steps, rk)
+    v, ckind, n, secs = time_cpu(case, warm, steps, rk)
     line = {
-        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": args.warmup,
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": warm,
         "ms_per_step": secs * 1e3 / max(n, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (init_case-equivalent painter, seeded)", "impl": "reference",
-        "config": {"workload": case.name, "cells": case.cells, "materials": case.cfg.nmat, "cfl": case.cfl,
-                   "scheme": {"ad": "AD split", "direct": "Direct"}.get(args.remap, "DirectCF"),
-                   "parallelism": "single"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": ckind,
-                         "sample": f"{case.name}: steps {args.warmup + 1}..{args.warmup + n}, single thread "
+        "config": config_of(case, args.remap, 1),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": ckind, "cpu": cpu_model(),
+                         "nproc": os.cpu_count(),
+                         "sample": f"{case.name}: steps {warm + 1}..{warm + n} of the workload, single thread "
                                    f"(the reference has no threading), {secs:.1f} s"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -431,10 +471,10 @@ def run_reference(args, world, rank, pg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--remap", default="directcf", choices=["directcf", "ad", "direct"],
                     help="remap engine: DirectCF (the path), the AD split scheme or the Direct faces-only "
                          "engine (SURVEY 8f)")

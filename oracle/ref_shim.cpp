@@ -546,3 +546,196 @@ extern "C" int h2dr_convergence(const char* name, const int* meshes, int nmesh, 
     if (rc && err_what) std::snprintf(err_what, err_cap, "%s", c.err.what);
     return rc;
 }
+
+// ---- sub-step entry points and the scalar kernels (h2d.h, the reference's
+// predict / correct / remap_single_axis and its public scalar functions) ----
+extern "C" {
+
+int h2dr_predict(h2dr_ctx* c, double dt, h2d_half* out) {
+    return guarded(c, -1, 0, [&] {
+        const HalfStepState h = predict(c->s, c->mats, dt, c->pv);
+        if (!out) return;
+        get(h.x_half, out->x_half);
+        get(h.u_half, out->u_half);
+        get(h.vol_half, out->vol_half);
+        for (int a = 0; a < c->s.nmat; ++a) {
+            get(h.e_half[a], out->e_half[a]);
+            get(h.p_half[a], out->p_half[a]);
+        }
+        get(h.p_mix_half, out->p_mix_half);
+        get(h.q, out->q);
+        out->floor_count = h.floor_count;
+    });
+}
+
+int h2dr_correct(h2dr_ctx* c, double dt, const h2d_half* in, h2d_lagrange* out) {
+    const Mesh& m = c->s.mesh;
+    HalfStepState h;
+    h.u_half = Field<Vec2>(m.nx + 1, m.ny + 1);
+    put(h.u_half, in->u_half);
+    for (int a = 0; a < c->s.nmat; ++a) {
+        h.p_half[a] = Field<double>(m.nx, m.ny);
+        put(h.p_half[a], in->p_half[a]);
+    }
+    h.q = Field<double>(m.nx, m.ny);
+    put(h.q, in->q);
+    h.floor_count = in->floor_count;
+    return guarded(c, -1, 0, [&] {
+        c->lag = correct(c->s, c->mats, h, dt);
+        c->have_lag = true;
+        lag_out(c->lag, out, c->s.nmat);
+    });
+}
+
+int h2dr_remap_single_axis(h2dr_ctx* c, double dt, int axis_x, int remap_velocity, h2d_remap_diag* diag) {
+    if (!c->have_lag) {
+        set_err(c, H2D_ERR_INVALID, "remap_single_axis without a LagrangeResult", -1, -1, -1, 0);
+        return H2D_ERR_INVALID;
+    }
+    return guarded(c, -1, 0, [&] {
+        RemapDiag d;
+        if (diag) {
+            d.max_k_violation = diag->max_k_violation;
+            d.k_clip_count = diag->k_clip_count;
+            d.mass_fix_count = diag->mass_fix_count;
+        }
+        c->s = remap_single_axis(c->s, c->mats, c->lag, dt, axis_x ? Axis::X : Axis::Y, c->rc,
+                                 remap_velocity != 0, diag ? &d : nullptr);
+        if (diag) {
+            diag->max_k_violation = d.max_k_violation;
+            diag->k_clip_count = d.k_clip_count;
+            diag->mass_fix_count = d.mass_fix_count;
+        }
+        c->have_lag = false;
+    });
+}
+
+namespace {
+void st3(const double* x, Stencil3x3& st) {
+    for (int p = 0; p < 3; ++p)
+        for (int q = 0; q < 3; ++q) {
+            st.a[p][q] = x[p * 3 + q];
+            st.xl[p][q] = {x[9 + p * 3 + q], x[18 + p * 3 + q]};
+        }
+}
+// one record of h2d_scalar_eval through the reference function; true = it threw
+bool ref_scalar(int op, const double* x, double* o) {
+    try {
+        switch (op) {
+        case H2D_SC_VAN_LEER: o[0] = van_leer(x[0]); break;
+        case H2D_SC_LIMITED_GRADIENT: o[0] = limited_gradient_1d(x[0], x[1], x[2], x[3], x[4], x[5]); break;
+        case H2D_SC_FACE_VALUE: {
+            Stencil1D d{{x[1], x[2], x[3]}, {x[4], x[5], x[6]}};
+            o[0] = face_value(static_cast<int>(x[0]), d, x[7], x[8], x[9]);
+            break;
+        }
+        case H2D_SC_CORNER_VALUE: {
+            Stencil3x3 st;
+            st3(x + 1, st);
+            const double* k = x + 28;
+            CornerKin kin;
+            kin.dxp = k[0];
+            kin.dyp = k[1];
+            kin.lag_wx = k[2];
+            kin.lag_wy = k[3];
+            kin.sgn_fx = k[4];
+            kin.u_fx_dt = k[5];
+            kin.sgn_fy = k[6];
+            kin.u_fy_dt = k[7];
+            kin.eval_rel = {k[8], k[9]};
+            kin.dx = k[10];
+            kin.dy = k[11];
+            o[0] = corner_value(static_cast<CornerScheme>(static_cast<int>(x[0])), st, kin);
+            break;
+        }
+        case H2D_SC_MULTID_PLANE: {
+            Stencil3x3 st;
+            st3(x, st);
+            const PlaneRecon pl = multid_plane(st, x[27], x[28]);
+            const double v[] = {pl.a0, pl.center.x, pl.center.y, pl.grad_raw.x, pl.grad_raw.y, pl.grad.x, pl.grad.y};
+            std::memcpy(o, v, sizeof v);
+            break;
+        }
+        case H2D_SC_CLIPPED_FRACTION: o[0] = clipped_fraction(x[0], x[1], {x[2], x[3]}, x[4]); break;
+        case H2D_SC_PLACE_INTERFACE:
+            o[0] = place_interface(x[0], {x[1], x[2]}, Rect{{x[3], x[4]}, {x[5], x[6]}}).d;
+            break;
+        case H2D_SC_YOUNGS_NORMAL: {
+            Field<double> k1(3, 3);
+            for (int di = -1; di <= 1; ++di)
+                for (int dj = -1; dj <= 1; ++dj) k1(1 + di, 1 + dj) = x[(di + 1) * 3 + dj + 1];
+            const Vec2 n = youngs_normal(k1, 1, 1, x[9], x[10]);
+            o[0] = n.x;
+            o[1] = n.y;
+            break;
+        }
+        case H2D_SC_CELL_VOLUME:
+            o[0] = cell_volume({x[0], x[1]}, {x[2], x[3]}, {x[4], x[5]}, {x[6], x[7]});
+            break;
+        case H2D_SC_CF_CORNER_FLUX: {
+            const CornerFlux f = cf_corner_flux({x[0], x[1]}, x[2]);
+            o[0] = f.dvol;
+            o[1] = f.sx;
+            o[2] = f.sy;
+            break;
+        }
+        case H2D_SC_CF_FACE_FLUX_X:
+        case H2D_SC_CF_FACE_FLUX_Y: {
+            const CfFaceFlux f = op == H2D_SC_CF_FACE_FLUX_X ? cf_face_flux_x(x[0], x[1], {x[2], x[3]}, {x[4], x[5]})
+                                                              : cf_face_flux_y(x[0], x[1], {x[2], x[3]}, {x[4], x[5]});
+            o[0] = f.dvol;
+            o[1] = f.wlo;
+            o[2] = f.whi;
+            break;
+        }
+        case H2D_SC_PSEUDO_VISCOSITY:
+            o[0] = pseudo_viscosity(x[0], x[1], x[2], PseudoViscosityParams{x[3], x[4]}, x[5]);
+            break;
+        case H2D_SC_DIV_U_CELL: {
+            Field<Vec2> u(1, 1);
+            u(0, 0) = {x[0], x[1]};
+            u(1, 0) = {x[2], x[3]};
+            u(0, 1) = {x[4], x[5]};
+            u(1, 1) = {x[6], x[7]};
+            o[0] = div_u_cell(Mesh(3, 3, x[8], x[9]), u, 0, 0);
+            break;
+        }
+        case H2D_SC_GRAD_PQ_NODE: {
+            Field<double> p(3, 3), q(3, 3);
+            const int ci[4] = {0, 1, 0, 1}, cj[4] = {0, 0, 1, 1};
+            for (int r = 0; r < 4; ++r) {
+                p(ci[r], cj[r]) = x[r];
+                q(ci[r], cj[r]) = x[4 + r];
+            }
+            const Vec2 g = grad_pq_node(Mesh(3, 3, x[8], x[9]), p, q, 1, 1);
+            o[0] = g.x;
+            o[1] = g.y;
+            break;
+        }
+        case H2D_SC_AD_FACE_FLUX: {
+            // one X face of ad_face_fluxes on a 3 x 3 mesh whose dy and cv are the record's
+            const double dy = x[3], dx = x[4] / x[3];
+            Field<Vec2> uh(4, 4);
+            uh(0, 0) = {x[0], 0.0};
+            uh(0, 1) = {x[1], 0.0};
+            o[0] = ad_face_fluxes(Axis::X, Mesh(3, 3, dx, dy), uh, x[2])(0, 0);
+            break;
+        }
+        default: return true;
+        }
+    } catch (const std::exception&) {
+        return true;
+    }
+    return false;
+}
+}  // namespace
+
+int h2dr_scalar_eval(int op, int n, const double* in, double* out, int* flags) {
+    for (int r = 0; r < n; ++r) {
+        const bool bad = ref_scalar(op, in + (size_t)r * H2D_SC_IN, out + (size_t)r * H2D_SC_OUT);
+        if (flags) flags[r] = bad ? 1 : 0;
+    }
+    return 0;
+}
+
+}  // extern "C"

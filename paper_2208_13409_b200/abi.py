@@ -61,6 +61,12 @@ class LagrangeView(C.Structure):
                 ("q", _dp), ("floor_count", C.c_int)]
 
 
+class HalfView(C.Structure):
+    """h2d_half: HalfStepState (lagrange.hpp:14-24)."""
+    _fields_ = [("x_half", _dp), ("u_half", _dp), ("vol_half", _dp), ("e_half", _dp * MAX_MAT),
+                ("p_half", _dp * MAX_MAT), ("p_mix_half", _dp), ("q", _dp), ("floor_count", C.c_int)]
+
+
 class RemapDiag(C.Structure):
     """hydro::RemapDiag (remap.hpp:42-46)."""
     _fields_ = [("max_k_violation", C.c_double), ("k_clip_count", C.c_int),
@@ -204,6 +210,52 @@ class HostLagrange:
         return v
 
 
+SC_IN, SC_OUT = 48, 8  # H2D_SC_IN / H2D_SC_OUT
+(SC_VAN_LEER, SC_LIMITED_GRADIENT, SC_FACE_VALUE, SC_CORNER_VALUE, SC_MULTID_PLANE, SC_CLIPPED_FRACTION,
+ SC_PLACE_INTERFACE, SC_YOUNGS_NORMAL, SC_CELL_VOLUME, SC_CF_CORNER_FLUX, SC_CF_FACE_FLUX_X, SC_CF_FACE_FLUX_Y,
+ SC_PSEUDO_VISCOSITY, SC_DIV_U_CELL, SC_GRAD_PQ_NODE, SC_AD_FACE_FLUX) = range(16)
+
+
+@dataclass
+class HostHalf:
+    """Host copy of a HalfStepState (lagrange.hpp:14-24)."""
+    x_half: np.ndarray
+    u_half: np.ndarray
+    vol_half: np.ndarray
+    e_half: np.ndarray
+    p_half: np.ndarray
+    p_mix_half: np.ndarray
+    q: np.ndarray
+    floor_count: int = 0
+
+    @classmethod
+    def empty(cls, nx: int, ny: int) -> "HostHalf":
+        cs, ns = (ny + 2 * GHOST, nx + 2 * GHOST), (ny + 1 + 2 * GHOST, nx + 1 + 2 * GHOST)
+        return cls(np.zeros(ns + (2,)), np.zeros(ns + (2,)), np.zeros(cs), np.zeros((MAX_MAT,) + cs),
+                   np.zeros((MAX_MAT,) + cs), np.zeros(cs), np.zeros(cs))
+
+    def view(self) -> HalfView:
+        v = HalfView()
+        v.x_half, v.u_half, v.vol_half = _ptr(self.x_half), _ptr(self.u_half), _ptr(self.vol_half)
+        for a in range(MAX_MAT):
+            v.e_half[a], v.p_half[a] = _ptr(self.e_half[a]), _ptr(self.p_half[a])
+        v.p_mix_half, v.q, v.floor_count = _ptr(self.p_mix_half), _ptr(self.q), self.floor_count
+        return v
+
+
+def scalar_eval(lib: "Library", op: int, records: np.ndarray):
+    """h2d_scalar_eval over records[n, <= SC_IN] -> (out[n, SC_OUT], flags[n])."""
+    n = len(records)
+    inp = np.zeros((n, SC_IN))
+    inp[:, :records.shape[1]] = records
+    out = np.zeros((n, SC_OUT))
+    flags = np.zeros(n, np.int32)
+    rc = lib.fn["scalar_eval"](op, n, _ptr(inp), _ptr(out), flags.ctypes.data_as(C.POINTER(C.c_int)))
+    if rc:
+        raise errors.from_code(rc, f"{lib.prefix}scalar_eval failed ({rc})")
+    return out, flags
+
+
 @dataclass
 class RunResult:
     steps_done: int
@@ -242,6 +294,10 @@ _EXTRA = {
     "load_state": ([C.c_void_p, C.c_char_p], C.c_int),
     "save_state_host": ([C.POINTER(Config), C.POINTER(StateView), C.c_char_p], C.c_int),
     "load_state_host": ([C.POINTER(Config), C.POINTER(StateView), C.c_char_p], C.c_int),
+    "predict": ([C.c_void_p, C.c_double, C.POINTER(HalfView)], C.c_int),
+    "correct": ([C.c_void_p, C.c_double, C.POINTER(HalfView), C.POINTER(LagrangeView)], C.c_int),
+    "remap_single_axis": ([C.c_void_p, C.c_double, C.c_int, C.c_int, C.POINTER(RemapDiag)], C.c_int),
+    "scalar_eval": ([C.c_int, C.c_int, _dp, _dp, C.POINTER(C.c_int)], C.c_int),
     "launch_count": ([], C.c_longlong),
     "step_timed": ([C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_float)], C.c_int),
     "flush_l2": ([C.c_void_p, C.c_longlong], C.c_int),
@@ -344,6 +400,27 @@ class Solver:
         if out:
             out.floor_count = v.floor_count
         return out
+
+    def predict(self, dt: float) -> HostHalf:
+        """HalfStepState predict(State, MaterialSet, dt, PseudoViscosityParams)."""
+        out = HostHalf.empty(self.nx, self.ny)
+        v = out.view()
+        self._check(self.lib.fn["predict"](self._h, dt, C.byref(v)))
+        out.floor_count = v.floor_count
+        return out
+
+    def correct(self, dt: float, half: HostHalf) -> HostLagrange:
+        """LagrangeResult correct(State, MaterialSet, HalfStepState, dt)."""
+        out = HostLagrange.empty(self.nx, self.ny)
+        v = out.view()
+        self._check(self.lib.fn["correct"](self._h, dt, C.byref(half.view()), C.byref(v)))
+        out.floor_count = v.floor_count
+        return out
+
+    def remap_single_axis(self, dt: float, axis_x: bool, remap_velocity: bool = True,
+                          diag: Optional[RemapDiag] = None):
+        self._check(self.lib.fn["remap_single_axis"](self._h, dt, int(axis_x), int(remap_velocity),
+                                                     C.byref(diag) if diag is not None else None))
 
     def set_lagrange(self, lag: HostLagrange):
         self._check(self.lib.fn["set_lagrange"](self._h, C.byref(lag.view())))

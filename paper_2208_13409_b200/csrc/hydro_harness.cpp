@@ -434,17 +434,18 @@ struct Counters {
 
 // the dynamic branch: cfl_dt -> lagrange_step -> remap_step -> nan_scan -> make_diag
 void run_dynamic(const CaseSpec& cs, Resident& dev, const StepHook& hook, RunReport& rep, Counters& cnt) {
-    const int cap = cs.max_steps > 0 ? cs.max_steps : 65536;
+    constexpr int kChunk = 65536;  // the device run loop's dt / StepDiag log capacity per call
     std::vector<double> dts;
     std::vector<h2d_step_diag> ser;
-    auto call = [&](int max_steps, bool series) {
+    // one h2d_run call from the State's step `from` up to (absolute) step `to`
+    auto call = [&](int from, int to, bool series) {
         h2d_run_args a;
         std::memset(&a, 0, sizeof a);
-        a.max_steps = max_steps;
+        a.max_steps = to;
         a.t_end = cs.t_end;
         a.cfl = cs.cfl;
         a.remap_kind = remap_code(cs.scheme);
-        dts.assign(max_steps > 0 ? max_steps : cap, 0.0);
+        dts.assign(static_cast<size_t>(to - from), 0.0);
         a.dt_log = dts.data();
         a.dt_log_cap = static_cast<int>(dts.size());
         if (series) {
@@ -455,25 +456,27 @@ void run_dynamic(const CaseSpec& cs, Resident& dev, const StepHook& hook, RunRep
         const int rc = h2d_run(dev.h, &a);
         cnt.add(a);
         if (series)
-            for (int q = 0; q < a.steps_done; ++q) rep.series.push_back(Resident::from_c(ser[q]));
+            for (int q = 0; q < a.steps_done && q < a.series_cap; ++q) rep.series.push_back(Resident::from_c(ser[q]));
         if (rc) Resident::rethrow(dev.error(), &cs);
-        return a;
+        return a.steps_done;
     };
     // the StepDiag sums: the device run loop reduces them as a fixed-order
     // tree (within n 2^-53 sum|x| of the reference's serial loop); a hook, or a
     // mesh up to kSerialDiagCells, gets the reference's serial sums bit for bit
     // (h2d_step_diag_now after every device step)
     constexpr long long kSerialDiagCells = 1LL << 20;
-    if (!hook && static_cast<long long>(cs.nx) * cs.ny > kSerialDiagCells) {
-        call(cs.max_steps, true);
-        return;
-    }
-    for (int step = rep.initial_state.step;; ++step) {
+    const bool fast = !hook && static_cast<long long>(cs.nx) * cs.ny > kSerialDiagCells;
+    for (int step = rep.initial_state.step;;) {
         if (cs.max_steps > 0 && step >= cs.max_steps) break;
-        const h2d_run_args a = call(step + 1, false);
-        if (a.steps_done == 0) break;  // t_end reached
-        rep.series.push_back(dev.diag_now(dts[a.steps_done - 1]));
-        if (hook) hook(dev.download(), rep.series.back());
+        int to = fast ? step + kChunk : step + 1;
+        if (cs.max_steps > 0 && to > cs.max_steps) to = cs.max_steps;
+        const int done = call(step, to, fast);
+        step += done;
+        if (!fast && done == 1) {
+            rep.series.push_back(dev.diag_now(dts[0]));
+            if (hook) hook(dev.download(), rep.series.back());
+        }
+        if (done < to - (step - done)) break;  // t_end reached
     }
 }
 
