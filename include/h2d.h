@@ -295,6 +295,23 @@ int h2d_halo_unpack(h2d_ctx* ctx, int dx, int dy, const void* dev_buf);
 /* counters, dt log and first error of the block's run (like h2d_run) */
 int h2d_block_result(h2d_ctx* ctx, h2d_run_args* args);
 
+/* The block run loop with the data plane in the library: every step of
+ * every block, the one max all-reduce of {next wave speed, first cfl error,
+ * first error, done} and the one halo exchange (8 neighbours, corners
+ * included) are enqueued on the device; the exchange overlaps the next step's
+ * Lagrange tiles on owned data; the host polls every 16 steps. A transport
+ * is either NCCL (one block per process: rank = by * px + bx of a px x py
+ * grid, the communicator created here from an id of h2d_nccl_unique_id,
+ * libnccl.so.2 opened at run time) or in-process (all px * py blocks of the
+ * decomposition in this process, one device, rank order). Counters, dt log
+ * and errors per block come from h2d_block_result afterwards. */
+typedef struct h2d_comm h2d_comm;
+int h2d_nccl_unique_id(unsigned char id[128]);
+int h2d_comm_nccl(const unsigned char id[128], int px, int py, int rank, h2d_ctx* block, h2d_comm** out);
+int h2d_comm_local(h2d_ctx* const* blocks, int px, int py, h2d_comm** out);
+void h2d_comm_destroy(h2d_comm* comm);
+int h2d_blocks_run(h2d_comm* comm, int max_steps, double t_end, double cfl, int* steps_done);
+
 /* ---- benchmark support (no reference counterpart) ---------------------- */
 /* Kernels launched by this library in the calling process so far. */
 long long h2d_launch_count(void);
@@ -317,7 +334,7 @@ int h2d_flush_l2(h2d_ctx* ctx, long long bytes);
 
 /* HalfStepState (lagrange.hpp:14-24). */
 typedef struct {
-    double* x_half;  /* node Vec2 (filled by the caller's layer: node_pos + 0.5 dt u) */
+    double* x_half;  /* node Vec2 */
     double* u_half;  /* node Vec2 */
     double* vol_half;
     double* e_half[H2D_MAX_MAT];

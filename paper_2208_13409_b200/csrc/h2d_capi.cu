@@ -63,6 +63,8 @@ struct h2d_ctx {
     void* diag_mem = nullptr;       // DiagRed scratch of k_post / the node update
     size_t diag_tick_bytes = 0;     // the ticket words at the start of diag_mem
     double* diag_log = nullptr;     // device StepDiag log of h2d_run (kDiagRec doubles per step)
+    cudaGraphExec_t graph_rest[2] = {nullptr, nullptr};  // block data plane: the step after the Lagrange kernel
+    long long graph_rest_kernels = 0;
 };
 
 namespace {
@@ -779,6 +781,8 @@ void h2d_destroy(h2d_ctx* c) {
             if (g) cudaGraphExecDestroy(g);
     for (auto& g : c->graph_dir)
         if (g) cudaGraphExecDestroy(g);
+    for (auto& g : c->graph_rest)
+        if (g) cudaGraphExecDestroy(g);
     if (c->ad_mem) cudaFree(c->ad_mem);
     if (c->st) cudaStreamSynchronize(c->st);
     if (c->arena) cudaFree(c->arena);
@@ -994,12 +998,15 @@ int h2d_predict(h2d_ctx* c, double dt, h2d_half* out) {
     }
     launch_begin(c->ctl, 1, dt, c->st);
     launch_lagrange_mode(d, 0, 1, c->st);
+    launch_xhalf(d, d.ulx, d.uly, c->st);  // x_half in the u_lag scratch (predict has no u_lag)
     if (int rc = check_launch(c)) return rc;
     if (int rc = ctl_pull(c)) return rc;
     if (int rc = decode_error(c, false)) return rc;
     if (out) {
         const int nx = c->nx, ny = c->ny;
         if (int rc = get_vec(c, out->u_half, d.uhx, d.uhy, nx + 1, ny + 1)) return rc;
+        CK(cudaStreamSynchronize(c->st));
+        if (int rc = get_vec(c, out->x_half, d.ulx, d.uly, nx + 1, ny + 1)) return rc;
         CK(cudaStreamSynchronize(c->st));
         if (int rc = get_plane(c, out->vol_half, d.vol_lag, nx, ny)) return rc;
         for (int a = 0; a < c->nmat; ++a) {
@@ -1724,6 +1731,386 @@ int h2d_block_result(h2d_ctx* c, h2d_run_args* a) {
 
 int h2d_last_error(h2d_ctx* c, h2d_error* e) {
     *e = c->err;
+    return 0;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Block-decomposition data plane: the whole multi-block run
+// loop in the library, with the State, the control block and every per-step
+// exchange on the device.  Per step and block, on the block's compute stream
+// st and its communication stream cs:
+//
+//   st: wait(apply) -> k_step_start + Lagrange tiles on owned data
+//       -> wait(halo) -> Lagrange edge tiles -> rest of the step (graph)
+//       -> k_red_pack: {next wave speed, ~next cfl error, ~error, done}
+//   cs: wait(red) -> ONE max all-reduce of the four words -> k_red_apply
+//       (global dt input and first error; a pre-commit error anywhere rolls
+//       every committed block back) -> record(apply) -> pack every halo
+//       rectangle (8 neighbours, corners included) into one buffer ->
+//       grouped send/recv with the neighbours -> unpack -> record(halo)
+//
+// so the halo exchange overlaps the next step's Lagrange tiles on owned
+// data, and the host only polls the control blocks every kPollSteps steps.
+// Transports: NCCL (one block per process, the communicator owned here,
+// opened at run time from libnccl.so.2) or in-process (every block of the
+// decomposition in this process on one device: device-to-device copies and a
+// one-block max kernel, same stream structure).
+// ===========================================================================
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is opened with dlopen
+
+namespace {
+
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    bool load() {
+        if (h) return true;
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+        auto sym = [&](auto& f, const char* n) { f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, n)); return f != nullptr; };
+        return sym(GetUniqueId, "ncclGetUniqueId") && sym(CommInitRank, "ncclCommInitRank") &&
+               sym(CommDestroy, "ncclCommDestroy") && sym(AllReduce, "ncclAllReduce") && sym(Send, "ncclSend") &&
+               sym(Recv, "ncclRecv") && sym(GroupStart, "ncclGroupStart") && sym(GroupEnd, "ncclGroupEnd");
+    }
+};
+NcclApi g_nccl;
+
+const int kDirs[8][2] = {{-1, -1}, {0, -1}, {1, -1}, {-1, 0}, {1, 0}, {-1, 1}, {0, 1}, {1, 1}};
+int dir_index(int dx, int dy) {
+    for (int q = 0; q < 8; ++q)
+        if (kDirs[q][0] == dx && kDirs[q][1] == dy) return q;
+    return -1;
+}
+
+}  // namespace
+
+struct h2d_comm {
+    int kind = 0;  // 0 in-process, 1 NCCL
+    int px = 1, py = 1;
+    ncclComm_t nccl = nullptr;
+    struct Side {
+        h2d_ctx* c = nullptr;
+        int rank = 0, bx = 0, by = 0;
+        int peer[8];                 // neighbour rank per direction (-1: global boundary)
+        HaloPlan pk{}, up{};         // pack / unpack rectangles, segments ordered like kDirs
+        int seg_pk[8], seg_up[8];    // segment of direction q in pk / up (-1: none)
+        double *send = nullptr, *recv = nullptr;
+        unsigned long long* red = nullptr;
+        cudaStream_t cs = nullptr;
+        cudaEvent_t e_red = nullptr, e_apply = nullptr, e_packed = nullptr, e_halo = nullptr;
+    };
+    std::vector<Side> side;
+    unsigned long long** red_ptrs = nullptr;  // device array of every side's red (in-process)
+    cudaEvent_t e_all = nullptr;
+};
+
+namespace {
+
+void comm_free(h2d_comm* m) {
+    for (auto& sd : m->side) {
+        if (sd.c) cudaSetDevice(sd.c->device);
+        if (sd.cs) cudaStreamSynchronize(sd.cs);
+        if (sd.send) cudaFree(sd.send);
+        if (sd.recv) cudaFree(sd.recv);
+        if (sd.red) cudaFree(sd.red);
+        for (cudaEvent_t e : {sd.e_red, sd.e_apply, sd.e_packed, sd.e_halo})
+            if (e) cudaEventDestroy(e);
+        if (sd.cs) cudaStreamDestroy(sd.cs);
+    }
+    if (m->red_ptrs) cudaFree(m->red_ptrs);
+    if (m->e_all) cudaEventDestroy(m->e_all);
+    if (m->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(m->nccl);
+    delete m;
+}
+
+// planes of State parity p exchanged with the neighbours (state_lists at p)
+void lists_at(h2d_ctx* c, int p, FieldList& cl, FieldList& nl) {
+    const int keep = c->cur;
+    c->cur = p;
+    state_lists(c, cl, nl);
+    c->cur = keep;
+}
+
+int side_setup(h2d_comm* m, h2d_comm::Side& sd) {
+    h2d_ctx* c = sd.c;
+    cudaSetDevice(c->device);
+    if (!c->is_block) return H2D_ERR_INVALID;
+    FieldList cl, nl;
+    state_lists(c, cl, nl);
+    sd.pk.n = sd.up.n = 0;
+    sd.pk.off[0] = sd.up.off[0] = 0;
+    for (int q = 0; q < 8; ++q) {
+        const int x = sd.bx + kDirs[q][0], y = sd.by + kDirs[q][1];
+        sd.peer[q] = (x >= 0 && x < m->px && y >= 0 && y < m->py) ? y * m->px + x : -1;
+        sd.seg_pk[q] = sd.seg_up[q] = -1;
+        if (sd.peer[q] < 0) continue;
+        for (int pack = 1; pack >= 0; --pack) {
+            HaloPlan& pl = pack ? sd.pk : sd.up;
+            Rng rc, rn;
+            halo_rects(c, kDirs[q][0], kDirs[q][1], pack != 0, rc, rn);
+            (pack ? sd.seg_pk : sd.seg_up)[q] = pl.n;
+            pl.rc[pl.n] = rc;
+            pl.rn[pl.n] = rn;
+            pl.off[pl.n + 1] = pl.off[pl.n] + rect_doubles(cl, nl, rc, rn);
+            ++pl.n;
+        }
+    }
+    CK(cudaMalloc(&sd.send, (size_t)(sd.pk.off[sd.pk.n] > 0 ? sd.pk.off[sd.pk.n] : 1) * sizeof(double)));
+    CK(cudaMalloc(&sd.recv, (size_t)(sd.up.off[sd.up.n] > 0 ? sd.up.off[sd.up.n] : 1) * sizeof(double)));
+    CK(cudaMalloc(&sd.red, 4 * sizeof(unsigned long long)));
+    CK(cudaStreamCreateWithFlags(&sd.cs, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&sd.e_red, &sd.e_apply, &sd.e_packed, &sd.e_halo})
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    // the Lagrange tiles whose stencil reads owned data only: tile origins
+    // (i0, j0) with cells [i0-1, i0+LTX] and nodes [i0-1, i0+LTX+1] inside
+    // the owned range on every side that has a neighbour (walls are local)
+    const h2d_block& b = c->blk;
+    const int ltx = lag_tile_w(), lty = lag_tile_h();
+    Rng in{-(1 << 29), 1 << 29, -(1 << 29), 1 << 29};
+    if (sd.bx > 0) in.i0 = b.oi + 1;
+    if (sd.bx < m->px - 1) in.i1 = b.oi + b.bnx - 1 - ltx;
+    if (sd.by > 0) in.j0 = b.oj + 1;
+    if (sd.by < m->py - 1) in.j1 = b.oj + b.bny - 1 - lty;
+    c->base.lag_inner = in;
+    // the step after the Lagrange kernel, per State parity
+    for (int p = 0; p < 2; ++p) {
+        if (c->graph_rest[p]) continue;
+        cudaGraph_t g = nullptr;
+        const long long before = launch_count();
+        CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+        launch_step_block_rest(make_dev(c, p, 1), c->st);
+        CK(cudaStreamEndCapture(c->st, &g));
+        c->graph_rest_kernels = launch_count() - before;
+        add_launches(-c->graph_rest_kernels);
+        const cudaError_t e = cudaGraphInstantiate(&c->graph_rest[p], g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+    }
+    return 0;
+}
+
+int comm_finish(h2d_comm* m, h2d_comm** out) {
+    for (auto& sd : m->side)
+        if (int rc = side_setup(m, sd)) {
+            comm_free(m);
+            return rc;
+        }
+    if (m->kind == 0) {
+        h2d_ctx* c = m->side[0].c;
+        std::vector<unsigned long long*> ptrs;
+        for (auto& sd : m->side) ptrs.push_back(sd.red);
+        CK(cudaMalloc(&m->red_ptrs, ptrs.size() * sizeof(void*)));
+        CK(cudaMemcpy(m->red_ptrs, ptrs.data(), ptrs.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        CK(cudaEventCreateWithFlags(&m->e_all, cudaEventDisableTiming));
+    }
+    *out = m;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int h2d_nccl_unique_id(unsigned char id[128]) {
+    if (!g_nccl.load()) return H2D_ERR_INVALID;
+    ncclUniqueId u;
+    if (g_nccl.GetUniqueId(&u) != ncclSuccess) return H2D_ERR_DEVICE;
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, 128);
+    return 0;
+}
+
+int h2d_comm_nccl(const unsigned char id[128], int px, int py, int rank, h2d_ctx* blk, h2d_comm** out) {
+    *out = nullptr;
+    if (!blk || px < 1 || py < 1 || rank < 0 || rank >= px * py) return H2D_ERR_INVALID;
+    if (!g_nccl.load()) {
+        set_err(blk, H2D_ERR_INVALID, "libnccl.so.2 not found");
+        return H2D_ERR_INVALID;
+    }
+    h2d_ctx* c = blk;
+    cudaSetDevice(c->device);
+    h2d_comm* m = new h2d_comm();
+    m->kind = 1;
+    m->px = px;
+    m->py = py;
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    if (g_nccl.CommInitRank(&m->nccl, px * py, u, rank) != ncclSuccess) {
+        delete m;
+        set_err(c, H2D_ERR_DEVICE, "ncclCommInitRank failed");
+        return H2D_ERR_DEVICE;
+    }
+    h2d_comm::Side sd;
+    sd.c = c;
+    sd.rank = rank;
+    sd.bx = rank % px;
+    sd.by = rank / px;
+    m->side.push_back(sd);
+    return comm_finish(m, out);
+}
+
+int h2d_comm_local(h2d_ctx* const* blocks, int px, int py, h2d_comm** out) {
+    *out = nullptr;
+    if (!blocks || px < 1 || py < 1) return H2D_ERR_INVALID;
+    h2d_comm* m = new h2d_comm();
+    m->kind = 0;
+    m->px = px;
+    m->py = py;
+    for (int r = 0; r < px * py; ++r) {
+        h2d_comm::Side sd;
+        sd.c = blocks[r];
+        sd.rank = r;
+        sd.bx = r % px;
+        sd.by = r / px;
+        if (!sd.c || sd.c->device != blocks[0]->device) {
+            delete m;
+            return H2D_ERR_INVALID;
+        }
+        m->side.push_back(sd);
+    }
+    return comm_finish(m, out);
+}
+
+void h2d_comm_destroy(h2d_comm* m) {
+    if (m) comm_free(m);
+}
+
+int h2d_blocks_run(h2d_comm* m, int max_steps, double t_end, double cfl, int* steps_out) {
+    constexpr int kPollSteps = 16;
+    if (steps_out) *steps_out = 0;
+    h2d_ctx* c = m->side[0].c;  // CK's error target
+    const int n = (int)m->side.size();
+    for (auto& sd : m->side)
+        if (int rc = h2d_block_begin(sd.c, max_steps, t_end, cfl)) return rc;
+    std::vector<int> parity(n);
+    for (int b = 0; b < n; ++b) parity[b] = m->side[b].c->cur;
+
+    // the all-reduce + apply of every block's four words, on the cs streams
+    auto combine = [&]() -> int {
+        for (auto& sd : m->side) {
+            launch_red_pack(sd.c->ctl, sd.red, sd.c->st);
+            CK(cudaEventRecord(sd.e_red, sd.c->st));
+            CK(cudaStreamWaitEvent(sd.cs, sd.e_red, 0));
+        }
+        if (m->kind == 1) {
+            auto& sd = m->side[0];
+            if (g_nccl.AllReduce(sd.red, sd.red, 4, ncclUint64, ncclMax, m->nccl, sd.cs) != ncclSuccess) {
+                set_err(c, H2D_ERR_DEVICE, "ncclAllReduce failed");
+                return H2D_ERR_DEVICE;
+            }
+        } else {
+            auto& s0 = m->side[0];
+            for (int b = 1; b < n; ++b) CK(cudaStreamWaitEvent(s0.cs, m->side[b].e_red, 0));
+            launch_red_local(m->red_ptrs, n, s0.cs);
+            CK(cudaEventRecord(m->e_all, s0.cs));
+            for (int b = 1; b < n; ++b) CK(cudaStreamWaitEvent(m->side[b].cs, m->e_all, 0));
+        }
+        for (auto& sd : m->side) {
+            launch_red_apply(sd.c->ctl, sd.red, sd.cs);
+            CK(cudaEventRecord(sd.e_apply, sd.cs));
+        }
+        return check_launch(c);
+    };
+    // the halo exchange of State parity p[b] (after combine, on cs)
+    auto exchange = [&](const std::vector<int>& p) -> int {
+        for (int b = 0; b < n; ++b) {
+            auto& sd = m->side[b];
+            FieldList cl, nl;
+            lists_at(sd.c, p[b], cl, nl);
+            launch_halo_multi(make_dev(sd.c, p[b], 1), cl, nl, sd.pk, sd.send, 1, sd.cs);
+            CK(cudaEventRecord(sd.e_packed, sd.cs));
+        }
+        if (m->kind == 1) {
+            auto& sd = m->side[0];
+            if (g_nccl.GroupStart() != ncclSuccess) return H2D_ERR_DEVICE;
+            for (int q = 0; q < 8; ++q) {
+                if (sd.peer[q] < 0) continue;
+                const int a = sd.seg_pk[q], r = sd.seg_up[q];
+                g_nccl.Send(sd.send + sd.pk.off[a], (size_t)(sd.pk.off[a + 1] - sd.pk.off[a]), ncclFloat64, sd.peer[q],
+                            m->nccl, sd.cs);
+                g_nccl.Recv(sd.recv + sd.up.off[r], (size_t)(sd.up.off[r + 1] - sd.up.off[r]), ncclFloat64, sd.peer[q],
+                            m->nccl, sd.cs);
+            }
+            if (g_nccl.GroupEnd() != ncclSuccess) {
+                set_err(c, H2D_ERR_DEVICE, "NCCL halo exchange failed");
+                return H2D_ERR_DEVICE;
+            }
+        } else {  // pull: my halo segment for direction q is the neighbour's pack segment for -q
+            for (int b = 0; b < n; ++b) {
+                auto& sd = m->side[b];
+                for (int q = 0; q < 8; ++q) {
+                    if (sd.peer[q] < 0) continue;
+                    auto& nb = m->side[sd.peer[q]];
+                    const int a = nb.seg_pk[dir_index(-kDirs[q][0], -kDirs[q][1])], r = sd.seg_up[q];
+                    CK(cudaStreamWaitEvent(sd.cs, nb.e_packed, 0));
+                    CK(cudaMemcpyAsync(sd.recv + sd.up.off[r], nb.send + nb.pk.off[a],
+                                       (size_t)(sd.up.off[r + 1] - sd.up.off[r]) * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, sd.cs));
+                }
+            }
+        }
+        for (int b = 0; b < n; ++b) {
+            auto& sd = m->side[b];
+            FieldList cl, nl;
+            lists_at(sd.c, p[b], cl, nl);
+            launch_halo_multi(make_dev(sd.c, p[b], 1), cl, nl, sd.up, sd.recv, 0, sd.cs);
+            CK(cudaEventRecord(sd.e_halo, sd.cs));
+        }
+        return check_launch(c);
+    };
+
+    if (int rc = combine()) return rc;  // the initial State's global wave speed
+    for (auto& sd : m->side) CK(cudaEventRecord(sd.e_halo, sd.cs));  // the uploaded halos are current
+    for (;;) {
+        int chunk = kPollSteps;
+        if (max_steps > 0) {
+            const int left = max_steps - m->side[0].c->hctl->step;
+            if (left <= 0) break;
+            chunk = left < chunk ? left : chunk;
+        }
+        for (int q = 0; q < chunk; ++q) {
+            for (int b = 0; b < n; ++b) {
+                auto& sd = m->side[b];
+                h2d_ctx* bc = sd.c;
+                const Dev d = make_dev(bc, parity[b], 1);
+                CK(cudaStreamWaitEvent(bc->st, sd.e_apply, 0));
+                launch_step_block_head(d, 1, bc->st);
+                CK(cudaStreamWaitEvent(bc->st, sd.e_halo, 0));
+                launch_step_block_head(d, 2, bc->st);
+                CK(cudaGraphLaunch(bc->graph_rest[parity[b]], bc->st));
+                add_launches(bc->graph_rest_kernels);
+                parity[b] ^= 1;
+            }
+            if (int rc = combine()) return rc;
+            if (int rc = exchange(parity)) return rc;
+        }
+        bool stop = false;
+        for (int b = 0; b < n; ++b) {
+            auto& sd = m->side[b];
+            CK(cudaStreamSynchronize(sd.cs));
+            if (int rc = ctl_pull(sd.c)) return rc;
+            parity[b] = sd.c->hctl->cur;
+            if (sd.c->hctl->err_key != kNoErr || sd.c->hctl->done) stop = true;
+        }
+        if (stop) break;
+    }
+    for (auto& sd : m->side) {
+        CK(cudaStreamSynchronize(sd.cs));
+        if (int rc = ctl_pull(sd.c)) return rc;
+        sd.c->cur = sd.c->hctl->cur;
+    }
+    if (steps_out) *steps_out = m->side[0].c->hctl->steps_done;
     return 0;
 }
 

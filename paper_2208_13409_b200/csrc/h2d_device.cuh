@@ -196,6 +196,11 @@ struct Dev {
     int* sl_list;  // the pending slivers in the reference order (k_slivers), one int per cell of capacity
     Ctl* ctl;
     const TmaSet* tma;  // host pointer: the launch passes *tma by value (__grid_constant__)
+    // block mode: the fused Lagrange kernel runs in two launches around the
+    // halo exchange: lag_sel 1 = only the tiles whose origin lies in
+    // lag_inner (their stencil reads owned data only), 2 = the others, 0 = all
+    Rng lag_inner;
+    int lag_sel;
     int scan_nodes;     // run loop: the node update also runs nan_scan's node part (harness.cpp:353-357)
     int diag;           // run loop: reduce the step's make_diag values (k_post cells, node update momentum)
     DiagScratch dsc;    // diagnostics block partials ([0] k_post, [1] node update) + k_diag_reduce scratch

@@ -558,6 +558,7 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     const int nx = d.nx, ny = d.ny;
     const Rng rn = d.r_lagn;
     const int i0 = rn.i0 + blockIdx.x * LTX, j0 = rn.j0 + blockIdx.y * LTY;
+    if (d.lag_sel && (in(d.lag_inner, i0, j0) != (d.lag_sel == 1))) return;
     const double dt = step_dt(d.ctl);
     const double cv = d.cv;
     // ---- cells [i0-1, i0+LTX] x [j0-1, j0+LTY]: Q^n and predict
@@ -3622,6 +3623,153 @@ void launch_step(const Dev& dd, int fused_start, cudaStream_t s) {
     launch_remap_core(d, s);
     launch_post(d, 1, s);
     launch_tail(d, fused_start, s);
+}
+
+// ---- block mode: the step split around the halo exchange ----------------------
+// head(1): the step start (dt from the all-reduced wave speed) and the fused
+// Lagrange tiles that read owned data only; head(2): the remaining tiles,
+// launched once the halo has arrived; rest: everything after the Lagrange
+// kernel (captured as a CUDA graph per State parity)
+void launch_step_block_head(const Dev& dd, int part, cudaStream_t s) {
+    Dev d = dd;
+    d.scan_nodes = 1;
+    d.diag = 1;
+    d.lag_sel = part;
+    if (part == 1) { k_step_start<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy); ++g_launches; }
+    const dim3 g = tiles_of(d.r_lagn, LTX, H2D_FTY), b(LTX * H2D_FTY);
+    if (d.nmat == 3)
+        { k_lag_fused<3><<<g, b, 0, s>>>(d); ++g_launches; }
+    else if (d.nmat == 2)
+        { k_lag_fused<2><<<g, b, 0, s>>>(d); ++g_launches; }
+    else
+        { k_lag_fused<1><<<g, b, 0, s>>>(d); ++g_launches; }
+}
+// HalfStepState::x_half (lagrange.cpp:87-93): node_pos(i, j) + (0.5 dt) u over
+// every stored node, ghosts included
+__global__ void k_xhalf(Dev d, double* xh, double* yh) {
+    const double dt = step_dt(d.ctl);
+    const double h = 0.5 * dt;
+    int i, j;
+    tid2(i, j, d.win_n.i0, d.win_n.j0);
+    if (!in(d.win_n, i, j)) return;
+    const int n = ix(d, i, j);
+    xh[n] = (d.x0 + i * d.dx) + h * d.ux[n];
+    yh[n] = (d.y0 + j * d.dy) + h * d.uy[n];
+}
+void launch_xhalf(const Dev& d, double* xh, double* yh, cudaStream_t s) {
+    k_xhalf<<<grid_of(d.win_n), blk2(), 0, s>>>(d, xh, yh);
+    ++g_launches;
+}
+
+int lag_tile_w() { return LTX; }
+int lag_tile_h() { return H2D_FTY; }
+void launch_step_block_rest(const Dev& dd, cudaStream_t s) {
+    Dev d = dd;
+    d.scan_nodes = 1;
+    d.diag = 1;
+    launch_lag_ghosts(d, s);
+    launch_remap_core(d, s);
+    launch_post(d, 1, s);
+    launch_tail(d, 0, s);
+}
+
+// the per-step scalars of a block, combined across blocks by ONE max-reduction
+// of four 64-bit words: the next wave-speed maximum (a non-negative double's
+// bits order as integers), the complements of the first cfl_dt error key and
+// of the first error key (max of ~key = ~min of key), and done
+__global__ void k_red_pack(const Ctl* c, unsigned long long* red) {
+    red[0] = c->next_wmax_bits;
+    red[1] = ~c->next_err_key;
+    red[2] = ~c->err_key;
+    red[3] = (unsigned long long)c->done;
+}
+// back into the control block: the global values the single domain would
+// hold; when the first error precedes the commit, a block that committed its
+// step undoes it (the decomposed State stays at the last common step)
+__global__ void k_red_apply(Ctl* c, const unsigned long long* red) {
+    c->next_wmax_bits = red[0];
+    c->next_err_key = ~red[1];
+    const unsigned long long e = ~red[2];
+    c->err_key = e;
+    if (e != kNoErr && (int)(e >> 58) < PH_NAN_CELL && c->committed) {
+        c->time = c->prev_time;
+        c->step -= 1;
+        c->cur ^= 1;
+        if (c->counted) {
+            c->steps_done -= 1;
+            c->floor_count -= c->step_floor;
+            c->k_clip_count -= c->step_clip;
+            c->mass_fix_count -= c->step_fix;
+            c->max_k_violation = c->prev_max_k_violation;
+        }
+        c->committed = 0;
+        c->counted = 0;
+    }
+}
+// in-process blocks: the max over every block's four words, written back to all
+__global__ void k_red_local(unsigned long long* const* red, int n) {
+    const int w = threadIdx.x;
+    if (w >= 4) return;
+    unsigned long long m = 0;
+    for (int b = 0; b < n; ++b) m = red[b][w] > m ? red[b][w] : m;
+    for (int b = 0; b < n; ++b) red[b][w] = m;
+}
+void launch_red_pack(const Ctl* c, unsigned long long* red, cudaStream_t s) {
+    k_red_pack<<<1, 1, 0, s>>>(c, red);
+    ++g_launches;
+}
+void launch_red_apply(Ctl* c, const unsigned long long* red, cudaStream_t s) {
+    k_red_apply<<<1, 1, 0, s>>>(c, red);
+    ++g_launches;
+}
+void launch_red_local(unsigned long long* const* red, int n, cudaStream_t s) {
+    k_red_local<<<1, 32, 0, s>>>(red, n);
+    ++g_launches;
+}
+
+// every halo rectangle of a block in ONE launch: segment q covers the
+// rectangles rc[q] (cell planes) and rn[q] (node planes), laid out from
+// off[q] in the buffer (k_rect_xfer's order inside a segment)
+__global__ void k_halo_multi(Dev d, FieldList cells, FieldList nodes, HaloPlan plan, double* buf, int to_buf) {
+    const long long total = plan.off[plan.n];
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        int q = 0;
+        while (t >= plan.off[q + 1]) ++q;
+        const Rng rc = plan.rc[q], rn = plan.rn[q];
+        const long long u = t - plan.off[q];
+        const int wc = rc.i1 - rc.i0, wn = rn.i1 - rn.i0;
+        const long long ac = (long long)wc * (rc.j1 - rc.j0), an = (long long)wn * (rn.j1 - rn.j0);
+        double* pl;
+        int i, j;
+        if (u < ac * cells.n) {
+            const int f = (int)(u / ac);
+            const long long r = u - f * ac;
+            pl = cells.f[f];
+            i = rc.i0 + (int)(r % wc);
+            j = rc.j0 + (int)(r / wc);
+        } else {
+            const long long v = u - ac * cells.n;
+            const int f = (int)(v / an);
+            const long long r = v - f * an;
+            pl = nodes.f[f];
+            i = rn.i0 + (int)(r % wn);
+            j = rn.j0 + (int)(r / wn);
+        }
+        if (to_buf)
+            buf[t] = pl[ix(d, i, j)];
+        else
+            pl[ix(d, i, j)] = buf[t];
+    }
+}
+void launch_halo_multi(const Dev& d, const FieldList& cells, const FieldList& nodes, const HaloPlan& plan,
+                       double* buf, int to_buf, cudaStream_t s) {
+    const long long n = plan.off[plan.n];
+    if (n <= 0) return;
+    unsigned nb = nblk(n, 256);
+    if (nb > 148u * 8u) nb = 148u * 8u;
+    k_halo_multi<<<nb, 256, 0, s>>>(d, cells, nodes, plan, buf, to_buf);
+    ++g_launches;
 }
 
 // One AD directional pass (remap.cpp:469-589) writing into dout's planes.

@@ -27,6 +27,13 @@ struct AdIO {
     int axis_x;     // 1: X pass, 0: Y pass
 };
 
+// the halo rectangles of one block, one segment per neighbour direction
+struct HaloPlan {
+    int n;
+    Rng rc[8], rn[8];
+    long long off[9];
+};
+
 long long launch_count();
 int tma_node_box_w();  // remap-tile TMA box sizes (doubles)
 int tma_node_box_h();
@@ -70,6 +77,17 @@ void launch_commit_finish(const Dev& d, cudaStream_t s);               // wave s
 void launch_commit(Ctl* c, int advance, cudaStream_t s);
 void launch_normals_api(const Dev& d, cudaStream_t s);
 void launch_rollback(Ctl* c, cudaStream_t s);
+// block-mode data plane (h2d_blocks_run)
+void launch_step_block_head(const Dev& d, int part, cudaStream_t s);  // part 1: start + inner tiles, 2: edge tiles
+void launch_step_block_rest(const Dev& d, cudaStream_t s);
+void launch_xhalf(const Dev& d, double* xh, double* yh, cudaStream_t s);  // HalfStepState::x_half
+int lag_tile_w();  // the fused Lagrange kernel's node tile
+int lag_tile_h();
+void launch_red_pack(const Ctl* c, unsigned long long* red, cudaStream_t s);
+void launch_red_apply(Ctl* c, const unsigned long long* red, cudaStream_t s);
+void launch_red_local(unsigned long long* const* red, int n, cudaStream_t s);
+void launch_halo_multi(const Dev& d, const FieldList& cells, const FieldList& nodes, const HaloPlan& plan,
+                       double* buf, int to_buf, cudaStream_t s);
 void launch_rect_xfer(const Dev& d, const FieldList& cells, const FieldList& nodes, Rng rc, Rng rn, double* buf,
                       int to_buf, cudaStream_t s);
 void launch_global_xfer(const Dev& d, double* buf, Rng r, double* px, double* py, int vec, int to_block,

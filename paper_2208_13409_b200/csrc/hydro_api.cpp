@@ -339,8 +339,10 @@ HalfStepState predict(const State& s, const MaterialSet& mats, double dt, const 
     }
     r.p_mix_half = Field<double>(nx, ny);
     r.q = Field<double>(nx, ny);
+    r.x_half = Field<Vec2>(nx + 1, ny + 1);
     h2d_half out;
     std::memset(&out, 0, sizeof out);
+    out.x_half = pv(r.x_half);
     out.u_half = pv(r.u_half);
     out.vol_half = p(r.vol_half);
     for (int a = 0; a < s.nmat; ++a) {
@@ -351,10 +353,6 @@ HalfStepState predict(const State& s, const MaterialSet& mats, double dt, const 
     out.q = p(r.q);
     check(h, h2d_predict(h, dt, &out));
     r.floor_count = out.floor_count;
-    // x_half: node positions at the half step, output only (lagrange.cpp:88-93)
-    r.x_half = Field<Vec2>(nx + 1, ny + 1);
-    for (int j = -kGhost; j <= ny + kGhost; ++j)
-        for (int i = -kGhost; i <= nx + kGhost; ++i) r.x_half(i, j) = m.node_pos(i, j) + 0.5 * dt * s.u(i, j);
     return r;
 }
 

@@ -97,6 +97,11 @@ _SIGS = {
     "halo_pack": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p], C.c_int),
     "halo_unpack": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p], C.c_int),
     "block_result": ([C.c_void_p, C.POINTER(RunArgs)], C.c_int),
+    "nccl_unique_id": ([C.c_char_p], C.c_int),
+    "comm_nccl": ([C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+    "comm_local": ([C.POINTER(C.c_void_p), C.c_int, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "comm_destroy": ([C.c_void_p], None),
+    "blocks_run": ([C.c_void_p, C.c_int, C.c_double, C.c_double, C.POINTER(C.c_int)], C.c_int),
 }
 
 
@@ -185,6 +190,51 @@ class BlockSolver:
             err = errors.from_record(rec)
         a.block_series = ser[:a.steps_done].copy() if ser is not None else None
         return a, dts[:a.steps_done], err
+
+
+class DeviceComm:
+    """The library's block data plane (h2d_comm + h2d_blocks_run): the run
+    loop of a decomposition with the per-step all-reduce and halo exchange
+    enqueued on the device (NCCL across processes, or every block of the
+    decomposition in this process on one device)."""
+
+    def __init__(self, blocks: Sequence[BlockSolver], px: int, py: int, nccl_id: Optional[bytes] = None,
+                 rank: int = 0):
+        self.blocks = list(blocks)
+        self.lib = self.blocks[0].lib
+        self._h = C.c_void_p()
+        if nccl_id is None:
+            arr = (C.c_void_p * len(self.blocks))(*[b._h.value for b in self.blocks])
+            rc = self.lib.fn["comm_local"](arr, px, py, C.byref(self._h))
+        else:
+            assert len(self.blocks) == 1
+            rc = self.lib.fn["comm_nccl"](nccl_id, px, py, rank, self.blocks[0]._h, C.byref(self._h))
+        if rc:
+            self.blocks[0]._check(rc)
+            raise errors.from_code(rc, f"h2d_comm creation failed ({rc})")
+
+    @staticmethod
+    def unique_id(lib: Library) -> bytes:
+        bind(lib)
+        buf = C.create_string_buffer(128)
+        rc = lib.fn["nccl_unique_id"](buf)
+        if rc:
+            raise errors.from_code(rc, "h2d_nccl_unique_id failed")
+        return buf.raw
+
+    def run(self, max_steps: int, t_end: float, cfl: float) -> int:
+        done = C.c_int(0)
+        rc = self.lib.fn["blocks_run"](self._h, max_steps, t_end, cfl, C.byref(done))
+        if rc:
+            self.blocks[0]._check(rc)
+        return done.value
+
+    def close(self):
+        if self._h:
+            self.lib.fn["comm_destroy"](self._h)
+            self._h = C.c_void_p()
+
+    __del__ = close
 
 
 _SUMS = ("mass", "mass_mat", "momentum_x", "momentum_y", "internal_energy")

@@ -80,3 +80,107 @@ def test_halo_plan_matches_library():
                 rc, rn = multi.halo_rects(sp, 64, 64, dx, dy, bool(pack))
                 want = ((rc[1] - rc[0]) * (rc[3] - rc[2]) * nc + (rn[1] - rn[0]) * (rn[3] - rn[2]) * nn) * 8
                 assert b.halo_bytes(dx, dy, pack) == want
+
+
+# ---- the library's data plane (h2d_comm + h2d_blocks_run) -------------------
+def _blocks_device(case, steps, px, py):
+    """The whole decomposed run loop inside the library: per step every
+    block's graph, one max all-reduce of the four control words and one
+    halo exchange enqueued on the device (in-process transport: every
+    block on this GPU), the host polling every 16 steps."""
+    lib = helpers.product_lib()
+    init = helpers.prepared(lib, case.cfg, case.paint()).download()
+    specs = multi.decompose(case.cfg.mesh.nx, case.cfg.mesh.ny, px, py)
+    blocks = [multi.BlockSolver(lib, case.cfg, sp) for sp in specs]
+    for b in blocks:
+        b.upload(init)
+    comm = multi.DeviceComm(blocks, px, py)
+    comm.run(steps, 1e30, case.cfl)
+    comm.close()
+    out = HostState.empty(case.cfg.mesh.nx, case.cfg.mesh.ny, case.cfg.nmat)
+    results = []
+    for b in blocks:
+        b.download_into(out)
+        results.append(b.result(steps))
+    return out, results
+
+
+@pytest.mark.parametrize("px,py", [(2, 1), (1, 2), (2, 2), (4, 2)])
+@pytest.mark.parametrize("which", ["riemann", "triple", "bubble", "voronoi3"])
+def test_device_data_plane_bitwise_equal_single_domain(which, px, py):
+    case = {"riemann": cases.riemann2d(64), "triple": cases.triple_point(96, 48),
+            "bubble": cases.shock_bubble(64), "voronoi3": cases.voronoi3(128)}[which]
+    steps = 40
+    ref, r, err = _single(case, steps)
+    got, results = _blocks_device(case, steps, px, py)
+    assert err is None
+    for a, dts, e in results:
+        assert e is None
+        assert a.steps_done == r.steps_done
+        assert np.array_equal(dts, r.dts)
+    assert sum(a.diag.k_clip_count for a, _, _ in results) == r.diag["k_clip_count"]
+    assert sum(a.diag.mass_fix_count for a, _, _ in results) == r.diag["mass_fix_count"]
+    assert sum(a.floor_count for a, _, _ in results) == r.floor_count
+    assert helpers.bitwise_diff(got, ref, helpers.STATE_FIELDS) == []
+    assert (got.step, got.time) == (ref.step, ref.time)
+
+
+def test_device_data_plane_reproduces_the_reference_abort():
+    """the device-side combine rolls back the blocks that committed when the
+    first error (any block) precedes the commit: same error, same State."""
+    case = cases.triple_point(32, 16)
+    ref, r, err = _single(case, 1000)
+    assert err is not None
+    got, results = _blocks_device(case, 1000, 2, 2)
+    for a, dts, e in results:
+        assert (type(e).__name__, e.what, e.i, e.j) == err[:4]
+        assert a.steps_done == r.steps_done
+    assert helpers.bitwise_diff(got, ref, helpers.STATE_FIELDS) == []
+
+
+def test_device_data_plane_until_t_end():
+    """a run to t_end (max_steps = 0): the last dt is clipped to t_end and
+    every block stops at the same step."""
+    case = cases.sedov(64)
+    lib = helpers.product_lib()
+    s = helpers.prepared(lib, case.cfg, case.paint())
+    t_end = 0.002
+    r = s.run(0, t_end=t_end, cfl=case.cfl)
+    ref = s.download()
+    init = helpers.prepared(lib, case.cfg, case.paint()).download()
+    specs = multi.decompose(64, 64, 2, 2)
+    blocks = [multi.BlockSolver(lib, case.cfg, sp) for sp in specs]
+    for b in blocks:
+        b.upload(init)
+    comm = multi.DeviceComm(blocks, 2, 2)
+    comm.run(0, t_end, case.cfl)
+    comm.close()
+    got = HostState.empty(64, 64, 1)
+    for b in blocks:
+        b.download_into(got)
+        a, dts, e = b.result(r.steps_done + 1)
+        assert e is None and np.array_equal(dts, r.dts)
+    assert helpers.bitwise_diff(got, ref, helpers.STATE_FIELDS, 1) == []
+
+
+def test_nccl_transport_single_rank():
+    """The NCCL transport with a one-rank communicator owned by the library
+    (1 x 1 decomposition: the all-reduce runs, no neighbours): equal to the
+    single domain. Two or more ranks need two or more GPUs (bench.py --gpus)."""
+    case = cases.triple_point(64, 32)
+    steps = 30
+    ref, r, err = _single(case, steps)
+    lib = helpers.product_lib()
+    init = helpers.prepared(lib, case.cfg, case.paint()).download()
+    spec = multi.decompose(64, 32, 1, 1)[0]
+    blk = multi.BlockSolver(lib, case.cfg, spec)
+    blk.upload(init)
+    uid = multi.DeviceComm.unique_id(lib)
+    comm = multi.DeviceComm([blk], 1, 1, nccl_id=uid, rank=0)
+    comm.run(steps, 1e30, case.cfl)
+    comm.close()
+    got = HostState.empty(64, 32, 2)
+    blk.download_into(got)
+    a, dts, e = blk.result(steps)
+    assert e is None and np.array_equal(dts, r.dts)
+    assert helpers.bitwise_diff(got, ref, helpers.STATE_FIELDS) == []
