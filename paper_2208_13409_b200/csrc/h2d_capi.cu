@@ -618,10 +618,15 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
         return H2D_ERR_INVALID;
     }
     const int nm = c->nmat;
-    // plane count: 2 x State (6 + 3 nm) + Lagrange (7 + 2 nm) + remap scratch
-    const size_t planes = 2 * (9 + 3 * nm) + (7 + 2 * nm) + (25 + 15 * nm) + 8;
+    // fp64 planes, exactly as carved below: 2 x State (3 nm + 9; one material
+    // shares its normals between the parities), the LagrangeResult (7) and
+    // per material p_half, e_lag, me, sliver m / m*e (5 nm), the remap scratch
+    // (13), the AoS staging (2). 1 / 2 / 3 materials: 49 / 62 / 73 planes,
+    // i.e. with the 10 byte planes ~402 / 506 / 594 B per cell: 16384^2 x 3
+    // materials (configuration 5) fits one B200
+    const size_t planes = 2 * (3 * (size_t)nm + 9) - (nm == 1 ? 2 : 0) + 7 + 5 * (size_t)nm + 13 + 2;
     const size_t bytes_planes = planes * ((c->fsz * sizeof(double) + 255) & ~size_t(255));
-    const size_t bytes_small = 12 * ((c->fsz + 255) & ~size_t(255)) + ((size_t)c->R * 4 + 256);
+    const size_t bytes_small = 10 * ((c->fsz + 255) & ~size_t(255)) + ((size_t)c->R * 4 + 256);
     c->arena_bytes = bytes_planes + bytes_small + 4096;
     if (cudaMalloc(&c->arena, c->arena_bytes) != cudaSuccess) return fail(H2D_ERR_NOMEM);
     cudaMemsetAsync(c->arena, 0, c->arena_bytes, c->st);

@@ -55,6 +55,8 @@ __global__ void k_scalar(int op, int n, const double* __restrict__ in, double* _
     if (r >= n) return;
     const double* x = in + (size_t)r * IN;
     double* o = out + (size_t)r * OUT;
+#pragma unroll
+    for (int q = 0; q < OUT; ++q) o[q] = 0.0;
     bool bad = false;
     switch (op) {
     case H2D_SC_VAN_LEER:
