@@ -54,8 +54,13 @@ PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0
 
 
-def workload(name):
+def workload(name, full=True):
+    """The bench workloads (BASELINE.json configs[0..4]); c5 is the whole
+    16384^2 three-material mesh (about 594 B per cell on the device: it fits
+    one B200); full=False gives one GPU's 4096 x 8192 block of it."""
     from paper_2208_13409_b200 import cases
+    if name == "c5" and full:
+        return cases.voronoi3(16384)
     if name == "c1":
         return cases.riemann2d(256)
     if name == "c2":
@@ -199,6 +204,16 @@ def ncu_traffic(workload, kernel):
         return None, None
 
 
+def cpu_sample(name, case):
+    """The case the CPU legs time: the workload itself, except c5, whose
+    16384^2 three-material State does not fit a host process of the C
+    restatement: its lower-left 2048^2 block (same cells, same sites)."""
+    if name == "c5" and case.cfg.mesh.nx > 4096:
+        from paper_2208_13409_b200 import cases
+        return cases.voronoi3(2048, 2048, n_full=case.cfg.mesh.nx), "lower-left 2048^2 block of the mesh, "
+    return case, ""
+
+
 def time_cpu(case, warm, steps, remap_kind=None):
     """Wall-clock the CPU implementation on `steps` steps after `warm`."""
     from paper_2208_13409_b200 import abi
@@ -290,11 +305,17 @@ def run_product(args, world, rank, local, pg):
     #     State: upload, K device steps, download, all inside the timed region;
     # (2) e2e_per_step_api: the value API every step (upload State -> one step
     #     -> download State), i.e. a caller that keeps its State on the host.
+    s.close()  # one context at a time (a 16384^2 three-material context takes ~161 GB)
     se = abi.Solver(lib, case.cfg, local)
     se.init_from(painted)
     se.run(1, cfl=case.cfl, log_dt=False, kind=kind)  # one-time setup (graph capture) outside the timed region
     se.init_from(painted)
-    host = pinned_state(case.cfg.mesh.nx, case.cfg.mesh.ny, nmat, case.cfg.mesh.dx * case.cfg.mesh.dy)
+    pinned = cells <= (1 << 27)  # a 16384^2 three-material State (39 GB) stays in pageable memory
+    if pinned:
+        host = pinned_state(case.cfg.mesh.nx, case.cfg.mesh.ny, nmat, case.cfg.mesh.dx * case.cfg.mesh.dy)
+    else:
+        from paper_2208_13409_b200.abi import HostState
+        host = HostState.empty(case.cfg.mesh.nx, case.cfg.mesh.ny, nmat, case.cfg.mesh.dx * case.cfg.mesh.dy)
     st0 = se.download()
     fields = ("m", "e", "k", "vol", "m_mix", "e_mix", "rho_mix", "p_mix", "iface_normal", "u")
     for f in fields:
@@ -369,72 +390,93 @@ def run_product(args, world, rank, local, pg):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # a bounded sample: about 3e7 cell-updates (10-30 s of one core)
-        v, ckind, n, secs = time_cpu(case, 0, min(args.cpu_steps, max(1, int(3e7 // case.cells))), kind)
+        sc, where = cpu_sample(args.workload, case)
+        v, ckind, n, secs = time_cpu(sc, 0, min(args.cpu_steps, max(1, int(3e7 // sc.cells))), kind)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": ckind, "cpu": cpu_model(),
                                 "nproc": os.cpu_count(),
-                                "sample": f"{case.name}: first {n} steps from t=0, single thread, {secs:.1f} s"}
+                                "sample": f"{case.name}: {where}first {n} steps from t=0, single thread, "
+                                          f"{secs:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
 
 def run_product_multi(args, world, rank, local, pg):
-    """N > 1: 2D block decomposition, one block per rank (NCCL halo exchange
-    + scalar all-reduce per step); weak scaling: each GPU keeps a 1024^2
-    Sedov block (the global mesh grows with N)."""
+    """N > 1: the workload's global mesh split into px x py blocks (strong
+    scaling: the same problem as N = 1), one block per rank. Each rank paints
+    and initialises only its own window (h2d_block_init_window); the whole
+    run loop, with ONE max all-reduce of four control words and ONE halo
+    exchange (8 neighbours, corners included) per step, runs inside the
+    library over an NCCL communicator it owns (h2d_comm_nccl +
+    h2d_blocks_run: device-side combine, exchange overlapped with the
+    Lagrange tiles on owned data, host polling every 16 steps)."""
     import torch
     import paper_2208_13409_b200 as pkg
-    from paper_2208_13409_b200 import cases, multi
+    from paper_2208_13409_b200 import multi
 
-    px, py = multi.grid_shape(world, 1, 1)
-    if args.workload != "c2":
-        raise SystemExit("multi-GPU bench runs the config-2 workload")
-    case = cases.sedov_weak(px, py)
+    case = workload(args.workload, full=True)
+    nx, ny, nmat = case.cfg.mesh.nx, case.cfg.mesh.ny, case.cfg.nmat
+    px, py = multi.grid_shape(world, nx, ny)
     lib = pkg.product_library()
-    painted = case.paint()
-    init = pkg.Solver(lib, case.cfg, local)
-    init.init_from(painted)
-    g0 = init.download()
-    init.close()
-    spec = multi.decompose(case.cfg.mesh.nx, case.cfg.mesh.ny, px, py)[rank]
+    spec = multi.decompose(nx, ny, px, py)[rank]
     blk = multi.BlockSolver(lib, case.cfg, spec, local)
-    blk.upload(g0)
-    tr = multi.DistTransport(blk, px, py, torch.device("cuda", local))
-    multi.run_blocks([blk], tr, args.warmup, 1e30, case.cfl)
-    clocks = Clocks(local)
+    t_paint = time.perf_counter()
+    win = case.paint(blk.window())
+    t_paint = time.perf_counter() - t_paint
+    # the NCCL id travels once through torch.distributed (plumbing)
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(multi.DeviceComm.unique_id(lib)), dtype=torch.uint8))
+    if pg is not None:
+        pg.broadcast(uid, 0)
+    comm = multi.DeviceComm([blk], px, py, nccl_id=bytes(uid.cpu().numpy().tobytes()), rank=rank)
+    # e2e (the timed region includes the host -> device upload of this rank's
+    # painted window, the run and the download of the owned State)
     barrier(pg)
+    t0 = time.perf_counter()
+    blk.init_window(win)
+    comm.run(args.warmup, 1e30, case.cfl)
+    warm_ms = comm.device_ms
+    clocks = Clocks(local)
     clocks.start()
     launches0 = lib.fn["launch_count"]()
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record()
-    done = multi.run_blocks([blk], tr, args.warmup + args.steps, 1e30, case.cfl)
-    t1.record()
-    torch.cuda.synchronize()
+    done = comm.run(args.warmup + args.steps, 1e30, case.cfl) - args.warmup
+    dev_ms = comm.device_ms
     launches = lib.fn["launch_count"]() - launches0
     clk = clocks.stop()
+    from paper_2208_13409_b200.abi import HostState
+    own = HostState.empty(nx, ny, nmat) if nx * ny <= (1 << 26) else None
+    if own is not None:
+        blk.download_into(own)
+    e2e_s = max_over_ranks(pg, time.perf_counter() - t0)
     barrier(pg)
-    total_s = max_over_ranks(pg, t0.elapsed_time(t1) / 1e3)
+    total_s = max_over_ranks(pg, dev_ms / 1e3)
     cells = case.cells
     value = cells * done / total_s
     ms_step = total_s * 1e3 / max(done, 1)
     peak, peak_kind = hbm_peak()
     per_gpu = spec.bnx * spec.bny
-    achieved = B_MIN[1] * per_gpu / (ms_step / 1e3) / 1e9
-    halo = sum(blk.halo_bytes(dx, dy, 1) for dx, dy in tr.send)
+    achieved = B_MIN[nmat] * per_gpu / (ms_step / 1e3) / 1e9
+    halo_doubles = sum(blk.halo_bytes(dx, dy, 1) for dx, dy in multi.DIRS
+                       if spec.neighbour(px, py, dx, dy) is not None) // 8
+    comm.close()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": done, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (init_case-equivalent painter)",
-        "config": {"workload": case.name, "cells": cells, "cells_per_gpu": per_gpu, "materials": 1,
-                   "parallelism": f"2D blocks {px}x{py}, halo {multi.HALO}, 1 NCCL halo exchange (8 neighbours) + "
-                                  f"1 scalar all-reduce per step", "halo_bytes_sent_per_step_rank0": halo,
-                   "l2": "per-GPU working set >> L2"},
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (init_case-equivalent painter, seeded; each rank paints its own window)",
+        "config": config_of(case, args.remap, world,
+                            parallelism=f"2D blocks {px}x{py}, halo {blk.halo}; per step 1 NCCL max all-reduce "
+                                        f"(4 words) + 1 grouped NCCL halo exchange, in the library"),
+        "cells_per_gpu": per_gpu, "halo_doubles_sent_rank0": halo_doubles, "paint_s_rank0": t_paint,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_kind,
-                     "basis": f"per GPU: {B_MIN[1]} B/cell-step x {per_gpu} cells"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 24, "d2h_bytes_per_step": 32,
-                "path": "device-resident block run loop; per step the wave-speed / error scalars go "
-                        "device->host->all-reduce->device"},
+                     "basis": f"per GPU: {B_MIN[nmat]} B/cell-step x {per_gpu} owned cells / step time"},
+        "e2e": {"value": cells * (args.warmup + done) / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": (win.m[:nmat].nbytes * 3 + win.u.nbytes) / (args.warmup + done),
+                "d2h_bytes_per_step": (sum(getattr(own, f).nbytes for f in ("m", "e", "k", "vol", "m_mix", "e_mix",
+                                                                        "rho_mix", "p_mix", "iface_normal", "u"))
+                                       / (args.warmup + done)) if own is not None else 0,
+                "path": "h2d_block_init_window (painted window up) + h2d_blocks_run (warm-up + timed steps) + "
+                        "h2d_block_download (owned State down), wall clock, max over ranks"},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
@@ -447,13 +489,14 @@ def run_reference(args, world, rank, pg):
         return
     from paper_2208_13409_b200 import abi
     case = workload(args.workload)
+    sc, where = cpu_sample(args.workload, case)
     # a bounded sample: about 1.2e8 cell-updates (~1 min of one core), at
     # least one step; warm-up steps only where they fit the same budget
-    budget = max(1, int(1.2e8 // case.cells))
+    budget = max(1, int(1.2e8 // sc.cells))
     steps = max(1, min(args.steps, budget))
     warm = min(args.warmup, budget - steps)
     rk = {"ad": abi.REMAP_AD, "direct": abi.REMAP_DIRECT}.get(args.remap, abi.REMAP_DIRECTCF)
-    v, ckind, n, secs = time_cpu(case, warm, steps, rk)
+    v, ckind, n, secs = time_cpu(sc, warm, steps, rk)
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": warm,
         "ms_per_step": secs * 1e3 / max(n, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -461,8 +504,8 @@ def run_reference(args, world, rank, pg):
         "config": config_of(case, args.remap, 1),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": ckind, "cpu": cpu_model(),
                          "nproc": os.cpu_count(),
-                         "sample": f"{case.name}: steps {warm + 1}..{warm + n} of the workload, single thread "
-                                   f"(the reference has no threading), {secs:.1f} s"},
+                         "sample": f"{case.name}: {where}steps {warm + 1}..{warm + n} of the workload, single "
+                                   f"thread (the reference has no threading), {secs:.1f} s"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -481,12 +524,14 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--blocks", action="store_true",
+                    help="run the block-decomposition data plane (NCCL, per-rank painting) even on one GPU")
     args = ap.parse_args()
     world, rank, local, pg = dist_setup(args.gpus)
     try:
         if args.impl == "reference":
             run_reference(args, world, rank, pg)
-        elif world > 1:
+        elif world > 1 or args.blocks:
             run_product_multi(args, world, rank, local, pg)
         else:
             run_product(args, world, rank, local, pg)

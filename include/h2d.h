@@ -277,6 +277,17 @@ int h2d_create_block(const h2d_config* cfg, const h2d_block* blk, int device, h2
 /* window upload / owned-region download in the GLOBAL reference layout */
 int h2d_block_upload(h2d_ctx* ctx, const h2d_state* global_state);
 int h2d_block_download(h2d_ctx* ctx, h2d_state* global_state);
+/* The block's initial State from a painted WINDOW of the global mesh (each
+ * rank paints only its own window; no global host State): the arrays of `win`
+ * hold the cells [wi0, wi0 + wnx) x [wj0, wj0 + wny) (wnx * wny doubles,
+ * row-major, no ghost layers) and the nodes [wi0, wi0 + wnx] x [wj0, wj0 + wny]
+ * ((wnx + 1) (wny + 1) Vec2); m, e, k per material and u are read. The window
+ * should cover the block's storage window clipped to the mesh. Then the
+ * init_case tail on the device (fill_ghosts at the global walls,
+ * sync_derived, update_interface_normals; harness.cpp:286-288); the first
+ * exchange of h2d_blocks_run makes the halo exact. */
+int h2d_block_init_window(h2d_ctx* ctx, const h2d_state* win, int wi0, int wj0, int wnx, int wny, int step,
+                          double time);
 /* run control: begin (computes the owned wave speed of the initial State),
  * one graph-launched step, the scalars to combine across blocks
  * {next wave-speed max bits (MAX), next cfl error key (MIN), error key (MIN),
@@ -310,7 +321,9 @@ int h2d_nccl_unique_id(unsigned char id[128]);
 int h2d_comm_nccl(const unsigned char id[128], int px, int py, int rank, h2d_ctx* block, h2d_comm** out);
 int h2d_comm_local(h2d_ctx* const* blocks, int px, int py, h2d_comm** out);
 void h2d_comm_destroy(h2d_comm* comm);
-int h2d_blocks_run(h2d_comm* comm, int max_steps, double t_end, double cfl, int* steps_done);
+/* device_ms (nullable): CUDA-event time from the first step's start to the
+ * last step's exchange (the slowest block of this process) */
+int h2d_blocks_run(h2d_comm* comm, int max_steps, double t_end, double cfl, int* steps_done, float* device_ms);
 
 /* ---- benchmark support (no reference counterpart) ---------------------- */
 /* Kernels launched by this library in the calling process so far. */

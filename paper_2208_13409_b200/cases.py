@@ -21,8 +21,8 @@ from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .abi import (BC_WALL, CORNER_LINEARDIAG, EOS_PERFECT, EOS_STIFFENED, Config, HostState, GHOST,
-                  make_config)
+from .abi import (BC_WALL, CORNER_LINEARDIAG, EOS_PERFECT, EOS_STIFFENED, GHOST, MAX_MAT, Config, HostState,
+                  StateView, _ptr, make_config)
 
 K_PURE_TOL = 1e-10  # state.hpp:17
 
@@ -135,16 +135,62 @@ def _coverage(r: Region, lox, loy, hix, hiy, dx, dy, mask) -> np.ndarray:
     return out
 
 
-def paint(cfg: Config, regions: Sequence[Region]) -> HostState:
+@dataclass
+class WindowState:
+    """A painted window of the global mesh (per-rank painting for the block
+    decomposition, h2d_block_init_window): cells [wi0, wi0 + wnx) x
+    [wj0, wj0 + wny), nodes [wi0, wi0 + wnx] x [wj0, wj0 + wny], no ghost
+    layers; m, e, k (MAX_MAT, wny, wnx), u (wny + 1, wnx + 1, 2)."""
+    wi0: int
+    wj0: int
+    wnx: int
+    wny: int
+    nmat: int
+    m: np.ndarray
+    e: np.ndarray
+    k: np.ndarray
+    u: np.ndarray
+
+    @classmethod
+    def empty(cls, wi0, wj0, wnx, wny, nmat):
+        z = np.zeros((MAX_MAT, wny, wnx))
+        return cls(wi0, wj0, wnx, wny, nmat, z.copy(), z.copy(), z.copy(), np.zeros((wny + 1, wnx + 1, 2)))
+
+    def view(self) -> StateView:
+        v = StateView()
+        for a in range(MAX_MAT):
+            v.m[a], v.e[a], v.k[a] = _ptr(self.m[a]), _ptr(self.e[a]), _ptr(self.k[a])
+        v.u = _ptr(self.u)
+        return v
+
+    def into(self, st: HostState):
+        """Copy into a global HostState's interior."""
+        g = GHOST
+        cs = (slice(g + self.wj0, g + self.wj0 + self.wny), slice(g + self.wi0, g + self.wi0 + self.wnx))
+        for a in range(self.nmat):
+            st.k[a][cs] = self.k[a]
+            st.m[a][cs] = self.m[a]
+            st.e[a][cs] = self.e[a]
+        st.u[g + self.wj0:g + self.wj0 + self.wny + 1, g + self.wi0:g + self.wi0 + self.wnx + 1] = self.u
+        return st
+
+
+def paint(cfg: Config, regions: Sequence[Region], window=None):
     """Interior of init_case (harness.cpp:226-284); ghosts/derived/normals are
-    completed on the solver by ``Solver.init_from``."""
+    completed on the solver by ``Solver.init_from``. With window = (wi0,
+    wj0, wnx, wny) only that window is painted (a WindowState, the same
+    per-cell arithmetic)."""
     m = cfg.mesh
-    nx, ny, dx, dy, x0, y0 = m.nx, m.ny, m.dx, m.dy, m.x0, m.y0
+    if window is None:
+        w = paint(cfg, regions, (0, 0, m.nx, m.ny))
+        return w.into(HostState.empty(m.nx, m.ny, cfg.nmat, m.dx * m.dy))
+    wi0, wj0, nx, ny = window
+    dx, dy, x0, y0 = m.dx, m.dy, m.x0, m.y0
     nmat = cfg.nmat
     eos = [(cfg.eos[a].kind, cfg.eos[a].gamma, cfg.eos[a].pi) for a in range(nmat)]
     cv = dx * dy
-    i = np.arange(nx, dtype=np.float64)[None, :]
-    j = np.arange(ny, dtype=np.float64)[:, None]
+    i = np.arange(wi0, wi0 + nx, dtype=np.float64)[None, :]
+    j = np.arange(wj0, wj0 + ny, dtype=np.float64)[:, None]
     lox, loy = x0 + i * dx, y0 + j * dy              # node_pos(i, j)
     hix, hiy = x0 + (i + 1) * dx, y0 + (j + 1) * dy  # node_pos(i+1, j+1)
     cenx, ceny = x0 + (i + 0.5) * dx, y0 + (j + 0.5) * dy
@@ -185,16 +231,15 @@ def paint(cfg: Config, regions: Sequence[Region]) -> HostState:
         for arr in (karr, marr, mearr):
             arr[b] = np.where(snap, arr[b] + arr[a], arr[b])
             arr[a] = np.where(snap, 0.0, arr[a])
-    st = HostState.empty(nx, ny, nmat, cv)
-    g = GHOST
+    st = WindowState.empty(wi0, wj0, nx, ny, nmat)
     for a in range(nmat):
-        st.k[a, g:g + ny, g:g + nx] = karr[a]
-        st.m[a, g:g + ny, g:g + nx] = marr[a]
+        st.k[a] = karr[a]
+        st.m[a] = marr[a]
         with np.errstate(divide="ignore", invalid="ignore"):
-            st.e[a, g:g + ny, g:g + nx] = np.where(marr[a] > 0.0, mearr[a] / marr[a], 0.0)
+            st.e[a] = np.where(marr[a] > 0.0, mearr[a] / marr[a], 0.0)
     # node velocities: last region containing the node (harness.cpp:277-284)
-    ni = np.arange(nx + 1, dtype=np.float64)[None, :]
-    nj = np.arange(ny + 1, dtype=np.float64)[:, None]
+    ni = np.arange(wi0, wi0 + nx + 1, dtype=np.float64)[None, :]
+    nj = np.arange(wj0, wj0 + ny + 1, dtype=np.float64)[:, None]
     px, py = x0 + ni * dx, y0 + nj * dy
     ux = np.zeros((ny + 1, nx + 1))
     uy = np.zeros((ny + 1, nx + 1))
@@ -202,8 +247,8 @@ def paint(cfg: Config, regions: Sequence[Region]) -> HostState:
         inside = np.nonzero(np.broadcast_to(_contains(reg, px, py), ux.shape))
         ux[inside] = reg.u[0]
         uy[inside] = reg.u[1]
-    st.u[g:g + ny + 1, g:g + nx + 1, 0] = ux
-    st.u[g:g + ny + 1, g:g + nx + 1, 1] = uy
+    st.u[..., 0] = ux
+    st.u[..., 1] = uy
     return st
 
 
@@ -220,8 +265,8 @@ class Case:
     def cells(self) -> int:
         return self.cfg.mesh.nx * self.cfg.mesh.ny
 
-    def paint(self) -> HostState:
-        return paint(self.cfg, self.regions)
+    def paint(self, window=None):
+        return paint(self.cfg, self.regions, window)
 
 
 def _mesh_cfg(nx, ny, lx, ly, eos, **kw) -> Config:
@@ -335,7 +380,7 @@ def _nearest(px: np.ndarray, py: np.ndarray, xy: np.ndarray, chunk: int = 1 << 1
     return out.reshape(px.shape)
 
 
-def paint_voronoi3(cfg: Config, sites, sub: int = 4) -> HostState:
+def paint_voronoi3(cfg: Config, sites, sub: int = 4, window=None):
     """Config 5's initial State (three materials, gammas 1.4 / 1.5 / 1.67).
     Node u: the nearest site's velocity.  Cells: a cell whose four corners
     have the same nearest site lies in that site's (convex) Voronoi region and
@@ -343,22 +388,24 @@ def paint_voronoi3(cfg: Config, sites, sub: int = 4) -> HostState:
     sampled on sub x sub points: k_a = n_a / sub^2, m_a = (sum of the
     samples' rho, in sample order) * (cv / sub^2), e_a = (sum of rho e) /
     (sum of rho)."""
-    xy, mat, rho, p, uv = sites
     m = cfg.mesh
-    nx, ny, dx, dy, x0, y0 = m.nx, m.ny, m.dx, m.dy, m.x0, m.y0
+    if window is None:
+        w = paint_voronoi3(cfg, sites, sub, (0, 0, m.nx, m.ny))
+        return w.into(HostState.empty(m.nx, m.ny, 3, m.dx * m.dy))
+    wi0, wj0, nx, ny = window
+    xy, mat, rho, p, uv = sites
+    dx, dy, x0, y0 = m.dx, m.dy, m.x0, m.y0
     gam = np.array([cfg.eos[a].gamma for a in range(3)])
     e_site = p / ((gam[mat] - 1.0) * rho)
     cv = dx * dy
-    st = HostState.empty(nx, ny, 3, cv)
-    g = GHOST
-    xn = x0 + np.arange(nx + 1) * dx
-    yn = y0 + np.arange(ny + 1) * dy
+    st = WindowState.empty(wi0, wj0, nx, ny, 3)
+    xn = x0 + np.arange(wi0, wi0 + nx + 1) * dx
+    yn = y0 + np.arange(wj0, wj0 + ny + 1) * dy
     lab = _nearest(np.broadcast_to(xn[None, :], (ny + 1, nx + 1)), np.broadcast_to(yn[:, None], (ny + 1, nx + 1)), xy)
-    st.u[g:g + ny + 1, g:g + nx + 1, 0] = uv[lab, 0]
-    st.u[g:g + ny + 1, g:g + nx + 1, 1] = uv[lab, 1]
+    st.u[..., 0] = uv[lab, 0]
+    st.u[..., 1] = uv[lab, 1]
     c00 = lab[:-1, :-1]
     pure = (c00 == lab[:-1, 1:]) & (c00 == lab[1:, :-1]) & (c00 == lab[1:, 1:])
-    I = (slice(g, g + ny), slice(g, g + nx))
     kk = np.zeros((3, ny, nx))
     mm = np.zeros((3, ny, nx))
     ee = np.zeros((3, ny, nx))
@@ -372,8 +419,8 @@ def paint_voronoi3(cfg: Config, sites, sub: int = 4) -> HostState:
     if jj.size:
         ns = sub * sub
         offs = (np.arange(sub) + 0.5) / sub
-        sx = x0 + (ii[:, None, None] + offs[None, None, :]) * dx  # [cell, q (row), s (col)]
-        sy = y0 + (jj[:, None, None] + offs[None, :, None]) * dy
+        sx = x0 + ((ii + wi0)[:, None, None] + offs[None, None, :]) * dx  # [cell, q (row), s (col)]
+        sy = y0 + ((jj + wj0)[:, None, None] + offs[None, :, None]) * dy
         sx, sy = np.broadcast_to(sx, (ii.size, sub, sub)), np.broadcast_to(sy, (ii.size, sub, sub))
         sl = _nearest(np.ascontiguousarray(sx), np.ascontiguousarray(sy), xy).reshape(ii.size, ns)
         smat, srho, sre = mat[sl], rho[sl], rho[sl] * e_site[sl]
@@ -389,9 +436,9 @@ def paint_voronoi3(cfg: Config, sites, sub: int = 4) -> HostState:
             mm[a][jj, ii] = rs * (cv / float(ns))
             ee[a][jj, ii] = np.where(cnt > 0, res / np.where(cnt > 0, rs, 1.0), 0.0)
     for a in range(3):
-        st.k[a][I] = kk[a]
-        st.m[a][I] = mm[a]
-        st.e[a][I] = ee[a]
+        st.k[a] = kk[a]
+        st.m[a] = mm[a]
+        st.e[a] = ee[a]
     return st
 
 
@@ -399,8 +446,8 @@ def paint_voronoi3(cfg: Config, sites, sub: int = 4) -> HostState:
 class VoronoiCase(Case):
     sites: tuple = ()
 
-    def paint(self) -> HostState:
-        return paint_voronoi3(self.cfg, self.sites)
+    def paint(self, window=None):
+        return paint_voronoi3(self.cfg, self.sites, window=window)
 
 
 def voronoi3(nx: int = 16384, ny: Optional[int] = None, n_full: Optional[int] = None, nsites: int = 64,

@@ -2509,6 +2509,9 @@ __global__ void k_normals(Dev d, int api) {
     int i, j;
     tid2(i, j, 0, 0);
     if (i >= d.nx || j >= d.ny) return;
+    // a decomposition block: only cells whose 3x3 stencil is stored (the
+    // outer halo ring is made exact by the first halo exchange)
+    if (!in(d.win_c, i - 1, j - 1) || !in(d.win_c, i + 1, j + 1)) return;
     const double* k0 = api ? d.k[0] : d.nk[0];
     const double* k1 = api ? d.k[1] : d.nk[1];
     double* nx_ = api ? const_cast<double*>(d.nrx) : d.nnrx;

@@ -97,11 +97,14 @@ _SIGS = {
     "halo_pack": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p], C.c_int),
     "halo_unpack": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p], C.c_int),
     "block_result": ([C.c_void_p, C.POINTER(RunArgs)], C.c_int),
+    "block_init_window": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double],
+                          C.c_int),
     "nccl_unique_id": ([C.c_char_p], C.c_int),
     "comm_nccl": ([C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
     "comm_local": ([C.POINTER(C.c_void_p), C.c_int, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "comm_destroy": ([C.c_void_p], None),
-    "blocks_run": ([C.c_void_p, C.c_int, C.c_double, C.c_double, C.POINTER(C.c_int)], C.c_int),
+    "blocks_run": ([C.c_void_p, C.c_int, C.c_double, C.c_double, C.POINTER(C.c_int), C.POINTER(C.c_float)],
+                   C.c_int),
 }
 
 
@@ -119,6 +122,7 @@ class BlockSolver:
     def __init__(self, lib: Library, cfg: Config, spec: BlockSpec, device: int = 0, halo: int = HALO):
         self.lib, self.cfg, self.spec = bind(lib), cfg, spec
         self._h = C.c_void_p()
+        self.halo = halo
         b = Block(spec.oi, spec.oj, spec.bnx, spec.bny, halo)
         rc = lib.fn["create_block"](C.byref(cfg), C.byref(b), device, C.byref(self._h))
         if rc:
@@ -144,6 +148,22 @@ class BlockSolver:
         v = g.view()
         self._check(self.lib.fn["block_download"](self._h, C.byref(v)))
         g.step, g.time = v.step, v.time
+
+    def window(self) -> Tuple[int, int, int, int]:
+        """(wi0, wj0, wnx, wny): the block's storage window clipped to the
+        mesh, the cells a rank paints for h2d_block_init_window."""
+        s, H = self.spec, self.halo
+        nx, ny = self.cfg.mesh.nx, self.cfg.mesh.ny
+        i0, j0 = max(0, s.oi - H), max(0, s.oj - H)
+        i1, j1 = min(nx, s.oi + s.bnx + H), min(ny, s.oj + s.bny + H)
+        return i0, j0, i1 - i0, j1 - j0
+
+    def init_window(self, w, step: int = 0, time: float = 0.0):
+        """The block's initial State from a painted window (cases.WindowState):
+        per-rank painting, then init_case's tail on the device."""
+        v = w.view()
+        self._check(self.lib.fn["block_init_window"](self._h, C.byref(v), w.wi0, w.wj0, w.wnx, w.wny, step,
+                                                     time))
 
     def begin(self, max_steps: int, t_end: float, cfl: float):
         self._check(self.lib.fn["block_begin"](self._h, max_steps, t_end, cfl))
@@ -223,10 +243,15 @@ class DeviceComm:
         return buf.raw
 
     def run(self, max_steps: int, t_end: float, cfl: float) -> int:
+        """Run to max_steps (absolute) / t_end; returns the steps done. The
+        device time of the steps (CUDA events on the block's streams) is
+        left in self.device_ms."""
         done = C.c_int(0)
-        rc = self.lib.fn["blocks_run"](self._h, max_steps, t_end, cfl, C.byref(done))
+        ms = C.c_float(0.0)
+        rc = self.lib.fn["blocks_run"](self._h, max_steps, t_end, cfl, C.byref(done), C.byref(ms))
         if rc:
             self.blocks[0]._check(rc)
+        self.device_ms = ms.value
         return done.value
 
     def close(self):

@@ -12,7 +12,8 @@ HEADER = os.path.join(helpers.ROOT, "include", "h2d.h")
 # product-only: benchmark support, the block decomposition, and the field / checkpoint I/O
 # (the I/O is checked against the reference writer itself, tests/test_io.py)
 PRODUCT_ONLY_PREFIXES = ("launch_count", "step_timed", "flush_l2", "create_block", "block_", "halo_",
-                         "write_fields", "diag_line", "save_state", "load_state")
+                         "write_fields", "diag_line", "save_state", "load_state", "comm_", "blocks_run",
+                         "nccl_unique_id")
 
 
 def declared():

@@ -160,3 +160,23 @@ def test_gloo_halo_exchange_fills_every_halo_cell(world, px, py):
     res = sorted(q.get(timeout=10) for _ in range(world))
     assert all(p.exitcode == 0 for p in procs)
     assert res == [(r, 0) for r in range(world)]
+
+
+@pytest.mark.parametrize("which", ["triple", "bubble", "voronoi3", "riemann"])
+def test_window_paint_equals_global_paint(which):
+    """Per-rank painting (cases.paint(window=...)) gives, bit for bit, the
+    cells and nodes of the global painter inside the window."""
+    from paper_2208_13409_b200 import cases
+    case = {"triple": cases.triple_point(70, 30), "bubble": cases.shock_bubble(96),
+            "voronoi3": cases.voronoi3(80), "riemann": cases.riemann2d(40)}[which]
+    full = case.paint()
+    g = 2
+    nx, ny = case.cfg.mesh.nx, case.cfg.mesh.ny
+    for (wi0, wj0, wnx, wny) in ((0, 0, 17, 11), (13, 5, min(30, nx - 13), min(20, ny - 5)), (nx - 9, ny - 7, 9, 7)):
+        w = case.paint((wi0, wj0, wnx, wny))
+        for a in range(case.cfg.nmat):
+            for f in ("m", "e", "k"):
+                want = getattr(full, f)[a][g + wj0:g + wj0 + wny, g + wi0:g + wi0 + wnx]
+                assert np.array_equal(getattr(w, f)[a].view(np.int64), want.view(np.int64)), (f, a)
+        want_u = full.u[g + wj0:g + wj0 + wny + 1, g + wi0:g + wi0 + wnx + 1]
+        assert np.array_equal(w.u.view(np.int64), want_u.view(np.int64))

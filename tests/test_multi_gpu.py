@@ -184,3 +184,31 @@ def test_nccl_transport_single_rank():
     a, dts, e = blk.result(steps)
     assert e is None and np.array_equal(dts, r.dts)
     assert helpers.bitwise_diff(got, ref, helpers.STATE_FIELDS) == []
+
+
+@pytest.mark.parametrize("px,py", [(2, 1), (2, 2), (4, 2)])
+@pytest.mark.parametrize("which", ["triple", "bubble", "voronoi3"])
+def test_window_init_blocks_equal_single_domain(which, px, py):
+    """Per-rank painting: every block paints and initialises only its own
+    window (h2d_block_init_window: fill_ghosts at the global walls,
+    sync_derived, interface normals on the window; the first exchange makes
+    the halo exact), no global host State; the run equals the single
+    domain's bit for bit."""
+    case = {"triple": cases.triple_point(96, 48), "bubble": cases.shock_bubble(64),
+            "voronoi3": cases.voronoi3(128)}[which]
+    steps = 25
+    ref, r, err = _single(case, steps)
+    lib = helpers.product_lib()
+    specs = multi.decompose(case.cfg.mesh.nx, case.cfg.mesh.ny, px, py)
+    blocks = [multi.BlockSolver(lib, case.cfg, sp) for sp in specs]
+    for b in blocks:
+        b.init_window(case.paint(b.window()))
+    comm = multi.DeviceComm(blocks, px, py)
+    comm.run(steps, 1e30, case.cfl)
+    comm.close()
+    got = HostState.empty(case.cfg.mesh.nx, case.cfg.mesh.ny, case.cfg.nmat)
+    for b in blocks:
+        b.download_into(got)
+        a, dts, e = b.result(steps)
+        assert e is None and np.array_equal(dts, r.dts)
+    assert helpers.bitwise_diff(got, ref, helpers.STATE_FIELDS) == []
