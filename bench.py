@@ -59,8 +59,8 @@ def workload(name, full=True):
     16384^2 three-material mesh (about 594 B per cell on the device: it fits
     one B200); full=False gives one GPU's 4096 x 8192 block of it."""
     from paper_2208_13409_b200 import cases
-    if name == "c5" and full:
-        return cases.voronoi3(16384)
+    if name == "c5":
+        return c5_case(cases.voronoi3(16384) if full else cases.voronoi3(4096, 8192, n_full=16384))
     if name == "c1":
         return cases.riemann2d(256)
     if name == "c2":
@@ -69,9 +69,17 @@ def workload(name, full=True):
         return cases.triple_point(2048, 1024)
     if name == "c4":
         return cases.shock_bubble(8192)
-    if name == "c5":  # one GPU's block of the 8-GPU (4 x 2) decomposition of the 16384^2 problem
-        return cases.voronoi3(4096, 8192, n_full=16384)
     raise SystemExit(f"unknown workload {name}")
+
+
+def c5_case(case):
+    """Configuration 5 runs with the sliver-energy safeguard
+    (H2D_OPT_SLIVER_ENERGY, include/h2d.h; default off elsewhere): without it
+    a remapped sliver's negative energy aborts the Voronoi case within tens
+    of steps, as the reference's own two-material proxy does."""
+    from paper_2208_13409_b200 import abi
+    case.cfg.options = abi.OPT_SLIVER_ENERGY
+    return case
 
 
 def hbm_peak():
@@ -186,6 +194,7 @@ SCHEMES = {"ad": "AD split (X/Y alternating)", "direct": "Direct (faces only)"}
 def config_of(case, remap, world, parallelism=None):
     """The `config` object, identical for the product and the reference arm."""
     return {"workload": case.name, "cells": case.cells, "materials": case.cfg.nmat, "cfl": case.cfl,
+            "options": "sliver-energy safeguard (H2D_OPT_SLIVER_ENERGY)" if case.cfg.options else "none",
             "scheme": SCHEMES.get(remap, "DirectCF") + " face_order=2 LinearDiag interface_degrade",
             "steps_from": "t=0 (+ warm-up steps)",
             "parallelism": parallelism or ("replicas" if world > 1 else "single"),
@@ -210,7 +219,7 @@ def cpu_sample(name, case):
     restatement: its lower-left 2048^2 block (same cells, same sites)."""
     if name == "c5" and case.cfg.mesh.nx > 4096:
         from paper_2208_13409_b200 import cases
-        return cases.voronoi3(2048, 2048, n_full=case.cfg.mesh.nx), "lower-left 2048^2 block of the mesh, "
+        return c5_case(cases.voronoi3(2048, 2048, n_full=case.cfg.mesh.nx)), "lower-left 2048^2 block of the mesh, "
     return case, ""
 
 

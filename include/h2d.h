@@ -94,7 +94,20 @@ typedef struct {
     int face_order;        /* ReconConfig::face_order */
     int corner;            /* H2D_CORNER_* */
     int interface_degrade; /* ReconConfig::interface_degrade */
+    int options;           /* H2D_OPT_* bits, 0 = the reference scheme */
 } h2d_config;
+
+/* Options with no reference counterpart (default off; every parity claim is
+ * for options == 0):
+ * H2D_OPT_SLIVER_ENERGY — configuration 5's sliver-energy safeguard: after
+ *   finalize_cells' sliver pass (remap.cpp:194-226), a material of a cell with
+ *   positive mass and NEGATIVE specific internal energy (a remapped sliver;
+ *   the reference floors energies in the Lagrangian phase only,
+ *   lagrange.cpp:119-124, and then throws UnphysicalStateError from
+ *   sound_speed, eos.hpp:31-32) hands its m*e to the cell's largest-mass other
+ *   material when that sum stays positive (total m*e conserved), else drops
+ *   it; its own e becomes 0 (P = 0, c = 0). */
+enum { H2D_OPT_SLIVER_ENERGY = 1 };
 
 /* Host view of a reference State (state.hpp:39-63).  Any derived pointer
  * (vol, m_mix, e_mix, rho_mix, p_mix) may be NULL on upload, in which case

@@ -868,6 +868,31 @@ static void push_sliver(ctx_t* c, size_t* npend, int i, int j, int a) {
     ++*npend;
 }
 
+/* H2D_OPT_SLIVER_ENERGY (no reference counterpart, include/h2d.h): a material
+ * with m > 0 and e < 0 after the sliver pass hands m*e to the cell's
+ * largest-mass other material if the sum stays positive, else drops it;
+ * its e becomes 0. Materials in index order. */
+static void sliver_energy_fix(ctx_t* c) {
+    work_t* w = &c->w;
+    for (int j = 0; j < c->ny; ++j)
+        for (int i = 0; i < c->nx; ++i)
+            for (int a = 0; a < c->nmat; ++a) {
+                if (!(A(w->m[a], i, j) > 0.0 && A(w->e[a], i, j) < 0.0)) continue;
+                int b = -1;
+                for (int q = 0; q < c->nmat; ++q)
+                    if (q != a && A(w->m[q], i, j) > 0.0 && (b < 0 || A(w->m[q], i, j) > A(w->m[b], i, j))) b = q;
+                if (b >= 0) {
+                    const double meb = A(w->me[b], i, j) + A(w->me[a], i, j);
+                    if (meb > 0.0) {
+                        A(w->me[b], i, j) = meb;
+                        A(w->e[b], i, j) = meb / A(w->m[b], i, j);
+                    }
+                }
+                A(w->me[a], i, j) = 0.0;
+                A(w->e[a], i, j) = 0.0;
+            }
+}
+
 /* finalize_cells, remap.cpp:146-234 */
 static void finalize_cells(ctx_t* c) {
     work_t* w = &c->w;
@@ -1021,6 +1046,7 @@ static void finalize_cells(ctx_t* c) {
             A(w->mcell, si, sj) += sm;
         }
     }
+    if (c->cfg.options & H2D_OPT_SLIVER_ENERGY) sliver_energy_fix(c);
     for (int a = 0; a < c->nmat; ++a) {
         ghost_cells(c, w->m[a]);
         ghost_cells(c, w->me[a]);

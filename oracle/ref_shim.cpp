@@ -715,9 +715,11 @@ bool ref_scalar(int op, const double* x, double* o) {
         case H2D_SC_AD_FACE_FLUX: {
             // one X face of ad_face_fluxes on a 3 x 3 mesh whose dy and cv are the record's
             const double dy = x[3], dx = x[4] / x[3];
-            Field<Vec2> uh(4, 4);
+            Field<Vec2> uh(4, 4);  // the other faces of column 0 cancel: (0, 1), (0, 2) carry 0
             uh(0, 0) = {x[0], 0.0};
             uh(0, 1) = {x[1], 0.0};
+            uh(0, 2) = {-x[1], 0.0};
+            uh(0, 3) = {x[1], 0.0};
             o[0] = ad_face_fluxes(Axis::X, Mesh(3, 3, dx, dy), uh, x[2])(0, 0);
             break;
         }

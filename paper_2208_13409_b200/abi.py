@@ -28,6 +28,7 @@ EOS_PERFECT, EOS_STIFFENED = 0, 1
 CORNER_UPWIND, CORNER_AVGMIN, CORNER_LINEARXY, CORNER_LINEARDIAG, CORNER_MULTID = range(5)
 REMAP_AD, REMAP_DIRECT, REMAP_DIRECTCF = range(3)
 DUMP_CSV, DUMP_VTK = 0, 1  # DumpFormat, io.hpp:9
+OPT_SLIVER_ENERGY = 1  # H2D_OPT_SLIVER_ENERGY (no reference counterpart, default off)
 
 _dp = C.POINTER(C.c_double)
 
@@ -47,7 +48,7 @@ class Config(C.Structure):
     """MaterialSet + PseudoViscosityParams + ReconConfig (h2d_config)."""
     _fields_ = [("mesh", Mesh), ("nmat", C.c_int), ("eos", Eos * MAX_MAT),
                 ("pv_a1", C.c_double), ("pv_a2", C.c_double), ("face_order", C.c_int),
-                ("corner", C.c_int), ("interface_degrade", C.c_int)]
+                ("corner", C.c_int), ("interface_degrade", C.c_int), ("options", C.c_int)]
 
 
 class StateView(C.Structure):
@@ -102,7 +103,8 @@ class RunArgs(C.Structure):
 
 
 def make_config(nx, ny, dx, dy, x0=0.0, y0=0.0, bc_x=BC_WALL, bc_y=BC_WALL, eos=((EOS_PERFECT, 1.4, 0.0),),
-                a1=0.2, a2=1.0, face_order=2, corner=CORNER_LINEARDIAG, interface_degrade=True) -> Config:
+                a1=0.2, a2=1.0, face_order=2, corner=CORNER_LINEARDIAG, interface_degrade=True,
+                options=0) -> Config:
     """Build an h2d_config; defaults are the reference defaults
     (lagrange.hpp:7-10, reconstruct.hpp:9-13) with walls on every side."""
     cfg = Config()
@@ -112,6 +114,7 @@ def make_config(nx, ny, dx, dy, x0=0.0, y0=0.0, bc_x=BC_WALL, bc_y=BC_WALL, eos=
         cfg.eos[a] = Eos(kind, gamma, pi)
     cfg.pv_a1, cfg.pv_a2 = a1, a2
     cfg.face_order, cfg.corner, cfg.interface_degrade = face_order, corner, int(bool(interface_degrade))
+    cfg.options = options
     return cfg
 
 

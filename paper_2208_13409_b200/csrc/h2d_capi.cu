@@ -697,6 +697,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     d.corner_diag = cfg->corner == H2D_CORNER_LINEARDIAG;
     d.corner = cfg->corner;
     d.degrade = cfg->interface_degrade != 0;
+    d.opt_energy = (cfg->options & H2D_OPT_SLIVER_ENERGY) != 0;
     d.remap_velocity = 1;
     d.q = plane(c);
     d.pmh = plane(c);

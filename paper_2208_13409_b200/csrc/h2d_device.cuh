@@ -173,6 +173,7 @@ struct Dev {
     int face_order, corner_diag, degrade, remap_velocity;
     int corner;  // CornerScheme (H2D_CORNER_*): Upwind, AvgMin, LinearXY, LinearDiag, Multid
     int direct;  // 1: the Direct engine (faces only) instead of DirectCF
+    int opt_energy;  // H2D_OPT_SLIVER_ENERGY (no reference counterpart, default off)
 
     // current (read) State
     const double *m[kMatSlots], *e[kMatSlots], *k[kMatSlots], *m_mix, *e_mix, *rho_mix, *p_mix, *nrx, *nry, *ux, *uy;

@@ -3579,11 +3579,50 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
 }
 
 // slivers + finalize_cells ghost fill + flux ghosts
+// H2D_OPT_SLIVER_ENERGY (include/h2d.h; oracle sliver_energy_fix): after the
+// sliver pass, a material with m > 0 and e < 0 hands m*e to the cell's
+// largest-mass other material if the sum stays positive, else drops it; its
+// e becomes 0 (materials in index order)
+template <int NM>
+__global__ void k_energy_fix(Dev d) {
+    pdl_enter();
+    if (halted(d.ctl)) return;
+    int i, j;
+    tid2(i, j, d.r_gath.i0, d.r_gath.j0);
+    if (!in(d.r_gath, i, j)) return;
+    const int c = ix(d, i, j);
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        if (!(d.nm[a][c] > 0.0 && d.ne[a][c] < 0.0)) continue;
+        int b = -1;
+#pragma unroll
+        for (int q = 0; q < NM; ++q)
+            if (q != a && d.nm[q][c] > 0.0 && (b < 0 || d.nm[q][c] > d.nm[b][c])) b = q;
+        if (b >= 0) {
+            const double meb = d.me[b][c] + d.me[a][c];
+            if (meb > 0.0) {
+                d.me[b][c] = meb;
+                d.ne[b][c] = meb / d.nm[b][c];
+            }
+        }
+        d.me[a][c] = 0.0;
+        d.ne[a][c] = 0.0;
+    }
+}
+
 void launch_remap_slivers(const Dev& d, cudaStream_t s) {
     if (d.nmat == 3)
         pdl(k_slivers<3>, dim3(1), dim3(SLB), 0, s, d);
     else if (d.nmat == 2)
         pdl(k_slivers<2>, dim3(1), dim3(SLB), 0, s, d);
+    if (d.opt_energy) {
+        if (d.nmat == 3)
+            pdl(k_energy_fix<3>, grid_of(d.r_gath), blk2(), 0, s, d);
+        else if (d.nmat == 2)
+            pdl(k_energy_fix<2>, grid_of(d.r_gath), blk2(), 0, s, d);
+        else
+            pdl(k_energy_fix<1>, grid_of(d.r_gath), blk2(), 0, s, d);
+    }
     // finalize_cells ghost fill (remap.cpp:227-233) + face / corner flux ghosts
     FieldList fl{};
     int q = 0;

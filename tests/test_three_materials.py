@@ -152,3 +152,77 @@ def test_device_absent_material_reduces_to_two(gpu, orc, absent):
     r3, _ = helpers.run_capture(sg, steps, cfl)
     assert np.array_equal(r2.dts, r3.dts)
     assert same_as_two(sg.download(), s2.download(), slots) == []
+
+
+# ---- H2D_OPT_SLIVER_ENERGY: configuration 5 to its 100 steps ----------------
+def _voronoi_opt(n):
+    c = cases.voronoi3(n)
+    c.cfg.options = abi.OPT_SLIVER_ENERGY
+    return c
+
+
+def test_voronoi_aborts_without_the_safeguard(orc):
+    """Like the reference's own two-material proxy, the
+    scheme as the reference defines it aborts the Voronoi case: a remapped
+    sliver's e goes negative and sound_speed throws (eos.hpp:31-32)."""
+    c = cases.voronoi3(64)
+    s = helpers.prepared(orc, c.cfg, c.paint())
+    r, err = helpers.run_capture(s, 100, c.cfl)
+    assert err is not None and err[0] == "UnphysicalStateError" and r.steps_done < 100
+
+
+@pytest.mark.parametrize("n", [64, 128])
+def test_voronoi_safeguard_runs_100_steps(orc, n):
+    """With the (non-default) sliver-energy safeguard the case runs its 100
+    steps; mass is conserved per material up to sliver moves and in total."""
+    c = _voronoi_opt(n)
+    painted = c.paint()
+    s = helpers.prepared(orc, c.cfg, painted)
+    m0 = sum(float(np.sum(painted.cell(painted.m)[a])) for a in range(3))
+    r, err = helpers.run_capture(s, 100, c.cfl)
+    assert err is None and r.steps_done == 100
+    st = s.download()
+    m1 = sum(float(np.sum(st.cell(st.m)[a])) for a in range(3))
+    assert abs(m1 - m0) <= 1e-12 * m0
+    k = st.cell(st.k)[:3]
+    assert (k >= 0.0).all() and (k <= 1.0).all()
+    assert np.all(st.cell(st.e)[:3][st.cell(st.m)[:3] > 0] >= 0.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [64, 256])
+def test_device_voronoi_safeguard_bitwise(gpu, orc, n):
+    c = _voronoi_opt(n)
+    painted = c.paint()
+    sg = helpers.prepared(gpu, c.cfg, painted)
+    so = helpers.prepared(orc, c.cfg, painted)
+    rg, eg = helpers.run_capture(sg, 100, c.cfl)
+    ro, eo = helpers.run_capture(so, 100, c.cfl)
+    assert eg is None and eo is None and rg.steps_done == 100
+    assert np.array_equal(rg.dts, ro.dts)
+    assert rg.diag == ro.diag and rg.floor_count == ro.floor_count
+    assert helpers.bitwise_diff(sg.download(), so.download(), helpers.STATE_FIELDS, 3) == []
+
+
+@pytest.mark.gpu
+def test_device_voronoi_safeguard_blocks_bitwise(gpu):
+    """the safeguard under the block data plane (window init, 4 x 2 blocks)."""
+    from paper_2208_13409_b200 import multi
+    c = _voronoi_opt(128)
+    steps = 100
+    s = helpers.prepared(gpu, c.cfg, c.paint())
+    r = s.run(steps, cfl=c.cfl)
+    ref = s.download()
+    specs = multi.decompose(128, 128, 4, 2)
+    blocks = [multi.BlockSolver(gpu, c.cfg, sp) for sp in specs]
+    for b in blocks:
+        b.init_window(c.paint(b.window()))
+    comm = multi.DeviceComm(blocks, 4, 2)
+    comm.run(steps, 1e30, c.cfl)
+    comm.close()
+    got = HostState.empty(128, 128, 3)
+    for b in blocks:
+        b.download_into(got)
+        a, dts, e = b.result(steps)
+        assert e is None and np.array_equal(dts, r.dts)
+    assert helpers.bitwise_diff(got, ref, helpers.STATE_FIELDS, 3) == []
