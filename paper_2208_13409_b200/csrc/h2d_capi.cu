@@ -64,6 +64,10 @@ struct h2d_ctx {
     size_t diag_tick_bytes = 0;     // the ticket words at the start of diag_mem
     double* diag_log = nullptr;     // device StepDiag log of h2d_run (kDiagRec doubles per step)
     cudaGraphExec_t graph_rest[2] = {nullptr, nullptr};  // block data plane: the step after the Lagrange kernel
+    // the run loops keep no derived planes (m_mix, e_mix, rho_mix, p_mix, vol):
+    // set after a run step, cleared by ensure_derived (sync_derived on the
+    // current State) before anything reads the State
+    bool derived_stale = false;
     long long graph_rest_kernels = 0;
 };
 
@@ -376,6 +380,17 @@ void enqueue_step(h2d_ctx* c, int parity) { launch_step(make_dev(c, parity, 1), 
 // into the previous step's k_tail on a single domain)
 void start_first(h2d_ctx* c) {
     if (!c->is_block) launch_step_start(make_dev(c, c->cur, 1), c->st);
+}
+
+// rebuild the derived planes of the current State after run-loop steps
+// (sync_derived, state.cpp:120-143: the values k_post computed in registers)
+int ensure_derived(h2d_ctx* c) {
+    if (!c->derived_stale) return 0;
+    launch_sync(make_dev(c, c->cur, 1), 0, 0, c->st);
+    if (int rc = check_launch(c)) return rc;
+    CK(cudaStreamSynchronize(c->st));
+    c->derived_stale = false;
+    return 0;
 }
 
 // cfl_dt of the current State into the control block's "next" slots, which
@@ -825,12 +840,15 @@ int h2d_upload_state(h2d_ctx* c, const h2d_state* v) {
     c->hctl->step = v->step;
     c->hctl->time = v->time;
     if (int rc = ctl_push(c)) return rc;
+    c->derived_stale = false;
     if (!derived) return h2d_sync_derived(c);
     CK(cudaStreamSynchronize(c->st));
     return 0;
 }
 
 int h2d_download_state(h2d_ctx* c, h2d_state* v) {
+    cudaSetDevice(c->device);
+    if (int rc_ = ensure_derived(c)) return rc_;
     cudaSetDevice(c->device);
     const int nx = c->nx, ny = c->ny;
     const StateBufs& s = c->sb[c->cur];
@@ -864,6 +882,7 @@ int h2d_fill_ghosts(h2d_ctx* c) {
 
 int h2d_sync_derived(h2d_ctx* c) {
     cudaSetDevice(c->device);
+    c->derived_stale = false;
     launch_sync(make_dev(c, c->cur, 1), 0, 0, c->st);
     if (int rc = check_launch(c)) return rc;
     CK(cudaStreamSynchronize(c->st));
@@ -888,6 +907,8 @@ int h2d_update_interface_normals(h2d_ctx* c) {
 
 int h2d_cfl_dt(h2d_ctx* c, double cfl, double* dt) {
     cudaSetDevice(c->device);
+    if (int rc_ = ensure_derived(c)) return rc_;
+    cudaSetDevice(c->device);
     if (int rc = ctl_reset(c)) return rc;
     c->hctl->cfl = cfl;
     if (int rc = ctl_push(c)) return rc;
@@ -902,6 +923,8 @@ int h2d_cfl_dt(h2d_ctx* c, double cfl, double* dt) {
 }
 
 int h2d_lagrange_step(h2d_ctx* c, double dt, h2d_lagrange* out) {
+    cudaSetDevice(c->device);
+    if (int rc_ = ensure_derived(c)) return rc_;
     cudaSetDevice(c->device);
     c->have_lag = false;
     if (int rc = ctl_reset(c)) return rc;
@@ -950,6 +973,8 @@ int h2d_set_lagrange(h2d_ctx* c, const h2d_lagrange* in) {
 
 int h2d_remap_step(h2d_ctx* c, double dt, int kind, int x_first, int remap_velocity, h2d_remap_diag* diag) {
     cudaSetDevice(c->device);
+    if (int rc_ = ensure_derived(c)) return rc_;
+    cudaSetDevice(c->device);
     if (kind != H2D_REMAP_DIRECTCF && !(kind == H2D_REMAP_AD && !c->is_block && c->nmat <= 2) &&
         !(kind == H2D_REMAP_DIRECT && !c->is_block)) {
         set_err(c, H2D_ERR_INVALID, "the device runs DirectCF, Direct and (single-domain, <= 2 materials) AD");
@@ -986,6 +1011,8 @@ int h2d_remap_step(h2d_ctx* c, double dt, int kind, int x_first, int remap_veloc
 // ---- sub-step entry points (lagrange.hpp predict / correct, remap.hpp
 // remap_single_axis) and the scalar kernels ---------------------------------
 int h2d_predict(h2d_ctx* c, double dt, h2d_half* out) {
+    cudaSetDevice(c->device);
+    if (int rc_ = ensure_derived(c)) return rc_;
     cudaSetDevice(c->device);
     c->have_lag = false;
     if (c->is_block) {
@@ -1029,6 +1056,8 @@ int h2d_predict(h2d_ctx* c, double dt, h2d_half* out) {
 
 int h2d_correct(h2d_ctx* c, double dt, const h2d_half* in, h2d_lagrange* out) {
     cudaSetDevice(c->device);
+    if (int rc_ = ensure_derived(c)) return rc_;
+    cudaSetDevice(c->device);
     c->have_lag = false;
     if (c->is_block || !in || !in->u_half || !in->q) {
         set_err(c, H2D_ERR_INVALID, "correct needs a single-domain context and a HalfStepState");
@@ -1069,6 +1098,8 @@ int h2d_correct(h2d_ctx* c, double dt, const h2d_half* in, h2d_lagrange* out) {
 }
 
 int h2d_remap_single_axis(h2d_ctx* c, double dt, int axis_x, int remap_velocity, h2d_remap_diag* diag) {
+    cudaSetDevice(c->device);
+    if (int rc_ = ensure_derived(c)) return rc_;
     cudaSetDevice(c->device);
     if (c->is_block || c->nmat > 2) {
         set_err(c, H2D_ERR_INVALID, "remap_single_axis runs on single-domain contexts with <= 2 materials");
@@ -1204,6 +1235,7 @@ int h2d_run(h2d_ctx* c, h2d_run_args* a) {
         if (h.err_key != kNoErr || h.done) break;
     }
     c->cur = h.cur;
+    c->derived_stale = true;
     a->steps_done = h.steps_done;
     a->floor_count += h.floor_count;
     a->diag.k_clip_count += h.k_clip_count;
@@ -1228,6 +1260,8 @@ int h2d_totals(h2d_ctx* c, double out[6]) {
 
 // {mass, mass_mat0, mass_mat1, momentum x, momentum y, internal energy, mass_mat2}
 static int totals7(h2d_ctx* c, double out[7]) {
+    cudaSetDevice(c->device);
+    if (int rc_ = ensure_derived(c)) return rc_;
     // compute_totals (state.cpp:145-160) is a serial fp64 sum: read the
     // fields back and add them in the reference order so totals are exact.
     cudaSetDevice(c->device);
@@ -1277,6 +1311,8 @@ static int totals7(h2d_ctx* c, double out[7]) {
 }
 
 int h2d_step_diag_now(h2d_ctx* c, double dt, h2d_step_diag* out) {
+    cudaSetDevice(c->device);
+    if (int rc_ = ensure_derived(c)) return rc_;
     // make_diag (harness.cpp:360-376) on the host, in the reference's order
     double t[7];
     if (int rc = totals7(c, t)) return rc;
@@ -1379,6 +1415,7 @@ int h2d_load_state(h2d_ctx* c, const char* path) {
 }
 
 int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_kind, float ms[8]) {
+    c->derived_stale = true;  // run-loop steps keep no derived planes
     cudaSetDevice(c->device);
     const bool ad = remap_kind == H2D_REMAP_AD, dir = remap_kind == H2D_REMAP_DIRECT;
     if (!(remap_kind == H2D_REMAP_DIRECTCF || (ad && !c->is_block && c->nmat <= 2) || (dir && !c->is_block))) {
@@ -1527,11 +1564,8 @@ void state_lists(h2d_ctx* c, FieldList& cl, FieldList& nl) {
         cl.f[cl.n++] = sb.e[a];
         cl.f[cl.n++] = sb.k[a];
     }
-    cl.f[cl.n++] = sb.vol;
-    cl.f[cl.n++] = sb.m_mix;
-    cl.f[cl.n++] = sb.e_mix;
-    cl.f[cl.n++] = sb.rho_mix;
-    cl.f[cl.n++] = sb.p_mix;
+    // (the derived planes are not part of the exchange: the step rebuilds
+    // what it needs from m and k, ensure_derived the rest when read)
     cl.f[cl.n++] = sb.nrx;
     cl.f[cl.n++] = sb.nry;
     nl.f[nl.n++] = sb.ux;
@@ -1600,6 +1634,7 @@ int h2d_block_upload(h2d_ctx* c, const h2d_state* g) {
     if (int rc = ctl_pull(c)) return rc;
     c->hctl->step = g->step;
     c->hctl->time = g->time;
+    c->derived_stale = false;
     return ctl_push(c);
 }
 
@@ -1646,6 +1681,8 @@ int h2d_block_init_window(h2d_ctx* c, const h2d_state* w, int wi0, int wj0, int 
 }
 
 int h2d_block_download(h2d_ctx* c, h2d_state* g) {
+    cudaSetDevice(c->device);
+    if (int rc_ = ensure_derived(c)) return rc_;
     cudaSetDevice(c->device);
     const Dev& d = c->base;
     StateBufs& s = c->sb[c->cur];
@@ -1712,6 +1749,7 @@ int h2d_block_set(h2d_ctx* c, const unsigned long long in[3]) {
 
 int h2d_block_step(h2d_ctx* c) {
     cudaSetDevice(c->device);
+    c->derived_stale = true;
     if (int rc = launch_step_graph(c, c->cur)) return rc;
     if (int rc = ctl_pull(c)) return rc;
     c->cur = c->hctl->cur;
@@ -2040,8 +2078,10 @@ int h2d_blocks_run(h2d_comm* m, int max_steps, double t_end, double cfl, int* st
     if (device_ms) *device_ms = 0.0f;
     h2d_ctx* c = m->side[0].c;  // CK's error target
     const int n = (int)m->side.size();
-    for (auto& sd : m->side)
+    for (auto& sd : m->side) {
         if (int rc = h2d_block_begin(sd.c, max_steps, t_end, cfl)) return rc;
+        sd.c->derived_stale = true;
+    }
     std::vector<int> parity(n);
     for (int b = 0; b < n; ++b) parity[b] = m->side[b].c->cur;
 

@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     pdl_enter();
     constexpr int LTY = H2D_FTY;
     constexpr int CW = LTX + 2, CH = LTY + 2, NC = CW * CH, NN = (LTX + 1) * (LTY + 1);
-    __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC];
+    __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC], s_mm[NC];
     __shared__ double shx[NN], shy[NN];
     __shared__ int s_halt;
     const int tid = threadIdx.x;
@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     RowCol<CW, LTX * LTY> rc0(tid);
     for (int t = tid; t < NC; t += LTX * LTY, rc0.step()) {
         const int ci = i0 - 1 + rc0.c, cj = j0 - 1 + rc0.r;
-        double q = 0.0, pmix = 0.0, ph[NM] = {};
+        double q = 0.0, pmix = 0.0, ph[NM] = {}, mmix = 0.0;
         if (in(d.win_c, ci, cj) && ci >= -1 && cj >= -1 && ci <= nx && cj <= ny) {
             const int i = (ci < 0 || ci >= nx) ? wrap_cell(ci, nx, d.per_x) : ci;
             const int j = (cj < 0 || cj >= ny) ? wrap_cell(cj, ny, d.per_y) : cj;
@@ -583,6 +583,12 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
                 ma[a] = d.m[a][c];
                 en[a] = d.e[a][c];
             }
+            // the State's m_mix / rho_mix (sync_derived, state.cpp:120-143) from
+            // the partial masses: the run loop does not keep the derived planes
+            // (they are rebuilt bit-identically when the State is read)
+#pragma unroll
+            for (int a = 0; a < NM; ++a)
+                if (ka[a] > 0.0) mmix += ma[a];
             const double ux_l = 0.5 * (u00x + u01x);
             const double ux_r = 0.5 * (u10x + u11x);
             const double uy_b = 0.5 * (u00y + u10y);
@@ -599,7 +605,7 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
                     cs += ka[a] * sound(d, a, rho_a, pa, bad);
                 }
                 if (bad && canon) raise(d.ctl, ekey(PH_Q_UNPHYS, j, i, 0));
-                const double rho = d.rho_mix[c];
+                const double rho = div_cv(d, mmix);
                 const double du = d.L * fabs(div);
                 q = rho * d.a1 * du * cs + d.a2 * rho * du * du;
             }
@@ -634,6 +640,7 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
         }
         s_q[t] = q;
         s_pmh[t] = pmix;
+        s_mm[t] = mmix;
 #pragma unroll
         for (int a = 0; a < NM; ++a) s_ph[a][t] = ph[a];
     }
@@ -646,8 +653,8 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
         if (in(rn, i, j)) {
             const int ta = rc1.c + rc1.r * CW;  // cell (i-1, j-1) in the cell tile
             const int tb = ta + 1, tc = ta + CW, te = tc + 1;
-            const int a = ix(d, i - 1, j - 1), b = ix(d, i, j - 1), c = ix(d, i - 1, j), e = ix(d, i, j);
-            const double mp = 0.25 * (d.m_mix[a] + d.m_mix[b] + d.m_mix[c] + d.m_mix[e]);
+            const int e = ix(d, i, j);
+            const double mp = 0.25 * (s_mm[ta] + s_mm[tb] + s_mm[tc] + s_mm[te]);
             const double rho_p = div_cv(d, mp);
             const double pq_a = s_pmh[ta] + s_q[ta], pq_b = s_pmh[tb] + s_q[tb];
             const double pq_c = s_pmh[tc] + s_q[tc], pq_e = s_pmh[te] + s_q[te];
@@ -2753,11 +2760,13 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
             p += ka[a] * eos_p(d, a, rho_a, ea[a]);
         }
         emix = m > 0.0 ? me / m : 0.0;
-        d.nm_mix[c] = m;
-        d.ne_mix[c] = emix;
-        d.nrho_mix[c] = div_cv(d, m);
-        d.np_mix[c] = p;
-        d.nvol[c] = cv;
+        if (!run_loop) {  // the run loop keeps no derived planes (rebuilt when the State is read)
+            d.nm_mix[c] = m;
+            d.ne_mix[c] = emix;
+            d.nrho_mix[c] = div_cv(d, m);
+            d.np_mix[c] = p;
+            d.nvol[c] = cv;
+        }
     }
     // make_diag's cell part (harness.cpp:360-376, state.cpp:148-153): this
     // cell's terms go to shared memory now (registers stay free for the rest)

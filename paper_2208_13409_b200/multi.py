@@ -435,5 +435,5 @@ def halo_rects(spec: BlockSpec, nx: int, ny: int, dx: int, dy: int, pack: bool, 
 
 def state_planes(nmat: int) -> Tuple[int, int]:
     """(cell planes, node planes) exchanged per step: m, e, k per material,
-    vol, m_mix, e_mix, rho_mix, p_mix, normal x/y | u x/y."""
-    return 3 * nmat + 7, 2
+    normal x/y | u x/y (the derived fields are rebuilt on the device)."""
+    return 3 * nmat + 2, 2
