@@ -11,7 +11,9 @@ from .abi import (BC_PERIODIC, BC_WALL, CORNER_LINEARDIAG, CORNER_UPWIND, EOS_PE
                   REMAP_DIRECTCF, HostLagrange, HostState, Library, RemapDiag, Solver, make_config)
 
 PKG_DIR = _os.path.dirname(_os.path.abspath(__file__))
-PRODUCT_LIB = _os.path.join(PKG_DIR, "libh2d.so")
+# H2D_PRODUCT_LIB selects another build of the same sources (tools/variants.py
+# builds launch-bound / tile variants for measurement); default: the in-tree build
+PRODUCT_LIB = _os.environ.get("H2D_PRODUCT_LIB") or _os.path.join(PKG_DIR, "libh2d.so")
 
 _product = None
 

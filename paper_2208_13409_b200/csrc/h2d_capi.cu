@@ -566,7 +566,7 @@ int make_tmas(h2d_ctx* c) {
     return 0;
 }
 
-int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx** out);
+int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx** out, bool block);
 
 }  // namespace
 
@@ -583,7 +583,7 @@ int h2d_create(const h2d_config* cfg, int device, h2d_ctx** out) {
     whole.bnx = cfg->mesh.nx;
     whole.bny = cfg->mesh.ny;
     whole.halo = G;
-    return create_ctx(cfg, &whole, device, out);
+    return create_ctx(cfg, &whole, device, out, false);
 }
 
 int h2d_create_block(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx** out) {
@@ -593,7 +593,7 @@ int h2d_create_block(const h2d_config* cfg, const h2d_block* blk, int device, h2
     if (blk->halo < 8 || blk->oi < 0 || blk->oj < 0 || blk->bnx < blk->halo || blk->bny < blk->halo ||
         blk->oi + blk->bnx > m.nx || blk->oj + blk->bny > m.ny)
         return H2D_ERR_INVALID;
-    const int rc = create_ctx(cfg, blk, device, out);
+    const int rc = create_ctx(cfg, blk, device, out, true);
     if (!rc) (*out)->is_block = true;
     return rc;
 }
@@ -601,7 +601,7 @@ int h2d_create_block(const h2d_config* cfg, const h2d_block* blk, int device, h2
 }  // extern "C"
 
 namespace {
-int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx** out) {
+int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx** out, bool block) {
     *out = nullptr;
     const h2d_mesh& m = cfg->mesh;
     if (m.nx < 3 || m.ny < 3) return H2D_ERR_SIM;        // Mesh::Mesh, mesh.hpp:27
@@ -633,13 +633,18 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
         return H2D_ERR_INVALID;
     }
     const int nm = c->nmat;
-    // fp64 planes, exactly as carved below: 2 x State (3 nm + 9; one material
-    // shares its normals between the parities), the LagrangeResult (7) and
-    // per material p_half, e_lag, me, sliver m / m*e (5 nm), the remap scratch
-    // (13), the AoS staging (2). 1 / 2 / 3 materials: 49 / 62 / 73 planes,
-    // i.e. with the 10 byte planes ~402 / 506 / 594 B per cell: 16384^2 x 3
-    // materials (configuration 5) fits one B200
-    const size_t planes = 2 * (3 * (size_t)nm + 9) - (nm == 1 ? 2 : 0) + 7 + 5 * (size_t)nm + 13 + 2;
+    // fp64 planes, exactly as carved below: 2 x State (3 nm + 9; a single
+    // domain shares its normals between the parities: one material carries
+    // them unchanged, and with 2-3 materials the normals are updated in place
+    // (only mixed cells change; a step that fails before k_post never touches
+    // them, and a decomposition block, which can be rolled back after
+    // k_post, keeps two copies), the LagrangeResult (7) and per material
+    // p_half, e_lag, me, sliver m / m*e (5 nm), the remap scratch (13), the
+    // AoS staging (2). Single domain, 1 / 2 / 3 materials: 49 / 60 / 71
+    // planes, i.e. with the 10 byte planes ~402 / 490 / 578 B per cell:
+    // 16384^2 x 3 materials (configuration 5) fits one B200
+    const bool shared_nrm = nm == 1 || !block;
+    const size_t planes = 2 * (3 * (size_t)nm + 9) - (shared_nrm ? 2 : 0) + 7 + 5 * (size_t)nm + 13 + 2;
     const size_t bytes_planes = planes * ((c->fsz * sizeof(double) + 255) & ~size_t(255));
     const size_t bytes_small = 10 * ((c->fsz + 255) & ~size_t(255)) + ((size_t)c->R * 4 + 256);
     c->arena_bytes = bytes_planes + bytes_small + 4096;
@@ -658,10 +663,10 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
         s.e_mix = plane(c);
         s.rho_mix = plane(c);
         s.p_mix = plane(c);
-        if (p == 0 || nm >= 2) {
+        if (p == 0 || !shared_nrm) {
             s.nrx = plane(c);
             s.nry = plane(c);
-        } else {  // one material: the normals are carried unchanged, so both parities share them
+        } else {  // both parities share the normals (see the plane count above)
             s.nrx = c->sb[0].nrx;
             s.nry = c->sb[0].nry;
         }
@@ -776,7 +781,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     if (ctl_push(c)) return fail(H2D_ERR_DEVICE);
     // make_state defaults (state.cpp:5-23): k0 = 1, normals (1, 0), vol = dx*dy
     for (int p = 0; p < 2; ++p) {
-        if (fill_plane(c, c->sb[p].k[0], 1.0) || (p == 0 || nm >= 2 ? fill_plane(c, c->sb[p].nrx, 1.0) : 0) ||
+        if (fill_plane(c, c->sb[p].k[0], 1.0) || (p == 0 || !shared_nrm ? fill_plane(c, c->sb[p].nrx, 1.0) : 0) ||
             fill_plane(c, c->sb[p].vol, d.cv))
             return fail(H2D_ERR_DEVICE);
     }

@@ -1445,18 +1445,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // DIR: the Direct engine (remap.cpp:593-724): face volumes fd * width, the
 // X / Y-displaced interfaces, no corner fluxes (items and dmc zero)
 template <int NM, bool XC = false, bool DIR = false>
-__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
+#ifndef H2D_RT_MINB1
+#define H2D_RT_MINB1 4
+#endif
+#ifndef H2D_RT_MINB2
+#define H2D_RT_MINB2 3
+#endif
+#ifndef H2D_RT_MINB3
+#define H2D_RT_MINB3 2
+#endif
+__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ? H2D_RT_MINB2 : H2D_RT_MINB3)) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
     pdl_enter();
     extern __shared__ __align__(128) char smem_raw[];
     __shared__ int s_halt;
     __shared__ __align__(8) uint64_t s_bar;
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        s_halt = halted(d.ctl);
-        mbar_init(&s_bar, 1);
-    }
-    __syncthreads();
-    if (s_halt) return;
     const int nx = d.nx, ny = d.ny;
     const Rng rg = d.r_gath;
     // TMA wants the box's first column 16-byte aligned (an even plane
@@ -1473,7 +1476,12 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
     // T.kk hold k until phase 2 turns them into densities and volumes.
     // Node values outside the window are never read (every use below is
     // guarded by the window), so whatever the plane holds there is harmless.
+    // The copies are issued before the halt flag is read, so the control
+    // block's load latency overlaps them (a halted step waits for its copies
+    // before the CTA exits: its shared memory must not be handed on while a
+    // copy is still writing it).
     if (tid == 0) {
+        mbar_init(&s_bar, 1);
         constexpr uint32_t bytes = 2u * RNW * RNH * 8u + 3u * NM * RCW * RCH * 8u;
         const int x = T.ci0 + d.H - d.oi, y = T.cj0 + d.H - d.oj;  // plane column / row of the region origin
         mbar_expect_tx(&s_bar, bytes);
@@ -1485,9 +1493,15 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? 4 : (NM == 2 ? 3 : 2)) k_
             tma_load_2d(T.rho[a], &tm.t[TM_M0 + a], x, y, &s_bar);
             tma_load_2d(NM >= 2 ? T.kk[a] : T.vl, &tm.t[TM_K0 + a], x, y, &s_bar);
         }
+        s_halt = halted(d.ctl);
     }
     const double dt = step_dt(d.ctl);
     const double cv = d.cv;
+    __syncthreads();
+    if (s_halt) {
+        if (tid == 0) mbar_wait(&s_bar, 0);
+        return;
+    }
     mbar_wait(&s_bar, 0);
     // ---- quiescent tile: u_half == 0 at every node of the tile's faces and
     // corners makes every face / corner flux volume of the tile zero, so no
@@ -2263,8 +2277,11 @@ __device__ __forceinline__ void dual_corner_items(const Dev& d, int i, int j) {
 
 // All dual-mesh items of one unique node (i, j): its X and Y dual faces and
 // its two diagonal corner exchanges (remap.cpp:995-1069).
+#ifndef H2D_DUAL_MINB
+#define H2D_DUAL_MINB 8
+#endif
 template <bool XC = false>
-__global__ void __launch_bounds__(128, 8) k_dual_items(Dev d) {
+__global__ void __launch_bounds__(128, H2D_DUAL_MINB) k_dual_items(Dev d) {
     pdl_enter();
     if (halted(d.ctl)) return;
     int i, j;
@@ -2720,8 +2737,11 @@ __global__ void k_global_xfer(Dev d, double* buf, Rng r, double* px, double* py,
 // (remap.cpp:102-114, vof.cpp:10-22), and in the run loop nan_scan
 // (harness.cpp:347-358) plus the wave speed of the next step's cfl_dt
 // (harness.cpp:293-310), so the State is read once.
+#ifndef H2D_POST_MINB
+#define H2D_POST_MINB 5
+#endif
 template <int NM>
-__global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
+__global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop) {
     pdl_enter();
     __shared__ unsigned long long sw[8];
     // per-thread diagnostics terms (block of 32 x 8); fewer than three
@@ -2789,7 +2809,6 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
     if (act) {
         if (interior && in(d.r_nrm, i, j)) {
             if (NM >= 2) {  // normals of the new fractions
-                double nrx = d.nrx[c], nry = d.nry[c];
                 bool mixed = is_mixed(ka[0]);
                 int hi = 1;
                 if (NM == 3) {  // Youngs normal of the interface pair's k_hi (pair3)
@@ -2797,6 +2816,15 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
                     mixed = mixed3(k3);
                     int lo;
                     pair3(k3, lo, hi);
+                }
+                // in place (a single domain's parities share the normal
+                // plane): it already holds the old normal, which a non-mixed
+                // cell keeps, so only mixed cells are read and written
+                const bool inplace = d.nrx == d.nnrx;
+                double nrx = 0.0, nry = 0.0;
+                if (mixed || !inplace) {
+                    nrx = d.nrx[c];
+                    nry = d.nry[c];
                 }
                 if (mixed) {
                     const double* kh = d.nk[hi];
@@ -2811,8 +2839,10 @@ __global__ void __launch_bounds__(256, 5) k_post(Dev d, int run_loop) {
                         nry = gy / g;
                     }
                 }
-                d.nnrx[c] = nrx;
-                d.nnry[c] = nry;
+                if (mixed || !inplace) {
+                    d.nnrx[c] = nrx;
+                    d.nnry[c] = nry;
+                }
             }
             if (run_loop && own_cell(d, i, j)) {
                 if (!isfinite(m) | !isfinite(emix) | !isfinite(p)) raise(d.ctl, ekey(PH_NAN_CELL, j, i, 0));

@@ -8,7 +8,7 @@ import bench  # noqa: E402
 import paper_2208_13409_b200 as pkg  # noqa: E402
 
 name, q = sys.argv[1], int(sys.argv[2])
-case = bench.workload(name)
+case = bench.workload("c5", full=False) if name == "c5b" else bench.workload(name)
 s = pkg.solver(case.cfg)
 s.init_from(case.paint())
 if q:
