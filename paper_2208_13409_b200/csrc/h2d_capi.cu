@@ -755,8 +755,10 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     };
     d.sliver = bytes_plane();
     for (int q = 0; q < 4; ++q) d.dflag[q] = bytes_plane();
-    d.sl_segs = reinterpret_cast<unsigned*>(bytes_plane());  // >= R*P/8 bytes needed
+    d.sl_segs = reinterpret_cast<unsigned*>(bytes_plane());  // two bitmaps of <= R*(P/8+4) bytes each
+    d.sl_segs2 = d.sl_segs + c->fsz / 8;                     // (the second at byte fsz/2 of the plane)
     d.sl_list = reinterpret_cast<int*>(bytes_plane());       // 4 byte planes: one int per cell
+    d.sl_cap = (int)c->fsz;
     for (int q = 0; q < 3; ++q) (void)bytes_plane();
     d.sl_rows = reinterpret_cast<unsigned*>(c->arena + c->arena_used);
     c->arena_used += ((size_t)c->R * 4 + 255) & ~size_t(255);

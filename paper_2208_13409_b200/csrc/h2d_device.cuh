@@ -97,6 +97,10 @@ struct Ctl {
     double* diag_log;
     int diag_log_cap;
     int pad3_;
+    // sliver rounds (k_sliver_list / k_sliver_round / k_sliver_tail)
+    int sl_n;                 // pending slivers listed this step
+    int sl_on;                // the parallel rounds run (not periodic, list fits)
+    int sl_cnt[8];            // slivers applied per round
 };
 
 // StepDiag + Totals (harness.hpp:66-72, state.hpp:93-98) slots of Ctl::dg
@@ -194,7 +198,10 @@ struct Dev {
     // sliver index: bit (i - r_gath.i0) of word [(j - r_gath.j0) * nwx + (i - r_gath.i0) / 32]
     // in sl_segs, bit (j - r_gath.j0) % 32 of sl_rows[(j - r_gath.j0) / 32]; cleared as consumed
     unsigned *sl_rows, *sl_segs;
-    int* sl_list;  // the pending slivers in the reference order (k_slivers), one int per cell of capacity
+    unsigned* sl_segs2;  // the second pending-set bitmap of the sliver rounds (k_sliver_round)
+    int* sl_list;  // the pending slivers in the reference order (k_sliver_list), sl_cap ints: [0, cap/4) the
+                   // list, [cap/4, cap/2) the tail list, then one status byte per list entry
+    int sl_cap;
     Ctl* ctl;
     const TmaSet* tma;  // host pointer: the launch passes *tma by value (__grid_constant__)
     // block mode: the fused Lagrange kernel runs in two launches around the

@@ -1975,110 +1975,349 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int& total) {
     return r;
 }
 
+// The sliver redistribution runs in three steps (launch_remap_slivers):
+//  1. k_sliver_list (one block): the pending slivers in the reference's
+//     row-major order, listed from the row / segment bitmaps finalize_cell
+//     set (rows compacted, per-row counts scanned, positions written); the
+//     segment bitmap stays set: it is the pending set P_0 of step 2.
+//  2. k_sliver_round r = 0 .. kSlRounds-1 (whole GPU): a sliver reads and
+//     writes only cells within Chebyshev distance 2 of its own cell (its two
+//     candidate rings, remap.cpp:200-216, or the cell itself, :217-225), so
+//     two slivers further than 4 apart never touch a common cell. A pending
+//     sliver with no EARLIER pending sliver within distance 4 (the bitmap P_r
+//     of the slivers still pending) sees exactly the values the reference's
+//     sequential loop would show it -- every earlier sliver that could change
+//     them is applied, no later one has run -- so all such slivers of a round
+//     are applied at once, one thread each (they are pairwise more than 4
+//     apart: of two closer ones the later is blocked by the earlier). P_{r+1}
+//     is the same set minus the round's slivers, kept in the other bitmap.
+//     Rounds stop when a round applies fewer than kSlMinProgress (a chain of
+//     dependent slivers: one per round).
+//  3. k_sliver_tail (one block): the slivers still pending, in order, are
+//     applied by one warp with the pipelined record path below (exact for a
+//     chain), and the bitmaps are cleared.
+// Periodic meshes (conflicts wrap around) and lists longer than a quarter of
+// the list capacity skip step 2.
+#ifndef H2D_SL_ROUNDS
+#define H2D_SL_ROUNDS 8
+#endif
+constexpr int kSlRounds = H2D_SL_ROUNDS, kSlMinProgress = 32, kSlGrid = 148;
+static_assert(kSlRounds <= 8, "Ctl::sl_cnt holds 8 rounds");
+
 template <int NM>
-__global__ void __launch_bounds__(SLB, 1) k_slivers(Dev d) {
+__device__ __forceinline__ void sliver_chunk_list(const Dev& d, const Rng& rg, int* s_rows, int* s_off, int* s_warp,
+                                                  int r0, int base, int& total) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int nrow = rg.j1 - rg.j0, nwx = (rg.i1 - rg.i0 + 31) >> 5;
+    constexpr int NRW = SLROWS / 32;
+    unsigned rb = 0u;
+    const int rw = (r0 >> 5) + tid;
+    if (tid < NRW && (r0 + 32 * tid) < nrow) {
+        rb = d.sl_rows[rw];
+        if (rb) d.sl_rows[rw] = 0u;
+    }
+    int nrows;
+    const int rpos = block_excl_scan(__popc(rb), s_warp, nrows);
+    for (unsigned b = rb, q = rpos; b; b &= b - 1, ++q) s_rows[q] = r0 + 32 * tid + __ffs(b) - 1;
+    __syncthreads();
+    total = 0;
+    if (nrows == 0) return;
+    // slivers per row (one warp per row), scanned into offsets
+    for (int k = wid; k < nrows; k += SLB / 32) {
+        const unsigned* seg = d.sl_segs + (size_t)s_rows[k] * nwx;
+        int cnt = 0;
+        for (int w = lane; w < nwx; w += 32) cnt += __popc(seg[w]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0) s_off[k] = cnt;
+    }
+    __syncthreads();
+    {
+        int run = 0;  // SLROWS / SLB rows per thread, scanned by blocks of consecutive rows
+        constexpr int PER = SLROWS / SLB;
+        int loc[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int k = tid * PER + q;
+            loc[q] = k < nrows ? s_off[k] : 0;
+            run += loc[q];
+        }
+        int tot;
+        int off = block_excl_scan(run, s_warp, tot);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int k = tid * PER + q;
+            if (k < nrows) s_off[k] = base + off;
+            off += loc[q];
+        }
+        total = tot;
+    }
+    __syncthreads();
+    // positions, row-major (words in order, bits in order)
+    for (int k = wid; k < nrows; k += SLB / 32) {
+        const int jr = s_rows[k];
+        const unsigned* seg = d.sl_segs + (size_t)jr * nwx;
+        int pb = s_off[k];
+        for (int w0 = 0; w0 < nwx; w0 += 32) {
+            const int w = w0 + lane;
+            unsigned bits = w < nwx ? seg[w] : 0u;
+            const int c = __popc(bits);
+            int x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            int p = pb + x - c;
+            for (; bits; bits &= bits - 1, ++p) d.sl_list[p] = jr * (rg.i1 - rg.i0) + (w << 5) + __ffs(bits) - 1;
+            pb += __shfl_sync(0xffffffffu, x, 31);
+        }
+    }
+    __syncthreads();
+}
+
+template <int NM>
+__global__ void __launch_bounds__(SLB, 1) k_sliver_list(Dev d) {
     pdl_enter();
-    __shared__ int s_halt, s_total;
+    __shared__ int s_halt;
     __shared__ int s_rows[SLROWS], s_off[SLROWS];
+    __shared__ int s_warp[64];
+    if (threadIdx.x == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
+    const Rng rg = d.r_gath;
+    const int nrow = rg.j1 - rg.j0;
+    int n = 0;
+    for (int r0 = 0; r0 < nrow; r0 += SLROWS) {
+        int t;
+        sliver_chunk_list<NM>(d, rg, s_rows, s_off, s_warp, r0, n, t);
+        n += t;
+    }
+    if (threadIdx.x == 0) {
+        Ctl* c = d.ctl;
+        c->sl_n = n;
+        c->sl_on = !(d.per_x || d.per_y || n > d.sl_cap / 4);
+        for (int q = 0; q < kSlRounds; ++q) c->sl_cnt[q] = 0;
+    }
+}
+
+__device__ __forceinline__ uint8_t* sl_status(const Dev& d) {
+    return reinterpret_cast<uint8_t*>(d.sl_list + d.sl_cap / 2);
+}
+__device__ __forceinline__ int* sl_tail(const Dev& d) { return d.sl_list + d.sl_cap / 4; }
+__device__ __forceinline__ unsigned* sl_bits(const Dev& d, int r) { return (r & 1) ? d.sl_segs2 : d.sl_segs; }
+
+// any pending sliver EARLIER than (jr, ir) in row-major order within
+// Chebyshev distance 4 (rows jr-4 .. jr-1: columns ir-4 .. ir+4; row jr:
+// ir-4 .. ir-1), in the bitmap P
+__device__ __forceinline__ bool sl_blocked(const unsigned* P, int nwx, int W, int jr, int ir) {
+    // the window spans at most two words per row: all ten loads issue together
+    const int c0 = ir - 4 < 0 ? 0 : ir - 4, c1u = ir + 4 < W - 1 ? ir + 4 : W - 1;
+    const int w0 = c0 >> 5;
+    unsigned acc = 0u;
+#pragma unroll
+    for (int dq = 4; dq >= 0; --dq) {
+        const int q = jr - dq;
+        const int c1 = dq ? c1u : ir - 1;
+        if (q < 0 || c1 < c0) continue;
+        const int w1 = c1 >> 5;
+        const unsigned lo = c0 & 31;
+        const unsigned hi0 = w1 == w0 ? (c1 & 31) : 31;
+        acc |= __ldcg(P + (size_t)q * nwx + w0) & (0xffffffffu >> (31 - hi0)) & (0xffffffffu << lo);
+        if (w1 != w0) acc |= __ldcg(P + (size_t)q * nwx + w1) & (0xffffffffu >> (31 - (c1 & 31)));
+    }
+    return acc != 0u;
+}
+
+// candidates L0 .. L1-1 of a sliver at (si, sj) for material a: all loads
+// issued together, then the first strict maximum of k among m > 0
+template <int L0, int L1>
+__device__ __forceinline__ void sliver_scan(const Dev& d, const Rng& rg, int a, int si, int sj, int& best, double& bk,
+                                            double& bm) {
+    double mv[L1 - L0], kv[L1 - L0];
+    int nc[L1 - L0];
+#pragma unroll
+    for (int q = 0; q < L1 - L0; ++q) {
+        int di, dj, ring;
+        sliver_offset(L0 + q, di, dj, ring);
+        const int ni = si + di, nj = sj + dj;
+        const bool ok = ni >= 0 && ni < d.nx && nj >= 0 && nj < d.ny && in(rg, ni, nj);
+        nc[q] = ok ? ix(d, ni, nj) : -1;
+        mv[q] = ok ? d.nm[a][nc[q]] : 0.0;
+        kv[q] = ok ? d.nk[a][nc[q]] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < L1 - L0; ++q)
+        if (nc[q] >= 0 && !(mv[q] <= 0.0) && (best < 0 || kv[q] > bk)) {
+            best = nc[q];
+            bk = kv[q];
+            bm = mv[q];
+        }
+}
+
+// One pending record (cell v of the list, every flagged material, a = 0
+// first as the reference pushes them, remap.cpp:170-181) applied by ONE
+// thread: the candidate scan of remap.cpp:200-216 (ring 1 before ring 2,
+// row-major inside a ring, first strict maximum of k among m > 0), the
+// carrier update, else the partner material at the sliver's own cell.
+template <int NM>
+__device__ __forceinline__ void sliver_apply_thread(const Dev& d, const Rng& rg, int v) {
+    const int W = rg.i1 - rg.i0;
+    const int sj = rg.j0 + v / W, si = rg.i0 + v % W;
+    const int c = ix(d, si, sj);
+    const int fl = d.sliver[c];
+    const bool own = own_cell(d, si, sj);
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
+        if (!(fl & (1 << a))) continue;
+        const double smv = d.slm[a][c], smev = d.slme[a][c];
+        // ring 1 (8 candidates), then ring 2 (16) only if ring 1 had none:
+        // each ring's loads are issued together (no dependent chain)
+        int best = -1;
+        double bk = 0.0, bm = 0.0;
+        sliver_scan<0, 8>(d, rg, a, si, sj, best, bk, bm);
+        if (best < 0) sliver_scan<8, 24>(d, rg, a, si, sj, best, bk, bm);
+        if (best >= 0 && bm + smv > 0.0) {  // the carrier takes the sliver (remap.cpp:212-216)
+            const double nm = bm + smv, nme = d.me[a][best] + smev;
+            d.nm[a][best] = nm;
+            d.me[a][best] = nme;
+            d.ne[a][best] = nme / nm;
+            d.mcell[best] = d.mcell[best] + smv;
+        } else {  // no carrier: the partner material at the sliver's own cell (:217-225)
+            int pa = 1 - a;
+            if (NM == 3) {
+                const double k3[3] = {d.nk[0][c], d.nk[1][c], d.nk[NM - 1][c]};
+                pa = largest_other3(k3, a);
+            }
+            if (own) atomicAdd(&d.ctl->step_fix, 1);
+            const double nm = d.nm[pa][c] + smv, nme = d.me[pa][c] + smev;
+            d.nm[pa][c] = nm;
+            d.me[pa][c] = nme;
+            d.ne[pa][c] = nme / nm;
+            d.mcell[c] = d.mcell[c] + smv;
+        }
+    }
+}
+
+// round r runs when the rounds are on and every earlier round applied at
+// least kSlMinProgress slivers (a round that did not run counted none)
+__device__ __forceinline__ bool sl_round_runs(const Ctl* c, int r) {
+    return __ldcg(&c->sl_on) && (r == 0 || __ldcg(&c->sl_cnt[r - 1]) >= kSlMinProgress);
+}
+
+template <int NM>
+__global__ void __launch_bounds__(256) k_sliver_round(Dev d, int r) {
+    pdl_enter();
+    const Ctl* cc = d.ctl;
+    if (halted(cc)) return;
+    const int n = __ldcg(&cc->sl_n);
+    if (!sl_round_runs(cc, r) || n == 0) return;
+    const Rng rg = d.r_gath;
+    const int W = rg.i1 - rg.i0, nwx = (W + 31) >> 5;
+    const unsigned* P = sl_bits(d, r);
+    unsigned* Q = sl_bits(d, r + 1);  // P_{r-1} -> P_{r+1}
+    uint8_t* st = sl_status(d);
+    int applied = 0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int v = d.sl_list[k];
+        const int jr = v / W, ir = v % W;
+        unsigned* qw = Q + (size_t)jr * nwx + (ir >> 5);
+        const unsigned bit = 1u << (ir & 31);
+        const int s = r == 0 ? 0xff : st[k];
+        if (s != 0xff) {
+            if (s == r - 1) atomicAnd(qw, ~bit);  // applied last round: leaves P_{r+1}
+            continue;
+        }
+        if (sl_blocked(P, nwx, W, jr, ir)) {
+            st[k] = 0xff;
+            if (r == 0) atomicOr(qw, bit);  // pending into P_1
+            continue;
+        }
+        sliver_apply_thread<NM>(d, rg, v);
+        st[k] = (uint8_t)r;
+        if (r > 0) atomicAnd(qw, ~bit);
+        ++applied;
+    }
+    const int tot = __reduce_add_sync(0xffffffffu, applied);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&d.ctl->sl_cnt[r], tot);
+}
+
+template <int NM>
+__global__ void __launch_bounds__(SLB, 1) k_sliver_tail(Dev d) {
+    pdl_enter();
+    __shared__ int s_halt, s_n;
     __shared__ int s_warp[64];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) s_halt = halted(d.ctl);
     __syncthreads();
     if (s_halt) return;
     const Rng rg = d.r_gath;
-    const int nrow = rg.j1 - rg.j0, nwx = (rg.i1 - rg.i0 + 31) >> 5;
-    int di = 0, dj = 0, ring = 3;
-    if (lane < 24) sliver_offset(lane, di, dj, ring);
-    for (int r0 = 0; r0 < nrow; r0 += SLROWS) {
-        // (1) rows of this chunk holding slivers, in order
-        constexpr int NRW = SLROWS / 32;
-        unsigned rb = 0u;
-        const int rw = (r0 >> 5) + tid;
-        if (tid < NRW && (r0 + 32 * tid) < nrow) {
-            rb = d.sl_rows[rw];
-            if (rb) d.sl_rows[rw] = 0u;
-        }
-        int nrows;
-        const int rpos = block_excl_scan(__popc(rb), s_warp, nrows);
-        for (unsigned b = rb, q = rpos; b; b &= b - 1, ++q) s_rows[q] = r0 + 32 * tid + __ffs(b) - 1;
-        __syncthreads();
-        if (nrows == 0) continue;
-        // (2) slivers per row (one warp per row), (3) scanned into offsets
-        for (int k = wid; k < nrows; k += SLB / 32) {
-            const unsigned* seg = d.sl_segs + (size_t)s_rows[k] * nwx;
-            int cnt = 0;
-            for (int w = lane; w < nwx; w += 32) cnt += __popc(seg[w]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-            if (lane == 0) s_off[k] = cnt;
-        }
-        __syncthreads();
-        {
-            int run = 0;  // SLROWS / SLB rows per thread, scanned by blocks of consecutive rows
-            constexpr int PER = SLROWS / SLB;
-            int loc[PER];
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int k = tid * PER + q;
-                loc[q] = k < nrows ? s_off[k] : 0;
-                run += loc[q];
-            }
-            int tot;
-            int base = block_excl_scan(run, s_warp, tot);
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const int k = tid * PER + q;
-                if (k < nrows) s_off[k] = base;
-                base += loc[q];
-            }
-            if (tid == 0) s_total = tot;
-        }
-        __syncthreads();
-        // (4) positions, row-major (words in order, bits in order), words cleared
-        for (int k = wid; k < nrows; k += SLB / 32) {
-            const int jr = s_rows[k];
-            unsigned* seg = d.sl_segs + (size_t)jr * nwx;
-            int base = s_off[k];
-            for (int w0 = 0; w0 < nwx; w0 += 32) {
-                const int w = w0 + lane;
-                unsigned bits = w < nwx ? seg[w] : 0u;
-                if (bits) seg[w] = 0u;
-                const int c = __popc(bits);
-                int x = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
-                int p = base + x - c;
-                for (; bits; bits &= bits - 1, ++p) d.sl_list[p] = jr * (rg.i1 - rg.i0) + (w << 5) + __ffs(bits) - 1;
-                base += __shfl_sync(0xffffffffu, x, 31);
+    const int W = rg.i1 - rg.i0, nwx = (W + 31) >> 5;
+    const int n = d.ctl->sl_n;
+    int last = -1;  // the last round that ran
+    while (last + 1 < kSlRounds && sl_round_runs(d.ctl, last + 1)) ++last;
+    const bool rounds = last >= 0;
+    const uint8_t* st = sl_status(d);
+    // the pending records, in order, and the bitmaps cleared: P_last holds the
+    // records pending at round `last`, P_{last+1} those pending after it
+    const int* list = d.sl_list;
+    int np = n;
+    if (rounds) {
+        int* tl = sl_tail(d);
+        const int per = (n + SLB - 1) / SLB, k0 = tid * per, k1 = min(n, k0 + per);
+        int cnt = 0;
+        for (int k = k0; k < k1; ++k) cnt += st[k] == 0xff;
+        int tot;
+        int pos = block_excl_scan(cnt, s_warp, tot);
+        unsigned* Pa = sl_bits(d, last);
+        unsigned* Pb = sl_bits(d, last + 1);
+        for (int k = k0; k < k1; ++k) {
+            const int s = st[k];
+            if (s != 0xff && s != last) continue;
+            const int v = d.sl_list[k];
+            const int jr = v / W, ir = v % W;
+            const size_t wq = (size_t)jr * nwx + (ir >> 5);
+            const unsigned bit = 1u << (ir & 31);
+            atomicAnd(Pa + wq, ~bit);
+            if (s == 0xff) {
+                atomicAnd(Pb + wq, ~bit);
+                tl[pos++] = v;
             }
         }
+        if (tid == 0) s_n = tot;
         __syncthreads();
-        // (5) one warp applies them in order, SLD records in flight
-        if (wid == 0) {
-            const int n = s_total;
-            SliverRec<NM> r0v, r1v, r2v, r3v;
-            if (0 < n) sliver_load(d, rg, d.sl_list[0], lane, di, dj, r0v);
-            if (1 < n) sliver_load(d, rg, d.sl_list[1], lane, di, dj, r1v);
-            if (2 < n) sliver_load(d, rg, d.sl_list[2], lane, di, dj, r2v);
-            if (3 < n) sliver_load(d, rg, d.sl_list[3], lane, di, dj, r3v);
-            for (int k = 0; k < n; k += SLD) {
-                sliver_apply_rec(d, r0v, lane, ring, r1v, r2v, r3v);
-                if (k + 4 < n) sliver_load(d, rg, d.sl_list[k + 4], lane, di, dj, r0v);
-                if (k + 1 >= n) break;
-                sliver_apply_rec(d, r1v, lane, ring, r2v, r3v, r0v);
-                if (k + 5 < n) sliver_load(d, rg, d.sl_list[k + 5], lane, di, dj, r1v);
-                if (k + 2 >= n) break;
-                sliver_apply_rec(d, r2v, lane, ring, r3v, r0v, r1v);
-                if (k + 6 < n) sliver_load(d, rg, d.sl_list[k + 6], lane, di, dj, r2v);
-                if (k + 3 >= n) break;
-                sliver_apply_rec(d, r3v, lane, ring, r0v, r1v, r2v);
-                if (k + 7 < n) sliver_load(d, rg, d.sl_list[k + 7], lane, di, dj, r3v);
-            }
+        np = s_n;
+        list = tl;
+    } else {
+        for (int k = tid; k < n; k += SLB) {
+            const int v = d.sl_list[k];
+            const int jr = v / W, ir = v % W;
+            atomicAnd(d.sl_segs + (size_t)jr * nwx + (ir >> 5), ~(1u << (ir & 31)));
         }
-        __syncthreads();
+    }
+    __syncthreads();
+    // one warp applies the remaining records in order, SLD records in flight
+    if (wid == 0 && np > 0) {
+        int di = 0, dj = 0, ring = 3;
+        if (lane < 24) sliver_offset(lane, di, dj, ring);
+        SliverRec<NM> r0v, r1v, r2v, r3v;
+        if (0 < np) sliver_load(d, rg, list[0], lane, di, dj, r0v);
+        if (1 < np) sliver_load(d, rg, list[1], lane, di, dj, r1v);
+        if (2 < np) sliver_load(d, rg, list[2], lane, di, dj, r2v);
+        if (3 < np) sliver_load(d, rg, list[3], lane, di, dj, r3v);
+        for (int k = 0; k < np; k += SLD) {
+            sliver_apply_rec(d, r0v, lane, ring, r1v, r2v, r3v);
+            if (k + 4 < np) sliver_load(d, rg, list[k + 4], lane, di, dj, r0v);
+            if (k + 1 >= np) break;
+            sliver_apply_rec(d, r1v, lane, ring, r2v, r3v, r0v);
+            if (k + 5 < np) sliver_load(d, rg, list[k + 5], lane, di, dj, r1v);
+            if (k + 2 >= np) break;
+            sliver_apply_rec(d, r2v, lane, ring, r3v, r0v, r1v);
+            if (k + 6 < np) sliver_load(d, rg, list[k + 6], lane, di, dj, r2v);
+            if (k + 3 >= np) break;
+            sliver_apply_rec(d, r3v, lane, ring, r0v, r1v, r2v);
+            if (k + 7 < np) sliver_load(d, rg, list[k + 7], lane, di, dj, r3v);
+        }
     }
 }
 
@@ -3650,10 +3889,15 @@ __global__ void k_energy_fix(Dev d) {
 }
 
 void launch_remap_slivers(const Dev& d, cudaStream_t s) {
-    if (d.nmat == 3)
-        pdl(k_slivers<3>, dim3(1), dim3(SLB), 0, s, d);
-    else if (d.nmat == 2)
-        pdl(k_slivers<2>, dim3(1), dim3(SLB), 0, s, d);
+    if (d.nmat == 3) {
+        pdl(k_sliver_list<3>, dim3(1), dim3(SLB), 0, s, d);
+        for (int r = 0; r < kSlRounds; ++r) pdl(k_sliver_round<3>, dim3(kSlGrid), dim3(256), 0, s, d, r);
+        pdl(k_sliver_tail<3>, dim3(1), dim3(SLB), 0, s, d);
+    } else if (d.nmat == 2) {
+        pdl(k_sliver_list<2>, dim3(1), dim3(SLB), 0, s, d);
+        for (int r = 0; r < kSlRounds; ++r) pdl(k_sliver_round<2>, dim3(kSlGrid), dim3(256), 0, s, d, r);
+        pdl(k_sliver_tail<2>, dim3(1), dim3(SLB), 0, s, d);
+    }
     if (d.opt_energy) {
         if (d.nmat == 3)
             pdl(k_energy_fix<3>, grid_of(d.r_gath), blk2(), 0, s, d);
