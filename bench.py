@@ -365,7 +365,7 @@ def run_product(args, world, rank, local, pg):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (init_case-equivalent painter, seeded)",
         "config": config_of(case, args.remap, world),
         "phases_ms": dict(ph, note=f"{n_ph} un-graphed steps after the timed ones, CUDA events between "
@@ -508,7 +508,7 @@ def run_reference(args, world, rank, pg):
     v, ckind, n, secs = time_cpu(sc, warm, steps, rk)
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n, "warmup": warm,
-        "ms_per_step": secs * 1e3 / max(n, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": secs * 1e3 / max(n, 1), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (init_case-equivalent painter, seeded)", "impl": "reference",
         "config": config_of(case, args.remap, 1),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": ckind, "cpu": cpu_model(),

@@ -678,6 +678,7 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
     d.nx = m.nx;
     d.ny = m.ny;
     d.P = c->P;
+    d.fsz = (int)c->fsz;
     d.oi = blk->oi;
     d.oj = blk->oj;
     d.H = H;

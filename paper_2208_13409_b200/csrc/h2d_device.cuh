@@ -10,6 +10,16 @@
 #include <cuda.h>  // CUtensorMap (the type only; maps are encoded through the runtime's driver entry point)
 #include <math_constants.h>
 #include <cfloat>
+#ifdef H2D_CHECKED
+// checked build (tools/variants.py build checked -DH2D_CHECKED): every plane
+// index, shared-memory tile index and sliver-list slot is bounds-checked on
+// the device (assert -> cudaErrorAssert); the substitute for compute-sanitizer
+// memcheck, which this pool does not run
+#include <cassert>
+#define H2D_CHECK(x) assert(x)
+#else
+#define H2D_CHECK(x) ((void)0)
+#endif
 
 #define H2D_DEV __device__ __forceinline__
 
@@ -212,11 +222,16 @@ struct Dev {
     int scan_nodes;     // run loop: the node update also runs nan_scan's node part (harness.cpp:353-357)
     int diag;           // run loop: reduce the step's make_diag values (k_post cells, node update momentum)
     DiagScratch dsc;    // diagnostics block partials ([0] k_post, [1] node update) + k_diag_reduce scratch
+    int fsz;            // doubles per plane (P * R; the bound H2D_CHECKED tests plane indices against)
 };
 
 // 32-bit plane offsets: P * R < 2^31 for every mesh up to 16384^2 (checked at
 // context creation), which halves the index arithmetic of the stencils.
-H2D_DEV int ix(const Dev& d, int i, int j) { return j * d.P + i + d.off; }
+H2D_DEV int ix(const Dev& d, int i, int j) {
+    const int q = j * d.P + i + d.off;
+    H2D_CHECK(q >= 0 && q < d.fsz);
+    return q;
+}
 H2D_DEV bool in(const Rng& r, int i, int j) { return i >= r.i0 && i < r.i1 && j >= r.j0 && j < r.j1; }
 
 H2D_DEV double div_dx(const Dev& d, double x, double k) {  // x / (k * dx), k a power of two

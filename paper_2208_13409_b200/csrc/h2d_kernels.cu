@@ -801,8 +801,14 @@ struct Tile {
     // flux items of one sub-phase (X faces, then Y faces, then corners share
     // the buffer): dm, dme, dva per material
     double* it[3][kMatSlots];
-    __device__ __forceinline__ int c(int i, int j) const { return (i - ci0) + (j - cj0) * RCW; }
-    __device__ __forceinline__ int n(int i, int j) const { return (i - ci0) + (j - cj0) * RNW; }
+    __device__ __forceinline__ int c(int i, int j) const {
+        H2D_CHECK(i - ci0 >= 0 && i - ci0 < RCW && j - cj0 >= 0 && j - cj0 < RCH);
+        return (i - ci0) + (j - cj0) * RCW;
+    }
+    __device__ __forceinline__ int n(int i, int j) const {
+        H2D_CHECK(i - ci0 >= 0 && i - ci0 < RNW && j - cj0 >= 0 && j - cj0 < RNH);
+        return (i - ci0) + (j - cj0) * RNW;
+    }
     // cf_corner_flux (remap.cpp:16-25) at region node q, recomputed from the
     // staged u_half (zero outside the window); sx / sy are meaningful only
     // when the returned volume is nonzero
@@ -1445,6 +1451,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // DIR: the Direct engine (remap.cpp:593-724): face volumes fd * width, the
 // X / Y-displaced interfaces, no corner fluxes (items and dmc zero)
 template <int NM, bool XC = false, bool DIR = false>
+#ifndef H2D_RT_SPLITBAR
+#define H2D_RT_SPLITBAR 0
+#endif
 #ifndef H2D_RT_MINB1
 #define H2D_RT_MINB1 4
 #endif
@@ -1458,7 +1467,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     pdl_enter();
     extern __shared__ __align__(128) char smem_raw[];
     __shared__ int s_halt;
-    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ __align__(8) uint64_t s_bar, s_bar2;
     const int tid = threadIdx.x;
     const int nx = d.nx, ny = d.ny;
     const Rng rg = d.r_gath;
@@ -1480,18 +1489,25 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     // block's load latency overlaps them (a halted step waits for its copies
     // before the CTA exits: its shared memory must not be handed on while a
     // copy is still writing it).
+    // H2D_RT_SPLITBAR: the node planes complete one mbarrier, the cell planes
+    // a second, so the quiescent test and phase 1 start before the cell
+    // planes have landed
+    constexpr bool kSplit = H2D_RT_SPLITBAR != 0;
+    uint64_t* bar_c = kSplit ? &s_bar2 : &s_bar;
     if (tid == 0) {
         mbar_init(&s_bar, 1);
-        constexpr uint32_t bytes = 2u * RNW * RNH * 8u + 3u * NM * RCW * RCH * 8u;
+        if (kSplit) mbar_init(&s_bar2, 1);
+        constexpr uint32_t nbytes = 2u * RNW * RNH * 8u, cbytes = 3u * NM * RCW * RCH * 8u;
         const int x = T.ci0 + d.H - d.oi, y = T.cj0 + d.H - d.oj;  // plane column / row of the region origin
-        mbar_expect_tx(&s_bar, bytes);
+        mbar_expect_tx(&s_bar, kSplit ? nbytes : nbytes + cbytes);
         tma_load_2d(T.hx, &tm.t[TM_UHX], x, y, &s_bar);
         tma_load_2d(T.hy, &tm.t[TM_UHY], x, y, &s_bar);
+        if (kSplit) mbar_expect_tx(bar_c, cbytes);
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
-            tma_load_2d(T.el[a], &tm.t[TM_EL0 + a], x, y, &s_bar);
-            tma_load_2d(T.rho[a], &tm.t[TM_M0 + a], x, y, &s_bar);
-            tma_load_2d(NM >= 2 ? T.kk[a] : T.vl, &tm.t[TM_K0 + a], x, y, &s_bar);
+            tma_load_2d(T.el[a], &tm.t[TM_EL0 + a], x, y, bar_c);
+            tma_load_2d(T.rho[a], &tm.t[TM_M0 + a], x, y, bar_c);
+            tma_load_2d(NM >= 2 ? T.kk[a] : T.vl, &tm.t[TM_K0 + a], x, y, bar_c);
         }
         s_halt = halted(d.ctl);
     }
@@ -1499,7 +1515,10 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     const double cv = d.cv;
     __syncthreads();
     if (s_halt) {
-        if (tid == 0) mbar_wait(&s_bar, 0);
+        if (tid == 0) {
+            mbar_wait(&s_bar, 0);
+            if (kSplit) mbar_wait(bar_c, 0);
+        }
         return;
     }
     mbar_wait(&s_bar, 0);
@@ -1520,6 +1539,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
             }
         }
         if (!__syncthreads_or(moving)) {
+            if (kSplit) mbar_wait(bar_c, 0);
             const int ni1 = min(nx, rg.i1), nj1 = min(ny, rg.j1);
             RowCol<RTX + 1, RTX * RTY> rz(tid);
             for (int t = tid; t < NCF; t += RTX * RTY, rz.step()) {
@@ -1591,6 +1611,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
         T.fydv[t] = fyv;
     }
     __syncthreads();
+    if (kSplit) mbar_wait(bar_c, 0);
     // ---- phase 2, cell items: Lagrangian volume, densities, centroids,
     // interfaces (remap.cpp:769-824)
     RowCol<RCW, RTX * RTY> rs3(tid);
@@ -1660,7 +1681,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     const int tx = tid % RTX, ty = tid / RTX;
     const int i = i0 + tx, j = j0 + ty;
     const bool act = in(rg, i, j);
-    const int c = ix(d, i, j);
+    const int c = act ? ix(d, i, j) : 0;
     const int tc = T.c(i, j);
     double m[NM], me[NM], va[NM];
     if (act) {
@@ -1670,7 +1691,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
             const double m0 = d.m[a][c];
             m[a] = m0;
             me[a] = m0 * T.el[a][tc];
-            va[a] = d.k[a][c] * vl;
+            va[a] = (NM >= 2 ? T.kk[a][tc] : d.k[a][c]) * vl;  // (T.kk: the staged k, unchanged)
         }
     }
     auto add = [&](int a, int q, bool neg) {  // the skip of remap.cpp:860,929
@@ -2069,7 +2090,10 @@ __device__ __forceinline__ void sliver_chunk_list(const Dev& d, const Rng& rg, i
                 if (lane >= o) x += y;
             }
             int p = pb + x - c;
-            for (; bits; bits &= bits - 1, ++p) d.sl_list[p] = jr * (rg.i1 - rg.i0) + (w << 5) + __ffs(bits) - 1;
+            for (; bits; bits &= bits - 1, ++p) {
+                H2D_CHECK(p < d.sl_cap);
+                d.sl_list[p] = jr * (rg.i1 - rg.i0) + (w << 5) + __ffs(bits) - 1;
+            }
             pb += __shfl_sync(0xffffffffu, x, 31);
         }
     }
@@ -2997,10 +3021,16 @@ __global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop
     unsigned long long wb = 0ull;
     const bool act = in(d.r_sync, i, j);
     const bool interior = i >= 0 && j >= 0 && i < nx && j < ny;
-    const int c = ix(d, i, j);
+    const int c = act ? ix(d, i, j) : 0;
     const double cv = d.cv;
     double ka[NM], ma[NM], ea[NM];
     double m = 0.0, emix = 0.0, p = 0.0;
+    // the next step's sound speed (cfl_dt, harness.cpp:293-313) comes out of
+    // the same per-material loop as the mixture pressure: the materials with
+    // k >= kThermoTol, in index order, from the same rho_a and p_a (the
+    // wave-speed block below only adds |u|)
+    double cs = 0.0;
+    bool cs_bad = false;
     if (act) {
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
@@ -3016,7 +3046,9 @@ __global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop
             me += ma[a] * ea[a];
             if (ka[a] < kThermoTol) continue;
             const double rho_a = rho_of(d, ma[a], ka[a]);
-            p += ka[a] * eos_p(d, a, rho_a, ea[a]);
+            const double pa = eos_p(d, a, rho_a, ea[a]);
+            p += ka[a] * pa;
+            if (run_loop) cs += ka[a] * sound(d, a, rho_a, pa, cs_bad);
         }
         emix = m > 0.0 ? me / m : 0.0;
         if (!run_loop) {  // the run loop keeps no derived planes (rebuilt when the State is read)
@@ -3085,17 +3117,8 @@ __global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop
             }
             if (run_loop && own_cell(d, i, j)) {
                 if (!isfinite(m) | !isfinite(emix) | !isfinite(p)) raise(d.ctl, ekey(PH_NAN_CELL, j, i, 0));
-                // next step's wave speed on the new State
-                double cs = 0.0;
-                bool bad = false;
-#pragma unroll
-                for (int a = 0; a < NM; ++a) {
-                    if (ka[a] < kThermoTol) continue;
-                    const double rho_a = rho_of(d, ma[a], ka[a]);
-                    const double pa = eos_p(d, a, rho_a, ea[a]);
-                    cs += ka[a] * sound(d, a, rho_a, pa, bad);
-                }
-                if (bad) atomicMin(&d.ctl->next_err_key, ekey(PH_CFL_UNPHYS, j, i, 0));
+                // next step's wave speed on the new State (cs from above)
+                if (cs_bad) atomicMin(&d.ctl->next_err_key, ekey(PH_CFL_UNPHYS, j, i, 0));
                 double umax = 0.0;
 #pragma unroll
                 for (int dj = 0; dj <= 1; ++dj)

@@ -16,7 +16,7 @@ from paper_2208_13409_b200.abi import GHOST, HostLagrange, HostState, Solver
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_LIB = os.path.join(ROOT, "oracle", "libh2d_oracle.so")
 REF_LIB = os.path.join(ROOT, "oracle", "_ref", "libh2d_ref.so")
-PRODUCT_LIB = os.path.join(ROOT, "paper_2208_13409_b200", "libh2d.so")
+PRODUCT_LIB = os.environ.get("H2D_PRODUCT_LIB") or os.path.join(ROOT, "paper_2208_13409_b200", "libh2d.so")
 
 STATE_FIELDS = ("m", "e", "k", "vol", "m_mix", "e_mix", "rho_mix", "p_mix", "iface_normal", "u")
 LAG_FIELDS = ("u_half", "u_lag", "e_lag", "vol_lag", "q")
