@@ -1452,7 +1452,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // X / Y-displaced interfaces, no corner fluxes (items and dmc zero)
 template <int NM, bool XC = false, bool DIR = false>
 #ifndef H2D_RT_SPLITBAR
-#define H2D_RT_SPLITBAR 0
+#define H2D_RT_SPLITBAR 1
 #endif
 #ifndef H2D_RT_MINB1
 #define H2D_RT_MINB1 4
