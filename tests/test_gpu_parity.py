@@ -1,5 +1,8 @@
-"""Parity of the CUDA product (libh2d.so, through the C-ABI) against the C
-restatement oracle, which is itself pinned to the reference
+"""Parity of the CUDA product (libh2d.so, through the C-ABI) against the
+REFERENCE library itself (oracle/_ref, h2dr_, built from /root/reference and
+shipped to the GPU box) wherever it can hold the case (at most two
+materials, no build option of this product), else against the C
+restatement oracle, which is pinned bit for bit to the reference
 (test_oracle_vs_reference.py).  The bar is bit-exact: every State and
 LagrangeResult byte, every dt, the mixed-cell set, the RemapDiag counters,
 floor counts and the first located error."""
@@ -16,8 +19,14 @@ from paper_2208_13409_b200.abi import BC_PERIODIC, BC_WALL, CORNER_LINEARDIAG, C
 pytestmark = pytest.mark.gpu
 
 
+def _checker(orc, cfg):
+    """The reference itself when it can run the case, else the oracle."""
+    ref = helpers.ref_lib()
+    return ref if ref is not None and cfg.nmat <= 2 and not getattr(cfg, "options", 0) else orc
+
+
 def _pair(gpu, orc, cfg, painted):
-    return helpers.prepared(gpu, cfg, painted), helpers.prepared(orc, cfg, painted)
+    return helpers.prepared(gpu, cfg, painted), helpers.prepared(_checker(orc, cfg), cfg, painted)
 
 
 def test_init_helpers(gpu, orc):
