@@ -61,6 +61,7 @@ struct h2d_ctx {
     void* flush = nullptr;
     size_t flush_bytes = 0;
     void* diag_mem = nullptr;       // DiagRed scratch of k_post / the node update
+    void* tcls_mem = nullptr;       // Dev::tcls, the remap tiles' material classes
     size_t diag_tick_bytes = 0;     // the ticket words at the start of diag_mem
     double* diag_log = nullptr;     // device StepDiag log of h2d_run (kDiagRec doubles per step)
     cudaGraphExec_t graph_rest[2] = {nullptr, nullptr};  // block data plane: the step after the Lagrange kernel
@@ -781,6 +782,18 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
         d.dsc.part[0] = pp + (size_t)kDiagBlocks * DG_N;
         d.dsc.part[1] = d.dsc.part[0] + n0 * DG_NCELL;
     }
+    {  // one class byte per remap tile (launch_remap_tile's grid; three materials)
+        const int shift = (d.r_gath.i0 - G + d.H - d.oi) & 1;  // tile_shift (h2d_kernels.cu)
+        const int w = d.r_gath.i1 - (d.r_gath.i0 - shift), h = d.r_gath.j1 - d.r_gath.j0;
+        d.tq_nx = std::max(1, (w + remap_tile_w() - 1) / remap_tile_w());
+        d.tq_ny = std::max(1, (h + remap_tile_h() - 1) / remap_tile_h());
+        if (nm == 3) {
+            const size_t n = (size_t)d.tq_nx * d.tq_ny;
+            if (cudaMalloc(&c->tcls_mem, n) != cudaSuccess) return fail(H2D_ERR_NOMEM);
+            if (cudaMemset(c->tcls_mem, 3, n) != cudaSuccess) return fail(H2D_ERR_DEVICE);
+            d.tcls = static_cast<uint8_t*>(c->tcls_mem);
+        }
+    }
     if (ctl_push(c)) return fail(H2D_ERR_DEVICE);
     // make_state defaults (state.cpp:5-23): k0 = 1, normals (1, 0), vol = dx*dy
     for (int p = 0; p < 2; ++p) {
@@ -820,6 +833,7 @@ void h2d_destroy(h2d_ctx* c) {
     if (c->dt_log) cudaFree(c->dt_log);
     if (c->diag_log) cudaFree(c->diag_log);
     if (c->diag_mem) cudaFree(c->diag_mem);
+    if (c->tcls_mem) cudaFree(c->tcls_mem);
     if (c->xbuf) cudaFree(c->xbuf);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;

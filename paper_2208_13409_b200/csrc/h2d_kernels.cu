@@ -539,6 +539,9 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
 // (lagrange.cpp:135-142, 146-196). Q, p_half and p_mix_half never leave the
 // chip; the API path (h2d_lagrange_step) keeps the two-kernel form because
 // it returns Q.
+#ifndef H2D_LAG_SMEMC
+#define H2D_LAG_SMEMC 0
+#endif
 template <int NM>
 #ifndef H2D_FTY
 #define H2D_FTY 8
@@ -550,6 +553,11 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     constexpr int CW = LTX + 2, CH = LTY + 2, NC = CW * CH, NN = (LTX + 1) * (LTY + 1);
     __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC], s_mm[NC];
     __shared__ double shx[NN], shy[NN];
+#if H2D_LAG_SMEMC
+    // the State values of the tile's cells, loaded once by the cell pass and
+    // read back by the own-cell correct
+    __shared__ double s_k[NM][NC], s_m[NM][NC], s_e[NM][NC];
+#endif
     __shared__ int s_halt;
     const int tid = threadIdx.x;
     if (tid == 0) s_halt = halted(d.ctl);
@@ -582,6 +590,11 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
                 ka[a] = d.k[a][c];
                 ma[a] = d.m[a][c];
                 en[a] = d.e[a][c];
+#if H2D_LAG_SMEMC
+                s_k[a][t] = ka[a];
+                s_m[a][t] = ma[a];
+                s_e[a][t] = en[a];
+#endif
             }
             // the State's m_mix / rho_mix (sync_derived, state.cpp:120-143) from
             // the partial masses: the run loop does not keep the derived planes
@@ -697,13 +710,31 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     const double qn = s_q[tcell];
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
+#if H2D_LAG_SMEMC
+        const double ka = s_k[a][tcell];
+        const double en = s_e[a][tcell];
+#else
+#if H2D_LAG_SMEMC
+        const double ka = s_k[a][tcell];
+        const double en = s_e[a][tcell];
+#else
         const double ka = d.k[a][n];
         const double en = d.e[a][n];
+#endif
+#endif
         double ea = 0.0;
         if (ka < kThermoTol) {
             if (ka > 0.0) ea = en;
         } else {
+#if H2D_LAG_SMEMC
+            const double ma = s_m[a][tcell];
+#else
+#if H2D_LAG_SMEMC
+            const double ma = s_m[a][tcell];
+#else
             const double ma = d.m[a][n];
+#endif
+#endif
             const double rho_n = rho_of(d, ma, ka);
             double dv = 0.0;  // vol == cv: rho_l == rho_n, the difference of inverses is +0
             if (!(vol == cv && fabs(rho_n) >= DBL_MIN)) {
@@ -1416,6 +1447,28 @@ __device__ __forceinline__ void finalize_cell(const Dev& d, const Rng& rg, int i
     }
 }
 
+// A mapped tile's cell (k_remap_tile MAP): slots 0 / 1 hold materials mat0 <
+// mat1; the absent material rabs contributes exactly what the three-material
+// gather gives it -- its m, m * e_lag and k * v, no flux -- and the cell is
+// finalised by the three-material rule (vf: the volume its k multiplies, cv on
+// the quiescent path, the Lagrangian volume otherwise)
+__device__ __forceinline__ void finalize_mapped(const Dev& d, const Rng& rg, int i, int j, int c, int tx, bool own,
+                                                const double* m2, const double* me2, const double* va2, int mat0,
+                                                int mat1, int rabs, double vf) {
+    double m[3], me[3], va[3];
+    m[mat0] = m2[0];
+    me[mat0] = me2[0];
+    va[mat0] = va2[0];
+    m[mat1] = m2[1];
+    me[mat1] = me2[1];
+    va[mat1] = va2[1];
+    const double m0 = d.m[rabs][c];
+    m[rabs] = m0;
+    me[rabs] = m0 * d.el[rabs][c];
+    va[rabs] = d.k[rabs][c] * vf;
+    finalize_cell<3>(d, rg, i, j, c, tx, own, m, me, va);
+}
+
 // plane column of the remap tiles' first region column (rg.i0 - 2) is odd
 __host__ __device__ __forceinline__ int tile_shift(const Dev& d) { return (d.r_gath.i0 - G + d.H - d.oi) & 1; }
 
@@ -1450,7 +1503,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // out-of-line calls cost the default kernels registers; see launch_remap_tile)
 // DIR: the Direct engine (remap.cpp:593-724): face volumes fd * width, the
 // X / Y-displaced interfaces, no corner fluxes (items and dmc zero)
-template <int NM, bool XC = false, bool DIR = false>
+// MAP (NM = 2 only): a three-material context's tile whose staged region
+// holds at most two materials (k_tile_class): the two present materials are
+// staged into the two slots and the kernel runs the two-material flux code on
+// them, which is the three-material code whenever the third material is
+// absent from every donor and stencil (k_tile_class checks the per-cell
+// conditions); finalize is the three-material one on the expanded vectors.
+template <int NM, bool XC = false, bool DIR = false, bool MAP = false>
+#ifndef H2D_RT_MAP3
+#define H2D_RT_MAP3 1
+#endif
 #ifndef H2D_RT_SPLITBAR
 #define H2D_RT_SPLITBAR 1
 #endif
@@ -1469,6 +1531,15 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     __shared__ int s_halt;
     __shared__ __align__(8) uint64_t s_bar, s_bar2;
     const int tid = threadIdx.x;
+    // three materials with tile classes: each tile runs in exactly one of the
+    // two launches (uniform over the CTA, before any copy is issued)
+    int rabs = 3;  // MAP: the absent material; slot a holds material mat[a]
+    if (MAP || (NM == 3 && !XC && !DIR && d.tcls)) {
+        rabs = d.tcls[blockIdx.y * gridDim.x + blockIdx.x];
+        if (MAP ? rabs == 3 : rabs != 3) return;
+    }
+    const int mat0 = MAP ? (rabs == 0 ? 1 : 0) : 0, mat1 = MAP ? (rabs == 2 ? 1 : 2) : 1;
+    auto mat = [&](int a) { return MAP ? (a == 0 ? mat0 : mat1) : a; };
     const int nx = d.nx, ny = d.ny;
     const Rng rg = d.r_gath;
     // TMA wants the box's first column 16-byte aligned (an even plane
@@ -1505,9 +1576,9 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
         if (kSplit) mbar_expect_tx(bar_c, cbytes);
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
-            tma_load_2d(T.el[a], &tm.t[TM_EL0 + a], x, y, bar_c);
-            tma_load_2d(T.rho[a], &tm.t[TM_M0 + a], x, y, bar_c);
-            tma_load_2d(NM >= 2 ? T.kk[a] : T.vl, &tm.t[TM_K0 + a], x, y, bar_c);
+            tma_load_2d(T.el[a], &tm.t[TM_EL0 + mat(a)], x, y, bar_c);
+            tma_load_2d(T.rho[a], &tm.t[TM_M0 + mat(a)], x, y, bar_c);
+            tma_load_2d(NM >= 2 ? T.kk[a] : T.vl, &tm.t[TM_K0 + mat(a)], x, y, bar_c);
         }
         s_halt = halted(d.ctl);
     }
@@ -1562,7 +1633,10 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
                 me[a] = m0 * T.el[a][tc];
                 va[a] = (NM >= 2 ? T.kk[a][tc] : T.vl[tc]) * cv;
             }
-            finalize_cell<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va);
+            if (MAP)
+                finalize_mapped(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va, mat0, mat1, rabs, cv);
+            else
+                finalize_cell<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va);
             return;
         }
     }
@@ -1688,7 +1762,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
         const double vl = T.vl[tc];
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
-            const double m0 = d.m[a][c];
+            const double m0 = d.m[mat(a)][c];
             m[a] = m0;
             me[a] = m0 * T.el[a][tc];
             va[a] = (NM >= 2 ? T.kk[a][tc] : d.k[a][c]) * vl;  // (T.kk: the staged k, unchanged)
@@ -1796,7 +1870,10 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
             for (int a = 0; a < NM; ++a) add(a, cq[q], donor);
         }
     }
-    finalize_cell<NM>(d, rg, i, j, c, tx, own, m, me, va);
+    if (MAP)
+        finalize_mapped(d, rg, i, j, c, tx, own, m, me, va, mat0, mat1, rabs, T.vl[tc]);
+    else
+        finalize_cell<NM>(d, rg, i, j, c, tx, own, m, me, va);
 }
 
 
@@ -3753,6 +3830,8 @@ void remap_init() {
                          (int)remap_smem_bytes<2, true>());
     cudaFuncSetAttribute(k_remap_tile<3, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)remap_smem_bytes<3, true>());
+    cudaFuncSetAttribute(k_remap_tile<2, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)remap_smem_bytes<2>());
     done = true;
 }
 
@@ -3847,7 +3926,71 @@ void launch_remap_core(const Dev& d, cudaStream_t s) {
     launch_remap_dual(d, s);
 }
 
+// Three materials: the class of each remap tile (Dev::tcls). A material r is
+// absent from a tile when no cell of the tile's staged region (the 36 x 12
+// TMA box, zero past the plane) has k_r > 0 or m_r != 0. The two-slot kernel
+// on the other two materials (lo < hi) is then the three-material kernel,
+// given that every region cell satisfies
+//  * a cell holding lo alone is not mixed in the two-material sense
+//    (mixed3 == is_mixed(k_lo), remap.cpp:100 / oracle mixed3), and
+//  * a non-mixed donor's material is the same: largest3(k) == (k_lo < 0.5 ?
+//    hi : lo) (remap.cpp:255-263 / oracle split_flux);
+// (with k_r = 0 the mixed split, the interface fraction and the degrade
+// tests reduce to the two-material expressions term by term). The class is
+// the highest such r, else 3.
+__device__ __forceinline__ bool map_ok(const double* k, int r) {
+    const int lo = r == 0 ? 1 : 0, hi = r == 2 ? 1 : 2;
+    if (k[lo] > 0.0 && !(k[hi] > 0.0) && is_mixed(k[lo])) return false;
+    if (!mixed3(k) && largest3(k) != (k[lo] < 0.5 ? hi : lo)) return false;
+    return true;
+}
+
+__global__ void __launch_bounds__(RTX * RTY) k_tile_class(Dev d) {
+    pdl_enter();
+    const int tid = threadIdx.x;
+    const Rng rg = d.r_gath;
+    const int i0 = rg.i0 - tile_shift(d) + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
+    const int x0 = i0 - G + d.H - d.oi, y0 = j0 - G + d.H - d.oj;  // plane column / row of the region origin
+    const int R = d.fsz / d.P;
+    unsigned pres = 0u, ok = 7u;
+    for (int t = tid; t < RCW * RCH; t += RTX * RTY) {
+        const int x = x0 + t % RCW, y = y0 + t / RCW;
+        if (x < 0 || x >= d.P || y < 0 || y >= R) continue;  // zero-filled by the copy: absent
+        const int q = y * d.P + x;
+        double k[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            k[a] = d.k[a][q];
+            if (k[a] > 0.0 || d.m[a][q] != 0.0) pres |= 1u << a;
+        }
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            if (!map_ok(k, r)) ok &= ~(1u << r);
+    }
+    __shared__ unsigned s_pres, s_ok;
+    if (tid == 0) {
+        s_pres = 0u;
+        s_ok = 7u;
+    }
+    __syncthreads();
+    pres = __reduce_or_sync(0xffffffffu, pres);
+    ok = __reduce_and_sync(0xffffffffu, ok);
+    if ((tid & 31) == 0) {
+        atomicOr(&s_pres, pres);
+        atomicAnd(&s_ok, ok);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int cls = 3;
+        for (int r = 2; r >= 0 && cls == 3; --r)
+            if (!((s_pres >> r) & 1u) && ((s_ok >> r) & 1u)) cls = r;
+        d.tcls[blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)cls;
+    }
+}
+
 // the fused flux tile kernel alone (timed separately by h2d_step_timed)
+int remap_tile_w() { return RTX; }
+int remap_tile_h() { return RTY; }
 int tma_node_box_w() { return RNW; }
 int tma_node_box_h() { return RNH; }
 int tma_cell_box_w() { return RCW; }
@@ -3869,8 +4012,19 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
         return;
     }
     if (d.nmat == 3)
-        xc ? pdl(k_remap_tile<3, true>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma)
-           : pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
+        if (xc) {
+            Dev dx = d;
+            dx.tcls = nullptr;
+            pdl(k_remap_tile<3, true>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, dx, *d.tma);
+        } else if (d.tcls && H2D_RT_MAP3) {  // per-tile: two-slot kernel where a material is absent
+            pdl(k_tile_class, gft, dim3(RTX * RTY), 0, s, d);
+            pdl(k_remap_tile<2, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
+            pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
+        } else {
+            Dev dx = d;
+            dx.tcls = nullptr;
+            pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, dx, *d.tma);
+        }
     else if (d.nmat == 2)
         xc ? pdl(k_remap_tile<2, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma)
            : pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);

@@ -35,6 +35,8 @@ struct HaloPlan {
 };
 
 long long launch_count();
+int remap_tile_w();  // remap-tile shape (cells): the tile-class grid
+int remap_tile_h();
 int tma_node_box_w();  // remap-tile TMA box sizes (doubles)
 int tma_node_box_h();
 int tma_cell_box_w();
