@@ -539,9 +539,6 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
 // (lagrange.cpp:135-142, 146-196). Q, p_half and p_mix_half never leave the
 // chip; the API path (h2d_lagrange_step) keeps the two-kernel form because
 // it returns Q.
-#ifndef H2D_LAG_SMEMC
-#define H2D_LAG_SMEMC 0
-#endif
 template <int NM>
 #ifndef H2D_FTY
 #define H2D_FTY 8
@@ -553,11 +550,6 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     constexpr int CW = LTX + 2, CH = LTY + 2, NC = CW * CH, NN = (LTX + 1) * (LTY + 1);
     __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC], s_mm[NC];
     __shared__ double shx[NN], shy[NN];
-#if H2D_LAG_SMEMC
-    // the State values of the tile's cells, loaded once by the cell pass and
-    // read back by the own-cell correct
-    __shared__ double s_k[NM][NC], s_m[NM][NC], s_e[NM][NC];
-#endif
     __shared__ int s_halt;
     const int tid = threadIdx.x;
     if (tid == 0) s_halt = halted(d.ctl);
@@ -590,11 +582,6 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
                 ka[a] = d.k[a][c];
                 ma[a] = d.m[a][c];
                 en[a] = d.e[a][c];
-#if H2D_LAG_SMEMC
-                s_k[a][t] = ka[a];
-                s_m[a][t] = ma[a];
-                s_e[a][t] = en[a];
-#endif
             }
             // the State's m_mix / rho_mix (sync_derived, state.cpp:120-143) from
             // the partial masses: the run loop does not keep the derived planes
@@ -710,31 +697,13 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     const double qn = s_q[tcell];
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
-#if H2D_LAG_SMEMC
-        const double ka = s_k[a][tcell];
-        const double en = s_e[a][tcell];
-#else
-#if H2D_LAG_SMEMC
-        const double ka = s_k[a][tcell];
-        const double en = s_e[a][tcell];
-#else
         const double ka = d.k[a][n];
         const double en = d.e[a][n];
-#endif
-#endif
         double ea = 0.0;
         if (ka < kThermoTol) {
             if (ka > 0.0) ea = en;
         } else {
-#if H2D_LAG_SMEMC
-            const double ma = s_m[a][tcell];
-#else
-#if H2D_LAG_SMEMC
-            const double ma = s_m[a][tcell];
-#else
             const double ma = d.m[a][n];
-#endif
-#endif
             const double rho_n = rho_of(d, ma, ka);
             double dv = 0.0;  // vol == cv: rho_l == rho_n, the difference of inverses is +0
             if (!(vol == cv && fabs(rho_n) >= DBL_MIN)) {
