@@ -782,12 +782,12 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
         d.dsc.part[0] = pp + (size_t)kDiagBlocks * DG_N;
         d.dsc.part[1] = d.dsc.part[0] + n0 * DG_NCELL;
     }
-    {  // one class byte per remap tile (launch_remap_tile's grid; three materials)
+    {  // one class byte per remap tile (launch_remap_tile's grid; 2-3 materials)
         const int shift = (d.r_gath.i0 - G + d.H - d.oi) & 1;  // tile_shift (h2d_kernels.cu)
         const int w = d.r_gath.i1 - (d.r_gath.i0 - shift), h = d.r_gath.j1 - d.r_gath.j0;
         d.tq_nx = std::max(1, (w + remap_tile_w() - 1) / remap_tile_w());
         d.tq_ny = std::max(1, (h + remap_tile_h() - 1) / remap_tile_h());
-        if (nm == 3) {
+        if (nm >= 2) {
             const size_t n = (size_t)d.tq_nx * d.tq_ny;
             if (cudaMalloc(&c->tcls_mem, n) != cudaSuccess) return fail(H2D_ERR_NOMEM);
             if (cudaMemset(c->tcls_mem, 3, n) != cudaSuccess) return fail(H2D_ERR_DEVICE);

@@ -223,10 +223,11 @@ struct Dev {
     int diag;           // run loop: reduce the step's make_diag values (k_post cells, node update momentum)
     DiagScratch dsc;    // diagnostics block partials ([0] k_post, [1] node update) + k_diag_reduce scratch
     int fsz;            // doubles per plane (P * R; the bound H2D_CHECKED tests plane indices against)
-    // three materials: one class byte per remap tile (k_tile_class; row-major
-    // over the remap grid, tq_nx x tq_ny): r < 3 = material r is absent from
-    // the tile's staged region and the tile runs the two-slot kernel, 3 = the
-    // three-material kernel. Null: every tile runs the kernel of its NM.
+    // two / three materials: one class byte per remap tile (k_tile_class;
+    // row-major over the remap grid, tq_nx x tq_ny): r < 3 = material r is
+    // absent from the tile's staged region and the tile runs the kernel with
+    // one slot fewer, 3 = the kernel of the context's material count. Null:
+    // every tile runs the kernel of its NM.
     uint8_t* tcls;
     int tq_nx, tq_ny;
 };

@@ -1421,21 +1421,26 @@ __device__ __forceinline__ void finalize_cell(const Dev& d, const Rng& rg, int i
 // gather gives it -- its m, m * e_lag and k * v, no flux -- and the cell is
 // finalised by the three-material rule (vf: the volume its k multiplies, cv on
 // the quiescent path, the Lagrangian volume otherwise)
+// (NS slots: NS = 2 in a three-material context, NS = 1 in a two-material one)
+template <int NS>
 __device__ __forceinline__ void finalize_mapped(const Dev& d, const Rng& rg, int i, int j, int c, int tx, bool own,
-                                                const double* m2, const double* me2, const double* va2, int mat0,
+                                                const double* ms, const double* mes, const double* vas, int mat0,
                                                 int mat1, int rabs, double vf) {
-    double m[3], me[3], va[3];
-    m[mat0] = m2[0];
-    me[mat0] = me2[0];
-    va[mat0] = va2[0];
-    m[mat1] = m2[1];
-    me[mat1] = me2[1];
-    va[mat1] = va2[1];
+    constexpr int NC = NS + 1;
+    double m[NC], me[NC], va[NC];
+    m[mat0] = ms[0];
+    me[mat0] = mes[0];
+    va[mat0] = vas[0];
+    if (NS == 2) {
+        m[mat1] = ms[NS - 1];
+        me[mat1] = mes[NS - 1];
+        va[mat1] = vas[NS - 1];
+    }
     const double m0 = d.m[rabs][c];
     m[rabs] = m0;
     me[rabs] = m0 * d.el[rabs][c];
     va[rabs] = d.k[rabs][c] * vf;
-    finalize_cell<3>(d, rg, i, j, c, tx, own, m, me, va);
+    finalize_cell<NC>(d, rg, i, j, c, tx, own, m, me, va);
 }
 
 // plane column of the remap tiles' first region column (rg.i0 - 2) is odd
@@ -1482,6 +1487,13 @@ template <int NM, bool XC = false, bool DIR = false, bool MAP = false>
 #ifndef H2D_RT_MAP3
 #define H2D_RT_MAP3 1
 #endif
+// H2D_RT_MAP2: the same per-tile mapping for two materials (one-material
+// kernel on single-material tiles); bit-identical but measured slower (C4
+// remap 3.70 -> 4.56 ms incl. its classification pass, profiles/
+// r02_var_map2_rejected.jsonl), so off
+#ifndef H2D_RT_MAP2
+#define H2D_RT_MAP2 0
+#endif
 #ifndef H2D_RT_SPLITBAR
 #define H2D_RT_SPLITBAR 1
 #endif
@@ -1502,12 +1514,14 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     const int tid = threadIdx.x;
     // three materials with tile classes: each tile runs in exactly one of the
     // two launches (uniform over the CTA, before any copy is issued)
-    int rabs = 3;  // MAP: the absent material; slot a holds material mat[a]
-    if (MAP || (NM == 3 && !XC && !DIR && d.tcls)) {
+    int rabs = 3;  // MAP: the absent material; slot a holds material mat(a)
+    if (MAP || (NM >= 2 && !XC && !DIR && d.tcls)) {
         rabs = d.tcls[blockIdx.y * gridDim.x + blockIdx.x];
         if (MAP ? rabs == 3 : rabs != 3) return;
     }
-    const int mat0 = MAP ? (rabs == 0 ? 1 : 0) : 0, mat1 = MAP ? (rabs == 2 ? 1 : 2) : 1;
+    // NM = 2 slots of a three-material context: the two present materials in
+    // order; NM = 1 slot of a two-material context: the present one
+    const int mat0 = MAP ? (NM == 2 ? (rabs == 0 ? 1 : 0) : 1 - rabs) : 0, mat1 = MAP ? (rabs == 2 ? 1 : 2) : 1;
     auto mat = [&](int a) { return MAP ? (a == 0 ? mat0 : mat1) : a; };
     const int nx = d.nx, ny = d.ny;
     const Rng rg = d.r_gath;
@@ -1603,7 +1617,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
                 va[a] = (NM >= 2 ? T.kk[a][tc] : T.vl[tc]) * cv;
             }
             if (MAP)
-                finalize_mapped(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va, mat0, mat1, rabs, cv);
+                finalize_mapped<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va, mat0, mat1, rabs, cv);
             else
                 finalize_cell<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va);
             return;
@@ -1734,7 +1748,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
             const double m0 = d.m[mat(a)][c];
             m[a] = m0;
             me[a] = m0 * T.el[a][tc];
-            va[a] = (NM >= 2 ? T.kk[a][tc] : d.k[a][c]) * vl;  // (T.kk: the staged k, unchanged)
+            va[a] = (NM >= 2 ? T.kk[a][tc] : d.k[mat(a)][c]) * vl;  // (T.kk: the staged k, unchanged)
         }
     }
     auto add = [&](int a, int q, bool neg) {  // the skip of remap.cpp:860,929
@@ -1840,7 +1854,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
         }
     }
     if (MAP)
-        finalize_mapped(d, rg, i, j, c, tx, own, m, me, va, mat0, mat1, rabs, T.vl[tc]);
+        finalize_mapped<NM>(d, rg, i, j, c, tx, own, m, me, va, mat0, mat1, rabs, T.vl[tc]);
     else
         finalize_cell<NM>(d, rg, i, j, c, tx, own, m, me, va);
 }
@@ -3801,6 +3815,8 @@ void remap_init() {
                          (int)remap_smem_bytes<3, true>());
     cudaFuncSetAttribute(k_remap_tile<2, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)remap_smem_bytes<2>());
+    cudaFuncSetAttribute(k_remap_tile<1, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)remap_smem_bytes<1>());
     done = true;
 }
 
@@ -3913,7 +3929,14 @@ __device__ __forceinline__ bool map_ok(const double* k, int r) {
     if (!mixed3(k) && largest3(k) != (k[lo] < 0.5 ? hi : lo)) return false;
     return true;
 }
+// Two materials: with r absent the one-material kernel on p = 1 - r is the
+// two-material one when every region cell is pure p in the reference's
+// sense (k_p >= 1 - kPureTol): no cell is mixed (remap.cpp:100), every donor
+// is p's (k0 < 0.5 <=> p = 1, remap.cpp:263) and no stencil degrades to
+// first order (remap.cpp:270-283).
+__device__ __forceinline__ bool map_ok2(const double* k, int r) { return k[1 - r] >= 1.0 - kPureTol; }
 
+template <int NM>
 __global__ void __launch_bounds__(RTX * RTY) k_tile_class(Dev d) {
     pdl_enter();
     const int tid = threadIdx.x;
@@ -3921,25 +3944,29 @@ __global__ void __launch_bounds__(RTX * RTY) k_tile_class(Dev d) {
     const int i0 = rg.i0 - tile_shift(d) + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
     const int x0 = i0 - G + d.H - d.oi, y0 = j0 - G + d.H - d.oj;  // plane column / row of the region origin
     const int R = d.fsz / d.P;
-    unsigned pres = 0u, ok = 7u;
+    unsigned pres = 0u, ok = (1u << NM) - 1u;
     for (int t = tid; t < RCW * RCH; t += RTX * RTY) {
         const int x = x0 + t % RCW, y = y0 + t / RCW;
-        if (x < 0 || x >= d.P || y < 0 || y >= R) continue;  // zero-filled by the copy: absent
-        const int q = y * d.P + x;
-        double k[3];
+        double k[NM];
+        if (x < 0 || x >= d.P || y < 0 || y >= R) {  // zero-filled by the copy: absent
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            k[a] = d.k[a][q];
-            if (k[a] > 0.0 || d.m[a][q] != 0.0) pres |= 1u << a;
+            for (int a = 0; a < NM; ++a) k[a] = 0.0;
+        } else {
+            const int q = y * d.P + x;
+#pragma unroll
+            for (int a = 0; a < NM; ++a) {
+                k[a] = d.k[a][q];
+                if (k[a] > 0.0 || d.m[a][q] != 0.0) pres |= 1u << a;
+            }
         }
 #pragma unroll
-        for (int r = 0; r < 3; ++r)
-            if (!map_ok(k, r)) ok &= ~(1u << r);
+        for (int r = 0; r < NM; ++r)
+            if (!(NM == 3 ? map_ok(k, r) : map_ok2(k, r))) ok &= ~(1u << r);
     }
     __shared__ unsigned s_pres, s_ok;
     if (tid == 0) {
         s_pres = 0u;
-        s_ok = 7u;
+        s_ok = (1u << NM) - 1u;
     }
     __syncthreads();
     pres = __reduce_or_sync(0xffffffffu, pres);
@@ -3951,7 +3978,7 @@ __global__ void __launch_bounds__(RTX * RTY) k_tile_class(Dev d) {
     __syncthreads();
     if (tid == 0) {
         int cls = 3;
-        for (int r = 2; r >= 0 && cls == 3; --r)
+        for (int r = NM - 1; r >= 0 && cls == 3; --r)
             if (!((s_pres >> r) & 1u) && ((s_ok >> r) & 1u)) cls = r;
         d.tcls[blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)cls;
     }
@@ -3986,7 +4013,7 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
             dx.tcls = nullptr;
             pdl(k_remap_tile<3, true>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, dx, *d.tma);
         } else if (d.tcls && H2D_RT_MAP3) {  // per-tile: two-slot kernel where a material is absent
-            pdl(k_tile_class, gft, dim3(RTX * RTY), 0, s, d);
+            pdl(k_tile_class<3>, gft, dim3(RTX * RTY), 0, s, d);
             pdl(k_remap_tile<2, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
             pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
         } else {
@@ -3995,8 +4022,19 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
             pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, dx, *d.tma);
         }
     else if (d.nmat == 2)
-        xc ? pdl(k_remap_tile<2, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma)
-           : pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
+        if (xc) {
+            Dev dx = d;
+            dx.tcls = nullptr;
+            pdl(k_remap_tile<2, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, dx, *d.tma);
+        } else if (d.tcls && H2D_RT_MAP2) {  // per-tile: one-material kernel where a material is absent
+            pdl(k_tile_class<2>, gft, dim3(RTX * RTY), 0, s, d);
+            pdl(k_remap_tile<1, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
+            pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
+        } else {
+            Dev dx = d;
+            dx.tcls = nullptr;
+            pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, dx, *d.tma);
+        }
     else
         xc ? pdl(k_remap_tile<1, true>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma)
            : pdl(k_remap_tile<1>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
