@@ -1427,19 +1427,17 @@ __device__ __forceinline__ void finalize_mapped(const Dev& d, const Rng& rg, int
                                                 const double* ms, const double* mes, const double* vas, int mat0,
                                                 int mat1, int rabs, double vf) {
     constexpr int NC = NS + 1;
-    double m[NC], me[NC], va[NC];
-    m[mat0] = ms[0];
-    me[mat0] = mes[0];
-    va[mat0] = vas[0];
-    if (NS == 2) {
-        m[mat1] = ms[NS - 1];
-        me[mat1] = mes[NS - 1];
-        va[mat1] = vas[NS - 1];
-    }
     const double m0 = d.m[rabs][c];
-    m[rabs] = m0;
-    me[rabs] = m0 * d.el[rabs][c];
-    va[rabs] = d.k[rabs][c] * vf;
+    const double mer = m0 * d.el[rabs][c], var = d.k[rabs][c] * vf;
+    // built with constant indices (selects), so the vectors stay in registers
+    double m[NC], me[NC], va[NC];
+#pragma unroll
+    for (int a = 0; a < NC; ++a) {
+        const bool s0 = a == mat0, s1 = NS == 2 && a == mat1;
+        m[a] = s0 ? ms[0] : (s1 ? ms[NS - 1] : m0);
+        me[a] = s0 ? mes[0] : (s1 ? mes[NS - 1] : mer);
+        va[a] = s0 ? vas[0] : (s1 ? vas[NS - 1] : var);
+    }
     finalize_cell<NC>(d, rg, i, j, c, tx, own, m, me, va);
 }
 
