@@ -542,11 +542,21 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
 template <int NM>
 #ifndef H2D_FTY
 #define H2D_FTY 8
-#define H2D_FMINB 5
 #endif
-__global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
+// 352 threads (11 warps) for a 32 x 8 tile: the 34 x 10 cell pass and the
+// 33 x 9 node pass take one round each (256 threads need two, the second
+// mostly idle at the barrier); CTAs per SM per material count as measured
+// (profiles/r02_var_lagthreads.jsonl, r02_var_lagthreads2.jsonl)
+#ifndef H2D_LAG_NT
+#define H2D_LAG_NT 352
+#endif
+#ifndef H2D_FMINB
+#define H2D_FMINB(NM) ((NM) == 2 ? 4 : 3)
+#endif
+__global__ void __launch_bounds__(H2D_LAG_NT, H2D_FMINB(NM)) k_lag_fused(Dev d) {
     pdl_enter();
     constexpr int LTY = H2D_FTY;
+    constexpr int NT = H2D_LAG_NT;  // threads (>= the tile's cells; extra ones help the halo passes)
     constexpr int CW = LTX + 2, CH = LTY + 2, NC = CW * CH, NN = (LTX + 1) * (LTY + 1);
     __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC], s_mm[NC];
     __shared__ double shx[NN], shy[NN];
@@ -562,8 +572,8 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     const double dt = step_dt(d.ctl);
     const double cv = d.cv;
     // ---- cells [i0-1, i0+LTX] x [j0-1, j0+LTY]: Q^n and predict
-    RowCol<CW, LTX * LTY> rc0(tid);
-    for (int t = tid; t < NC; t += LTX * LTY, rc0.step()) {
+    RowCol<CW, NT> rc0(tid);
+    for (int t = tid; t < NC; t += NT, rc0.step()) {
         const int ci = i0 - 1 + rc0.c, cj = j0 - 1 + rc0.r;
         double q = 0.0, pmix = 0.0, ph[NM] = {}, mmix = 0.0;
         if (in(d.win_c, ci, cj) && ci >= -1 && cj >= -1 && ci <= nx && cj <= ny) {
@@ -646,8 +656,8 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     }
     __syncthreads();
     // ---- nodes: u_half, u_lag
-    RowCol<LTX + 1, LTX * LTY> rc1(tid);
-    for (int t = tid; t < NN; t += LTX * LTY, rc1.step()) {
+    RowCol<LTX + 1, NT> rc1(tid);
+    for (int t = tid; t < NN; t += NT, rc1.step()) {
         const int i = i0 + rc1.c, j = j0 + rc1.r;
         double hx = 0.0, hy = 0.0;
         if (in(rn, i, j)) {
@@ -682,6 +692,7 @@ __global__ void __launch_bounds__(LTX * H2D_FTY, H2D_FMINB) k_lag_fused(Dev d) {
     }
     __syncthreads();
     // ---- own cells: correct
+    if (tid >= LTX * LTY) return;
     const int tx = tid % LTX, ty = tid / LTX;
     const int i = i0 + tx, j = j0 + ty;
     if (!in(d.r_lage, i, j)) return;
@@ -3882,11 +3893,11 @@ void launch_lagrange_run(const Dev& d, cudaStream_t s) {
 
 void launch_lag_fused(const Dev& d, cudaStream_t s) {
     if (d.nmat == 3)
-        pdl(k_lag_fused<3>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(LTX * H2D_FTY), 0, s, d);
+        pdl(k_lag_fused<3>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(H2D_LAG_NT), 0, s, d);
     else if (d.nmat == 2)
-        pdl(k_lag_fused<2>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(LTX * H2D_FTY), 0, s, d);
+        pdl(k_lag_fused<2>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(H2D_LAG_NT), 0, s, d);
     else
-        pdl(k_lag_fused<1>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(LTX * H2D_FTY), 0, s, d);
+        pdl(k_lag_fused<1>, tiles_of(d.r_lagn, LTX, H2D_FTY), dim3(H2D_LAG_NT), 0, s, d);
 }
 
 void launch_lag_ghosts(const Dev& d, cudaStream_t s) {
@@ -4143,7 +4154,7 @@ void launch_step_block_head(const Dev& dd, int part, cudaStream_t s) {
     d.diag = 1;
     d.lag_sel = part;
     if (part == 1) { k_step_start<<<1, 1, 0, s>>>(d.ctl, d.dx, d.dy); ++g_launches; }
-    const dim3 g = tiles_of(d.r_lagn, LTX, H2D_FTY), b(LTX * H2D_FTY);
+    const dim3 g = tiles_of(d.r_lagn, LTX, H2D_FTY), b(H2D_LAG_NT);
     if (d.nmat == 3)
         { k_lag_fused<3><<<g, b, 0, s>>>(d); ++g_launches; }
     else if (d.nmat == 2)
