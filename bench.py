@@ -443,12 +443,16 @@ def run_product_multi(args, world, rank, local, pg):
     barrier(pg)
     t0 = time.perf_counter()
     blk.init_window(win)
-    comm.run(args.warmup, 1e30, case.cfl)
+    from paper_2208_13409_b200 import abi as _abi
+    if args.remap == "direct":
+        raise SystemExit("block mode runs the DirectCF and AD remaps")
+    kind = _abi.REMAP_AD if args.remap == "ad" else _abi.REMAP_DIRECTCF
+    comm.run(args.warmup, 1e30, case.cfl, kind=kind)
     warm_ms = comm.device_ms
     clocks = Clocks(local)
     clocks.start()
     launches0 = lib.fn["launch_count"]()
-    done = comm.run(args.warmup + args.steps, 1e30, case.cfl)  # the steps of this call
+    done = comm.run(args.warmup + args.steps, 1e30, case.cfl, kind=kind)  # the steps of this call
     dev_ms = comm.device_ms
     launches = lib.fn["launch_count"]() - launches0
     clk = clocks.stop()
@@ -474,7 +478,8 @@ def run_product_multi(args, world, rank, local, pg):
         "data": "synthetic (init_case-equivalent painter, seeded; each rank paints its own window)",
         "config": config_of(case, args.remap, world,
                             parallelism=f"2D blocks {px}x{py}, halo {blk.halo}; per step 1 NCCL max all-reduce "
-                                        f"(4 words) + 1 grouped NCCL halo exchange, in the library"),
+                                        f"(4 words) + {2 if args.remap == 'ad' else 1} grouped NCCL halo "
+                                        f"exchange(s), in the library"),
         "cells_per_gpu": per_gpu, "halo_doubles_sent_rank0": halo_doubles, "paint_s_rank0": t_paint,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_kind,

@@ -337,6 +337,15 @@ void h2d_comm_destroy(h2d_comm* comm);
 /* device_ms (nullable): CUDA-event time from the first step's start to the
  * last step's exchange (the slowest block of this process) */
 int h2d_blocks_run(h2d_comm* comm, int max_steps, double t_end, double cfl, int* steps_done, float* device_ms);
+/* The same loop with the remap engine chosen: H2D_REMAP_DIRECTCF (as
+ * h2d_blocks_run: ONE halo exchange + one all-reduce per step) or
+ * H2D_REMAP_AD (run(kind = AD), harness.cpp:398-403 / remap.cpp:1110-1115, at
+ * most 2 materials): the split remap needs its neighbours' pass-0 Work
+ * (remap.cpp:87-97) before pass 1, i.e. a SECOND halo exchange per step
+ * between the two directional passes (PAPER.md:544 against :595). Owned
+ * values are bit-identical to the single-domain AD run. */
+int h2d_blocks_run_kind(h2d_comm* comm, int remap_kind, int max_steps, double t_end, double cfl, int* steps_done,
+                        float* device_ms);
 
 /* ---- benchmark support (no reference counterpart) ---------------------- */
 /* Kernels launched by this library in the calling process so far. */

@@ -1917,6 +1917,11 @@ struct h2d_comm {
         unsigned long long* red = nullptr;
         cudaStream_t cs = nullptr;
         cudaEvent_t e_red = nullptr, e_apply = nullptr, e_packed = nullptr, e_halo = nullptr;
+        // AD remap: the AdWork halo exchanged between the two passes (same
+        // rectangles, its own plane lists, offsets, buffers and events)
+        HaloPlan pk_ad{}, up_ad{};
+        double *send_ad = nullptr, *recv_ad = nullptr;
+        cudaEvent_t e_p0 = nullptr, e_packed_ad = nullptr, e_mid = nullptr;
     };
     std::vector<Side> side;
     unsigned long long** red_ptrs = nullptr;  // device array of every side's red (in-process)
@@ -1932,7 +1937,9 @@ void comm_free(h2d_comm* m) {
         if (sd.send) cudaFree(sd.send);
         if (sd.recv) cudaFree(sd.recv);
         if (sd.red) cudaFree(sd.red);
-        for (cudaEvent_t e : {sd.e_red, sd.e_apply, sd.e_packed, sd.e_halo})
+        if (sd.send_ad) cudaFree(sd.send_ad);
+        if (sd.recv_ad) cudaFree(sd.recv_ad);
+        for (cudaEvent_t e : {sd.e_red, sd.e_apply, sd.e_packed, sd.e_halo, sd.e_p0, sd.e_packed_ad, sd.e_mid})
             if (e) cudaEventDestroy(e);
         if (sd.cs) cudaStreamDestroy(sd.cs);
     }
@@ -1948,6 +1955,54 @@ void lists_at(h2d_ctx* c, int p, FieldList& cl, FieldList& nl) {
     c->cur = p;
     state_lists(c, cl, nl);
     c->cur = keep;
+}
+
+// AdWork planes a block needs from its neighbours before AD pass 1
+// (remap.cpp:87-97: the Work of pass 0)
+void ad_lists(h2d_ctx* c, FieldList& cl, FieldList& nl) {
+    const AdWork& W = c->adw;
+    cl = FieldList{};
+    nl = FieldList{};
+    for (int a = 0; a < c->nmat; ++a) {
+        cl.f[cl.n++] = W.m[a];
+        cl.f[cl.n++] = W.me[a];
+        cl.f[cl.n++] = W.e[a];
+        cl.f[cl.n++] = W.k[a];
+    }
+    cl.f[cl.n++] = W.mcell;
+    if (c->nmat == 2) {  // (one material: pass 1 reads the State's normals)
+        cl.f[cl.n++] = W.nrx;
+        cl.f[cl.n++] = W.nry;
+    }
+    nl.f[nl.n++] = W.ux;
+    nl.f[nl.n++] = W.uy;
+}
+
+// first AD run of a communicator: the AdWork planes, the plans of the
+// mid-step exchange and its buffers
+int side_setup_ad(h2d_comm::Side& sd) {
+    h2d_ctx* c = sd.c;
+    cudaSetDevice(c->device);
+    if (c->nmat > 2) {
+        set_err(c, H2D_ERR_INVALID, "the AD remap holds at most 2 materials");
+        return H2D_ERR_INVALID;
+    }
+    if (int rc = ensure_ad(c)) return rc;
+    if (sd.send_ad) return 0;
+    FieldList cl, nl;
+    ad_lists(c, cl, nl);
+    sd.pk_ad = sd.pk;
+    sd.up_ad = sd.up;
+    for (int pack = 1; pack >= 0; --pack) {
+        HaloPlan& pl = pack ? sd.pk_ad : sd.up_ad;
+        pl.off[0] = 0;
+        for (int q = 0; q < pl.n; ++q) pl.off[q + 1] = pl.off[q] + rect_doubles(cl, nl, pl.rc[q], pl.rn[q]);
+    }
+    CK(cudaMalloc(&sd.send_ad, (size_t)(sd.pk_ad.off[sd.pk_ad.n] > 0 ? sd.pk_ad.off[sd.pk_ad.n] : 1) * sizeof(double)));
+    CK(cudaMalloc(&sd.recv_ad, (size_t)(sd.up_ad.off[sd.up_ad.n] > 0 ? sd.up_ad.off[sd.up_ad.n] : 1) * sizeof(double)));
+    for (cudaEvent_t* e : {&sd.e_p0, &sd.e_packed_ad, &sd.e_mid})
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    return 0;
 }
 
 int side_setup(h2d_comm* m, h2d_comm::Side& sd) {
@@ -2095,11 +2150,24 @@ void h2d_comm_destroy(h2d_comm* m) {
 }
 
 int h2d_blocks_run(h2d_comm* m, int max_steps, double t_end, double cfl, int* steps_out, float* device_ms) {
+    return h2d_blocks_run_kind(m, H2D_REMAP_DIRECTCF, max_steps, t_end, cfl, steps_out, device_ms);
+}
+
+int h2d_blocks_run_kind(h2d_comm* m, int remap_kind, int max_steps, double t_end, double cfl, int* steps_out,
+                        float* device_ms) {
     constexpr int kPollSteps = 16;
     if (steps_out) *steps_out = 0;
     if (device_ms) *device_ms = 0.0f;
     h2d_ctx* c = m->side[0].c;  // CK's error target
     const int n = (int)m->side.size();
+    const bool ad = remap_kind == H2D_REMAP_AD;
+    if (!ad && remap_kind != H2D_REMAP_DIRECTCF) {
+        set_err(c, H2D_ERR_INVALID, "block mode runs the DirectCF and AD remaps");
+        return H2D_ERR_INVALID;
+    }
+    if (ad)
+        for (auto& sd : m->side)
+            if (int rc = side_setup_ad(sd)) return rc;
     for (auto& sd : m->side) {
         if (int rc = h2d_block_begin(sd.c, max_steps, t_end, cfl)) return rc;
         sd.c->derived_stale = true;
@@ -2133,25 +2201,37 @@ int h2d_blocks_run(h2d_comm* m, int max_steps, double t_end, double cfl, int* st
         }
         return check_launch(c);
     };
-    // the halo exchange of State parity p[b] (after combine, on cs)
-    auto exchange = [&](const std::vector<int>& p) -> int {
+    // one halo exchange on the cs streams: mid = false the State of parity
+    // p[b] (after combine), mid = true the AdWork planes between the AD passes
+    auto exchange = [&](const std::vector<int>& p, bool mid) -> int {
+        auto lists = [&](h2d_comm::Side& sd, int par, FieldList& cl, FieldList& nl) {
+            if (mid)
+                ad_lists(sd.c, cl, nl);
+            else
+                lists_at(sd.c, par, cl, nl);
+        };
         for (int b = 0; b < n; ++b) {
             auto& sd = m->side[b];
             FieldList cl, nl;
-            lists_at(sd.c, p[b], cl, nl);
-            launch_halo_multi(make_dev(sd.c, p[b], 1), cl, nl, sd.pk, sd.send, 1, sd.cs);
-            CK(cudaEventRecord(sd.e_packed, sd.cs));
+            lists(sd, p[b], cl, nl);
+            launch_halo_multi(make_dev(sd.c, p[b], 1), cl, nl, mid ? sd.pk_ad : sd.pk, mid ? sd.send_ad : sd.send, 1,
+                              sd.cs);
+            CK(cudaEventRecord(mid ? sd.e_packed_ad : sd.e_packed, sd.cs));
         }
         if (m->kind == 1) {
             auto& sd = m->side[0];
+            const HaloPlan& pk = mid ? sd.pk_ad : sd.pk;
+            const HaloPlan& up = mid ? sd.up_ad : sd.up;
+            double* send = mid ? sd.send_ad : sd.send;
+            double* recv = mid ? sd.recv_ad : sd.recv;
             if (g_nccl.GroupStart() != ncclSuccess) return H2D_ERR_DEVICE;
             for (int q = 0; q < 8; ++q) {
                 if (sd.peer[q] < 0) continue;
                 const int a = sd.seg_pk[q], r = sd.seg_up[q];
-                g_nccl.Send(sd.send + sd.pk.off[a], (size_t)(sd.pk.off[a + 1] - sd.pk.off[a]), ncclFloat64, sd.peer[q],
-                            m->nccl, sd.cs);
-                g_nccl.Recv(sd.recv + sd.up.off[r], (size_t)(sd.up.off[r + 1] - sd.up.off[r]), ncclFloat64, sd.peer[q],
-                            m->nccl, sd.cs);
+                g_nccl.Send(send + pk.off[a], (size_t)(pk.off[a + 1] - pk.off[a]), ncclFloat64, sd.peer[q], m->nccl,
+                            sd.cs);
+                g_nccl.Recv(recv + up.off[r], (size_t)(up.off[r + 1] - up.off[r]), ncclFloat64, sd.peer[q], m->nccl,
+                            sd.cs);
             }
             if (g_nccl.GroupEnd() != ncclSuccess) {
                 set_err(c, H2D_ERR_DEVICE, "NCCL halo exchange failed");
@@ -2160,29 +2240,33 @@ int h2d_blocks_run(h2d_comm* m, int max_steps, double t_end, double cfl, int* st
         } else {  // pull: my halo segment for direction q is the neighbour's pack segment for -q
             for (int b = 0; b < n; ++b) {
                 auto& sd = m->side[b];
+                const HaloPlan& up = mid ? sd.up_ad : sd.up;
                 for (int q = 0; q < 8; ++q) {
                     if (sd.peer[q] < 0) continue;
                     auto& nb = m->side[sd.peer[q]];
+                    const HaloPlan& npk = mid ? nb.pk_ad : nb.pk;
                     const int a = nb.seg_pk[dir_index(-kDirs[q][0], -kDirs[q][1])], r = sd.seg_up[q];
-                    CK(cudaStreamWaitEvent(sd.cs, nb.e_packed, 0));
-                    CK(cudaMemcpyAsync(sd.recv + sd.up.off[r], nb.send + nb.pk.off[a],
-                                       (size_t)(sd.up.off[r + 1] - sd.up.off[r]) * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, sd.cs));
+                    CK(cudaStreamWaitEvent(sd.cs, mid ? nb.e_packed_ad : nb.e_packed, 0));
+                    CK(cudaMemcpyAsync((mid ? sd.recv_ad : sd.recv) + up.off[r],
+                                       (mid ? nb.send_ad : nb.send) + npk.off[a],
+                                       (size_t)(up.off[r + 1] - up.off[r]) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       sd.cs));
                 }
             }
         }
         for (int b = 0; b < n; ++b) {
             auto& sd = m->side[b];
             FieldList cl, nl;
-            lists_at(sd.c, p[b], cl, nl);
-            launch_halo_multi(make_dev(sd.c, p[b], 1), cl, nl, sd.up, sd.recv, 0, sd.cs);
-            CK(cudaEventRecord(sd.e_halo, sd.cs));
+            lists(sd, p[b], cl, nl);
+            launch_halo_multi(make_dev(sd.c, p[b], 1), cl, nl, mid ? sd.up_ad : sd.up, mid ? sd.recv_ad : sd.recv, 0,
+                              sd.cs);
+            CK(cudaEventRecord(mid ? sd.e_mid : sd.e_halo, sd.cs));
         }
         return check_launch(c);
     };
 
     if (int rc = combine()) return rc;  // the initial State's global wave speed
-    if (int rc = exchange(parity)) return rc;  // the initial halos (exact after a window init)
+    if (int rc = exchange(parity, false)) return rc;  // the initial halos (exact after a window init)
     std::vector<cudaEvent_t> t0(n), t1(n);
     for (int b = 0; b < n; ++b) {
         CK(cudaEventCreate(&t0[b]));
@@ -2198,7 +2282,9 @@ int h2d_blocks_run(h2d_comm* m, int max_steps, double t_end, double cfl, int* st
             if (left <= 0) break;
             chunk = left < chunk ? left : chunk;
         }
+        const int step0 = m->side[0].c->hctl->step;
         for (int q = 0; q < chunk; ++q) {
+            const int x_first = (step0 + q) % 2 == 0;  // harness.cpp:401
             for (int b = 0; b < n; ++b) {
                 auto& sd = m->side[b];
                 h2d_ctx* bc = sd.c;
@@ -2207,12 +2293,28 @@ int h2d_blocks_run(h2d_comm* m, int max_steps, double t_end, double cfl, int* st
                 launch_step_block_head(d, 1, bc->st);
                 CK(cudaStreamWaitEvent(bc->st, sd.e_halo, 0));
                 launch_step_block_head(d, 2, bc->st);
+                if (ad) {  // pass 0 on this block's window, then its AdWork halo goes out
+                    launch_step_block_ad_mid(d, bc->adw, x_first, bc->st);
+                    CK(cudaEventRecord(sd.e_p0, bc->st));
+                    CK(cudaStreamWaitEvent(sd.cs, sd.e_p0, 0));
+                    continue;
+                }
                 CK(cudaGraphLaunch(bc->graph_rest[parity[b]], bc->st));
                 add_launches(bc->graph_rest_kernels);
                 parity[b] ^= 1;
             }
+            if (ad) {  // the split remap's second exchange, then pass 1 and the rest of the step
+                if (int rc = exchange(parity, true)) return rc;
+                for (int b = 0; b < n; ++b) {
+                    auto& sd = m->side[b];
+                    h2d_ctx* bc = sd.c;
+                    CK(cudaStreamWaitEvent(bc->st, sd.e_mid, 0));
+                    launch_step_block_ad_rest(make_dev(bc, parity[b], 1), bc->adw, x_first, bc->st);
+                    parity[b] ^= 1;
+                }
+            }
             if (int rc = combine()) return rc;
-            if (int rc = exchange(parity)) return rc;
+            if (int rc = exchange(parity, false)) return rc;
         }
         bool stop = false;
         for (int b = 0; b < n; ++b) {

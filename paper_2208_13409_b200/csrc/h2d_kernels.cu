@@ -3645,8 +3645,8 @@ __global__ void k_ad_normals(Dev d, AdIO w) {
     pdl_enter();
     if (halted(d.ctl)) return;
     int i, j;
-    tid2(i, j, 0, 0);
-    if (i >= d.nx || j >= d.ny || !in(d.win_c, i, j)) return;
+    tid2(i, j, d.r_nrm.i0, d.r_nrm.j0);  // (a block: the cells whose 3x3 fractions are exact after the pass)
+    if (!in(d.r_nrm, i, j)) return;
     const int c = ix(d, i, j);
     double nrx = w.nrx[c], nry = w.nry[c];
     if (is_mixed(d.nk[0][c])) {
@@ -4324,7 +4324,7 @@ static void launch_ad_pass(const Dev& dout, const AdIO& w, int remap_velocity, c
         launch_ghost_multi(dout, none, fu, 0, 1, s);
     }
     if (dout.nmat == 2 && w.pass == 0) {  // pass 1's normals are k_post's
-        pdl(k_ad_normals, grid_rect(dout.nx, dout.ny), blk2(), 0, s, dout, w);
+        pdl(k_ad_normals, grid_of(dout.r_nrm), blk2(), 0, s, dout, w);
         FieldList fc{};
         fc.n = 2;
         fc.f[0] = dout.nnrx;
@@ -4333,10 +4333,13 @@ static void launch_ad_pass(const Dev& dout, const AdIO& w, int remap_velocity, c
     }
 }
 
-void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_velocity, int run_loop, cudaStream_t s) {
+// The two directional passes (remap.cpp:1110-1115). Pass 0 writes the AdWork
+// planes, pass 1 reads them and writes the next State; a decomposition block
+// exchanges the AdWork halo between the two (launch_step_block_ad_*).
+void launch_ad_first(const Dev& d, const AdWork& W, int x_first, int remap_velocity, cudaStream_t s) {
     const int nm = d.nmat;
     Dev d0 = d;  // pass 0 writes the AdWork
-    AdIO w0{}, w1{};
+    AdIO w0{};
     for (int a = 0; a < nm; ++a) {
         d0.nm[a] = W.m[a];
         d0.ne[a] = W.e[a];
@@ -4345,10 +4348,6 @@ void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_veloc
         w0.m[a] = d.m[a];
         w0.e[a] = d.el[a];
         w0.k[a] = d.k[a];
-        w1.m[a] = W.m[a];
-        w1.me[a] = W.me[a];
-        w1.e[a] = W.e[a];
-        w1.k[a] = W.k[a];
     }
     d0.mcell = W.mcell;
     d0.nux = W.ux;
@@ -4364,6 +4363,17 @@ void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_veloc
     w0.pass = 0;
     w0.axis_x = x_first ? 1 : 0;
     launch_ad_pass(d0, w0, remap_velocity, s);
+}
+
+void launch_ad_second(const Dev& d, const AdWork& W, int x_first, int remap_velocity, int run_loop, cudaStream_t s) {
+    const int nm = d.nmat;
+    AdIO w1{};
+    for (int a = 0; a < nm; ++a) {
+        w1.m[a] = W.m[a];
+        w1.me[a] = W.me[a];
+        w1.e[a] = W.e[a];
+        w1.k[a] = W.k[a];
+    }
     w1.nrx = nm == 2 ? W.nrx : d.nrx;
     w1.nry = nm == 2 ? W.nry : d.nry;
     w1.mcell = W.mcell;
@@ -4380,6 +4390,30 @@ void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_veloc
         dp.nry = W.nry;
     }
     post_and_ghosts(dp, run_loop, s);
+}
+
+void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_velocity, int run_loop, cudaStream_t s) {
+    launch_ad_first(d, W, x_first, remap_velocity, s);
+    launch_ad_second(d, W, x_first, remap_velocity, run_loop, s);
+}
+
+// Block mode with the AD remap: the step after the Lagrange kernel in two
+// parts around the exchange of the AdWork halo (the split remap needs its
+// neighbours' pass-0 result before pass 1: one more exchange per step than
+// the unsplit DirectCF step, PAPER.md:544 / :595)
+void launch_step_block_ad_mid(const Dev& dd, const AdWork& W, int x_first, cudaStream_t s) {
+    Dev d = dd;
+    d.scan_nodes = 1;
+    d.diag = 1;
+    launch_lag_ghosts(d, s);
+    launch_ad_first(d, W, x_first, 1, s);
+}
+void launch_step_block_ad_rest(const Dev& dd, const AdWork& W, int x_first, cudaStream_t s) {
+    Dev d = dd;
+    d.scan_nodes = 1;
+    d.diag = 1;
+    launch_ad_second(d, W, x_first, 1, 1, s);
+    launch_tail(d, 0, s);
 }
 
 // remap_single_axis (remap.cpp:1098-1104): make_work + ONE directional pass

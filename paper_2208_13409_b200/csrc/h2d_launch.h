@@ -82,6 +82,8 @@ void launch_rollback(Ctl* c, cudaStream_t s);
 // block-mode data plane (h2d_blocks_run)
 void launch_step_block_head(const Dev& d, int part, cudaStream_t s);  // part 1: start + inner tiles, 2: edge tiles
 void launch_step_block_rest(const Dev& d, cudaStream_t s);
+void launch_step_block_ad_mid(const Dev& d, const AdWork& W, int x_first, cudaStream_t s);   // lag ghosts + AD pass 0
+void launch_step_block_ad_rest(const Dev& d, const AdWork& W, int x_first, cudaStream_t s);  // AD pass 1 + post + tail
 void launch_xhalf(const Dev& d, double* xh, double* yh, cudaStream_t s);  // HalfStepState::x_half
 int lag_tile_w();  // the fused Lagrange kernel's node tile
 int lag_tile_h();

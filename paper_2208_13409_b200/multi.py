@@ -105,6 +105,8 @@ _SIGS = {
     "comm_destroy": ([C.c_void_p], None),
     "blocks_run": ([C.c_void_p, C.c_int, C.c_double, C.c_double, C.POINTER(C.c_int), C.POINTER(C.c_float)],
                    C.c_int),
+    "blocks_run_kind": ([C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.POINTER(C.c_int),
+                         C.POINTER(C.c_float)], C.c_int),
 }
 
 
@@ -242,13 +244,15 @@ class DeviceComm:
             raise errors.from_code(rc, "h2d_nccl_unique_id failed")
         return buf.raw
 
-    def run(self, max_steps: int, t_end: float, cfl: float) -> int:
+    def run(self, max_steps: int, t_end: float, cfl: float, kind: int = 2) -> int:
         """Run to max_steps (absolute) / t_end; returns the steps done. The
         device time of the steps (CUDA events on the block's streams) is
-        left in self.device_ms."""
+        left in self.device_ms. kind: abi.REMAP_DIRECTCF (2: one halo
+        exchange per step) or abi.REMAP_AD (0: the split remap, a second
+        exchange between its two passes)."""
         done = C.c_int(0)
         ms = C.c_float(0.0)
-        rc = self.lib.fn["blocks_run"](self._h, max_steps, t_end, cfl, C.byref(done), C.byref(ms))
+        rc = self.lib.fn["blocks_run_kind"](self._h, kind, max_steps, t_end, cfl, C.byref(done), C.byref(ms))
         if rc:
             self.blocks[0]._check(rc)
         self.device_ms = ms.value

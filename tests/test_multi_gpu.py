@@ -6,15 +6,15 @@ import numpy as np
 import pytest
 
 import helpers
-from paper_2208_13409_b200 import cases, errors, multi
+from paper_2208_13409_b200 import abi, cases, errors, multi
 from paper_2208_13409_b200.abi import HostState
 
 pytestmark = pytest.mark.gpu
 
 
-def _single(case, steps):
+def _single(case, steps, kind=abi.REMAP_DIRECTCF):
     s = helpers.prepared(helpers.product_lib(), case.cfg, case.paint())
-    r, err = helpers.run_capture(s, steps, case.cfl)
+    r, err = helpers.run_capture(s, steps, case.cfl, kind=kind)
     return s.download(), r, err
 
 
@@ -83,7 +83,7 @@ def test_halo_plan_matches_library():
 
 
 # ---- the library's data plane (h2d_comm + h2d_blocks_run) -------------------
-def _blocks_device(case, steps, px, py):
+def _blocks_device(case, steps, px, py, kind=abi.REMAP_DIRECTCF):
     """The whole decomposed run loop inside the library: per step every
     block's graph, one max all-reduce of the four control words and one
     halo exchange enqueued on the device (in-process transport: every
@@ -95,7 +95,7 @@ def _blocks_device(case, steps, px, py):
     for b in blocks:
         b.upload(init)
     comm = multi.DeviceComm(blocks, px, py)
-    comm.run(steps, 1e30, case.cfl)
+    comm.run(steps, 1e30, case.cfl, kind=kind)
     comm.close()
     out = HostState.empty(case.cfg.mesh.nx, case.cfg.mesh.ny, case.cfg.nmat)
     results = []
@@ -103,6 +103,55 @@ def _blocks_device(case, steps, px, py):
         b.download_into(out)
         results.append(b.result(steps))
     return out, results
+
+
+# ---- the AD split remap in block mode (the split remap
+# needs a second halo exchange per step, between its two passes) --------------
+@pytest.mark.parametrize("px,py", [(2, 1), (1, 2), (2, 2), (4, 2)])
+@pytest.mark.parametrize("which", ["riemann", "sedov", "triple", "bubble"])
+def test_ad_blocks_bitwise_equal_single_domain(which, px, py):
+    case = {"riemann": cases.riemann2d(64), "sedov": cases.sedov(64), "triple": cases.triple_point(96, 48),
+            "bubble": cases.shock_bubble(64)}[which]
+    steps = 41  # odd: both axis orders end a run
+    ref, r, err = _single(case, steps, abi.REMAP_AD)
+    got, results = _blocks_device(case, steps, px, py, abi.REMAP_AD)
+    assert err is None
+    for a, dts, e in results:
+        assert e is None
+        assert a.steps_done == r.steps_done
+        assert np.array_equal(dts, r.dts)
+    assert sum(a.diag.k_clip_count for a, _, _ in results) == r.diag["k_clip_count"]
+    assert sum(a.diag.mass_fix_count for a, _, _ in results) == r.diag["mass_fix_count"]
+    assert sum(a.floor_count for a, _, _ in results) == r.floor_count
+    assert helpers.bitwise_diff(got, ref, helpers.STATE_FIELDS) == []
+    assert (got.step, got.time) == (ref.step, ref.time)
+
+
+def test_ad_blocks_reproduce_the_reference_abort():
+    """the AD run of the 64x32 triple point aborts; the decomposition raises
+    the same error at the same step and keeps the last completed State."""
+    case = cases.triple_point(64, 32)
+    ref, r, err = _single(case, 700, abi.REMAP_AD)
+    assert err is not None
+    got, results = _blocks_device(case, 700, 2, 2, abi.REMAP_AD)
+    for a, dts, e in results:
+        assert (type(e).__name__, e.what, e.i, e.j) == err[:4]
+        assert a.steps_done == r.steps_done
+        assert np.array_equal(dts[:r.steps_done], r.dts[:r.steps_done])
+    assert helpers.bitwise_diff(got, ref, helpers.STATE_FIELDS) == []
+
+
+def test_ad_blocks_refuse_three_materials():
+    case = cases.voronoi3(64)
+    lib = helpers.product_lib()
+    init = helpers.prepared(lib, case.cfg, case.paint()).download()
+    blocks = [multi.BlockSolver(lib, case.cfg, sp) for sp in multi.decompose(64, 64, 2, 1)]
+    for b in blocks:
+        b.upload(init)
+    comm = multi.DeviceComm(blocks, 2, 1)
+    with pytest.raises(errors.DeviceError):
+        comm.run(5, 1e30, case.cfl, kind=abi.REMAP_AD)
+    comm.close()
 
 
 @pytest.mark.parametrize("px,py", [(2, 1), (1, 2), (2, 2), (4, 2)])
