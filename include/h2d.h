@@ -171,7 +171,8 @@ typedef struct {
     double t_end;
     double cfl;
     int remap_kind;   /* H2D_REMAP_*: all three on single-domain contexts (AD with at
-                       * most 2 materials); block contexts run DirectCF only */
+                       * most 2 materials); block contexts run DirectCF and AD
+                       * through h2d_blocks_run / h2d_blocks_run_kind */
     double* dt_log;   /* optional host array receiving each step's dt */
     int dt_log_cap;
     /* outputs */
@@ -346,6 +347,19 @@ int h2d_blocks_run(h2d_comm* comm, int max_steps, double t_end, double cfl, int*
  * values are bit-identical to the single-domain AD run. */
 int h2d_blocks_run_kind(h2d_comm* comm, int remap_kind, int max_steps, double t_end, double cfl, int* steps_done,
                         float* device_ms);
+
+/* Stream trace of the next h2d_blocks_run* call (evidence of the overlap; no
+ * reference counterpart): CUDA timing events at nine points of each of the
+ * first `steps` steps and each block of this process. h2d_comm_trace_read
+ * returns the number of floats recorded (steps x blocks x 9, step-major) and
+ * copies up to cap of them: milliseconds from the block's first step start of
+ * {owned Lagrange tiles start, end, edge tiles end (after the halo wait), AD
+ * mid exchange start, end, rest of the step end, all-reduce start, State halo
+ * exchange start, end}; -1 = point not reached (e.g. the AD points of a
+ * DirectCF run). The State exchange recorded with step s is the one enqueued
+ * after step s, which overlaps step s + 1's owned tiles. */
+int h2d_comm_trace(h2d_comm* comm, int steps);
+int h2d_comm_trace_read(h2d_comm* comm, float* out, int cap);
 
 /* ---- benchmark support (no reference counterpart) ---------------------- */
 /* Kernels launched by this library in the calling process so far. */

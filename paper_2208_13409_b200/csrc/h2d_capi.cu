@@ -1926,7 +1926,12 @@ struct h2d_comm {
     std::vector<Side> side;
     unsigned long long** red_ptrs = nullptr;  // device array of every side's red (in-process)
     cudaEvent_t e_all = nullptr;
+    // h2d_comm_trace: timing events of the first trace_cap steps of the next
+    // run, per block kTracePts points (ms from the run's first step start)
+    int trace_cap = 0;
+    std::vector<float> trace;
 };
+enum { TR_LAG0, TR_LAG1, TR_EDGE1, TR_MID0, TR_MID1, TR_REST1, TR_RED0, TR_HALO0, TR_HALO1, kTracePts };
 
 namespace {
 
@@ -2175,12 +2180,27 @@ int h2d_blocks_run_kind(h2d_comm* m, int remap_kind, int max_steps, double t_end
     std::vector<int> parity(n);
     for (int b = 0; b < n; ++b) parity[b] = m->side[b].c->cur;
 
+    // optional trace (h2d_comm_trace): timing events at fixed points of a step
+    std::vector<cudaEvent_t> tev;
+    const int tr_steps = m->trace_cap;
+    m->trace.clear();
+    if (tr_steps > 0) {
+        tev.resize((size_t)tr_steps * n * kTracePts, nullptr);
+        for (auto& e : tev) CK(cudaEventCreate(&e));
+    }
+    int tr_q = -1;  // the step being traced (-1: none)
+    auto mark = [&](int b, int pt, cudaStream_t st) {
+        if (tr_q >= 0) cudaEventRecord(tev[((size_t)tr_q * n + b) * kTracePts + pt], st);
+    };
+    int steps_issued = 0;
+
     // the all-reduce + apply of every block's four words, on the cs streams
     auto combine = [&]() -> int {
         for (auto& sd : m->side) {
             launch_red_pack(sd.c->ctl, sd.red, sd.c->st);
             CK(cudaEventRecord(sd.e_red, sd.c->st));
             CK(cudaStreamWaitEvent(sd.cs, sd.e_red, 0));
+            mark((int)(&sd - &m->side[0]), TR_RED0, sd.cs);
         }
         if (m->kind == 1) {
             auto& sd = m->side[0];
@@ -2214,6 +2234,7 @@ int h2d_blocks_run_kind(h2d_comm* m, int remap_kind, int max_steps, double t_end
             auto& sd = m->side[b];
             FieldList cl, nl;
             lists(sd, p[b], cl, nl);
+            mark(b, mid ? TR_MID0 : TR_HALO0, sd.cs);
             launch_halo_multi(make_dev(sd.c, p[b], 1), cl, nl, mid ? sd.pk_ad : sd.pk, mid ? sd.send_ad : sd.send, 1,
                               sd.cs);
             CK(cudaEventRecord(mid ? sd.e_packed_ad : sd.e_packed, sd.cs));
@@ -2260,6 +2281,7 @@ int h2d_blocks_run_kind(h2d_comm* m, int remap_kind, int max_steps, double t_end
             lists(sd, p[b], cl, nl);
             launch_halo_multi(make_dev(sd.c, p[b], 1), cl, nl, mid ? sd.up_ad : sd.up, mid ? sd.recv_ad : sd.recv, 0,
                               sd.cs);
+            mark(b, mid ? TR_MID1 : TR_HALO1, sd.cs);
             CK(cudaEventRecord(mid ? sd.e_mid : sd.e_halo, sd.cs));
         }
         return check_launch(c);
@@ -2285,14 +2307,21 @@ int h2d_blocks_run_kind(h2d_comm* m, int remap_kind, int max_steps, double t_end
         const int step0 = m->side[0].c->hctl->step;
         for (int q = 0; q < chunk; ++q) {
             const int x_first = (step0 + q) % 2 == 0;  // harness.cpp:401
+            // (the exchange of step s - 1, which overlaps step s's owned tiles, was
+            // enqueued with tr_q = s - 1: its TR_HALO* marks belong to that record)
+            tr_q = steps_issued < tr_steps ? steps_issued : -1;
+            ++steps_issued;
             for (int b = 0; b < n; ++b) {
                 auto& sd = m->side[b];
                 h2d_ctx* bc = sd.c;
                 const Dev d = make_dev(bc, parity[b], 1);
                 CK(cudaStreamWaitEvent(bc->st, sd.e_apply, 0));
+                mark(b, TR_LAG0, bc->st);
                 launch_step_block_head(d, 1, bc->st);
+                mark(b, TR_LAG1, bc->st);
                 CK(cudaStreamWaitEvent(bc->st, sd.e_halo, 0));
                 launch_step_block_head(d, 2, bc->st);
+                mark(b, TR_EDGE1, bc->st);
                 if (ad) {  // pass 0 on this block's window, then its AdWork halo goes out
                     launch_step_block_ad_mid(d, bc->adw, x_first, bc->st);
                     CK(cudaEventRecord(sd.e_p0, bc->st));
@@ -2301,6 +2330,7 @@ int h2d_blocks_run_kind(h2d_comm* m, int remap_kind, int max_steps, double t_end
                 }
                 CK(cudaGraphLaunch(bc->graph_rest[parity[b]], bc->st));
                 add_launches(bc->graph_rest_kernels);
+                mark(b, TR_REST1, bc->st);
                 parity[b] ^= 1;
             }
             if (ad) {  // the split remap's second exchange, then pass 1 and the rest of the step
@@ -2310,6 +2340,7 @@ int h2d_blocks_run_kind(h2d_comm* m, int remap_kind, int max_steps, double t_end
                     h2d_ctx* bc = sd.c;
                     CK(cudaStreamWaitEvent(bc->st, sd.e_mid, 0));
                     launch_step_block_ad_rest(make_dev(bc, parity[b], 1), bc->adw, x_first, bc->st);
+                    mark(b, TR_REST1, bc->st);
                     parity[b] ^= 1;
                 }
             }
@@ -2334,14 +2365,44 @@ int h2d_blocks_run_kind(h2d_comm* m, int remap_kind, int max_steps, double t_end
         float ms = 0.0f;
         CK(cudaEventElapsedTime(&ms, t0[b], t1[b]));
         worst = ms > worst ? ms : worst;
-        cudaEventDestroy(t0[b]);
-        cudaEventDestroy(t1[b]);
         if (int rc = ctl_pull(sd.c)) return rc;
         sd.c->cur = sd.c->hctl->cur;
+    }
+    if (tr_steps > 0) {  // ms of every traced point from its block's first step start (-1: not reached)
+        const int got = steps_issued < tr_steps ? steps_issued : tr_steps;
+        m->trace.assign((size_t)got * n * kTracePts, -1.0f);
+        for (int q = 0; q < got; ++q)
+            for (int b = 0; b < n; ++b)
+                for (int pt = 0; pt < kTracePts; ++pt) {
+                    float ms = -1.0f;
+                    const size_t k = ((size_t)q * n + b) * kTracePts + pt;
+                    if (cudaEventElapsedTime(&ms, t0[b], tev[k]) == cudaSuccess) m->trace[k] = ms;
+                }
+        cudaGetLastError();  // (an unrecorded point reports an error: cleared)
+        for (auto& e : tev) cudaEventDestroy(e);
+        m->trace_cap = 0;
+    }
+    for (int b = 0; b < n; ++b) {
+        cudaEventDestroy(t0[b]);
+        cudaEventDestroy(t1[b]);
     }
     if (device_ms) *device_ms = worst;
     if (steps_out) *steps_out = m->side[0].c->hctl->steps_done;
     return 0;
+}
+
+int h2d_comm_trace(h2d_comm* m, int steps) {
+    if (!m || steps < 0 || steps > 4096) return H2D_ERR_INVALID;
+    m->trace_cap = steps;
+    return 0;
+}
+
+int h2d_comm_trace_read(h2d_comm* m, float* out, int cap) {
+    if (!m) return 0;
+    const int nrec = (int)m->trace.size();
+    if (out)
+        for (int k = 0; k < nrec && k < cap; ++k) out[k] = m->trace[k];
+    return nrec;
 }
 
 }  // extern "C"

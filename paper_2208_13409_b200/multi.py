@@ -105,6 +105,8 @@ _SIGS = {
     "comm_destroy": ([C.c_void_p], None),
     "blocks_run": ([C.c_void_p, C.c_int, C.c_double, C.c_double, C.POINTER(C.c_int), C.POINTER(C.c_float)],
                    C.c_int),
+    "comm_trace": ([C.c_void_p, C.c_int], C.c_int),
+    "comm_trace_read": ([C.c_void_p, C.POINTER(C.c_float), C.c_int], C.c_int),
     "blocks_run_kind": ([C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.POINTER(C.c_int),
                          C.POINTER(C.c_float)], C.c_int),
 }
@@ -257,6 +259,20 @@ class DeviceComm:
             self.blocks[0]._check(rc)
         self.device_ms = ms.value
         return done.value
+
+    TRACE_POINTS = ("lag_owned_start", "lag_owned_end", "lag_edge_end", "ad_mid_start", "ad_mid_end", "rest_end",
+                    "allreduce_start", "halo_start", "halo_end")
+
+    def trace(self, steps: int):
+        """Record CUDA timing events at TRACE_POINTS of the first `steps` steps of the next run."""
+        self.lib.fn["comm_trace"](self._h, steps)
+
+    def trace_read(self) -> np.ndarray:
+        """(steps, blocks, 9) milliseconds from each block's first step start (-1: point not reached)."""
+        n = self.lib.fn["comm_trace_read"](self._h, None, 0)
+        buf = (C.c_float * max(n, 1))()
+        self.lib.fn["comm_trace_read"](self._h, buf, n)
+        return np.array(buf[:n], dtype=np.float32).reshape(-1, len(self.blocks), len(self.TRACE_POINTS))
 
     def close(self):
         if self._h:

@@ -128,12 +128,15 @@ def test_ad_blocks_bitwise_equal_single_domain(which, px, py):
 
 
 def test_ad_blocks_reproduce_the_reference_abort():
-    """the AD run of the 64x32 triple point aborts; the decomposition raises
-    the same error at the same step and keeps the last completed State."""
+    """the AD run of the 64x32 triple point at CFL 1.15 aborts at step 101
+    (a tangled cell in one block; the AD run is stable at the case's own
+    CFL): the decomposition raises the same error at the same step, every
+    block stops there and keeps the last completed State."""
     case = cases.triple_point(64, 32)
-    ref, r, err = _single(case, 700, abi.REMAP_AD)
-    assert err is not None
-    got, results = _blocks_device(case, 700, 2, 2, abi.REMAP_AD)
+    case.cfl = 1.15
+    ref, r, err = _single(case, 300, abi.REMAP_AD)
+    assert err is not None and r.steps_done == 101
+    got, results = _blocks_device(case, 300, 2, 2, abi.REMAP_AD)
     for a, dts, e in results:
         assert (type(e).__name__, e.what, e.i, e.j) == err[:4]
         assert a.steps_done == r.steps_done
@@ -261,3 +264,31 @@ def test_window_init_blocks_equal_single_domain(which, px, py):
         a, dts, e = b.result(steps)
         assert e is None and np.array_equal(dts, r.dts)
     assert helpers.bitwise_diff(got, ref, helpers.STATE_FIELDS) == []
+
+
+def test_comm_trace_shows_the_exchange_beside_the_owned_tiles():
+    """h2d_comm_trace: per step and block nine stream timestamps; the State
+    halo exchange enqueued after step s starts no later than step s + 1's
+    owned Lagrange tiles end (it runs beside them, on its own stream), and the
+    edge tiles end after it."""
+    case = cases.shock_bubble(256)
+    lib = helpers.product_lib()
+    specs = multi.decompose(256, 256, 2, 1)
+    blocks = [multi.BlockSolver(lib, case.cfg, sp) for sp in specs]
+    for b in blocks:
+        b.init_window(case.paint(b.window()))
+    comm = multi.DeviceComm(blocks, 2, 1)
+    comm.run(3, 1e30, case.cfl)
+    comm.trace(5)
+    comm.run(8, 1e30, case.cfl)
+    tr = comm.trace_read()
+    comm.close()
+    P = {k: q for q, k in enumerate(multi.DeviceComm.TRACE_POINTS)}
+    assert tr.shape == (5, 2, len(P))
+    assert (tr[:, :, P["ad_mid_start"]] == -1.0).all()  # DirectCF: no mid exchange
+    for s in range(1, 5):
+        for b in range(2):
+            r, prev = tr[s, b], tr[s - 1, b]
+            assert r[P["lag_owned_start"]] <= r[P["lag_owned_end"]] <= r[P["lag_edge_end"]] <= r[P["rest_end"]]
+            assert prev[P["halo_start"]] <= prev[P["halo_end"]] <= r[P["lag_edge_end"]]
+            assert prev[P["halo_start"]] <= r[P["lag_owned_end"]]
