@@ -539,7 +539,6 @@ __global__ void __launch_bounds__(LTX * LTY) k_lag_nodes(Dev d, int write_vol_la
 // (lagrange.cpp:135-142, 146-196). Q, p_half and p_mix_half never leave the
 // chip; the API path (h2d_lagrange_step) keeps the two-kernel form because
 // it returns Q.
-template <int NM>
 #ifndef H2D_FTY
 #define H2D_FTY 8
 #endif
@@ -553,22 +552,25 @@ template <int NM>
 #ifndef H2D_FMINB
 #define H2D_FMINB(NM) ((NM) == 2 ? 4 : 3)
 #endif
-__global__ void __launch_bounds__(H2D_LAG_NT, H2D_FMINB(NM)) k_lag_fused(Dev d) {
-    pdl_enter();
+#ifndef H2D_LAG_INTERIOR
+#define H2D_LAG_INTERIOR 1
+#endif
+// INT: an interior tile (uniform over the CTA, see k_lag_fused): every cell
+// of its 34 x 10 pass is a mesh cell inside the window (no ghost image, no
+// wrap), every node of its 33 x 9 pass lies inside r_lagn off the walls, and
+// every own cell is in r_lagc / r_lage and owned, so the range tests of the
+// general path are all true and are compiled out (same arithmetic, same
+// bits; C4 Lagrange 2.81 -> 2.60 ms, profiles/r02_var_laginterior.jsonl)
+template <int NM, bool INT>
+__device__ __forceinline__ void lag_fused_body(const Dev& d, const int i0, const int j0, double* s_q, double* s_pmh,
+                                               double (*s_ph)[(LTX + 2) * (H2D_FTY + 2)], double* s_mm, double* shx,
+                                               double* shy) {
     constexpr int LTY = H2D_FTY;
     constexpr int NT = H2D_LAG_NT;  // threads (>= the tile's cells; extra ones help the halo passes)
     constexpr int CW = LTX + 2, CH = LTY + 2, NC = CW * CH, NN = (LTX + 1) * (LTY + 1);
-    __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC], s_mm[NC];
-    __shared__ double shx[NN], shy[NN];
-    __shared__ int s_halt;
     const int tid = threadIdx.x;
-    if (tid == 0) s_halt = halted(d.ctl);
-    __syncthreads();
-    if (s_halt) return;
     const int nx = d.nx, ny = d.ny;
     const Rng rn = d.r_lagn;
-    const int i0 = rn.i0 + blockIdx.x * LTX, j0 = rn.j0 + blockIdx.y * LTY;
-    if (d.lag_sel && (in(d.lag_inner, i0, j0) != (d.lag_sel == 1))) return;
     const double dt = step_dt(d.ctl);
     const double cv = d.cv;
     // ---- cells [i0-1, i0+LTX] x [j0-1, j0+LTY]: Q^n and predict
@@ -576,12 +578,12 @@ __global__ void __launch_bounds__(H2D_LAG_NT, H2D_FMINB(NM)) k_lag_fused(Dev d) 
     for (int t = tid; t < NC; t += NT, rc0.step()) {
         const int ci = i0 - 1 + rc0.c, cj = j0 - 1 + rc0.r;
         double q = 0.0, pmix = 0.0, ph[NM] = {}, mmix = 0.0;
-        if (in(d.win_c, ci, cj) && ci >= -1 && cj >= -1 && ci <= nx && cj <= ny) {
-            const int i = (ci < 0 || ci >= nx) ? wrap_cell(ci, nx, d.per_x) : ci;
-            const int j = (cj < 0 || cj >= ny) ? wrap_cell(cj, ny, d.per_y) : cj;
+        if (INT || (in(d.win_c, ci, cj) && ci >= -1 && cj >= -1 && ci <= nx && cj <= ny)) {
+            const int i = (!INT && (ci < 0 || ci >= nx)) ? wrap_cell(ci, nx, d.per_x) : ci;
+            const int j = (!INT && (cj < 0 || cj >= ny)) ? wrap_cell(cj, ny, d.per_y) : cj;
             // the canonical evaluation (errors, floor counts): an own interior cell of this tile
             const bool canon = ci == i && cj == j && ci >= i0 && ci < i0 + LTX && cj >= j0 && cj < j0 + LTY &&
-                               in(d.r_lagc, i, j) && own_cell(d, i, j);
+                               (INT || (in(d.r_lagc, i, j) && own_cell(d, i, j)));
             const int c = ix(d, i, j);
             const int n10 = ix(d, i + 1, j), n01 = ix(d, i, j + 1), n11 = ix(d, i + 1, j + 1);
             const double u00x = d.ux[c], u00y = d.uy[c], u10x = d.ux[n10], u10y = d.uy[n10];
@@ -660,7 +662,7 @@ __global__ void __launch_bounds__(H2D_LAG_NT, H2D_FMINB(NM)) k_lag_fused(Dev d) 
     for (int t = tid; t < NN; t += NT, rc1.step()) {
         const int i = i0 + rc1.c, j = j0 + rc1.r;
         double hx = 0.0, hy = 0.0;
-        if (in(rn, i, j)) {
+        if (INT || in(rn, i, j)) {
             const int ta = rc1.c + rc1.r * CW;  // cell (i-1, j-1) in the cell tile
             const int tb = ta + 1, tc = ta + CW, te = tc + 1;
             const int e = ix(d, i, j);
@@ -678,9 +680,10 @@ __global__ void __launch_bounds__(H2D_LAG_NT, H2D_FMINB(NM)) k_lag_fused(Dev d) 
             // wall nodes (state.cpp:90-95) before correct reads u_half
             // (lagrange.cpp:142,155): the wall-node gradient is a rounding
             // residue of ((b + e) - a) - c with mirrored a = b, c = e
-            if (!d.per_x && (i == 0 || i == nx)) hx = 0.0;
-            if (!d.per_y && (j == 0 || j == ny)) hy = 0.0;
-            if ((i < i0 + LTX || i == rn.i1 - 1) && (j < j0 + LTY || j == rn.j1 - 1)) {
+            if (!INT && !d.per_x && (i == 0 || i == nx)) hx = 0.0;
+            if (!INT && !d.per_y && (j == 0 || j == ny)) hy = 0.0;
+            if (INT ? (i < i0 + LTX && j < j0 + LTY)
+                    : ((i < i0 + LTX || i == rn.i1 - 1) && (j < j0 + LTY || j == rn.j1 - 1))) {
                 d.uhx[e] = hx;
                 d.uhy[e] = hy;
                 d.ulx[e] = 2.0 * hx - ux;
@@ -695,8 +698,8 @@ __global__ void __launch_bounds__(H2D_LAG_NT, H2D_FMINB(NM)) k_lag_fused(Dev d) 
     if (tid >= LTX * LTY) return;
     const int tx = tid % LTX, ty = tid / LTX;
     const int i = i0 + tx, j = j0 + ty;
-    if (!in(d.r_lage, i, j)) return;
-    const bool own = own_cell(d, i, j);
+    if (!INT && !in(d.r_lage, i, j)) return;
+    const bool own = INT || own_cell(d, i, j);
     const int q00 = tx + ty * (LTX + 1), q10 = q00 + 1, q01 = q00 + LTX + 1, q11 = q01 + 1;
     bool tangled = false;
     const double vol =
@@ -731,6 +734,38 @@ __global__ void __launch_bounds__(H2D_LAG_NT, H2D_FMINB(NM)) k_lag_fused(Dev d) 
         d.el[a][n] = ea;
     }
     if (floors && own) bump_floor(d.ctl, floors);
+}
+
+template <int NM>
+__global__ void __launch_bounds__(H2D_LAG_NT, H2D_FMINB(NM)) k_lag_fused(Dev d) {
+    pdl_enter();
+    constexpr int LTY = H2D_FTY;
+    constexpr int NC = (LTX + 2) * (LTY + 2), NN = (LTX + 1) * (LTY + 1);
+    __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC], s_mm[NC];
+    __shared__ double shx[NN], shy[NN];
+    __shared__ int s_halt;
+    if (threadIdx.x == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
+    const Rng rn = d.r_lagn;
+    const int i0 = rn.i0 + blockIdx.x * LTX, j0 = rn.j0 + blockIdx.y * LTY;
+    if (d.lag_sel && (in(d.lag_inner, i0, j0) != (d.lag_sel == 1))) return;
+    // interior tile: cells [i0-1, i0+LTX] x [j0-1, j0+LTY] are mesh cells inside
+    // the window, nodes [i0, i0+LTX] x [j0, j0+LTY] lie inside r_lagn, off the
+    // walls and before the range's last row / column, the own cells inside
+    // r_lagc, r_lage and the owned range
+    bool interior = false;
+    if (H2D_LAG_INTERIOR) {
+        const int ia = i0 - 1, ib = i0 + LTX, ja = j0 - 1, jb = j0 + LTY;  // inclusive cell bounds of the pass
+        interior = ia >= 0 && ib < d.nx && ja >= 0 && jb < d.ny && in(d.win_c, ia, ja) && in(d.win_c, ib, jb) &&
+                   i0 >= 1 && ib <= d.nx - 1 && j0 >= 1 && jb <= d.ny - 1 && ib < rn.i1 - 1 && jb < rn.j1 - 1 &&
+                   in(d.r_lagc, i0, j0) && in(d.r_lagc, ib - 1, jb - 1) && in(d.r_lage, i0, j0) &&
+                   in(d.r_lage, ib - 1, jb - 1) && own_cell(d, i0, j0) && own_cell(d, ib - 1, jb - 1);
+    }
+    if (interior)
+        lag_fused_body<NM, true>(d, i0, j0, s_q, s_pmh, s_ph, s_mm, shx, shy);
+    else
+        lag_fused_body<NM, false>(d, i0, j0, s_q, s_pmh, s_ph, s_mm, shx, shy);
 }
 
 // ---------------------------------------------------------------------------
@@ -2656,6 +2691,7 @@ __global__ void __launch_bounds__(128, H2D_DUAL_MINB) k_dual_items(Dev d) {
 // X face i+1 (-), Y face j (+), Y face j+1 (-), corner (i-1, j-1, pair (1,1))
 // (-), own pairs (+, +), corner (i-1, j+1, pair (1,-1)) (-) — then
 // apply_dual_update (remap.cpp:444-464) and the wall condition (:462).
+template <int NM>
 __device__ __forceinline__ void node_update_walls_at(const Dev& d, int i, int j, double& px, double& py) {
     const int nx = d.nx, ny = d.ny;
     if (!in(d.r_node, i, j) || i < 0 || j < 0 || i > nx || j > ny) return;
@@ -2689,7 +2725,8 @@ __device__ __forceinline__ void node_update_walls_at(const Dev& d, int i, int j,
     if (fpm) { ax += -d.dc_x[1][pm]; ay += -d.dc_y[1][pm]; }
     const int c00 = pp, c10 = ix(d, i, j - 1), c01 = ix(d, i - 1, j);
     double l00 = 0.0, l10 = 0.0, l01 = 0.0, l11 = 0.0;  // make_work's mcell (remap.cpp:133-138)
-    for (int a = 0; a < d.nmat; ++a) {
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
         l00 += d.m[a][c00];
         l10 += d.m[a][c10];
         l01 += d.m[a][c01];
@@ -2704,7 +2741,8 @@ __device__ __forceinline__ void node_update_walls_at(const Dev& d, int i, int j,
     if (j == 0 || j == ny) uy = 0.0;
     d.nux[s] = ux;
     d.nuy[s] = uy;
-    d.unrm[s] = sqrt(ux * ux + uy * uy);
+    const double u2 = ux * ux + uy * uy;  // (a node at rest: sqrt(+0) = +0 without the sqrt)
+    d.unrm[s] = u2 == 0.0 ? 0.0 : sqrt(u2);
     if (d.scan_nodes && own_node(d, i, j) && (!isfinite(ux) | !isfinite(uy)))
         raise(d.ctl, ekey(PH_NAN_NODE, j, i, 0));  // nan_scan on the new u (harness.cpp:353-357)
     if (d.diag && own_node(d, i, j)) {  // compute_totals' momentum term (state.cpp:154-158)
@@ -2722,13 +2760,14 @@ __device__ __forceinline__ void node_momentum(const Dev& d, double px, double py
     warp_partial<2>(v, op, d.dsc.part[1]);
 }
 
+template <int NM>
 __global__ void k_node_update_walls(Dev d) {
     pdl_enter();
     if (halted(d.ctl)) return;  // one load per warp: warp-uniform
     int i, j;
     tid2(i, j, d.r_node.i0, d.r_node.j0);
     double px = 0.0, py = 0.0;
-    node_update_walls_at(d, i, j, px, py);
+    node_update_walls_at<NM>(d, i, j, px, py);
     node_momentum(d, px, py);
 }
 
@@ -3072,24 +3111,22 @@ __global__ void k_global_xfer(Dev d, double* buf, Rng r, double* px, double* py,
 #ifndef H2D_POST_MINB
 #define H2D_POST_MINB 5
 #endif
-template <int NM>
-__global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop) {
-    pdl_enter();
-    __shared__ unsigned long long sw[8];
-    // per-thread diagnostics terms (block of 32 x 8); fewer than three
-    // materials keep no DG_MM2 plane (its partial is written as 0)
+#ifndef H2D_POST_INTERIOR
+#define H2D_POST_INTERIOR 1
+#endif
+// INT: every cell of the block is a mesh cell inside r_sync, r_nrm and the
+// owned range (uniform over the block, see k_post): the range tests are true
+// and compiled out
+template <int NM, bool INT>
+__device__ __forceinline__ void post_body(const Dev& d, const int run_loop, unsigned long long* sw,
+                                          double (*s_dg)[256]) {
     constexpr int NDG = NM == 3 ? DG_NCELL : DG_NCELL - 1;
-    __shared__ double s_dg[NDG][256];
-    __shared__ int s_halt;
-    if (threadIdx.x == 0 && threadIdx.y == 0) s_halt = halted(d.ctl);
-    __syncthreads();
-    if (s_halt) return;
     int i, j;
     tid2(i, j, d.r_sync.i0, d.r_sync.j0);
     const int nx = d.nx, ny = d.ny;
     unsigned long long wb = 0ull;
-    const bool act = in(d.r_sync, i, j);
-    const bool interior = i >= 0 && j >= 0 && i < nx && j < ny;
+    const bool act = INT || in(d.r_sync, i, j);
+    const bool interior = INT || (i >= 0 && j >= 0 && i < nx && j < ny);
     const int c = act ? ix(d, i, j) : 0;
     const double cv = d.cv;
     double ka[NM], ma[NM], ea[NM];
@@ -3133,7 +3170,7 @@ __global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop
     // and are folded after the kernel's closing barrier
     const int tl = threadIdx.y * blockDim.x + threadIdx.x;
     if (run_loop && d.diag) {
-        const bool on = act && interior && own_cell(d, i, j);
+        const bool on = INT || (act && interior && own_cell(d, i, j));
         const double rho = div_cv(d, m);
         constexpr int sh = NM == 3 ? 0 : 1;  // plane of slot k >= DG_MINR: k - sh
         s_dg[DG_MASS][tl] = on ? m : 0.0;
@@ -3147,7 +3184,7 @@ __global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop
         s_dg[DG_MAXP - sh][tl] = on ? p : -CUDART_INF;
     }
     if (act) {
-        if (interior && in(d.r_nrm, i, j)) {
+        if (INT || (interior && in(d.r_nrm, i, j))) {
             if (NM >= 2) {  // normals of the new fractions
                 bool mixed = is_mixed(ka[0]);
                 int hi = 1;
@@ -3184,7 +3221,7 @@ __global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop
                     d.nnry[c] = nry;
                 }
             }
-            if (run_loop && own_cell(d, i, j)) {
+            if (run_loop && (INT || own_cell(d, i, j))) {
                 if (!isfinite(m) | !isfinite(emix) | !isfinite(p)) raise(d.ctl, ekey(PH_NAN_CELL, j, i, 0));
                 // next step's wave speed on the new State (cs from above)
                 if (cs_bad) atomicMin(&d.ctl->next_err_key, ekey(PH_CFL_UNPHYS, j, i, 0));
@@ -3226,6 +3263,31 @@ __global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop
             if (NM < 3 && t == 0) part[DG_MM2] = 0.0;
         }
     }
+}
+
+template <int NM>
+__global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop) {
+    pdl_enter();
+    __shared__ unsigned long long sw[8];
+    // per-thread diagnostics terms (block of 32 x 8); fewer than three
+    // materials keep no DG_MM2 plane (its partial is written as 0)
+    constexpr int NDG = NM == 3 ? DG_NCELL : DG_NCELL - 1;
+    __shared__ double s_dg[NDG][256];
+    __shared__ int s_halt;
+    if (threadIdx.x == 0 && threadIdx.y == 0) s_halt = halted(d.ctl);
+    __syncthreads();
+    if (s_halt) return;
+    bool interior = false;
+    if (H2D_POST_INTERIOR) {
+        const int ia = d.r_sync.i0 + (int)(blockIdx.x * blockDim.x), ja = d.r_sync.j0 + (int)(blockIdx.y * blockDim.y);
+        const int ib = ia + (int)blockDim.x - 1, jb = ja + (int)blockDim.y - 1;
+        interior = ia >= 0 && ja >= 0 && ib < d.nx && jb < d.ny && in(d.r_sync, ia, ja) && in(d.r_sync, ib, jb) &&
+                   in(d.r_nrm, ia, ja) && in(d.r_nrm, ib, jb) && own_cell(d, ia, ja) && own_cell(d, ib, jb);
+    }
+    if (interior)
+        post_body<NM, true>(d, run_loop, sw, s_dg);
+    else
+        post_body<NM, false>(d, run_loop, sw, s_dg);
 }
 
 // ---------------------------------------------------------------------------
@@ -4124,7 +4186,9 @@ void launch_remap_dual(const Dev& d, cudaStream_t s) {
         if (d.per_x || d.per_y)  // periodic seams reorder the node sums: sorted gather
             pdl(k_node_update, grid_of(d.r_node), blk2(), 0, s, d);
         else
-            pdl(k_node_update_walls, grid_of(d.r_node), blk2(), 0, s, d);
+            d.nmat == 3   ? pdl(k_node_update_walls<3>, grid_of(d.r_node), blk2(), 0, s, d)
+            : d.nmat == 2 ? pdl(k_node_update_walls<2>, grid_of(d.r_node), blk2(), 0, s, d)
+                          : pdl(k_node_update_walls<1>, grid_of(d.r_node), blk2(), 0, s, d);
     }
 }
 
