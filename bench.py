@@ -406,7 +406,7 @@ def run_product(args, world, rank, local, pg):
                                 "sample": f"{case.name}: {where}first {n} steps from t=0, single thread, "
                                           f"{secs:.1f} s"}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def run_product_multi(args, world, rank, local, pg):
@@ -495,7 +495,7 @@ def run_product_multi(args, world, rank, local, pg):
         "clocks": clk,
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def run_reference(args, world, rank, pg):
@@ -522,10 +522,31 @@ def run_reference(args, world, rank, pg):
                                    f"thread (the reference has no threading), {secs:.1f} s"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_OUT = None
+
+
+def quiet_stdout():
+    """Keep stdout for the ONE JSON line: file descriptor 1 is pointed at
+    stderr for the rest of the run, so a library that writes to the C stdout
+    (NCCL prints its version banner there) cannot add lines to it."""
+    global _OUT
+    if _OUT is None:
+        sys.stdout.flush()
+        _OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    out = _OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    quiet_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

@@ -1463,23 +1463,28 @@ __device__ __forceinline__ void finalize_cell(const Dev& d, const Rng& rg, int i
 }
 
 // A mapped tile's cell (k_remap_tile MAP): slots 0 / 1 hold materials mat0 <
-// mat1; the absent material rabs contributes exactly what the three-material
-// gather gives it -- its m, m * e_lag and k * v, no flux -- and the cell is
-// finalised by the three-material rule (vf: the volume its k multiplies, cv on
-// the quiescent path, the Lagrangian volume otherwise)
-// (NS slots: NS = 2 in a three-material context, NS = 1 in a two-material one)
-template <int NS>
+// mat1 of a context with NC materials; every absent material contributes
+// exactly what the NC-material gather gives it -- its m, m * e_lag and k * v,
+// no flux -- and the cell is finalised by the NC-material rule (vf: the
+// volume its k multiplies, cv on the quiescent path, the Lagrangian volume
+// otherwise). (NS, NC) = (2, 3): one material absent from a three-material
+// tile; (1, 2): from a two-material tile; (1, 3): a three-material context's
+// tile that holds one material only.
+template <int NS, int NC>
 __device__ __forceinline__ void finalize_mapped(const Dev& d, const Rng& rg, int i, int j, int c, int tx, bool own,
                                                 const double* ms, const double* mes, const double* vas, int mat0,
-                                                int mat1, int rabs, double vf) {
-    constexpr int NC = NS + 1;
-    const double m0 = d.m[rabs][c];
-    const double mer = m0 * d.el[rabs][c], var = d.k[rabs][c] * vf;
+                                                int mat1, double vf) {
     // built with constant indices (selects), so the vectors stay in registers
     double m[NC], me[NC], va[NC];
 #pragma unroll
     for (int a = 0; a < NC; ++a) {
         const bool s0 = a == mat0, s1 = NS == 2 && a == mat1;
+        double m0 = 0.0, mer = 0.0, var = 0.0;
+        if (!s0 && !s1) {  // an absent material: its own planes
+            m0 = d.m[a][c];
+            mer = m0 * d.el[a][c];
+            var = d.k[a][c] * vf;
+        }
         m[a] = s0 ? ms[0] : (s1 ? ms[NS - 1] : m0);
         me[a] = s0 ? mes[0] : (s1 ? mes[NS - 1] : mer);
         va[a] = s0 ? vas[0] : (s1 ? vas[NS - 1] : var);
@@ -1538,6 +1543,11 @@ template <int NM, bool XC = false, bool DIR = false, bool MAP = false>
 #ifndef H2D_RT_MAP2
 #define H2D_RT_MAP2 0
 #endif
+// H2D_RT_MAP31: a three-material context's tile that holds ONE material runs
+// the one-slot kernel (class 4 + p)
+#ifndef H2D_RT_MAP31
+#define H2D_RT_MAP31 1
+#endif
 #ifndef H2D_RT_SPLITBAR
 #define H2D_RT_SPLITBAR 1
 #endif
@@ -1558,14 +1568,25 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     const int tid = threadIdx.x;
     // three materials with tile classes: each tile runs in exactly one of the
     // two launches (uniform over the CTA, before any copy is issued)
-    int rabs = 3;  // MAP: the absent material; slot a holds material mat(a)
+    // tile class (k_tile_class): 0..2 = that material is absent (two slots of a
+    // three-material context, one slot of a two-material one), 3 = the
+    // context's own kernel, 4..6 = a three-material context's tile holding
+    // only material cls - 4 (one slot); slot a holds material mat(a)
+    int rabs = 3;
     if (MAP || (NM >= 2 && !XC && !DIR && d.tcls)) {
         rabs = d.tcls[blockIdx.y * gridDim.x + blockIdx.x];
-        if (MAP ? rabs == 3 : rabs != 3) return;
+        if (!MAP) {
+            if (rabs != 3) return;
+        } else if (NM == 2) {
+            if (rabs > 2) return;
+        } else {
+            if (d.nmat == 3 ? rabs < 4 : rabs > 1) return;
+        }
     }
     // NM = 2 slots of a three-material context: the two present materials in
     // order; NM = 1 slot of a two-material context: the present one
-    const int mat0 = MAP ? (NM == 2 ? (rabs == 0 ? 1 : 0) : 1 - rabs) : 0, mat1 = MAP ? (rabs == 2 ? 1 : 2) : 1;
+    const int mat0 = MAP ? (NM == 2 ? (rabs == 0 ? 1 : 0) : (d.nmat == 3 ? rabs - 4 : 1 - rabs)) : 0,
+              mat1 = MAP ? (rabs == 2 ? 1 : 2) : 1;
     auto mat = [&](int a) { return MAP ? (a == 0 ? mat0 : mat1) : a; };
     const int nx = d.nx, ny = d.ny;
     const Rng rg = d.r_gath;
@@ -1575,7 +1596,18 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     // gathered, and land outside every range a later phase reads)
     const int sx = tile_shift(d);
     const int i0 = rg.i0 - sx + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
+    // the 128-byte-aligned start of the tile as an OFFSET from the shared array
+    // (not a pointer rebuilt from an integer: the compiler then keeps the
+    // shared address space and emits LDS / STS with 32-bit addresses instead
+    // of generic LD / ST for every tile access)
+#ifndef H2D_RT_SMEMPTR
+#define H2D_RT_SMEMPTR 1
+#endif
+#if H2D_RT_SMEMPTR
+    char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+#else
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+#endif
     const Tile<NM> T = carve_tile<NM, DIR>(smem, i0 - G, j0 - G);
     // ---- phase 0: one thread stages the tile + halo with TMA (2D boxes of
     // the planes, zero-filled past the plane): u_half on the node region,
@@ -1660,8 +1692,10 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
                 me[a] = m0 * T.el[a][tc];
                 va[a] = (NM >= 2 ? T.kk[a][tc] : T.vl[tc]) * cv;
             }
-            if (MAP)
-                finalize_mapped<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va, mat0, mat1, rabs, cv);
+            if (MAP && NM == 1 && d.nmat == 3)
+                finalize_mapped<NM, 3>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va, mat0, mat1, cv);
+            else if (MAP)
+                finalize_mapped<NM, NM + 1>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va, mat0, mat1, cv);
             else
                 finalize_cell<NM>(d, rg, i, j, c, tx, own_cell(d, i, j), m, me, va);
             return;
@@ -1897,8 +1931,10 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
             for (int a = 0; a < NM; ++a) add(a, cq[q], donor);
         }
     }
-    if (MAP)
-        finalize_mapped<NM>(d, rg, i, j, c, tx, own, m, me, va, mat0, mat1, rabs, T.vl[tc]);
+    if (MAP && NM == 1 && d.nmat == 3)
+        finalize_mapped<NM, 3>(d, rg, i, j, c, tx, own, m, me, va, mat0, mat1, T.vl[tc]);
+    else if (MAP)
+        finalize_mapped<NM, NM + 1>(d, rg, i, j, c, tx, own, m, me, va, mat0, mat1, T.vl[tc]);
     else
         finalize_cell<NM>(d, rg, i, j, c, tx, own, m, me, va);
 }
@@ -4015,7 +4051,7 @@ __global__ void __launch_bounds__(RTX * RTY) k_tile_class(Dev d) {
     const int i0 = rg.i0 - tile_shift(d) + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
     const int x0 = i0 - G + d.H - d.oi, y0 = j0 - G + d.H - d.oj;  // plane column / row of the region origin
     const int R = d.fsz / d.P;
-    unsigned pres = 0u, ok = (1u << NM) - 1u;
+    unsigned pres = 0u, ok = (1u << NM) - 1u, pure = (1u << NM) - 1u;  // pure: k_a >= 1 - kPureTol in every region cell
     for (int t = tid; t < RCW * RCH; t += RTX * RTY) {
         const int x = x0 + t % RCW, y = y0 + t / RCW;
         double k[NM];
@@ -4031,26 +4067,40 @@ __global__ void __launch_bounds__(RTX * RTY) k_tile_class(Dev d) {
             }
         }
 #pragma unroll
-        for (int r = 0; r < NM; ++r)
+        for (int r = 0; r < NM; ++r) {
             if (!(NM == 3 ? map_ok(k, r) : map_ok2(k, r))) ok &= ~(1u << r);
+            if (!(k[r] >= 1.0 - kPureTol)) pure &= ~(1u << r);
+        }
     }
-    __shared__ unsigned s_pres, s_ok;
+    __shared__ unsigned s_pres, s_ok, s_pure;
     if (tid == 0) {
         s_pres = 0u;
         s_ok = (1u << NM) - 1u;
+        s_pure = (1u << NM) - 1u;
     }
     __syncthreads();
     pres = __reduce_or_sync(0xffffffffu, pres);
     ok = __reduce_and_sync(0xffffffffu, ok);
+    pure = __reduce_and_sync(0xffffffffu, pure);
     if ((tid & 31) == 0) {
         atomicOr(&s_pres, pres);
         atomicAnd(&s_ok, ok);
+        atomicAnd(&s_pure, pure);
     }
     __syncthreads();
     if (tid == 0) {
         int cls = 3;
         for (int r = NM - 1; r >= 0 && cls == 3; --r)
             if (!((s_pres >> r) & 1u) && ((s_ok >> r) & 1u)) cls = r;
+        // three materials, ONE present (p) and pure in every region cell: the
+        // two-slot mapping (either absent material, both conditions hold) whose
+        // second slot is absent too and meets the two-material condition
+        // (map_ok2: every region cell pure p), i.e. the one-material kernel
+        if (NM == 3 && H2D_RT_MAP31)
+            for (int p = 0; p < 3; ++p) {
+                const unsigned others = 7u & ~(1u << p);
+                if (s_pres == (1u << p) && (s_ok & others) == others && ((s_pure >> p) & 1u)) cls = 4 + p;
+            }
         d.tcls[blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)cls;
     }
 }
@@ -4085,6 +4135,8 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
             pdl(k_remap_tile<3, true>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, dx, *d.tma);
         } else if (d.tcls && H2D_RT_MAP3) {  // per-tile: two-slot kernel where a material is absent
             pdl(k_tile_class<3>, gft, dim3(RTX * RTY), 0, s, d);
+            if (H2D_RT_MAP31)
+                pdl(k_remap_tile<1, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
             pdl(k_remap_tile<2, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
             pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
         } else {
