@@ -62,6 +62,8 @@ struct h2d_ctx {
     size_t flush_bytes = 0;
     void* diag_mem = nullptr;       // DiagRed scratch of k_post / the node update
     void* tcls_mem = nullptr;       // Dev::tcls, the remap tiles' material classes
+    void* pcls_mem = nullptr;       // Dev::pcls, the post blocks' classification masks
+    void* tlist_mem = nullptr;      // Dev::tcnt + Dev::tlist, the per-class tile lists
     size_t diag_tick_bytes = 0;     // the ticket words at the start of diag_mem
     double* diag_log = nullptr;     // device StepDiag log of h2d_run (kDiagRec doubles per step)
     cudaGraphExec_t graph_rest[2] = {nullptr, nullptr};  // block data plane: the step after the Lagrange kernel
@@ -396,7 +398,11 @@ int ensure_derived(h2d_ctx* c) {
 
 // cfl_dt of the current State into the control block's "next" slots, which
 // the first k_step_start of a run consumes (later steps get them from k_post)
-void enqueue_cfl_next(h2d_ctx* c) { launch_cfl_next(make_dev(c, c->cur, 1), c->st); }
+void enqueue_cfl_next(h2d_ctx* c) {
+    const Dev d = make_dev(c, c->cur, 1);
+    launch_cfl_next(d, c->st);
+    launch_cls_flags(d, c->st);  // and the tile-classification masks of the current State (Dev::pcls)
+}
 
 // The run-loop step is a fixed sequence of ~20 kernels whose arguments only
 // depend on the State parity: capture it once per parity as a CUDA graph and
@@ -787,12 +793,37 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
         const int w = d.r_gath.i1 - (d.r_gath.i0 - shift), h = d.r_gath.j1 - d.r_gath.j0;
         d.tq_nx = std::max(1, (w + remap_tile_w() - 1) / remap_tile_w());
         d.tq_ny = std::max(1, (h + remap_tile_h() - 1) / remap_tile_h());
+        d.tlist = d.tcnt = nullptr;
+        d.tlist_cap = 0;
         if (nm >= 2) {
             const size_t n = (size_t)d.tq_nx * d.tq_ny;
             if (cudaMalloc(&c->tcls_mem, n) != cudaSuccess) return fail(H2D_ERR_NOMEM);
             if (cudaMemset(c->tcls_mem, 3, n) != cudaSuccess) return fail(H2D_ERR_DEVICE);
             d.tcls = static_cast<uint8_t*>(c->tcls_mem);
+            if (remap_uses_lists() && remap_uses_classes(nm)) {  // Dev::tlist: 4 counters, then nm lists of n tiles
+                if (cudaMalloc(&c->tlist_mem, (4 + (size_t)nm * n) * sizeof(int)) != cudaSuccess)
+                    return fail(H2D_ERR_NOMEM);
+                if (cudaMemset(c->tlist_mem, 0, (4 + (size_t)nm * n) * sizeof(int)) != cudaSuccess)
+                    return fail(H2D_ERR_DEVICE);
+                d.tcnt = static_cast<int*>(c->tlist_mem);
+                d.tlist = d.tcnt + 4;
+                d.tlist_cap = (int)n;
+            }
         }
+    }
+#ifndef H2D_CLS_POST
+#define H2D_CLS_POST 1
+#endif
+    d.pcls = nullptr;
+    d.pcls_nx = 0;
+    d.cls_post = 0;
+    if (H2D_CLS_POST && remap_uses_classes(nm) && !block) {  // Dev::pcls, one mask per k_post block (over r_sync)
+        const int pw = (d.r_sync.i1 - d.r_sync.i0 + 31) / 32, ph = (d.r_sync.j1 - d.r_sync.j0 + 7) / 8;
+        const size_t n = (size_t)std::max(1, pw) * std::max(1, ph);
+        if (cudaMalloc(&c->pcls_mem, n * sizeof(uint16_t)) != cudaSuccess) return fail(H2D_ERR_NOMEM);
+        if (cudaMemset(c->pcls_mem, 0xFF, n * sizeof(uint16_t)) != cudaSuccess) return fail(H2D_ERR_DEVICE);
+        d.pcls = static_cast<uint16_t*>(c->pcls_mem);
+        d.pcls_nx = std::max(1, pw);
     }
     if (ctl_push(c)) return fail(H2D_ERR_DEVICE);
     // make_state defaults (state.cpp:5-23): k0 = 1, normals (1, 0), vol = dx*dy
@@ -834,6 +865,8 @@ void h2d_destroy(h2d_ctx* c) {
     if (c->diag_log) cudaFree(c->diag_log);
     if (c->diag_mem) cudaFree(c->diag_mem);
     if (c->tcls_mem) cudaFree(c->tcls_mem);
+    if (c->pcls_mem) cudaFree(c->pcls_mem);
+    if (c->tlist_mem) cudaFree(c->tlist_mem);
     if (c->xbuf) cudaFree(c->xbuf);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
@@ -1469,6 +1502,7 @@ int h2d_step_timed(h2d_ctx* c, double cfl, double t_end, int phases, int remap_k
         d.scan_nodes = 1;  // as the run-loop graph
         d.diag = 1;
         d.direct = dir;
+        d.cls_post = d.pcls != nullptr;
         CK(cudaEventRecord(c->ev[0], c->st));
         launch_step_start(d, c->st);
         CK(cudaEventRecord(c->ev[1], c->st));

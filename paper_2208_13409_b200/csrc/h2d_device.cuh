@@ -230,6 +230,18 @@ struct Dev {
     // every tile runs the kernel of its NM.
     uint8_t* tcls;
     int tq_nx, tq_ny;
+    // single domain: the classification masks (cell_cls_mask) ORed per k_post
+    // block (32 x 8 cells over r_sync, pcls_nx blocks per row), written by
+    // k_post for the State it produces; cls_post: this launch sequence is a
+    // run-loop step, whose tile classes come from them (k_tile_class_post)
+    uint16_t* pcls;
+    int pcls_nx, cls_post;
+    // per-class tile lists (k_remap_tile, H2D_RT_LISTS): slot s (= slots of the
+    // kernel - 1) holds tcnt[s] tile indices at tlist[s * tlist_cap ...],
+    // appended by the classification kernel of the step. Null: the class
+    // kernels run over the whole tile grid.
+    int *tlist, *tcnt;
+    int tlist_cap;
 };
 
 // 32-bit plane offsets: P * R < 2^31 for every mesh up to 16384^2 (checked at

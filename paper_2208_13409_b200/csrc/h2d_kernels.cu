@@ -1560,11 +1560,18 @@ template <int NM, bool XC = false, bool DIR = false, bool MAP = false>
 #ifndef H2D_RT_MINB3
 #define H2D_RT_MINB3 2
 #endif
-__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ? H2D_RT_MINB2 : H2D_RT_MINB3)) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
-    pdl_enter();
-    extern __shared__ __align__(128) char smem_raw[];
-    __shared__ int s_halt;
-    __shared__ __align__(8) uint64_t s_bar, s_bar2;
+// H2D_RT_LISTS: tile classes dispatched through per-class tile lists and
+// persistent CTAs (k_remap_tile) instead of whole-grid launches whose CTAs of
+// another class exit at once
+#ifndef H2D_RT_LISTS
+#define H2D_RT_LISTS 1
+#endif
+// One tile (bx, by) of class rabs; par: the parity of the mbarrier phase this
+// call completes (a persistent CTA runs one tile after another on the same
+// two mbarriers, initialised once by the kernel)
+__device__ __forceinline__ void remap_tile_body(const Dev& d, const TmaSet& tm, const int bx, const int by,
+                                                const int rabs, const uint32_t par, char* smem_raw, int& s_halt,
+                                                uint64_t& s_bar, uint64_t& s_bar2) {
     const int tid = threadIdx.x;
     // three materials with tile classes: each tile runs in exactly one of the
     // two launches (uniform over the CTA, before any copy is issued)
@@ -1572,17 +1579,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     // three-material context, one slot of a two-material one), 3 = the
     // context's own kernel, 4..6 = a three-material context's tile holding
     // only material cls - 4 (one slot); slot a holds material mat(a)
-    int rabs = 3;
-    if (MAP || (NM >= 2 && !XC && !DIR && d.tcls)) {
-        rabs = d.tcls[blockIdx.y * gridDim.x + blockIdx.x];
-        if (!MAP) {
-            if (rabs != 3) return;
-        } else if (NM == 2) {
-            if (rabs > 2) return;
-        } else {
-            if (d.nmat == 3 ? rabs < 4 : rabs > 1) return;
-        }
-    }
+    // (the kernel below picks the tiles of this instantiation's classes)
     // NM = 2 slots of a three-material context: the two present materials in
     // order; NM = 1 slot of a two-material context: the present one
     const int mat0 = MAP ? (NM == 2 ? (rabs == 0 ? 1 : 0) : (d.nmat == 3 ? rabs - 4 : 1 - rabs)) : 0,
@@ -1595,7 +1592,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     // grid one column left (the extra column's items are computed, never
     // gathered, and land outside every range a later phase reads)
     const int sx = tile_shift(d);
-    const int i0 = rg.i0 - sx + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
+    const int i0 = rg.i0 - sx + bx * RTX, j0 = rg.j0 + by * RTY;
     // the 128-byte-aligned start of the tile as an OFFSET from the shared array
     // (not a pointer rebuilt from an integer: the compiler then keeps the
     // shared address space and emits LDS / STS with 32-bit addresses instead
@@ -1625,8 +1622,6 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     constexpr bool kSplit = H2D_RT_SPLITBAR != 0;
     uint64_t* bar_c = kSplit ? &s_bar2 : &s_bar;
     if (tid == 0) {
-        mbar_init(&s_bar, 1);
-        if (kSplit) mbar_init(&s_bar2, 1);
         constexpr uint32_t nbytes = 2u * RNW * RNH * 8u, cbytes = 3u * NM * RCW * RCH * 8u;
         const int x = T.ci0 + d.H - d.oi, y = T.cj0 + d.H - d.oj;  // plane column / row of the region origin
         mbar_expect_tx(&s_bar, kSplit ? nbytes : nbytes + cbytes);
@@ -1646,12 +1641,12 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
     __syncthreads();
     if (s_halt) {
         if (tid == 0) {
-            mbar_wait(&s_bar, 0);
-            if (kSplit) mbar_wait(bar_c, 0);
+            mbar_wait(&s_bar, par);
+            if (kSplit) mbar_wait(bar_c, par);
         }
         return;
     }
-    mbar_wait(&s_bar, 0);
+    mbar_wait(&s_bar, par);
     // ---- quiescent tile: u_half == 0 at every node of the tile's faces and
     // corners makes every face / corner flux volume of the tile zero, so no
     // flux is gathered (the reference skips zero volumes, remap.cpp:860,929),
@@ -1669,7 +1664,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
             }
         }
         if (!__syncthreads_or(moving)) {
-            if (kSplit) mbar_wait(bar_c, 0);
+            if (kSplit) mbar_wait(bar_c, par);
             const int ni1 = min(nx, rg.i1), nj1 = min(ny, rg.j1);
             RowCol<RTX + 1, RTX * RTY> rz(tid);
             for (int t = tid; t < NCF; t += RTX * RTY, rz.step()) {
@@ -1746,7 +1741,7 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
         T.fydv[t] = fyv;
     }
     __syncthreads();
-    if (kSplit) mbar_wait(bar_c, 0);
+    if (kSplit) mbar_wait(bar_c, par);
     // ---- phase 2, cell items: Lagrangian volume, densities, centroids,
     // interfaces (remap.cpp:769-824)
     RowCol<RCW, RTX * RTY> rs3(tid);
@@ -1939,6 +1934,56 @@ __global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ?
         finalize_cell<NM>(d, rg, i, j, c, tx, own, m, me, va);
 }
 
+
+// The launch: one tile per CTA (the grid is the tile grid), or -- contexts
+// with tile classes and H2D_RT_LISTS -- persistent CTAs that take the tiles of
+// this instantiation's classes from the class's list (Dev::tlist, written by
+// the classification kernel) one after another.
+template <int NM, bool XC = false, bool DIR = false, bool MAP = false>
+__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ? H2D_RT_MINB2 : H2D_RT_MINB3)) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
+    pdl_enter();
+    extern __shared__ __align__(128) char smem_raw[];
+    __shared__ int s_halt;
+    __shared__ __align__(8) uint64_t s_bar, s_bar2;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        if (H2D_RT_SPLITBAR) mbar_init(&s_bar2, 1);
+    }
+    const bool classes = MAP || (NM >= 2 && !XC && !DIR && d.tcls);
+    const bool listed = classes && d.tlist;  // slot NM - 1 holds this instantiation's tiles
+    int n = 1, q = 0, stride = 1;
+    if (listed) {
+        n = d.tcnt[NM - 1];
+        q = blockIdx.x;
+        stride = gridDim.x;
+    }
+    uint32_t par = 0;
+    for (; q < n; q += stride) {  // (one call site: the body is inlined once)
+        // tile class (k_tile_class): 0..2 = that material is absent (two slots of
+        // a three-material context, one slot of a two-material one), 3 = the
+        // context's own kernel, 4..6 = a three-material context's tile holding
+        // only material cls - 4 (one slot); slot a holds material mat(a)
+        int bx = blockIdx.x, by = blockIdx.y, rabs = 3;
+        if (listed) {
+            const int t = d.tlist[(size_t)(NM - 1) * d.tlist_cap + q];
+            bx = t % d.tq_nx;
+            by = t / d.tq_nx;
+            rabs = d.tcls[t];
+        } else if (classes) {
+            rabs = d.tcls[blockIdx.y * gridDim.x + blockIdx.x];
+            if (!MAP) {
+                if (rabs != 3) return;
+            } else if (NM == 2) {
+                if (rabs > 2) return;
+            } else {
+                if (d.nmat == 3 ? rabs < 4 : rabs > 1) return;
+            }
+        }
+        remap_tile_body<NM, XC, DIR, MAP>(d, tm, bx, by, rabs, par, smem_raw, s_halt, s_bar, s_bar2);
+        par ^= 1u;
+        if (listed) __syncthreads();  // every thread is done with the tile's shared memory before the next copies land
+    }
+}
 
 __device__ __forceinline__ void sliver_offset(int lane, int& di, int& dj, int& ring) {
     if (lane < 8) {  // ring 1: (dj, di) row-major, centre skipped
@@ -3147,6 +3192,90 @@ __global__ void k_global_xfer(Dev d, double* buf, Rng r, double* px, double* py,
 #ifndef H2D_POST_MINB
 #define H2D_POST_MINB 5
 #endif
+// Three materials: the class of each remap tile (Dev::tcls). A material r is
+// absent from a tile when no cell of the tile's staged region (the 36 x 12
+// TMA box, zero past the plane) has k_r > 0 or m_r != 0. The two-slot kernel
+// on the other two materials (lo < hi) is then the three-material kernel,
+// given that every region cell satisfies
+//  * a cell holding lo alone is not mixed in the two-material sense
+//    (mixed3 == is_mixed(k_lo), remap.cpp:100 / oracle mixed3), and
+//  * a non-mixed donor's material is the same: largest3(k) == (k_lo < 0.5 ?
+//    hi : lo) (remap.cpp:255-263 / oracle split_flux);
+// (with k_r = 0 the mixed split, the interface fraction and the degrade
+// tests reduce to the two-material expressions term by term). The class is
+// the highest such r, else 3.
+__device__ __forceinline__ bool map_ok(const double* k, int r) {
+    const int lo = r == 0 ? 1 : 0, hi = r == 2 ? 1 : 2;
+    if (k[lo] > 0.0 && !(k[hi] > 0.0) && is_mixed(k[lo])) return false;
+    if (!mixed3(k) && largest3(k) != (k[lo] < 0.5 ? hi : lo)) return false;
+    return true;
+}
+// Two materials: with r absent the one-material kernel on p = 1 - r is the
+// two-material one when every region cell is pure p in the reference's
+// sense (k_p >= 1 - kPureTol): no cell is mixed (remap.cpp:100), every donor
+// is p's (k0 < 0.5 <=> p = 1, remap.cpp:263) and no stencil degrades to
+// first order (remap.cpp:270-283).
+__device__ __forceinline__ bool map_ok2(const double* k, int r) { return k[1 - r] >= 1.0 - kPureTol; }
+
+// One cell's terms of the tile classification (k_tile_class): material a is
+// present (bits 0-2), the mapping condition of "r absent" fails (bits 3-5),
+// k_a is not pure (bits 6-8); OR over the cells of a tile's staged region
+template <int NM>
+__device__ __forceinline__ unsigned cell_cls_mask(const double* k, const double* m) {
+    unsigned mk = 0u;
+#pragma unroll
+    for (int r = 0; r < NM; ++r) {
+        if (k[r] > 0.0 || m[r] != 0.0) mk |= 1u << r;
+        if (!(NM == 3 ? map_ok(k, r) : map_ok2(k, r))) mk |= 8u << r;
+        if (!(k[r] >= 1.0 - kPureTol)) mk |= 64u << r;
+    }
+    return mk;
+}
+// the list (Dev::tlist slot) a tile of class cls goes to: slot = slots of the
+// kernel that runs it - 1
+template <int NM>
+__device__ __forceinline__ int cls_slot(int cls) {
+    if (cls == 3) return NM - 1;
+    if (NM == 3) return cls < 3 ? 1 : 0;
+    return 0;  // two materials: one absent
+}
+// append tile t to its class's list; called by every thread of a warp
+// (tiles: one thread each; valid = this lane has a tile): one atomic per
+// warp and slot
+template <int NM>
+__device__ __forceinline__ void list_append(const Dev& d, int t, int cls, bool valid) {
+    if (!d.tlist) return;
+    const int slot = valid ? cls_slot<NM>(cls) : -1;
+    const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int sl = 0; sl < NM; ++sl) {
+        const unsigned m = __ballot_sync(0xffffffffu, slot == sl);
+        if (!m) continue;
+        int base = 0;
+        if (lane == (unsigned)(__ffs(m) - 1)) base = atomicAdd(&d.tcnt[sl], __popc(m));
+        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+        if (slot == sl) d.tlist[(size_t)sl * d.tlist_cap + base + __popc(m & ((1u << lane) - 1u))] = t;
+    }
+}
+// the class of a tile from the OR of its region's cell masks (see k_tile_class)
+template <int NM>
+__device__ __forceinline__ int cls_of_mask(unsigned mk) {
+    const unsigned pres = mk & 7u, ok = ~(mk >> 3) & 7u, pure = ~(mk >> 6) & 7u;
+    int cls = 3;
+    for (int r = NM - 1; r >= 0 && cls == 3; --r)
+        if (!((pres >> r) & 1u) && ((ok >> r) & 1u)) cls = r;
+    // three materials, ONE present (p) and pure in every region cell: the
+    // two-slot mapping (either absent material, both conditions hold) whose
+    // second slot is absent too and meets the two-material condition
+    // (map_ok2: every region cell pure p), i.e. the one-material kernel
+    if (NM == 3 && H2D_RT_MAP31)
+        for (int p = 0; p < 3; ++p) {
+            const unsigned others = 7u & ~(1u << p);
+            if (pres == (1u << p) && (ok & others) == others && ((pure >> p) & 1u)) cls = 4 + p;
+        }
+    return cls;
+}
+
 #ifndef H2D_POST_INTERIOR
 #define H2D_POST_INTERIOR 1
 #endif
@@ -3155,7 +3284,7 @@ __global__ void k_global_xfer(Dev d, double* buf, Rng r, double* px, double* py,
 // and compiled out
 template <int NM, bool INT>
 __device__ __forceinline__ void post_body(const Dev& d, const int run_loop, unsigned long long* sw,
-                                          double (*s_dg)[256]) {
+                                          double (*s_dg)[256], unsigned* s_cls) {
     constexpr int NDG = NM == 3 ? DG_NCELL : DG_NCELL - 1;
     int i, j;
     tid2(i, j, d.r_sync.i0, d.r_sync.j0);
@@ -3173,6 +3302,7 @@ __device__ __forceinline__ void post_body(const Dev& d, const int run_loop, unsi
     // wave-speed block below only adds |u|)
     double cs = 0.0;
     bool cs_bad = false;
+    unsigned cmk = 0u;  // this cell's classification mask (cell_cls_mask)
     if (act) {
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
@@ -3193,6 +3323,7 @@ __device__ __forceinline__ void post_body(const Dev& d, const int run_loop, unsi
             if (run_loop) cs += ka[a] * sound(d, a, rho_a, pa, cs_bad);
         }
         emix = m > 0.0 ? me / m : 0.0;
+        if (NM >= 2 && run_loop && d.pcls) cmk = cell_cls_mask<NM>(ka, ma);  // for the next step's tile classes
         if (!run_loop) {  // the run loop keeps no derived planes (rebuilt when the State is read)
             d.nm_mix[c] = m;
             d.ne_mix[c] = emix;
@@ -3279,10 +3410,15 @@ __device__ __forceinline__ void post_body(const Dev& d, const int run_loop, unsi
         }
         const int t = threadIdx.y * blockDim.x + threadIdx.x;
         if ((t & 31) == 0) sw[t >> 5] = wb;
+        if (NM >= 2 && d.pcls) {  // (every thread of the block is here: no early exit above)
+            cmk = __reduce_or_sync(0xffffffffu, cmk);
+            if ((t & 31) == 0 && cmk) atomicOr(s_cls, cmk);
+        }
         __syncthreads();
         if (t == 0) {
             for (int w = 1; w < (int)(blockDim.x * blockDim.y) / 32; ++w) wb = sw[w] > wb ? sw[w] : wb;
             if (wb) atomicMax(&d.ctl->next_wmax_bits, wb);
+            if (NM >= 2 && d.pcls) d.pcls[blockIdx.y * gridDim.x + blockIdx.x] = (uint16_t)*s_cls;
         }
         if (d.diag) {  // warp w folds diagnostics planes w, w + 8 over the block's 256 cells (fixed order)
             double* part = d.dsc.part[0] + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * DG_NCELL;
@@ -3310,7 +3446,11 @@ __global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop
     constexpr int NDG = NM == 3 ? DG_NCELL : DG_NCELL - 1;
     __shared__ double s_dg[NDG][256];
     __shared__ int s_halt;
-    if (threadIdx.x == 0 && threadIdx.y == 0) s_halt = halted(d.ctl);
+    __shared__ unsigned s_cls;
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        s_halt = halted(d.ctl);
+        s_cls = 0u;
+    }
     __syncthreads();
     if (s_halt) return;
     bool interior = false;
@@ -3321,9 +3461,9 @@ __global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop
                    in(d.r_nrm, ia, ja) && in(d.r_nrm, ib, jb) && own_cell(d, ia, ja) && own_cell(d, ib, jb);
     }
     if (interior)
-        post_body<NM, true>(d, run_loop, sw, s_dg);
+        post_body<NM, true>(d, run_loop, sw, s_dg, &s_cls);
     else
-        post_body<NM, false>(d, run_loop, sw, s_dg);
+        post_body<NM, false>(d, run_loop, sw, s_dg, &s_cls);
 }
 
 // ---------------------------------------------------------------------------
@@ -4018,31 +4158,6 @@ void launch_remap_core(const Dev& d, cudaStream_t s) {
     launch_remap_dual(d, s);
 }
 
-// Three materials: the class of each remap tile (Dev::tcls). A material r is
-// absent from a tile when no cell of the tile's staged region (the 36 x 12
-// TMA box, zero past the plane) has k_r > 0 or m_r != 0. The two-slot kernel
-// on the other two materials (lo < hi) is then the three-material kernel,
-// given that every region cell satisfies
-//  * a cell holding lo alone is not mixed in the two-material sense
-//    (mixed3 == is_mixed(k_lo), remap.cpp:100 / oracle mixed3), and
-//  * a non-mixed donor's material is the same: largest3(k) == (k_lo < 0.5 ?
-//    hi : lo) (remap.cpp:255-263 / oracle split_flux);
-// (with k_r = 0 the mixed split, the interface fraction and the degrade
-// tests reduce to the two-material expressions term by term). The class is
-// the highest such r, else 3.
-__device__ __forceinline__ bool map_ok(const double* k, int r) {
-    const int lo = r == 0 ? 1 : 0, hi = r == 2 ? 1 : 2;
-    if (k[lo] > 0.0 && !(k[hi] > 0.0) && is_mixed(k[lo])) return false;
-    if (!mixed3(k) && largest3(k) != (k[lo] < 0.5 ? hi : lo)) return false;
-    return true;
-}
-// Two materials: with r absent the one-material kernel on p = 1 - r is the
-// two-material one when every region cell is pure p in the reference's
-// sense (k_p >= 1 - kPureTol): no cell is mixed (remap.cpp:100), every donor
-// is p's (k0 < 0.5 <=> p = 1, remap.cpp:263) and no stencil degrades to
-// first order (remap.cpp:270-283).
-__device__ __forceinline__ bool map_ok2(const double* k, int r) { return k[1 - r] >= 1.0 - kPureTol; }
-
 template <int NM>
 __global__ void __launch_bounds__(RTX * RTY) k_tile_class(Dev d) {
     pdl_enter();
@@ -4051,67 +4166,128 @@ __global__ void __launch_bounds__(RTX * RTY) k_tile_class(Dev d) {
     const int i0 = rg.i0 - tile_shift(d) + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
     const int x0 = i0 - G + d.H - d.oi, y0 = j0 - G + d.H - d.oj;  // plane column / row of the region origin
     const int R = d.fsz / d.P;
-    unsigned pres = 0u, ok = (1u << NM) - 1u, pure = (1u << NM) - 1u;  // pure: k_a >= 1 - kPureTol in every region cell
+    unsigned mk = 0u;
     for (int t = tid; t < RCW * RCH; t += RTX * RTY) {
         const int x = x0 + t % RCW, y = y0 + t / RCW;
-        double k[NM];
+        double k[NM], m[NM];
         if (x < 0 || x >= d.P || y < 0 || y >= R) {  // zero-filled by the copy: absent
 #pragma unroll
-            for (int a = 0; a < NM; ++a) k[a] = 0.0;
+            for (int a = 0; a < NM; ++a) k[a] = m[a] = 0.0;
         } else {
             const int q = y * d.P + x;
 #pragma unroll
             for (int a = 0; a < NM; ++a) {
                 k[a] = d.k[a][q];
-                if (k[a] > 0.0 || d.m[a][q] != 0.0) pres |= 1u << a;
+                m[a] = d.m[a][q];
             }
         }
-#pragma unroll
-        for (int r = 0; r < NM; ++r) {
-            if (!(NM == 3 ? map_ok(k, r) : map_ok2(k, r))) ok &= ~(1u << r);
-            if (!(k[r] >= 1.0 - kPureTol)) pure &= ~(1u << r);
-        }
+        mk |= cell_cls_mask<NM>(k, m);
     }
-    __shared__ unsigned s_pres, s_ok, s_pure;
-    if (tid == 0) {
-        s_pres = 0u;
-        s_ok = (1u << NM) - 1u;
-        s_pure = (1u << NM) - 1u;
-    }
+    __shared__ unsigned s_mk;
+    if (tid == 0) s_mk = 0u;
     __syncthreads();
-    pres = __reduce_or_sync(0xffffffffu, pres);
-    ok = __reduce_and_sync(0xffffffffu, ok);
-    pure = __reduce_and_sync(0xffffffffu, pure);
-    if ((tid & 31) == 0) {
-        atomicOr(&s_pres, pres);
-        atomicAnd(&s_ok, ok);
-        atomicAnd(&s_pure, pure);
-    }
+    mk = __reduce_or_sync(0xffffffffu, mk);
+    if ((tid & 31) == 0) atomicOr(&s_mk, mk);
     __syncthreads();
-    if (tid == 0) {
-        int cls = 3;
-        for (int r = NM - 1; r >= 0 && cls == 3; --r)
-            if (!((s_pres >> r) & 1u) && ((s_ok >> r) & 1u)) cls = r;
-        // three materials, ONE present (p) and pure in every region cell: the
-        // two-slot mapping (either absent material, both conditions hold) whose
-        // second slot is absent too and meets the two-material condition
-        // (map_ok2: every region cell pure p), i.e. the one-material kernel
-        if (NM == 3 && H2D_RT_MAP31)
-            for (int p = 0; p < 3; ++p) {
-                const unsigned others = 7u & ~(1u << p);
-                if (s_pres == (1u << p) && (s_ok & others) == others && ((s_pure >> p) & 1u)) cls = 4 + p;
-            }
-        d.tcls[blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)cls;
+    if (tid < 32) {  // (warp 0: list_append is a warp-wide call)
+        const int t = blockIdx.y * gridDim.x + blockIdx.x, cls = cls_of_mask<NM>(s_mk);
+        if (tid == 0) d.tcls[t] = (uint8_t)cls;
+        list_append<NM>(d, t, cls, tid == 0);
     }
 }
 
+// Run loop, single domain: the cell masks come from k_post of the step
+// before, which holds the new State's k and m in registers anyway (one OR per
+// 32 x 8 post block, Dev::pcls; the first step of a call gets them from
+// k_cls_flags): a tile's class is the OR over the post blocks that cover its
+// staged region (a superset of the region: a tile next to another material is
+// classified a little more cautiously, never less), one thread per tile
+template <int NM>
+__global__ void k_tile_class_post(Dev d, int ntx, int nty) {
+    pdl_enter();
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = t < ntx * nty;
+    const int bx = valid ? t % ntx : 0, by = valid ? t / ntx : 0;
+    const Rng rg = d.r_gath, rs = d.r_sync;
+    const int i0 = rg.i0 - tile_shift(d) + bx * RTX, j0 = rg.j0 + by * RTY;
+    // region cells [i0 - 2, i0 + RTX + 2) x [j0 - 2, j0 + RTY + 2), clipped to the stored cells (r_sync)
+    const int ilo = max(i0 - G, rs.i0), ihi = min(i0 + RTX + G, rs.i1) - 1;
+    const int jlo = max(j0 - G, rs.j0), jhi = min(j0 + RTY + G, rs.j1) - 1;
+    unsigned mk = 0u;
+    for (int q = (jlo - rs.j0) / 8; q <= (jhi - rs.j0) / 8; ++q)
+        for (int p = (ilo - rs.i0) / 32; p <= (ihi - rs.i0) / 32; ++p) mk |= d.pcls[q * d.pcls_nx + p];
+    const int cls = cls_of_mask<NM>(mk);
+    if (valid) d.tcls[t] = (uint8_t)cls;
+    list_append<NM>(d, t, cls, valid);
+}
+
+// the cell masks of the CURRENT State per post block (the first step of a call)
+template <int NM>
+__global__ void __launch_bounds__(256) k_cls_flags(Dev d) {
+    __shared__ unsigned s_mk;
+    const int tl = threadIdx.y * blockDim.x + threadIdx.x;
+    if (tl == 0) s_mk = 0u;
+    __syncthreads();
+    int i, j;
+    tid2(i, j, d.r_sync.i0, d.r_sync.j0);
+    unsigned mk = 0u;
+    if (in(d.r_sync, i, j)) {
+        const int c = ix(d, i, j);
+        double k[NM], m[NM];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            k[a] = d.k[a][c];
+            m[a] = d.m[a][c];
+        }
+        mk = cell_cls_mask<NM>(k, m);
+    }
+    mk = __reduce_or_sync(0xffffffffu, mk);
+    if ((tl & 31) == 0 && mk) atomicOr(&s_mk, mk);
+    __syncthreads();
+    if (tl == 0) d.pcls[blockIdx.y * gridDim.x + blockIdx.x] = (uint16_t)s_mk;
+}
+
 // the fused flux tile kernel alone (timed separately by h2d_step_timed)
+int remap_uses_lists() { return H2D_RT_LISTS; }
+int remap_uses_classes(int nmat) { return (nmat == 3 && H2D_RT_MAP3) || (nmat == 2 && H2D_RT_MAP2); }
 int remap_tile_w() { return RTX; }
 int remap_tile_h() { return RTY; }
 int tma_node_box_w() { return RNW; }
 int tma_node_box_h() { return RNH; }
 int tma_cell_box_w() { return RCW; }
 int tma_cell_box_h() { return RCH; }
+
+__global__ void k_zero4(int* p) {
+    pdl_enter();
+    if (threadIdx.x < 4) p[threadIdx.x] = 0;
+}
+
+// tile classes: from the post blocks' masks in the run loop of a single
+// domain (Dev::cls_post), else from the State itself
+static void launch_tile_class(const Dev& d, dim3 gft, cudaStream_t s) {
+    if (d.tlist) pdl(k_zero4, dim3(1), dim3(32), 0, s, d.tcnt);  // the class lists start empty
+    if (d.cls_post && d.pcls) {
+        const int n = (int)(gft.x * gft.y);
+        if (d.nmat == 3)
+            pdl(k_tile_class_post<3>, dim3(nblk(n, 256)), dim3(256), 0, s, d, (int)gft.x, (int)gft.y);
+        else
+            pdl(k_tile_class_post<2>, dim3(nblk(n, 256)), dim3(256), 0, s, d, (int)gft.x, (int)gft.y);
+    } else if (d.nmat == 3) {
+        pdl(k_tile_class<3>, gft, dim3(RTX * RTY), 0, s, d);
+    } else {
+        pdl(k_tile_class<2>, gft, dim3(RTX * RTY), 0, s, d);
+    }
+}
+
+// the post blocks' masks of the current State (start of a run; later steps get them from k_post)
+void launch_cls_flags(const Dev& d, cudaStream_t s) {
+    if (!d.pcls || d.nmat < 2) return;
+    const dim3 gp = tiles_of(d.r_sync, 32, 8);
+    if (d.nmat == 3)
+        { k_cls_flags<3><<<gp, dim3(32, 8), 0, s>>>(d); ++g_launches; }
+    else
+        { k_cls_flags<2><<<gp, dim3(32, 8), 0, s>>>(d); ++g_launches; }
+}
 
 void launch_remap_tile(const Dev& d, cudaStream_t s) {
     remap_init();
@@ -4132,30 +4308,38 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
         if (xc) {
             Dev dx = d;
             dx.tcls = nullptr;
+            dx.tlist = nullptr;
             pdl(k_remap_tile<3, true>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, dx, *d.tma);
         } else if (d.tcls && H2D_RT_MAP3) {  // per-tile: two-slot kernel where a material is absent
-            pdl(k_tile_class<3>, gft, dim3(RTX * RTY), 0, s, d);
+            launch_tile_class(d, gft, s);
+            // (listed: persistent CTAs, a few per SM, each class from its list)
+            const dim3 g1 = d.tlist ? dim3(148 * H2D_RT_MINB1) : gft, g2 = d.tlist ? dim3(148 * H2D_RT_MINB2) : gft,
+                       g3 = d.tlist ? dim3(148 * H2D_RT_MINB3) : gft;
             if (H2D_RT_MAP31)
-                pdl(k_remap_tile<1, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
-            pdl(k_remap_tile<2, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
-            pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
+                pdl(k_remap_tile<1, false, false, true>, g1, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
+            pdl(k_remap_tile<2, false, false, true>, g2, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
+            pdl(k_remap_tile<3>, g3, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
         } else {
             Dev dx = d;
             dx.tcls = nullptr;
+            dx.tlist = nullptr;
             pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, dx, *d.tma);
         }
     else if (d.nmat == 2)
         if (xc) {
             Dev dx = d;
             dx.tcls = nullptr;
+            dx.tlist = nullptr;
             pdl(k_remap_tile<2, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, dx, *d.tma);
         } else if (d.tcls && H2D_RT_MAP2) {  // per-tile: one-material kernel where a material is absent
-            pdl(k_tile_class<2>, gft, dim3(RTX * RTY), 0, s, d);
-            pdl(k_remap_tile<1, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
-            pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
+            launch_tile_class(d, gft, s);
+            const dim3 g1 = d.tlist ? dim3(148 * H2D_RT_MINB1) : gft, g2 = d.tlist ? dim3(148 * H2D_RT_MINB2) : gft;
+            pdl(k_remap_tile<1, false, false, true>, g1, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
+            pdl(k_remap_tile<2>, g2, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
         } else {
             Dev dx = d;
             dx.tcls = nullptr;
+            dx.tlist = nullptr;
             pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, dx, *d.tma);
         }
     else
@@ -4252,6 +4436,7 @@ void launch_step(const Dev& dd, int fused_start, cudaStream_t s) {
     Dev d = dd;
     d.scan_nodes = 1;
     d.diag = 1;
+    d.cls_post = d.pcls != nullptr;  // the step before (or launch_cls_flags) left the post blocks' masks
     if (!fused_start) pdl(k_step_start, dim3(1), dim3(1), 0, s, d.ctl, d.dx, d.dy);
     launch_lagrange_run(d, s);
     launch_remap_core(d, s);

@@ -35,6 +35,8 @@ struct HaloPlan {
 };
 
 long long launch_count();
+int remap_uses_lists();  // class tiles go through per-class lists and persistent CTAs
+int remap_uses_classes(int nmat);  // the remap tile launches dispatch on per-tile material classes
 int remap_tile_w();  // remap-tile shape (cells): the tile-class grid
 int remap_tile_h();
 int tma_node_box_w();  // remap-tile TMA box sizes (doubles)
@@ -74,6 +76,7 @@ void launch_step(const Dev& d, int fused_start, cudaStream_t s);  // one run-loo
 void launch_remap_ad(const Dev& d, const AdWork& W, int x_first, int remap_velocity, int run_loop, cudaStream_t s);
 void launch_step_ad(const Dev& d, const AdWork& W, int x_first, int fused_start, cudaStream_t s);  // one AD run-loop step
 void launch_cfl_next(const Dev& d, cudaStream_t s);
+void launch_cls_flags(const Dev& d, cudaStream_t s);  // Dev::pcls of the current State (start of a run)
 void launch_step_start(const Dev& d, cudaStream_t s);
 void launch_commit_finish(const Dev& d, cudaStream_t s);               // wave speed of the current State
 void launch_commit(Ctl* c, int advance, cudaStream_t s);
