@@ -63,7 +63,6 @@ struct h2d_ctx {
     void* diag_mem = nullptr;       // DiagRed scratch of k_post / the node update
     void* tcls_mem = nullptr;       // Dev::tcls, the remap tiles' material classes
     void* pcls_mem = nullptr;       // Dev::pcls, the post blocks' classification masks
-    void* tlist_mem = nullptr;      // Dev::tcnt + Dev::tlist, the per-class tile lists
     size_t diag_tick_bytes = 0;     // the ticket words at the start of diag_mem
     double* diag_log = nullptr;     // device StepDiag log of h2d_run (kDiagRec doubles per step)
     cudaGraphExec_t graph_rest[2] = {nullptr, nullptr};  // block data plane: the step after the Lagrange kernel
@@ -793,22 +792,11 @@ int create_ctx(const h2d_config* cfg, const h2d_block* blk, int device, h2d_ctx*
         const int w = d.r_gath.i1 - (d.r_gath.i0 - shift), h = d.r_gath.j1 - d.r_gath.j0;
         d.tq_nx = std::max(1, (w + remap_tile_w() - 1) / remap_tile_w());
         d.tq_ny = std::max(1, (h + remap_tile_h() - 1) / remap_tile_h());
-        d.tlist = d.tcnt = nullptr;
-        d.tlist_cap = 0;
         if (nm >= 2) {
             const size_t n = (size_t)d.tq_nx * d.tq_ny;
             if (cudaMalloc(&c->tcls_mem, n) != cudaSuccess) return fail(H2D_ERR_NOMEM);
             if (cudaMemset(c->tcls_mem, 3, n) != cudaSuccess) return fail(H2D_ERR_DEVICE);
             d.tcls = static_cast<uint8_t*>(c->tcls_mem);
-            if (remap_uses_lists() && remap_uses_classes(nm)) {  // Dev::tlist: 4 counters, then nm lists of n tiles
-                if (cudaMalloc(&c->tlist_mem, (4 + (size_t)nm * n) * sizeof(int)) != cudaSuccess)
-                    return fail(H2D_ERR_NOMEM);
-                if (cudaMemset(c->tlist_mem, 0, (4 + (size_t)nm * n) * sizeof(int)) != cudaSuccess)
-                    return fail(H2D_ERR_DEVICE);
-                d.tcnt = static_cast<int*>(c->tlist_mem);
-                d.tlist = d.tcnt + 4;
-                d.tlist_cap = (int)n;
-            }
         }
     }
 #ifndef H2D_CLS_POST
@@ -866,7 +854,6 @@ void h2d_destroy(h2d_ctx* c) {
     if (c->diag_mem) cudaFree(c->diag_mem);
     if (c->tcls_mem) cudaFree(c->tcls_mem);
     if (c->pcls_mem) cudaFree(c->pcls_mem);
-    if (c->tlist_mem) cudaFree(c->tlist_mem);
     if (c->xbuf) cudaFree(c->xbuf);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;

@@ -236,12 +236,6 @@ struct Dev {
     // run-loop step, whose tile classes come from them (k_tile_class_post)
     uint16_t* pcls;
     int pcls_nx, cls_post;
-    // per-class tile lists (k_remap_tile, H2D_RT_LISTS): slot s (= slots of the
-    // kernel - 1) holds tcnt[s] tile indices at tlist[s * tlist_cap ...],
-    // appended by the classification kernel of the step. Null: the class
-    // kernels run over the whole tile grid.
-    int *tlist, *tcnt;
-    int tlist_cap;
 };
 
 // 32-bit plane offsets: P * R < 2^31 for every mesh up to 16384^2 (checked at

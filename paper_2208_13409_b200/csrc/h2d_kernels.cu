@@ -1560,18 +1560,11 @@ template <int NM, bool XC = false, bool DIR = false, bool MAP = false>
 #ifndef H2D_RT_MINB3
 #define H2D_RT_MINB3 2
 #endif
-// H2D_RT_LISTS: tile classes dispatched through per-class tile lists and
-// persistent CTAs (k_remap_tile) instead of whole-grid launches whose CTAs of
-// another class exit at once
-#ifndef H2D_RT_LISTS
-#define H2D_RT_LISTS 1
-#endif
-// One tile (bx, by) of class rabs; par: the parity of the mbarrier phase this
-// call completes (a persistent CTA runs one tile after another on the same
-// two mbarriers, initialised once by the kernel)
-__device__ __forceinline__ void remap_tile_body(const Dev& d, const TmaSet& tm, const int bx, const int by,
-                                                const int rabs, const uint32_t par, char* smem_raw, int& s_halt,
-                                                uint64_t& s_bar, uint64_t& s_bar2) {
+__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ? H2D_RT_MINB2 : H2D_RT_MINB3)) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
+    pdl_enter();
+    extern __shared__ __align__(128) char smem_raw[];
+    __shared__ int s_halt;
+    __shared__ __align__(8) uint64_t s_bar, s_bar2;
     const int tid = threadIdx.x;
     // three materials with tile classes: each tile runs in exactly one of the
     // two launches (uniform over the CTA, before any copy is issued)
@@ -1579,7 +1572,17 @@ __device__ __forceinline__ void remap_tile_body(const Dev& d, const TmaSet& tm, 
     // three-material context, one slot of a two-material one), 3 = the
     // context's own kernel, 4..6 = a three-material context's tile holding
     // only material cls - 4 (one slot); slot a holds material mat(a)
-    // (the kernel below picks the tiles of this instantiation's classes)
+    int rabs = 3;
+    if (MAP || (NM >= 2 && !XC && !DIR && d.tcls)) {
+        rabs = d.tcls[blockIdx.y * gridDim.x + blockIdx.x];
+        if (!MAP) {
+            if (rabs != 3) return;
+        } else if (NM == 2) {
+            if (rabs > 2) return;
+        } else {
+            if (d.nmat == 3 ? rabs < 4 : rabs > 1) return;
+        }
+    }
     // NM = 2 slots of a three-material context: the two present materials in
     // order; NM = 1 slot of a two-material context: the present one
     const int mat0 = MAP ? (NM == 2 ? (rabs == 0 ? 1 : 0) : (d.nmat == 3 ? rabs - 4 : 1 - rabs)) : 0,
@@ -1592,7 +1595,7 @@ __device__ __forceinline__ void remap_tile_body(const Dev& d, const TmaSet& tm, 
     // grid one column left (the extra column's items are computed, never
     // gathered, and land outside every range a later phase reads)
     const int sx = tile_shift(d);
-    const int i0 = rg.i0 - sx + bx * RTX, j0 = rg.j0 + by * RTY;
+    const int i0 = rg.i0 - sx + blockIdx.x * RTX, j0 = rg.j0 + blockIdx.y * RTY;
     // the 128-byte-aligned start of the tile as an OFFSET from the shared array
     // (not a pointer rebuilt from an integer: the compiler then keeps the
     // shared address space and emits LDS / STS with 32-bit addresses instead
@@ -1622,6 +1625,8 @@ __device__ __forceinline__ void remap_tile_body(const Dev& d, const TmaSet& tm, 
     constexpr bool kSplit = H2D_RT_SPLITBAR != 0;
     uint64_t* bar_c = kSplit ? &s_bar2 : &s_bar;
     if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        if (kSplit) mbar_init(&s_bar2, 1);
         constexpr uint32_t nbytes = 2u * RNW * RNH * 8u, cbytes = 3u * NM * RCW * RCH * 8u;
         const int x = T.ci0 + d.H - d.oi, y = T.cj0 + d.H - d.oj;  // plane column / row of the region origin
         mbar_expect_tx(&s_bar, kSplit ? nbytes : nbytes + cbytes);
@@ -1641,12 +1646,12 @@ __device__ __forceinline__ void remap_tile_body(const Dev& d, const TmaSet& tm, 
     __syncthreads();
     if (s_halt) {
         if (tid == 0) {
-            mbar_wait(&s_bar, par);
-            if (kSplit) mbar_wait(bar_c, par);
+            mbar_wait(&s_bar, 0);
+            if (kSplit) mbar_wait(bar_c, 0);
         }
         return;
     }
-    mbar_wait(&s_bar, par);
+    mbar_wait(&s_bar, 0);
     // ---- quiescent tile: u_half == 0 at every node of the tile's faces and
     // corners makes every face / corner flux volume of the tile zero, so no
     // flux is gathered (the reference skips zero volumes, remap.cpp:860,929),
@@ -1664,7 +1669,7 @@ __device__ __forceinline__ void remap_tile_body(const Dev& d, const TmaSet& tm, 
             }
         }
         if (!__syncthreads_or(moving)) {
-            if (kSplit) mbar_wait(bar_c, par);
+            if (kSplit) mbar_wait(bar_c, 0);
             const int ni1 = min(nx, rg.i1), nj1 = min(ny, rg.j1);
             RowCol<RTX + 1, RTX * RTY> rz(tid);
             for (int t = tid; t < NCF; t += RTX * RTY, rz.step()) {
@@ -1741,7 +1746,7 @@ __device__ __forceinline__ void remap_tile_body(const Dev& d, const TmaSet& tm, 
         T.fydv[t] = fyv;
     }
     __syncthreads();
-    if (kSplit) mbar_wait(bar_c, par);
+    if (kSplit) mbar_wait(bar_c, 0);
     // ---- phase 2, cell items: Lagrangian volume, densities, centroids,
     // interfaces (remap.cpp:769-824)
     RowCol<RCW, RTX * RTY> rs3(tid);
@@ -1934,56 +1939,6 @@ __device__ __forceinline__ void remap_tile_body(const Dev& d, const TmaSet& tm, 
         finalize_cell<NM>(d, rg, i, j, c, tx, own, m, me, va);
 }
 
-
-// The launch: one tile per CTA (the grid is the tile grid), or -- contexts
-// with tile classes and H2D_RT_LISTS -- persistent CTAs that take the tiles of
-// this instantiation's classes from the class's list (Dev::tlist, written by
-// the classification kernel) one after another.
-template <int NM, bool XC = false, bool DIR = false, bool MAP = false>
-__global__ void __launch_bounds__(RTX * RTY, NM == 1 ? H2D_RT_MINB1 : (NM == 2 ? H2D_RT_MINB2 : H2D_RT_MINB3)) k_remap_tile(Dev d, const __grid_constant__ TmaSet tm) {
-    pdl_enter();
-    extern __shared__ __align__(128) char smem_raw[];
-    __shared__ int s_halt;
-    __shared__ __align__(8) uint64_t s_bar, s_bar2;
-    if (threadIdx.x == 0) {
-        mbar_init(&s_bar, 1);
-        if (H2D_RT_SPLITBAR) mbar_init(&s_bar2, 1);
-    }
-    const bool classes = MAP || (NM >= 2 && !XC && !DIR && d.tcls);
-    const bool listed = classes && d.tlist;  // slot NM - 1 holds this instantiation's tiles
-    int n = 1, q = 0, stride = 1;
-    if (listed) {
-        n = d.tcnt[NM - 1];
-        q = blockIdx.x;
-        stride = gridDim.x;
-    }
-    uint32_t par = 0;
-    for (; q < n; q += stride) {  // (one call site: the body is inlined once)
-        // tile class (k_tile_class): 0..2 = that material is absent (two slots of
-        // a three-material context, one slot of a two-material one), 3 = the
-        // context's own kernel, 4..6 = a three-material context's tile holding
-        // only material cls - 4 (one slot); slot a holds material mat(a)
-        int bx = blockIdx.x, by = blockIdx.y, rabs = 3;
-        if (listed) {
-            const int t = d.tlist[(size_t)(NM - 1) * d.tlist_cap + q];
-            bx = t % d.tq_nx;
-            by = t / d.tq_nx;
-            rabs = d.tcls[t];
-        } else if (classes) {
-            rabs = d.tcls[blockIdx.y * gridDim.x + blockIdx.x];
-            if (!MAP) {
-                if (rabs != 3) return;
-            } else if (NM == 2) {
-                if (rabs > 2) return;
-            } else {
-                if (d.nmat == 3 ? rabs < 4 : rabs > 1) return;
-            }
-        }
-        remap_tile_body<NM, XC, DIR, MAP>(d, tm, bx, by, rabs, par, smem_raw, s_halt, s_bar, s_bar2);
-        par ^= 1u;
-        if (listed) __syncthreads();  // every thread is done with the tile's shared memory before the next copies land
-    }
-}
 
 __device__ __forceinline__ void sliver_offset(int lane, int& di, int& dj, int& ring) {
     if (lane < 8) {  // ring 1: (dj, di) row-major, centre skipped
@@ -3231,32 +3186,6 @@ __device__ __forceinline__ unsigned cell_cls_mask(const double* k, const double*
     }
     return mk;
 }
-// the list (Dev::tlist slot) a tile of class cls goes to: slot = slots of the
-// kernel that runs it - 1
-template <int NM>
-__device__ __forceinline__ int cls_slot(int cls) {
-    if (cls == 3) return NM - 1;
-    if (NM == 3) return cls < 3 ? 1 : 0;
-    return 0;  // two materials: one absent
-}
-// append tile t to its class's list; called by every thread of a warp
-// (tiles: one thread each; valid = this lane has a tile): one atomic per
-// warp and slot
-template <int NM>
-__device__ __forceinline__ void list_append(const Dev& d, int t, int cls, bool valid) {
-    if (!d.tlist) return;
-    const int slot = valid ? cls_slot<NM>(cls) : -1;
-    const unsigned lane = threadIdx.x & 31u;
-#pragma unroll
-    for (int sl = 0; sl < NM; ++sl) {
-        const unsigned m = __ballot_sync(0xffffffffu, slot == sl);
-        if (!m) continue;
-        int base = 0;
-        if (lane == (unsigned)(__ffs(m) - 1)) base = atomicAdd(&d.tcnt[sl], __popc(m));
-        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-        if (slot == sl) d.tlist[(size_t)sl * d.tlist_cap + base + __popc(m & ((1u << lane) - 1u))] = t;
-    }
-}
 // the class of a tile from the OR of its region's cell masks (see k_tile_class)
 template <int NM>
 __device__ __forceinline__ int cls_of_mask(unsigned mk) {
@@ -4189,11 +4118,7 @@ __global__ void __launch_bounds__(RTX * RTY) k_tile_class(Dev d) {
     mk = __reduce_or_sync(0xffffffffu, mk);
     if ((tid & 31) == 0) atomicOr(&s_mk, mk);
     __syncthreads();
-    if (tid < 32) {  // (warp 0: list_append is a warp-wide call)
-        const int t = blockIdx.y * gridDim.x + blockIdx.x, cls = cls_of_mask<NM>(s_mk);
-        if (tid == 0) d.tcls[t] = (uint8_t)cls;
-        list_append<NM>(d, t, cls, tid == 0);
-    }
+    if (tid == 0) d.tcls[blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)cls_of_mask<NM>(s_mk);
 }
 
 // Run loop, single domain: the cell masks come from k_post of the step
@@ -4206,8 +4131,8 @@ template <int NM>
 __global__ void k_tile_class_post(Dev d, int ntx, int nty) {
     pdl_enter();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = t < ntx * nty;
-    const int bx = valid ? t % ntx : 0, by = valid ? t / ntx : 0;
+    if (t >= ntx * nty) return;
+    const int bx = t % ntx, by = t / ntx;
     const Rng rg = d.r_gath, rs = d.r_sync;
     const int i0 = rg.i0 - tile_shift(d) + bx * RTX, j0 = rg.j0 + by * RTY;
     // region cells [i0 - 2, i0 + RTX + 2) x [j0 - 2, j0 + RTY + 2), clipped to the stored cells (r_sync)
@@ -4216,9 +4141,7 @@ __global__ void k_tile_class_post(Dev d, int ntx, int nty) {
     unsigned mk = 0u;
     for (int q = (jlo - rs.j0) / 8; q <= (jhi - rs.j0) / 8; ++q)
         for (int p = (ilo - rs.i0) / 32; p <= (ihi - rs.i0) / 32; ++p) mk |= d.pcls[q * d.pcls_nx + p];
-    const int cls = cls_of_mask<NM>(mk);
-    if (valid) d.tcls[t] = (uint8_t)cls;
-    list_append<NM>(d, t, cls, valid);
+    d.tcls[t] = (uint8_t)cls_of_mask<NM>(mk);
 }
 
 // the cell masks of the CURRENT State per post block (the first step of a call)
@@ -4248,7 +4171,6 @@ __global__ void __launch_bounds__(256) k_cls_flags(Dev d) {
 }
 
 // the fused flux tile kernel alone (timed separately by h2d_step_timed)
-int remap_uses_lists() { return H2D_RT_LISTS; }
 int remap_uses_classes(int nmat) { return (nmat == 3 && H2D_RT_MAP3) || (nmat == 2 && H2D_RT_MAP2); }
 int remap_tile_w() { return RTX; }
 int remap_tile_h() { return RTY; }
@@ -4257,15 +4179,9 @@ int tma_node_box_h() { return RNH; }
 int tma_cell_box_w() { return RCW; }
 int tma_cell_box_h() { return RCH; }
 
-__global__ void k_zero4(int* p) {
-    pdl_enter();
-    if (threadIdx.x < 4) p[threadIdx.x] = 0;
-}
-
 // tile classes: from the post blocks' masks in the run loop of a single
 // domain (Dev::cls_post), else from the State itself
 static void launch_tile_class(const Dev& d, dim3 gft, cudaStream_t s) {
-    if (d.tlist) pdl(k_zero4, dim3(1), dim3(32), 0, s, d.tcnt);  // the class lists start empty
     if (d.cls_post && d.pcls) {
         const int n = (int)(gft.x * gft.y);
         if (d.nmat == 3)
@@ -4308,38 +4224,30 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
         if (xc) {
             Dev dx = d;
             dx.tcls = nullptr;
-            dx.tlist = nullptr;
             pdl(k_remap_tile<3, true>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, dx, *d.tma);
         } else if (d.tcls && H2D_RT_MAP3) {  // per-tile: two-slot kernel where a material is absent
             launch_tile_class(d, gft, s);
-            // (listed: persistent CTAs, a few per SM, each class from its list)
-            const dim3 g1 = d.tlist ? dim3(148 * H2D_RT_MINB1) : gft, g2 = d.tlist ? dim3(148 * H2D_RT_MINB2) : gft,
-                       g3 = d.tlist ? dim3(148 * H2D_RT_MINB3) : gft;
             if (H2D_RT_MAP31)
-                pdl(k_remap_tile<1, false, false, true>, g1, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
-            pdl(k_remap_tile<2, false, false, true>, g2, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
-            pdl(k_remap_tile<3>, g3, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
+                pdl(k_remap_tile<1, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
+            pdl(k_remap_tile<2, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
+            pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
         } else {
             Dev dx = d;
             dx.tcls = nullptr;
-            dx.tlist = nullptr;
             pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, dx, *d.tma);
         }
     else if (d.nmat == 2)
         if (xc) {
             Dev dx = d;
             dx.tcls = nullptr;
-            dx.tlist = nullptr;
             pdl(k_remap_tile<2, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, dx, *d.tma);
         } else if (d.tcls && H2D_RT_MAP2) {  // per-tile: one-material kernel where a material is absent
             launch_tile_class(d, gft, s);
-            const dim3 g1 = d.tlist ? dim3(148 * H2D_RT_MINB1) : gft, g2 = d.tlist ? dim3(148 * H2D_RT_MINB2) : gft;
-            pdl(k_remap_tile<1, false, false, true>, g1, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
-            pdl(k_remap_tile<2>, g2, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
+            pdl(k_remap_tile<1, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
+            pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
         } else {
             Dev dx = d;
             dx.tcls = nullptr;
-            dx.tlist = nullptr;
             pdl(k_remap_tile<2>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, dx, *d.tma);
         }
     else

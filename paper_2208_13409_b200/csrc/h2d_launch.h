@@ -35,7 +35,6 @@ struct HaloPlan {
 };
 
 long long launch_count();
-int remap_uses_lists();  // class tiles go through per-class lists and persistent CTAs
 int remap_uses_classes(int nmat);  // the remap tile launches dispatch on per-tile material classes
 int remap_tile_w();  // remap-tile shape (cells): the tile-class grid
 int remap_tile_h();
