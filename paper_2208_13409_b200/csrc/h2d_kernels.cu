@@ -16,6 +16,8 @@
 
 #include <atomic>
 
+#include <type_traits>
+
 namespace h2d {
 
 // ---------------------------------------------------------------------------
@@ -1547,6 +1549,11 @@ template <int NM, bool XC = false, bool DIR = false, bool MAP = false>
 // the one-slot kernel (class 4 + p)
 #ifndef H2D_RT_MAP31
 #define H2D_RT_MAP31 1
+#endif
+// H2D_RT_MAP32: the two-slot class (one material absent) has its own launch;
+// 0: those tiles run the three-slot kernel (one whole-grid launch less)
+#ifndef H2D_RT_MAP32
+#define H2D_RT_MAP32 1
 #endif
 #ifndef H2D_RT_SPLITBAR
 #define H2D_RT_SPLITBAR 1
@@ -3191,8 +3198,9 @@ template <int NM>
 __device__ __forceinline__ int cls_of_mask(unsigned mk) {
     const unsigned pres = mk & 7u, ok = ~(mk >> 3) & 7u, pure = ~(mk >> 6) & 7u;
     int cls = 3;
-    for (int r = NM - 1; r >= 0 && cls == 3; --r)
-        if (!((pres >> r) & 1u) && ((ok >> r) & 1u)) cls = r;
+    if (NM == 2 || H2D_RT_MAP32)
+        for (int r = NM - 1; r >= 0 && cls == 3; --r)
+            if (!((pres >> r) & 1u) && ((ok >> r) & 1u)) cls = r;
     // three materials, ONE present (p) and pure in every region cell: the
     // two-slot mapping (either absent material, both conditions hold) whose
     // second slot is absent too and meets the two-material condition
@@ -3354,12 +3362,23 @@ __device__ __forceinline__ void post_body(const Dev& d, const int run_loop, unsi
             for (int pl = t >> 5; pl < NDG; pl += 8) {
                 const int k = (NM == 3 || pl < DG_MM2) ? pl : pl + 1;  // the slot of plane pl
                 const int lane = t & 31, op = dg_op(k);
-                double v = s_dg[pl][lane];
+                // (op is uniform over the warp: one copy of the fold per operation,
+                // so dg_comb is a single add / min / max instead of all three + selects)
+                auto fold = [&](auto opc) {
+                    constexpr int OP = decltype(opc)::value;
+                    double v = s_dg[pl][lane];
 #pragma unroll
-                for (int q = 1; q < 8; ++q) v = dg_comb(op, v, s_dg[pl][lane + 32 * q]);
+                    for (int q = 1; q < 8; ++q) v = dg_comb(OP, v, s_dg[pl][lane + 32 * q]);
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v = dg_comb(op, v, __shfl_down_sync(0xffffffffu, v, o));
-                if (lane == 0) part[k] = v;
+                    for (int o = 16; o > 0; o >>= 1) v = dg_comb(OP, v, __shfl_down_sync(0xffffffffu, v, o));
+                    if (lane == 0) part[k] = v;
+                };
+                if (op == 0)
+                    fold(std::integral_constant<int, 0>{});
+                else if (op == 1)
+                    fold(std::integral_constant<int, 1>{});
+                else
+                    fold(std::integral_constant<int, 2>{});
             }
             if (NM < 3 && t == 0) part[DG_MM2] = 0.0;
         }
@@ -4229,7 +4248,8 @@ void launch_remap_tile(const Dev& d, cudaStream_t s) {
             launch_tile_class(d, gft, s);
             if (H2D_RT_MAP31)
                 pdl(k_remap_tile<1, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<1>(), s, d, *d.tma);
-            pdl(k_remap_tile<2, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
+            if (H2D_RT_MAP32)
+                pdl(k_remap_tile<2, false, false, true>, gft, dim3(RTX * RTY), remap_smem_bytes<2>(), s, d, *d.tma);
             pdl(k_remap_tile<3>, gft, dim3(RTX * RTY), remap_smem_bytes<3>(), s, d, *d.tma);
         } else {
             Dev dx = d;
