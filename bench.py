@@ -297,7 +297,10 @@ def run_product(args, world, rank, local, pg):
             continue
         kms = max_over_ranks(pg, ph[grp])
         ach = nbytes[nmat] * cells / (kms / 1e3) / 1e9
-        kern[grp] = {"kernel": f"{kname}<{nmat}>", "ms": kms, "bytes_per_cell": nbytes[nmat],
+        label = f"{kname}<{nmat}>"
+        if grp == "remap_tile" and nmat == 3:  # per-tile material classes: one launch per slot count
+            label = "k_remap_tile<1|2|3> (class launches)"
+        kern[grp] = {"kernel": label, "ms": kms, "bytes_per_cell": nbytes[nmat],
                      "achieved": ach, "frac": ach / peak,
                      "share_of_step": kms / ph["total"] if ph["total"] > 0 else None}
     dom = max(kern, key=lambda g: kern[g]["ms"])

@@ -52,10 +52,14 @@ __device__ __forceinline__ bool own_yface(const Dev& d, int i, int j) {  // cell
 // updates through).
 __device__ __forceinline__ void bump_kviol(Ctl* ctl, double viol) {
     namespace cg = cooperative_groups;
+    // a value that does not exceed the running maximum cannot change it (a
+    // stale cached read only lets a few more threads through): most cells with
+    // a rounding-level violation stop here, before the warp reduction
+    const unsigned long long mine = (unsigned long long)__double_as_longlong(viol);
+    if (mine <= __ldca(&ctl->kviol_bits)) return;
     const auto g = cg::coalesced_threads();
-    const unsigned long long v = cg::reduce(g, (unsigned long long)__double_as_longlong(viol),
-                                            cg::greater<unsigned long long>());
-    if (g.thread_rank() == 0 && v > __ldca(&ctl->kviol_bits)) atomicMax(&ctl->kviol_bits, v);
+    const unsigned long long v = cg::reduce(g, mine, cg::greater<unsigned long long>());
+    if (g.thread_rank() == 0) atomicMax(&ctl->kviol_bits, v);
 }
 __device__ __forceinline__ void bump_clip(Ctl* ctl) {
     const auto g = cooperative_groups::coalesced_threads();
@@ -745,26 +749,30 @@ __global__ void __launch_bounds__(H2D_LAG_NT, H2D_FMINB(NM)) k_lag_fused(Dev d) 
     constexpr int NC = (LTX + 2) * (LTY + 2), NN = (LTX + 1) * (LTY + 1);
     __shared__ double s_q[NC], s_pmh[NC], s_ph[NM][NC], s_mm[NC];
     __shared__ double shx[NN], shy[NN];
-    __shared__ int s_halt;
-    if (threadIdx.x == 0) s_halt = halted(d.ctl);
-    __syncthreads();
-    if (s_halt) return;
+    __shared__ int s_halt, s_int;
     const Rng rn = d.r_lagn;
     const int i0 = rn.i0 + blockIdx.x * LTX, j0 = rn.j0 + blockIdx.y * LTY;
-    if (d.lag_sel && (in(d.lag_inner, i0, j0) != (d.lag_sel == 1))) return;
-    // interior tile: cells [i0-1, i0+LTX] x [j0-1, j0+LTY] are mesh cells inside
-    // the window, nodes [i0, i0+LTX] x [j0, j0+LTY] lie inside r_lagn, off the
-    // walls and before the range's last row / column, the own cells inside
-    // r_lagc, r_lage and the owned range
-    bool interior = false;
-    if (H2D_LAG_INTERIOR) {
-        const int ia = i0 - 1, ib = i0 + LTX, ja = j0 - 1, jb = j0 + LTY;  // inclusive cell bounds of the pass
-        interior = ia >= 0 && ib < d.nx && ja >= 0 && jb < d.ny && in(d.win_c, ia, ja) && in(d.win_c, ib, jb) &&
-                   i0 >= 1 && ib <= d.nx - 1 && j0 >= 1 && jb <= d.ny - 1 && ib < rn.i1 - 1 && jb < rn.j1 - 1 &&
-                   in(d.r_lagc, i0, j0) && in(d.r_lagc, ib - 1, jb - 1) && in(d.r_lage, i0, j0) &&
-                   in(d.r_lage, ib - 1, jb - 1) && own_cell(d, i0, j0) && own_cell(d, ib - 1, jb - 1);
+    if (threadIdx.x == 0) {
+        s_halt = halted(d.ctl);
+        // interior tile: cells [i0-1, i0+LTX] x [j0-1, j0+LTY] are mesh cells
+        // inside the window, nodes [i0, i0+LTX] x [j0, j0+LTY] lie inside
+        // r_lagn, off the walls and before the range's last row / column, the
+        // own cells inside r_lagc, r_lage and the owned range (one thread
+        // evaluates the ~60 instructions of it, not all 352)
+        bool interior = false;
+        if (H2D_LAG_INTERIOR) {
+            const int ia = i0 - 1, ib = i0 + LTX, ja = j0 - 1, jb = j0 + LTY;  // inclusive cell bounds of the pass
+            interior = ia >= 0 && ib < d.nx && ja >= 0 && jb < d.ny && in(d.win_c, ia, ja) && in(d.win_c, ib, jb) &&
+                       i0 >= 1 && ib <= d.nx - 1 && j0 >= 1 && jb <= d.ny - 1 && ib < rn.i1 - 1 && jb < rn.j1 - 1 &&
+                       in(d.r_lagc, i0, j0) && in(d.r_lagc, ib - 1, jb - 1) && in(d.r_lage, i0, j0) &&
+                       in(d.r_lage, ib - 1, jb - 1) && own_cell(d, i0, j0) && own_cell(d, ib - 1, jb - 1);
+        }
+        s_int = interior;
     }
-    if (interior)
+    __syncthreads();
+    if (s_halt) return;
+    if (d.lag_sel && (in(d.lag_inner, i0, j0) != (d.lag_sel == 1))) return;
+    if (s_int)
         lag_fused_body<NM, true>(d, i0, j0, s_q, s_pmh, s_ph, s_mm, shx, shy);
     else
         lag_fused_body<NM, false>(d, i0, j0, s_q, s_pmh, s_ph, s_mm, shx, shy);
@@ -3393,22 +3401,24 @@ __global__ void __launch_bounds__(256, H2D_POST_MINB) k_post(Dev d, int run_loop
     // materials keep no DG_MM2 plane (its partial is written as 0)
     constexpr int NDG = NM == 3 ? DG_NCELL : DG_NCELL - 1;
     __shared__ double s_dg[NDG][256];
-    __shared__ int s_halt;
+    __shared__ int s_halt, s_int;
     __shared__ unsigned s_cls;
     if (threadIdx.x == 0 && threadIdx.y == 0) {
         s_halt = halted(d.ctl);
         s_cls = 0u;
+        bool interior = false;  // (uniform over the block: one thread evaluates it)
+        if (H2D_POST_INTERIOR) {
+            const int ia = d.r_sync.i0 + (int)(blockIdx.x * blockDim.x),
+                      ja = d.r_sync.j0 + (int)(blockIdx.y * blockDim.y);
+            const int ib = ia + (int)blockDim.x - 1, jb = ja + (int)blockDim.y - 1;
+            interior = ia >= 0 && ja >= 0 && ib < d.nx && jb < d.ny && in(d.r_sync, ia, ja) && in(d.r_sync, ib, jb) &&
+                       in(d.r_nrm, ia, ja) && in(d.r_nrm, ib, jb) && own_cell(d, ia, ja) && own_cell(d, ib, jb);
+        }
+        s_int = interior;
     }
     __syncthreads();
     if (s_halt) return;
-    bool interior = false;
-    if (H2D_POST_INTERIOR) {
-        const int ia = d.r_sync.i0 + (int)(blockIdx.x * blockDim.x), ja = d.r_sync.j0 + (int)(blockIdx.y * blockDim.y);
-        const int ib = ia + (int)blockDim.x - 1, jb = ja + (int)blockDim.y - 1;
-        interior = ia >= 0 && ja >= 0 && ib < d.nx && jb < d.ny && in(d.r_sync, ia, ja) && in(d.r_sync, ib, jb) &&
-                   in(d.r_nrm, ia, ja) && in(d.r_nrm, ib, jb) && own_cell(d, ia, ja) && own_cell(d, ib, jb);
-    }
-    if (interior)
+    if (s_int)
         post_body<NM, true>(d, run_loop, sw, s_dg, &s_cls);
     else
         post_body<NM, false>(d, run_loop, sw, s_dg, &s_cls);
