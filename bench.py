@@ -4,11 +4,15 @@
 Product arm (default): the CUDA library through its C-ABI.  A "step" is one
 pass of the hot path over the whole mesh: cfl_dt -> lagrange_step ->
 remap_step(DirectCF) -> nan_scan (harness.cpp:390-412).  The default workload is
-the largest BASELINE.json configuration that fits one GPU: configs[3], the
-two-material shock-bubble on 8192^2 cells (the 16384^2 three-material
-configs[4] needs two GPUs), with synthetic initial data painted exactly like
-the reference's init_case (seeded bubble perturbation).  W warm-up steps, then K timed steps, each bracketed by CUDA events
-on the library's stream with an L2 flush (512 MiB write) between steps.
+configs[3] of BASELINE.json, the two-material shock-bubble on 8192^2 cells: the
+largest configuration the reference itself can hold (kMaxMat = 2), so its
+results are pinned to the reference bit for bit.  (--workload c5 runs the
+16384^2 three-material configs[4], which also fits one B200 at ~156 GB; it is
+this build's N-material extension, runs with the documented sliver-energy
+safeguard, and its default run takes several minutes to paint.)  Synthetic
+initial data painted exactly like the reference's init_case (seeded bubble
+perturbation).  W warm-up steps, then K timed steps, each bracketed by CUDA
+events on the library's stream with an L2 flush (512 MiB write) between steps.
 
 Reference arm (--impl reference): the reference's own CPU implementation
 (oracle/_ref, compiled from /root/reference/proj) on the host, same workload

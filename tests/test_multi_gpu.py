@@ -157,6 +157,20 @@ def test_ad_blocks_refuse_three_materials():
     comm.close()
 
 
+def test_blocks_refuse_the_direct_engine():
+    """block mode runs DirectCF and AD; the faces-only Direct engine is single-domain only."""
+    case = cases.riemann2d(64)
+    lib = helpers.product_lib()
+    init = helpers.prepared(lib, case.cfg, case.paint()).download()
+    blocks = [multi.BlockSolver(lib, case.cfg, sp) for sp in multi.decompose(64, 64, 2, 1)]
+    for b in blocks:
+        b.upload(init)
+    comm = multi.DeviceComm(blocks, 2, 1)
+    with pytest.raises(errors.DeviceError):
+        comm.run(5, 1e30, case.cfl, kind=abi.REMAP_DIRECT)
+    comm.close()
+
+
 @pytest.mark.parametrize("px,py", [(2, 1), (1, 2), (2, 2), (4, 2)])
 @pytest.mark.parametrize("which", ["riemann", "triple", "bubble", "voronoi3"])
 def test_device_data_plane_bitwise_equal_single_domain(which, px, py):
